@@ -1,0 +1,145 @@
+/* include/lsg.h — C ABI of the B200-native SOLAR loading planner ("lsg").
+ *
+ * This is the drop-in boundary for the reference library's hot path
+ * (/root/reference/proj, namespace loadsched). Every entry point is plain C:
+ * integers, plain pointers and sizes, no torch or STL types. Each function
+ * cites the reference interface it replaces. The host C++ layer
+ * (paper_2211_00224_b200/host/loadsched_b200.hpp) re-exposes the reference's
+ * own C++ signatures on top of these calls; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Return value: 0 on success, else the reference ErrorClass code
+ *    (errors.hpp:11-18): 2 Config, 3 Validation, 4 Capability, 6 Storage,
+ *    7 Internal. lsg_last_error() returns a thread-local message.
+ *  - "d_" pointers are device (HBM) pointers; "h_" pointers are host memory.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Device-pointer
+ *    calls are asynchronous on the stream unless stated; calls that must
+ *    report a device-detected invariant failure synchronise the stream once.
+ *  - Sample ids are uint32 on the device (the reference SampleId is uint64,
+ *    trace.hpp:11; D < 2^31 is enforced, widening happens in the host layer).
+ *  - Hit tags travel in bit 31 of an item: item = id | (hit ? LSG_HIT_BIT : 0).
+ *  - Keys/next-use values: LSG_NEVER means "never used again" (buffer.hpp:19).
+ */
+#ifndef LSG_H
+#define LSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSG_HIT_BIT 0x80000000u
+#define LSG_NEVER 0xFFFFFFFEu
+
+/* Mirrors PipelineConfig (config.hpp:17-36) minus the cost-model fields,
+ * which do not reach the hot path. Field order is ABI. */
+typedef struct lsg_config {
+    uint64_t dataset_size;    /* D  (TraceConfig::dataset_size) */
+    uint32_t num_epochs;      /* E */
+    uint32_t num_nodes;       /* N */
+    uint64_t local_batch;     /* b */
+    uint64_t seed;
+    int32_t drop_last;
+    int32_t policy;           /* 0 clairvoyant, 1 lru (Policy, buffer.hpp:16) */
+    uint64_t buffer_capacity; /* C per node */
+    int32_t graph_mode;       /* 0 global, 1 pernode (WindowMode) */
+    int32_t insert_redundant; /* chunk_insert_redundant */
+    uint64_t chunk_threshold;
+    int32_t optim_order, optim_remap, optim_balance, optim_chunk;
+    uint32_t pso_swarm, pso_iters, pso_stagnation, pso_restart;
+    double pso_p_personal, pso_p_global, pso_inertia, pso_kick;
+} lsg_config;
+
+/* Derived plan shape (TraceConfig::steps_per_epoch, trace.cpp:12-16). */
+typedef struct lsg_shape {
+    uint64_t global_batch;    /* B = N*b */
+    uint64_t steps_per_epoch; /* S */
+    uint64_t keep;            /* ids kept per epoch (S*B under drop_last, else D) */
+    uint64_t total_steps;     /* T = E*S */
+    uint64_t total_items;     /* E*keep */
+} lsg_shape;
+
+/* Device outputs of lsg_plan (PlanOutput, pipeline.hpp:17-22 flattened).
+ * Any pointer may be NULL except items/node_off, which the planner needs. */
+typedef struct lsg_plan_out {
+    uint32_t* trace;        /* [E][keep]  AccessTrace.epochs */
+    uint64_t* graph;        /* [E][E]     ReuseGraph.weights */
+    uint32_t* order;        /* [E]        SchedulePlan.order.order */
+    uint64_t* cost;         /* [1]        SchedulePlan.order.cost */
+    uint64_t* hist;         /* [pso_iters] PsoResult.history */
+    uint32_t* iters;        /* [1]        PsoResult.iterations */
+    uint32_t* items;        /* [E*keep]   node lists, steps in execution order */
+    uint32_t* node_off;     /* [T][N+1]   per-step list offsets */
+    uint32_t* fetch_before; /* [T][N]     StepPlan.fetches_before */
+    uint32_t* fetch_after;  /* [T][N]     StepPlan.fetches_after */
+} lsg_plan_out;
+
+int lsg_version(void);
+const char* lsg_last_error(void);
+
+/* Validation + derived shape; Config errors as TraceConfig::validate
+ * (trace.cpp:18-24) and PipelineConfig::validate (config.cpp:11-22). */
+int lsg_shape_of(const lsg_config* cfg, lsg_shape* out);
+
+/* ---- K1: generate_trace(const TraceConfig&) -> AccessTrace
+ *      (trace.hpp:40, trace.cpp:26-43). d_trace: [E][keep] uint32. */
+int lsg_generate_trace(const lsg_config* cfg, uint32_t* d_trace, void* stream);
+
+/* ---- K2/K3: build_reuse_graph(trace, buffer_size, mode) -> ReuseGraph
+ *      (reuse_graph.hpp:53, reuse_graph.cpp:77-101). d_trace: [E][len]
+ *      (any ids < D, repeats allowed, as read_trace admits); d_w: [E][E]. */
+int lsg_build_reuse_graph(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64_t D,
+                          uint32_t N, uint64_t b, int32_t drop_last, uint64_t buffer_size,
+                          int32_t mode, uint64_t* d_w, void* stream);
+
+/* ---- K4: pso_order(graph, PsoParams) -> PsoResult
+ *      (epoch_order.hpp:60, epoch_order.cpp:121-221). Bit-exact. */
+int lsg_pso_order(const uint64_t* d_w, uint32_t E, uint32_t swarm, uint32_t iters,
+                  double p_personal, double p_global, double inertia, double kick,
+                  uint32_t stagnation, uint32_t restart, uint64_t seed, uint32_t* d_order,
+                  uint64_t* d_cost, uint64_t* d_hist, uint32_t* d_iters, void* stream);
+
+/* ---- K1..K6: plan_schedule(const PipelineConfig&) -> PlanOutput
+ *      (pipeline.hpp:27, pipeline.cpp:32-120). Synchronises `stream` once to
+ *      report device-side invariant failures (InternalError). */
+int lsg_plan(const lsg_config* cfg, const lsg_plan_out* out, void* stream);
+
+/* Same, with host outputs (pinned or pageable): the e2e path. Host arrays
+ * follow lsg_plan_out layout; NULL members are skipped. */
+int lsg_plan_host(const lsg_config* cfg, const lsg_plan_out* h_out, void* stream);
+
+/* ---- K7: simulate_plan(plan, capacity, policy, false) -> SimResult
+ *      (buffer.hpp:117-118, buffer.cpp:183-247). The plan is given in the
+ *      lsg_plan_out item/offset layout with `T` steps of N nodes. Replays
+ *      nodes [node_begin, node_end) only (per-rank sharding); rows of other
+ *      nodes are left untouched. d_hits/d_misses: [T][N]. Optional d_slot
+ *      ([total items]) receives, per access, the HBM buffer slot the sample
+ *      occupies after its access (LSG_NEVER when it was bypassed). */
+int lsg_simulate(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N,
+                 uint64_t D, uint64_t capacity, int32_t policy, uint32_t node_begin,
+                 uint32_t node_end, uint32_t* d_hits, uint32_t* d_misses, uint32_t* d_slot,
+                 void* stream);
+
+/* ---- K9: Store payload (store.cpp:70-80) of samples ids[0..n) written to
+ *      dst rows: row r of `dst` (row pitch sample_bytes) receives the bytes
+ *      Store::read_one(ids[r]) would return for fill_seed. */
+int lsg_store_fill(const uint32_t* d_ids, uint64_t n, uint64_t sample_bytes, uint64_t fill_seed,
+                   void* d_dst, void* stream);
+
+/* ---- K8: batch gather from an HBM-resident sample buffer
+ *      (replaces Store::read_one/read_chunk, store.hpp:42-44, for buffered
+ *      samples). out row r = buf row slots[r]; rows are sample_bytes long and
+ *      16-byte aligned. */
+int lsg_gather(const void* d_buf, const uint32_t* d_slots, uint64_t n, uint64_t sample_bytes,
+               void* d_out, void* stream);
+
+/* Number of kernel launches issued by this library since load (for the
+ * bench's gpu_launches claim). */
+uint64_t lsg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

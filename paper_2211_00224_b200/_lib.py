@@ -1,0 +1,115 @@
+"""ctypes binding of the lsg C ABI (include/lsg.h).
+
+The shared library is built in-tree (``make lib`` / ``__graft_entry__.build()``)
+as ``paper_2211_00224_b200/libsolar_b200.so``. There is no fallback: if the
+library is missing or a CUDA device is absent, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsolar_b200.so")
+
+HIT_BIT = 0x80000000
+NEVER = 0xFFFFFFFE
+
+# Reference ErrorClass codes (errors.hpp:11-18)
+CONFIG, VALIDATION, CAPABILITY, CALIBRATION, STORAGE, INTERNAL = 2, 3, 4, 5, 6, 7
+
+
+class LsgConfig(ctypes.Structure):
+    """Field-for-field mirror of ``lsg_config`` (include/lsg.h)."""
+
+    _fields_ = [
+        ("dataset_size", ctypes.c_uint64),
+        ("num_epochs", ctypes.c_uint32),
+        ("num_nodes", ctypes.c_uint32),
+        ("local_batch", ctypes.c_uint64),
+        ("seed", ctypes.c_uint64),
+        ("drop_last", ctypes.c_int32),
+        ("policy", ctypes.c_int32),
+        ("buffer_capacity", ctypes.c_uint64),
+        ("graph_mode", ctypes.c_int32),
+        ("insert_redundant", ctypes.c_int32),
+        ("chunk_threshold", ctypes.c_uint64),
+        ("optim_order", ctypes.c_int32),
+        ("optim_remap", ctypes.c_int32),
+        ("optim_balance", ctypes.c_int32),
+        ("optim_chunk", ctypes.c_int32),
+        ("pso_swarm", ctypes.c_uint32),
+        ("pso_iters", ctypes.c_uint32),
+        ("pso_stagnation", ctypes.c_uint32),
+        ("pso_restart", ctypes.c_uint32),
+        ("pso_p_personal", ctypes.c_double),
+        ("pso_p_global", ctypes.c_double),
+        ("pso_inertia", ctypes.c_double),
+        ("pso_kick", ctypes.c_double),
+    ]
+
+
+class LsgShape(ctypes.Structure):
+    _fields_ = [
+        ("global_batch", ctypes.c_uint64),
+        ("steps_per_epoch", ctypes.c_uint64),
+        ("keep", ctypes.c_uint64),
+        ("total_steps", ctypes.c_uint64),
+        ("total_items", ctypes.c_uint64),
+    ]
+
+
+class LsgPlanOut(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in (
+        "trace", "graph", "order", "cost", "hist", "iters", "items", "node_off",
+        "fetch_before", "fetch_after")]
+
+
+EXPORTS = [
+    "lsg_version", "lsg_last_error", "lsg_shape_of", "lsg_generate_trace",
+    "lsg_build_reuse_graph", "lsg_pso_order", "lsg_plan", "lsg_plan_host", "lsg_simulate",
+    "lsg_store_fill", "lsg_gather", "lsg_launch_count",
+]
+
+
+class LsgError(RuntimeError):
+    """Raised with the reference ErrorClass code of the failing call."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the CUDA library (no fallback: raises if it is not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"lsg CUDA library not built: {LIB_PATH} missing (run `make lib` or "
+                "__graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        P, u64, u32, i32, dbl = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_int32,
+                                 ctypes.c_double)
+        L.lsg_version.restype = ctypes.c_int
+        L.lsg_last_error.restype = ctypes.c_char_p
+        L.lsg_launch_count.restype = u64
+        L.lsg_shape_of.argtypes = [ctypes.POINTER(LsgConfig), ctypes.POINTER(LsgShape)]
+        L.lsg_generate_trace.argtypes = [ctypes.POINTER(LsgConfig), P, P]
+        L.lsg_build_reuse_graph.argtypes = [P, u32, u64, u64, u32, u64, i32, u64, i32, P, P]
+        L.lsg_pso_order.argtypes = [P, u32, u32, u32, dbl, dbl, dbl, dbl, u32, u32, u64, P, P, P, P, P]
+        L.lsg_plan.argtypes = [ctypes.POINTER(LsgConfig), ctypes.POINTER(LsgPlanOut), P]
+        L.lsg_plan_host.argtypes = [ctypes.POINTER(LsgConfig), ctypes.POINTER(LsgPlanOut), P]
+        L.lsg_simulate.argtypes = [P, P, u64, u32, u64, u64, i32, u32, u32, P, P, P, P]
+        L.lsg_store_fill.argtypes = [P, u64, u64, u64, P, P]
+        L.lsg_gather.argtypes = [P, P, u64, u64, P, P]
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise LsgError(rc, lib().lsg_last_error().decode())

@@ -1,0 +1,115 @@
+// gather.cu — K8 batch gather from the HBM-resident sample buffer and K9 the
+// synthetic Store payload fill.
+//
+// K8 replaces the per-sample pread of Store::read_one (store.cpp:123-139) for
+// buffered samples: out row r = buf row slots[r]. It is a pure HBM copy
+// (read once, write once), so it is written as a persistent grid over 16 KiB
+// tiles with 128-bit loads issued 4-deep before their stores (MLP >= 4 per
+// thread) and evict-first hints on both sides (the batch is consumed by the
+// trainer, the buffer row is not re-read this step).
+//
+// K9 reproduces the Store payload (store.cpp:70-80): byte j of the payload is
+// byte j%8 (little-endian) of mix(fill_seed + (j/8 + 1)*gamma), and sample i
+// occupies payload bytes [i*size, (i+1)*size). Being counter-based, every
+// 8-byte word is computed independently.
+#include "common.cuh"
+
+namespace lsg {
+
+namespace {
+
+constexpr int kGatherThreads = 256;
+constexpr int kUnroll = 4;
+constexpr uint32_t kTileVec = kGatherThreads * kUnroll;  // uint4 per tile (16 KiB)
+
+__global__ void __launch_bounds__(kGatherThreads) k_gather(const uint4* __restrict__ buf,
+                                                           const uint32_t* __restrict__ slots,
+                                                           uint64_t n, uint64_t vec_per_row,
+                                                           uint64_t tiles_per_row,
+                                                           uint4* __restrict__ out) {
+    const uint64_t ntiles = n * tiles_per_row;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t row = tile / tiles_per_row;
+        const uint64_t c0 = (tile - row * tiles_per_row) * kTileVec;
+        const uint4* src = buf + uint64_t(__ldg(&slots[row])) * vec_per_row;
+        uint4* dst = out + row * vec_per_row;
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t c = c0 + u * kGatherThreads + threadIdx.x;
+            if (c < vec_per_row) v[u] = __ldcs(&src[c]);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t c = c0 + u * kGatherThreads + threadIdx.x;
+            if (c < vec_per_row) __stcs(&dst[c], v[u]);
+        }
+    }
+}
+
+// payload word path: sample_bytes % 16 == 0
+__global__ void __launch_bounds__(256) k_store_fill_vec(const uint32_t* __restrict__ ids, uint64_t n,
+                                                        uint64_t words_per_row, uint64_t seed,
+                                                        ulonglong2* __restrict__ dst) {
+    const uint64_t pairs = words_per_row / 2;
+    const uint64_t total = n * pairs;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t row = i / pairs, p = i - row * pairs;
+        const uint64_t word0 = uint64_t(ids[row]) * words_per_row + 2 * p;  // payload word index
+        ulonglong2 v;
+        v.x = mix64(seed + (word0 + 1) * kGamma);
+        v.y = mix64(seed + (word0 + 2) * kGamma);
+        __stcs(&dst[row * pairs + p], v);
+    }
+}
+
+// general byte path
+__global__ void k_store_fill_bytes(const uint32_t* __restrict__ ids, uint64_t n, uint64_t size,
+                                   uint64_t seed, uint8_t* __restrict__ dst) {
+    const uint64_t total = n * size;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t row = i / size, c = i - row * size;
+        const uint64_t j = uint64_t(ids[row]) * size + c;
+        dst[i] = uint8_t(mix64(seed + (j / 8 + 1) * kGamma) >> (8 * (j % 8)));
+    }
+}
+
+}  // namespace
+
+int gather_device(const void* d_buf, const uint32_t* d_slots, uint64_t n, uint64_t sample_bytes,
+                  void* d_out, cudaStream_t st) {
+    if (n == 0) return kOk;
+    if (sample_bytes == 0 || sample_bytes % 16 != 0)
+        return set_error(kValidation, "gather: sample_bytes must be a positive multiple of 16");
+    if ((reinterpret_cast<uintptr_t>(d_buf) | reinterpret_cast<uintptr_t>(d_out)) & 15)
+        return set_error(kValidation, "gather: buffers must be 16-byte aligned");
+    const uint64_t vpr = sample_bytes / 16;
+    const uint64_t tpr = (vpr + kTileVec - 1) / kTileVec;
+    const uint64_t tiles = n * tpr;
+    const unsigned grid = unsigned(std::min<uint64_t>(tiles, 148ull * 8));
+    k_gather<<<grid, kGatherThreads, 0, st>>>(static_cast<const uint4*>(d_buf), d_slots, n, vpr, tpr,
+                                              static_cast<uint4*>(d_out));
+    LSG_LAUNCH_CHECK("k_gather");
+    return kOk;
+}
+
+int store_fill_device(const uint32_t* d_ids, uint64_t n, uint64_t sample_bytes, uint64_t seed,
+                      void* d_dst, cudaStream_t st) {
+    if (n == 0) return kOk;
+    if (sample_bytes == 0) return set_error(kStorage, "store_fill: sample_size must be >= 1");
+    if (sample_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(d_dst) & 15) == 0) {
+        const uint64_t wpr = sample_bytes / 8;
+        k_store_fill_vec<<<grid_for(n * wpr / 2, 256, 148 * 16), 256, 0, st>>>(
+            d_ids, n, wpr, seed, static_cast<ulonglong2*>(d_dst));
+        LSG_LAUNCH_CHECK("k_store_fill_vec");
+    } else {
+        k_store_fill_bytes<<<grid_for(n * sample_bytes, 256, 148 * 16), 256, 0, st>>>(
+            d_ids, n, sample_bytes, seed, static_cast<uint8_t*>(d_dst));
+        LSG_LAUNCH_CHECK("k_store_fill_bytes");
+    }
+    return kOk;
+}
+
+}  // namespace lsg

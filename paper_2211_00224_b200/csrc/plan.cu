@@ -1,0 +1,761 @@
+// plan.cu — K5 (step-granular next use), sorted step batches, and K6: the
+// persistent planner step loop of plan_schedule (pipeline.cpp:32-120):
+// per step, locality remap (locality.cpp:7-42) or slicing (:57-73), fetch
+// balancing (balance.cpp:10-39) and the clairvoyant buffer advance
+// (buffer.cpp:37-46) for every node, bit-exact.
+//
+// The step recurrence (6,400 dependent steps at config 2) runs inside ONE
+// persistent CTA: no per-step launches, no host round trips; all state stays
+// in HBM/L2 (keys, holder masks, bucket bitmaps) and shared memory (the
+// current batch). Per step:
+//
+//  A  load batch ids, next-use keys and N-bit holder masks; classify items
+//     as no-holder / single-holder / multi-holder; per-warp ranks of singles
+//     with __match_any_sync (order-preserving, no atomics).
+//  B  per-node exclusive scan of the per-warp counts (warp k scans node k).
+//  C  exact S_k(j) (singles of node k before j) for every multi item.
+//  D  ONE warp resolves the multi-holder items serially, lanes = nodes:
+//     c_k = min(b, S_k(j) + M_k); argmin over holders with c_k < b,
+//     ties -> lowest k (__reduce_min_sync on (c<<5)|k).  This is the only
+//     serial part of the remap; singles then need no serial pass:
+//     single j (holder k) is a hit iff S_k(j) + M_k(<j) < b.
+//  E/F fetches fill nodes in ascending order up to b (prefix over free slots).
+//  G  balance is simulated on the N fetch counts only (thread 0); donors and
+//     recipients are disjoint, donor d's i-th move gives its i-th largest
+//     fetch id, recipients append in move order.
+//  H  final node lists -> plan output (ids | hit tag), offsets, fetch counts.
+//  I  buffer advance, nodes in parallel. Within a (node, step) an item is a
+//     hit iff it was resident at step start (every miss inserts a key beyond
+//     the current step, so current-step residents are never the eviction
+//     maximum). Runs of hits re-key; runs of misses insert then drop the
+//     (size - C)+ largest (key, id): streaming "keep the C smallest".
+//     Eviction walks a per-node "maybe non-empty" bucket bitmap over future
+//     steps (key = next-use step) and, inside bucket g', the step-g' batch in
+//     descending id order testing key == g' (the reference's tie rule: equal
+//     keys evict the larger id first). kNeverUsed keys live in an exact
+//     per-node id bitmap scanned from the top.
+#include "common.cuh"
+
+namespace lsg {
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kMaxN = 32;
+constexpr uint32_t kMaxB = 8192;
+constexpr uint32_t kFetch = 0xFFFFFFFFu;
+
+// ----------------------------------------------------------------- K5 ----
+// nu for the access of x at execution epoch i, position pos: the first
+// later execution epoch j whose kept prefix contains x gives
+// j*S + floor(inv/B) (the global step of its next use), else kNever.
+__global__ void k_nextuse(const uint32_t* __restrict__ trace, const uint32_t* __restrict__ order,
+                          const uint32_t* __restrict__ inv, uint32_t E, uint32_t keep, uint32_t D,
+                          uint32_t S, uint32_t B, uint32_t* __restrict__ nu) {
+    const uint32_t i = blockIdx.y;
+    const uint32_t e = order[i];
+    for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < keep; pos += gridDim.x * blockDim.x) {
+        const uint32_t x = trace[size_t(e) * keep + pos];
+        uint32_t r = kNever;
+        for (uint32_t j = i + 1; j < E; ++j) {
+            const uint32_t p2 = inv[size_t(order[j]) * D + x];
+            if (p2 != kNone) {
+                r = j * S + p2 / B;
+                break;
+            }
+        }
+        nu[size_t(i) * keep + pos] = r;
+    }
+}
+
+// Each step's batch sorted by descending id (bucket enumeration order).
+__global__ void __launch_bounds__(1024) k_sort_batches(const uint32_t* __restrict__ trace,
+                                                       const uint32_t* __restrict__ order,
+                                                       uint32_t keep, uint32_t S, uint32_t B,
+                                                       uint32_t P2, uint32_t* __restrict__ sb) {
+    extern __shared__ uint32_t sk[];
+    const uint32_t g = blockIdx.x, i = g / S, t = g % S;
+    const uint32_t lo = t * B, len = min(B, keep - lo);
+    const uint32_t* row = trace + size_t(order[i]) * keep + lo;
+    for (uint32_t r = threadIdx.x; r < P2; r += blockDim.x) sk[r] = r < len ? row[r] : 0xFFFFFFFFu;
+    __syncthreads();
+    for (uint32_t size = 2; size <= P2; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t r = threadIdx.x; r < P2 / 2; r += blockDim.x) {
+                const uint32_t a = 2 * stride * (r / stride) + (r % stride), c = a + stride;
+                const bool up = (a & size) == 0;
+                const uint32_t x = sk[a], y = sk[c];
+                if ((x > y) == up) { sk[a] = y; sk[c] = x; }
+            }
+            __syncthreads();
+        }
+    }
+    uint32_t* out = sb + size_t(i) * keep + lo;
+    for (uint32_t r = threadIdx.x; r < len; r += blockDim.x) out[r] = sk[len - 1 - r];
+}
+
+// ----------------------------------------------------------------- K6 ----
+struct LoopArgs {
+    uint32_t D, N, b, B, S, E, keep, T, C;
+    int remap, balance;
+    uint32_t nzw;                    // words per node in the bucket bitmap
+    uint32_t infw;                   // words per node in the never-used bitmap
+    const uint32_t* trace;           // [E][keep]
+    const uint32_t* order;           // [E]
+    const uint32_t* nu;              // [E*keep] execution order
+    const uint32_t* sb;              // [E*keep] execution order, desc per step
+    uint32_t* key;                   // [N][D]
+    uint32_t* hm;                    // [D] holder masks
+    uint32_t* nz;                    // [N][nzw]
+    uint32_t* infbm;                 // [N][infw]
+    uint32_t* smul;                  // [B][N] scratch
+    uint32_t* mpos;                  // [N][b] scratch
+    uint32_t* mres;                  // [B] scratch
+    uint32_t* mv;                    // [B] scratch: moves (d | r<<8 | q<<16)
+    uint32_t* dmoves;                // [N][B] scratch: donor's i-th move
+    uint32_t* items;                 // [E*keep] output
+    uint32_t* node_off;              // [T][N+1] output
+    uint32_t* fb;                    // [T][N] output (may be null)
+    uint32_t* fa;                    // [T][N] output (may be null)
+    uint32_t* status;
+};
+
+struct Shared {
+    uint32_t* sx;     // [B] ids
+    uint32_t* snu;    // [B] next-use keys
+    uint32_t* smask;  // [B] holder masks at step start
+    uint32_t* sinfo;  // [B] per-item scratch
+    uint32_t* pre;    // [B] pre-balance lists, node k at k*b (j | hit tag)
+    uint32_t* fin;    // [B] final lists (j | k<<16 | hit tag)
+};
+
+struct Small {
+    uint32_t wcnt[kWarps][kMaxN];   // per-warp single counts -> bases
+    uint32_t cm[kWarps][kMaxN];     // per-chunk single lanes per holder
+    uint32_t wmul[kWarps];          // per-warp multi counts -> bases
+    uint32_t wfet[kWarps];          // per-warp fetch counts -> bases
+    uint32_t tot[kMaxN];            // singles per node
+    uint32_t mtot[kMaxN];           // multi assigned per node
+    uint32_t size[kMaxN];           // hits per node (list prefix)
+    uint32_t free_pre[kMaxN + 1];   // prefix of free capacity
+    uint32_t lenk[kMaxN];           // pre-balance list length
+    uint32_t fcnt[kMaxN];           // fetches before balance
+    uint32_t outk[kMaxN], ink[kMaxN];
+    uint32_t thr[kMaxN];            // donor moved-id threshold
+    uint32_t noff[kMaxN + 1];       // final offsets
+    uint32_t bsize[kMaxN];          // buffer occupancy
+    uint32_t top[kMaxN];            // bucket upper bound
+    uint32_t inftop[kMaxN];         // never-used bitmap upper word bound
+    uint32_t infcnt[kMaxN];         // never-used residents
+    uint32_t nmulti, nfetch, nmoves;
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// buffer.cpp:37-41 (re-key) / :42-46 (insert) without the eviction: key
+// update plus the bucket / never-used summaries.
+__device__ __forceinline__ void set_key(const LoopArgs& a, Small& sm, uint32_t k, uint32_t x,
+                                        uint32_t nu) {
+    a.key[size_t(k) * a.D + x] = nu;
+    if (nu == kNever) {
+        atomicOr(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
+        atomicAdd(&sm.infcnt[k], 1u);
+        atomicMax(&sm.inftop[k], x >> 5);
+    } else {
+        atomicOr(&a.nz[size_t(k) * a.nzw + (nu >> 5)], 1u << (nu & 31));
+        atomicMax(&sm.top[k], nu);
+    }
+}
+
+__device__ __forceinline__ void drop(const LoopArgs& a, uint32_t k, uint32_t x) {
+    a.key[size_t(k) * a.D + x] = kNone;
+    atomicAnd(&a.hm[x], ~(1u << k));
+}
+
+// Remove the `need` largest (key, id) residents of node k. Whole warp.
+__device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t need, uint32_t lane) {
+    const uint32_t lt = lanemask_lt();
+    while (need > 0) {
+        if (sm.infcnt[k] > 0) {  // kNeverUsed bucket: ids descending
+            uint32_t* bm = a.infbm + size_t(k) * a.infw;
+            int32_t wi = int32_t(sm.inftop[k]);
+            bool found = false;
+            while (wi >= 0 && !found) {
+                const int32_t myw = wi - int32_t(lane);
+                const uint32_t v = myw >= 0 ? __ldcg(&bm[myw]) : 0u;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+                if (bal) {
+                    const uint32_t src = __ffs(bal) - 1;
+                    const int32_t hw = wi - int32_t(src);
+                    uint32_t word = __shfl_sync(0xFFFFFFFFu, v, src);
+                    // take bits from the top of this word
+                    while (word && need > 0) {
+                        const uint32_t bit = 31 - __clz(word);
+                        word &= ~(1u << bit);
+                        const uint32_t x = uint32_t(hw) * 32 + bit;
+                        if (lane == 0) {
+                            drop(a, k, x);
+                            atomicAnd(&bm[hw], ~(1u << bit));
+                        }
+                        --need;
+                        if (lane == 0) { sm.infcnt[k] -= 1; sm.bsize[k] -= 1; }
+                    }
+                    if (lane == 0) sm.inftop[k] = uint32_t(hw);
+                    found = true;
+                } else {
+                    wi -= 32;
+                }
+                __syncwarp();
+            }
+            if (!found) {  // bookkeeping says never-used residents exist
+                if (lane == 0) { atomicOr(a.status, 2u); sm.infcnt[k] = 0; }
+                __syncwarp();
+            }
+            continue;
+        }
+        // highest possibly non-empty finite bucket
+        uint32_t* nzk = a.nz + size_t(k) * a.nzw;
+        int32_t wi = int32_t(sm.top[k] >> 5);
+        int32_t beta = -1;
+        while (wi >= 0) {
+            const int32_t myw = wi - int32_t(lane);
+            const uint32_t v = myw >= 0 ? __ldcg(&nzk[myw]) : 0u;
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+            if (bal) {
+                const uint32_t src = __ffs(bal) - 1;
+                const uint32_t word = __shfl_sync(0xFFFFFFFFu, v, src);
+                beta = (wi - int32_t(src)) * 32 + (31 - __clz(word));
+                break;
+            }
+            wi -= 32;
+        }
+        if (beta < 0) {
+            if (lane == 0) atomicOr(a.status, 4u);
+            return;
+        }
+        // scan the step-beta batch (desc ids) for members key == beta
+        const uint32_t gi = uint32_t(beta) / a.S, gt = uint32_t(beta) % a.S;
+        const uint32_t lo = gt * a.B, blen = min(a.B, a.keep - lo);
+        const uint32_t* cand = a.sb + size_t(gi) * a.keep + lo;
+        const uint32_t* keyk = a.key + size_t(k) * a.D;
+        uint32_t c = 0;
+        for (; c < blen && need > 0; c += 32) {
+            const uint32_t r = c + lane;
+            uint32_t x = 0;
+            bool mem = false;
+            if (r < blen) {
+                x = cand[r];
+                mem = __ldcg(&keyk[x]) == uint32_t(beta);
+            }
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mem);
+            const uint32_t rank = __popc(bal & lt);
+            if (mem && rank < need) drop(a, k, x);
+            const uint32_t took = min(uint32_t(__popc(bal)), need);
+            need -= took;
+            if (lane == 0) sm.bsize[k] -= took;
+        }
+        __syncwarp();
+        if (c >= blen && need > 0) {
+            // whole bucket scanned and exhausted: it is empty now
+            if (lane == 0) atomicAnd(&nzk[beta >> 5], ~(1u << (beta & 31)));
+        }
+        if (lane == 0) sm.top[k] = uint32_t(beta);
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
+    extern __shared__ __align__(16) uint32_t dyn[];
+    __shared__ Small sm;
+    Shared s;
+    s.sx = dyn;
+    s.snu = dyn + a.B;
+    s.smask = dyn + 2 * a.B;
+    s.sinfo = dyn + 3 * a.B;
+    s.pre = dyn + 4 * a.B;
+    s.fin = dyn + 5 * a.B;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t N = a.N, b = a.b;
+    const uint32_t lt = lanemask_lt();
+    if (tid < kMaxN) {
+        sm.bsize[tid] = 0;
+        sm.top[tid] = 0;
+        sm.inftop[tid] = 0;
+        sm.infcnt[tid] = 0;
+    }
+    __syncthreads();
+    size_t gbase = 0;
+    for (uint32_t g = 0; g < a.T; ++g) {
+        const uint32_t i = g / a.S, t = g % a.S;
+        const uint32_t lo = t * a.B, len = min(a.B, a.keep - lo);
+        const uint32_t* row = a.trace + size_t(a.order[i]) * a.keep + lo;
+        const uint32_t* nurow = a.nu + size_t(i) * a.keep + lo;
+        const uint32_t R = ((len + kThreads - 1) / kThreads) * 32;  // items per warp
+        const uint32_t j0 = w * R, j1 = min(j0 + R, len);
+
+        // ---------------- A: load + classify + per-warp single ranks
+        if (lane < kMaxN) sm.wcnt[w][lane] = 0;
+        uint32_t wm = 0;
+        __syncwarp();
+        for (uint32_t c = j0; c < j0 + R; c += 32) {
+            const uint32_t j = c + lane;
+            const bool valid = j < j1;
+            uint32_t x = 0, nu = 0, m = 0;
+            if (valid) {
+                x = row[j];
+                nu = nurow[j];
+                m = __ldcg(&a.hm[x]);
+                s.sx[j] = x;
+                s.snu[j] = nu;
+                s.smask[j] = m;
+            }
+            if (!a.remap) continue;
+            const uint32_t hc = __popc(m);
+            const bool single = valid && hc == 1, multi = valid && hc >= 2;
+            const uint32_t h = single ? __ffs(m) - 1 : 0;
+            if (lane < kMaxN) sm.cm[w][lane] = 0;
+            __syncwarp();
+            const uint32_t grp = __match_any_sync(0xFFFFFFFFu, single ? h : 0x100u + lane);
+            if (single && lane == uint32_t(__ffs(grp) - 1)) sm.cm[w][h] = grp;
+            __syncwarp();
+            if (single) s.sinfo[j] = sm.wcnt[w][h] + __popc(grp & lt);
+            const uint32_t mb = __ballot_sync(0xFFFFFFFFu, multi);
+            if (multi) {
+                s.sinfo[j] = wm + __popc(mb & lt);
+                uint32_t mm = m;
+                while (mm) {
+                    const uint32_t k = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    a.smul[size_t(j) * N + k] = sm.wcnt[w][k] + __popc(sm.cm[w][k] & lt);
+                }
+            }
+            __syncwarp();
+            if (single && lane == uint32_t(__ffs(grp) - 1)) sm.wcnt[w][h] += __popc(grp);
+            wm += __popc(mb);
+            __syncwarp();
+        }
+        if (lane == 0) sm.wmul[w] = wm;
+        __syncthreads();
+
+        if (a.remap) {
+            // ------------ B: scans over warps (warp k: node k; warp 31: multi)
+            if (w < N) {
+                const uint32_t v = sm.wcnt[lane][w];
+                uint32_t inc = v;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                    if (lane >= uint32_t(d)) inc += o;
+                }
+                sm.wcnt[lane][w] = inc - v;
+                if (lane == 31) sm.tot[w] = inc;
+            }
+            if (w == kWarps - 1) {
+                const uint32_t v = sm.wmul[lane];
+                uint32_t inc = v;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                    if (lane >= uint32_t(d)) inc += o;
+                }
+                sm.wmul[lane] = inc - v;
+                if (lane == 31) sm.nmulti = inc;
+            }
+            __syncthreads();
+            // ------------ C: global ranks; exact S_k(j) for multi items
+            for (uint32_t j = j0 + lane; j < j1; j += 32) {
+                const uint32_t m = s.smask[j];
+                const uint32_t hc = __popc(m);
+                if (hc == 1) {
+                    s.sinfo[j] += sm.wcnt[w][__ffs(m) - 1];
+                } else if (hc >= 2) {
+                    const uint32_t mi = sm.wmul[w] + s.sinfo[j];
+                    s.sinfo[j] = mi;
+                    s.pre[mi] = j;  // multi list (pre is free until F)
+                    uint32_t mm = m;
+                    while (mm) {
+                        const uint32_t k = __ffs(mm) - 1;
+                        mm &= mm - 1;
+                        a.smul[size_t(j) * N + k] += sm.wcnt[w][k];
+                    }
+                }
+            }
+            __syncthreads();
+            // ------------ D: serial multi-holder pass, lanes = nodes
+            if (w == 0) {
+                uint32_t M = 0;
+                const uint32_t nm = sm.nmulti;
+                uint32_t jn = nm ? s.pre[0] : 0;
+                uint32_t mkn = nm ? s.smask[jn] : 0;
+                uint32_t sn = (nm && lane < N) ? a.smul[size_t(jn) * N + lane] : 0;
+                for (uint32_t mi = 0; mi < nm; ++mi) {
+                    const uint32_t j = jn, mk = mkn, sk = sn;
+                    if (mi + 1 < nm) {  // prefetch the next item
+                        jn = s.pre[mi + 1];
+                        mkn = s.smask[jn];
+                        sn = lane < N ? a.smul[size_t(jn) * N + lane] : 0;
+                    }
+                    const bool in = lane < N && ((mk >> lane) & 1u);
+                    const uint32_t cnt = min(b, sk + M);
+                    const uint32_t keyv = (in && cnt < b) ? ((cnt << 5) | lane) : 0xFFFFFFFFu;
+                    const uint32_t best = __reduce_min_sync(0xFFFFFFFFu, keyv);
+                    if (best != 0xFFFFFFFFu && lane == (best & 31)) {
+                        a.mpos[size_t(lane) * b + M] = j;
+                        ++M;
+                    }
+                    if (lane == 0) a.mres[mi] = best;
+                }
+                if (lane < N) sm.mtot[lane] = M;
+            }
+            __syncthreads();
+            // ------------ E: hits/positions for singles; fetch ranks
+            uint32_t wf = 0;
+            for (uint32_t c = j0; c < j0 + R; c += 32) {
+                const uint32_t j = c + lane;
+                const bool valid = j < j1;
+                bool fetch = false;
+                if (valid) {
+                    const uint32_t m = s.smask[j];
+                    const uint32_t hc = __popc(m);
+                    if (hc == 1) {
+                        const uint32_t h = __ffs(m) - 1;
+                        const uint32_t S = s.sinfo[j];
+                        // M_h(<j): multi items before j assigned to h
+                        const uint32_t* mp = a.mpos + size_t(h) * b;
+                        uint32_t lo2 = 0, hi2 = sm.mtot[h];
+                        while (lo2 < hi2) {
+                            const uint32_t mid = (lo2 + hi2) >> 1;
+                            if (mp[mid] < j) lo2 = mid + 1; else hi2 = mid;
+                        }
+                        const uint32_t pos = S + lo2;
+                        if (pos < b) s.sinfo[j] = (h << 24) | pos;
+                        else fetch = true;
+                    } else if (hc >= 2) {
+                        const uint32_t r = a.mres[s.sinfo[j]];
+                        if (r != 0xFFFFFFFFu) s.sinfo[j] = ((r & 31) << 24) | (r >> 5);
+                        else fetch = true;
+                    } else {
+                        fetch = true;
+                    }
+                }
+                const uint32_t fbal = __ballot_sync(0xFFFFFFFFu, fetch);
+                if (fetch) s.sinfo[j] = kFetch - (wf + __popc(fbal & lt)) ;  // encoded below
+                wf += __popc(fbal);
+            }
+            if (lane == 0) sm.wfet[w] = wf;
+            if (tid < N) sm.size[tid] = min(b, sm.tot[tid] + sm.mtot[tid]);
+            __syncthreads();
+            if (w == 0) {
+                const uint32_t v = sm.wfet[lane];
+                uint32_t inc = v;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                    if (lane >= uint32_t(d)) inc += o;
+                }
+                sm.wfet[lane] = inc - v;
+                const uint32_t F = __shfl_sync(0xFFFFFFFFu, inc, 31);
+                // free-capacity prefix over nodes (ascending fill, locality.cpp:33-39)
+                const uint32_t fr = lane < N ? b - sm.size[lane] : 0;
+                uint32_t pinc = fr;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, pinc, d);
+                    if (lane >= uint32_t(d)) pinc += o;
+                }
+                const uint32_t pex = pinc - fr;
+                if (lane < N) {
+                    sm.free_pre[lane] = pex;
+                    const uint32_t got = F > pex ? min(fr, F - pex) : 0u;
+                    sm.fcnt[lane] = got;
+                    sm.lenk[lane] = sm.size[lane] + got;
+                }
+                if (lane == N - 1) sm.free_pre[N] = pinc;
+                if (lane == 0) sm.nfetch = F;
+                const uint32_t totfree = __shfl_sync(0xFFFFFFFFu, pinc, N - 1);
+                if (lane == 0 && F > totfree) atomicOr(a.status, 8u);  // ran out of capacity
+            }
+            __syncthreads();
+            // ------------ F: pre-balance lists [hits in batch order][fetches]
+            for (uint32_t j = j0 + lane; j < j1; j += 32) {
+                const uint32_t v = s.sinfo[j];
+                if (v >= kFetch - kMaxB) {
+                    const uint32_t f = sm.wfet[w] + (kFetch - v);
+                    // node with free_pre[k] <= f < free_pre[k+1]
+                    uint32_t k = 0;
+                    while (k + 1 < N && sm.free_pre[k + 1] <= f) ++k;
+                    const uint32_t pos = sm.size[k] + (f - sm.free_pre[k]);
+                    s.pre[k * b + pos] = j;
+                } else {
+                    s.pre[(v >> 24) * b + (v & 0xFFFFFF)] = j | kHit;
+                }
+            }
+        } else {
+            // slice_step (locality.cpp:57-73): node k = positions [k*b, (k+1)*b)
+            for (uint32_t j = tid; j < len; j += kThreads) {
+                const uint32_t k = j / b;
+                const bool hit = (s.smask[j] >> k) & 1u;
+                s.pre[j] = j | (hit ? kHit : 0u);
+            }
+            if (tid < N) {
+                const uint32_t l0 = min(tid * b, len), l1 = min(l0 + b, len);
+                sm.lenk[tid] = l1 - l0;
+                sm.size[tid] = 0;
+            }
+            __syncthreads();
+            if (tid < N) {
+                uint32_t f = 0;
+                for (uint32_t p = 0; p < sm.lenk[tid]; ++p) f += (s.pre[tid * b + p] & kHit) ? 0u : 1u;
+                sm.fcnt[tid] = f;
+            }
+        }
+        __syncthreads();
+
+        // ---------------- G: balance on counts (balance.cpp:10-39)
+        if (tid < N) {
+            sm.outk[tid] = 0;
+            sm.ink[tid] = 0;
+            sm.thr[tid] = 0;
+            if (a.fb) a.fb[size_t(g) * N + tid] = sm.fcnt[tid];
+        }
+        __syncthreads();
+        if (a.balance && tid == 0) {
+            uint32_t cnt[kMaxN];
+            for (uint32_t k = 0; k < N; ++k) cnt[k] = sm.fcnt[k];
+            uint32_t nmv = 0;
+            for (;;) {
+                uint32_t d = 0, r = 0;
+                for (uint32_t k = 1; k < N; ++k) {
+                    if (cnt[k] > cnt[d]) d = k;
+                    if (cnt[k] < cnt[r]) r = k;
+                }
+                if (cnt[d] - cnt[r] <= 1) break;
+                const uint32_t q = sm.ink[r];
+                a.dmoves[size_t(d) * a.B + sm.outk[d]] = r | (q << 8);
+                sm.outk[d] += 1;
+                sm.ink[r] = q + 1;
+                --cnt[d];
+                ++cnt[r];
+                ++nmv;
+            }
+            sm.nmoves = nmv;
+        }
+        __syncthreads();
+        // donors: the out_k-th largest fetch id is the moved/kept threshold
+        if (a.balance && sm.nmoves) {
+            for (uint32_t k = 0; k < N; ++k) {
+                const uint32_t out = sm.outk[k];
+                if (!out) continue;
+                const uint32_t L = sm.lenk[k];
+                for (uint32_t p = tid; p < L; p += kThreads) {
+                    const uint32_t e = s.pre[k * b + p];
+                    if (e & kHit) continue;
+                    const uint32_t x = s.sx[e & 0xFFFF];
+                    uint32_t rank = 0;
+                    for (uint32_t p2 = 0; p2 < L; ++p2) {
+                        const uint32_t e2 = s.pre[k * b + p2];
+                        if (!(e2 & kHit) && s.sx[e2 & 0xFFFF] > x) ++rank;
+                    }
+                    if (rank == out - 1) sm.thr[k] = x;
+                }
+            }
+            __syncthreads();
+        }
+        // ---------------- H: final lists + outputs
+        if (w == 0) {
+            const uint32_t L = lane < N ? sm.lenk[lane] - sm.outk[lane] + sm.ink[lane] : 0;
+            uint32_t inc = L;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                if (lane >= uint32_t(d)) inc += o;
+            }
+            if (lane < N) {
+                sm.noff[lane] = inc - L;
+                a.node_off[size_t(g) * (N + 1) + lane] = inc - L;
+                if (a.fa) a.fa[size_t(g) * N + lane] = sm.fcnt[lane] - sm.outk[lane] + sm.ink[lane];
+            }
+            if (lane == N - 1) {
+                sm.noff[N] = inc;
+                a.node_off[size_t(g) * (N + 1) + N] = inc;
+                if (inc != len) atomicOr(a.status, 16u);  // multiset size check
+            }
+        }
+        __syncthreads();
+        // warp k places node k's pre-balance list (k < N)
+        for (uint32_t k = w; k < N; k += kWarps) {
+            const uint32_t L = sm.lenk[k], out = sm.outk[k], thr = sm.thr[k];
+            uint32_t shift = 0;
+            for (uint32_t c = 0; c < L; c += 32) {
+                const uint32_t p = c + lane;
+                uint32_t e = 0;
+                bool moved = false;
+                if (p < L) {
+                    e = s.pre[k * b + p];
+                    moved = out && !(e & kHit) && s.sx[e & 0xFFFF] >= thr;
+                }
+                const uint32_t mbal = __ballot_sync(0xFFFFFFFFu, moved);
+                if (p < L) {
+                    uint32_t dst;
+                    if (moved) {
+                        // rank among moved = number of moved ids larger than this one
+                        const uint32_t x = s.sx[e & 0xFFFF];
+                        uint32_t rank = 0;
+                        for (uint32_t p2 = 0; p2 < L; ++p2) {
+                            const uint32_t e2 = s.pre[k * b + p2];
+                            if (!(e2 & kHit) && s.sx[e2 & 0xFFFF] > x) ++rank;
+                        }
+                        const uint32_t mvv = a.dmoves[size_t(k) * a.B + rank];
+                        const uint32_t r = mvv & 0xFF, q = mvv >> 8;
+                        dst = sm.noff[r] + (sm.lenk[r]) + q;
+                        s.fin[dst] = (e & 0xFFFF) | (r << 16);
+                    } else {
+                        dst = sm.noff[k] + p - (shift + __popc(mbal & lt));
+                        s.fin[dst] = (e & 0xFFFF) | (k << 16) | (e & kHit);
+                    }
+                    a.items[gbase + dst] = s.sx[e & 0xFFFF] | (e & kHit);
+                }
+                shift += __popc(mbal);
+            }
+        }
+        __syncthreads();
+
+        // ---------------- I: buffer advance, nodes in parallel
+        if (a.remap) {  // tagged hits form each list's prefix: one re-key run
+            for (uint32_t p = tid; p < len; p += kThreads) {
+                const uint32_t e = s.fin[p];
+                if (!(e & kHit)) continue;
+                const uint32_t j = e & 0xFFFF, k = (e >> 16) & 0xFF;
+                set_key(a, sm, k, s.sx[j], s.snu[j]);
+            }
+            __syncthreads();
+        }
+        for (uint32_t k = w; k < N; k += kWarps) {
+            const uint32_t begin = sm.noff[k] + (a.remap ? sm.size[k] : 0u), end = sm.noff[k + 1];
+            for (uint32_t c = begin; c < end; c += 32) {
+                const uint32_t p = c + lane;
+                const bool valid = p < end;
+                uint32_t j = 0;
+                bool res = false;
+                if (valid) {
+                    j = s.fin[p] & 0xFFFF;
+                    res = (s.smask[j] >> k) & 1u;  // residency at step start
+                }
+                const uint32_t vbal = __ballot_sync(0xFFFFFFFFu, valid);
+                const uint32_t rbal = __ballot_sync(0xFFFFFFFFu, res);
+                // walk the chunk's runs in order
+                uint32_t done = 0;
+                while (done != vbal) {
+                    const uint32_t first = __ffs(vbal & ~done) - 1;
+                    const bool hitrun = (rbal >> first) & 1u;
+                    // run = maximal lanes from `first` with the same residency
+                    const uint32_t same = hitrun ? rbal : (vbal & ~rbal);
+                    const uint32_t after = (~same) & vbal & ~((1u << first) - 1u) & ~(1u << first);
+                    const uint32_t stop = after ? __ffs(after) - 1 : 32u;
+                    const uint32_t run = (stop == 32 ? 0xFFFFFFFFu : ((1u << stop) - 1u)) & ~((1u << first) - 1u) & vbal;
+                    const bool mine = (run >> lane) & 1u;
+                    if (mine) {
+                        const uint32_t x = s.sx[j];
+                        set_key(a, sm, k, x, s.snu[j]);
+                        if (!hitrun) atomicOr(&a.hm[x], 1u << k);
+                    }
+                    __syncwarp();
+                    if (!hitrun) {
+                        const uint32_t m = __popc(run);
+                        uint32_t need = 0;
+                        if (lane == 0) {
+                            sm.bsize[k] += m;
+                            need = sm.bsize[k] > a.C ? sm.bsize[k] - a.C : 0u;
+                        }
+                        need = __shfl_sync(0xFFFFFFFFu, need, 0);
+                        __syncwarp();
+                        if (need) evict_walk(a, sm, k, need, lane);
+                    }
+                    __syncwarp();
+                    done |= run;
+                }
+            }
+        }
+        __syncthreads();
+        gbase += len;
+    }
+}
+
+}  // namespace
+
+
+int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, const uint32_t* d_trace,
+                     const uint32_t* d_order, const uint32_t* d_inv, uint32_t* d_items,
+                     uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
+                     cudaStream_t st) {
+    if (dm.N > kMaxN)
+        return set_error(kCapability, "plan: device planner supports num_nodes <= 32 in this build");
+    if (dm.B > kMaxB)
+        return set_error(kCapability, "plan: device planner supports global batch <= 8192 in this build");
+    if (dm.T >= 0xFFFFFFF0ull) return set_error(kCapability, "plan: too many steps");
+    Scratch sc(st);
+    const size_t EK = size_t(dm.E) * dm.keep;
+    uint32_t* nu = sc.get<uint32_t>(EK);
+    uint32_t* sb = sc.get<uint32_t>(EK);
+    LoopArgs a{};
+    a.D = uint32_t(dm.D);
+    a.N = dm.N;
+    a.b = dm.b;
+    a.B = uint32_t(dm.B);
+    a.S = uint32_t(dm.S);
+    a.E = dm.E;
+    a.keep = uint32_t(dm.keep);
+    a.T = uint32_t(dm.T);
+    a.C = uint32_t(std::min<uint64_t>(C, 0xFFFFFFF0ull));
+    a.remap = remap;
+    a.balance = balance;
+    a.nzw = uint32_t((dm.T + 31) / 32 + 1);
+    a.infw = uint32_t((dm.D + 31) / 32);
+    a.key = sc.get<uint32_t>(size_t(dm.N) * dm.D);
+    a.hm = sc.get<uint32_t>(dm.D);
+    a.nz = sc.get<uint32_t>(size_t(dm.N) * a.nzw);
+    a.infbm = sc.get<uint32_t>(size_t(dm.N) * a.infw);
+    a.smul = sc.get<uint32_t>(size_t(dm.B) * dm.N);
+    a.mpos = sc.get<uint32_t>(size_t(dm.N) * dm.b);
+    a.mres = sc.get<uint32_t>(dm.B);
+    a.mv = sc.get<uint32_t>(dm.B);
+    a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B);
+    if (!nu || !sb || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.mpos || !a.mres ||
+        !a.mv || !a.dmoves)
+        return set_error(kInternal, "plan: scratch allocation failed");
+    LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(dm.N) * dm.D * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.hm, 0, dm.D * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.nz, 0, size_t(dm.N) * a.nzw * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.infbm, 0, size_t(dm.N) * a.infw * 4, st));
+    // K5
+    k_nextuse<<<dim3(grid_for(dm.keep, 256, 1024), dm.E), 256, 0, st>>>(
+        d_trace, d_order, d_inv, dm.E, uint32_t(dm.keep), uint32_t(dm.D), uint32_t(dm.S), uint32_t(dm.B), nu);
+    LSG_LAUNCH_CHECK("k_nextuse");
+    // sorted batches
+    uint32_t P2 = 1;
+    while (P2 < dm.B) P2 <<= 1;
+    k_sort_batches<<<uint32_t(dm.T), 1024, P2 * 4, st>>>(d_trace, d_order, uint32_t(dm.keep),
+                                                          uint32_t(dm.S), uint32_t(dm.B), P2, sb);
+    LSG_LAUNCH_CHECK("k_sort_batches");
+    a.trace = d_trace;
+    a.order = d_order;
+    a.nu = nu;
+    a.sb = sb;
+    a.items = d_items;
+    a.node_off = d_node_off;
+    a.fb = d_fb;
+    a.fa = d_fa;
+    a.status = d_status;
+    const size_t smem = size_t(6) * dm.B * 4;
+    LSG_CUDA(cudaFuncSetAttribute(k_plan_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_plan_loop<<<1, kThreads, smem, st>>>(a);
+    LSG_LAUNCH_CHECK("k_plan_loop");
+    return kOk;
+}
+
+}  // namespace lsg

@@ -1,0 +1,438 @@
+// replay.cu — K7: per-rank clairvoyant replay of a plan (simulate_plan,
+// buffer.cpp:183-247, with next_use_chain :103-112), bit-exact hits/misses
+// per (step, node), plus the HBM slot each access lands in (for K8).
+//
+// Each node's buffer is independent, so one CTA replays one node (ranks shard
+// across GPUs by node range). Keys are positions in the node's own flattened
+// sequence; the position of list item i at step g is encoded as g*B + i, which
+// orders exactly like the flattened position and needs no per-node prefix.
+//
+//  1. step bases (exclusive scan of step lengths), one block;
+//  2. backward pass per node: next-use key of every access from a per-node
+//     last-seen table, one step at a time, parallel inside the step; a
+//     (node, step) that repeats an id is detected here (the within-step
+//     batching below assumes ids are unique per (node, step), which every plan
+//     plan_schedule emits satisfies);
+//  3. forward replay per node: an item is a hit iff resident at step start;
+//     runs of hits re-key, runs of misses insert then evict the (size-C)+
+//     largest (key, id) — bucket = step of the next use, candidates = that
+//     step's list of this node in reverse (keys are unique positions, so no
+//     ties), kNeverUsed residents in an id bitmap scanned from the top.
+#include "common.cuh"
+
+namespace lsg {
+
+namespace {
+
+constexpr int kRT = 256;  // threads per node CTA
+constexpr uint32_t kRMaxList = 8192;
+
+__device__ __forceinline__ uint32_t lanemask_lt_r() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// exclusive scan of node_off[g][N] over g -> gb[g] (one block, chunked)
+__global__ void __launch_bounds__(1024) k_step_bases(const uint32_t* __restrict__ node_off, uint32_t T,
+                                                     uint32_t N, uint64_t* __restrict__ gb) {
+    __shared__ uint64_t part[32];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint32_t c = 0; c < T; c += 1024) {
+        const uint32_t g = c + threadIdx.x;
+        const uint64_t v = g < T ? node_off[size_t(g) * (N + 1) + N] : 0;
+        uint64_t inc = v;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= uint32_t(d)) inc += o;
+        }
+        if (lane == 31) part[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            uint64_t p = part[lane], pi = p;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pi, d);
+                if (lane >= uint32_t(d)) pi += o;
+            }
+            part[lane] = pi - p;
+        }
+        __syncthreads();
+        if (g < T) gb[g] = carry + part[w] + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += part[w] + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) gb[T] = carry;
+}
+
+struct ReplayArgs {
+    uint32_t T, N, D, B, C, k0;
+    uint32_t nzw, infw;
+    const uint32_t* items;
+    const uint32_t* node_off;
+    const uint64_t* gb;
+    uint32_t* nuk;     // [total items] next-use key per access
+    uint32_t* last;    // [N][D]
+    uint32_t* key;     // [N][D]
+    uint32_t* slot;    // [N][D]
+    uint32_t* nz;      // [N][nzw]
+    uint32_t* infbm;   // [N][infw]
+    uint32_t* fstack;  // [N][C] freed slots
+    uint32_t* hits;    // [T][N]
+    uint32_t* misses;  // [T][N]
+    uint32_t* slot_out;  // [total items] or null
+    uint32_t* status;
+};
+
+// backward pass: next-use key (g'*B + i') of every access on this node
+__global__ void __launch_bounds__(kRT) k_replay_nextuse(ReplayArgs a) {
+    const uint32_t k = a.k0 + blockIdx.x;
+    uint32_t* last = a.last + size_t(k) * a.D;
+    for (int64_t g = int64_t(a.T) - 1; g >= 0; --g) {
+        const uint32_t* off = a.node_off + size_t(g) * (a.N + 1);
+        const uint32_t o = off[k], L = off[k + 1] - o;
+        const uint64_t base = a.gb[g] + o;
+        for (uint32_t i = threadIdx.x; i < L; i += kRT) {
+            const uint32_t x = a.items[base + i] & ~kHit;
+            const uint32_t v = __ldcg(&last[x]);
+            a.nuk[base + i] = v == kNone ? kNever : v;
+        }
+        __syncthreads();
+        const uint32_t here = uint32_t(g) * a.B;
+        for (uint32_t i = threadIdx.x; i < L; i += kRT) {
+            const uint32_t x = a.items[base + i] & ~kHit;
+            const uint32_t old = atomicExch(&last[x], here + i);
+            if (old != kNone && old / a.B == uint32_t(g)) atomicOr(a.status, 32u);  // repeat in step
+        }
+        __syncthreads();
+    }
+}
+
+struct RShared {
+    uint32_t size, top, inftop, infcnt, fresh, nfree;
+    uint32_t nruns;
+    uint32_t hitcnt;
+    uint32_t wsum[kRT / 32];
+};
+
+__device__ __forceinline__ void r_set_key(const ReplayArgs& a, RShared& sh, uint32_t k, uint32_t x,
+                                          uint32_t nu) {
+    a.key[size_t(k) * a.D + x] = nu;
+    if (nu == kNever) {
+        atomicOr(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
+        atomicAdd(&sh.infcnt, 1u);
+        atomicMax(&sh.inftop, x >> 5);
+    } else {
+        const uint32_t beta = nu / a.B;
+        atomicOr(&a.nz[size_t(k) * a.nzw + (beta >> 5)], 1u << (beta & 31));
+        atomicMax(&sh.top, beta);
+    }
+}
+
+// evict the `need` largest keys of node k (warp 0)
+__device__ void r_evict(const ReplayArgs& a, RShared& sh, uint32_t k, uint32_t need, uint32_t lane) {
+    const uint32_t lt = lanemask_lt_r();
+    uint32_t* keyk = a.key + size_t(k) * a.D;
+    uint32_t* slotk = a.slot + size_t(k) * a.D;
+    uint32_t* fs = a.fstack + size_t(k) * a.C;
+    while (need > 0) {
+        if (sh.infcnt > 0) {
+            uint32_t* bm = a.infbm + size_t(k) * a.infw;
+            int32_t wi = int32_t(sh.inftop);
+            bool found = false;
+            while (wi >= 0 && !found) {
+                const int32_t myw = wi - int32_t(lane);
+                const uint32_t v = myw >= 0 ? __ldcg(&bm[myw]) : 0u;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+                if (bal) {
+                    const uint32_t src = __ffs(bal) - 1;
+                    const int32_t hw = wi - int32_t(src);
+                    uint32_t word = __shfl_sync(0xFFFFFFFFu, v, src);
+                    while (word && need > 0) {
+                        const uint32_t bit = 31 - __clz(word);
+                        word &= ~(1u << bit);
+                        const uint32_t x = uint32_t(hw) * 32 + bit;
+                        if (lane == 0) {
+                            keyk[x] = kNone;
+                            atomicAnd(&bm[hw], ~(1u << bit));
+                            const uint32_t s = slotk[x];
+                            if (s != kNone && a.fstack) { fs[sh.nfree++] = s; slotk[x] = kNone; }
+                            sh.infcnt -= 1;
+                            sh.size -= 1;
+                        }
+                        --need;
+                    }
+                    if (lane == 0) sh.inftop = uint32_t(hw);
+                    found = true;
+                } else {
+                    wi -= 32;
+                }
+                __syncwarp();
+            }
+            if (!found) {
+                if (lane == 0) { atomicOr(a.status, 2u); sh.infcnt = 0; }
+                __syncwarp();
+            }
+            continue;
+        }
+        uint32_t* nzk = a.nz + size_t(k) * a.nzw;
+        int32_t wi = int32_t(sh.top >> 5);
+        int32_t beta = -1;
+        while (wi >= 0) {
+            const int32_t myw = wi - int32_t(lane);
+            const uint32_t v = myw >= 0 ? __ldcg(&nzk[myw]) : 0u;
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+            if (bal) {
+                const uint32_t src = __ffs(bal) - 1;
+                const uint32_t word = __shfl_sync(0xFFFFFFFFu, v, src);
+                beta = (wi - int32_t(src)) * 32 + (31 - __clz(word));
+                break;
+            }
+            wi -= 32;
+        }
+        if (beta < 0) {
+            if (lane == 0) atomicOr(a.status, 4u);
+            return;
+        }
+        const uint32_t* off = a.node_off + size_t(beta) * (a.N + 1);
+        const uint32_t o = off[k], L = off[k + 1] - o;
+        const uint64_t base = a.gb[beta] + o;
+        const uint32_t kb = uint32_t(beta) * a.B;
+        uint32_t c = 0;
+        for (; c < L && need > 0; c += 32) {
+            const uint32_t r = c + lane;  // reverse list order: largest position first
+            bool mem = false;
+            uint32_t x = 0, idx = 0;
+            if (r < L) {
+                idx = L - 1 - r;
+                x = a.items[base + idx] & ~kHit;
+                mem = __ldcg(&keyk[x]) == kb + idx;
+            }
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mem);
+            const uint32_t rank = __popc(bal & lt);
+            const uint32_t took = min(uint32_t(__popc(bal)), need);
+            const bool ev = mem && rank < need;
+            uint32_t s = kNone;
+            if (ev) {
+                keyk[x] = kNone;
+                s = slotk[x];
+                slotk[x] = kNone;
+            }
+            // freed slots pushed in eviction order (deterministic)
+            const bool push = ev && s != kNone && a.fstack;
+            const uint32_t sbal = __ballot_sync(0xFFFFFFFFu, push);
+            const uint32_t nf = sh.nfree;
+            if (push) fs[nf + __popc(sbal & lt)] = s;
+            __syncwarp();
+            need -= took;
+            if (lane == 0) {
+                sh.size -= took;
+                sh.nfree = nf + __popc(sbal);
+            }
+            __syncwarp();
+        }
+        if (c >= L && need > 0 && lane == 0) atomicAnd(&nzk[beta >> 5], ~(1u << (beta & 31)));
+        if (lane == 0) sh.top = uint32_t(beta);
+        __syncwarp();
+    }
+}
+
+// forward replay, one CTA per node
+__global__ void __launch_bounds__(kRT) k_replay(ReplayArgs a) {
+    __shared__ RShared sh;
+    extern __shared__ __align__(16) uint32_t rdyn[];
+    uint32_t* sx = rdyn;                                       // [B] ids | resident bit
+    uint16_t* rstart = reinterpret_cast<uint16_t*>(rdyn + a.B);  // [B+1] run starts
+    const uint32_t k = a.k0 + blockIdx.x;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) {
+        sh.size = 0;
+        sh.top = 0;
+        sh.inftop = 0;
+        sh.infcnt = 0;
+        sh.fresh = 0;
+        sh.nfree = 0;
+    }
+    __syncthreads();
+    uint32_t* keyk = a.key + size_t(k) * a.D;
+    uint32_t* slotk = a.slot + size_t(k) * a.D;
+    uint32_t* fs = a.fstack + size_t(k) * a.C;
+    for (uint32_t g = 0; g < a.T; ++g) {
+        const uint32_t* off = a.node_off + size_t(g) * (a.N + 1);
+        const uint32_t o = off[k], L = off[k + 1] - o;
+        const uint64_t base = a.gb[g] + o;
+        if (L > kRMaxList) {
+            if (tid == 0) atomicOr(a.status, 64u);
+            return;
+        }
+        // load + residency at step start; run boundaries
+        uint32_t hitc = 0;
+        for (uint32_t c = 0; c < L; c += kRT) {
+            const uint32_t i = c + tid;
+            bool res = false, chg = false;
+            if (i < L) {
+                const uint32_t x = a.items[base + i] & ~kHit;
+                res = __ldcg(&keyk[x]) != kNone;
+                sx[i] = x | (res ? kHit : 0u);
+                if (a.slot_out) a.slot_out[base + i] = res ? slotk[x] : kNever;
+                hitc += res;
+            }
+            __syncthreads();
+            if (i < L) chg = i == 0 || ((sx[i] ^ sx[i - 1]) & kHit);
+            // block-wide prefix of chg (run ids), chunk-local then carried
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, chg);
+            if (lane == 0) sh.wsum[w] = __popc(bal);
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t s = c == 0 ? 0u : sh.nruns;
+                for (int q = 0; q < kRT / 32; ++q) { const uint32_t v = sh.wsum[q]; sh.wsum[q] = s; s += v; }
+                sh.nruns = s;
+            }
+            __syncthreads();
+            if (i < L) {
+                const uint32_t rid = sh.wsum[w] + __popc(bal & lanemask_lt_r()) + (chg ? 1u : 0u) - 1u;
+                if (chg) rstart[rid] = uint16_t(i);
+            }
+            __syncthreads();
+        }
+        // hit count
+        for (int s = 16; s > 0; s >>= 1) hitc += __shfl_xor_sync(0xFFFFFFFFu, hitc, s);
+        if (lane == 0) sh.wsum[w] = hitc;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t h = 0;
+            for (int q = 0; q < kRT / 32; ++q) h += sh.wsum[q];
+            a.hits[size_t(g) * a.N + k] = h;
+            a.misses[size_t(g) * a.N + k] = L - h;
+            rstart[sh.nruns] = uint16_t(L);
+        }
+        __syncthreads();
+        const uint32_t nruns = L ? sh.nruns : 0;
+        for (uint32_t r = 0; r < nruns; ++r) {
+            const uint32_t r0 = rstart[r], r1 = rstart[r + 1];
+            const bool hitrun = sx[r0] & kHit;
+            for (uint32_t i = r0 + tid; i < r1; i += kRT)
+                r_set_key(a, sh, k, sx[i] & ~kHit, a.nuk[base + i]);
+            __syncthreads();
+            if (!hitrun) {
+                if (w == 0) {
+                    uint32_t need = 0;
+                    if (lane == 0) {
+                        sh.size += r1 - r0;
+                        need = sh.size > a.C ? sh.size - a.C : 0u;
+                    }
+                    need = __shfl_sync(0xFFFFFFFFu, need, 0);
+                    if (need) r_evict(a, sh, k, need, lane);
+                    __syncwarp();
+                    // survivors of the run take slots, in list order
+                    if (a.slot_out) {
+                        for (uint32_t c = r0; c < r1; c += 32) {
+                            const uint32_t i = c + lane;
+                            bool surv = false;
+                            uint32_t x = 0;
+                            if (i < r1) {
+                                x = sx[i] & ~kHit;
+                                surv = __ldcg(&keyk[x]) != kNone;
+                            }
+                            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, surv);
+                            const uint32_t rank = __popc(bal & lanemask_lt_r());
+                            const uint32_t nf = sh.nfree, fr = sh.fresh;
+                            if (surv) {
+                                uint32_t s;
+                                if (rank < nf) s = fs[nf - 1 - rank];
+                                else s = fr + (rank - nf);
+                                slotk[x] = s;
+                                a.slot_out[base + i] = s;
+                            }
+                            __syncwarp();
+                            if (lane == 0) {
+                                const uint32_t n = __popc(bal);
+                                const uint32_t from_stack = min(n, nf);
+                                sh.nfree = nf - from_stack;
+                                sh.fresh = fr + (n - from_stack);
+                            }
+                            __syncwarp();
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N,
+                    uint64_t D, uint64_t C, uint32_t k0, uint32_t k1, uint32_t* d_hits,
+                    uint32_t* d_misses, uint32_t* d_slot, uint32_t* d_status, cudaStream_t st) {
+    if (k1 <= k0 || T == 0) return kOk;
+    Scratch sc(st);
+    uint64_t* gb = sc.get<uint64_t>(T + 1);
+    if (!gb) return set_error(kInternal, "simulate: scratch allocation failed");
+    k_step_bases<<<1, 1024, 0, st>>>(d_node_off, uint32_t(T), N, gb);
+    LSG_LAUNCH_CHECK("k_step_bases");
+    uint64_t total = 0, B = 0;
+    LSG_CUDA(cudaMemcpyAsync(&total, gb + T, 8, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaStreamSynchronize(st));
+    // B = the step stride of the position keys: max list length over steps
+    // is bounded by the step length, so use the longest step.
+    {
+        // key stride = the longest step (a node list never exceeds its step)
+        uint64_t* hgb = nullptr;
+        LSG_CUDA(cudaMallocHost(&hgb, (T + 1) * 8));
+        LSG_CUDA(cudaMemcpyAsync(hgb, gb, (T + 1) * 8, cudaMemcpyDeviceToHost, st));
+        LSG_CUDA(cudaStreamSynchronize(st));
+        for (uint64_t g = 0; g < T; ++g) B = std::max<uint64_t>(B, hgb[g + 1] - hgb[g]);
+        cudaFreeHost(hgb);
+    }
+    if (B == 0) B = 1;
+    if (T * B >= 0xFFFFFFF0ull) return set_error(kCapability, "simulate: plan too large for 32-bit position keys");
+    if (B > kRMaxList) return set_error(kCapability, "simulate: step longer than 8192 samples");
+    ReplayArgs a{};
+    a.T = uint32_t(T);
+    a.N = N;
+    a.D = uint32_t(D);
+    a.B = uint32_t(B);
+    a.C = uint32_t(std::min<uint64_t>(C, 0xFFFFFFF0ull));
+    a.k0 = k0;
+    a.nzw = uint32_t((T + 31) / 32 + 1);
+    a.infw = uint32_t((D + 31) / 32);
+    a.items = d_items;
+    a.node_off = d_node_off;
+    a.gb = gb;
+    const uint32_t nk = k1 - k0;
+    // per-node state is indexed by absolute node id; allocate N rows
+    a.nuk = sc.get<uint32_t>(total);
+    a.last = sc.get<uint32_t>(size_t(N) * D);
+    a.key = sc.get<uint32_t>(size_t(N) * D);
+    a.slot = sc.get<uint32_t>(size_t(N) * D);
+    a.nz = sc.get<uint32_t>(size_t(N) * a.nzw);
+    a.infbm = sc.get<uint32_t>(size_t(N) * a.infw);
+    a.fstack = d_slot ? sc.get<uint32_t>(size_t(N) * std::min<uint64_t>(C, D)) : nullptr;
+    a.C = uint32_t(std::min<uint64_t>(C, 0xFFFFFFF0ull));
+    if (!a.nuk || !a.last || !a.key || !a.slot || !a.nz || !a.infbm || (d_slot && !a.fstack))
+        return set_error(kInternal, "simulate: scratch allocation failed");
+    LSG_CUDA(cudaMemsetAsync(a.last, 0xFF, size_t(N) * D * 4, st));  // kNone = no later access
+    LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(N) * D * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.slot, 0xFF, size_t(N) * D * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.nz, 0, size_t(N) * a.nzw * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.infbm, 0, size_t(N) * a.infw * 4, st));
+    a.hits = d_hits;
+    a.misses = d_misses;
+    a.slot_out = d_slot;
+    a.status = d_status;
+    k_replay_nextuse<<<nk, kRT, 0, st>>>(a);
+    LSG_LAUNCH_CHECK("k_replay_nextuse");
+    const size_t smem = size_t(B) * 4 + (B + 2) * 2 + 16;
+    LSG_CUDA(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_replay<<<nk, kRT, smem, st>>>(a);
+    LSG_LAUNCH_CHECK("k_replay");
+    return kOk;
+}
+
+}  // namespace lsg

@@ -1,0 +1,379 @@
+"""Python mirror of the reference ``loadsched`` planner API, backed by the
+sm_100a kernels through the C ABI (include/lsg.h).
+
+Names, argument meaning and error classes follow the reference headers
+(/root/reference/proj/include/loadsched/*.hpp, cited per function) so parity
+tests read like the reference's own tests. Tensors live on the current CUDA
+device; uint32 data is carried in int32 tensors (same bits) and uint64 in
+int64 tensors. Every call goes to the CUDA library; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from ._lib import HIT_BIT, NEVER, LsgConfig, LsgError, LsgPlanOut, LsgShape, check, lib
+
+__all__ = [
+    "TraceConfig", "PsoParams", "PipelineConfig", "AccessTrace", "ReuseGraph", "EpochOrder",
+    "PsoResult", "SchedulePlan", "PlanOutput", "SimResult", "generate_trace", "build_reuse_graph",
+    "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "simulate_plan",
+    "store_fill", "gather", "Error", "ConfigError", "ValidationError", "CapabilityError",
+    "StorageError", "InternalError", "HIT_BIT", "NEVER",
+]
+
+
+# --------------------------------------------------------------- errors --
+# errors.hpp:10-46 — one class per ErrorClass, all subclasses of LsgError.
+class Error(LsgError):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class ValidationError(Error):
+    pass
+
+
+class CapabilityError(Error):
+    pass
+
+
+class StorageError(Error):
+    pass
+
+
+class InternalError(Error):
+    pass
+
+
+_BY_CODE = {_lib.CONFIG: ConfigError, _lib.VALIDATION: ValidationError,
+            _lib.CAPABILITY: CapabilityError, _lib.STORAGE: StorageError,
+            _lib.INTERNAL: InternalError}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise _BY_CODE.get(rc, Error)(rc, lib().lsg_last_error().decode())
+
+
+# --------------------------------------------------------------- config --
+@dataclass
+class TraceConfig:
+    """trace.hpp:15-27"""
+
+    dataset_size: int = 0
+    num_epochs: int = 0
+    num_nodes: int = 0
+    local_batch: int = 0
+    seed: int = 0
+    drop_last: bool = True
+
+    def global_batch(self) -> int:
+        return self.num_nodes * self.local_batch
+
+    def steps_per_epoch(self) -> int:  # trace.cpp:12-16
+        B = self.global_batch()
+        if B == 0:
+            return 0
+        return self.dataset_size // B if self.drop_last else -(-self.dataset_size // B)
+
+    def keep(self) -> int:
+        return self.steps_per_epoch() * self.global_batch() if self.drop_last else self.dataset_size
+
+
+@dataclass
+class PsoParams:
+    """epoch_order.hpp:18-29"""
+
+    swarm_size: int = 32
+    max_iters: int = 500
+    p_personal: float = 0.5
+    p_global: float = 0.5
+    inertia: float = 0.5
+    kick: float = 1.0
+    stagnation_limit: int = 100
+    restart_limit: int = 20
+    seed: int = 0
+
+
+@dataclass
+class PipelineConfig:
+    """config.hpp:17-36 (cost-model fields omitted: they never reach the path)."""
+
+    trace: TraceConfig = field(default_factory=TraceConfig)
+    buffer_capacity: int = 0
+    policy: str = "clairvoyant"       # "clairvoyant" | "lru"
+    graph_mode: str = "global"        # "global" | "pernode"
+    chunk_threshold: int = 15
+    chunk_insert_redundant: bool = False
+    pso: PsoParams = field(default_factory=PsoParams)
+    optim_order: bool = True
+    optim_remap: bool = True
+    optim_balance: bool = True
+    optim_chunk: bool = True
+
+    def to_c(self) -> LsgConfig:
+        c = LsgConfig()
+        t = self.trace
+        c.dataset_size, c.num_epochs, c.num_nodes = t.dataset_size, t.num_epochs, t.num_nodes
+        c.local_batch, c.seed, c.drop_last = t.local_batch, t.seed, int(t.drop_last)
+        c.policy = 0 if self.policy == "clairvoyant" else 1
+        c.buffer_capacity = self.buffer_capacity
+        c.graph_mode = 0 if self.graph_mode == "global" else 1
+        c.insert_redundant = int(self.chunk_insert_redundant)
+        c.chunk_threshold = self.chunk_threshold
+        c.optim_order, c.optim_remap = int(self.optim_order), int(self.optim_remap)
+        c.optim_balance, c.optim_chunk = int(self.optim_balance), int(self.optim_chunk)
+        p = self.pso
+        c.pso_swarm, c.pso_iters, c.pso_stagnation, c.pso_restart = (
+            p.swarm_size, p.max_iters, p.stagnation_limit, p.restart_limit)
+        c.pso_p_personal, c.pso_p_global, c.pso_inertia, c.pso_kick = (
+            p.p_personal, p.p_global, p.inertia, p.kick)
+        return c
+
+    def shape(self) -> LsgShape:
+        sh = LsgShape()
+        c = self.to_c()
+        _check(lib().lsg_shape_of(ctypes.byref(c), ctypes.byref(sh)))
+        return sh
+
+    def validate(self) -> None:  # config.cpp:11-22
+        self.shape()
+
+
+# ---------------------------------------------------------------- types --
+@dataclass
+class AccessTrace:
+    """trace.hpp:33-38; epochs: int32 [E, keep] on device (uint32 ids)."""
+
+    config: TraceConfig
+    epochs: torch.Tensor
+
+
+@dataclass
+class ReuseGraph:
+    """reuse_graph.hpp:23-35; weights: int64 [E, E] on device."""
+
+    num_epochs: int
+    buffer_size: int
+    mode: str
+    weights: torch.Tensor
+
+
+@dataclass
+class EpochOrder:
+    order: torch.Tensor  # int32 [E]
+    cost: int
+
+
+@dataclass
+class PsoResult:
+    """epoch_order.hpp:39-43"""
+
+    best: EpochOrder
+    history: torch.Tensor  # int64 [iterations]
+    iterations: int
+
+
+@dataclass
+class SchedulePlan:
+    """plan.hpp:33-53 in flat device layout: steps in execution order; step g's
+    node k list is items[base_g + node_off[g,k] : base_g + node_off[g,k+1]]
+    with base_g = sum of earlier steps' lengths; bit 31 of an item = hit tag."""
+
+    dataset_size: int
+    num_nodes: int
+    local_batch: int
+    steps_per_epoch: int
+    order: EpochOrder
+    items: torch.Tensor         # int32 [E*keep]
+    node_off: torch.Tensor      # int32 [T, N+1]
+    fetches_before: torch.Tensor  # int32 [T, N]
+    fetches_after: torch.Tensor   # int32 [T, N]
+
+
+@dataclass
+class PlanOutput:
+    """pipeline.hpp:17-22"""
+
+    trace: AccessTrace
+    graph: ReuseGraph
+    pso: PsoResult | None
+    plan: SchedulePlan
+
+
+@dataclass
+class SimResult:
+    """buffer.hpp:106-111; rows as [T, N] tensors (execution order, nodes ascending)."""
+
+    hits: torch.Tensor
+    misses: torch.Tensor
+    total_hits: int
+    total_misses: int
+    slots: torch.Tensor | None = None
+
+
+def _stream() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _dev() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2211_00224_b200 requires a CUDA (sm_100a) device")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+# ------------------------------------------------------------- functions --
+def generate_trace(config: TraceConfig) -> AccessTrace:
+    """trace.hpp:40 / trace.cpp:26-43 — K1 on device."""
+    pc = PipelineConfig(trace=config, buffer_capacity=1)
+    c = pc.to_c()
+    keep = config.keep() if config.global_batch() else 0
+    out = torch.empty((max(config.num_epochs, 1), max(keep, 1)), dtype=torch.int32, device=_dev())
+    _check(lib().lsg_generate_trace(ctypes.byref(c), _ptr(out), _stream()))
+    return AccessTrace(config, out[: config.num_epochs, :keep])
+
+
+def build_reuse_graph(trace: AccessTrace, buffer_size: int, mode: str = "global") -> ReuseGraph:
+    """reuse_graph.hpp:53 / reuse_graph.cpp:77-101 — K2+K3 on device. The trace
+    may repeat ids (read_trace admits it)."""
+    ep = trace.epochs.contiguous()
+    E, L = ep.shape
+    w = torch.empty((max(E, 1), max(E, 1)), dtype=torch.int64, device=ep.device)
+    cfg = trace.config
+    _check(lib().lsg_build_reuse_graph(_ptr(ep), E, L, cfg.dataset_size, cfg.num_nodes,
+                                       cfg.local_batch, int(cfg.drop_last), buffer_size,
+                                       0 if mode == "global" else 1, _ptr(w), _stream()))
+    return ReuseGraph(E, buffer_size, mode, w[:E, :E])
+
+
+def pso_order(graph: ReuseGraph, params: PsoParams) -> PsoResult:
+    """epoch_order.hpp:60 / epoch_order.cpp:121-221 — K4, bit-exact."""
+    E = graph.num_epochs
+    dev = graph.weights.device
+    order = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    cost = torch.empty(1, dtype=torch.int64, device=dev)
+    hist = torch.empty(max(params.max_iters, 1), dtype=torch.int64, device=dev)
+    iters = torch.empty(1, dtype=torch.int32, device=dev)
+    w = graph.weights.contiguous()
+    _check(lib().lsg_pso_order(_ptr(w), E, params.swarm_size, params.max_iters, params.p_personal,
+                               params.p_global, params.inertia, params.kick,
+                               params.stagnation_limit, params.restart_limit, params.seed,
+                               _ptr(order), _ptr(cost), _ptr(hist), _ptr(iters), _stream()))
+    n = int(iters.item())
+    return PsoResult(EpochOrder(order[:E], int(cost.item())), hist[:n], n)
+
+
+def identity_order(graph: ReuseGraph) -> EpochOrder:
+    """epoch_order.hpp:63"""
+    E = graph.num_epochs
+    if E == 0:
+        raise ValidationError(_lib.VALIDATION, "identity_order: empty graph")
+    idx = torch.arange(E, device=graph.weights.device)
+    cost = int(graph.weights[idx[:-1], idx[1:]].sum().item()) if E > 1 else 0
+    return EpochOrder(idx.to(torch.int32), cost)
+
+
+def _plan_buffers(config: PipelineConfig, dev):
+    sh = config.shape()
+    E, N, T = config.trace.num_epochs, config.trace.num_nodes, int(sh.total_steps)
+    mk = lambda n, dt: torch.empty(max(int(n), 1), dtype=dt, device=dev)  # noqa: E731
+    bufs = dict(trace=mk(sh.total_items, torch.int32), graph=mk(E * E, torch.int64),
+                order=mk(E, torch.int32), cost=mk(1, torch.int64),
+                hist=mk(config.pso.max_iters, torch.int64), iters=mk(1, torch.int32),
+                items=mk(sh.total_items, torch.int32), node_off=mk(T * (N + 1), torch.int32),
+                fetch_before=mk(T * N, torch.int32), fetch_after=mk(T * N, torch.int32))
+    return sh, bufs
+
+
+def _wrap_plan(config: PipelineConfig, sh, b) -> PlanOutput:
+    t = config.trace
+    E, N, T, keep = t.num_epochs, t.num_nodes, int(sh.total_steps), int(sh.keep)
+    trace = AccessTrace(t, b["trace"][: E * keep].view(E, keep))
+    graph = ReuseGraph(E, config.buffer_capacity, config.graph_mode, b["graph"][: E * E].view(E, E))
+    order = EpochOrder(b["order"][:E], int(b["cost"][0]))
+    pso = None
+    if config.optim_order:
+        n = int(b["iters"][0])
+        pso = PsoResult(order, b["hist"][:n], n)
+    plan = SchedulePlan(t.dataset_size, N, t.local_batch, int(sh.steps_per_epoch), order,
+                        b["items"][: E * keep], b["node_off"][: T * (N + 1)].view(T, N + 1),
+                        b["fetch_before"][: T * N].view(T, N), b["fetch_after"][: T * N].view(T, N))
+    return PlanOutput(trace, graph, pso, plan)
+
+
+def plan_schedule(config: PipelineConfig) -> PlanOutput:
+    """pipeline.hpp:27 / pipeline.cpp:32-120 — K1..K6 on device, outputs in HBM."""
+    sh, b = _plan_buffers(config, _dev())
+    out = LsgPlanOut(**{k: v.data_ptr() for k, v in b.items()})
+    c = config.to_c()
+    _check(lib().lsg_plan(ctypes.byref(c), ctypes.byref(out), _stream()))
+    return _wrap_plan(config, sh, b)
+
+
+def plan_schedule_host(config: PipelineConfig, pinned: bool = True) -> PlanOutput:
+    """plan_schedule with host outputs through lsg_plan_host (the e2e path):
+    device work plus the device->host copies of the whole plan."""
+    _dev()
+    sh = config.shape()
+    E, N, T = config.trace.num_epochs, config.trace.num_nodes, int(sh.total_steps)
+    mk = lambda n, dt: torch.empty(max(int(n), 1), dtype=dt, pin_memory=pinned)  # noqa: E731
+    b = dict(trace=mk(sh.total_items, torch.int32), graph=mk(E * E, torch.int64),
+             order=mk(E, torch.int32), cost=mk(1, torch.int64),
+             hist=mk(config.pso.max_iters, torch.int64), iters=mk(1, torch.int32),
+             items=mk(sh.total_items, torch.int32), node_off=mk(T * (N + 1), torch.int32),
+             fetch_before=mk(T * N, torch.int32), fetch_after=mk(T * N, torch.int32))
+    out = LsgPlanOut(**{k: v.data_ptr() for k, v in b.items()})
+    c = config.to_c()
+    _check(lib().lsg_plan_host(ctypes.byref(c), ctypes.byref(out), _stream()))
+    return _wrap_plan(config, sh, b)
+
+
+def simulate_plan(plan: SchedulePlan, capacity: int, policy: str = "clairvoyant",
+                  node_range: tuple[int, int] | None = None, want_slots: bool = False) -> SimResult:
+    """buffer.hpp:117-118 / buffer.cpp:183-247 — K7 per-rank replay. node_range
+    restricts the replay to ranks [k0, k1) (multi-GPU sharding)."""
+    N = plan.num_nodes
+    T = plan.node_off.shape[0]
+    k0, k1 = node_range if node_range is not None else (0, N)
+    dev = plan.items.device
+    hits = torch.zeros((T, N), dtype=torch.int32, device=dev)
+    misses = torch.zeros((T, N), dtype=torch.int32, device=dev)
+    slots = torch.empty(max(plan.items.numel(), 1), dtype=torch.int32, device=dev) if want_slots else None
+    _check(lib().lsg_simulate(_ptr(plan.items.contiguous()), _ptr(plan.node_off.contiguous()), T, N,
+                              plan.dataset_size, capacity, 0 if policy == "clairvoyant" else 1,
+                              k0, k1, _ptr(hits), _ptr(misses), _ptr(slots), _stream()))
+    return SimResult(hits, misses, int(hits.sum().item()), int(misses.sum().item()),
+                     slots[: plan.items.numel()] if slots is not None else None)
+
+
+def store_fill(ids: torch.Tensor, sample_bytes: int, fill_seed: int,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """K9: rows = Store::read_one(ids[r]) payload (store.cpp:70-80)."""
+    ids = ids.to(torch.int32).contiguous()
+    n = ids.numel()
+    if out is None:
+        out = torch.empty((n, sample_bytes), dtype=torch.uint8, device=ids.device)
+    _check(lib().lsg_store_fill(_ptr(ids), n, sample_bytes, fill_seed, _ptr(out), _stream()))
+    return out
+
+
+def gather(buf: torch.Tensor, slots: torch.Tensor, sample_bytes: int,
+           out: torch.Tensor | None = None) -> torch.Tensor:
+    """K8: out row r = buf row slots[r] (the HBM-buffer batch fetch)."""
+    slots = slots.to(torch.int32).contiguous()
+    n = slots.numel()
+    if out is None:
+        out = torch.empty((n, sample_bytes), dtype=torch.uint8, device=buf.device)
+    _check(lib().lsg_gather(_ptr(buf), _ptr(slots), n, sample_bytes, _ptr(out), _stream()))
+    return out
