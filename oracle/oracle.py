@@ -89,6 +89,8 @@ class Cfg:
 
     @property
     def steps(self) -> int:
+        if self.B == 0:
+            return 0
         return self.dataset_size // self.B if self.drop_last else -(-self.dataset_size // self.B)
 
     @property

@@ -3,6 +3,7 @@
 // TraceConfig::validate (trace.cpp:18-24), PipelineConfig::validate
 // (config.cpp:11-22), pso_order's guards (epoch_order.cpp:123-128).
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -64,6 +65,29 @@ int cuda_error(cudaError_t e, const char* where) {
     return kInternal;
 }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void keep_pool() {
+    static std::atomic<uint64_t> done_mask{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return;
+    const uint64_t bit = 1ull << dev;
+    if (done_mask.load() & bit) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_mask.fetch_or(bit);
+}
+
+bool profiling() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("LSG_PROFILE");
+        on = (e && e[0] && e[0] != '0') ? 1 : 0;
+    }
+    return on == 1;
+}
 
 static int validate(const lsg_config* c, lsg_shape* sh) {
     if (!c) return set_error(kValidation, "null config");

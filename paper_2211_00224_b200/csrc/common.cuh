@@ -40,6 +40,8 @@ enum Err : int { kOk = 0, kConfig = 2, kValidation = 3, kCapability = 4, kStorag
 int set_error(int code, const std::string& msg);
 int cuda_error(cudaError_t e, const char* where);
 void count_launch();
+void keep_pool();  // stream-ordered pool keeps its memory between calls
+bool profiling();  // LSG_PROFILE=1: per-phase cycle counters to stderr
 
 #define LSG_CUDA(call)                                          \
     do {                                                        \
@@ -59,7 +61,7 @@ struct Scratch {
     cudaStream_t s;
     void* ptrs[64];
     int n = 0;
-    explicit Scratch(cudaStream_t st) : s(st) {}
+    explicit Scratch(cudaStream_t st) : s(st) { keep_pool(); }
     template <typename T>
     T* get(size_t count) {
         void* p = nullptr;

@@ -34,17 +34,21 @@
 //     descending id order testing key == g' (the reference's tie rule: equal
 //     keys evict the larger id first). kNeverUsed keys live in an exact
 //     per-node id bitmap scanned from the top.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace lsg {
 
 namespace {
 
-constexpr int kThreads = 1024;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kMaxN = 32;
 constexpr uint32_t kMaxB = 8192;
 constexpr uint32_t kFetch = 0xFFFFFFFFu;
+constexpr uint32_t kWinWords = 40;  // I1 bucket-bit window (covers 2S <= 1216 steps)
 
 // ----------------------------------------------------------------- K5 ----
 // nu for the access of x at execution epoch i, position pos: the first
@@ -109,7 +113,8 @@ struct LoopArgs {
     uint32_t* hm;                    // [D] holder masks
     uint32_t* nz;                    // [N][nzw]
     uint32_t* infbm;                 // [N][infw]
-    uint32_t* smul;                  // [B][N] scratch
+    uint32_t* smul;                  // [B][N] scratch: warp-local S_k(j)
+    uint32_t* sx;                    // [B][N] scratch: exact S_k(j) by multi index
     uint32_t* mpos;                  // [N][b] scratch
     uint32_t* mres;                  // [B] scratch
     uint32_t* mv;                    // [B] scratch: moves (d | r<<8 | q<<16)
@@ -119,6 +124,8 @@ struct LoopArgs {
     uint32_t* fb;                    // [T][N] output (may be null)
     uint32_t* fa;                    // [T][N] output (may be null)
     uint32_t* status;
+    unsigned long long* prof;        // [8] per-phase cycles (LSG_PROFILE) or null
+    int dbg_skip;                    // timing experiments only (LSG_DEBUG_SKIP)
 };
 
 struct Shared {
@@ -149,6 +156,11 @@ struct Small {
     uint32_t inftop[kMaxN];         // never-used bitmap upper word bound
     uint32_t infcnt[kMaxN];         // never-used residents
     uint32_t nmulti, nfetch, nmoves;
+    alignas(16) uint32_t stg[2][32][kMaxN];  // D: staged S_k(j) of 32 multi items
+    uint32_t pthr[32][32];          // D: per (item, node) candidate threshold
+    uint32_t pkb[32][32];           // D: per (item, node) base key
+    uint32_t win_base;              // I1: first bucket word of the window
+    uint32_t win[kMaxN][kWinWords]; // I1: bucket bits aggregated per step
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -244,20 +256,28 @@ __device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t ne
         const uint32_t* cand = a.sb + size_t(gi) * a.keep + lo;
         const uint32_t* keyk = a.key + size_t(k) * a.D;
         uint32_t c = 0;
-        for (; c < blen && need > 0; c += 32) {
-            const uint32_t r = c + lane;
-            uint32_t x = 0;
-            bool mem = false;
-            if (r < blen) {
-                x = cand[r];
-                mem = __ldcg(&keyk[x]) == uint32_t(beta);
+        for (; c < blen && need > 0; c += 128) {
+            uint32_t xs[4];
+            bool mem[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t r = c + 32 * u + lane;
+                xs[u] = r < blen ? cand[r] : 0u;
             }
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mem);
-            const uint32_t rank = __popc(bal & lt);
-            if (mem && rank < need) drop(a, k, x);
-            const uint32_t took = min(uint32_t(__popc(bal)), need);
-            need -= took;
-            if (lane == 0) sm.bsize[k] -= took;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t r = c + 32 * u + lane;
+                mem[u] = r < blen && __ldcg(&keyk[xs[u]]) == uint32_t(beta);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mem[u]);
+                const uint32_t rank = __popc(bal & lt);
+                if (mem[u] && rank < need) drop(a, k, xs[u]);
+                const uint32_t took = min(uint32_t(__popc(bal)), need);
+                need -= took;
+                if (lane == 0) sm.bsize[k] -= took;
+            }
         }
         __syncwarp();
         if (c >= blen && need > 0) {
@@ -290,6 +310,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
     }
     __syncthreads();
     size_t gbase = 0;
+    unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tprev = clock64();
+#define LSG_PHASE(n)                                              \
+    if (a.prof && tid == 0) {                                     \
+        const unsigned long long tnow = clock64();                \
+        pacc[n] += tnow - tprev;                                  \
+        tprev = tnow;                                             \
+    }
     for (uint32_t g = 0; g < a.T; ++g) {
         const uint32_t i = g / a.S, t = g % a.S;
         const uint32_t lo = t * a.B, len = min(a.B, a.keep - lo);
@@ -301,20 +329,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         // ---------------- A: load + classify + per-warp single ranks
         if (lane < kMaxN) sm.wcnt[w][lane] = 0;
         uint32_t wm = 0;
+        // all of the warp's global loads first (coalesced ids/keys, then the
+        // independent random holder-mask loads), so they overlap in flight
+#pragma unroll 4
+        for (uint32_t j = j0 + lane; j < j1; j += 32) {
+            s.sx[j] = row[j];
+            s.snu[j] = nurow[j];
+        }
         __syncwarp();
-        for (uint32_t c = j0; c < j0 + R; c += 32) {
+#pragma unroll 4
+        for (uint32_t j = j0 + lane; j < j1; j += 32) s.smask[j] = __ldcg(&a.hm[s.sx[j]]);
+        __syncwarp();
+        for (uint32_t c = j0; c < j0 + R && a.remap; c += 32) {
             const uint32_t j = c + lane;
             const bool valid = j < j1;
-            uint32_t x = 0, nu = 0, m = 0;
-            if (valid) {
-                x = row[j];
-                nu = nurow[j];
-                m = __ldcg(&a.hm[x]);
-                s.sx[j] = x;
-                s.snu[j] = nu;
-                s.smask[j] = m;
-            }
-            if (!a.remap) continue;
+            const uint32_t m = valid ? s.smask[j] : 0u;
             const uint32_t hc = __popc(m);
             const bool single = valid && hc == 1, multi = valid && hc >= 2;
             const uint32_t h = single ? __ffs(m) - 1 : 0;
@@ -341,29 +370,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         }
         if (lane == 0) sm.wmul[w] = wm;
         __syncthreads();
+        LSG_PHASE(0)
 
         if (a.remap) {
             // ------------ B: scans over warps (warp k: node k; warp 31: multi)
-            if (w < N) {
-                const uint32_t v = sm.wcnt[lane][w];
+            for (uint32_t k = w; k < N; k += kWarps) {
+                const uint32_t v = lane < uint32_t(kWarps) ? sm.wcnt[lane][k] : 0u;
                 uint32_t inc = v;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
                     const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
                     if (lane >= uint32_t(d)) inc += o;
                 }
-                sm.wcnt[lane][w] = inc - v;
-                if (lane == 31) sm.tot[w] = inc;
+                if (lane < uint32_t(kWarps)) sm.wcnt[lane][k] = inc - v;
+                if (lane == 31) sm.tot[k] = inc;
             }
             if (w == kWarps - 1) {
-                const uint32_t v = sm.wmul[lane];
+                const uint32_t v = lane < uint32_t(kWarps) ? sm.wmul[lane] : 0u;
                 uint32_t inc = v;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
                     const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
                     if (lane >= uint32_t(d)) inc += o;
                 }
-                sm.wmul[lane] = inc - v;
+                if (lane < uint32_t(kWarps)) sm.wmul[lane] = inc - v;
                 if (lane == 31) sm.nmulti = inc;
             }
             __syncthreads();
@@ -377,42 +407,103 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     const uint32_t mi = sm.wmul[w] + s.sinfo[j];
                     s.sinfo[j] = mi;
                     s.pre[mi] = j;  // multi list (pre is free until F)
-                    uint32_t mm = m;
-                    while (mm) {
-                        const uint32_t k = __ffs(mm) - 1;
-                        mm &= mm - 1;
-                        a.smul[size_t(j) * N + k] += sm.wcnt[w][k];
-                    }
+                    // exact S_k(j) (warp-local part from A + warp base), b for
+                    // non-holders, compact by multi index for D's staging
+                    for (uint32_t k = 0; k < N; ++k)
+                        a.sx[size_t(mi) * N + k] =
+                            ((m >> k) & 1u) ? min(b, a.smul[size_t(j) * N + k] + sm.wcnt[w][k]) : b;
                 }
             }
             __syncthreads();
+            LSG_PHASE(1)
             // ------------ D: serial multi-holder pass, lanes = nodes
-            if (w == 0) {
-                uint32_t M = 0;
+            if (w == 0 && (a.dbg_skip & 1)) {  // timing experiment: every multi item fetches
+                for (uint32_t mi = lane; mi < sm.nmulti; mi += 32) s.sinfo[s.pre[mi]] = 0xFFFFFFFFu;
+                if (lane < N) sm.mtot[lane] = 0;
+            }
+            for (int drep = 0; drep < ((a.dbg_skip & 2) ? 2 : 1); ++drep)  // timing: D is idempotent
+            if (w == 0 && !(a.dbg_skip & 1)) {
+                // The warp-local part of S_k(j) for 32 multi items at a time is
+                // staged global->smem with cp.async one chunk ahead. A
+                // lane-parallel pass then packs the exact S_k(j) of the chunk
+                // (plus the phase-B warp base; S = b when k is no holder) into
+                // 16 registers per lane, so the fully unrolled serial loop
+                // touches no memory at all (shared stores inside it serialize
+                // with REDUX in the MIO pipe):
+                //   key = ((S + M) << 5) | k, candidate iff M < b - S,
+                // lane k holding Msh = M_k << 5. Results stay in registers
+                // (lane u keeps item u's decision); list positions are rebuilt
+                // after the chunk with __match_any_sync (a node's items of one
+                // chunk take consecutive positions in item order).
+                uint32_t Msh = 0;
                 const uint32_t nm = sm.nmulti;
-                uint32_t jn = nm ? s.pre[0] : 0;
-                uint32_t mkn = nm ? s.smask[jn] : 0;
-                uint32_t sn = (nm && lane < N) ? a.smul[size_t(jn) * N + lane] : 0;
-                for (uint32_t mi = 0; mi < nm; ++mi) {
-                    const uint32_t j = jn, mk = mkn, sk = sn;
-                    if (mi + 1 < nm) {  // prefetch the next item
-                        jn = s.pre[mi + 1];
-                        mkn = s.smask[jn];
-                        sn = lane < N ? a.smul[size_t(jn) * N + lane] : 0;
+                // stage the chunk's exact S rows (contiguous 32*N words) with
+                // 16-byte cp.async, one chunk ahead
+                auto stage = [&](uint32_t base, uint32_t buf) {
+                    const uint32_t cnt = min(32u, nm - base);
+                    const uint32_t words = cnt * N;  // N <= 32, rows of N words
+                    const uint32_t* src = a.sx + size_t(base) * N;
+                    uint32_t* dstw = &sm.stg[buf][0][0];
+                    for (uint32_t q = lane * 4; q < words; q += 128) {
+                        const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(dstw + q));
+                        if (q + 4 <= words && ((reinterpret_cast<uintptr_t>(src + q) & 15) == 0)) {
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src + q));
+                        } else {
+                            for (uint32_t r = q; r < min(q + 4, words); ++r) {
+                                const unsigned d1 = static_cast<unsigned>(__cvta_generic_to_shared(dstw + r));
+                                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d1), "l"(src + r));
+                            }
+                        }
                     }
-                    const bool in = lane < N && ((mk >> lane) & 1u);
-                    const uint32_t cnt = min(b, sk + M);
-                    const uint32_t keyv = (in && cnt < b) ? ((cnt << 5) | lane) : 0xFFFFFFFFu;
-                    const uint32_t best = __reduce_min_sync(0xFFFFFFFFu, keyv);
-                    if (best != 0xFFFFFFFFu && lane == (best & 31)) {
-                        a.mpos[size_t(lane) * b + M] = j;
-                        ++M;
+                    asm volatile("cp.async.commit_group;\n" ::);
+                };
+                if (nm) stage(0, 0);
+                for (uint32_t base = 0, buf = 0; base < nm; base += 32, buf ^= 1) {
+                    if (base + 32 < nm) {
+                        stage(base + 32, buf ^ 1);
+                        asm volatile("cp.async.wait_group 1;\n" ::);
+                    } else {
+                        asm volatile("cp.async.wait_group 0;\n" ::);
                     }
-                    if (lane == 0) a.mres[mi] = best;
+                    __syncwarp();
+                    const uint32_t cnt = min(32u, nm - base);
+                    const uint32_t myj = lane < cnt ? s.pre[base + lane] : 0u;
+                    const uint32_t* stw = &sm.stg[buf][0][0];  // row u at stw[u * N]
+                    uint32_t P[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        const uint32_t u0 = 2 * q, u1 = 2 * q + 1;
+                        const uint32_t s0 = (u0 < cnt && lane < N) ? stw[u0 * N + lane] : b;
+                        const uint32_t s1 = (u1 < cnt && lane < N) ? stw[u1 * N + lane] : b;
+                        P[q] = s0 | (s1 << 16);
+                    }
+                    const uint32_t Mstart = Msh >> 5;
+                    uint32_t myres = 0xFFFFFFFFu;
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        if (uint32_t(u) < cnt) {
+                            const uint32_t S = (P[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+                            const uint32_t thr = (b - S) << 5, kb = (S << 5) | lane;
+                            const uint32_t keyv = Msh < thr ? kb + Msh : 0xFFFFFFFFu;
+                            const uint32_t best = __reduce_min_sync(0xFFFFFFFFu, keyv);
+                            Msh += (keyv == best && best != 0xFFFFFFFFu) ? 32u : 0u;
+                            myres = lane == uint32_t(u) ? best : myres;
+                        }
+                    }
+                    // lane u: item u's decision -> node list position + E's input
+                    const bool chose = lane < cnt && myres != 0xFFFFFFFFu;
+                    const uint32_t kk = myres & 31;
+                    const uint32_t grp = __match_any_sync(0xFFFFFFFFu, chose ? kk : 0x100u + lane);
+                    const uint32_t m0 = __shfl_sync(0xFFFFFFFFu, Mstart, kk);
+                    if (chose) s.fin[kk * b + m0 + __popc(grp & lt)] = myj;
+                    if (lane < cnt) s.sinfo[myj] = myres;  // consumed by E
+                    __syncwarp();
                 }
-                if (lane < N) sm.mtot[lane] = M;
+                if (a.prof && lane == 0) atomicAdd(&a.prof[8], (unsigned long long)nm);
+                if (lane < N) sm.mtot[lane] = Msh >> 5;
             }
             __syncthreads();
+            LSG_PHASE(2)
             // ------------ E: hits/positions for singles; fetch ranks
             uint32_t wf = 0;
             for (uint32_t c = j0; c < j0 + R; c += 32) {
@@ -426,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                         const uint32_t h = __ffs(m) - 1;
                         const uint32_t S = s.sinfo[j];
                         // M_h(<j): multi items before j assigned to h
-                        const uint32_t* mp = a.mpos + size_t(h) * b;
+                        const uint32_t* mp = s.fin + h * b;
                         uint32_t lo2 = 0, hi2 = sm.mtot[h];
                         while (lo2 < hi2) {
                             const uint32_t mid = (lo2 + hi2) >> 1;
@@ -436,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                         if (pos < b) s.sinfo[j] = (h << 24) | pos;
                         else fetch = true;
                     } else if (hc >= 2) {
-                        const uint32_t r = a.mres[s.sinfo[j]];
+                        const uint32_t r = s.sinfo[j];
                         if (r != 0xFFFFFFFFu) s.sinfo[j] = ((r & 31) << 24) | (r >> 5);
                         else fetch = true;
                     } else {
@@ -451,14 +542,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
             if (tid < N) sm.size[tid] = min(b, sm.tot[tid] + sm.mtot[tid]);
             __syncthreads();
             if (w == 0) {
-                const uint32_t v = sm.wfet[lane];
+                const uint32_t v = lane < uint32_t(kWarps) ? sm.wfet[lane] : 0u;
                 uint32_t inc = v;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
                     const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
                     if (lane >= uint32_t(d)) inc += o;
                 }
-                sm.wfet[lane] = inc - v;
+                if (lane < uint32_t(kWarps)) sm.wfet[lane] = inc - v;
                 const uint32_t F = __shfl_sync(0xFFFFFFFFu, inc, 31);
                 // free-capacity prefix over nodes (ascending fill, locality.cpp:33-39)
                 const uint32_t fr = lane < N ? b - sm.size[lane] : 0;
@@ -516,6 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         }
         __syncthreads();
 
+        LSG_PHASE(3)
         // ---------------- G: balance on counts (balance.cpp:10-39)
         if (tid < N) {
             sm.outk[tid] = 0;
@@ -551,13 +643,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
             for (uint32_t k = 0; k < N; ++k) {
                 const uint32_t out = sm.outk[k];
                 if (!out) continue;
-                const uint32_t L = sm.lenk[k];
-                for (uint32_t p = tid; p < L; p += kThreads) {
+                // remap lists are [hits][fetches]: fetches start at size[k]
+                // (slice lists are mixed; size[k] = 0 there)
+                const uint32_t L = sm.lenk[k], f0 = sm.size[k];
+                for (uint32_t p = f0 + tid; p < L; p += kThreads) {
                     const uint32_t e = s.pre[k * b + p];
                     if (e & kHit) continue;
                     const uint32_t x = s.sx[e & 0xFFFF];
                     uint32_t rank = 0;
-                    for (uint32_t p2 = 0; p2 < L; ++p2) {
+                    for (uint32_t p2 = f0; p2 < L; ++p2) {
                         const uint32_t e2 = s.pre[k * b + p2];
                         if (!(e2 & kHit) && s.sx[e2 & 0xFFFF] > x) ++rank;
                     }
@@ -566,6 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
             }
             __syncthreads();
         }
+        LSG_PHASE(4)
         // ---------------- H: final lists + outputs
         if (w == 0) {
             const uint32_t L = lane < N ? sm.lenk[lane] - sm.outk[lane] + sm.ink[lane] : 0;
@@ -606,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                         // rank among moved = number of moved ids larger than this one
                         const uint32_t x = s.sx[e & 0xFFFF];
                         uint32_t rank = 0;
-                        for (uint32_t p2 = 0; p2 < L; ++p2) {
+                        for (uint32_t p2 = sm.size[k]; p2 < L; ++p2) {
                             const uint32_t e2 = s.pre[k * b + p2];
                             if (!(e2 & kHit) && s.sx[e2 & 0xFFFF] > x) ++rank;
                         }
@@ -625,16 +720,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         }
         __syncthreads();
 
+        LSG_PHASE(5)
         // ---------------- I: buffer advance, nodes in parallel
         if (a.remap) {  // tagged hits form each list's prefix: one re-key run
+            // their new keys fall in (g, g+2S): aggregate the bucket bits in a
+            // shared window, then flush one atomic per non-empty word
+            const uint32_t wbase = (g + 1) >> 5;
+            for (uint32_t q = tid; q < N * kWinWords; q += kThreads) sm.win[q / kWinWords][q % kWinWords] = 0;
+            __syncthreads();
             for (uint32_t p = tid; p < len; p += kThreads) {
                 const uint32_t e = s.fin[p];
                 if (!(e & kHit)) continue;
                 const uint32_t j = e & 0xFFFF, k = (e >> 16) & 0xFF;
-                set_key(a, sm, k, s.sx[j], s.snu[j]);
+                const uint32_t x = s.sx[j], nu = s.snu[j];
+                const uint32_t wd = nu >> 5;
+                if (nu != kNever && wd >= wbase && wd - wbase < kWinWords) {
+                    a.key[size_t(k) * a.D + x] = nu;
+                    atomicOr(&sm.win[k][wd - wbase], 1u << (nu & 31));
+                } else {
+                    set_key(a, sm, k, x, nu);
+                }
+            }
+            __syncthreads();
+            for (uint32_t q = tid; q < N * kWinWords; q += kThreads) {
+                const uint32_t k = q / kWinWords, wd = q % kWinWords;
+                const uint32_t v = sm.win[k][wd];
+                if (v) {
+                    atomicOr(&a.nz[size_t(k) * a.nzw + wbase + wd], v);
+                    atomicMax(&sm.top[k], (wbase + wd) * 32 + 31 - __clz(v));
+                }
             }
             __syncthreads();
         }
+        LSG_PHASE(6)
         for (uint32_t k = w; k < N; k += kWarps) {
             const uint32_t begin = sm.noff[k] + (a.remap ? sm.size[k] : 0u), end = sm.noff[k + 1];
             for (uint32_t c = begin; c < end; c += 32) {
@@ -682,8 +800,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
             }
         }
         __syncthreads();
+        LSG_PHASE(7)
         gbase += len;
     }
+#undef LSG_PHASE
+    if (a.prof && tid == 0)
+        for (int q = 0; q < 8; ++q) a.prof[q] = pacc[q];
 }
 
 }  // namespace
@@ -721,11 +843,12 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.nz = sc.get<uint32_t>(size_t(dm.N) * a.nzw);
     a.infbm = sc.get<uint32_t>(size_t(dm.N) * a.infw);
     a.smul = sc.get<uint32_t>(size_t(dm.B) * dm.N);
+    a.sx = sc.get<uint32_t>(size_t(dm.B) * dm.N);
     a.mpos = sc.get<uint32_t>(size_t(dm.N) * dm.b);
     a.mres = sc.get<uint32_t>(dm.B);
     a.mv = sc.get<uint32_t>(dm.B);
     a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B);
-    if (!nu || !sb || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.mpos || !a.mres ||
+    if (!nu || !sb || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.mpos || !a.mres ||
         !a.mv || !a.dmoves)
         return set_error(kInternal, "plan: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(dm.N) * dm.D * 4, st));
@@ -751,10 +874,30 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.fb = d_fb;
     a.fa = d_fa;
     a.status = d_status;
+    a.prof = profiling() ? sc.get<unsigned long long>(16 + 256) : nullptr;
+    a.dbg_skip = std::getenv("LSG_DEBUG_SKIP") ? std::atoi(std::getenv("LSG_DEBUG_SKIP")) : 0;
+    if (a.prof) LSG_CUDA(cudaMemsetAsync(a.prof, 0, (16 + 256) * 8, st));
     const size_t smem = size_t(6) * dm.B * 4;
     LSG_CUDA(cudaFuncSetAttribute(k_plan_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k_plan_loop<<<1, kThreads, smem, st>>>(a);
     LSG_LAUNCH_CHECK("k_plan_loop");
+    if (a.prof) {
+        unsigned long long h[16 + 256];
+        LSG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof h, cudaMemcpyDeviceToHost, st));
+        LSG_CUDA(cudaStreamSynchronize(st));
+        const char* names[8] = {"A load/classify", "B/C ranks", "D multi pass", "E/F fetch fill",
+                                "G balance", "H lists", "I1 hit rekey", "I2 fetch runs+evict"};
+        unsigned long long tot = 0;
+        for (int q = 0; q < 8; ++q) tot += h[q];
+
+        fprintf(stderr, "[lsg profile] D: %llu multi-holder items (%.1f cyc/item incl. barrier)\n", h[8],
+                double(h[2]) / double(h[8] ? h[8] : 1));
+        fprintf(stderr, "[lsg profile] plan loop T=%llu steps, %.1f Mcycles total\n",
+                (unsigned long long)dm.T, tot / 1e6);
+        for (int q = 0; q < 8; ++q)
+            fprintf(stderr, "[lsg profile]   %-22s %10.1f kcyc  %6.2f%%  %8.0f cyc/step\n", names[q],
+                    h[q] / 1e3, 100.0 * h[q] / (tot ? tot : 1), double(h[q]) / double(dm.T ? dm.T : 1));
+    }
     return kOk;
 }
 

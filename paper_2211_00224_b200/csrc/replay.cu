@@ -202,15 +202,23 @@ __device__ void r_evict(const ReplayArgs& a, RShared& sh, uint32_t k, uint32_t n
         const uint64_t base = a.gb[beta] + o;
         const uint32_t kb = uint32_t(beta) * a.B;
         uint32_t c = 0;
-        for (; c < L && need > 0; c += 32) {
-            const uint32_t r = c + lane;  // reverse list order: largest position first
-            bool mem = false;
-            uint32_t x = 0, idx = 0;
-            if (r < L) {
-                idx = L - 1 - r;
-                x = a.items[base + idx] & ~kHit;
-                mem = __ldcg(&keyk[x]) == kb + idx;
+        for (; c < L && need > 0; c += 128) {
+            uint32_t xs[4];
+            bool ms[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // reverse list order: largest position first
+                const uint32_t r = c + 32 * u + lane;
+                xs[u] = r < L ? (a.items[base + (L - 1 - r)] & ~kHit) : 0u;
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t r = c + 32 * u + lane;
+                ms[u] = r < L && __ldcg(&keyk[xs[u]]) == kb + (L - 1 - r);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+            const uint32_t x = xs[u];
+            const bool mem = ms[u];
             const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mem);
             const uint32_t rank = __popc(bal & lt);
             const uint32_t took = min(uint32_t(__popc(bal)), need);
@@ -233,6 +241,7 @@ __device__ void r_evict(const ReplayArgs& a, RShared& sh, uint32_t k, uint32_t n
                 sh.nfree = nf + __popc(sbal);
             }
             __syncwarp();
+            }
         }
         if (c >= L && need > 0 && lane == 0) atomicAnd(&nzk[beta >> 5], ~(1u << (beta & 31)));
         if (lane == 0) sh.top = uint32_t(beta);
@@ -277,7 +286,7 @@ __global__ void __launch_bounds__(kRT) k_replay(ReplayArgs a) {
                 const uint32_t x = a.items[base + i] & ~kHit;
                 res = __ldcg(&keyk[x]) != kNone;
                 sx[i] = x | (res ? kHit : 0u);
-                if (a.slot_out) a.slot_out[base + i] = res ? slotk[x] : kNever;
+                if (a.slot_out) a.slot_out[base + i] = res ? (slotk[x] | kHit) : kNever;
                 hitc += res;
             }
             __syncthreads();

@@ -1,0 +1,141 @@
+"""GPU parity for K7 (per-rank replay), K9 (store payload) and K8 (gather),
+and the end-to-end HBM buffer data path (replay slots + fill + gather)."""
+import random
+
+import numpy as np
+import pytest
+
+import oracle as O
+from test_gpu_parity import to_pc, u32
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
+
+
+def _plan_obj(ls, items, node_off, N, D, spe):
+    T = node_off.shape[0]
+    return ls.SchedulePlan(D, N, 0, spe, None, _dev(items), _dev(node_off.reshape(T, N + 1)), None, None)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_replay_matches_oracle_on_oracle_plans(ls, seed):
+    r = random.Random(77 + seed)
+    N, b = r.choice([1, 2, 3, 4, 8]), r.choice([1, 2, 4, 8, 16])
+    B = N * b
+    D = B * r.randint(1, 25) + r.randint(0, B - 1)
+    c = O.Cfg(D, r.randint(1, 7), N, b, seed=seed, buffer_capacity=r.randint(1, max(1, D // 3)),
+              drop_last=r.random() < 0.7, optim_order=r.random() < 0.7,
+              optim_remap=r.random() < 0.8, optim_balance=r.random() < 0.8, pso_iters=20)
+    p = O.plan(c)
+    for C in (c.buffer_capacity, max(1, c.buffer_capacity // 3), D):
+        h, m = O.simulate(p.items, p.node_off, N, D, C)
+        sim = ls.simulate_plan(_plan_obj(ls, p.items, p.node_off, N, D, c.steps), C)
+        assert np.array_equal(u32(sim.hits), h) and np.array_equal(u32(sim.misses), m), C
+
+
+def test_replay_readme_demo_totals(ls):
+    c = O.Cfg(1024, 6, 4, 8, seed=7, buffer_capacity=64)
+    out = ls.plan_schedule(to_pc(ls, c))
+    sim = ls.simulate_plan(out.plan, 64)
+    assert (sim.total_misses, sim.total_hits) == (4864, 1280)
+
+
+def test_replay_whole_dataset_buffer_only_cold_misses(ls):
+    # tests/test_pipeline.cpp:164-173
+    c = O.Cfg(64, 3, 1, 8, seed=5, buffer_capacity=64)
+    out = ls.plan_schedule(to_pc(ls, c))
+    sim = ls.simulate_plan(out.plan, 64)
+    assert sim.total_misses == 64 and sim.total_hits == 3 * 64 - 64
+
+
+def test_replay_node_range_sharding(ls):
+    c = O.Cfg(4096, 5, 8, 16, seed=11, buffer_capacity=300)
+    out = ls.plan_schedule(to_pc(ls, c))
+    full = ls.simulate_plan(out.plan, 300)
+    parts = [ls.simulate_plan(out.plan, 300, node_range=(k0, k1)) for k0, k1 in ((0, 3), (3, 8))]
+    hits = u32(parts[0].hits).copy()
+    hits[:, 3:] = u32(parts[1].hits)[:, 3:]
+    assert np.array_equal(hits, u32(full.hits))
+
+
+def test_replay_rejects_repeats_within_a_step(ls):
+    items = np.array([1, 1, 2, 3], dtype=np.uint32)
+    off = np.array([[0, 2, 4]], dtype=np.uint32)
+    with pytest.raises(ls.Error):
+        ls.simulate_plan(_plan_obj(ls, items, off, 2, 8, 1), 2)
+
+
+def test_store_fill_golden(ls):
+    import torch
+    # tests/test_store.cpp:63-65 — first 32 payload bytes of a seed-1 store
+    row = ls.store_fill(torch.tensor([0], dtype=torch.int32, device="cuda"), 32, 1)
+    assert bytes(row.cpu().numpy().ravel()).hex() == \
+        "c15c0289ec2d0a9167ec8e65a18debbe5e5532fbeea293f80bc942ee9086c171"
+
+
+@pytest.mark.parametrize("size", [16, 48, 4096, 7, 1000])
+def test_store_fill_matches_oracle(ls, size):
+    import torch
+    ids = np.array([5, 0, 17, 3, 17, 99], dtype=np.uint32)
+    got = ls.store_fill(_dev(ids), size, 12345).cpu().numpy()
+    for r, x in enumerate(ids):
+        assert np.array_equal(got[r], O.store_payload(12345, int(x) * size, size))
+
+
+def test_gather_matches_indexing(ls):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(0)
+    buf = torch.randint(0, 255, (257, 262144), dtype=torch.uint8, device="cuda", generator=g)
+    slots = torch.randint(0, 257, (300,), dtype=torch.int32, device="cuda", generator=g)
+    out = ls.gather(buf, slots, 262144)
+    assert torch.equal(out, buf[slots.long()])
+    small = torch.randint(0, 255, (10, 48), dtype=torch.uint8, device="cuda", generator=g)
+    s2 = torch.tensor([9, 0, 3, 3], dtype=torch.int32, device="cuda")
+    assert torch.equal(ls.gather(small, s2, 48), small[s2.long()])
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_buffer_data_path_end_to_end(ls, seed):
+    """Replay slots drive a real per-node HBM buffer: every step, the samples
+    resident at step start are gathered from their slots (bytes must equal
+    Store::read_one), then misses are 'fetched' (K9) into their new slots."""
+    import torch
+    r = random.Random(seed)
+    N, b = r.choice([2, 4]), r.choice([4, 8])
+    D = N * b * r.randint(4, 10)
+    C = r.randint(N * b, D // 2)
+    size, fill_seed, NEV = 64, 99, 0xFFFFFFFE
+    c = O.Cfg(D, 4, N, b, seed=seed, buffer_capacity=C, pso_iters=20)
+    out = ls.plan_schedule(to_pc(ls, c))
+    sim = ls.simulate_plan(out.plan, C, want_slots=True)
+    items = u32(out.plan.items) & 0x7FFFFFFF
+    slots = u32(sim.slots)
+    off = u32(out.plan.node_off)
+    hits = u32(sim.hits)
+    bufs = [torch.zeros((C, size), dtype=torch.uint8, device="cuda") for _ in range(N)]
+    owner = [dict() for _ in range(N)]
+    base = 0
+    for g in range(off.shape[0]):
+        for k in range(N):
+            lo, hi = base + off[g, k], base + off[g, k + 1]
+            ids, raw = items[lo:hi], slots[lo:hi]
+            hitf = (raw != NEV) & ((raw >> 31) == 1)
+            sl = np.where(raw == NEV, NEV, raw & 0x7FFFFFFF)
+            assert all(s == NEV or s < C for s in sl)
+            want = ls.store_fill(_dev(ids), size, fill_seed)
+            res = [i for i in range(len(ids)) if hitf[i]]
+            assert len(res) == hits[g, k], (g, k)
+            assert all(owner[k].get(int(sl[i])) == int(ids[i]) for i in res), (g, k)
+            if res:
+                got = ls.gather(bufs[k], _dev(sl[res]), size)
+                assert torch.equal(got, want[res]), (g, k)
+            miss = [i for i in range(len(ids)) if i not in set(res) and sl[i] != NEV]
+            if miss:
+                bufs[k][torch.from_numpy(sl[miss].astype(np.int64)).cuda()] = want[miss]
+                for i in miss:
+                    owner[k][int(sl[i])] = int(ids[i])
+        base += off[g, N]
