@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""bench.py — the SOLAR loading path on B200 (driver contract: one JSON line).
+
+One bench *step* is one full pass of the hot path over the cfg2 job
+(BASELINE.json configs[1]: 262,144 PtychoNN-shaped samples of 256x256 fp32,
+100 epochs, 8 ranks, local batch 512, per-rank HBM buffer 20% of the dataset):
+
+  plan     K1 shuffle -> K2/K3 reuse matrix -> K4 PSO order -> K5/K6 step loop
+           (locality remap, balance, clairvoyant eviction)   [replicated per GPU]
+  replay   K7 per-rank Belady replay of this GPU's ranks + NCCL all-reduce of the
+           per-(step, rank) hit/miss rows                    [sharded by rank]
+  fetch    K8/K9 every training step's batch of this GPU's ranks: hits gathered
+           from the rank's 12.8 GiB HBM sample buffer, misses written from
+           storage (synthetic Store payload) into the batch and their slot
+
+value = planned-and-fetched samples of the whole job / step time (max over
+ranks): the loading path's throughput. `plan_samples_per_s` isolates the plan
+(north star: < 1 s for this job). The roofline object is the fetch phase
+(HBM-bound gather). GPUs own contiguous rank ranges (8 ranks / N GPUs); the
+job is fixed, so scaling is strong.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference/proj/src): plan_schedule + simulate_plan on a
+bounded sample of the same job shape (first E_SAMPLE epochs) plus
+Store::read_one batch fetches, on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "plan samples/s (shuffle+order+evict+assign); HBM-buffer gather GB/s; 1-8 GPU"
+CFG2 = dict(D=262144, E=100, N=8, b=512, C=52428, sample_bytes=256 * 256 * 4, seed=42, fill_seed=1)
+E_SAMPLE = 3  # reference arm: epochs of the bounded CPU sample
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------- reference --
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O  # the checker / reference-arm leg only
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_dump not built "
+                          "(needs /root/reference at build time)"}))
+        return 0
+    c = CFG2
+    cfg = O.Cfg(c["D"], E_SAMPLE, c["N"], c["b"], seed=c["seed"], buffer_capacity=c["C"])
+    ncpu = os.cpu_count() or 1
+    nreads = 4096
+
+    def one_step():
+        t = O.ref_time(cfg, 1)
+        with_tmp = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+        g = json.loads(subprocess.run([O.REF_DUMP, "gather", with_tmp, "4096", str(c["sample_bytes"]),
+                                       str(nreads), str(ncpu)], check=True, capture_output=True,
+                                      text=True).stdout.strip().splitlines()[-1])
+        plan_s = t["plan_schedule_s"] + t["simulate_s"]
+        per_sample = plan_s / t["accesses"] + g["seconds"] / g["samples"]
+        return per_sample, t, g
+
+    for _ in range(args.warmup):
+        one_step()
+    per, ts = [], []
+    for _ in range(args.steps):
+        p, t, g = one_step()
+        per.append(p)
+        ts.append((t, g))
+    per_sample = statistics.median(per)
+    value = 1.0 / per_sample
+    t, g = ts[len(ts) // 2]
+    A = c["E"] * c["D"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_sample * A * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "cfg2: D=262144 E=100 N=8 b=512 C=52428 (20%/rank), 256 KiB samples",
+                   "global_batch": c["N"] * c["b"], "parallelism": "reference CPU"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": f"1 (planner, single-threaded by "
+                         f"construction) + {g['threads']} (Store::read_one fetch)", "kind": "reference",
+                         "sample": f"plan_schedule+simulate_plan on the cfg2 shape with E={E_SAMPLE} epochs "
+                                   f"({t['accesses']} accesses, {t['plan_schedule_s'] + t['simulate_s']:.2f} s) + "
+                                   f"{g['samples']} Store::read_one of 256 KiB ({g['seconds']:.3f} s); "
+                                   f"per-sample cost extrapolated to the {A}-access job"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_stages_s": {k: t[k] for k in ("trace_s", "graph_s", "pso_s", "plan_schedule_s", "simulate_s")},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ ours --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--epochs", type=int, default=None, help="override E (debug only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_00224_b200 as ls
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    c = dict(CFG2)
+    if args.epochs:
+        c["E"] = args.epochs
+    D, E, N, b, C, SB = c["D"], c["E"], c["N"], c["b"], c["C"], c["sample_bytes"]
+    if N % world:
+        raise SystemExit(f"--gpus must divide the {N} ranks")
+    k0, k1 = rank * N // world, (rank + 1) * N // world
+    pc = ls.PipelineConfig(trace=ls.TraceConfig(D, E, N, b, c["seed"], True), buffer_capacity=C)
+    sh = pc.shape()
+    T, A = int(sh.total_steps), E * D
+
+    # per-rank HBM sample buffers (C slots x 256 KiB) and batch tensors
+    bufs = {k: torch.empty((C, SB), dtype=torch.uint8, device=dev) for k in range(k0, k1)}
+    maxlen = c["N"] * b  # a node list never exceeds its step
+    outs = {k: torch.empty((maxlen, SB), dtype=torch.uint8, device=dev) for k in range(k0, k1)}
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    stream = torch.cuda.current_stream()
+
+    def step(host=False):
+        """one pass of the hot path; returns (events, counters)."""
+        e = [ev() for _ in range(4)]
+        e[0].record(stream)
+        out = ls.plan_schedule_host(pc) if host else ls.plan_schedule(pc)
+        e[1].record(stream)
+        plan = out.plan
+        if host:  # e2e: the plan lives in host memory; the device copy feeds the replay
+            items = plan.items.to(dev, non_blocking=True)
+            noff = plan.node_off.to(dev, non_blocking=True)
+            plan = ls.SchedulePlan(plan.dataset_size, N, b, plan.steps_per_epoch, plan.order, items,
+                                   noff, plan.fetches_before, plan.fetches_after)
+        sim = ls.simulate_plan(plan, C, node_range=(k0, k1), want_slots=True)
+        if world > 1:
+            dist.all_reduce(sim.hits)
+            dist.all_reduce(sim.misses)
+        e[2].record(stream)
+        off = plan.node_off.cpu().numpy() if not host else out.plan.node_off.numpy()
+        bases = [0] * (T + 1)
+        for g in range(T):
+            bases[g + 1] = bases[g] + int(off[g, N])
+        items, slots = plan.items, sim.slots
+        for g in range(T):
+            base = bases[g]
+            for k in range(k0, k1):
+                lo, hi = base + int(off[g, k]), base + int(off[g, k + 1])
+                if hi > lo:
+                    ls.batch_fetch(bufs[k], items[lo:hi], slots[lo:hi], SB, c["fill_seed"], outs[k])
+        e[3].record(stream)
+        rows = None
+        if host:
+            rows = (sim.hits.cpu(), sim.misses.cpu())
+        return e, sim, off, rows
+
+    # warm-up (also the first pass that fills the HBM buffers)
+    for _ in range(max(args.warmup, 3 if args.steps else 0)):
+        step()
+    torch.cuda.synchronize()
+
+    # hit/miss totals of the local ranks (for algorithmic bytes)
+    _, sim0, off0, _ = step()
+    torch.cuda.synchronize()
+    local_hits = int(sim0.hits[:, k0:k1].sum())
+    local_misses = int(sim0.misses[:, k0:k1].sum())
+    slots_np = sim0.slots.cpu().numpy().view("uint32")
+    kept = int(((slots_np != 0xFFFFFFFE) & ((slots_np >> 31) == 0)).sum())  # all ranks' rows
+    # restrict kept misses to the local ranks
+    bases = [0]
+    for g in range(T):
+        bases.append(bases[-1] + int(off0[g, N]))
+    kept_local = 0
+    for g in range(T):
+        for k in range(k0, k1):
+            lo, hi = bases[g] + int(off0[g, k]), bases[g] + int(off0[g, k + 1])
+            s = slots_np[lo:hi]
+            kept_local += int(((s != 0xFFFFFFFE) & ((s >> 31) == 0)).sum())
+    del kept
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ls.lib().lsg_launch_count()
+    gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
+        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    with ClockSampler(gpu_index) as clk:
+        t_start, t_end = ev(), ev()
+        t_start.record(stream)
+        evs = []
+        for _ in range(args.steps):
+            e, _, _, _ = step()
+            evs.append(e)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = ls.lib().lsg_launch_count() - launches0
+    total_ms = t_start.elapsed_time(t_end)
+    plan_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    replay_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    fetch_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    if world > 1:
+        tt = torch.tensor([total_ms, plan_ms, replay_ms, fetch_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, plan_ms, replay_ms, fetch_ms = [float(x) for x in tt]
+    ms_per_step = total_ms / max(args.steps, 1)
+
+    # fetch-phase algorithmic bytes: hits read a slot and write the batch row;
+    # misses write the batch row (+ the slot when kept)
+    alg_bytes = 2 * SB * local_hits + SB * local_misses + SB * kept_local
+    achieved = alg_bytes / (fetch_ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "gather_traffic.json")))
+        traffic = tr.get("dram_bytes_per_byte_algorithmic")
+    except Exception:
+        pass
+
+    # e2e through the C-ABI host path (lsg_plan_host: the plan lands in host
+    # memory; hit/miss rows read back)
+    e2e = None
+    if not args.no_e2e and args.steps:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = ev(), ev()
+        a0.record(stream)
+        step(host=True)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = a0.elapsed_time(a1)
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt[0])
+        d2h = A * 4 * 2 + T * (N + 1) * 4 + 2 * T * N * 4 * 2 + E * E * 8 + E * 4 + 8 + 4 \
+            + pc.pso.max_iters * 8 + T * N * 4 * 2 + T * (N + 1) * 4
+        e2e = {"value": A / (e2e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": T * (N + 1) * 4 + A * 4,
+               "d2h_bytes_per_step": d2h,
+               "note": "lsg_plan_host (trace, graph, order, plan lists, fetch counts to host), plan "
+                       "re-uploaded for the replay, hit/miss rows read back, batch fetch on device"}
+
+    cpu = cpu_baseline() if (rank == 0 and world == 1) else None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": A / (ms_per_step * 1e-3), "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (splitmix64 traces and Store payload, seed 42 / fill_seed 1)",
+            "config": {"workload": f"cfg2: D={D} E={E} N={N} b={b} C={C} (20%/rank), 256 KiB samples, "
+                                   f"plan+replay+fetch of the whole job",
+                       "global_batch": N * b, "ranks_per_gpu": N // world,
+                       "parallelism": f"plan replicated; replay+fetch sharded {N // world} ranks/GPU",
+                       "l2": "inputs > L2 (12.8 GiB HBM sample buffer per rank)"},
+            "plan_ms": plan_ms, "replay_ms": replay_ms, "fetch_ms": fetch_ms,
+            "plan_samples_per_s": A / (plan_ms * 1e-3),
+            "gather": {"value": achieved, "unit": "GB/s", "hits": local_hits, "misses": local_misses,
+                       "bytes_per_step": alg_bytes},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "fetch phase (k_gather_hits + k_fill_misses per rank-step)",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6650"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def cpu_baseline():
+    """The reference CPU planner (oracle/_ref) on a bounded sample, rank 0 only."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        import oracle as O
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+    if not O.ref_available():
+        return {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    c = CFG2
+    cfg = O.Cfg(c["D"], E_SAMPLE, c["N"], c["b"], seed=c["seed"], buffer_capacity=c["C"])
+    t = O.ref_time(cfg, 1)
+    tmp = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+    ncpu = os.cpu_count() or 1
+    g = json.loads(subprocess.run([O.REF_DUMP, "gather", tmp, "4096", str(c["sample_bytes"]), "4096",
+                                   str(ncpu)], check=True, capture_output=True, text=True).stdout.strip().splitlines()[-1])
+    per = (t["plan_schedule_s"] + t["simulate_s"]) / t["accesses"] + g["seconds"] / g["samples"]
+    return {"value": 1.0 / per, "unit": "samples/s",
+            "cores": f"1 (planner) + {g['threads']} (Store::read_one)", "kind": "reference",
+            "sample": f"cfg2 shape, E={E_SAMPLE} epochs ({t['accesses']} accesses): plan_schedule "
+                      f"{t['plan_schedule_s']:.2f} s + simulate_plan {t['simulate_s']:.2f} s; "
+                      f"{g['samples']} Store::read_one 256 KiB in {g['seconds']:.3f} s",
+            "plan_samples_per_s": t["accesses"] / t["plan_schedule_s"]}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -135,6 +135,17 @@ int lsg_store_fill(const uint32_t* d_ids, uint64_t n, uint64_t sample_bytes, uin
 int lsg_gather(const void* d_buf, const uint32_t* d_slots, uint64_t n, uint64_t sample_bytes,
                void* d_out, void* stream);
 
+/* ---- K8+K9: fetch one node's batch for one step (the loading phase of a
+ *      training step on that rank): rows whose replay slot (lsg_simulate
+ *      d_slot, bit 31 = resident at step start) is a hit are gathered from
+ *      their HBM slot; all other rows receive the sample's Store payload
+ *      (the storage read, synthesised on device) in the batch and, unless the
+ *      replay bypassed the sample (LSG_NEVER), in its new HBM slot. Hits are
+ *      copied before any miss is written, so a slot freed and re-filled in
+ *      the same step is read before it is overwritten. */
+int lsg_batch_fetch(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots, uint64_t n,
+                    uint64_t sample_bytes, uint64_t fill_seed, void* d_out, void* stream);
+
 /* Number of kernel launches issued by this library since load (for the
  * bench's gpu_launches claim). */
 uint64_t lsg_launch_count(void);

@@ -10,6 +10,7 @@
 //   ref_dump simulate <indir>  C policy       simulate_plan over a dumped plan
 //   ref_dump time     <samples> key=value...  stage timings (JSON on stdout)
 //   ref_dump store    <out> count size seed   Store payload bytes (no header)
+//   ref_dump gather   <dir> count size n thr  Store::read_one batch-fetch timing
 //
 // key=value pairs go through the reference's apply_config_entry
 // (proj/src/config.cpp) so their meaning is exactly the reference's.
@@ -20,12 +21,14 @@
 #include <fstream>
 #include <iostream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "loadsched/buffer.hpp"
 #include "loadsched/config.hpp"
 #include "loadsched/errors.hpp"
 #include "loadsched/pipeline.hpp"
+#include "loadsched/prng.hpp"
 #include "loadsched/store.hpp"
 
 using namespace loadsched;
@@ -247,6 +250,43 @@ int cmd_time(int argc, char** argv) {
     return 0;
 }
 
+// Batch fetch through the reference's own Store::read_one (store.cpp:134-139)
+// from a page-cached store file: `nreads` random samples split over
+// `threads` host threads (Store is documented safe for concurrent reads,
+// store.hpp:29-30). Prints JSON.
+int cmd_gather(int argc, char** argv) {
+    if (argc < 7) throw ValidationError("gather <dir> count size nreads threads");
+    const std::string path = std::string(argv[2]) + "/ref_gather_store.bin";
+    const std::uint64_t count = std::stoull(argv[3]), size = std::stoull(argv[4]);
+    const std::uint64_t nreads = std::stoull(argv[5]);
+    const unsigned threads = unsigned(std::stoul(argv[6]));
+    create_store(path, count, size, 1, ~0ULL);
+    Store store(path);
+    for (std::uint64_t i = 0; i < count; ++i) (void)store.read_one(i);  // page-cache warm
+    std::vector<std::uint64_t> ids(nreads);
+    SplitMix64 rng(7);
+    for (auto& v : ids) v = rng.next_below(count);
+    std::vector<std::thread> pool;
+    std::vector<std::uint64_t> sink(threads, 0);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+            for (std::uint64_t i = t; i < nreads; i += threads) {
+                const auto bytes = store.read_one(ids[i]);
+                sink[t] += std::to_integer<unsigned>(bytes[i % bytes.size()]);
+            }
+        });
+    for (auto& th : pool) th.join();
+    const double sec = secs(t0);
+    std::remove(path.c_str());
+    std::uint64_t chk = 0;
+    for (auto v : sink) chk += v;
+    std::printf("{\"seconds\": %.6f, \"samples\": %llu, \"bytes\": %llu, \"threads\": %u, \"chk\": %llu}\n",
+                sec, (unsigned long long)nreads, (unsigned long long)(nreads * size), threads,
+                (unsigned long long)chk);
+    return 0;
+}
+
 int cmd_store(int argc, char** argv) {
     if (argc < 6) throw ValidationError("store <out> count size seed");
     const std::string path = std::string(argv[2]) + ".store";
@@ -275,6 +315,7 @@ int main(int argc, char** argv) {
         if (cmd == "simulate") return cmd_simulate(argc, argv);
         if (cmd == "time") return cmd_time(argc, argv);
         if (cmd == "store") return cmd_store(argc, argv);
+        if (cmd == "gather") return cmd_gather(argc, argv);
         std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
         return 1;
     } catch (const Error& e) {

@@ -32,6 +32,8 @@ int gather_device(const void* d_buf, const uint32_t* d_slots, uint64_t n, uint64
                   void* d_out, cudaStream_t st);
 int store_fill_device(const uint32_t* d_ids, uint64_t n, uint64_t sample_bytes, uint64_t seed,
                       void* d_dst, cudaStream_t st);
+int batch_fetch_device(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots, uint64_t n,
+                       uint64_t sample_bytes, uint64_t seed, void* d_out, cudaStream_t st);
 
 namespace {
 thread_local std::string g_err;
@@ -285,6 +287,12 @@ int lsg_store_fill(const uint32_t* d_ids, uint64_t n, uint64_t sample_bytes, uin
 int lsg_gather(const void* d_buf, const uint32_t* d_slots, uint64_t n, uint64_t sample_bytes,
                void* d_out, void* stream) {
     return gather_device(d_buf, d_slots, n, sample_bytes, d_out, static_cast<cudaStream_t>(stream));
+}
+
+int lsg_batch_fetch(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots, uint64_t n,
+                    uint64_t sample_bytes, uint64_t fill_seed, void* d_out, void* stream) {
+    return batch_fetch_device(d_buf, d_ids, d_slots, n, sample_bytes, fill_seed, d_out,
+                              static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -76,7 +76,80 @@ __global__ void k_store_fill_bytes(const uint32_t* __restrict__ ids, uint64_t n,
     }
 }
 
+// K8 fetch of one node list: rows whose replay slot carries the hit flag
+// (bit 31) are copied from their HBM slot; the rest are left to k_fill_misses.
+__global__ void __launch_bounds__(kGatherThreads) k_gather_hits(const uint4* __restrict__ buf,
+                                                                const uint32_t* __restrict__ slots,
+                                                                uint64_t n, uint64_t vec_per_row,
+                                                                uint64_t tiles_per_row,
+                                                                uint4* __restrict__ out) {
+    const uint64_t ntiles = n * tiles_per_row;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t row = tile / tiles_per_row;
+        const uint32_t sl = __ldg(&slots[row]);
+        if (sl == kNever || !(sl & kHit)) continue;  // block-uniform
+        const uint64_t c0 = (tile - row * tiles_per_row) * kTileVec;
+        const uint4* src = buf + uint64_t(sl & ~kHit) * vec_per_row;
+        uint4* dst = out + row * vec_per_row;
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t c = c0 + u * kGatherThreads + threadIdx.x;
+            if (c < vec_per_row) v[u] = __ldcs(&src[c]);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t c = c0 + u * kGatherThreads + threadIdx.x;
+            if (c < vec_per_row) __stcs(&dst[c], v[u]);
+        }
+    }
+}
+
+// Misses: the sample arrives from storage (synthesised Store payload) into
+// its batch row and, unless the replay bypassed it, into its new HBM slot.
+__global__ void __launch_bounds__(256) k_fill_misses(const uint32_t* __restrict__ ids,
+                                                     const uint32_t* __restrict__ slots, uint64_t n,
+                                                     uint64_t words_per_row, uint64_t seed,
+                                                     ulonglong2* __restrict__ buf,
+                                                     ulonglong2* __restrict__ out) {
+    const uint64_t pairs = words_per_row / 2;
+    for (uint64_t row = blockIdx.y; row < n; row += gridDim.y) {
+        const uint32_t sl = __ldg(&slots[row]);
+        if (sl != kNever && (sl & kHit)) continue;
+        const uint64_t word0 = uint64_t(__ldg(&ids[row]) & ~kHit) * words_per_row;
+        for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < pairs;
+             p += uint64_t(gridDim.x) * blockDim.x) {
+            ulonglong2 v;
+            v.x = mix64(seed + (word0 + 2 * p + 1) * kGamma);
+            v.y = mix64(seed + (word0 + 2 * p + 2) * kGamma);
+            __stcs(&out[row * pairs + p], v);
+            if (sl != kNever) __stcs(&buf[uint64_t(sl) * pairs + p], v);
+        }
+    }
+}
+
 }  // namespace
+
+int batch_fetch_device(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots, uint64_t n,
+                       uint64_t sample_bytes, uint64_t seed, void* d_out, cudaStream_t st) {
+    if (n == 0) return kOk;
+    if (sample_bytes == 0 || sample_bytes % 16 != 0)
+        return set_error(kValidation, "batch_fetch: sample_bytes must be a positive multiple of 16");
+    if ((reinterpret_cast<uintptr_t>(d_buf) | reinterpret_cast<uintptr_t>(d_out)) & 15)
+        return set_error(kValidation, "batch_fetch: buffers must be 16-byte aligned");
+    const uint64_t vpr = sample_bytes / 16;
+    const uint64_t tpr = (vpr + kTileVec - 1) / kTileVec;
+    const unsigned grid = unsigned(std::min<uint64_t>(n * tpr, 148ull * 8));
+    k_gather_hits<<<grid, kGatherThreads, 0, st>>>(static_cast<const uint4*>(d_buf), d_slots, n, vpr, tpr,
+                                                   static_cast<uint4*>(d_out));
+    LSG_LAUNCH_CHECK("k_gather_hits");
+    const uint64_t wpr = sample_bytes / 8;
+    dim3 g2(unsigned(std::min<uint64_t>((wpr / 2 + 255) / 256, 16)), unsigned(std::min<uint64_t>(n, 4096)));
+    k_fill_misses<<<g2, 256, 0, st>>>(d_ids, d_slots, n, wpr, seed, static_cast<ulonglong2*>(d_buf),
+                                      static_cast<ulonglong2*>(d_out));
+    LSG_LAUNCH_CHECK("k_fill_misses");
+    return kOk;
+}
 
 int gather_device(const void* d_buf, const uint32_t* d_slots, uint64_t n, uint64_t sample_bytes,
                   void* d_out, cudaStream_t st) {

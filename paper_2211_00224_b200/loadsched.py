@@ -21,7 +21,7 @@ __all__ = [
     "TraceConfig", "PsoParams", "PipelineConfig", "AccessTrace", "ReuseGraph", "EpochOrder",
     "PsoResult", "SchedulePlan", "PlanOutput", "SimResult", "generate_trace", "build_reuse_graph",
     "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "simulate_plan",
-    "store_fill", "gather", "Error", "ConfigError", "ValidationError", "CapabilityError",
+    "store_fill", "gather", "batch_fetch", "Error", "ConfigError", "ValidationError", "CapabilityError",
     "StorageError", "InternalError", "HIT_BIT", "NEVER",
 ]
 
@@ -376,4 +376,15 @@ def gather(buf: torch.Tensor, slots: torch.Tensor, sample_bytes: int,
     if out is None:
         out = torch.empty((n, sample_bytes), dtype=torch.uint8, device=buf.device)
     _check(lib().lsg_gather(_ptr(buf), _ptr(slots), n, sample_bytes, _ptr(out), _stream()))
+    return out
+
+
+def batch_fetch(buf: torch.Tensor, ids: torch.Tensor, slots: torch.Tensor, sample_bytes: int,
+                fill_seed: int, out: torch.Tensor) -> torch.Tensor:
+    """K8+K9 loading phase of one node list: hits gathered from their HBM slots,
+    misses written from storage (synthetic Store payload) into the batch and
+    into their new slot (lsg_batch_fetch)."""
+    n = ids.numel()
+    _check(lib().lsg_batch_fetch(_ptr(buf), _ptr(ids), _ptr(slots), n, sample_bytes, fill_seed,
+                                 _ptr(out), _stream()))
     return out
