@@ -191,6 +191,8 @@ def main():
     maxlen = c["N"] * b  # a node list never exceeds its step
     outs = {k: torch.empty((maxlen, SB), dtype=torch.uint8, device=dev) for k in range(k0, k1)}
 
+    fetcher = ls.StepFetcher([bufs[k] for k in range(k0, k1)], [outs[k] for k in range(k0, k1)],
+                             (k0, k1), SB, c["fill_seed"])
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     stream = torch.cuda.current_stream()
 
@@ -215,13 +217,10 @@ def main():
         bases = [0] * (T + 1)
         for g in range(T):
             bases[g + 1] = bases[g] + int(off[g, N])
-        items, slots = plan.items, sim.slots
+        items, slots, noff_d = plan.items, sim.slots, plan.node_off
         for g in range(T):
             base = bases[g]
-            for k in range(k0, k1):
-                lo, hi = base + int(off[g, k]), base + int(off[g, k + 1])
-                if hi > lo:
-                    ls.batch_fetch(bufs[k], items[lo:hi], slots[lo:hi], SB, c["fill_seed"], outs[k])
+            fetcher(items[base:], slots[base:], noff_d[g], int(off[g, k1]) - int(off[g, k0]))
         e[3].record(stream)
         rows = None
         if host:
@@ -288,10 +287,11 @@ def main():
     except Exception:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
+    traffic = traffic_ratio = None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "gather_traffic.json")))
-        traffic = tr.get("dram_bytes_per_byte_algorithmic")
+        traffic = tr.get("dram_bytes_per_launch")
+        traffic_ratio = tr.get("dram_bytes_per_byte_algorithmic")
     except Exception:
         pass
 
@@ -338,7 +338,10 @@ def main():
                        "bytes_per_step": alg_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "fetch phase (k_gather_hits + k_fill_misses per rank-step)",
+                         "traffic_note": "dram read+write bytes per k_fetch_step_hits launch (one step, all local "
+                                         "ranks) from profiles/r01_ncu_full_summary.txt; "
+                                         f"{traffic_ratio} x the launch's algorithmic bytes" if traffic else None,
+                         "kernel": "fetch phase (k_fetch_step_hits + k_fetch_step_misses, one pair per step)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6650"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -146,6 +146,16 @@ int lsg_gather(const void* d_buf, const uint32_t* d_slots, uint64_t n, uint64_t 
 int lsg_batch_fetch(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots, uint64_t n,
                     uint64_t sample_bytes, uint64_t fill_seed, void* d_out, void* stream);
 
+/* Same for every node of [node_begin, node_end) of one step in two launches:
+ * d_items/d_slots point at the step's first item (lsg_plan_out.items +
+ * step base), d_node_off at the step's [N+1] offsets, d_bufs/d_outs are
+ * DEVICE arrays of (node_end - node_begin) buffer / batch pointers. rows_hint
+ * (the number of rows in the range, or 0) only sizes the grid. */
+int lsg_fetch_step(void* const* d_bufs, void* const* d_outs, const uint32_t* d_items,
+                   const uint32_t* d_slots, const uint32_t* d_node_off, uint32_t node_begin,
+                   uint32_t node_end, uint64_t rows_hint, uint64_t sample_bytes, uint64_t fill_seed,
+                   void* stream);
+
 /* Number of kernel launches issued by this library since load (for the
  * bench's gpu_launches claim). */
 uint64_t lsg_launch_count(void);

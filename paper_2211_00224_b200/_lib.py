@@ -68,7 +68,7 @@ class LsgPlanOut(ctypes.Structure):
 EXPORTS = [
     "lsg_version", "lsg_last_error", "lsg_shape_of", "lsg_generate_trace",
     "lsg_build_reuse_graph", "lsg_pso_order", "lsg_plan", "lsg_plan_host", "lsg_simulate",
-    "lsg_store_fill", "lsg_gather", "lsg_batch_fetch", "lsg_launch_count",
+    "lsg_store_fill", "lsg_gather", "lsg_batch_fetch", "lsg_fetch_step", "lsg_launch_count",
 ]
 
 
@@ -107,6 +107,7 @@ def lib() -> ctypes.CDLL:
         L.lsg_store_fill.argtypes = [P, u64, u64, u64, P, P]
         L.lsg_gather.argtypes = [P, P, u64, u64, P, P]
         L.lsg_batch_fetch.argtypes = [P, P, P, u64, u64, u64, P, P]
+        L.lsg_fetch_step.argtypes = [P, P, P, P, P, u32, u32, u64, u64, u64, P]
         _lib = L
     return _lib
 

@@ -34,6 +34,9 @@ int store_fill_device(const uint32_t* d_ids, uint64_t n, uint64_t sample_bytes, 
                       void* d_dst, cudaStream_t st);
 int batch_fetch_device(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots, uint64_t n,
                        uint64_t sample_bytes, uint64_t seed, void* d_out, cudaStream_t st);
+int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* d_items,
+                      const uint32_t* d_slots, const uint32_t* d_node_off, uint32_t k0, uint32_t k1,
+                      uint64_t rows_hint, uint64_t sample_bytes, uint64_t seed, cudaStream_t st);
 
 namespace {
 thread_local std::string g_err;
@@ -293,6 +296,14 @@ int lsg_batch_fetch(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots,
                     uint64_t sample_bytes, uint64_t fill_seed, void* d_out, void* stream) {
     return batch_fetch_device(d_buf, d_ids, d_slots, n, sample_bytes, fill_seed, d_out,
                               static_cast<cudaStream_t>(stream));
+}
+
+int lsg_fetch_step(void* const* d_bufs, void* const* d_outs, const uint32_t* d_items,
+                   const uint32_t* d_slots, const uint32_t* d_node_off, uint32_t node_begin,
+                   uint32_t node_end, uint64_t rows_hint, uint64_t sample_bytes, uint64_t fill_seed,
+                   void* stream) {
+    return fetch_step_device(d_bufs, d_outs, d_items, d_slots, d_node_off, node_begin, node_end,
+                             rows_hint, sample_bytes, fill_seed, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -128,7 +128,102 @@ __global__ void __launch_bounds__(256) k_fill_misses(const uint32_t* __restrict_
     }
 }
 
+// Step-level fetch for a contiguous range of nodes [k0, k1): their lists are
+// contiguous in the step's item array (rows node_off[k0] .. node_off[k1]), so
+// one launch covers every local rank of the step. Row r of node k goes to
+// outs[k - k0] row r - node_off[k] and, for hits, comes from bufs[k - k0].
+struct StepFetch {
+    const uint32_t* items;     // step's items (ids | hit tag)
+    const uint32_t* slots;     // step's replay slots (bit 31 = resident at step start)
+    const uint32_t* node_off;  // [N+1] of the step
+    uint4* const* bufs;        // [k1-k0] HBM sample buffers
+    uint4* const* outs;        // [k1-k0] batch tensors
+    uint32_t k0, k1;
+    uint64_t vec_per_row, tiles_per_row, seed;
+};
+
+__device__ __forceinline__ uint32_t node_of_row(const StepFetch& f, uint32_t r) {
+    uint32_t k = f.k0;
+    while (k + 1 < f.k1 && __ldg(&f.node_off[k + 1]) <= r) ++k;
+    return k;
+}
+
+__global__ void __launch_bounds__(kGatherThreads) k_fetch_step_hits(StepFetch f) {
+    const uint32_t r0 = __ldg(&f.node_off[f.k0]);
+    const uint64_t nrows = __ldg(&f.node_off[f.k1]) - r0;
+    const uint64_t ntiles = nrows * f.tiles_per_row;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t rr = tile / f.tiles_per_row;
+        const uint32_t r = r0 + uint32_t(rr);
+        const uint32_t sl = __ldg(&f.slots[r]);
+        if (sl == kNever || !(sl & kHit)) continue;  // block-uniform
+        const uint32_t k = node_of_row(f, r);
+        const uint64_t c0 = (tile - rr * f.tiles_per_row) * kTileVec;
+        const uint4* src = f.bufs[k - f.k0] + uint64_t(sl & ~kHit) * f.vec_per_row;
+        uint4* dst = f.outs[k - f.k0] + uint64_t(r - __ldg(&f.node_off[k])) * f.vec_per_row;
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t c = c0 + u * kGatherThreads + threadIdx.x;
+            if (c < f.vec_per_row) v[u] = __ldcs(&src[c]);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint64_t c = c0 + u * kGatherThreads + threadIdx.x;
+            if (c < f.vec_per_row) __stcs(&dst[c], v[u]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
+    const uint32_t r0 = __ldg(&f.node_off[f.k0]), r1 = __ldg(&f.node_off[f.k1]);
+    const uint64_t pairs = f.vec_per_row;  // 16-byte pairs of payload words
+    for (uint32_t r = r0 + blockIdx.y; r < r1; r += gridDim.y) {
+        const uint32_t sl = __ldg(&f.slots[r]);
+        if (sl != kNever && (sl & kHit)) continue;
+        const uint32_t k = node_of_row(f, r);
+        const uint64_t word0 = uint64_t(__ldg(&f.items[r]) & ~kHit) * (2 * pairs);
+        ulonglong2* out = reinterpret_cast<ulonglong2*>(f.outs[k - f.k0]) + uint64_t(r - __ldg(&f.node_off[k])) * pairs;
+        ulonglong2* buf = sl != kNever ? reinterpret_cast<ulonglong2*>(f.bufs[k - f.k0]) + uint64_t(sl) * pairs : nullptr;
+        for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < pairs;
+             p += uint64_t(gridDim.x) * blockDim.x) {
+            ulonglong2 v;
+            v.x = mix64(f.seed + (word0 + 2 * p + 1) * kGamma);
+            v.y = mix64(f.seed + (word0 + 2 * p + 2) * kGamma);
+            __stcs(&out[p], v);
+            if (buf) __stcs(&buf[p], v);
+        }
+    }
+}
+
 }  // namespace
+
+int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* d_items,
+                      const uint32_t* d_slots, const uint32_t* d_node_off, uint32_t k0, uint32_t k1,
+                      uint64_t rows_hint, uint64_t sample_bytes, uint64_t seed, cudaStream_t st) {
+    if (k1 <= k0) return kOk;
+    if (sample_bytes == 0 || sample_bytes % 16 != 0)
+        return set_error(kValidation, "fetch_step: sample_bytes must be a positive multiple of 16");
+    StepFetch f;
+    f.items = d_items;
+    f.slots = d_slots;
+    f.node_off = d_node_off;
+    f.bufs = reinterpret_cast<uint4* const*>(d_bufs);
+    f.outs = reinterpret_cast<uint4* const*>(d_outs);
+    f.k0 = k0;
+    f.k1 = k1;
+    f.vec_per_row = sample_bytes / 16;
+    f.tiles_per_row = (f.vec_per_row + kTileVec - 1) / kTileVec;
+    f.seed = seed;
+    const uint64_t rows = rows_hint ? rows_hint : 1;
+    const unsigned grid = unsigned(std::min<uint64_t>(rows * f.tiles_per_row, 148ull * 8));
+    k_fetch_step_hits<<<grid, kGatherThreads, 0, st>>>(f);
+    LSG_LAUNCH_CHECK("k_fetch_step_hits");
+    dim3 g2(unsigned(std::min<uint64_t>((f.vec_per_row + 255) / 256, 8)), 256);
+    k_fetch_step_misses<<<g2, 256, 0, st>>>(f);
+    LSG_LAUNCH_CHECK("k_fetch_step_misses");
+    return kOk;
+}
 
 int batch_fetch_device(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots, uint64_t n,
                        uint64_t sample_bytes, uint64_t seed, void* d_out, cudaStream_t st) {

@@ -21,7 +21,7 @@ __all__ = [
     "TraceConfig", "PsoParams", "PipelineConfig", "AccessTrace", "ReuseGraph", "EpochOrder",
     "PsoResult", "SchedulePlan", "PlanOutput", "SimResult", "generate_trace", "build_reuse_graph",
     "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "simulate_plan",
-    "store_fill", "gather", "batch_fetch", "Error", "ConfigError", "ValidationError", "CapabilityError",
+    "store_fill", "gather", "batch_fetch", "StepFetcher", "Error", "ConfigError", "ValidationError", "CapabilityError",
     "StorageError", "InternalError", "HIT_BIT", "NEVER",
 ]
 
@@ -388,3 +388,24 @@ def batch_fetch(buf: torch.Tensor, ids: torch.Tensor, slots: torch.Tensor, sampl
     _check(lib().lsg_batch_fetch(_ptr(buf), _ptr(ids), _ptr(slots), n, sample_bytes, fill_seed,
                                  _ptr(out), _stream()))
     return out
+
+
+class StepFetcher:
+    """The per-step loading phase for a contiguous range of ranks (lsg_fetch_step):
+    owns the device arrays of buffer / batch pointers so one call fetches every
+    local rank's batch of a step."""
+
+    def __init__(self, bufs: list, outs: list, node_range: tuple[int, int], sample_bytes: int,
+                 fill_seed: int):
+        dev = bufs[0].device
+        self.k0, self.k1 = node_range
+        self.bufs, self.outs = bufs, outs
+        self.pb = torch.tensor([t.data_ptr() for t in bufs], dtype=torch.int64, device=dev)
+        self.po = torch.tensor([t.data_ptr() for t in outs], dtype=torch.int64, device=dev)
+        self.sample_bytes, self.fill_seed = sample_bytes, fill_seed
+
+    def __call__(self, items: torch.Tensor, slots: torch.Tensor, node_off_row: torch.Tensor,
+                 rows_hint: int = 0) -> None:
+        _check(lib().lsg_fetch_step(_ptr(self.pb), _ptr(self.po), _ptr(items), _ptr(slots),
+                                    _ptr(node_off_row), self.k0, self.k1, rows_hint,
+                                    self.sample_bytes, self.fill_seed, _stream()))

@@ -139,3 +139,33 @@ def test_buffer_data_path_end_to_end(ls, seed):
                 for i in miss:
                     owner[k][int(sl[i])] = int(ids[i])
         base += off[g, N]
+
+
+@pytest.mark.parametrize("seed,rng", [(0, None), (1, (1, 3)), (2, None)])
+def test_fetch_step_end_to_end(ls, seed, rng):
+    """lsg_fetch_step over the whole job: after every step each local rank's
+    batch rows equal Store::read_one of its list (hits from HBM slots, misses
+    from storage), i.e. the HBM buffers stay consistent with the replay."""
+    import torch
+    r = random.Random(100 + seed)
+    N, b = 4, r.choice([4, 8])
+    D = N * b * r.randint(5, 9)
+    C = r.randint(N * b, D // 2)
+    SB, fill = 48, 5
+    c = O.Cfg(D, 5, N, b, seed=seed, buffer_capacity=C, pso_iters=20)
+    out = ls.plan_schedule(to_pc(ls, c))
+    k0, k1 = rng or (0, N)
+    sim = ls.simulate_plan(out.plan, C, node_range=(k0, k1), want_slots=True)
+    bufs = [torch.zeros((C, SB), dtype=torch.uint8, device="cuda") for _ in range(k0, k1)]
+    outs = [torch.zeros((N * b, SB), dtype=torch.uint8, device="cuda") for _ in range(k0, k1)]
+    fetch = ls.StepFetcher(bufs, outs, (k0, k1), SB, fill)
+    off = u32(out.plan.node_off)
+    items = u32(out.plan.items) & 0x7FFFFFFF
+    base = 0
+    for g in range(off.shape[0]):
+        fetch(out.plan.items[base:], sim.slots[base:], out.plan.node_off[g], int(off[g, k1] - off[g, k0]))
+        for k in range(k0, k1):
+            lo, hi = base + off[g, k], base + off[g, k + 1]
+            want = ls.store_fill(_dev(items[lo:hi]), SB, fill)
+            assert torch.equal(outs[k - k0][: hi - lo], want), (g, k)
+        base += off[g, N]
