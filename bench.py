@@ -179,9 +179,9 @@ def main():
     if args.epochs:
         c["E"] = args.epochs
     D, E, N, b, C, SB = c["D"], c["E"], c["N"], c["b"], c["C"], c["sample_bytes"]
-    if N % world:
-        raise SystemExit(f"--gpus must divide the {N} ranks")
-    k0, k1 = rank * N // world, (rank + 1) * N // world
+    from paper_2211_00224_b200.parallel import combine_rows, rank_range
+
+    k0, k1 = rank_range(N, world, rank)
     pc = ls.PipelineConfig(trace=ls.TraceConfig(D, E, N, b, c["seed"], True), buffer_capacity=C)
     sh = pc.shape()
     T, A = int(sh.total_steps), E * D
@@ -209,9 +209,7 @@ def main():
             plan = ls.SchedulePlan(plan.dataset_size, N, b, plan.steps_per_epoch, plan.order, items,
                                    noff, plan.fetches_before, plan.fetches_after)
         sim = ls.simulate_plan(plan, C, node_range=(k0, k1), want_slots=True)
-        if world > 1:
-            dist.all_reduce(sim.hits)
-            dist.all_reduce(sim.misses)
+        combine_rows(sim.hits, sim.misses)
         e[2].record(stream)
         off = plan.node_off.cpu().numpy() if not host else out.plan.node_off.numpy()
         bases = [0] * (T + 1)
@@ -329,8 +327,8 @@ def main():
             "data": "synthetic (splitmix64 traces and Store payload, seed 42 / fill_seed 1)",
             "config": {"workload": f"cfg2: D={D} E={E} N={N} b={b} C={C} (20%/rank), 256 KiB samples, "
                                    f"plan+replay+fetch of the whole job",
-                       "global_batch": N * b, "ranks_per_gpu": N // world,
-                       "parallelism": f"plan replicated; replay+fetch sharded {N // world} ranks/GPU",
+                       "global_batch": N * b, "ranks_per_gpu": k1 - k0,
+                       "parallelism": f"plan replicated; replay+fetch sharded {k1 - k0} ranks/GPU",
                        "l2": "inputs > L2 (12.8 GiB HBM sample buffer per rank)"},
             "plan_ms": plan_ms, "replay_ms": replay_ms, "fetch_ms": fetch_ms,
             "plan_samples_per_s": A / (plan_ms * 1e-3),
