@@ -46,7 +46,8 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kMaxN = 32;
-constexpr uint32_t kMaxB = 8192;
+constexpr uint32_t kMaxSmemB = 8192;   // per-item arrays in shared memory up to here
+constexpr uint32_t kMaxB = 16384;      // then in L2-resident global scratch
 constexpr uint32_t kFetch = 0xFFFFFFFFu;
 constexpr uint32_t kWinWords = 40;  // I1 bucket-bit window (covers 2S <= 1216 steps)
 
@@ -124,6 +125,7 @@ struct LoopArgs {
     uint32_t* fb;                    // [T][N] output (may be null)
     uint32_t* fa;                    // [T][N] output (may be null)
     uint32_t* status;
+    uint32_t* gitems;                // [6][B] per-item arrays when they do not fit smem
     unsigned long long* prof;        // [8] per-phase cycles (LSG_PROFILE) or null
     int dbg_skip;                    // timing experiments only (LSG_DEBUG_SKIP)
 };
@@ -289,16 +291,18 @@ __device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t ne
     }
 }
 
+template <bool kSmemItems>
 __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
     extern __shared__ __align__(16) uint32_t dyn[];
     __shared__ Small sm;
     Shared s;
-    s.sx = dyn;
-    s.snu = dyn + a.B;
-    s.smask = dyn + 2 * a.B;
-    s.sinfo = dyn + 3 * a.B;
-    s.pre = dyn + 4 * a.B;
-    s.fin = dyn + 5 * a.B;
+    uint32_t* const items_base = kSmemItems ? dyn : a.gitems;
+    s.sx = items_base;
+    s.snu = items_base + a.B;
+    s.smask = items_base + 2 * a.B;
+    s.sinfo = items_base + 3 * a.B;
+    s.pre = items_base + 4 * a.B;
+    s.fin = items_base + 5 * a.B;
     const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t N = a.N, b = a.b;
     const uint32_t lt = lanemask_lt();
@@ -575,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
             // ------------ F: pre-balance lists [hits in batch order][fetches]
             for (uint32_t j = j0 + lane; j < j1; j += 32) {
                 const uint32_t v = s.sinfo[j];
-                if (v >= kFetch - kMaxB) {
+                if (v >= kFetch - 65536u) {
                     const uint32_t f = sm.wfet[w] + (kFetch - v);
                     // node with free_pre[k] <= f < free_pre[k+1]
                     uint32_t k = 0;
@@ -818,7 +822,7 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     if (dm.N > kMaxN)
         return set_error(kCapability, "plan: device planner supports num_nodes <= 32 in this build");
     if (dm.B > kMaxB)
-        return set_error(kCapability, "plan: device planner supports global batch <= 8192 in this build");
+        return set_error(kCapability, "plan: device planner supports global batch <= 16384 in this build");
     if (dm.T >= 0xFFFFFFF0ull) return set_error(kCapability, "plan: too many steps");
     Scratch sc(st);
     const size_t EK = size_t(dm.E) * dm.keep;
@@ -862,6 +866,7 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     // sorted batches
     uint32_t P2 = 1;
     while (P2 < dm.B) P2 <<= 1;
+    LSG_CUDA(cudaFuncSetAttribute(k_sort_batches, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P2 * 4)));
     k_sort_batches<<<uint32_t(dm.T), 1024, P2 * 4, st>>>(d_trace, d_order, uint32_t(dm.keep),
                                                           uint32_t(dm.S), uint32_t(dm.B), P2, sb);
     LSG_LAUNCH_CHECK("k_sort_batches");
@@ -874,12 +879,19 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.fb = d_fb;
     a.fa = d_fa;
     a.status = d_status;
+    const bool smem_items = dm.B <= kMaxSmemB;
+    a.gitems = smem_items ? nullptr : sc.get<uint32_t>(size_t(6) * dm.B);
+    if (!smem_items && !a.gitems) return set_error(kInternal, "plan: scratch allocation failed");
     a.prof = profiling() ? sc.get<unsigned long long>(16 + 256) : nullptr;
     a.dbg_skip = std::getenv("LSG_DEBUG_SKIP") ? std::atoi(std::getenv("LSG_DEBUG_SKIP")) : 0;
     if (a.prof) LSG_CUDA(cudaMemsetAsync(a.prof, 0, (16 + 256) * 8, st));
-    const size_t smem = size_t(6) * dm.B * 4;
-    LSG_CUDA(cudaFuncSetAttribute(k_plan_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k_plan_loop<<<1, kThreads, smem, st>>>(a);
+    if (smem_items) {
+        const size_t smem = size_t(6) * dm.B * 4;
+        LSG_CUDA(cudaFuncSetAttribute(k_plan_loop<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_plan_loop<true><<<1, kThreads, smem, st>>>(a);
+    } else {
+        k_plan_loop<false><<<1, kThreads, 0, st>>>(a);
+    }
     LSG_LAUNCH_CHECK("k_plan_loop");
     if (a.prof) {
         unsigned long long h[16 + 256];

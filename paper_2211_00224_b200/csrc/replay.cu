@@ -25,7 +25,7 @@ namespace lsg {
 namespace {
 
 constexpr int kRT = 256;  // threads per node CTA
-constexpr uint32_t kRMaxList = 8192;
+constexpr uint32_t kRMaxList = 32768;  // longest node list of one step
 
 __device__ __forceinline__ uint32_t lanemask_lt_r() {
     uint32_t m;
@@ -353,8 +353,7 @@ __global__ void __launch_bounds__(kRT) k_replay(ReplayArgs a) {
                                 uint32_t s;
                                 if (rank < nf) s = fs[nf - 1 - rank];
                                 else s = fr + (rank - nf);
-                                slotk[x] = s;
-                                a.slot_out[base + i] = s;
+                                slotk[x] = s;  // reported at the end of the step
                             }
                             __syncwarp();
                             if (lane == 0) {
@@ -370,6 +369,16 @@ __global__ void __launch_bounds__(kRT) k_replay(ReplayArgs a) {
                 __syncthreads();
             }
         }
+        // misses report the slot they hold at the END of the step: one that
+        // a later run of the same step evicted again is a bypass (its slot may
+        // already belong to another miss of this step)
+        if (a.slot_out)
+            for (uint32_t i = tid; i < L; i += kRT) {
+                const uint32_t v = sx[i];
+                if (v & kHit) continue;
+                const uint32_t x = v & ~kHit;
+                a.slot_out[base + i] = __ldcg(&keyk[x]) != kNone ? slotk[x] : kNever;
+            }
         __syncthreads();
     }
 }
@@ -387,21 +396,24 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     LSG_LAUNCH_CHECK("k_step_bases");
     uint64_t total = 0, B = 0;
     LSG_CUDA(cudaMemcpyAsync(&total, gb + T, 8, cudaMemcpyDeviceToHost, st));
-    LSG_CUDA(cudaStreamSynchronize(st));
-    // B = the step stride of the position keys: max list length over steps
-    // is bounded by the step length, so use the longest step.
     {
-        // key stride = the longest step (a node list never exceeds its step)
-        uint64_t* hgb = nullptr;
-        LSG_CUDA(cudaMallocHost(&hgb, (T + 1) * 8));
-        LSG_CUDA(cudaMemcpyAsync(hgb, gb, (T + 1) * 8, cudaMemcpyDeviceToHost, st));
+        // key stride = the longest node list of any step (keys are g*B + i)
+        uint32_t* hoff = nullptr;
+        const size_t nb = size_t(T) * (N + 1) * 4;
+        LSG_CUDA(cudaMallocHost(&hoff, nb));
+        LSG_CUDA(cudaMemcpyAsync(hoff, d_node_off, nb, cudaMemcpyDeviceToHost, st));
         LSG_CUDA(cudaStreamSynchronize(st));
-        for (uint64_t g = 0; g < T; ++g) B = std::max<uint64_t>(B, hgb[g + 1] - hgb[g]);
-        cudaFreeHost(hgb);
+        for (uint64_t g = 0; g < T; ++g)
+            for (uint32_t k = 0; k < N; ++k) {
+                const uint32_t* o = hoff + g * (N + 1);
+                if (o[k + 1] < o[k]) { cudaFreeHost(hoff); return set_error(kValidation, "simulate: node offsets not ascending"); }
+                B = std::max<uint64_t>(B, o[k + 1] - o[k]);
+            }
+        cudaFreeHost(hoff);
     }
     if (B == 0) B = 1;
     if (T * B >= 0xFFFFFFF0ull) return set_error(kCapability, "simulate: plan too large for 32-bit position keys");
-    if (B > kRMaxList) return set_error(kCapability, "simulate: step longer than 8192 samples");
+    if (B > kRMaxList) return set_error(kCapability, "simulate: node list longer than 32768 samples");
     ReplayArgs a{};
     a.T = uint32_t(T);
     a.N = N;

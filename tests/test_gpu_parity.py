@@ -199,3 +199,16 @@ def test_plan_errors(ls):
         ls.plan_schedule(to_pc(ls, O.Cfg(64, 2, 2, 4, buffer_capacity=0)))
     with pytest.raises(ls.ConfigError):
         ls.plan_schedule(to_pc(ls, O.Cfg(4, 2, 2, 4, buffer_capacity=3)))
+
+
+@pytest.mark.parametrize("D,E,N,b,frac,seed", [(65536, 3, 32, 512, 0.5 / 32, 1), (40000, 4, 16, 1000, 0.03, 2),
+                                               (32768 + 777, 3, 32, 300, 0.02, 3)])
+def test_plan_large_global_batch(ls, D, E, N, b, frac, seed):
+    """global batch > 8192: per-item arrays in L2-resident global scratch
+    (cfg5's 32-rank shape, b=512 -> B=16384)."""
+    c = O.Cfg(D, E, N, b, seed=seed, buffer_capacity=max(1, int(frac * D)), pso_iters=30,
+              drop_last=seed != 3)
+    out, ref = check_plan(ls, c)
+    sim = ls.simulate_plan(out.plan, c.buffer_capacity)
+    h, m = O.simulate(ref.items, ref.node_off, N, D, c.buffer_capacity)
+    assert np.array_equal(u32(sim.hits), h) and np.array_equal(u32(sim.misses), m)
