@@ -100,6 +100,33 @@ __global__ void __launch_bounds__(1024) k_sort_batches(const uint32_t* __restric
     for (uint32_t r = threadIdx.x; r < len; r += blockDim.x) out[r] = sk[len - 1 - r];
 }
 
+// Rank of x inside the descending-sorted batch of its next-use step (binary
+// search of the step's sorted row); kNone for kNeverUsed. The eviction buckets
+// index residents by this rank, so rank order == the reference's tie order.
+__global__ void k_nextrank(const uint32_t* __restrict__ trace, const uint32_t* __restrict__ order,
+                           const uint32_t* __restrict__ nu, const uint32_t* __restrict__ sb,
+                           uint32_t E, uint32_t keep, uint32_t S, uint32_t B,
+                           uint32_t* __restrict__ nr) {
+    const uint32_t i = blockIdx.y;
+    const uint32_t* row = trace + size_t(order[i]) * keep;
+    for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < keep; pos += gridDim.x * blockDim.x) {
+        const uint32_t v = nu[size_t(i) * keep + pos];
+        uint32_t r = kNone;
+        if (v != kNever) {
+            const uint32_t x = row[pos];
+            const uint32_t gi = v / S, gt = v % S, lo = gt * B, blen = min(B, keep - lo);
+            const uint32_t* cand = sb + size_t(gi) * keep + lo;
+            uint32_t a0 = 0, a1 = blen;  // first index with cand[idx] <= x (descending)
+            while (a0 < a1) {
+                const uint32_t mid = (a0 + a1) >> 1;
+                if (cand[mid] > x) a0 = mid + 1; else a1 = mid;
+            }
+            r = a0;
+        }
+        nr[size_t(i) * keep + pos] = r;
+    }
+}
+
 // ----------------------------------------------------------------- K6 ----
 struct LoopArgs {
     uint32_t D, N, b, B, S, E, keep, T, C;
@@ -110,6 +137,10 @@ struct LoopArgs {
     const uint32_t* order;           // [E]
     const uint32_t* nu;              // [E*keep] execution order
     const uint32_t* sb;              // [E*keep] execution order, desc per step
+    const uint32_t* nr;              // [E*keep] rank of the access's id in sb of its next use
+    uint32_t* rk;                    // [N][D] rank of a resident's id inside its key's batch
+    uint32_t* bm;                    // [N][T][BW] bucket membership bitmaps over ranks
+    uint32_t BW;                     // words per bucket bitmap (ceil(B/32))
     uint32_t* key;                   // [N][D]
     uint32_t* hm;                    // [D] holder masks
     uint32_t* nz;                    // [N][nzw]
@@ -174,8 +205,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // buffer.cpp:37-41 (re-key) / :42-46 (insert) without the eviction: key
 // update plus the bucket / never-used summaries.
 __device__ __forceinline__ void set_key(const LoopArgs& a, Small& sm, uint32_t k, uint32_t x,
-                                        uint32_t nu) {
+                                        uint32_t nu, uint32_t rank) {
     a.key[size_t(k) * a.D + x] = nu;
+    a.rk[size_t(k) * a.D + x] = rank;
+    if (nu != kNever)
+        atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
     if (nu == kNever) {
         atomicOr(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
         atomicAdd(&sm.infcnt[k], 1u);
@@ -192,7 +226,8 @@ __device__ __forceinline__ void drop(const LoopArgs& a, uint32_t k, uint32_t x) 
 }
 
 // Remove the `need` largest (key, id) residents of node k. Whole warp.
-__device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t need, uint32_t lane) {
+__device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t need, uint32_t lane,
+                           uint32_t g) {
     const uint32_t lt = lanemask_lt();
     while (need > 0) {
         if (sm.infcnt[k] > 0) {  // kNeverUsed bucket: ids descending
@@ -252,40 +287,56 @@ __device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t ne
             if (lane == 0) atomicOr(a.status, 4u);
             return;
         }
-        // scan the step-beta batch (desc ids) for members key == beta
+        // take members of bucket beta in rank order (rank 0 = largest id):
+        // future buckets are exact (an entry goes stale only once its step is
+        // reached, and evictions clear their own bits); a past bucket (only
+        // reached when nothing has a future use) is validated against key/rank.
         const uint32_t gi = uint32_t(beta) / a.S, gt = uint32_t(beta) % a.S;
         const uint32_t lo = gt * a.B, blen = min(a.B, a.keep - lo);
         const uint32_t* cand = a.sb + size_t(gi) * a.keep + lo;
-        const uint32_t* keyk = a.key + size_t(k) * a.D;
-        uint32_t c = 0;
-        for (; c < blen && need > 0; c += 128) {
-            uint32_t xs[4];
-            bool mem[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t r = c + 32 * u + lane;
-                xs[u] = r < blen ? cand[r] : 0u;
+        uint32_t* bw = a.bm + (size_t(k) * a.T + uint32_t(beta)) * a.BW;
+        const bool past = uint32_t(beta) <= g;
+        const uint32_t nwords = (blen + 31) >> 5;
+        bool left = false;  // members remain in the scanned words
+        uint32_t w0 = 0;
+        for (; w0 < nwords && need > 0; w0 += 32) {
+            const uint32_t wi2 = w0 + lane;
+            uint32_t word = wi2 < nwords ? __ldcg(&bw[wi2]) : 0u;
+            if (past && word) {  // drop stale bits
+                uint32_t m = word;
+                while (m) {
+                    const uint32_t bit = __ffs(m) - 1;
+                    m &= m - 1;
+                    const uint32_t x = cand[wi2 * 32 + bit];
+                    if (__ldcg(&a.key[size_t(k) * a.D + x]) != uint32_t(beta) ||
+                        __ldcg(&a.rk[size_t(k) * a.D + x]) != wi2 * 32 + bit)
+                        word &= ~(1u << bit);
+                }
             }
+            const uint32_t cnt = __popc(word);
+            uint32_t inc = cnt;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t r = c + 32 * u + lane;
-                mem[u] = r < blen && __ldcg(&keyk[xs[u]]) == uint32_t(beta);
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                if (lane >= uint32_t(d)) inc += o;
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, mem[u]);
-                const uint32_t rank = __popc(bal & lt);
-                if (mem[u] && rank < need) drop(a, k, xs[u]);
-                const uint32_t took = min(uint32_t(__popc(bal)), need);
-                need -= took;
-                if (lane == 0) sm.bsize[k] -= took;
+            const uint32_t before = inc - cnt, total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+            const uint32_t take = before < need ? min(cnt, need - before) : 0u;
+            uint32_t rest = word;
+            for (uint32_t t2 = 0; t2 < take; ++t2) {
+                const uint32_t bit = __ffs(rest) - 1;
+                rest &= rest - 1;
+                drop(a, k, cand[wi2 * 32 + bit]);
             }
+            if (wi2 < nwords && (rest != word || past)) bw[wi2] = rest;
+            left = left || (__ballot_sync(0xFFFFFFFFu, rest != 0) != 0);
+            const uint32_t took = min(total, need);
+            need -= took;
+            if (lane == 0) sm.bsize[k] -= took;
         }
         __syncwarp();
-        if (c >= blen && need > 0) {
-            // whole bucket scanned and exhausted: it is empty now
-            if (lane == 0) atomicAnd(&nzk[beta >> 5], ~(1u << (beta & 31)));
-        }
+        // every word scanned and nothing left: the bucket is empty now
+        if (w0 >= nwords && !left && lane == 0) atomicAnd(&nzk[beta >> 5], ~(1u << (beta & 31)));
         if (lane == 0) sm.top[k] = uint32_t(beta);
         __syncwarp();
     }
@@ -327,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         const uint32_t lo = t * a.B, len = min(a.B, a.keep - lo);
         const uint32_t* row = a.trace + size_t(a.order[i]) * a.keep + lo;
         const uint32_t* nurow = a.nu + size_t(i) * a.keep + lo;
+        const uint32_t* nrrow = a.nr + size_t(i) * a.keep + lo;
         const uint32_t R = ((len + kThreads - 1) / kThreads) * 32;  // items per warp
         const uint32_t j0 = w * R, j1 = min(j0 + R, len);
 
@@ -736,13 +788,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 const uint32_t e = s.fin[p];
                 if (!(e & kHit)) continue;
                 const uint32_t j = e & 0xFFFF, k = (e >> 16) & 0xFF;
-                const uint32_t x = s.sx[j], nu = s.snu[j];
+                const uint32_t x = s.sx[j], nu = s.snu[j], rank = nrrow[j];
                 const uint32_t wd = nu >> 5;
                 if (nu != kNever && wd >= wbase && wd - wbase < kWinWords) {
                     a.key[size_t(k) * a.D + x] = nu;
+                    a.rk[size_t(k) * a.D + x] = rank;
+                    atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
                     atomicOr(&sm.win[k][wd - wbase], 1u << (nu & 31));
                 } else {
-                    set_key(a, sm, k, x, nu);
+                    set_key(a, sm, k, x, nu, rank);
                 }
             }
             __syncthreads();
@@ -783,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     const bool mine = (run >> lane) & 1u;
                     if (mine) {
                         const uint32_t x = s.sx[j];
-                        set_key(a, sm, k, x, s.snu[j]);
+                        set_key(a, sm, k, x, s.snu[j], nrrow[j]);
                         if (!hitrun) atomicOr(&a.hm[x], 1u << k);
                     }
                     __syncwarp();
@@ -796,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                         }
                         need = __shfl_sync(0xFFFFFFFFu, need, 0);
                         __syncwarp();
-                        if (need) evict_walk(a, sm, k, need, lane);
+                        if (need) evict_walk(a, sm, k, need, lane, g);
                     }
                     __syncwarp();
                     done |= run;
@@ -828,6 +882,7 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     const size_t EK = size_t(dm.E) * dm.keep;
     uint32_t* nu = sc.get<uint32_t>(EK);
     uint32_t* sb = sc.get<uint32_t>(EK);
+    uint32_t* nr = sc.get<uint32_t>(EK);
     LoopArgs a{};
     a.D = uint32_t(dm.D);
     a.N = dm.N;
@@ -843,6 +898,9 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.nzw = uint32_t((dm.T + 31) / 32 + 1);
     a.infw = uint32_t((dm.D + 31) / 32);
     a.key = sc.get<uint32_t>(size_t(dm.N) * dm.D);
+    a.rk = sc.get<uint32_t>(size_t(dm.N) * dm.D);
+    a.BW = uint32_t((dm.B + 31) / 32);
+    a.bm = sc.get<uint32_t>(size_t(dm.N) * dm.T * a.BW);
     a.hm = sc.get<uint32_t>(dm.D);
     a.nz = sc.get<uint32_t>(size_t(dm.N) * a.nzw);
     a.infbm = sc.get<uint32_t>(size_t(dm.N) * a.infw);
@@ -852,12 +910,13 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.mres = sc.get<uint32_t>(dm.B);
     a.mv = sc.get<uint32_t>(dm.B);
     a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B);
-    if (!nu || !sb || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.mpos || !a.mres ||
+    if (!nu || !sb || !nr || !a.rk || !a.bm || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.mpos || !a.mres ||
         !a.mv || !a.dmoves)
         return set_error(kInternal, "plan: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(dm.N) * dm.D * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.hm, 0, dm.D * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.nz, 0, size_t(dm.N) * a.nzw * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.bm, 0, size_t(dm.N) * dm.T * a.BW * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.infbm, 0, size_t(dm.N) * a.infw * 4, st));
     // K5
     k_nextuse<<<dim3(grid_for(dm.keep, 256, 1024), dm.E), 256, 0, st>>>(
@@ -872,8 +931,12 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     LSG_LAUNCH_CHECK("k_sort_batches");
     a.trace = d_trace;
     a.order = d_order;
+    k_nextrank<<<dim3(grid_for(dm.keep, 256, 1024), dm.E), 256, 0, st>>>(
+        d_trace, d_order, nu, sb, dm.E, uint32_t(dm.keep), uint32_t(dm.S), uint32_t(dm.B), nr);
+    LSG_LAUNCH_CHECK("k_nextrank");
     a.nu = nu;
     a.sb = sb;
+    a.nr = nr;
     a.items = d_items;
     a.node_off = d_node_off;
     a.fb = d_fb;
