@@ -813,6 +813,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         LSG_PHASE(6)
         for (uint32_t k = w; k < N; k += kWarps) {
             const uint32_t begin = sm.noff[k] + (a.remap ? sm.size[k] : 0u), end = sm.noff[k + 1];
+            // a miss run may span chunks: insert as we go, evict once when the
+            // run ends (before the next hit run, or at the end of the list)
+            bool pending = false;
+            auto flush = [&]() {
+                uint32_t need = 0;
+                if (lane == 0) need = sm.bsize[k] > a.C ? sm.bsize[k] - a.C : 0u;
+                need = __shfl_sync(0xFFFFFFFFu, need, 0);
+                __syncwarp();
+                if (need) evict_walk(a, sm, k, need, lane, g);
+                __syncwarp();
+                pending = false;
+            };
             for (uint32_t c = begin; c < end; c += 32) {
                 const uint32_t p = c + lane;
                 const bool valid = p < end;
@@ -835,6 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     const uint32_t stop = after ? __ffs(after) - 1 : 32u;
                     const uint32_t run = (stop == 32 ? 0xFFFFFFFFu : ((1u << stop) - 1u)) & ~((1u << first) - 1u) & vbal;
                     const bool mine = (run >> lane) & 1u;
+                    if (hitrun && pending) flush();  // the miss run before it ends here
                     if (mine) {
                         const uint32_t x = s.sx[j];
                         set_key(a, sm, k, x, s.snu[j], nrrow[j]);
@@ -842,20 +855,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     }
                     __syncwarp();
                     if (!hitrun) {
-                        const uint32_t m = __popc(run);
-                        uint32_t need = 0;
-                        if (lane == 0) {
-                            sm.bsize[k] += m;
-                            need = sm.bsize[k] > a.C ? sm.bsize[k] - a.C : 0u;
-                        }
-                        need = __shfl_sync(0xFFFFFFFFu, need, 0);
-                        __syncwarp();
-                        if (need) evict_walk(a, sm, k, need, lane, g);
+                        if (lane == 0) sm.bsize[k] += __popc(run);
+                        pending = true;
                     }
                     __syncwarp();
                     done |= run;
                 }
             }
+            if (pending) flush();
         }
         __syncthreads();
         LSG_PHASE(7)
