@@ -2,30 +2,37 @@
 // buffer.cpp:183-247, with next_use_chain :103-112), bit-exact hits/misses
 // per (step, node), plus the HBM slot each access lands in (for K8).
 //
-// Each node's buffer is independent, so one CTA replays one node (ranks shard
-// across GPUs by node range). Keys are positions in the node's own flattened
-// sequence; the position of list item i at step g is encoded as g*B + i, which
-// orders exactly like the flattened position and needs no per-node prefix.
+// Each node's buffer is independent: one WARP replays one node (4 nodes per
+// CTA; ranks shard across GPUs by node range), so the per-run ordering below
+// costs warp syncs only and the node state lives in (warp-uniform) registers.
+// Keys are positions in the node's own flattened sequence, encoded g*L + i
+// (g = step, i = index in the node's step list, L = longest node list),
+// which orders exactly like the flattened position.
 //
 //  1. step bases (exclusive scan of step lengths), one block;
 //  2. backward pass per node: next-use key of every access from a per-node
-//     last-seen table, one step at a time, parallel inside the step; a
-//     (node, step) that repeats an id is detected here (the within-step
-//     batching below assumes ids are unique per (node, step), which every plan
-//     plan_schedule emits satisfies);
-//  3. forward replay per node: an item is a hit iff resident at step start;
-//     runs of hits re-key, runs of misses insert then evict the (size-C)+
-//     largest (key, id) — bucket = step of the next use, candidates = that
-//     step's list of this node in reverse (keys are unique positions, so no
-//     ties), kNeverUsed residents in an id bitmap scanned from the top.
+//     last-seen table, one step at a time, lane-parallel inside the step; a
+//     (node, step) that repeats an id is rejected (the batched replay below
+//     needs ids unique per (node, step), which every plan plan_schedule
+//     emits satisfies);
+//  3. forward replay per node: an item is a hit iff resident at step start
+//     (misses insert keys beyond the step, so no current-step resident is ever
+//     the eviction maximum); runs of hits re-key, runs of misses insert and
+//     evict the (size-C)+ largest keys once the run ends. Residents are
+//     indexed by (step of next use, list position) bitmaps. Every resident's
+//     key is in the future, and an eviction never needs more than the future
+//     residents, so the walk only meets exact buckets (a re-keyed hit leaves
+//     a stale bit in its current step, which is never reached). kNeverUsed
+//     residents sit in an id bitmap scanned from the top (ties by larger id,
+//     buffer.cpp:27-28).
 #include "common.cuh"
 
 namespace lsg {
 
 namespace {
 
-constexpr int kRT = 256;  // threads per node CTA
-constexpr uint32_t kRMaxList = 32768;  // longest node list of one step
+constexpr int kRWarps = 4;  // nodes per CTA
+constexpr uint32_t kRMaxList = 16384;
 
 __device__ __forceinline__ uint32_t lanemask_lt_r() {
     uint32_t m;
@@ -69,6 +76,311 @@ __global__ void __launch_bounds__(1024) k_step_bases(const uint32_t* __restrict_
 }
 
 struct ReplayArgs {
+    uint32_t T, N, D, L, C, k0, k1;
+    uint32_t nzw, infw, bw;  // words: per-node step bitmap, id bitmap, per-step list bitmap
+    const uint32_t* items;
+    const uint32_t* node_off;
+    const uint64_t* gb;
+    uint32_t* nuk;     // [total items] next-use key per access
+    uint32_t* last;    // [N][D]
+    uint32_t* key;     // [N][D]  kNone = not resident
+    uint32_t* slot;    // [N][D]
+    uint32_t* nz;      // [N][nzw] next-use steps that may hold residents
+    uint32_t* pbm;     // [N][T][bw] list positions per next-use step
+    uint32_t* infbm;   // [N][infw]
+    uint32_t* fstack;  // [N][C] freed slots (null when slots are not wanted)
+    uint32_t* hits;    // [T][N]
+    uint32_t* misses;  // [T][N]
+    uint32_t* slot_out;  // [total items] or null
+    uint32_t* status;
+};
+
+// backward pass: next-use key (g'*L + i') of every access on this node
+__global__ void __launch_bounds__(kRWarps * 32) k_replay_nextuse(ReplayArgs a) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t k = a.k0 + blockIdx.x * kRWarps + (threadIdx.x >> 5);
+    if (k >= a.k1) return;
+    uint32_t* last = a.last + size_t(k) * a.D;
+    for (int64_t g = int64_t(a.T) - 1; g >= 0; --g) {
+        const uint32_t* off = a.node_off + size_t(g) * (a.N + 1);
+        const uint32_t o = off[k], len = off[k + 1] - o;
+        const uint64_t base = a.gb[g] + o;
+        for (uint32_t i = lane; i < len; i += 32) {
+            const uint32_t x = a.items[base + i] & ~kHit;
+            const uint32_t v = __ldcg(&last[x]);
+            a.nuk[base + i] = v == kNone ? kNever : v;
+        }
+        __syncwarp();
+        const uint32_t here = uint32_t(g) * a.L;
+        for (uint32_t i = lane; i < len; i += 32) {
+            const uint32_t x = a.items[base + i] & ~kHit;
+            const uint32_t old = atomicExch(&last[x], here + i);
+            if (old != kNone && old / a.L == uint32_t(g)) atomicOr(a.status, 32u);  // repeat in step
+        }
+        __syncwarp();
+    }
+}
+
+// Warp-uniform node state (every lane holds the same values).
+struct NodeState {
+    uint32_t size, top, inftop, infcnt, fresh, nfree;
+};
+
+// Evict the `need` largest keys of node k (whole warp).
+__device__ void r_evict(const ReplayArgs& a, NodeState& ns, uint32_t k, uint32_t need, uint32_t lane,
+                        uint32_t lt) {
+    uint32_t* keyk = a.key + size_t(k) * a.D;
+    uint32_t* slotk = a.slot + size_t(k) * a.D;
+    uint32_t* fs = a.fstack ? a.fstack + size_t(k) * a.C : nullptr;
+    while (need > 0) {
+        if (ns.infcnt > 0) {  // never used again on this node: ids descending
+            uint32_t* bm = a.infbm + size_t(k) * a.infw;
+            int32_t wi = int32_t(ns.inftop);
+            bool found = false;
+            while (wi >= 0 && !found) {
+                const int32_t myw = wi - int32_t(lane);
+                const uint32_t v = myw >= 0 ? __ldcg(&bm[myw]) : 0u;
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+                if (bal) {
+                    const uint32_t src = __ffs(bal) - 1;
+                    const int32_t hw = wi - int32_t(src);
+                    const uint32_t word = __shfl_sync(0xFFFFFFFFu, v, src);
+                    const uint32_t take = min(uint32_t(__popc(word)), need);
+                    // lane t takes the t-th highest bit of the word
+                    uint32_t m = word, bit = 0;
+                    for (uint32_t t = 0; t <= lane && t < take; ++t) {
+                        bit = 31 - __clz(m);
+                        m &= ~(1u << bit);
+                    }
+                    uint32_t s = kNone;
+                    if (lane < take) {
+                        const uint32_t x = uint32_t(hw) * 32 + bit;
+                        keyk[x] = kNone;
+                        s = slotk[x];
+                        slotk[x] = kNone;
+                    }
+                    const bool push = lane < take && s != kNone && fs;
+                    const uint32_t sbal = __ballot_sync(0xFFFFFFFFu, push);
+                    if (push) fs[ns.nfree + __popc(sbal & lt)] = s;
+                    uint32_t rest = word;
+                    for (uint32_t t = 0; t < take; ++t) rest &= ~(1u << (31 - __clz(rest)));
+                    if (lane == 0) bm[hw] = rest;
+                    ns.nfree += __popc(sbal);
+                    ns.infcnt -= take;
+                    ns.size -= take;
+                    need -= take;
+                    ns.inftop = uint32_t(hw);
+                    found = true;
+                } else {
+                    wi -= 32;
+                }
+            }
+            __syncwarp();
+            if (!found) {
+                if (lane == 0) atomicOr(a.status, 2u);
+                ns.infcnt = 0;
+            }
+            continue;
+        }
+        uint32_t* nzk = a.nz + size_t(k) * a.nzw;
+        int32_t wi = int32_t(ns.top >> 5);
+        int32_t beta = -1;
+        while (wi >= 0) {
+            const int32_t myw = wi - int32_t(lane);
+            const uint32_t v = myw >= 0 ? __ldcg(&nzk[myw]) : 0u;
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
+            if (bal) {
+                const uint32_t src = __ffs(bal) - 1;
+                const uint32_t word = __shfl_sync(0xFFFFFFFFu, v, src);
+                beta = (wi - int32_t(src)) * 32 + (31 - __clz(word));
+                break;
+            }
+            wi -= 32;
+        }
+        if (beta < 0) {
+            if (lane == 0) atomicOr(a.status, 4u);
+            return;
+        }
+        const uint64_t lbase = a.gb[beta] + a.node_off[size_t(beta) * (a.N + 1) + k];
+        uint32_t* pw = a.pbm + (size_t(k) * a.T + uint32_t(beta)) * a.bw;
+        bool left = false;
+        int32_t w1 = int32_t(a.bw) - 1;
+        // positions descending: lane t of a group holds word (w1 - t)
+        for (; w1 >= 0 && need > 0; w1 -= 32) {
+            const int32_t myw = w1 - int32_t(lane);
+            const uint32_t word = myw >= 0 ? __ldcg(&pw[myw]) : 0u;
+            const uint32_t cnt = __popc(word);
+            uint32_t inc = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                if (lane >= uint32_t(d)) inc += o;
+            }
+            const uint32_t before = inc - cnt, total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+            const uint32_t take = before < need ? min(cnt, need - before) : 0u;
+            // freed slots, in eviction order (deterministic)
+            uint32_t rest = word, pushes = 0;
+            for (uint32_t t = 0; t < take; ++t) {
+                const uint32_t bit = 31 - __clz(rest);
+                rest &= ~(1u << bit);
+                const uint32_t x = a.items[lbase + uint32_t(myw) * 32 + bit] & ~kHit;
+                keyk[x] = kNone;
+                pushes += (fs && slotk[x] != kNone) ? 1u : 0u;
+            }
+            uint32_t pinc = pushes;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, pinc, d);
+                if (lane >= uint32_t(d)) pinc += o;
+            }
+            if (pushes) {
+                uint32_t r2 = word, q = ns.nfree + pinc - pushes;
+                for (uint32_t t = 0; t < take; ++t) {
+                    const uint32_t bit = 31 - __clz(r2);
+                    r2 &= ~(1u << bit);
+                    const uint32_t x = a.items[lbase + uint32_t(myw) * 32 + bit] & ~kHit;
+                    const uint32_t s = slotk[x];
+                    if (s != kNone) {
+                        fs[q++] = s;
+                        slotk[x] = kNone;
+                    }
+                }
+            }
+            ns.nfree += __shfl_sync(0xFFFFFFFFu, pinc, 31);
+            if (myw >= 0 && rest != word) pw[myw] = rest;
+            left = left || (__ballot_sync(0xFFFFFFFFu, rest != 0) != 0);
+            const uint32_t took = min(total, need);
+            need -= took;
+            ns.size -= took;
+        }
+        __syncwarp();
+        if (w1 < 0 && !left && lane == 0) atomicAnd(&nzk[beta >> 5], ~(1u << (beta & 31)));
+        ns.top = uint32_t(beta);
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kRWarps * 32) k_replay(ReplayArgs a) {
+    extern __shared__ __align__(16) uint32_t rdyn[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint32_t k = a.k0 + blockIdx.x * kRWarps + wib;
+    if (k >= a.k1) return;
+    const uint32_t lt = lanemask_lt_r();
+    uint32_t* sx = rdyn + size_t(wib) * a.L;  // this node's list: id | resident-at-start bit
+    uint32_t* keyk = a.key + size_t(k) * a.D;
+    uint32_t* slotk = a.slot + size_t(k) * a.D;
+    uint32_t* fs = a.fstack ? a.fstack + size_t(k) * a.C : nullptr;
+    uint32_t* nzk = a.nz + size_t(k) * a.nzw;
+    uint32_t* infk = a.infbm + size_t(k) * a.infw;
+    NodeState ns{0, 0, 0, 0, 0, 0};
+    for (uint32_t g = 0; g < a.T; ++g) {
+        const uint32_t* off = a.node_off + size_t(g) * (a.N + 1);
+        const uint32_t o = off[k], len = off[k + 1] - o;
+        const uint64_t base = a.gb[g] + o;
+        // load + residency at step start
+        uint32_t hitc = 0;
+        for (uint32_t i = lane; i < len; i += 32) {
+            const uint32_t x = a.items[base + i] & ~kHit;
+            const bool res = __ldcg(&keyk[x]) != kNone;
+            sx[i] = x | (res ? kHit : 0u);
+            if (a.slot_out && res) a.slot_out[base + i] = slotk[x] | kHit;
+            hitc += res;
+        }
+        hitc = __reduce_add_sync(0xFFFFFFFFu, hitc);
+        if (lane == 0) {
+            a.hits[size_t(g) * a.N + k] = hitc;
+            a.misses[size_t(g) * a.N + k] = len - hitc;
+        }
+        __syncwarp();
+        // runs in list order; a miss run may span chunks and is evicted once
+        bool pending = false;
+        uint32_t run0 = 0;
+        auto flush = [&](uint32_t run1) {
+            const uint32_t need = ns.size > a.C ? ns.size - a.C : 0u;
+            if (need) r_evict(a, ns, k, need, lane, lt);
+            __syncwarp();
+            if (fs) {  // survivors of the run take slots, in list order
+                for (uint32_t c = run0; c < run1; c += 32) {
+                    const uint32_t i = c + lane;
+                    bool surv = false;
+                    uint32_t x = 0;
+                    if (i < run1) {
+                        x = sx[i] & ~kHit;
+                        surv = __ldcg(&keyk[x]) != kNone;
+                    }
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, surv);
+                    const uint32_t rank = __popc(bal & lt);
+                    if (surv) slotk[x] = rank < ns.nfree ? fs[ns.nfree - 1 - rank] : ns.fresh + (rank - ns.nfree);
+                    const uint32_t n = __popc(bal);
+                    const uint32_t from_stack = min(n, ns.nfree);
+                    ns.nfree -= from_stack;
+                    ns.fresh += n - from_stack;
+                    __syncwarp();
+                }
+            }
+            pending = false;
+        };
+        for (uint32_t c = 0; c < len; c += 32) {
+            const uint32_t i = c + lane;
+            const bool valid = i < len;
+            const uint32_t v = valid ? sx[i] : 0u;
+            const uint32_t x = v & ~kHit;
+            const uint32_t nu = valid ? a.nuk[base + i] : kNever;
+            const uint32_t vbal = __ballot_sync(0xFFFFFFFFu, valid);
+            const uint32_t rbal = __ballot_sync(0xFFFFFFFFu, valid && (v & kHit));
+            uint32_t done = 0;
+            while (done != vbal) {
+                const uint32_t first = __ffs(vbal & ~done) - 1;
+                const bool hitrun = (rbal >> first) & 1u;
+                const uint32_t same = hitrun ? rbal : (vbal & ~rbal);
+                const uint32_t after = (~same) & vbal & ~((2u << first) - 1u);
+                const uint32_t stop = after ? __ffs(after) - 1 : 32u;
+                const uint32_t run = (stop == 32 ? 0xFFFFFFFFu : ((1u << stop) - 1u)) & ~((1u << first) - 1u) & vbal;
+                if (hitrun && pending) flush(c + first);
+                const bool mine = (run >> lane) & 1u;
+                const bool nev = mine && nu == kNever;
+                if (mine) {  // buffer.cpp:37-46 without the eviction
+                    keyk[x] = nu;
+                    if (nev) {
+                        atomicOr(&infk[x >> 5], 1u << (x & 31));
+                    } else {
+                        const uint32_t beta = nu / a.L, p = nu - beta * a.L;
+                        atomicOr(&a.pbm[(size_t(k) * a.T + beta) * a.bw + (p >> 5)], 1u << (p & 31));
+                        atomicOr(&nzk[beta >> 5], 1u << (beta & 31));
+                    }
+                }
+                const uint32_t nevb = __ballot_sync(0xFFFFFFFFu, nev);
+                ns.infcnt += __popc(nevb);
+                ns.inftop = max(ns.inftop, __reduce_max_sync(0xFFFFFFFFu, nev ? (x >> 5) : 0u));
+                ns.top = max(ns.top, __reduce_max_sync(0xFFFFFFFFu, (mine && !nev) ? nu / a.L : 0u));
+                if (!hitrun) {
+                    ns.size += __popc(run);
+                    if (!pending) run0 = c + first;
+                    pending = true;
+                }
+                __syncwarp();
+                done |= run;
+            }
+        }
+        if (pending) flush(len);
+        // misses report the slot they hold at the END of the step (one that a
+        // later run of the same step evicted again is a bypass)
+        if (a.slot_out)
+            for (uint32_t i = lane; i < len; i += 32) {
+                const uint32_t v = sx[i];
+                if (v & kHit) continue;
+                const uint32_t x = v & ~kHit;
+                a.slot_out[base + i] = __ldcg(&keyk[x]) != kNone ? slotk[x] : kNever;
+            }
+        __syncwarp();
+    }
+}
+
+// ---- long node lists (L > 128): one CTA per node, candidates of a bucket are
+// the node's list at that step scanned from its end (the round-1 design).
+constexpr int kRT = 256;
+
+struct ReplayArgsCta {
     uint32_t T, N, D, B, C, k0;
     uint32_t nzw, infw;
     const uint32_t* items;
@@ -88,7 +400,7 @@ struct ReplayArgs {
 };
 
 // backward pass: next-use key (g'*B + i') of every access on this node
-__global__ void __launch_bounds__(kRT) k_replay_nextuse(ReplayArgs a) {
+__global__ void __launch_bounds__(kRT) k_replay_nextuse_cta(ReplayArgsCta a) {
     const uint32_t k = a.k0 + blockIdx.x;
     uint32_t* last = a.last + size_t(k) * a.D;
     for (int64_t g = int64_t(a.T) - 1; g >= 0; --g) {
@@ -111,14 +423,14 @@ __global__ void __launch_bounds__(kRT) k_replay_nextuse(ReplayArgs a) {
     }
 }
 
-struct RShared {
+struct RSharedCta {
     uint32_t size, top, inftop, infcnt, fresh, nfree;
     uint32_t nruns;
     uint32_t hitcnt;
     uint32_t wsum[kRT / 32];
 };
 
-__device__ __forceinline__ void r_set_key(const ReplayArgs& a, RShared& sh, uint32_t k, uint32_t x,
+__device__ __forceinline__ void r_set_key_cta(const ReplayArgsCta& a, RSharedCta& sh, uint32_t k, uint32_t x,
                                           uint32_t nu) {
     a.key[size_t(k) * a.D + x] = nu;
     if (nu == kNever) {
@@ -133,7 +445,7 @@ __device__ __forceinline__ void r_set_key(const ReplayArgs& a, RShared& sh, uint
 }
 
 // evict the `need` largest keys of node k (warp 0)
-__device__ void r_evict(const ReplayArgs& a, RShared& sh, uint32_t k, uint32_t need, uint32_t lane) {
+__device__ void r_evict_cta(const ReplayArgsCta& a, RSharedCta& sh, uint32_t k, uint32_t need, uint32_t lane) {
     const uint32_t lt = lanemask_lt_r();
     uint32_t* keyk = a.key + size_t(k) * a.D;
     uint32_t* slotk = a.slot + size_t(k) * a.D;
@@ -250,8 +562,8 @@ __device__ void r_evict(const ReplayArgs& a, RShared& sh, uint32_t k, uint32_t n
 }
 
 // forward replay, one CTA per node
-__global__ void __launch_bounds__(kRT) k_replay(ReplayArgs a) {
-    __shared__ RShared sh;
+__global__ void __launch_bounds__(kRT) k_replay_cta(ReplayArgsCta a) {
+    __shared__ RSharedCta sh;
     extern __shared__ __align__(16) uint32_t rdyn[];
     uint32_t* sx = rdyn;                                       // [B] ids | resident bit
     uint16_t* rstart = reinterpret_cast<uint16_t*>(rdyn + a.B);  // [B+1] run starts
@@ -324,7 +636,7 @@ __global__ void __launch_bounds__(kRT) k_replay(ReplayArgs a) {
             const uint32_t r0 = rstart[r], r1 = rstart[r + 1];
             const bool hitrun = sx[r0] & kHit;
             for (uint32_t i = r0 + tid; i < r1; i += kRT)
-                r_set_key(a, sh, k, sx[i] & ~kHit, a.nuk[base + i]);
+                r_set_key_cta(a, sh, k, sx[i] & ~kHit, a.nuk[base + i]);
             __syncthreads();
             if (!hitrun) {
                 if (w == 0) {
@@ -334,7 +646,7 @@ __global__ void __launch_bounds__(kRT) k_replay(ReplayArgs a) {
                         need = sh.size > a.C ? sh.size - a.C : 0u;
                     }
                     need = __shfl_sync(0xFFFFFFFFu, need, 0);
-                    if (need) r_evict(a, sh, k, need, lane);
+                    if (need) r_evict_cta(a, sh, k, need, lane);
                     __syncwarp();
                     // survivors of the run take slots, in list order
                     if (a.slot_out) {
@@ -394,10 +706,10 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     if (!gb) return set_error(kInternal, "simulate: scratch allocation failed");
     k_step_bases<<<1, 1024, 0, st>>>(d_node_off, uint32_t(T), N, gb);
     LSG_LAUNCH_CHECK("k_step_bases");
-    uint64_t total = 0, B = 0;
+    uint64_t total = 0, L = 0;
     LSG_CUDA(cudaMemcpyAsync(&total, gb + T, 8, cudaMemcpyDeviceToHost, st));
     {
-        // key stride = the longest node list of any step (keys are g*B + i)
+        // key stride = the longest node list of any step (keys are g*L + i)
         uint32_t* hoff = nullptr;
         const size_t nb = size_t(T) * (N + 1) * 4;
         LSG_CUDA(cudaMallocHost(&hoff, nb));
@@ -406,52 +718,75 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         for (uint64_t g = 0; g < T; ++g)
             for (uint32_t k = 0; k < N; ++k) {
                 const uint32_t* o = hoff + g * (N + 1);
-                if (o[k + 1] < o[k]) { cudaFreeHost(hoff); return set_error(kValidation, "simulate: node offsets not ascending"); }
-                B = std::max<uint64_t>(B, o[k + 1] - o[k]);
+                if (o[k + 1] < o[k]) {
+                    cudaFreeHost(hoff);
+                    return set_error(kValidation, "simulate: node offsets not ascending");
+                }
+                L = std::max<uint64_t>(L, o[k + 1] - o[k]);
             }
         cudaFreeHost(hoff);
     }
-    if (B == 0) B = 1;
-    if (T * B >= 0xFFFFFFF0ull) return set_error(kCapability, "simulate: plan too large for 32-bit position keys");
-    if (B > kRMaxList) return set_error(kCapability, "simulate: node list longer than 32768 samples");
+    if (L == 0) L = 1;
+    if (T * L >= 0xFFFFFFF0ull) return set_error(kCapability, "simulate: plan too large for 32-bit position keys");
+    if (L > kRMaxList) return set_error(kCapability, "simulate: node list longer than 16384 samples");
     ReplayArgs a{};
     a.T = uint32_t(T);
     a.N = N;
     a.D = uint32_t(D);
-    a.B = uint32_t(B);
+    a.L = uint32_t(L);
     a.C = uint32_t(std::min<uint64_t>(C, 0xFFFFFFF0ull));
     a.k0 = k0;
+    a.k1 = k1;
     a.nzw = uint32_t((T + 31) / 32 + 1);
     a.infw = uint32_t((D + 31) / 32);
+    a.bw = uint32_t((L + 31) / 32);
     a.items = d_items;
     a.node_off = d_node_off;
     a.gb = gb;
-    const uint32_t nk = k1 - k0;
     // per-node state is indexed by absolute node id; allocate N rows
     a.nuk = sc.get<uint32_t>(total);
     a.last = sc.get<uint32_t>(size_t(N) * D);
     a.key = sc.get<uint32_t>(size_t(N) * D);
     a.slot = sc.get<uint32_t>(size_t(N) * D);
     a.nz = sc.get<uint32_t>(size_t(N) * a.nzw);
+    a.pbm = L > 128 ? nullptr : sc.get<uint32_t>(size_t(N) * T * a.bw);
     a.infbm = sc.get<uint32_t>(size_t(N) * a.infw);
     a.fstack = d_slot ? sc.get<uint32_t>(size_t(N) * std::min<uint64_t>(C, D)) : nullptr;
-    a.C = uint32_t(std::min<uint64_t>(C, 0xFFFFFFF0ull));
-    if (!a.nuk || !a.last || !a.key || !a.slot || !a.nz || !a.infbm || (d_slot && !a.fstack))
+    if (!a.nuk || !a.last || !a.key || !a.slot || !a.nz || (L <= 128 && !a.pbm) || !a.infbm || (d_slot && !a.fstack))
         return set_error(kInternal, "simulate: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.last, 0xFF, size_t(N) * D * 4, st));  // kNone = no later access
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(N) * D * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.slot, 0xFF, size_t(N) * D * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.nz, 0, size_t(N) * a.nzw * 4, st));
+    if (a.pbm) LSG_CUDA(cudaMemsetAsync(a.pbm, 0, size_t(N) * T * a.bw * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.infbm, 0, size_t(N) * a.infw * 4, st));
     a.hits = d_hits;
     a.misses = d_misses;
     a.slot_out = d_slot;
     a.status = d_status;
-    k_replay_nextuse<<<nk, kRT, 0, st>>>(a);
+    const uint32_t nk = k1 - k0;
+    if (L > 128) {  // long lists: a CTA per node
+        ReplayArgsCta c{};
+        c.T = a.T; c.N = N; c.D = a.D; c.B = a.L; c.C = a.C; c.k0 = k0;
+        c.nzw = a.nzw; c.infw = a.infw;
+        c.items = d_items; c.node_off = d_node_off; c.gb = gb;
+        c.nuk = a.nuk; c.last = a.last; c.key = a.key; c.slot = a.slot; c.nz = a.nz;
+        c.infbm = a.infbm; c.fstack = a.fstack; c.hits = d_hits; c.misses = d_misses;
+        c.slot_out = d_slot; c.status = d_status;
+        k_replay_nextuse_cta<<<nk, kRT, 0, st>>>(c);
+        LSG_LAUNCH_CHECK("k_replay_nextuse_cta");
+        const size_t smem = size_t(L) * 4 + (L + 2) * 2 + 16;
+        LSG_CUDA(cudaFuncSetAttribute(k_replay_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k_replay_cta<<<nk, kRT, smem, st>>>(c);
+        LSG_LAUNCH_CHECK("k_replay_cta");
+        return kOk;
+    }
+    const unsigned grid = (nk + kRWarps - 1) / kRWarps;
+    k_replay_nextuse<<<grid, kRWarps * 32, 0, st>>>(a);
     LSG_LAUNCH_CHECK("k_replay_nextuse");
-    const size_t smem = size_t(B) * 4 + (B + 2) * 2 + 16;
+    const size_t smem = size_t(kRWarps) * L * 4;
     LSG_CUDA(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k_replay<<<nk, kRT, smem, st>>>(a);
+    k_replay<<<grid, kRWarps * 32, smem, st>>>(a);
     LSG_LAUNCH_CHECK("k_replay");
     return kOk;
 }
