@@ -1,0 +1,210 @@
+// include/loadsched_gpu.hpp — C++ drop-in for the hot path of the reference
+// `loadsched` library (/root/reference/proj/include/loadsched), backed by the
+// sm_100a kernels through the C ABI (lsg.h).
+//
+// A caller of the reference keeps its code: the namespace, value types, field
+// names, function signatures and exception classes below follow the reference
+// API for the planner path (cited per declaration); results are bit-identical.
+// Everything is computed on the current CUDA device; inputs are uploaded and
+// outputs returned by value as the reference does. Out of this header (and out
+// of scope): text formats, Store files, the cost model,
+// chunk-read planning (StepPlan::reads stays empty), the LRU policy.
+#pragma once
+
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+namespace loadsched {
+
+// ---- errors.hpp:10-46 ----------------------------------------------------
+enum class ErrorClass { Config = 2, Validation = 3, Capability = 4, Calibration = 5, Storage = 6, Internal = 7 };
+
+class Error : public std::runtime_error {
+  public:
+    Error(ErrorClass c, const std::string& what) : std::runtime_error(what), cls_(c) {}
+    ErrorClass error_class() const { return cls_; }
+    int exit_code() const { return static_cast<int>(cls_); }
+
+  private:
+    ErrorClass cls_;
+};
+#define LOADSCHED_GPU_ERROR(Name, Cls)                                   \
+    struct Name : Error {                                                \
+        explicit Name(const std::string& w) : Error(ErrorClass::Cls, w) {} \
+    };
+LOADSCHED_GPU_ERROR(ConfigError, Config)
+LOADSCHED_GPU_ERROR(ValidationError, Validation)
+LOADSCHED_GPU_ERROR(CapabilityError, Capability)
+LOADSCHED_GPU_ERROR(StorageError, Storage)
+LOADSCHED_GPU_ERROR(InternalError, Internal)
+#undef LOADSCHED_GPU_ERROR
+
+using SampleId = std::uint64_t;  // trace.hpp:11 (device ids are 32-bit)
+using IdSet = std::unordered_set<SampleId>;
+
+// ---- trace.hpp:15-57 -------------------------------------------------------
+struct TraceConfig {
+    std::uint64_t dataset_size = 0;
+    std::uint32_t num_epochs = 0;
+    std::uint32_t num_nodes = 0;
+    std::uint64_t local_batch = 0;
+    std::uint64_t seed = 0;
+    bool drop_last = true;
+
+    std::uint64_t global_batch() const { return std::uint64_t(num_nodes) * local_batch; }
+    std::uint64_t steps_per_epoch() const;
+    void validate() const;
+};
+
+struct AccessTrace {
+    TraceConfig config;
+    std::vector<std::vector<SampleId>> epochs;
+    std::uint64_t epoch_length() const { return epochs.empty() ? 0 : epochs.front().size(); }
+};
+
+AccessTrace generate_trace(const TraceConfig& config);
+std::vector<SampleId> slice(const AccessTrace& trace, std::uint32_t epoch, std::uint64_t step,
+                            std::uint32_t node);
+std::vector<SampleId> global_batch(const AccessTrace& trace, std::uint32_t epoch, std::uint64_t step);
+
+// ---- reuse_graph.hpp:15-53 -------------------------------------------------
+enum class WindowMode { Global, PerNode };
+
+struct ReuseGraph {
+    std::uint32_t num_epochs = 0;
+    std::uint64_t buffer_size = 0;
+    WindowMode mode = WindowMode::Global;
+    std::vector<std::uint64_t> weights;  // row-major E x E
+    std::uint64_t weight(std::uint32_t u, std::uint32_t v) const { return weights[std::size_t(u) * num_epochs + v]; }
+};
+
+ReuseGraph build_reuse_graph(const AccessTrace& trace, std::uint64_t buffer_size, WindowMode mode);
+
+// ---- epoch_order.hpp:13-63 -------------------------------------------------
+struct EpochOrder {
+    std::vector<std::uint32_t> order;
+    std::uint64_t cost = 0;
+};
+
+struct PsoParams {
+    std::uint32_t swarm_size = 32;
+    std::uint32_t max_iters = 500;
+    double p_personal = 0.5;
+    double p_global = 0.5;
+    double inertia = 0.5;
+    double kick = 1.0;
+    std::uint32_t stagnation_limit = 100;
+    std::uint32_t restart_limit = 20;
+    std::uint64_t seed = 0;
+};
+
+struct PsoResult {
+    EpochOrder best;
+    std::vector<std::uint64_t> history;
+    std::uint32_t iterations = 0;
+};
+
+std::uint64_t path_cost(const ReuseGraph& graph, const std::vector<std::uint32_t>& order);
+PsoResult pso_order(const ReuseGraph& graph, const PsoParams& params);
+EpochOrder identity_order(const ReuseGraph& graph);
+
+// ---- plan.hpp:16-53 --------------------------------------------------------
+enum class Source { BufferHit, PfsFetch };
+
+struct Assigned {
+    SampleId id = 0;
+    Source source = Source::PfsFetch;
+    friend bool operator==(const Assigned&, const Assigned&) = default;
+};
+
+struct StepAssignment {
+    std::vector<std::vector<Assigned>> nodes;
+    std::vector<std::uint64_t> fetch_counts() const;
+    std::vector<SampleId> fetch_ids(std::uint32_t node) const;
+    std::uint64_t total_assigned() const;
+};
+
+struct Read {  // chunking.hpp:13-22 (present for layout; reads are not planned here)
+    enum class Kind { Single, Chunk };
+    Kind kind = Kind::Single;
+    SampleId start = 0, end = 0;
+};
+struct ChunkPlan {
+    std::vector<Read> reads;
+    std::uint64_t needed = 0, redundant = 0;
+};
+
+struct StepPlan {
+    StepAssignment assignment;
+    std::vector<std::uint64_t> fetches_before;
+    std::vector<std::uint64_t> fetches_after;
+    std::vector<ChunkPlan> reads;  // not produced by the device path
+};
+
+struct EpochPlan {
+    std::uint32_t epoch = 0;
+    std::vector<StepPlan> steps;
+};
+
+struct SchedulePlan {
+    std::uint64_t dataset_size = 0;
+    std::uint32_t num_nodes = 0;
+    std::uint64_t local_batch = 0;
+    std::uint64_t chunk_threshold = 0;
+    EpochOrder order;
+    std::vector<EpochPlan> epochs;
+};
+
+bool same_multiset(const StepAssignment& step, const std::vector<SampleId>& batch);
+
+// ---- buffer.hpp:16-118 (simulation results) --------------------------------
+enum class Policy { Clairvoyant, Lru };
+
+struct StepNodeStats {
+    std::uint32_t epoch = 0;
+    std::uint64_t step = 0;
+    std::uint32_t node = 0;
+    std::uint64_t hits = 0;
+    std::uint64_t misses = 0;
+};
+
+struct SimResult {
+    Policy policy = Policy::Clairvoyant;
+    std::vector<StepNodeStats> rows;
+    std::uint64_t total_hits = 0;
+    std::uint64_t total_misses = 0;
+};
+
+SimResult simulate_plan(const SchedulePlan& plan, std::uint64_t capacity, Policy policy,
+                        bool insert_redundant = false);
+
+// ---- config.hpp:17-36 / pipeline.hpp:17-27 ---------------------------------
+struct PipelineConfig {
+    TraceConfig trace;
+    std::uint64_t buffer_capacity = 0;
+    Policy policy = Policy::Clairvoyant;
+    WindowMode graph_mode = WindowMode::Global;
+    std::uint64_t chunk_threshold = 15;
+    bool chunk_insert_redundant = false;
+    PsoParams pso{};
+    bool optim_order = true;
+    bool optim_remap = true;
+    bool optim_balance = true;
+    bool optim_chunk = true;
+    void validate() const;
+};
+
+struct PlanOutput {
+    AccessTrace trace;
+    ReuseGraph graph;
+    std::optional<PsoResult> pso;
+    SchedulePlan plan;
+};
+
+PlanOutput plan_schedule(const PipelineConfig& config);
+
+}  // namespace loadsched

@@ -1,0 +1,354 @@
+// loadsched_gpu.cpp — the C++ `loadsched` API (include/loadsched_gpu.hpp) over
+// the lsg C ABI. Host code here only converts layouts (uint64 vectors <-> the
+// flat uint32 device layout), moves data, and maps status codes to the
+// reference's exception classes (errors.hpp:10-46); every computation on the
+// planner path runs in the CUDA library.
+#include "loadsched_gpu.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <numeric>
+
+#include "lsg.h"
+
+namespace loadsched {
+
+namespace {
+
+[[noreturn]] void throw_class(int rc, const std::string& msg) {
+    switch (rc) {
+        case 2: throw ConfigError(msg);
+        case 3: throw ValidationError(msg);
+        case 4: throw CapabilityError(msg);
+        case 6: throw StorageError(msg);
+        default: throw InternalError(msg);
+    }
+}
+
+void check(int rc) {
+    if (rc != 0) throw_class(rc, lsg_last_error());
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw InternalError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    explicit DevBuf(std::size_t n) { cuda_check(cudaMalloc(&p, std::max<std::size_t>(n, 1) * sizeof(T)), "cudaMalloc"); }
+    ~DevBuf() { cudaFree(p); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    void upload(const T* h, std::size_t n) { cuda_check(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice), "H2D"); }
+    void download(T* h, std::size_t n) const { cuda_check(cudaMemcpy(h, p, n * sizeof(T), cudaMemcpyDeviceToHost), "D2H"); }
+};
+
+lsg_config to_c(const PipelineConfig& c) {
+    lsg_config o{};
+    o.dataset_size = c.trace.dataset_size;
+    o.num_epochs = c.trace.num_epochs;
+    o.num_nodes = c.trace.num_nodes;
+    o.local_batch = c.trace.local_batch;
+    o.seed = c.trace.seed;
+    o.drop_last = c.trace.drop_last ? 1 : 0;
+    o.policy = c.policy == Policy::Clairvoyant ? 0 : 1;
+    o.buffer_capacity = c.buffer_capacity;
+    o.graph_mode = c.graph_mode == WindowMode::Global ? 0 : 1;
+    o.insert_redundant = c.chunk_insert_redundant ? 1 : 0;
+    o.chunk_threshold = c.chunk_threshold;
+    o.optim_order = c.optim_order;
+    o.optim_remap = c.optim_remap;
+    o.optim_balance = c.optim_balance;
+    o.optim_chunk = c.optim_chunk;
+    o.pso_swarm = c.pso.swarm_size;
+    o.pso_iters = c.pso.max_iters;
+    o.pso_stagnation = c.pso.stagnation_limit;
+    o.pso_restart = c.pso.restart_limit;
+    o.pso_p_personal = c.pso.p_personal;
+    o.pso_p_global = c.pso.p_global;
+    o.pso_inertia = c.pso.inertia;
+    o.pso_kick = c.pso.kick;
+    return o;
+}
+
+std::uint64_t keep_of(const TraceConfig& t) {
+    return t.drop_last ? t.steps_per_epoch() * t.global_batch() : t.dataset_size;
+}
+
+}  // namespace
+
+// trace.cpp:12-24 semantics
+std::uint64_t TraceConfig::steps_per_epoch() const {
+    const std::uint64_t B = global_batch();
+    if (B == 0) return 0;
+    return drop_last ? dataset_size / B : (dataset_size + B - 1) / B;
+}
+
+void TraceConfig::validate() const {
+    PipelineConfig p;
+    p.trace = *this;
+    p.buffer_capacity = 1;
+    const lsg_config c = to_c(p);
+    lsg_shape sh;
+    check(lsg_shape_of(&c, &sh));
+}
+
+void PipelineConfig::validate() const {
+    const lsg_config c = to_c(*this);
+    lsg_shape sh;
+    check(lsg_shape_of(&c, &sh));
+}
+
+AccessTrace generate_trace(const TraceConfig& config) {
+    PipelineConfig p;
+    p.trace = config;
+    p.buffer_capacity = 1;
+    const lsg_config c = to_c(p);
+    if (config.num_nodes == 0 || config.local_batch == 0 || config.num_epochs == 0 ||
+        config.dataset_size < config.global_batch())
+        check(lsg_generate_trace(&c, nullptr, nullptr));  // reports the ConfigError
+    const std::uint64_t keep = keep_of(config), E = config.num_epochs;
+    DevBuf<std::uint32_t> d(E * keep);
+    check(lsg_generate_trace(&c, d.p, nullptr));
+    std::vector<std::uint32_t> h(E * keep);
+    d.download(h.data(), h.size());
+    AccessTrace t;
+    t.config = config;
+    t.epochs.resize(E);
+    for (std::uint64_t e = 0; e < E; ++e) t.epochs[e].assign(h.begin() + e * keep, h.begin() + (e + 1) * keep);
+    return t;
+}
+
+// trace.cpp:45-70 (views of host data)
+std::vector<SampleId> slice(const AccessTrace& trace, std::uint32_t epoch, std::uint64_t step, std::uint32_t node) {
+    const TraceConfig& c = trace.config;
+    if (epoch >= trace.epochs.size()) throw ValidationError("slice: epoch out of range");
+    if (step >= c.steps_per_epoch()) throw ValidationError("slice: step out of range");
+    if (node >= c.num_nodes) throw ValidationError("slice: node out of range");
+    const auto& seq = trace.epochs[epoch];
+    const std::uint64_t lo = std::min<std::uint64_t>(step * c.global_batch() + std::uint64_t(node) * c.local_batch, seq.size());
+    const std::uint64_t hi = std::min<std::uint64_t>(lo + c.local_batch, seq.size());
+    return std::vector<SampleId>(seq.begin() + lo, seq.begin() + std::max(lo, hi));
+}
+
+std::vector<SampleId> global_batch(const AccessTrace& trace, std::uint32_t epoch, std::uint64_t step) {
+    const TraceConfig& c = trace.config;
+    if (epoch >= trace.epochs.size()) throw ValidationError("global_batch: epoch out of range");
+    if (step >= c.steps_per_epoch()) throw ValidationError("global_batch: step out of range");
+    const auto& seq = trace.epochs[epoch];
+    const std::uint64_t lo = std::min<std::uint64_t>(step * c.global_batch(), seq.size());
+    const std::uint64_t hi = std::min<std::uint64_t>(lo + c.global_batch(), seq.size());
+    return std::vector<SampleId>(seq.begin() + lo, seq.begin() + hi);
+}
+
+ReuseGraph build_reuse_graph(const AccessTrace& trace, std::uint64_t buffer_size, WindowMode mode) {
+    const std::uint32_t E = std::uint32_t(trace.epochs.size());
+    const std::uint64_t len = trace.epoch_length();
+    std::vector<std::uint32_t> flat(std::size_t(E) * len);
+    for (std::uint32_t e = 0; e < E; ++e) {
+        if (trace.epochs[e].size() != len) throw ValidationError("build_reuse_graph: ragged trace");
+        for (std::uint64_t i = 0; i < len; ++i) {
+            const SampleId x = trace.epochs[e][i];
+            if (x >= trace.config.dataset_size) throw ValidationError("build_reuse_graph: id out of range");
+            flat[std::size_t(e) * len + i] = std::uint32_t(x);
+        }
+    }
+    DevBuf<std::uint32_t> dt(flat.size());
+    dt.upload(flat.data(), flat.size());
+    DevBuf<std::uint64_t> dw(std::size_t(E) * E);
+    check(lsg_build_reuse_graph(dt.p, E, len, trace.config.dataset_size, trace.config.num_nodes,
+                                trace.config.local_batch, trace.config.drop_last ? 1 : 0, buffer_size,
+                                mode == WindowMode::Global ? 0 : 1, dw.p, nullptr));
+    ReuseGraph g;
+    g.num_epochs = E;
+    g.buffer_size = buffer_size;
+    g.mode = mode;
+    g.weights.resize(std::size_t(E) * E);
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    dw.download(g.weights.data(), g.weights.size());
+    return g;
+}
+
+// epoch_order.cpp:11-30
+std::uint64_t path_cost(const ReuseGraph& graph, const std::vector<std::uint32_t>& order) {
+    const std::uint32_t E = graph.num_epochs;
+    if (order.size() != E) throw ValidationError("path_cost: order length != num_epochs");
+    std::vector<bool> seen(E, false);
+    for (std::uint32_t v : order) {
+        if (v >= E || seen[v]) throw ValidationError("path_cost: order is not a permutation");
+        seen[v] = true;
+    }
+    std::uint64_t c = 0;
+    for (std::size_t i = 0; i + 1 < order.size(); ++i) c += graph.weight(order[i], order[i + 1]);
+    return c;
+}
+
+EpochOrder identity_order(const ReuseGraph& graph) {
+    EpochOrder r;
+    r.order.resize(graph.num_epochs);
+    std::iota(r.order.begin(), r.order.end(), 0u);
+    r.cost = path_cost(graph, r.order);
+    return r;
+}
+
+PsoResult pso_order(const ReuseGraph& graph, const PsoParams& p) {
+    const std::uint32_t E = graph.num_epochs;
+    if (E == 0) throw ValidationError("pso_order: empty graph");
+    DevBuf<std::uint64_t> dw(std::size_t(E) * E);
+    dw.upload(graph.weights.data(), graph.weights.size());
+    DevBuf<std::uint32_t> dord(E), diters(1);
+    DevBuf<std::uint64_t> dcost(1), dhist(p.max_iters);
+    check(lsg_pso_order(dw.p, E, p.swarm_size, p.max_iters, p.p_personal, p.p_global, p.inertia, p.kick,
+                        p.stagnation_limit, p.restart_limit, p.seed, dord.p, dcost.p, dhist.p, diters.p, nullptr));
+    PsoResult r;
+    r.best.order.resize(E);
+    dord.download(r.best.order.data(), E);
+    dcost.download(&r.best.cost, 1);
+    diters.download(&r.iterations, 1);
+    r.history.resize(r.iterations);
+    dhist.download(r.history.data(), r.iterations);
+    return r;
+}
+
+// plan.cpp:11-42
+std::vector<std::uint64_t> StepAssignment::fetch_counts() const {
+    std::vector<std::uint64_t> c(nodes.size(), 0);
+    for (std::size_t k = 0; k < nodes.size(); ++k)
+        for (const Assigned& a : nodes[k]) c[k] += a.source == Source::PfsFetch;
+    return c;
+}
+std::vector<SampleId> StepAssignment::fetch_ids(std::uint32_t node) const {
+    std::vector<SampleId> v;
+    for (const Assigned& a : nodes[node])
+        if (a.source == Source::PfsFetch) v.push_back(a.id);
+    return v;
+}
+std::uint64_t StepAssignment::total_assigned() const {
+    std::uint64_t n = 0;
+    for (const auto& l : nodes) n += l.size();
+    return n;
+}
+bool same_multiset(const StepAssignment& step, const std::vector<SampleId>& batch) {
+    std::vector<SampleId> got;
+    for (const auto& l : step.nodes)
+        for (const Assigned& a : l) got.push_back(a.id);
+    if (got.size() != batch.size()) return false;
+    std::vector<SampleId> want = batch;
+    std::sort(got.begin(), got.end());
+    std::sort(want.begin(), want.end());
+    return got == want;
+}
+
+PlanOutput plan_schedule(const PipelineConfig& config) {
+    const lsg_config c = to_c(config);
+    lsg_shape sh;
+    check(lsg_shape_of(&c, &sh));
+    const std::uint32_t E = config.trace.num_epochs, N = config.trace.num_nodes;
+    const std::uint64_t keep = sh.keep, S = sh.steps_per_epoch, T = sh.total_steps;
+    std::vector<std::uint32_t> trace(sh.total_items), order(E), items(sh.total_items), off(T * (N + 1)),
+        fb(T * N), fa(T * N);
+    std::vector<std::uint64_t> graph(std::size_t(E) * E), hist(config.pso.max_iters);
+    std::uint64_t cost = 0;
+    std::uint32_t iters = 0;
+    lsg_plan_out h{trace.data(), graph.data(), order.data(), &cost, hist.data(), &iters, items.data(),
+                   off.data(), fb.data(), fa.data()};
+    check(lsg_plan_host(&c, &h, nullptr));
+
+    PlanOutput out;
+    out.trace.config = config.trace;
+    out.trace.epochs.resize(E);
+    for (std::uint32_t e = 0; e < E; ++e)
+        out.trace.epochs[e].assign(trace.begin() + std::size_t(e) * keep, trace.begin() + std::size_t(e + 1) * keep);
+    out.graph.num_epochs = E;
+    out.graph.buffer_size = config.buffer_capacity;
+    out.graph.mode = config.graph_mode;
+    out.graph.weights = graph;
+    SchedulePlan& p = out.plan;
+    p.dataset_size = config.trace.dataset_size;
+    p.num_nodes = N;
+    p.local_batch = config.trace.local_batch;
+    p.chunk_threshold = config.optim_chunk ? config.chunk_threshold : 0;  // pipeline.cpp:52
+    p.order.order = order;
+    p.order.cost = cost;
+    if (config.optim_order) {
+        PsoResult r;
+        r.best = p.order;
+        r.history.assign(hist.begin(), hist.begin() + iters);
+        r.iterations = iters;
+        out.pso = r;
+    }
+    std::uint64_t base = 0;
+    for (std::uint32_t i = 0; i < E; ++i) {
+        EpochPlan ep;
+        ep.epoch = order[i];
+        for (std::uint64_t t = 0; t < S; ++t) {
+            const std::uint64_t g = std::uint64_t(i) * S + t;
+            const std::uint32_t* o = off.data() + g * (N + 1);
+            StepPlan st;
+            st.assignment.nodes.resize(N);
+            for (std::uint32_t k = 0; k < N; ++k) {
+                auto& list = st.assignment.nodes[k];
+                list.reserve(o[k + 1] - o[k]);
+                for (std::uint32_t q = o[k]; q < o[k + 1]; ++q) {
+                    const std::uint32_t v = items[base + q];
+                    list.push_back({SampleId(v & ~LSG_HIT_BIT), (v & LSG_HIT_BIT) ? Source::BufferHit : Source::PfsFetch});
+                }
+                st.fetches_before.push_back(fb[g * N + k]);
+                st.fetches_after.push_back(fa[g * N + k]);
+            }
+            base += o[N];
+            ep.steps.push_back(std::move(st));
+        }
+        p.epochs.push_back(std::move(ep));
+    }
+    return out;
+}
+
+SimResult simulate_plan(const SchedulePlan& plan, std::uint64_t capacity, Policy policy, bool insert_redundant) {
+    if (insert_redundant) throw CapabilityError("simulate_plan: insert_redundant is not on the device path");
+    const std::uint32_t N = plan.num_nodes;
+    std::vector<std::uint32_t> items, off;
+    std::uint64_t T = 0;
+    for (const EpochPlan& ep : plan.epochs)
+        for (const StepPlan& st : ep.steps) {
+            if (st.assignment.nodes.size() != N) throw ValidationError("simulate_plan: node count mismatch");
+            std::uint32_t o = 0;
+            for (const auto& list : st.assignment.nodes) {
+                off.push_back(o);
+                for (const Assigned& a : list) {
+                    if (a.id >= plan.dataset_size) throw ValidationError("simulate_plan: id out of range");
+                    items.push_back(std::uint32_t(a.id) | (a.source == Source::BufferHit ? LSG_HIT_BIT : 0u));
+                    ++o;
+                }
+            }
+            off.push_back(o);
+            ++T;
+        }
+    SimResult r;
+    r.policy = policy;
+    if (T == 0) return r;
+    DevBuf<std::uint32_t> di(items.size()), doff(off.size()), dh(T * N), dm(T * N);
+    di.upload(items.data(), items.size());
+    doff.upload(off.data(), off.size());
+    check(lsg_simulate(di.p, doff.p, T, N, plan.dataset_size, capacity, policy == Policy::Clairvoyant ? 0 : 1, 0, N,
+                       dh.p, dm.p, nullptr, nullptr));
+    std::vector<std::uint32_t> h(T * N), m(T * N);
+    dh.download(h.data(), h.size());
+    dm.download(m.data(), m.size());
+    std::uint64_t g = 0;
+    for (const EpochPlan& ep : plan.epochs)
+        for (std::size_t t = 0; t < ep.steps.size(); ++t, ++g)
+            for (std::uint32_t k = 0; k < N; ++k) {
+                r.rows.push_back({ep.epoch, t, k, h[g * N + k], m[g * N + k]});
+                r.total_hits += h[g * N + k];
+                r.total_misses += m[g * N + k];
+            }
+    return r;
+}
+
+}  // namespace loadsched
