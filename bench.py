@@ -40,6 +40,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "plan samples/s (shuffle+order+evict+assign); HBM-buffer gather GB/s; 1-8 GPU"
 CFG2 = dict(D=262144, E=100, N=8, b=512, C=52428, sample_bytes=256 * 256 * 4, seed=42, fill_seed=1)
+# cfg3 (CosmoFlow 128^3 x 4 fp16 = 16 MiB samples): b, E and C are unspecified
+# in BASELINE.json; SURVEY.md §8d chose b=8, E=10, C=8192 (128 GiB per rank)
+CFG3 = dict(D=65536, E=10, N=8, b=8, C=8192, sample_bytes=4 * 128 ** 3 * 2, seed=42, fill_seed=1)
+HBM_BUDGET = 150 * 2 ** 30  # bytes of sample buffers one GPU may hold
 E_SAMPLE = 3  # reference arm: epochs of the bounded CPU sample
 
 
@@ -161,6 +165,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--epochs", type=int, default=None, help="override E (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -175,20 +180,22 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    c = dict(CFG2)
+    c = dict(CFG2 if args.config == "cfg2" else CFG3)
     if args.epochs:
         c["E"] = args.epochs
     D, E, N, b, C, SB = c["D"], c["E"], c["N"], c["b"], c["C"], c["sample_bytes"]
     from paper_2211_00224_b200.parallel import combine_rows, rank_range
 
     k0, k1 = rank_range(N, world, rank)
+    # ranks whose HBM buffers fit on this GPU (cfg3: one 128 GiB buffer per GPU)
+    k1 = min(k1, k0 + max(1, HBM_BUDGET // (C * SB)))
     pc = ls.PipelineConfig(trace=ls.TraceConfig(D, E, N, b, c["seed"], True), buffer_capacity=C)
     sh = pc.shape()
     T, A = int(sh.total_steps), E * D
 
     # per-rank HBM sample buffers (C slots x 256 KiB) and batch tensors
     bufs = {k: torch.empty((C, SB), dtype=torch.uint8, device=dev) for k in range(k0, k1)}
-    maxlen = c["N"] * b  # a node list never exceeds its step
+    maxlen = min(c["N"] * b, 1024)  # node lists stay near b (checked below)
     outs = {k: torch.empty((maxlen, SB), dtype=torch.uint8, device=dev) for k in range(k0, k1)}
 
     fetcher = ls.StepFetcher([bufs[k] for k in range(k0, k1)], [outs[k] for k in range(k0, k1)],
@@ -212,6 +219,8 @@ def main():
         combine_rows(sim.hits, sim.misses)
         e[2].record(stream)
         off = plan.node_off.cpu().numpy() if not host else out.plan.node_off.numpy()
+        if int((off[:, k0 + 1:k1 + 1] - off[:, k0:k1]).max()) > maxlen:
+            raise SystemExit("a node list exceeds the batch tensor rows")
         bases = [0] * (T + 1)
         for g in range(T):
             bases[g + 1] = bases[g] + int(off[g, N])

@@ -219,7 +219,10 @@ int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* 
     const unsigned grid = unsigned(std::min<uint64_t>(rows * f.tiles_per_row, 148ull * 8));
     k_fetch_step_hits<<<grid, kGatherThreads, 0, st>>>(f);
     LSG_LAUNCH_CHECK("k_fetch_step_hits");
-    dim3 g2(unsigned(std::min<uint64_t>((f.vec_per_row + 255) / 256, 8)), 256);
+    // each miss row is spread over up to 256 blocks (a 16 MiB row is 1 Mi
+    // 16-byte pairs); rows are strided over grid.y
+    dim3 g2(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 256)),
+            unsigned(std::min<uint64_t>(std::max<uint64_t>(rows, 1), 1024)));
     k_fetch_step_misses<<<g2, 256, 0, st>>>(f);
     LSG_LAUNCH_CHECK("k_fetch_step_misses");
     return kOk;
