@@ -8,7 +8,7 @@
 // Everything is computed on the current CUDA device; inputs are uploaded and
 // outputs returned by value as the reference does. Out of this header (and out
 // of scope): text formats, Store files, the cost model,
-// chunk-read planning (StepPlan::reads stays empty), the LRU policy.
+// the LRU policy, chunk_insert_redundant.
 #pragma once
 
 #include <cstdint>
@@ -128,7 +128,7 @@ struct StepAssignment {
     std::uint64_t total_assigned() const;
 };
 
-struct Read {  // chunking.hpp:13-22 (present for layout; reads are not planned here)
+struct Read {  // chunking.hpp:13-22
     enum class Kind { Single, Chunk };
     Kind kind = Kind::Single;
     SampleId start = 0, end = 0;
@@ -142,7 +142,7 @@ struct StepPlan {
     StepAssignment assignment;
     std::vector<std::uint64_t> fetches_before;
     std::vector<std::uint64_t> fetches_after;
-    std::vector<ChunkPlan> reads;  // not produced by the device path
+    std::vector<ChunkPlan> reads;  // per node read plan (chunking.cpp / pipeline.cpp:83-88)
 };
 
 struct EpochPlan {

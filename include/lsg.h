@@ -74,6 +74,14 @@ typedef struct lsg_plan_out {
     uint32_t* node_off;     /* [T][N+1]   per-step list offsets */
     uint32_t* fetch_before; /* [T][N]     StepPlan.fetches_before */
     uint32_t* fetch_after;  /* [T][N]     StepPlan.fetches_after */
+    /* StepPlan.reads (pipeline.cpp:83-88): reads of list (g, k) at its item
+     * offsets, start == end for a Single read; counts and ChunkPlan.needed /
+     * .redundant per (g, k). NULL read_start skips chunk planning. */
+    uint32_t* read_start;   /* [E*keep] */
+    uint32_t* read_end;     /* [E*keep] */
+    uint32_t* read_count;   /* [T][N] */
+    uint32_t* read_needed;  /* [T][N] */
+    uint32_t* read_redundant; /* [T][N] */
 } lsg_plan_out;
 
 int lsg_version(void);

@@ -186,6 +186,7 @@ def lib() -> ctypes.CDLL:
         L.or_plan.argtypes = [ctypes.POINTER(OrConfig), P, P, P, P, P, P, P, P, P, P, P]
         L.or_simulate.argtypes = [P, P, u64, u32, u64, u64, i32, P, P]
         L.or_simulate_sequence.argtypes = [P, u64, u64, u64, i32, P]
+        L.or_plan_reads.argtypes = [P, P, u64, u32, i32, u64, P, P, P, P, P]
         L.or_store_payload.argtypes = [u64, u64, u64, P]
         L.or_store_payload.restype = None
         _lib = L
@@ -302,6 +303,19 @@ def simulate(items, node_off, N, D, C, policy="clairvoyant"):
     return hits, misses
 
 
+def plan_reads(items, node_off, N, chunked=True, threshold=15):
+    """chunking.cpp:9-33 / pipeline.cpp:21-28 reads of every (step, node) list."""
+    items = np.ascontiguousarray(items, dtype=np.uint32)
+    node_off = np.ascontiguousarray(node_off, dtype=np.uint32).reshape(-1, N + 1)
+    T = node_off.shape[0]
+    rs = np.zeros(max(items.size, 1), np.uint32)
+    re_ = np.zeros(max(items.size, 1), np.uint32)
+    cnt, need, red = (np.zeros((T, N), np.uint32) for _ in range(3))
+    _check(lib().or_plan_reads(_p(items), _p(node_off), T, N, int(chunked), threshold, _p(rs), _p(re_),
+                               _p(cnt), _p(need), _p(red)), "plan_reads")
+    return rs[: items.size], re_[: items.size], cnt, need, red
+
+
 def simulate_sequence(seq, C, policy="clairvoyant"):
     seq = np.ascontiguousarray(seq, dtype=np.uint32)
     D = int(seq.max()) + 1 if len(seq) else 1
@@ -344,6 +358,7 @@ def ref_plan(cfg: Cfg) -> PlanArrays:
             hits=rd("hits.u32", np.uint32).reshape(T, N),
             misses=rd("misses.u32", np.uint32).reshape(T, N),
             residency=np.fromfile(resp, dtype=np.uint64).reshape(T, N, 3) if os.path.exists(resp) else None,
+            extra={n: rd(n + ".u32", np.uint32) for n in ("rstart", "rend", "rcount", "rneed", "rred")},
         )
 
 

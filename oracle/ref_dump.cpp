@@ -87,6 +87,31 @@ void dump_plan(const std::string& dir, const SchedulePlan& plan) {
             }
         }
     }
+    // StepPlan::reads (chunking.cpp / pipeline.cpp:83-88) in the same layout:
+    // list (g, k)'s reads at its item offsets
+    std::vector<std::uint32_t> rstart(items.size(), 0), rend(items.size(), 0), rcount, rneed, rred;
+    std::size_t base = 0, g = 0;
+    for (const EpochPlan& ep : plan.epochs)
+        for (const StepPlan& st : ep.steps) {
+            for (std::uint32_t k = 0; k < N; ++k) {
+                const std::size_t lo = base + nodeoff[g * (N + 1) + k];
+                const ChunkPlan& cp = st.reads[k];
+                for (std::size_t r = 0; r < cp.reads.size(); ++r) {
+                    rstart[lo + r] = std::uint32_t(cp.reads[r].start);
+                    rend[lo + r] = std::uint32_t(cp.reads[r].end);
+                }
+                rcount.push_back(std::uint32_t(cp.reads.size()));
+                rneed.push_back(std::uint32_t(cp.needed));
+                rred.push_back(std::uint32_t(cp.redundant));
+            }
+            base += nodeoff[g * (N + 1) + N];
+            ++g;
+        }
+    dump(dir + "/rstart.u32", rstart);
+    dump(dir + "/rend.u32", rend);
+    dump(dir + "/rcount.u32", rcount);
+    dump(dir + "/rneed.u32", rneed);
+    dump(dir + "/rred.u32", rred);
     dump(dir + "/items.u32", items);
     dump(dir + "/nodeoff.u32", nodeoff);
     dump(dir + "/fb.u32", fb);

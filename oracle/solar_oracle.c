@@ -619,7 +619,7 @@ int or_plan(const or_config* c, uint32_t* trace, uint64_t* graph, uint32_t* orde
     }
     uint32_t* scratch = (uint32_t*)malloc((B + 1) * sizeof(uint32_t));
     uint32_t* fetch = (uint32_t*)malloc((B + 1) * sizeof(uint32_t));
-    uint32_t* red = NULL; uint64_t redcap = 0;
+    uint32_t* red = NULL;
     uint32_t** reds = (uint32_t**)calloc(N, sizeof(uint32_t*));
     uint64_t* nreds = (uint64_t*)calloc(N, sizeof(uint64_t));
     uint64_t* redcaps = (uint64_t*)calloc(N, sizeof(uint64_t));
@@ -782,4 +782,52 @@ void or_store_payload(uint64_t fill_seed, uint64_t offset, uint64_t n, uint8_t* 
         uint64_t word = mix64(fill_seed + (j / 8 + 1) * GAMMA);
         out[i] = (uint8_t)(word >> (8 * (j % 8)));
     }
+}
+
+/* ------------------------------------------------------------ chunking --- */
+/* chunking.cpp:9-33 (plan_chunks) and pipeline.cpp:21-28 (singles_plan) on
+ * each (step, node) fetch list of a finished plan. Reads of list (g, k) are
+ * written at that list's item offsets; counts/needed/redundant per (g, k). */
+int or_plan_reads(const uint32_t* items, const uint32_t* node_off, uint64_t T, uint32_t N,
+                  int chunked, uint64_t thr, uint32_t* rstart, uint32_t* rend, uint32_t* rcount,
+                  uint32_t* needed, uint32_t* redundant) {
+    if (chunked && thr == 0) return 3;
+    uint64_t base = 0;
+    uint32_t* ids = NULL;
+    uint64_t cap = 0;
+    for (uint64_t g = 0; g < T; ++g) {
+        const uint32_t* off = node_off + g * (N + 1);
+        for (uint32_t k = 0; k < N; ++k) {
+            const uint64_t lo = base + off[k], n = off[k + 1] - off[k];
+            if (n > cap) { cap = n; ids = (uint32_t*)realloc(ids, cap * sizeof(uint32_t)); }
+            uint64_t f = 0;
+            for (uint64_t q = 0; q < n; ++q)
+                if (!(items[lo + q] & OR_HIT_BIT)) ids[f++] = items[lo + q];
+            qsort(ids, f, sizeof(uint32_t), cmp_u32);
+            uint64_t nr = 0, red = 0, need = f;
+            if (chunked) {
+                uint64_t u = 0;
+                for (uint64_t q = 0; q < f; ++q) if (u == 0 || ids[u - 1] != ids[q]) ids[u++] = ids[q];
+                need = u;
+                uint64_t i = 0;
+                while (i < u) {
+                    uint64_t start = ids[i], j = i + 1;
+                    while (j < u && ids[j] - start + 1 <= thr) ++j;
+                    rstart[lo + nr] = (uint32_t)start;
+                    rend[lo + nr] = ids[j - 1];
+                    if (j - i > 1) red += (ids[j - 1] - start + 1) - (j - i);
+                    ++nr;
+                    i = j;
+                }
+            } else {
+                for (uint64_t q = 0; q < f; ++q) { rstart[lo + nr] = ids[q]; rend[lo + nr] = ids[q]; ++nr; }
+            }
+            rcount[g * N + k] = (uint32_t)nr;
+            needed[g * N + k] = (uint32_t)need;
+            redundant[g * N + k] = (uint32_t)red;
+        }
+        base += off[N];
+    }
+    free(ids);
+    return 0;
 }

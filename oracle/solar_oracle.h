@@ -91,6 +91,12 @@ int or_simulate(const uint32_t* items, const uint32_t* node_off, uint64_t T, uin
 int or_simulate_sequence(const uint32_t* seq, uint64_t n, uint64_t D, uint64_t C, int policy,
                          uint64_t* misses);
 
+/* chunking.cpp:9-33 / pipeline.cpp:21-28 on a finished plan: reads of list
+ * (g, k) at its item offsets (start == end: Single), per-list counts. */
+int or_plan_reads(const uint32_t* items, const uint32_t* node_off, uint64_t T, uint32_t N,
+                  int chunked, uint64_t thr, uint32_t* rstart, uint32_t* rend, uint32_t* rcount,
+                  uint32_t* needed, uint32_t* redundant);
+
 /* store.cpp:70-80: payload bytes [offset, offset+n) of a store with fill_seed. */
 void or_store_payload(uint64_t fill_seed, uint64_t offset, uint64_t n, uint8_t* out);
 

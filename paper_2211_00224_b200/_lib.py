@@ -62,7 +62,8 @@ class LsgShape(ctypes.Structure):
 class LsgPlanOut(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "trace", "graph", "order", "cost", "hist", "iters", "items", "node_off",
-        "fetch_before", "fetch_after")]
+        "fetch_before", "fetch_after", "read_start", "read_end", "read_count", "read_needed",
+        "read_redundant")]
 
 
 EXPORTS = [

@@ -28,6 +28,10 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
 int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N,
                     uint64_t D, uint64_t C, uint32_t k0, uint32_t k1, uint32_t* d_hits,
                     uint32_t* d_misses, uint32_t* d_slot, uint32_t* d_status, cudaStream_t st);
+int plan_reads_device(const uint32_t* d_items, const uint32_t* d_node_off, uint32_t T, uint32_t N,
+                      uint32_t S, uint32_t B, uint32_t keep, int chunked, uint64_t thr, uint32_t* rstart,
+                      uint32_t* rend, uint32_t* rcount, uint32_t* needed, uint32_t* redundant,
+                      cudaStream_t st);
 int gather_device(const void* d_buf, const uint32_t* d_slots, uint64_t n, uint64_t sample_bytes,
                   void* d_out, cudaStream_t st);
 int store_fill_device(const uint32_t* d_ids, uint64_t n, uint64_t sample_bytes, uint64_t seed,
@@ -217,6 +221,12 @@ int lsg_plan(const lsg_config* cfg, const lsg_plan_out* out, void* stream) {
                                order, inv, out->items, out->node_off, out->fetch_before,
                                out->fetch_after, status, st)))
         return rc;
+    // StepPlan.reads: plan_chunks when optim_chunk, singles otherwise (pipeline.cpp:83-88)
+    if ((rc = plan_reads_device(out->items, out->node_off, uint32_t(sh.total_steps), N,
+                                uint32_t(sh.steps_per_epoch), uint32_t(sh.global_batch), uint32_t(sh.keep),
+                                cfg->optim_chunk, cfg->chunk_threshold, out->read_start, out->read_end,
+                                out->read_count, out->read_needed, out->read_redundant, st)))
+        return rc;
     uint32_t h = 0;
     LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
     LSG_CUDA(cudaStreamSynchronize(st));
@@ -245,6 +255,11 @@ int lsg_plan_host(const lsg_config* cfg, const lsg_plan_out* h, void* stream) {
         {h->node_off, T * (N + 1) * 4, reinterpret_cast<void**>(&d.node_off)},
         {h->fetch_before, T * N * 4, reinterpret_cast<void**>(&d.fetch_before)},
         {h->fetch_after, T * N * 4, reinterpret_cast<void**>(&d.fetch_after)},
+        {h->read_start, sh.total_items * 4, reinterpret_cast<void**>(&d.read_start)},
+        {h->read_end, sh.total_items * 4, reinterpret_cast<void**>(&d.read_end)},
+        {h->read_count, T * N * 4, reinterpret_cast<void**>(&d.read_count)},
+        {h->read_needed, T * N * 4, reinterpret_cast<void**>(&d.read_needed)},
+        {h->read_redundant, T * N * 4, reinterpret_cast<void**>(&d.read_redundant)},
     };
     Scratch sc(st);
     for (Arr& a : arrs)

@@ -251,12 +251,12 @@ PlanOutput plan_schedule(const PipelineConfig& config) {
     const std::uint32_t E = config.trace.num_epochs, N = config.trace.num_nodes;
     const std::uint64_t keep = sh.keep, S = sh.steps_per_epoch, T = sh.total_steps;
     std::vector<std::uint32_t> trace(sh.total_items), order(E), items(sh.total_items), off(T * (N + 1)),
-        fb(T * N), fa(T * N);
+        fb(T * N), fa(T * N), rs(sh.total_items), re(sh.total_items), rc(T * N), rn(T * N), rr(T * N);
     std::vector<std::uint64_t> graph(std::size_t(E) * E), hist(config.pso.max_iters);
     std::uint64_t cost = 0;
     std::uint32_t iters = 0;
     lsg_plan_out h{trace.data(), graph.data(), order.data(), &cost, hist.data(), &iters, items.data(),
-                   off.data(), fb.data(), fa.data()};
+                   off.data(), fb.data(), fa.data(), rs.data(), re.data(), rc.data(), rn.data(), rr.data()};
     check(lsg_plan_host(&c, &h, nullptr));
 
     PlanOutput out;
@@ -300,6 +300,14 @@ PlanOutput plan_schedule(const PipelineConfig& config) {
                 }
                 st.fetches_before.push_back(fb[g * N + k]);
                 st.fetches_after.push_back(fa[g * N + k]);
+                ChunkPlan cp;  // chunking.hpp:24-28
+                for (std::uint32_t r = 0; r < rc[g * N + k]; ++r) {
+                    const std::size_t at = base + o[k] + r;
+                    cp.reads.push_back({rs[at] == re[at] ? Read::Kind::Single : Read::Kind::Chunk, rs[at], re[at]});
+                }
+                cp.needed = rn[g * N + k];
+                cp.redundant = rr[g * N + k];
+                st.reads.push_back(std::move(cp));
             }
             base += o[N];
             ep.steps.push_back(std::move(st));

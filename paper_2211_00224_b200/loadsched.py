@@ -196,6 +196,13 @@ class SchedulePlan:
     node_off: torch.Tensor      # int32 [T, N+1]
     fetches_before: torch.Tensor  # int32 [T, N]
     fetches_after: torch.Tensor   # int32 [T, N]
+    # StepPlan.reads (pipeline.cpp:83-88): list (g, k)'s reads at its item
+    # offsets (start == end: Single read), counts / needed / redundant [T, N]
+    read_start: torch.Tensor | None = None
+    read_end: torch.Tensor | None = None
+    read_count: torch.Tensor | None = None
+    read_needed: torch.Tensor | None = None
+    read_redundant: torch.Tensor | None = None
 
 
 @dataclass
@@ -292,7 +299,10 @@ def _plan_buffers(config: PipelineConfig, dev):
                 order=mk(E, torch.int32), cost=mk(1, torch.int64),
                 hist=mk(config.pso.max_iters, torch.int64), iters=mk(1, torch.int32),
                 items=mk(sh.total_items, torch.int32), node_off=mk(T * (N + 1), torch.int32),
-                fetch_before=mk(T * N, torch.int32), fetch_after=mk(T * N, torch.int32))
+                fetch_before=mk(T * N, torch.int32), fetch_after=mk(T * N, torch.int32),
+                read_start=mk(sh.total_items, torch.int32), read_end=mk(sh.total_items, torch.int32),
+                read_count=mk(T * N, torch.int32), read_needed=mk(T * N, torch.int32),
+                read_redundant=mk(T * N, torch.int32))
     return sh, bufs
 
 
@@ -308,7 +318,10 @@ def _wrap_plan(config: PipelineConfig, sh, b) -> PlanOutput:
         pso = PsoResult(order, b["hist"][:n], n)
     plan = SchedulePlan(t.dataset_size, N, t.local_batch, int(sh.steps_per_epoch), order,
                         b["items"][: E * keep], b["node_off"][: T * (N + 1)].view(T, N + 1),
-                        b["fetch_before"][: T * N].view(T, N), b["fetch_after"][: T * N].view(T, N))
+                        b["fetch_before"][: T * N].view(T, N), b["fetch_after"][: T * N].view(T, N),
+                        b["read_start"][: E * keep], b["read_end"][: E * keep],
+                        b["read_count"][: T * N].view(T, N), b["read_needed"][: T * N].view(T, N),
+                        b["read_redundant"][: T * N].view(T, N))
     return PlanOutput(trace, graph, pso, plan)
 
 
@@ -332,7 +345,10 @@ def plan_schedule_host(config: PipelineConfig, pinned: bool = True) -> PlanOutpu
              order=mk(E, torch.int32), cost=mk(1, torch.int64),
              hist=mk(config.pso.max_iters, torch.int64), iters=mk(1, torch.int32),
              items=mk(sh.total_items, torch.int32), node_off=mk(T * (N + 1), torch.int32),
-             fetch_before=mk(T * N, torch.int32), fetch_after=mk(T * N, torch.int32))
+             fetch_before=mk(T * N, torch.int32), fetch_after=mk(T * N, torch.int32),
+             read_start=mk(sh.total_items, torch.int32), read_end=mk(sh.total_items, torch.int32),
+             read_count=mk(T * N, torch.int32), read_needed=mk(T * N, torch.int32),
+             read_redundant=mk(T * N, torch.int32))
     out = LsgPlanOut(**{k: v.data_ptr() for k, v in b.items()})
     c = config.to_c()
     _check(lib().lsg_plan_host(ctypes.byref(c), ctypes.byref(out), _stream()))

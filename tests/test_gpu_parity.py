@@ -212,3 +212,26 @@ def test_plan_large_global_batch(ls, D, E, N, b, frac, seed):
     sim = ls.simulate_plan(out.plan, c.buffer_capacity)
     h, m = O.simulate(ref.items, ref.node_off, N, D, c.buffer_capacity)
     assert np.array_equal(u32(sim.hits), h) and np.array_equal(u32(sim.misses), m)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_plan_reads_match_oracle(ls, seed):
+    """StepPlan.reads: plan_chunks (chunking.cpp:9-33) or singles (pipeline.cpp:21-28)."""
+    r = random.Random(3000 + seed)
+    N, b = r.choice([1, 2, 4, 8]), r.choice([2, 4, 8, 32])
+    D = N * b * r.randint(2, 12) + r.randint(0, N * b - 1)
+    c = O.Cfg(D, r.randint(1, 5), N, b, seed=seed, buffer_capacity=r.randint(1, max(1, D // 3)),
+              optim_chunk=r.random() < 0.7, chunk_threshold=r.randint(1, 60), drop_last=r.random() < 0.7,
+              pso_iters=20)
+    out, ref = check_plan(ls, c)
+    rs, re_, cnt, need, red = O.plan_reads(ref.items, ref.node_off, N, c.optim_chunk, c.chunk_threshold)
+    p = out.plan
+    assert np.array_equal(u32(p.read_count), cnt) and np.array_equal(u32(p.read_needed), need)
+    assert np.array_equal(u32(p.read_redundant), red)
+    grs, gre = u32(p.read_start), u32(p.read_end)
+    base = 0
+    for g in range(ref.node_off.shape[0]):
+        for k in range(N):
+            lo, n = base + ref.node_off[g, k], cnt[g, k]
+            assert np.array_equal(grs[lo:lo + n], rs[lo:lo + n]) and np.array_equal(gre[lo:lo + n], re_[lo:lo + n])
+        base += ref.node_off[g, N]

@@ -194,3 +194,26 @@ def test_oracle_simulate_matches_reference_on_foreign_plans():
 def test_store_payload_matches_reference():
     got = O.ref_store(5, 24, 77)
     assert np.array_equal(got, O.store_payload(77, 0, 120))
+
+
+@ref
+@pytest.mark.parametrize("seed", range(12))
+def test_oracle_reads_match_reference(seed):
+    """StepPlan::reads (chunking.cpp:9-33, pipeline.cpp:21-28, :83-88)."""
+    r = random.Random(900 + seed)
+    N, b = r.choice([1, 2, 4]), r.choice([2, 4, 8])
+    D = N * b * r.randint(2, 10) + r.randint(0, N * b - 1)
+    cfg = O.Cfg(D, r.randint(1, 4), N, b, seed=seed, buffer_capacity=r.randint(1, max(1, D // 3)),
+                optim_chunk=r.random() < 0.7, chunk_threshold=r.randint(1, 40), pso_iters=20)
+    p, q = O.plan(cfg), O.ref_plan(cfg)
+    rs, re_, cnt, need, red = O.plan_reads(p.items, p.node_off, N, cfg.optim_chunk, cfg.chunk_threshold)
+    assert np.array_equal(cnt.ravel(), q.extra["rcount"]) and np.array_equal(need.ravel(), q.extra["rneed"])
+    assert np.array_equal(red.ravel(), q.extra["rred"])
+    base = 0
+    for g in range(p.node_off.shape[0]):
+        for k in range(N):
+            lo = base + p.node_off[g, k]
+            n = cnt[g, k]
+            assert np.array_equal(rs[lo:lo + n], q.extra["rstart"][lo:lo + n])
+            assert np.array_equal(re_[lo:lo + n], q.extra["rend"][lo:lo + n])
+        base += p.node_off[g, N]
