@@ -138,10 +138,9 @@ struct LoopArgs {
     const uint32_t* nu;              // [E*keep] execution order
     const uint32_t* sb;              // [E*keep] execution order, desc per step
     const uint32_t* nr;              // [E*keep] rank of the access's id in sb of its next use
-    uint32_t* rk;                    // [N][D] rank of a resident's id inside its key's batch
     uint32_t* bm;                    // [N][T][BW] bucket membership bitmaps over ranks
     uint32_t BW;                     // words per bucket bitmap (ceil(B/32))
-    uint32_t* key;                   // [N][D]
+    uint32_t* key;                   // [N][D] next-use step * B + rank, kNever, or kNone
     uint32_t* hm;                    // [D] holder masks
     uint32_t* nz;                    // [N][nzw]
     uint32_t* infbm;                 // [N][infw]
@@ -206,8 +205,8 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // update plus the bucket / never-used summaries.
 __device__ __forceinline__ void set_key(const LoopArgs& a, Small& sm, uint32_t k, uint32_t x,
                                         uint32_t nu, uint32_t rank) {
-    a.key[size_t(k) * a.D + x] = nu;
-    a.rk[size_t(k) * a.D + x] = rank;
+    // one word per resident: (next-use step, rank in that step's sorted batch)
+    a.key[size_t(k) * a.D + x] = nu == kNever ? kNever : nu * a.B + rank;
     if (nu != kNever)
         atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
     if (nu == kNever) {
@@ -308,8 +307,7 @@ __device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t ne
                     const uint32_t bit = __ffs(m) - 1;
                     m &= m - 1;
                     const uint32_t x = cand[wi2 * 32 + bit];
-                    if (__ldcg(&a.key[size_t(k) * a.D + x]) != uint32_t(beta) ||
-                        __ldcg(&a.rk[size_t(k) * a.D + x]) != wi2 * 32 + bit)
+                    if (__ldcg(&a.key[size_t(k) * a.D + x]) != uint32_t(beta) * a.B + wi2 * 32 + bit)
                         word &= ~(1u << bit);
                 }
             }
@@ -791,8 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 const uint32_t x = s.sx[j], nu = s.snu[j], rank = nrrow[j];
                 const uint32_t wd = nu >> 5;
                 if (nu != kNever && wd >= wbase && wd - wbase < kWinWords) {
-                    a.key[size_t(k) * a.D + x] = nu;
-                    a.rk[size_t(k) * a.D + x] = rank;
+                    a.key[size_t(k) * a.D + x] = nu * a.B + rank;
                     atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
                     atomicOr(&sm.win[k][wd - wbase], 1u << (nu & 31));
                 } else {
@@ -884,7 +881,8 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
         return set_error(kCapability, "plan: device planner supports num_nodes <= 32 in this build");
     if (dm.B > kMaxB)
         return set_error(kCapability, "plan: device planner supports global batch <= 16384 in this build");
-    if (dm.T >= 0xFFFFFFF0ull) return set_error(kCapability, "plan: too many steps");
+    if (dm.T * dm.B >= 0xFFFFFFF0ull)  // packed resident keys: step * B + rank
+        return set_error(kCapability, "plan: steps x global batch must stay below 2^32");
     Scratch sc(st);
     const size_t EK = size_t(dm.E) * dm.keep;
     uint32_t* nu = sc.get<uint32_t>(EK);
@@ -905,7 +903,6 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.nzw = uint32_t((dm.T + 31) / 32 + 1);
     a.infw = uint32_t((dm.D + 31) / 32);
     a.key = sc.get<uint32_t>(size_t(dm.N) * dm.D);
-    a.rk = sc.get<uint32_t>(size_t(dm.N) * dm.D);
     a.BW = uint32_t((dm.B + 31) / 32);
     a.bm = sc.get<uint32_t>(size_t(dm.N) * dm.T * a.BW);
     a.hm = sc.get<uint32_t>(dm.D);
@@ -917,7 +914,7 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.mres = sc.get<uint32_t>(dm.B);
     a.mv = sc.get<uint32_t>(dm.B);
     a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B);
-    if (!nu || !sb || !nr || !a.rk || !a.bm || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.mpos || !a.mres ||
+    if (!nu || !sb || !nr || !a.bm || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.mpos || !a.mres ||
         !a.mv || !a.dmoves)
         return set_error(kInternal, "plan: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(dm.N) * dm.D * 4, st));

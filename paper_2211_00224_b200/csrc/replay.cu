@@ -25,6 +25,8 @@
 //     a stale bit in its current step, which is never reached). kNeverUsed
 //     residents sit in an id bitmap scanned from the top (ties by larger id,
 //     buffer.cpp:27-28).
+#include <vector>
+
 #include "common.cuh"
 
 namespace lsg {
@@ -710,21 +712,17 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     LSG_CUDA(cudaMemcpyAsync(&total, gb + T, 8, cudaMemcpyDeviceToHost, st));
     {
         // key stride = the longest node list of any step (keys are g*L + i)
-        uint32_t* hoff = nullptr;
+        std::vector<uint32_t> hv(size_t(T) * (N + 1));
+        uint32_t* hoff = hv.data();
         const size_t nb = size_t(T) * (N + 1) * 4;
-        LSG_CUDA(cudaMallocHost(&hoff, nb));
         LSG_CUDA(cudaMemcpyAsync(hoff, d_node_off, nb, cudaMemcpyDeviceToHost, st));
         LSG_CUDA(cudaStreamSynchronize(st));
         for (uint64_t g = 0; g < T; ++g)
             for (uint32_t k = 0; k < N; ++k) {
                 const uint32_t* o = hoff + g * (N + 1);
-                if (o[k + 1] < o[k]) {
-                    cudaFreeHost(hoff);
-                    return set_error(kValidation, "simulate: node offsets not ascending");
-                }
+                if (o[k + 1] < o[k]) return set_error(kValidation, "simulate: node offsets not ascending");
                 L = std::max<uint64_t>(L, o[k + 1] - o[k]);
             }
-        cudaFreeHost(hoff);
     }
     if (L == 0) L = 1;
     if (T * L >= 0xFFFFFFF0ull) return set_error(kCapability, "simulate: plan too large for 32-bit position keys");
