@@ -463,9 +463,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     s.pre[mi] = j;  // multi list (pre is free until F)
                     // exact S_k(j) (warp-local part from A + warp base), b for
                     // non-holders, compact by multi index for D's staging
-                    for (uint32_t k = 0; k < N; ++k)
-                        a.sx[size_t(mi) * N + k] =
-                            ((m >> k) & 1u) ? min(b, a.smul[size_t(j) * N + k] + sm.wcnt[w][k]) : b;
+                    if (N <= 8) {
+                        // D8 keys: T_k = (S_k << 4) | k in rows of 8 words
+                        uint32_t t[8];
+#pragma unroll
+                        for (uint32_t k = 0; k < 8; ++k)
+                            t[k] = ((k < N && ((m >> k) & 1u)) ? min(b, a.smul[size_t(j) * N + k] + sm.wcnt[w][k]) : b) << 4 | k;
+                        uint4* dst = reinterpret_cast<uint4*>(a.sx + size_t(mi) * 8);
+                        dst[0] = make_uint4(t[0], t[1], t[2], t[3]);
+                        dst[1] = make_uint4(t[4], t[5], t[6], t[7]);
+                    } else {
+                        for (uint32_t k = 0; k < N; ++k)
+                            a.sx[size_t(mi) * N + k] =
+                                ((m >> k) & 1u) ? min(b, a.smul[size_t(j) * N + k] + sm.wcnt[w][k]) : b;
+                    }
                 }
             }
             __syncthreads();
@@ -476,6 +487,80 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 if (lane < N) sm.mtot[lane] = 0;
             }
             for (int drep = 0; drep < ((a.dbg_skip & 2) ? 2 : 1); ++drep)  // timing: D is idempotent
+            if (w == 0 && !(a.dbg_skip & 1) && N <= 8) {
+                // N <= 8: no warp reduction at all. Every lane runs the same
+                // serial decision on registers: node k's running count is
+                // Mk[k] = M_k << 4, item keys are T_k + Mk[k] with
+                // T_k = (S_k << 4) | k (phase C), and the winner is the
+                // minimum key below b << 4 (lowest k on ties, locality.cpp:
+                // 24-31). Clamping the minimum at kSent = (b << 4) - 1, whose
+                // low nibble no key has, makes "no candidate" update nothing.
+                // The rows of a chunk are staged in shared memory and read
+                // with broadcast 16-byte loads, off the dependency chain.
+                uint32_t Mk[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) Mk[k] = 0;
+                const uint32_t nm = sm.nmulti;
+                const uint32_t kSent = (b << 4) - 1u;
+                auto stage = [&](uint32_t base, uint32_t buf) {
+                    const uint32_t cnt = min(32u, nm - base);
+                    const uint32_t* src = a.sx + size_t(base) * 8;
+                    uint4* dst4 = reinterpret_cast<uint4*>(&sm.stg[buf][0][0]);
+                    for (uint32_t q = lane; q < 64; q += 32) {
+                        if (q < 2 * cnt) {
+                            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst4 + q));
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + 4 * q));
+                        } else {
+                            const uint32_t k0 = (q & 1) * 4;  // padding rows: no candidate
+                            dst4[q] = make_uint4(b << 4 | k0, b << 4 | (k0 + 1), b << 4 | (k0 + 2), b << 4 | (k0 + 3));
+                        }
+                    }
+                    asm volatile("cp.async.commit_group;\n" ::);
+                };
+                if (nm) stage(0, 0);
+                for (uint32_t base = 0, buf = 0; base < nm; base += 32, buf ^= 1) {
+                    if (base + 32 < nm) {
+                        stage(base + 32, buf ^ 1);
+                        asm volatile("cp.async.wait_group 1;\n" ::);
+                    } else {
+                        asm volatile("cp.async.wait_group 0;\n" ::);
+                    }
+                    __syncwarp();
+                    const uint32_t cnt = min(32u, nm - base);
+                    const uint32_t myj = lane < cnt ? s.pre[base + lane] : 0u;
+                    const uint4* rows = reinterpret_cast<const uint4*>(&sm.stg[buf][0][0]);
+                    uint32_t myres = kSent;
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        const uint4 r0 = rows[2 * u], r1 = rows[2 * u + 1];
+                        const uint32_t K0 = r0.x + Mk[0], K1 = r0.y + Mk[1], K2 = r0.z + Mk[2], K3 = r0.w + Mk[3];
+                        const uint32_t K4 = r1.x + Mk[4], K5 = r1.y + Mk[5], K6 = r1.z + Mk[6], K7 = r1.w + Mk[7];
+                        const uint32_t cl = __vimin3_u32(__vimin3_u32(K0, K1, K2), __vimin3_u32(K3, K4, K5),
+                                                         __vimin3_u32(K6, K7, kSent));
+                        Mk[0] += cl == K0 ? 16u : 0u; Mk[1] += cl == K1 ? 16u : 0u;
+                        Mk[2] += cl == K2 ? 16u : 0u; Mk[3] += cl == K3 ? 16u : 0u;
+                        Mk[4] += cl == K4 ? 16u : 0u; Mk[5] += cl == K5 ? 16u : 0u;
+                        Mk[6] += cl == K6 ? 16u : 0u; Mk[7] += cl == K7 ? 16u : 0u;
+                        myres = lane == uint32_t(u) ? cl : myres;
+                    }
+                    // lane u: item u's decision -> node list position + E's input
+                    if (lane < cnt) {
+                        if (myres != kSent) {
+                            const uint32_t kk = myres & 15u, c = myres >> 4;
+                            const uint32_t Sk = (&sm.stg[buf][0][0])[lane * 8 + kk] >> 4;  // row-major 8 words/item
+                            s.fin[kk * b + (c - Sk)] = myj;
+                            s.sinfo[myj] = (c << 5) | kk;  // consumed by E
+                        } else {
+                            s.sinfo[myj] = 0xFFFFFFFFu;
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (a.prof && lane == 0) atomicAdd(&a.prof[8], (unsigned long long)nm);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (lane == uint32_t(k) && uint32_t(k) < N) sm.mtot[k] = Mk[k] >> 4;
+            } else
             if (w == 0 && !(a.dbg_skip & 1)) {
                 // The warp-local part of S_k(j) for 32 multi items at a time is
                 // staged global->smem with cp.async one chunk ahead. A
@@ -533,6 +618,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     }
                     const uint32_t Mstart = Msh >> 5;
                     uint32_t myres = 0xFFFFFFFFu;
+                    for (int lrep = 0; lrep < ((a.dbg_skip & 4) ? 2 : 1); ++lrep) {  // timing only
+                    if (lrep) Msh = Mstart << 5;
 #pragma unroll
                     for (int u = 0; u < 32; ++u) {
                         if (uint32_t(u) < cnt) {
@@ -543,6 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                             Msh += (keyv == best && best != 0xFFFFFFFFu) ? 32u : 0u;
                             myres = lane == uint32_t(u) ? best : myres;
                         }
+                    }
                     }
                     // lane u: item u's decision -> node list position + E's input
                     const bool chose = lane < cnt && myres != 0xFFFFFFFFu;
@@ -909,7 +997,7 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.nz = sc.get<uint32_t>(size_t(dm.N) * a.nzw);
     a.infbm = sc.get<uint32_t>(size_t(dm.N) * a.infw);
     a.smul = sc.get<uint32_t>(size_t(dm.B) * dm.N);
-    a.sx = sc.get<uint32_t>(size_t(dm.B) * dm.N);
+    a.sx = sc.get<uint32_t>(size_t(dm.B) * std::max<uint32_t>(dm.N, 8u));  // D8 rows are 8 words
     a.mpos = sc.get<uint32_t>(size_t(dm.N) * dm.b);
     a.mres = sc.get<uint32_t>(dm.B);
     a.mv = sc.get<uint32_t>(dm.B);
