@@ -49,6 +49,8 @@ constexpr uint32_t kMaxN = 32;
 constexpr uint32_t kMaxSmemB = 8192;   // per-item arrays in shared memory up to here
 constexpr uint32_t kMaxB = 16384;      // then in L2-resident global scratch
 constexpr uint32_t kFetch = 0xFFFFFFFFu;
+constexpr uint32_t kDmv = 32;       // G: moves per donor kept in shared memory
+constexpr uint32_t kNotMoved = 0xFFFFFFFFu;
 constexpr uint32_t kWinWords = 40;  // I1 bucket-bit window (covers 2S <= 1216 steps)
 
 // ----------------------------------------------------------------- K5 ----
@@ -111,7 +113,7 @@ __global__ void k_nextrank(const uint32_t* __restrict__ trace, const uint32_t* _
     const uint32_t* row = trace + size_t(order[i]) * keep;
     for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < keep; pos += gridDim.x * blockDim.x) {
         const uint32_t v = nu[size_t(i) * keep + pos];
-        uint32_t r = kNone;
+        uint32_t r = kNever;
         if (v != kNever) {
             const uint32_t x = row[pos];
             const uint32_t gi = v / S, gt = v % S, lo = gt * B, blen = min(B, keep - lo);
@@ -121,7 +123,7 @@ __global__ void k_nextrank(const uint32_t* __restrict__ trace, const uint32_t* _
                 const uint32_t mid = (a0 + a1) >> 1;
                 if (cand[mid] > x) a0 = mid + 1; else a1 = mid;
             }
-            r = a0;
+            r = v * B + a0;  // packed resident key: next-use step, rank
         }
         nr[size_t(i) * keep + pos] = r;
     }
@@ -137,7 +139,8 @@ struct LoopArgs {
     const uint32_t* order;           // [E]
     const uint32_t* nu;              // [E*keep] execution order
     const uint32_t* sb;              // [E*keep] execution order, desc per step
-    const uint32_t* nr;              // [E*keep] rank of the access's id in sb of its next use
+    const uint32_t* nr;              // [E*keep] packed next-use key: step * B + rank in sb, or kNever
+    unsigned long long bdiv;         // ceil(2^64 / B) (B >= 2): step = umul64hi(key, bdiv)
     uint32_t* bm;                    // [N][T][BW] bucket membership bitmaps over ranks
     uint32_t BW;                     // words per bucket bitmap (ceil(B/32))
     uint32_t* key;                   // [N][D] next-use step * B + rank, kNever, or kNone
@@ -146,10 +149,7 @@ struct LoopArgs {
     uint32_t* infbm;                 // [N][infw]
     uint32_t* smul;                  // [B][N] scratch: warp-local S_k(j)
     uint32_t* sx;                    // [B][N] scratch: exact S_k(j) by multi index
-    uint32_t* mpos;                  // [N][b] scratch
-    uint32_t* mres;                  // [B] scratch
-    uint32_t* mv;                    // [B] scratch: moves (d | r<<8 | q<<16)
-    uint32_t* dmoves;                // [N][B] scratch: donor's i-th move
+    uint32_t* dmoves;                // [N][B] donor's i-th move (r | q<<8) beyond kDmv
     uint32_t* items;                 // [E*keep] output
     uint32_t* node_off;              // [T][N+1] output
     uint32_t* fb;                    // [T][N] output (may be null)
@@ -162,7 +162,7 @@ struct LoopArgs {
 
 struct Shared {
     uint32_t* sx;     // [B] ids
-    uint32_t* snu;    // [B] next-use keys
+    uint32_t* snu;    // [B] packed next-use keys (step * B + rank, kNever)
     uint32_t* smask;  // [B] holder masks at step start
     uint32_t* sinfo;  // [B] per-item scratch
     uint32_t* pre;    // [B] pre-balance lists, node k at k*b (j | hit tag)
@@ -181,7 +181,6 @@ struct Small {
     uint32_t lenk[kMaxN];           // pre-balance list length
     uint32_t fcnt[kMaxN];           // fetches before balance
     uint32_t outk[kMaxN], ink[kMaxN];
-    uint32_t thr[kMaxN];            // donor moved-id threshold
     uint32_t noff[kMaxN + 1];       // final offsets
     uint32_t bsize[kMaxN];          // buffer occupancy
     uint32_t top[kMaxN];            // bucket upper bound
@@ -189,8 +188,8 @@ struct Small {
     uint32_t infcnt[kMaxN];         // never-used residents
     uint32_t nmulti, nfetch, nmoves;
     alignas(16) uint32_t stg[2][32][kMaxN];  // D: staged S_k(j) of 32 multi items
-    uint32_t pthr[32][32];          // D: per (item, node) candidate threshold
-    uint32_t pkb[32][32];           // D: per (item, node) base key
+    uint32_t dmv[kMaxN][kDmv];      // G: donor's i-th move (r | q<<8), i < kDmv
+    uint32_t rq[kMaxN];             // G: recipient of each rank in a round
     uint32_t win_base;              // I1: first bucket word of the window
     uint32_t win[kMaxN][kWinWords]; // I1: bucket bits aggregated per step
 };
@@ -203,10 +202,14 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // buffer.cpp:37-41 (re-key) / :42-46 (insert) without the eviction: key
 // update plus the bucket / never-used summaries.
-__device__ __forceinline__ void set_key(const LoopArgs& a, Small& sm, uint32_t k, uint32_t x,
-                                        uint32_t nu, uint32_t rank) {
+__device__ __forceinline__ uint32_t key_step(const LoopArgs& a, uint32_t pk) {
+    return a.B == 1 ? pk : uint32_t(__umul64hi(pk, a.bdiv));
+}
+
+__device__ __forceinline__ void set_key(const LoopArgs& a, Small& sm, uint32_t k, uint32_t x, uint32_t pk) {
     // one word per resident: (next-use step, rank in that step's sorted batch)
-    a.key[size_t(k) * a.D + x] = nu == kNever ? kNever : nu * a.B + rank;
+    a.key[size_t(k) * a.D + x] = pk;
+    const uint32_t nu = pk == kNever ? kNever : key_step(a, pk), rank = pk - nu * a.B;
     if (nu != kNever)
         atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
     if (nu == kNever) {
@@ -340,7 +343,9 @@ __device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t ne
     }
 }
 
-template <bool kSmemItems>
+// kD8: N <= 8 (register-only multi-holder pass); the other path is not
+// instantiated, which keeps the step's instruction footprint small.
+template <bool kSmemItems, bool kD8>
 __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
     extern __shared__ __align__(16) uint32_t dyn[];
     __shared__ Small sm;
@@ -363,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
     }
     __syncthreads();
     size_t gbase = 0;
-    unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long pacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long tprev = clock64();
 #define LSG_PHASE(n)                                              \
     if (a.prof && tid == 0) {                                     \
@@ -375,8 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         const uint32_t i = g / a.S, t = g % a.S;
         const uint32_t lo = t * a.B, len = min(a.B, a.keep - lo);
         const uint32_t* row = a.trace + size_t(a.order[i]) * a.keep + lo;
-        const uint32_t* nurow = a.nu + size_t(i) * a.keep + lo;
-        const uint32_t* nrrow = a.nr + size_t(i) * a.keep + lo;
+        const uint32_t* pkrow = a.nr + size_t(i) * a.keep + lo;
         const uint32_t R = ((len + kThreads - 1) / kThreads) * 32;  // items per warp
         const uint32_t j0 = w * R, j1 = min(j0 + R, len);
 
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
 #pragma unroll 4
         for (uint32_t j = j0 + lane; j < j1; j += 32) {
             s.sx[j] = row[j];
-            s.snu[j] = nurow[j];
+            s.snu[j] = pkrow[j];
         }
         __syncwarp();
 #pragma unroll 4
@@ -461,33 +465,58 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     const uint32_t mi = sm.wmul[w] + s.sinfo[j];
                     s.sinfo[j] = mi;
                     s.pre[mi] = j;  // multi list (pre is free until F)
-                    // exact S_k(j) (warp-local part from A + warp base), b for
-                    // non-holders, compact by multi index for D's staging
-                    if (N <= 8) {
+                }
+            }
+            __syncwarp();
+            // exact S_k(j) rows of the warp's multi items (warp-local part from
+            // A + warp base; b for non-holders), compact by multi index for
+            // D's staging. Lane per item: the row's loads are all in flight.
+            {
+                const uint32_t mb0 = sm.wmul[w];
+                const uint32_t mcnt = (w + 1 < uint32_t(kWarps) ? sm.wmul[w + 1] : sm.nmulti) - mb0;
+                for (uint32_t q = lane; q < mcnt; q += 32) {
+                    const uint32_t mi = mb0 + q, j = s.pre[mi], m = s.smask[j];
+                    const uint32_t* sm_row = a.smul + size_t(j) * N;
+                    if (kD8) {
                         // D8 keys: T_k = (S_k << 4) | k in rows of 8 words
                         uint32_t t[8];
 #pragma unroll
                         for (uint32_t k = 0; k < 8; ++k)
-                            t[k] = ((k < N && ((m >> k) & 1u)) ? min(b, a.smul[size_t(j) * N + k] + sm.wcnt[w][k]) : b) << 4 | k;
+                            t[k] = (k < N && ((m >> k) & 1u)) ? __ldcg(&sm_row[k]) : 0u;
+#pragma unroll
+                        for (uint32_t k = 0; k < 8; ++k)
+                            t[k] = ((k < N && ((m >> k) & 1u)) ? min(b, t[k] + sm.wcnt[w][k]) : b) << 4 | k;
                         uint4* dst = reinterpret_cast<uint4*>(a.sx + size_t(mi) * 8);
                         dst[0] = make_uint4(t[0], t[1], t[2], t[3]);
                         dst[1] = make_uint4(t[4], t[5], t[6], t[7]);
                     } else {
                         for (uint32_t k = 0; k < N; ++k)
                             a.sx[size_t(mi) * N + k] =
-                                ((m >> k) & 1u) ? min(b, a.smul[size_t(j) * N + k] + sm.wcnt[w][k]) : b;
+                                ((m >> k) & 1u) ? min(b, __ldcg(&sm_row[k]) + sm.wcnt[w][k]) : b;
                     }
                 }
             }
             __syncthreads();
             LSG_PHASE(1)
-            // ------------ D: serial multi-holder pass, lanes = nodes
+            // ------------ D: serial multi-holder pass
+            // the other warps idle through D: pull the next step's id and key
+            // rows into L2 for phase A
+            if (w != 0 && g + 1 < a.T) {
+                const uint32_t i2 = (g + 1) / a.S, t2 = (g + 1) % a.S;
+                const uint32_t lo2 = t2 * a.B, len2 = min(a.B, a.keep - lo2);
+                const char* r0 = reinterpret_cast<const char*>(a.trace + size_t(a.order[i2]) * a.keep + lo2);
+                const char* r1 = reinterpret_cast<const char*>(a.nr + size_t(i2) * a.keep + lo2);
+                for (uint32_t off = (tid - 32) * 128; off < len2 * 4; off += (kThreads - 32) * 128) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(r0 + off));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(r1 + off));
+                }
+            }
             if (w == 0 && (a.dbg_skip & 1)) {  // timing experiment: every multi item fetches
                 for (uint32_t mi = lane; mi < sm.nmulti; mi += 32) s.sinfo[s.pre[mi]] = 0xFFFFFFFFu;
                 if (lane < N) sm.mtot[lane] = 0;
             }
             for (int drep = 0; drep < ((a.dbg_skip & 2) ? 2 : 1); ++drep)  // timing: D is idempotent
-            if (w == 0 && !(a.dbg_skip & 1) && N <= 8) {
+            if (kD8 && w == 0 && !(a.dbg_skip & 1)) {
                 // N <= 8: no warp reduction at all. Every lane runs the same
                 // serial decision on registers: node k's running count is
                 // Mk[k] = M_k << 4, item keys are T_k + Mk[k] with
@@ -556,12 +585,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     }
                     __syncwarp();
                 }
-                if (a.prof && lane == 0) atomicAdd(&a.prof[8], (unsigned long long)nm);
+                if (a.prof && lane == 0) atomicAdd(&a.prof[12], (unsigned long long)nm);
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     if (lane == uint32_t(k) && uint32_t(k) < N) sm.mtot[k] = Mk[k] >> 4;
             } else
-            if (w == 0 && !(a.dbg_skip & 1)) {
+            if (!kD8 && w == 0 && !(a.dbg_skip & 1)) {
                 // The warp-local part of S_k(j) for 32 multi items at a time is
                 // staged global->smem with cp.async one chunk ahead. A
                 // lane-parallel pass then packs the exact S_k(j) of the chunk
@@ -641,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     if (lane < cnt) s.sinfo[myj] = myres;  // consumed by E
                     __syncwarp();
                 }
-                if (a.prof && lane == 0) atomicAdd(&a.prof[8], (unsigned long long)nm);
+                if (a.prof && lane == 0) atomicAdd(&a.prof[12], (unsigned long long)nm);
                 if (lane < N) sm.mtot[lane] = Msh >> 5;
             }
             __syncthreads();
@@ -714,6 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 if (lane == 0 && F > totfree) atomicOr(a.status, 8u);  // ran out of capacity
             }
             __syncthreads();
+            LSG_PHASE(3)
             // ------------ F: pre-balance lists [hits in batch order][fetches]
             for (uint32_t j = j0 + lane; j < j1; j += 32) {
                 const uint32_t v = s.sinfo[j];
@@ -749,60 +779,82 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         }
         __syncthreads();
 
-        LSG_PHASE(3)
+        LSG_PHASE(4)
         // ---------------- G: balance on counts (balance.cpp:10-39)
-        if (tid < N) {
-            sm.outk[tid] = 0;
-            sm.ink[tid] = 0;
-            sm.thr[tid] = 0;
-            if (a.fb) a.fb[size_t(g) * N + tid] = sm.fcnt[tid];
-        }
-        __syncthreads();
-        if (a.balance && tid == 0) {
-            uint32_t cnt[kMaxN];
-            for (uint32_t k = 0; k < N; ++k) cnt[k] = sm.fcnt[k];
-            uint32_t nmv = 0;
-            for (;;) {
-                uint32_t d = 0, r = 0;
-                for (uint32_t k = 1; k < N; ++k) {
-                    if (cnt[k] > cnt[d]) d = k;
-                    if (cnt[k] < cnt[r]) r = k;
+        // warp 0, lanes = nodes. One move takes from the first argmax and gives
+        // to the first argmin, so donors at the top level M give one each in
+        // node order while recipients at the bottom level m receive one each
+        // in node order (donors and recipients stay disjoint): a round pairs
+        // the first n = min(#top, #bottom) of each, all while M - m >= 2.
+        // The donor's i-th move goes to recipient r as its q-th appended fetch.
+        if (w == 0) {
+            uint32_t c = lane < N ? sm.fcnt[lane] : 0u;
+            if (a.fb && lane < N) a.fb[size_t(g) * N + lane] = c;
+            uint32_t outc = 0, inn = 0, nmv = 0;
+            while (a.balance) {
+                const uint32_t M = __reduce_max_sync(0xFFFFFFFFu, lane < N ? c : 0u);
+                const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, lane < N ? c : 0xFFFFFFFFu);
+                if (M - m <= 1) break;
+                const uint32_t dm = __ballot_sync(0xFFFFFFFFu, lane < N && c == M);
+                const uint32_t rm = __ballot_sync(0xFFFFFFFFu, lane < N && c == m);
+                const uint32_t n = min(__popc(dm), __popc(rm));
+                const bool isd = (dm >> lane) & 1u, isr = (rm >> lane) & 1u;
+                const uint32_t rk = __popc((isd ? dm : rm) & lt);  // rank in its set
+                // the recipient of rank rk publishes (r, q) for the donor of rank rk
+                if (isr && rk < n) {
+                    sm.rq[rk] = lane | (inn << 8);
+                    ++c;
+                    ++inn;
                 }
-                if (cnt[d] - cnt[r] <= 1) break;
-                const uint32_t q = sm.ink[r];
-                a.dmoves[size_t(d) * a.B + sm.outk[d]] = r | (q << 8);
-                sm.outk[d] += 1;
-                sm.ink[r] = q + 1;
-                --cnt[d];
-                ++cnt[r];
-                ++nmv;
+                __syncwarp();
+                if (isd && rk < n) {
+                    const uint32_t rq = sm.rq[rk];
+                    if (outc < kDmv) sm.dmv[lane][outc] = rq;
+                    else a.dmoves[size_t(lane) * a.B + outc] = rq;
+                    --c;
+                    ++outc;
+                }
+                __syncwarp();
+                nmv += n;
             }
-            sm.nmoves = nmv;
+            if (lane < N) {
+                sm.outk[lane] = outc;
+                sm.ink[lane] = inn;
+            }
+            if (lane == 0) sm.nmoves = nmv;
         }
         __syncthreads();
-        // donors: the out_k-th largest fetch id is the moved/kept threshold
+        LSG_PHASE(5)
+        // donors (warp per donor): the i-th largest fetch id takes move i
+        // (balance.cpp:27-33 erases the largest remaining fetch id each move)
         if (a.balance && sm.nmoves) {
-            for (uint32_t k = 0; k < N; ++k) {
+            for (uint32_t k = w; k < N; k += kWarps) {
                 const uint32_t out = sm.outk[k];
                 if (!out) continue;
                 // remap lists are [hits][fetches]: fetches start at size[k]
                 // (slice lists are mixed; size[k] = 0 there)
                 const uint32_t L = sm.lenk[k], f0 = sm.size[k];
-                for (uint32_t p = f0 + tid; p < L; p += kThreads) {
-                    const uint32_t e = s.pre[k * b + p];
-                    if (e & kHit) continue;
-                    const uint32_t x = s.sx[e & 0xFFFF];
+                for (uint32_t c = f0; c < L; c += 32) {
+                    const uint32_t p = c + lane;
+                    const uint32_t e = p < L ? s.pre[k * b + p] : kHit;
+                    const bool isf = !(e & kHit);
+                    const uint32_t x = isf ? s.sx[e & 0xFFFF] : 0u;
                     uint32_t rank = 0;
-                    for (uint32_t p2 = f0; p2 < L; ++p2) {
-                        const uint32_t e2 = s.pre[k * b + p2];
-                        if (!(e2 & kHit) && s.sx[e2 & 0xFFFF] > x) ++rank;
+                    for (uint32_t c2 = f0; c2 < L; c2 += 32) {
+                        const uint32_t p2 = c2 + lane;
+                        const uint32_t e2 = p2 < L ? s.pre[k * b + p2] : kHit;
+                        const uint32_t y = !(e2 & kHit) ? s.sx[e2 & 0xFFFF] : 0u;  // 0 is never > x
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) rank += __shfl_sync(0xFFFFFFFFu, y, q) > x ? 1u : 0u;
                     }
-                    if (rank == out - 1) sm.thr[k] = x;
+                    if (isf)
+                        s.sinfo[e & 0xFFFF] = rank >= out ? kNotMoved
+                                              : rank < kDmv ? sm.dmv[k][rank] : a.dmoves[size_t(k) * a.B + rank];
                 }
             }
             __syncthreads();
         }
-        LSG_PHASE(4)
+        LSG_PHASE(6)
         // ---------------- H: final lists + outputs
         if (w == 0) {
             const uint32_t L = lane < N ? sm.lenk[lane] - sm.outk[lane] + sm.ink[lane] : 0;
@@ -826,7 +878,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         __syncthreads();
         // warp k places node k's pre-balance list (k < N)
         for (uint32_t k = w; k < N; k += kWarps) {
-            const uint32_t L = sm.lenk[k], out = sm.outk[k], thr = sm.thr[k];
+            const uint32_t L = sm.lenk[k], out = sm.outk[k];
             uint32_t shift = 0;
             for (uint32_t c = 0; c < L; c += 32) {
                 const uint32_t p = c + lane;
@@ -834,20 +886,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 bool moved = false;
                 if (p < L) {
                     e = s.pre[k * b + p];
-                    moved = out && !(e & kHit) && s.sx[e & 0xFFFF] >= thr;
+                    moved = out && !(e & kHit) && s.sinfo[e & 0xFFFF] != kNotMoved;
                 }
                 const uint32_t mbal = __ballot_sync(0xFFFFFFFFu, moved);
                 if (p < L) {
                     uint32_t dst;
                     if (moved) {
-                        // rank among moved = number of moved ids larger than this one
-                        const uint32_t x = s.sx[e & 0xFFFF];
-                        uint32_t rank = 0;
-                        for (uint32_t p2 = sm.size[k]; p2 < L; ++p2) {
-                            const uint32_t e2 = s.pre[k * b + p2];
-                            if (!(e2 & kHit) && s.sx[e2 & 0xFFFF] > x) ++rank;
-                        }
-                        const uint32_t mvv = a.dmoves[size_t(k) * a.B + rank];
+                        const uint32_t mvv = s.sinfo[e & 0xFFFF];  // (r, q) from G
                         const uint32_t r = mvv & 0xFF, q = mvv >> 8;
                         dst = sm.noff[r] + (sm.lenk[r]) + q;
                         s.fin[dst] = (e & 0xFFFF) | (r << 16);
@@ -862,7 +907,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         }
         __syncthreads();
 
-        LSG_PHASE(5)
+        LSG_PHASE(7)
         // ---------------- I: buffer advance, nodes in parallel
         if (a.remap) {  // tagged hits form each list's prefix: one re-key run
             // their new keys fall in (g, g+2S): aggregate the bucket bits in a
@@ -874,14 +919,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 const uint32_t e = s.fin[p];
                 if (!(e & kHit)) continue;
                 const uint32_t j = e & 0xFFFF, k = (e >> 16) & 0xFF;
-                const uint32_t x = s.sx[j], nu = s.snu[j], rank = nrrow[j];
+                const uint32_t x = s.sx[j], pk = s.snu[j];
+                const uint32_t nu = pk == kNever ? kNever : key_step(a, pk), rank = pk - nu * a.B;
                 const uint32_t wd = nu >> 5;
                 if (nu != kNever && wd >= wbase && wd - wbase < kWinWords) {
-                    a.key[size_t(k) * a.D + x] = nu * a.B + rank;
+                    a.key[size_t(k) * a.D + x] = pk;
                     atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
                     atomicOr(&sm.win[k][wd - wbase], 1u << (nu & 31));
                 } else {
-                    set_key(a, sm, k, x, nu, rank);
+                    set_key(a, sm, k, x, pk);
                 }
             }
             __syncthreads();
@@ -895,7 +941,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
             }
             __syncthreads();
         }
-        LSG_PHASE(6)
+        LSG_PHASE(8)
         for (uint32_t k = w; k < N; k += kWarps) {
             const uint32_t begin = sm.noff[k] + (a.remap ? sm.size[k] : 0u), end = sm.noff[k + 1];
             // a miss run may span chunks: insert as we go, evict once when the
@@ -935,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     if (hitrun && pending) flush();  // the miss run before it ends here
                     if (mine) {
                         const uint32_t x = s.sx[j];
-                        set_key(a, sm, k, x, s.snu[j], nrrow[j]);
+                        set_key(a, sm, k, x, s.snu[j]);
                         if (!hitrun) atomicOr(&a.hm[x], 1u << k);
                     }
                     __syncwarp();
@@ -950,12 +996,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
             if (pending) flush();
         }
         __syncthreads();
-        LSG_PHASE(7)
+        LSG_PHASE(9)
         gbase += len;
     }
 #undef LSG_PHASE
     if (a.prof && tid == 0)
-        for (int q = 0; q < 8; ++q) a.prof[q] = pacc[q];
+        for (int q = 0; q < 10; ++q) a.prof[q] = pacc[q];
 }
 
 }  // namespace
@@ -998,12 +1044,8 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.infbm = sc.get<uint32_t>(size_t(dm.N) * a.infw);
     a.smul = sc.get<uint32_t>(size_t(dm.B) * dm.N);
     a.sx = sc.get<uint32_t>(size_t(dm.B) * std::max<uint32_t>(dm.N, 8u));  // D8 rows are 8 words
-    a.mpos = sc.get<uint32_t>(size_t(dm.N) * dm.b);
-    a.mres = sc.get<uint32_t>(dm.B);
-    a.mv = sc.get<uint32_t>(dm.B);
     a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B);
-    if (!nu || !sb || !nr || !a.bm || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.mpos || !a.mres ||
-        !a.mv || !a.dmoves)
+    if (!nu || !sb || !nr || !a.bm || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.dmoves)
         return set_error(kInternal, "plan: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(dm.N) * dm.D * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.hm, 0, dm.D * 4, st));
@@ -1029,6 +1071,7 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.nu = nu;
     a.sb = sb;
     a.nr = nr;
+    a.bdiv = dm.B >= 2 ? ~0ull / dm.B + 1 : 0;
     a.items = d_items;
     a.node_off = d_node_off;
     a.fb = d_fb;
@@ -1042,26 +1085,29 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     if (a.prof) LSG_CUDA(cudaMemsetAsync(a.prof, 0, (16 + 256) * 8, st));
     if (smem_items) {
         const size_t smem = size_t(6) * dm.B * 4;
-        LSG_CUDA(cudaFuncSetAttribute(k_plan_loop<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        k_plan_loop<true><<<1, kThreads, smem, st>>>(a);
+        auto kern = dm.N <= 8 ? k_plan_loop<true, true> : k_plan_loop<true, false>;
+        LSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<1, kThreads, smem, st>>>(a);
     } else {
-        k_plan_loop<false><<<1, kThreads, 0, st>>>(a);
+        auto kern = dm.N <= 8 ? k_plan_loop<false, true> : k_plan_loop<false, false>;
+        kern<<<1, kThreads, 0, st>>>(a);
     }
     LSG_LAUNCH_CHECK("k_plan_loop");
     if (a.prof) {
         unsigned long long h[16 + 256];
         LSG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof h, cudaMemcpyDeviceToHost, st));
         LSG_CUDA(cudaStreamSynchronize(st));
-        const char* names[8] = {"A load/classify", "B/C ranks", "D multi pass", "E/F fetch fill",
-                                "G balance", "H lists", "I1 hit rekey", "I2 fetch runs+evict"};
+        const char* names[10] = {"A load/classify", "B/C ranks", "D multi pass", "E positions/fetch ranks",
+                                 "F pre-balance lists", "G1 balance moves", "G2 donor ranks", "H lists",
+                                 "I1 hit rekey", "I2 fetch runs+evict"};
         unsigned long long tot = 0;
-        for (int q = 0; q < 8; ++q) tot += h[q];
+        for (int q = 0; q < 10; ++q) tot += h[q];
 
-        fprintf(stderr, "[lsg profile] D: %llu multi-holder items (%.1f cyc/item incl. barrier)\n", h[8],
-                double(h[2]) / double(h[8] ? h[8] : 1));
+        fprintf(stderr, "[lsg profile] D: %llu multi-holder items (%.1f cyc/item incl. barrier)\n", h[12],
+                double(h[2]) / double(h[12] ? h[12] : 1));
         fprintf(stderr, "[lsg profile] plan loop T=%llu steps, %.1f Mcycles total\n",
                 (unsigned long long)dm.T, tot / 1e6);
-        for (int q = 0; q < 8; ++q)
+        for (int q = 0; q < 10; ++q)
             fprintf(stderr, "[lsg profile]   %-22s %10.1f kcyc  %6.2f%%  %8.0f cyc/step\n", names[q],
                     h[q] / 1e3, 100.0 * h[q] / (tot ? tot : 1), double(h[q]) / double(dm.T ? dm.T : 1));
     }

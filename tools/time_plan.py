@@ -15,7 +15,10 @@ CFGS = {
     "cfg5_N32_E3": (1 << 20, 3, 32, 512, (1 << 20) // 64),
     "cfg5_N32_E10": (1 << 20, 10, 32, 512, (1 << 20) // 64),
 }
-names = sys.argv[1:] or list(CFGS)
+if __name__ != "__main__":
+    names = []
+else:
+    names = sys.argv[1:] or list(CFGS)
 for name in names:
     D, E, N, b, C = CFGS[name]
     pc = ls.PipelineConfig(trace=ls.TraceConfig(D, E, N, b, 42, True), buffer_capacity=C)
