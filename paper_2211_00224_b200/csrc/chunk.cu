@@ -95,6 +95,19 @@ __global__ void k_plan_reads(ReadArgs a) {
     }
 }
 
+// longest list of the plan (sizes the per-warp sort slices)
+__global__ void k_max_list(const uint32_t* __restrict__ node_off, uint32_t T, uint32_t N, uint32_t* out) {
+    uint32_t m = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < uint64_t(T) * N;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t g = uint32_t(i / N), k = uint32_t(i % N);
+        const uint32_t* off = node_off + size_t(g) * (N + 1);
+        m = max(m, off[k + 1] - off[k]);
+    }
+    m = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 }  // namespace
 
 int plan_reads_device(const uint32_t* d_items, const uint32_t* d_node_off, uint32_t T, uint32_t N,
@@ -105,7 +118,20 @@ int plan_reads_device(const uint32_t* d_items, const uint32_t* d_node_off, uint3
     if (chunked && thr == 0) return set_error(kValidation, "plan_chunks: threshold must be >= 1");
     ReadArgs a{d_items, d_node_off, T, N, S, B, keep, 1, chunked, uint32_t(std::min<uint64_t>(thr, 0xFFFFFFFFu)),
                rstart, rend, rcount, needed, redundant};
-    while (a.P2 < B) a.P2 <<= 1;  // a node list never exceeds its step
+    uint32_t lmax = B;  // a node list never exceeds its step
+    if (B > 4096) {     // wide steps: size the slices by the longest list
+        Scratch sc(st);
+        uint32_t* d_m = sc.get<uint32_t>(1);
+        if (!d_m) return set_error(kInternal, "plan_reads: scratch allocation failed");
+        LSG_CUDA(cudaMemsetAsync(d_m, 0, 4, st));
+        k_max_list<<<grid_for(uint64_t(T) * N, 256, 592), 256, 0, st>>>(d_node_off, T, N, d_m);
+        LSG_LAUNCH_CHECK("k_max_list");
+        LSG_CUDA(cudaMemcpyAsync(&lmax, d_m, 4, cudaMemcpyDeviceToHost, st));
+        LSG_CUDA(cudaStreamSynchronize(st));
+    }
+    while (a.P2 < lmax) a.P2 <<= 1;
+    if (size_t(a.P2) * 4 > 200u * 1024)
+        return set_error(kCapability, "plan_reads: a node list is too long for the device chunk planner");
     const uint32_t wpb = std::max<uint32_t>(1, std::min<uint32_t>(8, (96u * 1024) / (4 * a.P2)));
     const size_t smem = size_t(wpb) * a.P2 * 4;
     LSG_CUDA(cudaFuncSetAttribute(k_plan_reads, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

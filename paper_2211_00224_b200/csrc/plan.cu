@@ -1007,19 +1007,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
 }  // namespace
 
 
+int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, const uint32_t* d_trace,
+                     const uint32_t* d_order, const uint32_t* d_nu, uint32_t* d_items, uint32_t* d_node_off,
+                     uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status, cudaStream_t st);
+
 int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, const uint32_t* d_trace,
                      const uint32_t* d_order, const uint32_t* d_inv, uint32_t* d_items,
                      uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
                      cudaStream_t st) {
-    if (dm.N > kMaxN)
-        return set_error(kCapability, "plan: device planner supports num_nodes <= 32 in this build");
-    if (dm.B > kMaxB)
-        return set_error(kCapability, "plan: device planner supports global batch <= 16384 in this build");
-    if (dm.T * dm.B >= 0xFFFFFFF0ull)  // packed resident keys: step * B + rank
-        return set_error(kCapability, "plan: steps x global batch must stay below 2^32");
+    // wide worlds (N > 32, global batch > 16384, or packed keys beyond 32
+    // bits) run the cluster step loop of plan_wide.cu; LSG_PLAN_WIDE=1 forces
+    // it for any shape (parity tests of that path on small configs)
+    const char* fw = std::getenv("LSG_PLAN_WIDE");
+    const bool wide = dm.N > kMaxN || dm.B > kMaxB || dm.T * dm.B >= 0xFFFFFFF0ull || (fw && fw[0] == '1');
     Scratch sc(st);
     const size_t EK = size_t(dm.E) * dm.keep;
     uint32_t* nu = sc.get<uint32_t>(EK);
+    if (wide) {
+        if (!nu) return set_error(kInternal, "plan: scratch allocation failed");
+        k_nextuse<<<dim3(grid_for(dm.keep, 256, 1024), dm.E), 256, 0, st>>>(
+            d_trace, d_order, d_inv, dm.E, uint32_t(dm.keep), uint32_t(dm.D), uint32_t(dm.S), uint32_t(dm.B), nu);
+        LSG_LAUNCH_CHECK("k_nextuse");
+        return plan_wide_device(dm, C, remap, balance, d_trace, d_order, nu, d_items, d_node_off, d_fb, d_fa,
+                                d_status, st);
+    }
     uint32_t* sb = sc.get<uint32_t>(EK);
     uint32_t* nr = sc.get<uint32_t>(EK);
     LoopArgs a{};

@@ -1,0 +1,1004 @@
+// plan_wide.cu — K6 for wide jobs: the planner step loop of plan_schedule
+// (pipeline.cpp:68-118) when the simulated world has more than 32 nodes or a
+// global batch beyond one CTA's shared memory (BASELINE cfg5: 1,048,576 ids,
+// 32-256 logical ranks, b=512, so B = N*b reaches 131,072 ids per step).
+//
+// Same semantics as k_plan_loop (plan.cu), bit-exact with remap_step
+// (locality.cpp:7-42) / slice_step (:57-73), balance_step (balance.cpp:10-39)
+// and ClairvoyantBuffer::access (buffer.cpp:37-46), but laid out for width:
+//
+//  * one persistent thread-block CLUSTER (16 CTAs x 512 threads when the
+//    device allows it) walks the T dependent steps; the phases of a step are
+//    separated by cluster barriers, cross-CTA prefix sums read the other CTAs'
+//    shared-memory totals through DSMEM;
+//  * holder masks are W = ceil(N/32) words per id;
+//  * per-item work (classification, single-holder ranks, positions) is spread
+//    over every warp of the cluster; the multi-holder remap is the only serial
+//    pass (one warp, lanes = candidate holders, REDUX.MIN on (count, node));
+//  * balance is simulated on the N fetch counts in rounds: every round pairs
+//    the i-th first-argmax node with the i-th first-argmin node, which is the
+//    reference's move sequence (the argmax/argmin only change when a level
+//    set is exhausted); donor d's q-th move gives its q-th largest fetch id;
+//  * each node's buffer is a dense slot array of (next-use step, id) plus a
+//    per-node count of residents per next-use step ("bins"). A miss run
+//    inserts its ids, then evicts the (size - C)+ largest (key, id): the
+//    threshold bin comes from the counts (walked from the top, 32 bins per
+//    ballot), one scan of the slots flags everything above it, a radix select
+//    on the ids picks the largest ones inside the threshold bin (equal keys
+//    evict the larger id first, buffer.cpp:27-28), and the slot array is
+//    compacted by moving survivors from the tail into the holes.
+//
+// Node-level work (lists, buffer advance) runs one warp per node.
+#include <cooperative_groups.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace lsg {
+
+namespace {
+
+constexpr int kWT = 512;                // threads per CTA
+constexpr int kWW = kWT / 32;           // warps per CTA
+constexpr uint32_t kWMaxN = 256;        // simulated nodes
+constexpr uint32_t kSortCap = 512;      // donor fetch entries sorted in shared memory
+constexpr uint32_t kHitM = 0x80000000u;
+constexpr uint32_t kIdM = 0x7FFFFFFFu;
+constexpr uint32_t kClsSingle = 1u << 30;
+constexpr uint32_t kClsMulti = 2u << 30;
+
+struct WideArgs {
+    uint32_t D, N, W, b, B, S, keep, T, C;
+    uint32_t SC;                      // slots per node (C + B)
+    uint32_t EBW;                     // eviction-flag words per node
+    uint32_t MBW;                     // moved-flag words per node
+    int remap, balance;
+    const uint32_t* trace;            // [E][keep]
+    const uint32_t* order;            // [E]
+    const uint32_t* nu;               // [E*keep] next-use step, execution order
+    uint32_t* hm;                     // [D][W] holder masks
+    uint32_t* where;                  // [N][D] slot of a resident id, kNone otherwise
+    unsigned long long* slot;         // [N][SC] (key << 32 | id), dense in [0, size)
+    uint32_t* cnt;                    // [N][T+1] residents per key bin (bin T = never used)
+    uint32_t* nst;                    // [N][4] size, top finite key
+    uint32_t* evb;                    // [N][EBW] eviction flags (zero between uses)
+    uint32_t* cand;                   // [N][SC] threshold-bin slots
+    uint32_t* holes;                  // [N][SC] compaction holes
+    uint32_t* movedbm;                // [N][MBW] moved pre-list positions (zero between uses)
+    // per-step scratch, batch position j
+    uint32_t* jx;                     // [B] id
+    uint32_t* jnu;                    // [B] next-use step
+    uint32_t* jmask;                  // [B][W] holder masks at step start
+    uint32_t* jcls;                   // [B] class | holder
+    uint32_t* jS;                     // [B] singles: S_k(j); multi: multi index
+    uint32_t* pre;                    // [B] pre-balance lists (j | hit)
+    uint32_t* fin;                    // [B] final lists (j | hit)
+    uint32_t* mj;                     // [B] multi index -> j
+    uint32_t* mpo;                    // [B] multi index -> pair offset
+    uint32_t* mhc;                    // [B] multi index -> candidate pairs
+    uint32_t* pairs;                  // [B*N] (S_k << 10 | k), S_k < b
+    uint32_t* massign;                // [B] (position << 10 | node) or kNone
+    uint32_t* mpos;                   // [N][b] j of node k's assigned multis, in order
+    uint32_t* recv;                   // [N][b] donor's q-th move: (ii << 10 | recipient)
+    uint32_t* items;                  // [E*keep] output
+    uint32_t* node_off;               // [T][N+1] output
+    uint32_t* fb;                     // [T][N] output (may be null)
+    uint32_t* fa;                     // [T][N] output (may be null)
+    uint32_t* status;
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt_w() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, v, d);
+        if (lane >= uint32_t(d)) v += o;
+    }
+    return v;
+}
+
+__device__ __forceinline__ uint32_t bin_of(uint32_t key, uint32_t T) { return key == kNever ? T : key; }
+
+// Remove the m = size - C largest (key, id) residents of node k (one warp).
+__device__ void wide_evict(const WideArgs& a, uint32_t k, uint32_t& bsz, uint32_t& top, uint32_t g,
+                           uint32_t lane, uint32_t* hist) {
+    const uint32_t lt = lanemask_lt_w();
+    const uint32_t m = bsz - a.C;
+    uint32_t* cntk = a.cnt + size_t(k) * (a.T + 1);
+    unsigned long long* sk = a.slot + size_t(k) * a.SC;
+    uint32_t* evk = a.evb + size_t(k) * a.EBW;
+    uint32_t* cak = a.cand + size_t(k) * a.SC;
+    // ---- threshold bin: never-used first, then finite bins from the top
+    uint32_t tstar = 0, r = 0;
+    const uint32_t nev = __ldcg(&cntk[a.T]);
+    if (nev >= m) {
+        tstar = a.T;
+        r = m;
+    } else {
+        uint32_t acc = nev;
+        int32_t hi = int32_t(top);
+        bool found = false;
+        while (!found) {
+            if (hi <= int32_t(g)) {  // only current/stale keys left: impossible for a miss run
+                if (lane == 0) atomicOr(a.status, 8u);
+                return;
+            }
+            const int32_t bn = hi - int32_t(lane);
+            const uint32_t v = bn > int32_t(g) ? __ldcg(&cntk[bn]) : 0u;
+            const uint32_t incl = warp_incl_scan(v, lane);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, acc + incl >= m);
+            if (bal) {
+                const uint32_t L = __ffs(bal) - 1;
+                const uint32_t before = __shfl_sync(0xFFFFFFFFu, incl - v, L);
+                tstar = uint32_t(hi - int32_t(L));
+                r = m - (acc + before);
+                found = true;
+            } else {
+                acc += __shfl_sync(0xFFFFFFFFu, incl, 31);
+                hi -= 32;
+            }
+        }
+    }
+    // ---- one scan: flag bins above the threshold, collect the threshold bin
+    uint32_t ncand = 0;
+    for (uint32_t s0 = 0; s0 < bsz; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const bool valid = s < bsz;
+        const unsigned long long v = valid ? __ldcg(&sk[s]) : 0ull;
+        const uint32_t bn = bin_of(uint32_t(v >> 32), a.T);
+        const bool ev = valid && bn > tstar, cd = valid && bn == tstar;
+        const uint32_t evw = __ballot_sync(0xFFFFFFFFu, ev);
+        if (lane == 0) evk[s0 >> 5] = evw;
+        const uint32_t cb = __ballot_sync(0xFFFFFFFFu, cd);
+        if (cd) cak[ncand + __popc(cb & lt)] = s;
+        ncand += __popc(cb);
+    }
+    __syncwarp();
+    // ---- the r largest ids of the threshold bin (ids are distinct per node)
+    uint32_t thr = 0;
+    if (r < ncand) {
+        uint32_t prefix = 0, pmask = 0, rem = r;
+        for (int sh = 24; sh >= 0; sh -= 8) {
+            for (uint32_t q = lane; q < 256; q += 32) hist[q] = 0;
+            __syncwarp();
+            for (uint32_t q = lane; q < ncand; q += 32) {
+                const uint32_t id = uint32_t(__ldcg(&sk[__ldcg(&cak[q])]));
+                if ((id & pmask) == prefix) atomicAdd(&hist[(id >> sh) & 255u], 1u);
+            }
+            __syncwarp();
+            // lane l owns digits 255-8l .. 248-8l (descending)
+            uint32_t hv[8], lsum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                hv[q] = hist[255 - 8 * lane - q];
+                lsum += hv[q];
+            }
+            const uint32_t incl = warp_incl_scan(lsum, lane);
+            const uint32_t excl = incl - lsum;
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, excl < rem && incl >= rem);
+            const uint32_t L = __ffs(bal) - 1;
+            uint32_t dsel = 0, above = 0;
+            if (lane == L) {
+                uint32_t run = excl;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (run + hv[q] >= rem) {
+                        dsel = 255 - 8 * lane - q;
+                        above = run;
+                        break;
+                    }
+                    run += hv[q];
+                }
+            }
+            dsel = __shfl_sync(0xFFFFFFFFu, dsel, L);
+            above = __shfl_sync(0xFFFFFFFFu, above, L);
+            rem -= above;
+            prefix |= dsel << sh;
+            pmask |= 255u << sh;
+            __syncwarp();
+        }
+        thr = prefix;  // the r-th largest id of the bin
+    }
+    for (uint32_t q = lane; q < ncand; q += 32) {
+        const uint32_t s = __ldcg(&cak[q]);
+        if (r >= ncand || uint32_t(__ldcg(&sk[s])) >= thr) atomicOr(&evk[s >> 5], 1u << (s & 31));
+    }
+    __syncwarp();
+    // ---- drop the flagged residents; holes below the new size
+    const uint32_t newsize = bsz - m;
+    uint32_t* hk = a.holes + size_t(k) * a.SC;
+    uint32_t nh = 0;
+    const uint32_t kw = k >> 5, kb = 1u << (k & 31);
+    for (uint32_t s0 = 0; s0 < bsz; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const uint32_t word = __ldcg(&evk[s0 >> 5]);
+        const bool ev = s < bsz && ((word >> lane) & 1u);
+        if (ev) {
+            const unsigned long long v = __ldcg(&sk[s]);
+            const uint32_t x = uint32_t(v);
+            a.where[size_t(k) * a.D + x] = kNone;
+            atomicAnd(&a.hm[size_t(x) * a.W + kw], ~kb);
+            atomicSub(&cntk[bin_of(uint32_t(v >> 32), a.T)], 1u);
+        }
+        const bool hole = ev && s < newsize;
+        const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hole);
+        if (hole) hk[nh + __popc(hb & lt)] = s;
+        nh += __popc(hb);
+    }
+    __syncwarp();
+    // ---- survivors from the tail fill the holes
+    uint32_t nmv = 0;
+    for (uint32_t s0 = newsize & ~31u; s0 < bsz; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        const uint32_t word = __ldcg(&evk[s0 >> 5]);
+        const bool mv = s >= newsize && s < bsz && !((word >> lane) & 1u);
+        const uint32_t mb = __ballot_sync(0xFFFFFFFFu, mv);
+        if (mv) {
+            const uint32_t d = __ldcg(&hk[nmv + __popc(mb & lt)]);
+            const unsigned long long v = __ldcg(&sk[s]);
+            sk[d] = v;
+            a.where[size_t(k) * a.D + uint32_t(v)] = d;
+        }
+        nmv += __popc(mb);
+    }
+    if (nmv != nh && lane == 0) atomicOr(a.status, 16u);
+    __syncwarp();
+    for (uint32_t wd = lane; wd < (bsz + 31) / 32; wd += 32) evk[wd] = 0;
+    bsz = newsize;
+    if (tstar != a.T) top = tstar;
+    __syncwarp();
+}
+
+// Balance (balance.cpp:10-39) on the fetch counts in rounds (one warp).
+// Writes outk/ink and, when recv != null, recv[d*b + q] = (ii << 10 | r):
+// donor d's q-th move goes to recipient r as its ii-th appended fetch.
+__device__ void wide_balance(uint32_t N, uint32_t b, const uint32_t* fcnt, uint32_t* outk, uint32_t* ink,
+                             uint32_t* rl, uint32_t* rl2, uint32_t* recv, uint32_t* status, uint32_t lane) {
+    const uint32_t lt = lanemask_lt_w();
+    uint32_t cv[8], oq[8], iq[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t k = q * 32 + lane;
+        cv[q] = k < N ? fcnt[k] : 0u;
+        oq[q] = iq[q] = 0;
+    }
+    const uint32_t NQ = (N + 31) / 32;
+    for (;;) {
+        uint32_t mx = 0, mn = 0xFFFFFFFFu;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (uint32_t(q) < NQ && q * 32 + lane < N) {
+                mx = max(mx, cv[q]);
+                mn = min(mn, cv[q]);
+            }
+        }
+        mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+        mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+        if (mx - mn <= 1) break;
+        uint32_t nd = 0, nr = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (uint32_t(q) >= NQ) break;
+            const bool in = q * 32 + lane < N;
+            nd += __popc(__ballot_sync(0xFFFFFFFFu, in && cv[q] == mx));
+            nr += __popc(__ballot_sync(0xFFFFFFFFu, in && cv[q] == mn));
+        }
+        const uint32_t pn = min(nd, nr);
+        uint32_t acc = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (uint32_t(q) >= NQ) break;
+            const uint32_t k = q * 32 + lane;
+            const bool isr = k < N && cv[q] == mn;
+            const uint32_t br = __ballot_sync(0xFFFFFFFFu, isr);
+            if (isr) {
+                const uint32_t rk = acc + __popc(br & lt);
+                if (rk < pn) {
+                    rl[rk] = k;
+                    rl2[rk] = iq[q];
+                    iq[q] += 1;
+                    cv[q] += 1;
+                }
+            }
+            acc += __popc(br);
+        }
+        __syncwarp();
+        acc = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (uint32_t(q) >= NQ) break;
+            const uint32_t k = q * 32 + lane;
+            const bool isd = k < N && cv[q] == mx;
+            const uint32_t bd = __ballot_sync(0xFFFFFFFFu, isd);
+            if (isd) {
+                const uint32_t rk = acc + __popc(bd & lt);
+                if (rk < pn) {
+                    if (recv) recv[size_t(k) * b + oq[q]] = (rl2[rk] << 10) | rl[rk];
+                    oq[q] += 1;
+                    cv[q] -= 1;
+                }
+            }
+            acc += __popc(bd);
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t k = q * 32 + lane;
+        if (k < N) {
+            outk[k] = oq[q];
+            ink[k] = iq[q];
+            if (oq[q] && iq[q]) atomicOr(status, 32u);  // a recipient became a donor
+        }
+    }
+}
+
+// exclusive prefix of v[0..n) into out[0..n], out[n] = total (one warp)
+__device__ __forceinline__ void warp_prefix(const uint32_t* v, uint32_t* out, uint32_t n, uint32_t lane) {
+    uint32_t run = 0;
+    for (uint32_t k0 = 0; k0 < n; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const uint32_t x = k < n ? v[k] : 0u;
+        const uint32_t incl = warp_incl_scan(x, lane);
+        if (k < n) out[k] = run + incl - x;
+        run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    }
+    if (lane == 0) out[n] = run;
+}
+
+__global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t P = cl.num_blocks(), c = cl.block_rank();
+    extern __shared__ __align__(16) unsigned char wsm[];
+    const uint32_t N = a.N, W = a.W, b = a.b;
+    unsigned long long* sortb = reinterpret_cast<unsigned long long*>(wsm);  // [kWW][kSortCap]
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sortb + kWW * kSortCap);    // [kWW][256]
+    uint32_t* wc = hist + kWW * 256;      // [kWW][N]
+    uint32_t* cm = wc + kWW * N;          // [kWW][N]
+    uint32_t* ctot = cm + kWW * N;        // [N] CTA totals (read remotely)
+    uint32_t* base = ctot + N;            // [N]
+    uint32_t* tot = base + N;             // [N]
+    uint32_t* mk = tot + N;               // [N]
+    uint32_t* size = mk + N;              // [N]
+    uint32_t* fcnt = size + N;            // [N]
+    uint32_t* lenpre = fcnt + N;          // [N]
+    uint32_t* outk = lenpre + N;          // [N]
+    uint32_t* ink = outk + N;             // [N]
+    uint32_t* M = ink + N;                // [N] serial pass (CTA 0, read remotely)
+    uint32_t* rl = M + N;                 // [N]
+    uint32_t* rl2 = rl + N;               // [N]
+    uint32_t* lenfin = rl2 + N;           // [N]
+    uint32_t* freepre = lenfin + N;       // [N+1]
+    uint32_t* noffpre = freepre + N + 1;  // [N+1]
+    uint32_t* noff = noffpre + N + 1;     // [N+1]
+    __shared__ unsigned long long wsc[kWW];
+    __shared__ unsigned long long ctsc, msbase, mstot;
+    __shared__ uint32_t wsf[kWW];
+    __shared__ uint32_t ctf, fbase, ftot;
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t gw = c * kWW + w, GW = P * kWW;
+    const uint32_t lt = lanemask_lt_w();
+    unsigned long long* my_sort = sortb + w * kSortCap;
+    uint32_t* my_hist = hist + w * 256;
+    size_t gbase = 0;
+
+    for (uint32_t g = 0; g < a.T; ++g) {
+        const uint32_t i = g / a.S, t = g % a.S;
+        const uint32_t lo = t * a.B, len = min(a.B, a.keep - lo);
+        const uint32_t* row = a.trace + size_t(a.order[i]) * a.keep + lo;
+        const uint32_t* nurow = a.nu + size_t(i) * a.keep + lo;
+        const uint32_t R = ((len + GW * 32 - 1) / (GW * 32)) * 32;
+        const uint32_t j0 = min(gw * R, len), j1 = min(j0 + R, len);
+
+        // ------------------------------------------------ A: load + classify
+        for (uint32_t k = lane; k < N; k += 32) {
+            wc[w * N + k] = 0;
+            cm[w * N + k] = 0;
+        }
+        unsigned long long msc = 0;
+        __syncwarp();
+        for (uint32_t cb = j0; cb < j1; cb += 32) {
+            const uint32_t j = cb + lane;
+            const bool valid = j < j1;
+            uint32_t hc = 0, h = 0;
+            if (valid) {
+                const uint32_t x = row[j];
+                a.jx[j] = x;
+                a.jnu[j] = nurow[j];
+                for (uint32_t q = 0; q < W; ++q) {
+                    const uint32_t m = __ldcg(&a.hm[size_t(x) * W + q]);
+                    a.jmask[size_t(j) * W + q] = m;
+                    if (m && hc == 0) h = q * 32 + __ffs(m) - 1;
+                    hc += __popc(m);
+                }
+            }
+            if (a.remap) {
+                const bool single = valid && hc == 1, multi = valid && hc >= 2;
+                const uint32_t grp = __match_any_sync(0xFFFFFFFFu, single ? h : 0x10000u + lane);
+                if (single && lane == uint32_t(__ffs(grp) - 1)) wc[w * N + h] += __popc(grp);
+                const uint32_t mb = __ballot_sync(0xFFFFFFFFu, multi);
+                const uint32_t hs = __reduce_add_sync(0xFFFFFFFFu, multi ? hc : 0u);
+                msc += (static_cast<unsigned long long>(__popc(mb)) << 32) | hs;
+                if (valid) a.jcls[j] = single ? (kClsSingle | h) : (multi ? kClsMulti : 0u);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) wsc[w] = msc;
+        __syncthreads();
+        if (a.remap) {
+            for (uint32_t k = tid; k < N; k += kWT) {
+                uint32_t s = 0;
+                for (uint32_t w2 = 0; w2 < uint32_t(kWW); ++w2) {
+                    const uint32_t v = wc[w2 * N + k];
+                    wc[w2 * N + k] = s;
+                    s += v;
+                }
+                ctot[k] = s;
+            }
+            if (tid == 0) {
+                unsigned long long s = 0;
+                for (int w2 = 0; w2 < kWW; ++w2) {
+                    const unsigned long long v = wsc[w2];
+                    wsc[w2] = s;
+                    s += v;
+                }
+                ctsc = s;
+            }
+        }
+        cl.sync();  // (1)
+        if (a.remap) {
+            for (uint32_t k = tid; k < N; k += kWT) {
+                uint32_t bs = 0, tt = 0;
+                for (uint32_t c2 = 0; c2 < P; ++c2) {
+                    const uint32_t v = cl.map_shared_rank(ctot, c2)[k];
+                    if (c2 < c) bs += v;
+                    tt += v;
+                }
+                base[k] = bs;
+                tot[k] = tt;
+            }
+            if (tid == 0) {
+                unsigned long long bs = 0, tt = 0;
+                for (uint32_t c2 = 0; c2 < P; ++c2) {
+                    const unsigned long long v = *cl.map_shared_rank(&ctsc, c2);
+                    if (c2 < c) bs += v;
+                    tt += v;
+                }
+                msbase = bs;
+                mstot = tt;
+            }
+            __syncthreads();
+            // ------------------------------- A2: exact single ranks, multi pairs
+            for (uint32_t k = lane; k < N; k += 32) wc[w * N + k] += base[k];
+            unsigned long long mrun = msbase + wsc[w];
+            __syncwarp();
+            for (uint32_t cb = j0; cb < j1; cb += 32) {
+                const uint32_t j = cb + lane;
+                const bool valid = j < j1;
+                const uint32_t cls = valid ? a.jcls[j] : 0u;
+                const bool single = (cls >> 30) == 1u, multi = (cls >> 30) == 2u;
+                const uint32_t h = cls & 0x3FFu;
+                const uint32_t grp = __match_any_sync(0xFFFFFFFFu, single ? h : 0x10000u + lane);
+                const bool leader = single && lane == uint32_t(__ffs(grp) - 1);
+                if (leader) cm[w * N + h] = grp;
+                __syncwarp();
+                if (single) a.jS[j] = wc[w * N + h] + __popc(grp & lt);
+                const uint32_t mb = __ballot_sync(0xFFFFFFFFu, multi);
+                uint32_t hcv = 0;
+                if (multi)
+                    for (uint32_t q = 0; q < W; ++q) hcv += __popc(a.jmask[size_t(j) * W + q]);
+                const uint32_t hinc = warp_incl_scan(hcv, lane);
+                if (multi) {
+                    const uint32_t mi = uint32_t(mrun >> 32) + __popc(mb & lt);
+                    const uint32_t po = uint32_t(mrun) + hinc - hcv;
+                    uint32_t np = 0;
+                    for (uint32_t q = 0; q < W; ++q) {
+                        uint32_t m = a.jmask[size_t(j) * W + q];
+                        while (m) {
+                            const uint32_t k = q * 32 + __ffs(m) - 1;
+                            m &= m - 1;
+                            const uint32_t sk = wc[w * N + k] + __popc(cm[w * N + k] & lt);
+                            if (sk < b) a.pairs[po + np++] = (sk << 10) | k;
+                        }
+                    }
+                    a.mj[mi] = j;
+                    a.mpo[mi] = po;
+                    a.mhc[mi] = np;
+                    a.jS[j] = mi;
+                }
+                __syncwarp();
+                if (leader) {
+                    wc[w * N + h] += __popc(grp);
+                    cm[w * N + h] = 0;
+                }
+                mrun += (static_cast<unsigned long long>(__popc(mb)) << 32) |
+                        __shfl_sync(0xFFFFFFFFu, hinc, 31);
+                __syncwarp();
+            }
+        }
+        cl.sync();  // (2)
+
+        // --------------------------- B: serial multi-holder pass (CTA 0, warp 0)
+        if (a.remap && c == 0 && w == 0) {
+            for (uint32_t k = lane; k < N; k += 32) M[k] = 0;
+            __syncwarp();
+            const uint32_t nm = uint32_t(mstot >> 32);
+            for (uint32_t mi = 0; mi < nm; ++mi) {
+                const uint32_t np = __ldcg(&a.mhc[mi]), po = __ldcg(&a.mpo[mi]);
+                uint32_t best = 0xFFFFFFFFu;
+                for (uint32_t t0 = 0; t0 < np; t0 += 32) {
+                    if (t0 + lane < np) {
+                        const uint32_t pr = __ldcg(&a.pairs[po + t0 + lane]);
+                        const uint32_t k = pr & 0x3FFu;
+                        const uint32_t cc = min(b, (pr >> 10) + M[k]);
+                        if (cc < b) best = min(best, (cc << 10) | k);
+                    }
+                }
+                best = __reduce_min_sync(0xFFFFFFFFu, best);
+                if (lane == 0) {
+                    if (best != 0xFFFFFFFFu) {
+                        const uint32_t k = best & 0x3FFu;
+                        a.mpos[size_t(k) * b + M[k]] = __ldcg(&a.mj[mi]);
+                        M[k] += 1;
+                    }
+                    a.massign[mi] = best;
+                }
+                __syncwarp();
+            }
+        }
+        cl.sync();  // (3)
+
+        // ---------------------------------- C1: hit / fetch, fetch counts
+        if (a.remap) {
+            for (uint32_t k = tid; k < N; k += kWT) {
+                const uint32_t v = cl.map_shared_rank(M, 0)[k];
+                mk[k] = v;
+                size[k] = v + min(tot[k], b - v);
+            }
+        }
+        for (uint32_t k = lane; k < N; k += 32) wc[w * N + k] = 0;
+        __syncthreads();
+        uint32_t fw = 0;
+        for (uint32_t cb = j0; cb < j1; cb += 32) {
+            const uint32_t j = cb + lane;
+            const bool valid = j < j1;
+            bool hit = false;
+            uint32_t node = 0;
+            if (valid) {
+                if (a.remap) {
+                    const uint32_t cls = a.jcls[j];
+                    if ((cls >> 30) == 1u) hit = a.jS[j] < b - mk[cls & 0x3FFu];
+                    else if ((cls >> 30) == 2u) hit = __ldcg(&a.massign[a.jS[j]]) != 0xFFFFFFFFu;
+                } else {
+                    node = j / b;
+                    hit = (a.jmask[size_t(j) * W + (node >> 5)] >> (node & 31)) & 1u;
+                }
+            }
+            const bool isf = valid && !hit;
+            const uint32_t fbal = __ballot_sync(0xFFFFFFFFu, isf);
+            if (!a.remap) {
+                const uint32_t grp = __match_any_sync(0xFFFFFFFFu, isf ? node : 0x10000u + lane);
+                if (isf && lane == uint32_t(__ffs(grp) - 1)) wc[w * N + node] += __popc(grp);
+            }
+            fw += __popc(fbal);
+            __syncwarp();
+        }
+        if (lane == 0) wsf[w] = fw;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t s = 0;
+            for (int w2 = 0; w2 < kWW; ++w2) {
+                const uint32_t v = wsf[w2];
+                wsf[w2] = s;
+                s += v;
+            }
+            ctf = s;
+        }
+        if (!a.remap)
+            for (uint32_t k = tid; k < N; k += kWT) {
+                uint32_t s = 0;
+                for (uint32_t w2 = 0; w2 < uint32_t(kWW); ++w2) s += wc[w2 * N + k];
+                ctot[k] = s;
+            }
+        cl.sync();  // (4)
+        if (tid == 0) {
+            uint32_t bs = 0, tt = 0;
+            for (uint32_t c2 = 0; c2 < P; ++c2) {
+                const uint32_t v = *cl.map_shared_rank(&ctf, c2);
+                if (c2 < c) bs += v;
+                tt += v;
+            }
+            fbase = bs;
+            ftot = tt;
+        }
+        if (!a.remap)
+            for (uint32_t k = tid; k < N; k += kWT) {
+                uint32_t s = 0;
+                for (uint32_t c2 = 0; c2 < P; ++c2) s += cl.map_shared_rank(ctot, c2)[k];
+                fcnt[k] = s;
+            }
+        __syncthreads();
+        // node tables (warp 0 of every CTA; identical everywhere)
+        if (w == 0) {
+            if (a.remap) {
+                for (uint32_t k = lane; k < N; k += 32) rl[k] = b - size[k];
+                __syncwarp();
+                warp_prefix(rl, freepre, N, lane);
+                __syncwarp();
+                const uint32_t F = ftot;
+                if (lane == 0 && F > freepre[N]) atomicOr(a.status, 64u);  // ran out of capacity
+                for (uint32_t k = lane; k < N; k += 32) {
+                    const uint32_t f = F > freepre[k] ? min(b - size[k], F - freepre[k]) : 0u;
+                    fcnt[k] = f;
+                    lenpre[k] = size[k] + f;
+                }
+            } else {
+                for (uint32_t k = lane; k < N; k += 32) {
+                    const uint32_t l = len > k * b ? min(b, len - k * b) : 0u;
+                    lenpre[k] = l;
+                    size[k] = l - fcnt[k];
+                }
+            }
+            __syncwarp();
+            warp_prefix(lenpre, noffpre, N, lane);
+            __syncwarp();
+        }
+        __syncthreads();
+        // ------------------- C2: pre-balance positions (+ balance on warp 0)
+        if (w == 0) {
+            if (a.balance) {
+                wide_balance(N, b, fcnt, outk, ink, rl, rl2, c == 0 ? a.recv : nullptr, a.status, lane);
+            } else {
+                for (uint32_t k = lane; k < N; k += 32) outk[k] = ink[k] = 0;
+            }
+            __syncwarp();
+            for (uint32_t k = lane; k < N; k += 32) lenfin[k] = lenpre[k] - outk[k] + ink[k];
+            __syncwarp();
+            warp_prefix(lenfin, noff, N, lane);
+        }
+        {
+            uint32_t fr = fbase + wsf[w];
+            for (uint32_t cb = j0; cb < j1; cb += 32) {
+                const uint32_t j = cb + lane;
+                const bool valid = j < j1;
+                bool hit = false;
+                uint32_t node = 0, pos = 0;
+                if (valid) {
+                    if (a.remap) {
+                        const uint32_t cls = a.jcls[j];
+                        if ((cls >> 30) == 1u) {
+                            const uint32_t h = cls & 0x3FFu, S = a.jS[j];
+                            hit = S < b - mk[h];
+                            if (hit) {
+                                // multis assigned to h before j
+                                const uint32_t* mp = a.mpos + size_t(h) * b;
+                                uint32_t l0 = 0, l1 = mk[h];
+                                while (l0 < l1) {
+                                    const uint32_t mid = (l0 + l1) >> 1;
+                                    if (__ldcg(&mp[mid]) < j) l0 = mid + 1; else l1 = mid;
+                                }
+                                node = h;
+                                pos = S + l0;
+                            }
+                        } else if ((cls >> 30) == 2u) {
+                            const uint32_t best = __ldcg(&a.massign[a.jS[j]]);
+                            if (best != 0xFFFFFFFFu) {
+                                hit = true;
+                                node = best & 0x3FFu;
+                                pos = best >> 10;
+                            }
+                        }
+                    } else {
+                        node = j / b;
+                        pos = j - node * b;
+                        hit = (a.jmask[size_t(j) * W + (node >> 5)] >> (node & 31)) & 1u;
+                    }
+                }
+                const bool isf = valid && !hit;
+                const uint32_t fbal = __ballot_sync(0xFFFFFFFFu, isf);
+                if (isf && a.remap) {
+                    const uint32_t f = fr + __popc(fbal & lt);
+                    uint32_t l0 = 0, l1 = N;  // first k with freepre[k+1] > f
+                    while (l0 < l1) {
+                        const uint32_t mid = (l0 + l1) >> 1;
+                        if (freepre[mid + 1] > f) l1 = mid; else l0 = mid + 1;
+                    }
+                    node = l0;
+                    pos = size[node] + f - freepre[node];
+                }
+                if (valid) a.pre[noffpre[node] + pos] = j | (hit ? kHitM : 0u);
+                fr += __popc(fbal);
+            }
+        }
+        cl.sync();  // (5)
+
+        // --------------------------------- D: final lists (one warp per node)
+        for (uint32_t k = gw; k < N; k += GW) {
+            const uint32_t lp = lenpre[k], pb = noffpre[k], fbk = noff[k], nout = outk[k];
+            uint32_t* items = a.items + gbase;
+            if (nout == 0) {
+                for (uint32_t p = lane; p < lp; p += 32) {
+                    const uint32_t it = __ldcg(&a.pre[pb + p]);
+                    a.fin[fbk + p] = it;
+                    items[fbk + p] = __ldcg(&a.jx[it & kIdM]) | (it & kHitM);
+                }
+            } else {
+                uint32_t* mvk = a.movedbm + size_t(k) * a.MBW;
+                const bool fits = fcnt[k] <= kSortCap;
+                uint32_t nf = 0;
+                for (uint32_t p0 = 0; p0 < lp; p0 += 32) {
+                    const uint32_t p = p0 + lane;
+                    const uint32_t it = p < lp ? __ldcg(&a.pre[pb + p]) : kHitM;
+                    const bool isf = !(it & kHitM);
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, isf);
+                    if (isf && fits)
+                        my_sort[nf + __popc(bal & lt)] =
+                            (static_cast<unsigned long long>(__ldcg(&a.jx[it])) << 32) | p;
+                    nf += __popc(bal);
+                }
+                if (nf != fcnt[k] && lane == 0) atomicOr(a.status, 128u);
+                auto move_one = [&](uint32_t q, uint32_t p) {
+                    atomicOr(&mvk[p >> 5], 1u << (p & 31));
+                    const uint32_t rec = __ldcg(&a.recv[size_t(k) * b + q]);
+                    const uint32_t r = rec & 0x3FFu, ii = rec >> 10;
+                    const uint32_t dest = noff[r] + lenpre[r] + ii;
+                    const uint32_t it = __ldcg(&a.pre[pb + p]);
+                    a.fin[dest] = it;
+                    items[dest] = __ldcg(&a.jx[it & kIdM]);
+                };
+                if (fits) {
+                    uint32_t P2 = 1;
+                    while (P2 < nf) P2 <<= 1;
+                    for (uint32_t q = nf + lane; q < P2; q += 32) my_sort[q] = 0ull;
+                    __syncwarp();
+                    for (uint32_t sz = 2; sz <= P2; sz <<= 1) {
+                        for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+                            for (uint32_t r = lane; r < P2 / 2; r += 32) {
+                                const uint32_t x0 = 2 * st * (r / st) + (r % st), x1 = x0 + st;
+                                const bool desc = (x0 & sz) == 0;
+                                const unsigned long long u = my_sort[x0], v = my_sort[x1];
+                                if ((u < v) == desc) {
+                                    my_sort[x0] = v;
+                                    my_sort[x1] = u;
+                                }
+                            }
+                            __syncwarp();
+                        }
+                    }
+                    for (uint32_t q = lane; q < nout; q += 32) move_one(q, uint32_t(my_sort[q]));
+                } else {
+                    // repeated extraction of the largest unmoved fetch id
+                    for (uint32_t q = 0; q < nout; ++q) {
+                        unsigned long long best = 0;
+                        for (uint32_t p0 = 0; p0 < lp; p0 += 32) {
+                            const uint32_t p = p0 + lane;
+                            if (p < lp) {
+                                const uint32_t it = __ldcg(&a.pre[pb + p]);
+                                const bool mv = (__ldcg(&mvk[p >> 5]) >> (p & 31)) & 1u;
+                                if (!(it & kHitM) && !mv)
+                                    best = max(best, (static_cast<unsigned long long>(__ldcg(&a.jx[it]) + 1ull) << 32) | p);
+                            }
+                        }
+#pragma unroll
+                        for (int d = 16; d > 0; d >>= 1) best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, d));
+                        if (lane == 0) move_one(q, uint32_t(best));
+                        __syncwarp();
+                    }
+                }
+                __syncwarp();
+                uint32_t kept = 0;
+                for (uint32_t p0 = 0; p0 < lp; p0 += 32) {
+                    const uint32_t p = p0 + lane;
+                    const bool valid = p < lp;
+                    const uint32_t it = valid ? __ldcg(&a.pre[pb + p]) : 0u;
+                    const bool keep = valid && !((__ldcg(&mvk[p >> 5]) >> (p & 31)) & 1u);
+                    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+                    if (keep) {
+                        const uint32_t dst = fbk + kept + __popc(bal & lt);
+                        a.fin[dst] = it;
+                        items[dst] = __ldcg(&a.jx[it & kIdM]) | (it & kHitM);
+                    }
+                    kept += __popc(bal);
+                }
+                __syncwarp();
+                for (uint32_t wd = lane; wd < (lp + 31) / 32; wd += 32) mvk[wd] = 0;
+            }
+            if (lane == 0) {
+                a.node_off[size_t(g) * (N + 1) + k] = fbk;
+                if (k == N - 1) a.node_off[size_t(g) * (N + 1) + N] = noff[N];
+                if (a.fb) a.fb[size_t(g) * N + k] = fcnt[k];
+                if (a.fa) a.fa[size_t(g) * N + k] = fcnt[k] - outk[k] + ink[k];
+            }
+        }
+        cl.sync();  // (6)
+
+        // ------------------------------- E: buffer advance (one warp per node)
+        for (uint32_t k = gw; k < N; k += GW) {
+            uint32_t bsz = __ldcg(&a.nst[k * 4 + 0]), top = __ldcg(&a.nst[k * 4 + 1]);
+            const uint32_t lb = noff[k], le = noff[k + 1];
+            const uint32_t kw = k >> 5, kb = 1u << (k & 31);
+            uint32_t* cntk = a.cnt + size_t(k) * (a.T + 1);
+            unsigned long long* sk = a.slot + size_t(k) * a.SC;
+            bool pending = false;
+            for (uint32_t p0 = lb; p0 < le; p0 += 32) {
+                const uint32_t p = p0 + lane;
+                const bool valid = p < le;
+                uint32_t j = 0, x = 0, nuv = 0;
+                bool res = false;
+                if (valid) {
+                    j = __ldcg(&a.fin[p]) & kIdM;
+                    res = (__ldcg(&a.jmask[size_t(j) * W + kw]) & kb) != 0;  // residency at step start
+                    x = __ldcg(&a.jx[j]);
+                    nuv = __ldcg(&a.jnu[j]);
+                }
+                const uint32_t vbal = __ballot_sync(0xFFFFFFFFu, valid);
+                const uint32_t rbal = __ballot_sync(0xFFFFFFFFu, res);
+                uint32_t done = 0;
+                while (done != vbal) {
+                    const uint32_t first = __ffs(vbal & ~done) - 1;
+                    const bool hitrun = (rbal >> first) & 1u;
+                    const uint32_t same = hitrun ? rbal : (vbal & ~rbal);
+                    const uint32_t after = (~same) & vbal & ~((2u << first) - 1u);
+                    const uint32_t stop = after ? __ffs(after) - 1 : 32u;
+                    const uint32_t run = (stop == 32 ? 0xFFFFFFFFu : ((1u << stop) - 1u)) & ~((1u << first) - 1u) & vbal;
+                    const bool mine = (run >> lane) & 1u;
+                    if (hitrun && pending) {
+                        if (bsz > a.C) wide_evict(a, k, bsz, top, g, lane, my_hist);
+                        pending = false;
+                    }
+                    if (mine) {
+                        if (hitrun) {  // buffer.cpp:37-41 re-key
+                            const uint32_t s = __ldcg(&a.where[size_t(k) * a.D + x]);
+                            const uint32_t old = uint32_t(__ldcg(&sk[s]) >> 32);
+                            sk[s] = (static_cast<unsigned long long>(nuv) << 32) | x;
+                            if (old != nuv) {
+                                atomicSub(&cntk[bin_of(old, a.T)], 1u);
+                                atomicAdd(&cntk[bin_of(nuv, a.T)], 1u);
+                            }
+                        } else {  // buffer.cpp:42-46 insert
+                            const uint32_t s = bsz + __popc(run & lt);
+                            a.where[size_t(k) * a.D + x] = s;
+                            sk[s] = (static_cast<unsigned long long>(nuv) << 32) | x;
+                            atomicAdd(&cntk[bin_of(nuv, a.T)], 1u);
+                            atomicOr(&a.hm[size_t(x) * W + kw], kb);
+                        }
+                    }
+                    top = max(top, __reduce_max_sync(0xFFFFFFFFu, mine && nuv != kNever ? nuv : 0u));
+                    __syncwarp();
+                    if (!hitrun) {
+                        bsz += __popc(run);
+                        pending = true;
+                    }
+                    done |= run;
+                }
+            }
+            if (pending && bsz > a.C) wide_evict(a, k, bsz, top, g, lane, my_hist);
+            if (lane == 0) {
+                a.nst[k * 4 + 0] = bsz;
+                a.nst[k * 4 + 1] = top;
+            }
+            __syncwarp();
+        }
+        cl.sync();  // (7)
+        gbase += len;
+    }
+}
+
+}  // namespace
+
+int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, const uint32_t* d_trace,
+                     const uint32_t* d_order, const uint32_t* d_nu, uint32_t* d_items, uint32_t* d_node_off,
+                     uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status, cudaStream_t st) {
+    if (dm.N > kWMaxN)
+        return set_error(kCapability, "plan: device planner supports num_nodes <= 256 in this build");
+    if (dm.b >= (1u << 21)) return set_error(kCapability, "plan: local_batch must be < 2^21 on device");
+    if (dm.B >= (1ull << 30) || dm.T >= 0xFFFFFFF0ull)
+        return set_error(kCapability, "plan: global batch / steps too large for the device planner");
+    const uint32_t N = dm.N, W = (N + 31) / 32;
+    const uint64_t Ceff = std::min<uint64_t>(C, dm.D);
+    const uint64_t SC = Ceff + dm.B;
+    if (SC >= (1ull << 31)) return set_error(kCapability, "plan: buffer capacity too large for the device planner");
+    Scratch sc(st);
+    WideArgs a{};
+    a.D = uint32_t(dm.D);
+    a.N = N;
+    a.W = W;
+    a.b = dm.b;
+    a.B = uint32_t(dm.B);
+    a.S = uint32_t(dm.S);
+    a.keep = uint32_t(dm.keep);
+    a.T = uint32_t(dm.T);
+    a.C = uint32_t(Ceff);
+    a.SC = uint32_t(SC);
+    a.EBW = uint32_t((SC + 31) / 32);
+    a.MBW = (dm.b + 31) / 32;
+    a.remap = remap;
+    a.balance = balance;
+    a.trace = d_trace;
+    a.order = d_order;
+    a.nu = d_nu;
+    a.hm = sc.get<uint32_t>(size_t(dm.D) * W);
+    a.where = sc.get<uint32_t>(size_t(N) * dm.D);
+    a.slot = sc.get<unsigned long long>(size_t(N) * SC);
+    a.cnt = sc.get<uint32_t>(size_t(N) * (dm.T + 1));
+    a.nst = sc.get<uint32_t>(size_t(N) * 4);
+    a.evb = sc.get<uint32_t>(size_t(N) * a.EBW);
+    a.cand = sc.get<uint32_t>(size_t(N) * SC);
+    a.holes = sc.get<uint32_t>(size_t(N) * SC);
+    a.movedbm = sc.get<uint32_t>(size_t(N) * a.MBW);
+    a.jx = sc.get<uint32_t>(dm.B);
+    a.jnu = sc.get<uint32_t>(dm.B);
+    a.jmask = sc.get<uint32_t>(size_t(dm.B) * W);
+    a.jcls = sc.get<uint32_t>(dm.B);
+    a.jS = sc.get<uint32_t>(dm.B);
+    a.pre = sc.get<uint32_t>(dm.B);
+    a.fin = sc.get<uint32_t>(dm.B);
+    a.mj = sc.get<uint32_t>(dm.B);
+    a.mpo = sc.get<uint32_t>(dm.B);
+    a.mhc = sc.get<uint32_t>(dm.B);
+    a.pairs = sc.get<uint32_t>(size_t(dm.B) * N);
+    a.massign = sc.get<uint32_t>(dm.B);
+    a.mpos = sc.get<uint32_t>(size_t(N) * dm.b);
+    a.recv = sc.get<uint32_t>(size_t(N) * dm.b);
+    if (!a.hm || !a.where || !a.slot || !a.cnt || !a.nst || !a.evb || !a.cand || !a.holes || !a.movedbm ||
+        !a.jx || !a.jnu || !a.jmask || !a.jcls || !a.jS || !a.pre || !a.fin || !a.mj || !a.mpo || !a.mhc ||
+        !a.pairs || !a.massign || !a.mpos || !a.recv)
+        return set_error(kInternal, "plan: wide planner scratch allocation failed");
+    LSG_CUDA(cudaMemsetAsync(a.hm, 0, size_t(dm.D) * W * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.where, 0xFF, size_t(N) * dm.D * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.cnt, 0, size_t(N) * (dm.T + 1) * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.nst, 0, size_t(N) * 16, st));
+    LSG_CUDA(cudaMemsetAsync(a.evb, 0, size_t(N) * a.EBW * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.movedbm, 0, size_t(N) * a.MBW * 4, st));
+    a.items = d_items;
+    a.node_off = d_node_off;
+    a.fb = d_fb;
+    a.fa = d_fa;
+    a.status = d_status;
+
+    const size_t smem = size_t(kWW) * kSortCap * 8 + size_t(kWW) * 256 * 4 +
+                        (size_t(2) * kWW * N + 14 * size_t(N) + 3 * size_t(N + 1)) * 4;
+    LSG_CUDA(cudaFuncSetAttribute(k_plan_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    LSG_CUDA(cudaFuncSetAttribute(k_plan_wide, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    int want = 16;
+    if (const char* e = std::getenv("LSG_WIDE_CLUSTER")) want = std::max(1, std::min(16, std::atoi(e)));
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.blockDim = dim3(kWT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    int P = want;
+    for (; P >= 1; P >>= 1) {
+        cfg.gridDim = dim3(P);
+        attr[0].val.clusterDim.x = P;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, k_plan_wide, &cfg) == cudaSuccess && ncl >= 1) break;
+        cudaGetLastError();
+    }
+    if (P < 1) return set_error(kCapability, "plan: no thread-block cluster fits the wide planner");
+    LSG_CUDA(cudaLaunchKernelEx(&cfg, k_plan_wide, a));
+    LSG_LAUNCH_CHECK("k_plan_wide");
+    if (profiling()) {
+        LSG_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "[lsg profile] wide planner: cluster of %d CTAs x %d threads, %zu B smem, N=%u B=%llu T=%llu\n",
+                P, kWT, smem, N, (unsigned long long)dm.B, (unsigned long long)dm.T);
+    }
+    return kOk;
+}
+
+}  // namespace lsg

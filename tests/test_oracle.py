@@ -217,3 +217,23 @@ def test_oracle_reads_match_reference(seed):
             assert np.array_equal(rs[lo:lo + n], q.extra["rstart"][lo:lo + n])
             assert np.array_equal(re_[lo:lo + n], q.extra["rend"][lo:lo + n])
         base += p.node_off[g, N]
+
+
+@ref
+@pytest.mark.parametrize("seed", range(6))
+def test_oracle_matches_reference_many_nodes(seed):
+    """N > 32 simulated ranks (cfg5's 32-256 logical-rank sweep) at small D."""
+    r = random.Random(4200 + seed)
+    N, b = r.choice([33, 64, 100, 256]), r.choice([1, 2, 4])
+    B = N * b
+    D = B * r.randint(1, 6) + r.randint(0, B - 1)
+    cfg = O.Cfg(D, r.randint(1, 3), N, b, seed=r.randint(0, 1000),
+                buffer_capacity=r.randint(1, max(1, 2 * D // N)), drop_last=r.random() < 0.7,
+                optim_order=r.random() < 0.5, optim_remap=r.random() < 0.85,
+                optim_balance=r.random() < 0.85, pso_iters=20)
+    p, q = O.plan(cfg, residency=True), O.ref_plan(cfg)
+    for f in ("trace", "items", "node_off", "fb", "fa"):
+        assert np.array_equal(getattr(p, f), getattr(q, f)), f
+    h, m = O.simulate(p.items, p.node_off, N, D, cfg.buffer_capacity)
+    assert np.array_equal(p.residency, q.residency)
+    assert np.array_equal(h, q.hits) and np.array_equal(m, q.misses)
