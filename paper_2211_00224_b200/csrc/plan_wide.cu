@@ -46,6 +46,9 @@ constexpr int kWT = 512;                // threads per CTA
 constexpr int kWW = kWT / 32;           // warps per CTA
 constexpr uint32_t kWMaxN = 256;        // simulated nodes
 constexpr uint32_t kSortCap = 512;      // donor fetch entries sorted in shared memory
+constexpr uint32_t kMS = 1024;          // multi items staged per chunk (B pass)
+constexpr uint32_t kMP = kWW * kSortCap * 2 - 3 * kMS;  // staged pair words
+constexpr uint32_t kLevCap = 2048;      // balance levels handled in closed form
 constexpr uint32_t kHitM = 0x80000000u;
 constexpr uint32_t kIdM = 0x7FFFFFFFu;
 constexpr uint32_t kClsSingle = 1u << 30;
@@ -76,7 +79,8 @@ struct WideArgs {
     uint32_t* jcls;                   // [B] class | holder
     uint32_t* jS;                     // [B] singles: S_k(j); multi: multi index
     uint32_t* pre;                    // [B] pre-balance lists (j | hit)
-    uint32_t* fin;                    // [B] final lists (j | hit)
+    uint32_t* fx;                     // [B] final lists: id | resident-at-start << 31
+    uint32_t* fnu;                    // [B] final lists: next-use step
     uint32_t* mj;                     // [B] multi index -> j
     uint32_t* mpo;                    // [B] multi index -> pair offset
     uint32_t* mhc;                    // [B] multi index -> candidate pairs
@@ -84,11 +88,13 @@ struct WideArgs {
     uint32_t* massign;                // [B] (position << 10 | node) or kNone
     uint32_t* mpos;                   // [N][b] j of node k's assigned multis, in order
     uint32_t* recv;                   // [N][b] donor's q-th move: (ii << 10 | recipient)
+    uint32_t* ur;                     // [B] recipient units in move order
     uint32_t* items;                  // [E*keep] output
     uint32_t* node_off;               // [T][N+1] output
     uint32_t* fb;                     // [T][N] output (may be null)
     uint32_t* fa;                     // [T][N] output (may be null)
     uint32_t* status;
+    unsigned long long* prof;         // [16] per-phase cycles + counters (LSG_PROFILE) or null
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt_w() {
@@ -108,7 +114,19 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, uint32_t lane) {
 
 __device__ __forceinline__ uint32_t bin_of(uint32_t key, uint32_t T) { return key == kNever ? T : key; }
 
-// Remove the m = size - C largest (key, id) residents of node k (one warp).
+// drop resident (key, x) of node k: residency, holder bit, bin count
+__device__ __forceinline__ void evict_one(const WideArgs& a, uint32_t k, unsigned long long v) {
+    const uint32_t x = uint32_t(v);
+    a.where[size_t(k) * a.D + x] = kNone;
+    atomicAnd(&a.hm[size_t(x) * a.W + (k >> 5)], ~(1u << (k & 31)));
+    atomicSub(&a.cnt[size_t(k) * (a.T + 1) + bin_of(uint32_t(v >> 32), a.T)], 1u);
+}
+
+// Remove the m = size - C largest (key, id) residents of node k (one warp):
+// threshold bin from the per-bin counts, ONE scan of the slots that drops
+// every resident above it (holes below the new size are recorded, tail
+// survivors flagged), a radix select of the r largest ids inside the
+// threshold bin, then tail survivors move into the holes.
 __device__ void wide_evict(const WideArgs& a, uint32_t k, uint32_t& bsz, uint32_t& top, uint32_t g,
                            uint32_t lane, uint32_t* hist) {
     const uint32_t lt = lanemask_lt_w();
@@ -117,6 +135,7 @@ __device__ void wide_evict(const WideArgs& a, uint32_t k, uint32_t& bsz, uint32_
     unsigned long long* sk = a.slot + size_t(k) * a.SC;
     uint32_t* evk = a.evb + size_t(k) * a.EBW;
     uint32_t* cak = a.cand + size_t(k) * a.SC;
+    uint32_t* hk = a.holes + size_t(k) * a.SC;
     // ---- threshold bin: never-used first, then finite bins from the top
     uint32_t tstar = 0, r = 0;
     const uint32_t nev = __ldcg(&cntk[a.T]);
@@ -148,19 +167,37 @@ __device__ void wide_evict(const WideArgs& a, uint32_t k, uint32_t& bsz, uint32_
             }
         }
     }
-    // ---- one scan: flag bins above the threshold, collect the threshold bin
-    uint32_t ncand = 0;
-    for (uint32_t s0 = 0; s0 < bsz; s0 += 32) {
-        const uint32_t s = s0 + lane;
-        const bool valid = s < bsz;
-        const unsigned long long v = valid ? __ldcg(&sk[s]) : 0ull;
-        const uint32_t bn = bin_of(uint32_t(v >> 32), a.T);
-        const bool ev = valid && bn > tstar, cd = valid && bn == tstar;
-        const uint32_t evw = __ballot_sync(0xFFFFFFFFu, ev);
-        if (lane == 0) evk[s0 >> 5] = evw;
-        const uint32_t cb = __ballot_sync(0xFFFFFFFFu, cd);
-        if (cd) cak[ncand + __popc(cb & lt)] = s;
-        ncand += __popc(cb);
+    const uint32_t newsize = bsz - m;
+    if (a.prof && lane == 0) {
+        atomicAdd(&a.prof[8], 1ull);
+        atomicAdd(&a.prof[9], static_cast<unsigned long long>(bsz));
+    }
+    // ---- one scan (4 loads in flight per lane)
+    uint32_t ncand = 0, nh = 0;
+    for (uint32_t s0 = 0; s0 < bsz; s0 += 128) {
+        unsigned long long v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t s = s0 + u * 32 + lane;
+            v[u] = s < bsz ? __ldcg(&sk[s]) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t sb = s0 + u * 32, s = sb + lane;
+            const bool valid = s < bsz;
+            const uint32_t bn = bin_of(uint32_t(v[u] >> 32), a.T);
+            const bool ev = valid && bn > tstar, cd = valid && bn == tstar;
+            if (ev) evict_one(a, k, v[u]);
+            const bool hole = ev && s < newsize;
+            const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hole);
+            if (hole) hk[nh + __popc(hb & lt)] = s;
+            nh += __popc(hb);
+            const uint32_t tw = __ballot_sync(0xFFFFFFFFu, ev && s >= newsize);
+            if (lane == 0 && sb < bsz && sb + 31 >= newsize) evk[sb >> 5] = tw;
+            const uint32_t cb = __ballot_sync(0xFFFFFFFFu, cd);
+            if (cd) cak[ncand + __popc(cb & lt)] = s;
+            ncand += __popc(cb);
+        }
     }
     __syncwarp();
     // ---- the r largest ids of the threshold bin (ids are distinct per node)
@@ -208,26 +245,18 @@ __device__ void wide_evict(const WideArgs& a, uint32_t k, uint32_t& bsz, uint32_
         }
         thr = prefix;  // the r-th largest id of the bin
     }
-    for (uint32_t q = lane; q < ncand; q += 32) {
-        const uint32_t s = __ldcg(&cak[q]);
-        if (r >= ncand || uint32_t(__ldcg(&sk[s])) >= thr) atomicOr(&evk[s >> 5], 1u << (s & 31));
-    }
-    __syncwarp();
-    // ---- drop the flagged residents; holes below the new size
-    const uint32_t newsize = bsz - m;
-    uint32_t* hk = a.holes + size_t(k) * a.SC;
-    uint32_t nh = 0;
-    const uint32_t kw = k >> 5, kb = 1u << (k & 31);
-    for (uint32_t s0 = 0; s0 < bsz; s0 += 32) {
-        const uint32_t s = s0 + lane;
-        const uint32_t word = __ldcg(&evk[s0 >> 5]);
-        const bool ev = s < bsz && ((word >> lane) & 1u);
-        if (ev) {
+    for (uint32_t q0 = 0; q0 < ncand; q0 += 32) {
+        const uint32_t q = q0 + lane;
+        bool ev = false;
+        uint32_t s = 0;
+        if (q < ncand) {
+            s = __ldcg(&cak[q]);
             const unsigned long long v = __ldcg(&sk[s]);
-            const uint32_t x = uint32_t(v);
-            a.where[size_t(k) * a.D + x] = kNone;
-            atomicAnd(&a.hm[size_t(x) * a.W + kw], ~kb);
-            atomicSub(&cntk[bin_of(uint32_t(v >> 32), a.T)], 1u);
+            ev = r >= ncand || uint32_t(v) >= thr;
+            if (ev) {
+                evict_one(a, k, v);
+                if (s >= newsize) atomicOr(&evk[s >> 5], 1u << (s & 31));
+            }
         }
         const bool hole = ev && s < newsize;
         const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hole);
@@ -252,7 +281,7 @@ __device__ void wide_evict(const WideArgs& a, uint32_t k, uint32_t& bsz, uint32_
     }
     if (nmv != nh && lane == 0) atomicOr(a.status, 16u);
     __syncwarp();
-    for (uint32_t wd = lane; wd < (bsz + 31) / 32; wd += 32) evk[wd] = 0;
+    for (uint32_t wd = (newsize >> 5) + lane; wd < (bsz + 31) / 32; wd += 32) evk[wd] = 0;
     bsz = newsize;
     if (tstar != a.T) top = tstar;
     __syncwarp();
@@ -342,6 +371,165 @@ __device__ void wide_balance(uint32_t N, uint32_t b, const uint32_t* fcnt, uint3
     }
 }
 
+// Balance (balance.cpp:10-39) in closed form, all threads of the CTA.
+// With counts c_k, F = sum, L = F / N: the reference loop ends when every
+// count is L or L+1. A "donor unit" (k, l) is node k giving one fetch while
+// at count l; a "recipient unit" (k, l) is node k receiving one at count l.
+// The loop consumes donor units in (l desc, k asc) order and recipient units
+// in (l asc, k asc) order (the first argmax / argmin only change when a level
+// set is exhausted), and the t-th move pairs the t-th units of both lists.
+// Mandatory units: donors at levels >= L+2, recipients at levels <= L-1
+// (Dm, Rm of them); the longer side is padded with level-(L+1) donor or
+// level-L recipient units in node order. Donor k's q-th move is its unit at
+// level c_k - q and gives its q-th largest fetch id; the recipient appends it
+// as its (l - c_k)-th incoming fetch. CTA `writer` also writes recv[].
+__device__ void wide_balance_cf(const WideArgs& a, uint32_t N, uint32_t b, const uint32_t* fcnt, uint32_t* outk,
+                                uint32_t* ink, uint32_t* lv, uint32_t* bsc, uint32_t* rl, uint32_t* rl2,
+                                bool writer, uint32_t tid, uint32_t lane, uint32_t w) {
+    const uint32_t lt = lanemask_lt_w();
+    const uint32_t NQ = (N + 31) / 32;
+    uint32_t cv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t k = q * 32 + lane;
+        cv[q] = (uint32_t(q) < NQ && k < N) ? fcnt[k] : 0u;
+    }
+    if (w == 0) {
+        uint32_t mx = 0, mn = 0xFFFFFFFFu, sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (uint32_t(q) < NQ && q * 32 + lane < N) {
+                mx = max(mx, cv[q]);
+                mn = min(mn, cv[q]);
+                sum += cv[q];
+            }
+        mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+        mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+        sum = __reduce_add_sync(0xFFFFFFFFu, sum);
+        const uint32_t L = sum / N;
+        uint32_t dm = 0, rm = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (uint32_t(q) < NQ && q * 32 + lane < N) {
+                dm += cv[q] > L + 1 ? cv[q] - L - 1 : 0u;
+                rm += cv[q] < L ? L - cv[q] : 0u;
+            }
+        dm = __reduce_add_sync(0xFFFFFFFFu, dm);
+        rm = __reduce_add_sync(0xFFFFFFFFu, rm);
+        if (lane == 0) {
+            bsc[0] = L;
+            bsc[1] = dm;
+            bsc[2] = rm;
+            bsc[3] = mn;
+            bsc[4] = mx;
+        }
+    }
+    __syncthreads();
+    const uint32_t L = bsc[0], dm = bsc[1], rm = bsc[2], mn = bsc[3], mx = bsc[4];
+    if (mx - mn <= 1) {
+        for (uint32_t k = tid; k < N; k += kWT) outk[k] = ink[k] = 0;
+        __syncthreads();
+        return;
+    }
+    if (mx - mn + 1 > kLevCap) {  // very wide count spread: the round simulation
+        if (w == 0) wide_balance(N, b, fcnt, outk, ink, rl, rl2, writer ? a.recv : nullptr, a.status, lane);
+        __syncthreads();
+        return;
+    }
+    const uint32_t mv = max(dm, rm), od = mv - dm, orr = mv - rm;
+    uint32_t* lvge = lv;                // #{c_k >= l}
+    uint32_t* lvle = lv + kLevCap;      // #{c_k <= l}
+    uint32_t* lvds = lv + 2 * kLevCap;  // first donor unit of level l
+    uint32_t* lvrs = lv + 3 * kLevCap;  // first recipient unit of level l
+    for (uint32_t l = mn + w; l <= mx; l += kWW) {
+        uint32_t ge = 0, le = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (uint32_t(q) >= NQ) break;
+            const bool in = q * 32 + lane < N;
+            ge += __popc(__ballot_sync(0xFFFFFFFFu, in && cv[q] >= l));
+            le += __popc(__ballot_sync(0xFFFFFFFFu, in && cv[q] <= l));
+        }
+        if (lane == 0) {
+            lvge[l - mn] = ge;
+            lvle[l - mn] = le;
+        }
+    }
+    __syncthreads();
+    if (w == 0) {
+        // donor levels mx, mx-1, .., L+2 (suffix sums); recipient levels mn .. L-1
+        const uint32_t nd = mx >= L + 2 ? mx - L - 1 : 0u, nr = L > mn ? L - mn : 0u;
+        uint32_t run = 0;
+        for (uint32_t d0 = 0; d0 < nd; d0 += 32) {
+            const uint32_t d = d0 + lane;
+            const uint32_t v = d < nd ? lvge[mx - d - mn] : 0u;
+            const uint32_t incl = warp_incl_scan(v, lane);
+            if (d < nd) lvds[mx - d - mn] = run + incl - v;
+            run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+        run = 0;
+        for (uint32_t d0 = 0; d0 < nr; d0 += 32) {
+            const uint32_t d = d0 + lane;
+            const uint32_t v = d < nr ? lvle[d] : 0u;
+            const uint32_t incl = warp_incl_scan(v, lane);
+            if (d < nr) lvrs[d] = run + incl - v;
+            run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        }
+        // moves per node: mandatory units + the optional one
+        uint32_t accd = 0, accr = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            if (uint32_t(q) >= NQ) break;
+            const uint32_t k = q * 32 + lane;
+            const bool in = k < N;
+            const bool isd = in && cv[q] >= L + 1, isr = in && cv[q] <= L;
+            const uint32_t bd = __ballot_sync(0xFFFFFFFFu, isd), br = __ballot_sync(0xFFFFFFFFu, isr);
+            const uint32_t rd = accd + __popc(bd & lt), rr = accr + __popc(br & lt);
+            if (in) {
+                outk[k] = (cv[q] > L + 1 ? cv[q] - L - 1 : 0u) + ((isd && rd < od) ? 1u : 0u);
+                ink[k] = (cv[q] < L ? L - cv[q] : 0u) + ((isr && rr < orr) ? 1u : 0u);
+            }
+            accd += __popc(bd);
+            accr += __popc(br);
+        }
+    }
+    __syncthreads();
+    if (writer) {
+        // recipient units -> ur[t] = (ii << 10 | r)
+        for (uint32_t l = mn + w; l <= L; l += kWW) {
+            const uint32_t base = l < L ? lvrs[l - mn] : rm, lim = l < L ? 0xFFFFFFFFu : orr;
+            uint32_t acc = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (uint32_t(q) >= NQ) break;
+                const uint32_t k = q * 32 + lane;
+                const bool isr = k < N && cv[q] <= l;
+                const uint32_t br = __ballot_sync(0xFFFFFFFFu, isr);
+                const uint32_t rk = acc + __popc(br & lt);
+                if (isr && rk < lim) a.ur[base + rk] = ((l - cv[q]) << 10) | k;
+                acc += __popc(br);
+            }
+        }
+        __syncthreads();
+        // donor units: donor k's (c_k - l)-th move takes the t-th recipient unit
+        for (uint32_t l = L + 1 + w; l <= mx; l += kWW) {
+            const uint32_t base = l > L + 1 ? lvds[l - mn] : dm, lim = l > L + 1 ? 0xFFFFFFFFu : od;
+            uint32_t acc = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (uint32_t(q) >= NQ) break;
+                const uint32_t k = q * 32 + lane;
+                const bool isd = k < N && cv[q] >= l;
+                const uint32_t bd = __ballot_sync(0xFFFFFFFFu, isd);
+                const uint32_t rk = acc + __popc(bd & lt);
+                if (isd && rk < lim) a.recv[size_t(k) * b + (cv[q] - l)] = __ldcg(&a.ur[base + rk]);
+                acc += __popc(bd);
+            }
+        }
+    }
+    __syncthreads();
+}
+
 // exclusive prefix of v[0..n) into out[0..n], out[n] = total (one warp)
 __device__ __forceinline__ void warp_prefix(const uint32_t* v, uint32_t* out, uint32_t n, uint32_t lane) {
     uint32_t run = 0;
@@ -353,6 +541,53 @@ __device__ __forceinline__ void warp_prefix(const uint32_t* v, uint32_t* out, ui
         run += __shfl_sync(0xFFFFFFFFu, incl, 31);
     }
     if (lane == 0) out[n] = run;
+}
+
+// Multi-holder remap of staged items [mi0, mi0 + cntm) (one warp), exact
+// and speculative: lane l evaluates item q0 + l against the counts M at the
+// start of the batch. An item's decision depends only on M_k of its own
+// candidate holders, so every item before the first one that has a holder
+// chosen by an earlier lane of the batch decided exactly; that prefix
+// commits (its lanes chose distinct nodes), the batch restarts after it.
+// firstch[k] = earliest lane of the batch that chose node k (32: none).
+__device__ __forceinline__ void multi_pass(const uint32_t* pairs, uint32_t* mpos, uint32_t* massign, uint32_t* M,
+                                           uint32_t* firstch, uint32_t cntm, uint32_t mi0, uint32_t p0, bool pin,
+                                           const uint32_t* st_np, const uint32_t* st_po, const uint32_t* st_j,
+                                           const uint32_t* st_pr, uint32_t b, uint32_t lane) {
+    auto pair_at = [&](uint32_t po, uint32_t t) {
+        return pin ? st_pr[po + t] : __ldcg(&pairs[p0 + po + t]);
+    };
+    for (uint32_t q0 = 0; q0 < cntm;) {
+        const uint32_t q = q0 + lane;
+        const bool valid = q < cntm;
+        const uint32_t np = valid ? st_np[q] : 0u, po = valid ? st_po[q] : 0u;
+        uint32_t best = 0xFFFFFFFFu;
+        for (uint32_t t = 0; t < np; ++t) {
+            const uint32_t pr = pair_at(po, t), k = pr & 0x3FFu;
+            const uint32_t cc = min(b, (pr >> 10) + M[k]);
+            if (cc < b) best = min(best, (cc << 10) | k);
+        }
+        const bool chose = best != 0xFFFFFFFFu;
+        if (chose) atomicMin(&firstch[best & 0x3FFu], lane);
+        __syncwarp();
+        bool aff = false;
+        for (uint32_t t = 0; t < np && !aff; ++t) aff = firstch[pair_at(po, t) & 0x3FFu] < lane;
+        const uint32_t abal = __ballot_sync(0xFFFFFFFFu, aff);
+        const uint32_t nval = min(32u, cntm - q0);
+        const uint32_t ncommit = abal ? min(nval, uint32_t(__ffs(abal) - 1)) : nval;
+        __syncwarp();
+        if (chose) firstch[best & 0x3FFu] = 32u;
+        if (lane < ncommit) {
+            if (chose) {
+                const uint32_t k = best & 0x3FFu, mold = M[k];
+                M[k] = mold + 1;
+                mpos[size_t(k) * b + mold] = st_j[q];
+            }
+            massign[mi0 + q] = best;
+        }
+        __syncwarp();
+        q0 += ncommit;
+    }
 }
 
 __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
@@ -384,6 +619,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
     __shared__ unsigned long long ctsc, msbase, mstot;
     __shared__ uint32_t wsf[kWW];
     __shared__ uint32_t ctf, fbase, ftot;
+    __shared__ uint32_t bsc[8];
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t gw = c * kWW + w, GW = P * kWW;
@@ -391,6 +627,14 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
     unsigned long long* my_sort = sortb + w * kSortCap;
     uint32_t* my_hist = hist + w * 256;
     size_t gbase = 0;
+    unsigned long long pacc[7] = {0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tprev = clock64();
+#define WPHASE(n)                                                  \
+    if (a.prof && c == 0 && tid == 0) {                            \
+        const unsigned long long tnow = clock64();                 \
+        pacc[n] += tnow - tprev;                                   \
+        tprev = tnow;                                              \
+    }
 
     for (uint32_t g = 0; g < a.T; ++g) {
         const uint32_t i = g / a.S, t = g % a.S;
@@ -412,14 +656,17 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
             const bool valid = j < j1;
             uint32_t hc = 0, h = 0;
             if (valid) {
-                const uint32_t x = row[j];
+                const uint32_t x = row[j], nuj = nurow[j];
+                uint32_t mw[8];  // all mask loads in flight before any store
+#pragma unroll
+                for (int q = 0; q < 8; ++q) mw[q] = uint32_t(q) < W ? __ldcg(&a.hm[size_t(x) * W + q]) : 0u;
                 a.jx[j] = x;
-                a.jnu[j] = nurow[j];
-                for (uint32_t q = 0; q < W; ++q) {
-                    const uint32_t m = __ldcg(&a.hm[size_t(x) * W + q]);
-                    a.jmask[size_t(j) * W + q] = m;
-                    if (m && hc == 0) h = q * 32 + __ffs(m) - 1;
-                    hc += __popc(m);
+                a.jnu[j] = nuj;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (uint32_t(q) < W) a.jmask[size_t(j) * W + q] = mw[q];
+                    if (mw[q] && hc == 0) h = q * 32 + __ffs(mw[q]) - 1;
+                    hc += __popc(mw[q]);
                 }
             }
             if (a.remap) {
@@ -456,6 +703,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
             }
         }
         cl.sync();  // (1)
+        WPHASE(0)
         if (a.remap) {
             for (uint32_t k = tid; k < N; k += kWT) {
                 uint32_t bs = 0, tt = 0;
@@ -527,36 +775,53 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
             }
         }
         cl.sync();  // (2)
+        WPHASE(1)
 
-        // --------------------------- B: serial multi-holder pass (CTA 0, warp 0)
-        if (a.remap && c == 0 && w == 0) {
-            for (uint32_t k = lane; k < N; k += 32) M[k] = 0;
-            __syncwarp();
-            const uint32_t nm = uint32_t(mstot >> 32);
-            for (uint32_t mi = 0; mi < nm; ++mi) {
-                const uint32_t np = __ldcg(&a.mhc[mi]), po = __ldcg(&a.mpo[mi]);
-                uint32_t best = 0xFFFFFFFFu;
-                for (uint32_t t0 = 0; t0 < np; t0 += 32) {
-                    if (t0 + lane < np) {
-                        const uint32_t pr = __ldcg(&a.pairs[po + t0 + lane]);
-                        const uint32_t k = pr & 0x3FFu;
-                        const uint32_t cc = min(b, (pr >> 10) + M[k]);
-                        if (cc < b) best = min(best, (cc << 10) | k);
-                    }
-                }
-                best = __reduce_min_sync(0xFFFFFFFFu, best);
-                if (lane == 0) {
-                    if (best != 0xFFFFFFFFu) {
-                        const uint32_t k = best & 0x3FFu;
-                        a.mpos[size_t(k) * b + M[k]] = __ldcg(&a.mj[mi]);
-                        M[k] += 1;
-                    }
-                    a.massign[mi] = best;
-                }
-                __syncwarp();
+        // ---------------- B: serial multi-holder pass (CTA 0; warp 0 decides)
+        // The multi items' metadata and candidate pairs are staged in shared
+        // memory by the whole CTA, so the serial chain is shared-memory only:
+        // per item, lanes take its candidate (S_k, k) pairs, c_k = min(b,
+        // S_k + M_k), the winner is REDUX.MIN of (c_k << 10 | k) over c_k < b
+        // (lowest count, ties lowest k: locality.cpp:20-31).
+        if (a.remap && c == 0) {
+            uint32_t* st_np = reinterpret_cast<uint32_t*>(sortb);
+            uint32_t* st_po = st_np + kMS;
+            uint32_t* st_j = st_po + kMS;
+            uint32_t* st_pr = st_j + kMS;
+            for (uint32_t k = tid; k < N; k += kWT) {
+                M[k] = 0;
+                rl[k] = 32u;  // firstch of the speculative multi pass
             }
+            const uint32_t nm = uint32_t(mstot >> 32), npairs = uint32_t(mstot);
+            if (a.prof && tid == 0) {
+                atomicAdd(&a.prof[10], static_cast<unsigned long long>(nm));
+                atomicAdd(&a.prof[11], static_cast<unsigned long long>(npairs));
+            }
+            for (uint32_t mi0 = 0; mi0 < nm; mi0 += kMS) {
+                const uint32_t cntm = min(kMS, nm - mi0);
+                const uint32_t p0 = __ldcg(&a.mpo[mi0]);
+                const uint32_t p1 = mi0 + cntm < nm ? __ldcg(&a.mpo[mi0 + cntm]) : npairs;
+                const bool pin = p1 - p0 <= kMP;
+                for (uint32_t q = tid; q < cntm; q += kWT) {
+                    st_np[q] = __ldcg(&a.mhc[mi0 + q]);
+                    st_po[q] = __ldcg(&a.mpo[mi0 + q]) - p0;
+                    st_j[q] = __ldcg(&a.mj[mi0 + q]);
+                }
+                if (pin)
+                    for (uint32_t q = tid; q < p1 - p0; q += kWT) st_pr[q] = __ldcg(&a.pairs[p0 + q]);
+                __syncthreads();
+                const unsigned long long tb0 = clock64();
+                if (w == 0) {
+                    multi_pass(a.pairs, a.mpos, a.massign, M, rl, cntm, mi0, p0, pin, st_np, st_po, st_j, st_pr,
+                               b, lane);
+                    if (a.prof && lane == 0) atomicAdd(&a.prof[12], clock64() - tb0);
+                }
+                __syncthreads();
+            }
+
         }
         cl.sync();  // (3)
+        WPHASE(2)
 
         // ---------------------------------- C1: hit / fetch, fetch counts
         if (a.remap) {
@@ -611,6 +876,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
                 ctot[k] = s;
             }
         cl.sync();  // (4)
+        WPHASE(3)
         if (tid == 0) {
             uint32_t bs = 0, tt = 0;
             for (uint32_t c2 = 0; c2 < P; ++c2) {
@@ -654,18 +920,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
             __syncwarp();
         }
         __syncthreads();
-        // ------------------- C2: pre-balance positions (+ balance on warp 0)
-        if (w == 0) {
-            if (a.balance) {
-                wide_balance(N, b, fcnt, outk, ink, rl, rl2, c == 0 ? a.recv : nullptr, a.status, lane);
-            } else {
-                for (uint32_t k = lane; k < N; k += 32) outk[k] = ink[k] = 0;
-            }
-            __syncwarp();
-            for (uint32_t k = lane; k < N; k += 32) lenfin[k] = lenpre[k] - outk[k] + ink[k];
-            __syncwarp();
-            warp_prefix(lenfin, noff, N, lane);
-        }
+        // --------------------------- C2: pre-balance positions, then balance
         {
             uint32_t fr = fbase + wsf[w];
             for (uint32_t cb = j0; cb < j1; cb += 32) {
@@ -720,17 +975,38 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
                 fr += __popc(fbal);
             }
         }
+        if (a.balance) {
+            wide_balance_cf(a, N, b, fcnt, outk, ink, reinterpret_cast<uint32_t*>(sortb), bsc, rl, rl2, c == 0,
+                            tid, lane, w);
+        } else {
+            for (uint32_t k = tid; k < N; k += kWT) outk[k] = ink[k] = 0;
+            __syncthreads();
+        }
+        if (w == 0) {
+            for (uint32_t k = lane; k < N; k += 32) lenfin[k] = lenpre[k] - outk[k] + ink[k];
+            __syncwarp();
+            warp_prefix(lenfin, noff, N, lane);
+        }
         cl.sync();  // (5)
+        WPHASE(4)
 
         // --------------------------------- D: final lists (one warp per node)
         for (uint32_t k = gw; k < N; k += GW) {
             const uint32_t lp = lenpre[k], pb = noffpre[k], fbk = noff[k], nout = outk[k];
             uint32_t* items = a.items + gbase;
+            // final position dst of node kk: the plan item, and the buffer
+            // advance record (id | resident-at-step-start on kk, next use)
+            auto emit = [&](uint32_t kk, uint32_t dst, uint32_t it) {
+                const uint32_t j = it & kIdM, x = __ldcg(&a.jx[j]);
+                items[dst] = x | (it & kHitM);
+                const uint32_t res = (__ldcg(&a.jmask[size_t(j) * W + (kk >> 5)]) >> (kk & 31)) & 1u;
+                a.fx[dst] = x | (res << 31);
+                a.fnu[dst] = __ldcg(&a.jnu[j]);
+            };
             if (nout == 0) {
                 for (uint32_t p = lane; p < lp; p += 32) {
                     const uint32_t it = __ldcg(&a.pre[pb + p]);
-                    a.fin[fbk + p] = it;
-                    items[fbk + p] = __ldcg(&a.jx[it & kIdM]) | (it & kHitM);
+                    emit(k, fbk + p, it);
                 }
             } else {
                 uint32_t* mvk = a.movedbm + size_t(k) * a.MBW;
@@ -752,9 +1028,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
                     const uint32_t rec = __ldcg(&a.recv[size_t(k) * b + q]);
                     const uint32_t r = rec & 0x3FFu, ii = rec >> 10;
                     const uint32_t dest = noff[r] + lenpre[r] + ii;
-                    const uint32_t it = __ldcg(&a.pre[pb + p]);
-                    a.fin[dest] = it;
-                    items[dest] = __ldcg(&a.jx[it & kIdM]);
+                    emit(r, dest, __ldcg(&a.pre[pb + p]));
                 };
                 if (fits) {
                     uint32_t P2 = 1;
@@ -805,8 +1079,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
                     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
                     if (keep) {
                         const uint32_t dst = fbk + kept + __popc(bal & lt);
-                        a.fin[dst] = it;
-                        items[dst] = __ldcg(&a.jx[it & kIdM]) | (it & kHitM);
+                        emit(k, dst, it);
                     }
                     kept += __popc(bal);
                 }
@@ -821,26 +1094,38 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
             }
         }
         cl.sync();  // (6)
+        WPHASE(5)
 
         // ------------------------------- E: buffer advance (one warp per node)
+        // List order, runs of equal residency-at-step-start (buffer.cpp:37-46
+        // per access == re-key runs, and insert runs followed by one eviction
+        // of the (size - C)+ largest). Records are prefetched a chunk ahead;
+        // a resident's slot is read once per chunk and re-read only after an
+        // eviction in the same chunk (compaction may have moved it).
         for (uint32_t k = gw; k < N; k += GW) {
             uint32_t bsz = __ldcg(&a.nst[k * 4 + 0]), top = __ldcg(&a.nst[k * 4 + 1]);
             const uint32_t lb = noff[k], le = noff[k + 1];
             const uint32_t kw = k >> 5, kb = 1u << (k & 31);
             uint32_t* cntk = a.cnt + size_t(k) * (a.T + 1);
             unsigned long long* sk = a.slot + size_t(k) * a.SC;
+            const uint32_t* whk = a.where + size_t(k) * a.D;
             bool pending = false;
+            uint32_t nxr = 0, nnu = 0;
+            if (lb + lane < le) {
+                nxr = __ldcg(&a.fx[lb + lane]);
+                nnu = __ldcg(&a.fnu[lb + lane]);
+            }
             for (uint32_t p0 = lb; p0 < le; p0 += 32) {
-                const uint32_t p = p0 + lane;
-                const bool valid = p < le;
-                uint32_t j = 0, x = 0, nuv = 0;
-                bool res = false;
-                if (valid) {
-                    j = __ldcg(&a.fin[p]) & kIdM;
-                    res = (__ldcg(&a.jmask[size_t(j) * W + kw]) & kb) != 0;  // residency at step start
-                    x = __ldcg(&a.jx[j]);
-                    nuv = __ldcg(&a.jnu[j]);
+                const bool valid = p0 + lane < le;
+                const uint32_t xr = nxr, nuv = nnu;
+                if (p0 + 32 + lane < le) {
+                    nxr = __ldcg(&a.fx[p0 + 32 + lane]);
+                    nnu = __ldcg(&a.fnu[p0 + 32 + lane]);
                 }
+                const uint32_t x = xr & kIdM;
+                const bool res = valid && (xr >> 31);
+                uint32_t ws = res ? __ldcg(&whk[x]) : 0u;
+                uint32_t old = res ? uint32_t(__ldcg(&sk[ws]) >> 32) : 0u;
                 const uint32_t vbal = __ballot_sync(0xFFFFFFFFu, valid);
                 const uint32_t rbal = __ballot_sync(0xFFFFFFFFu, res);
                 uint32_t done = 0;
@@ -853,22 +1138,26 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
                     const uint32_t run = (stop == 32 ? 0xFFFFFFFFu : ((1u << stop) - 1u)) & ~((1u << first) - 1u) & vbal;
                     const bool mine = (run >> lane) & 1u;
                     if (hitrun && pending) {
-                        if (bsz > a.C) wide_evict(a, k, bsz, top, g, lane, my_hist);
+                        if (bsz > a.C) {
+                            wide_evict(a, k, bsz, top, g, lane, my_hist);
+                            if (res && !((done >> lane) & 1u)) {  // slots may have moved
+                                ws = __ldcg(&whk[x]);
+                                old = uint32_t(__ldcg(&sk[ws]) >> 32);
+                            }
+                        }
                         pending = false;
                     }
                     if (mine) {
                         if (hitrun) {  // buffer.cpp:37-41 re-key
-                            const uint32_t s = __ldcg(&a.where[size_t(k) * a.D + x]);
-                            const uint32_t old = uint32_t(__ldcg(&sk[s]) >> 32);
-                            sk[s] = (static_cast<unsigned long long>(nuv) << 32) | x;
+                            sk[ws] = (static_cast<unsigned long long>(nuv) << 32) | x;
                             if (old != nuv) {
                                 atomicSub(&cntk[bin_of(old, a.T)], 1u);
                                 atomicAdd(&cntk[bin_of(nuv, a.T)], 1u);
                             }
                         } else {  // buffer.cpp:42-46 insert
-                            const uint32_t s = bsz + __popc(run & lt);
-                            a.where[size_t(k) * a.D + x] = s;
-                            sk[s] = (static_cast<unsigned long long>(nuv) << 32) | x;
+                            const uint32_t s2 = bsz + __popc(run & lt);
+                            a.where[size_t(k) * a.D + x] = s2;
+                            sk[s2] = (static_cast<unsigned long long>(nuv) << 32) | x;
                             atomicAdd(&cntk[bin_of(nuv, a.T)], 1u);
                             atomicOr(&a.hm[size_t(x) * W + kw], kb);
                         }
@@ -890,8 +1179,12 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
             __syncwarp();
         }
         cl.sync();  // (7)
+        WPHASE(6)
         gbase += len;
     }
+#undef WPHASE
+    if (a.prof && c == 0 && tid == 0)
+        for (int q = 0; q < 7; ++q) a.prof[q] = pacc[q];
 }
 
 }  // namespace
@@ -942,7 +1235,8 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.jcls = sc.get<uint32_t>(dm.B);
     a.jS = sc.get<uint32_t>(dm.B);
     a.pre = sc.get<uint32_t>(dm.B);
-    a.fin = sc.get<uint32_t>(dm.B);
+    a.fx = sc.get<uint32_t>(dm.B);
+    a.fnu = sc.get<uint32_t>(dm.B);
     a.mj = sc.get<uint32_t>(dm.B);
     a.mpo = sc.get<uint32_t>(dm.B);
     a.mhc = sc.get<uint32_t>(dm.B);
@@ -950,9 +1244,10 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.massign = sc.get<uint32_t>(dm.B);
     a.mpos = sc.get<uint32_t>(size_t(N) * dm.b);
     a.recv = sc.get<uint32_t>(size_t(N) * dm.b);
+    a.ur = sc.get<uint32_t>(dm.B);
     if (!a.hm || !a.where || !a.slot || !a.cnt || !a.nst || !a.evb || !a.cand || !a.holes || !a.movedbm ||
-        !a.jx || !a.jnu || !a.jmask || !a.jcls || !a.jS || !a.pre || !a.fin || !a.mj || !a.mpo || !a.mhc ||
-        !a.pairs || !a.massign || !a.mpos || !a.recv)
+        !a.jx || !a.jnu || !a.jmask || !a.jcls || !a.jS || !a.pre || !a.fx || !a.fnu || !a.mj || !a.mpo || !a.mhc ||
+        !a.pairs || !a.massign || !a.mpos || !a.recv || !a.ur)
         return set_error(kInternal, "plan: wide planner scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.hm, 0, size_t(dm.D) * W * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.where, 0xFF, size_t(N) * dm.D * 4, st));
@@ -965,6 +1260,8 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.fb = d_fb;
     a.fa = d_fa;
     a.status = d_status;
+    a.prof = profiling() ? sc.get<unsigned long long>(16) : nullptr;
+    if (a.prof) LSG_CUDA(cudaMemsetAsync(a.prof, 0, 128, st));
 
     const size_t smem = size_t(kWW) * kSortCap * 8 + size_t(kWW) * 256 * 4 +
                         (size_t(2) * kWW * N + 14 * size_t(N) + 3 * size_t(N + 1)) * 4;
@@ -993,10 +1290,23 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     if (P < 1) return set_error(kCapability, "plan: no thread-block cluster fits the wide planner");
     LSG_CUDA(cudaLaunchKernelEx(&cfg, k_plan_wide, a));
     LSG_LAUNCH_CHECK("k_plan_wide");
-    if (profiling()) {
+    if (a.prof) {
+        unsigned long long h[16];
+        LSG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof h, cudaMemcpyDeviceToHost, st));
+        fprintf(stderr, "[lsg profile] wide planner: %llu evictions (%.0f slots scanned each), %llu multi items (%llu pairs)\n",
+                h[8], double(h[9]) / double(h[8] ? h[8] : 1), h[10], h[11]);
+        fprintf(stderr, "[lsg profile] wide planner: serial multi loop %.1f kcyc total (%.0f cyc/item)\n", h[12] / 1e3,
+                double(h[12]) / double(h[10] ? h[10] : 1));
         LSG_CUDA(cudaStreamSynchronize(st));
         fprintf(stderr, "[lsg profile] wide planner: cluster of %d CTAs x %d threads, %zu B smem, N=%u B=%llu T=%llu\n",
                 P, kWT, smem, N, (unsigned long long)dm.B, (unsigned long long)dm.T);
+        const char* names[7] = {"A load/classify", "A2 ranks/pairs", "B multi pass", "C1 hit/fetch counts",
+                                "C2 positions+balance", "D final lists", "E buffer advance"};
+        unsigned long long tot = 0;
+        for (int q = 0; q < 7; ++q) tot += h[q];
+        for (int q = 0; q < 7; ++q)
+            fprintf(stderr, "[lsg profile]   %-22s %10.1f kcyc  %6.2f%%  %8.0f cyc/step\n", names[q], h[q] / 1e3,
+                    100.0 * h[q] / (tot ? tot : 1), double(h[q]) / double(dm.T ? dm.T : 1));
     }
     return kOk;
 }

@@ -14,6 +14,9 @@ CFGS = {
     "cfg4": (131072, 500, 8, 64, 6553),
     "cfg5_N32_E3": (1 << 20, 3, 32, 512, (1 << 20) // 64),
     "cfg5_N32_E10": (1 << 20, 10, 32, 512, (1 << 20) // 64),
+    "cfg5_N64_E10": (1 << 20, 10, 64, 512, (1 << 20) // 128),
+    "cfg5_N128_E10": (1 << 20, 10, 128, 512, (1 << 20) // 256),
+    "cfg5_N256_E10": (1 << 20, 10, 256, 512, (1 << 20) // 512),
 }
 if __name__ != "__main__":
     names = []
