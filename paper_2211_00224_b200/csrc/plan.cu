@@ -1015,11 +1015,14 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
                      const uint32_t* d_order, const uint32_t* d_inv, uint32_t* d_items,
                      uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
                      cudaStream_t st) {
-    // wide worlds (N > 32, global batch > 16384, or packed keys beyond 32
-    // bits) run the cluster step loop of plan_wide.cu; LSG_PLAN_WIDE=1 forces
-    // it for any shape (parity tests of that path on small configs)
+    // wide worlds (N > 32, a global batch beyond shared memory, or packed
+    // keys beyond 32 bits) run the cluster step loop of plan_wide.cu, which
+    // is faster there (cfg5 N=32: 292 vs 528 us/step); LSG_PLAN_WIDE=1 / 0
+    // forces / forbids it (parity tests of both kernels on the same configs)
     const char* fw = std::getenv("LSG_PLAN_WIDE");
-    const bool wide = dm.N > kMaxN || dm.B > kMaxB || dm.T * dm.B >= 0xFFFFFFF0ull || (fw && fw[0] == '1');
+    bool wide = dm.N > kMaxN || dm.B > kMaxSmemB || dm.T * dm.B >= 0xFFFFFFF0ull;
+    if (fw && fw[0] == '1') wide = true;
+    if (fw && fw[0] == '0' && dm.N <= kMaxN && dm.B <= kMaxB && dm.T * dm.B < 0xFFFFFFF0ull) wide = false;
     Scratch sc(st);
     const size_t EK = size_t(dm.E) * dm.keep;
     uint32_t* nu = sc.get<uint32_t>(EK);

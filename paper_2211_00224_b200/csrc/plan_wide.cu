@@ -70,6 +70,7 @@ struct WideArgs {
     uint32_t* nst;                    // [N][4] size, top finite key
     uint32_t* evb;                    // [N][EBW] eviction flags (zero between uses)
     uint32_t* cand;                   // [N][SC] threshold-bin slots
+    uint32_t* candid;                 // [N][SC] their ids
     uint32_t* holes;                  // [N][SC] compaction holes
     uint32_t* movedbm;                // [N][MBW] moved pre-list positions (zero between uses)
     // per-step scratch, batch position j
@@ -122,21 +123,152 @@ __device__ __forceinline__ void evict_one(const WideArgs& a, uint32_t k, unsigne
     atomicSub(&a.cnt[size_t(k) * (a.T + 1) + bin_of(uint32_t(v >> 32), a.T)], 1u);
 }
 
-// Remove the m = size - C largest (key, id) residents of node k (one warp):
-// threshold bin from the per-bin counts, ONE scan of the slots that drops
-// every resident above it (holes below the new size are recorded, tail
-// survivors flagged), a radix select of the r largest ids inside the
-// threshold bin, then tail survivors move into the holes.
+// Eviction team: the tpn warps that own node k. The leader warp walks the
+// node's list; the whole team runs every eviction (scan, select, apply).
+struct Team {
+    uint32_t tpn, wr, bar_id;
+    uint32_t* ctl;   // [8] shared: cmd, tstar, bsz, newsize, hcount, ccount, r, prefix
+    uint32_t* hist;  // [256] shared radix histogram (the leader warp's)
+    __device__ __forceinline__ void sync() const {
+        if (tpn > 1) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(tpn * 32) : "memory");
+    }
+};
+
+// The team part of an eviction of node k (every warp of the team, identical
+// barriers): (1) scan slots [0, bsz) in 128-slot strides per warp, dropping
+// residents above the threshold bin at once, appending holes below the new
+// size and threshold-bin candidates (slot + id), writing tail flag words;
+// (2) radix select (8-bit digits, team histogram) of the r-th largest
+// candidate id; (3) drop the candidates at or above it.
+__device__ void evict_team(const WideArgs& a, uint32_t k, const Team& tm, uint32_t lane) {
+    const uint32_t lt = lanemask_lt_w();
+    const uint32_t tstar = tm.ctl[1], bsz = tm.ctl[2], newsize = tm.ctl[3], r = tm.ctl[6];
+    const uint32_t wr = tm.wr, tpn = tm.tpn;
+    unsigned long long* sk = a.slot + size_t(k) * a.SC;
+    uint32_t* evk = a.evb + size_t(k) * a.EBW;
+    uint32_t* cak = a.cand + size_t(k) * a.SC;
+    uint32_t* cid = a.candid + size_t(k) * a.SC;
+    uint32_t* hk = a.holes + size_t(k) * a.SC;
+    uint32_t* hcount = &tm.ctl[4];
+    for (uint32_t s0 = wr * 128; s0 < bsz; s0 += tpn * 128) {
+        unsigned long long v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t s = s0 + u * 32 + lane;
+            v[u] = s < bsz ? __ldcg(&sk[s]) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t sb = s0 + u * 32, s = sb + lane;
+            const bool valid = s < bsz;
+            const uint32_t bn = bin_of(uint32_t(v[u] >> 32), a.T);
+            const bool ev = valid && bn > tstar, cd = valid && bn == tstar;
+            if (ev) evict_one(a, k, v[u]);
+            const bool hole = ev && s < newsize;
+            const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hole);
+            if (hb) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(hcount, __popc(hb));
+                base = __shfl_sync(0xFFFFFFFFu, base, 0);
+                if (hole) hk[base + __popc(hb & lt)] = s;
+            }
+            const uint32_t tw = __ballot_sync(0xFFFFFFFFu, ev && s >= newsize);
+            if (lane == 0 && sb < bsz && sb + 31 >= newsize) evk[sb >> 5] = tw;
+            const uint32_t cb = __ballot_sync(0xFFFFFFFFu, cd);
+            if (cb) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&tm.ctl[5], __popc(cb));
+                base = __shfl_sync(0xFFFFFFFFu, base, 0);
+                if (cd) {
+                    cak[base + __popc(cb & lt)] = s;
+                    cid[base + __popc(cb & lt)] = uint32_t(v[u]);
+                }
+            }
+        }
+    }
+    tm.sync();
+    const uint32_t ncand = tm.ctl[5];
+    uint32_t thr = 0;
+    if (r < ncand) {
+        uint32_t prefix = 0, pmask = 0, rem = r;
+        for (int sh = 24; sh >= 0; sh -= 8) {
+            for (uint32_t q = wr * 32 + lane; q < 256; q += tpn * 32) tm.hist[q] = 0;
+            tm.sync();
+            __syncwarp();
+            for (uint32_t q = wr * 32 + lane; q < ncand; q += tpn * 32) {
+                const uint32_t id = __ldcg(&cid[q]);
+                if ((id & pmask) == prefix) atomicAdd(&tm.hist[(id >> sh) & 255u], 1u);
+            }
+            tm.sync();
+            __syncwarp();
+            // every warp derives the same digit: lane l owns digits 255-8l .. 248-8l
+            uint32_t hv[8], lsum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                hv[q] = tm.hist[255 - 8 * lane - q];
+                lsum += hv[q];
+            }
+            const uint32_t incl = warp_incl_scan(lsum, lane);
+            const uint32_t excl = incl - lsum;
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, excl < rem && incl >= rem);
+            const uint32_t L = __ffs(bal) - 1;
+            uint32_t dsel = 0, above = 0;
+            if (lane == L) {
+                uint32_t run = excl;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (run + hv[q] >= rem) {
+                        dsel = 255 - 8 * lane - q;
+                        above = run;
+                        break;
+                    }
+                    run += hv[q];
+                }
+            }
+            dsel = __shfl_sync(0xFFFFFFFFu, dsel, L);
+            above = __shfl_sync(0xFFFFFFFFu, above, L);
+            rem -= above;
+            prefix |= dsel << sh;
+            pmask |= 255u << sh;
+            __syncwarp();
+            tm.sync();  // histogram reads done before the next pass clears it
+        }
+        thr = prefix;  // the r-th largest id of the bin (ids are distinct per node)
+    }
+    for (uint32_t q0 = wr * 32; q0 < ncand; q0 += tpn * 32) {
+        const uint32_t q = q0 + lane;
+        bool ev = false;
+        uint32_t s = 0;
+        if (q < ncand && (r >= ncand || __ldcg(&cid[q]) >= thr)) {
+            s = __ldcg(&cak[q]);
+            ev = true;
+            evict_one(a, k, __ldcg(&sk[s]));
+            if (s >= newsize) atomicOr(&evk[s >> 5], 1u << (s & 31));
+        }
+        const bool hole = ev && s < newsize;
+        const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hole);
+        if (hb) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(hcount, __popc(hb));
+            base = __shfl_sync(0xFFFFFFFFu, base, 0);
+            if (hole) hk[base + __popc(hb & lt)] = s;
+        }
+    }
+    tm.sync();
+}
+
+// Remove the m = size - C largest (key, id) residents of node k (leader warp
+// of the team): threshold bin from the per-bin counts (never-used first,
+// then finite bins walked down from the top, 32 per ballot), the team part
+// above, then tail survivors move into the holes.
 __device__ void wide_evict(const WideArgs& a, uint32_t k, uint32_t& bsz, uint32_t& top, uint32_t g,
-                           uint32_t lane, uint32_t* hist) {
+                           uint32_t lane, const Team& tm) {
     const uint32_t lt = lanemask_lt_w();
     const uint32_t m = bsz - a.C;
     uint32_t* cntk = a.cnt + size_t(k) * (a.T + 1);
     unsigned long long* sk = a.slot + size_t(k) * a.SC;
     uint32_t* evk = a.evb + size_t(k) * a.EBW;
-    uint32_t* cak = a.cand + size_t(k) * a.SC;
     uint32_t* hk = a.holes + size_t(k) * a.SC;
-    // ---- threshold bin: never-used first, then finite bins from the top
     uint32_t tstar = 0, r = 0;
     const uint32_t nev = __ldcg(&cntk[a.T]);
     if (nev >= m) {
@@ -172,98 +304,20 @@ __device__ void wide_evict(const WideArgs& a, uint32_t k, uint32_t& bsz, uint32_
         atomicAdd(&a.prof[8], 1ull);
         atomicAdd(&a.prof[9], static_cast<unsigned long long>(bsz));
     }
-    // ---- one scan (4 loads in flight per lane)
-    uint32_t ncand = 0, nh = 0;
-    for (uint32_t s0 = 0; s0 < bsz; s0 += 128) {
-        unsigned long long v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t s = s0 + u * 32 + lane;
-            v[u] = s < bsz ? __ldcg(&sk[s]) : 0ull;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t sb = s0 + u * 32, s = sb + lane;
-            const bool valid = s < bsz;
-            const uint32_t bn = bin_of(uint32_t(v[u] >> 32), a.T);
-            const bool ev = valid && bn > tstar, cd = valid && bn == tstar;
-            if (ev) evict_one(a, k, v[u]);
-            const bool hole = ev && s < newsize;
-            const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hole);
-            if (hole) hk[nh + __popc(hb & lt)] = s;
-            nh += __popc(hb);
-            const uint32_t tw = __ballot_sync(0xFFFFFFFFu, ev && s >= newsize);
-            if (lane == 0 && sb < bsz && sb + 31 >= newsize) evk[sb >> 5] = tw;
-            const uint32_t cb = __ballot_sync(0xFFFFFFFFu, cd);
-            if (cd) cak[ncand + __popc(cb & lt)] = s;
-            ncand += __popc(cb);
-        }
+    if (lane == 0) {
+        tm.ctl[0] = 1;
+        tm.ctl[1] = tstar;
+        tm.ctl[2] = bsz;
+        tm.ctl[3] = newsize;
+        tm.ctl[4] = 0;
+        tm.ctl[5] = 0;
+        tm.ctl[6] = r;
     }
     __syncwarp();
-    // ---- the r largest ids of the threshold bin (ids are distinct per node)
-    uint32_t thr = 0;
-    if (r < ncand) {
-        uint32_t prefix = 0, pmask = 0, rem = r;
-        for (int sh = 24; sh >= 0; sh -= 8) {
-            for (uint32_t q = lane; q < 256; q += 32) hist[q] = 0;
-            __syncwarp();
-            for (uint32_t q = lane; q < ncand; q += 32) {
-                const uint32_t id = uint32_t(__ldcg(&sk[__ldcg(&cak[q])]));
-                if ((id & pmask) == prefix) atomicAdd(&hist[(id >> sh) & 255u], 1u);
-            }
-            __syncwarp();
-            // lane l owns digits 255-8l .. 248-8l (descending)
-            uint32_t hv[8], lsum = 0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                hv[q] = hist[255 - 8 * lane - q];
-                lsum += hv[q];
-            }
-            const uint32_t incl = warp_incl_scan(lsum, lane);
-            const uint32_t excl = incl - lsum;
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, excl < rem && incl >= rem);
-            const uint32_t L = __ffs(bal) - 1;
-            uint32_t dsel = 0, above = 0;
-            if (lane == L) {
-                uint32_t run = excl;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    if (run + hv[q] >= rem) {
-                        dsel = 255 - 8 * lane - q;
-                        above = run;
-                        break;
-                    }
-                    run += hv[q];
-                }
-            }
-            dsel = __shfl_sync(0xFFFFFFFFu, dsel, L);
-            above = __shfl_sync(0xFFFFFFFFu, above, L);
-            rem -= above;
-            prefix |= dsel << sh;
-            pmask |= 255u << sh;
-            __syncwarp();
-        }
-        thr = prefix;  // the r-th largest id of the bin
-    }
-    for (uint32_t q0 = 0; q0 < ncand; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        bool ev = false;
-        uint32_t s = 0;
-        if (q < ncand) {
-            s = __ldcg(&cak[q]);
-            const unsigned long long v = __ldcg(&sk[s]);
-            ev = r >= ncand || uint32_t(v) >= thr;
-            if (ev) {
-                evict_one(a, k, v);
-                if (s >= newsize) atomicOr(&evk[s >> 5], 1u << (s & 31));
-            }
-        }
-        const bool hole = ev && s < newsize;
-        const uint32_t hb = __ballot_sync(0xFFFFFFFFu, hole);
-        if (hole) hk[nh + __popc(hb & lt)] = s;
-        nh += __popc(hb);
-    }
-    __syncwarp();
+    tm.sync();
+    evict_team(a, k, tm, lane);
+    tm.sync();
+    const uint32_t nh = tm.ctl[4];
     // ---- survivors from the tail fill the holes
     uint32_t nmv = 0;
     for (uint32_t s0 = newsize & ~31u; s0 < bsz; s0 += 32) {
@@ -625,7 +679,12 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
     const uint32_t gw = c * kWW + w, GW = P * kWW;
     const uint32_t lt = lanemask_lt_w();
     unsigned long long* my_sort = sortb + w * kSortCap;
-    uint32_t* my_hist = hist + w * 256;
+    // eviction teams: tpn warps per node (power of two, within one CTA)
+    __shared__ uint32_t team_ctl[kWW][8];
+    uint32_t tpn = 1;
+    while (tpn * 2 <= uint32_t(kWW) && GW / (tpn * 2) >= N) tpn *= 2;
+    const Team tm{tpn, w % tpn, 1 + w / tpn, team_ctl[w / tpn], hist + (w - w % tpn) * 256};
+    const uint32_t tg = c * (kWW / tpn) + w / tpn, NT = GW / tpn;
     size_t gbase = 0;
     unsigned long long pacc[7] = {0, 0, 0, 0, 0, 0, 0};
     unsigned long long tprev = clock64();
@@ -1102,7 +1161,17 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
         // of the (size - C)+ largest). Records are prefetched a chunk ahead;
         // a resident's slot is read once per chunk and re-read only after an
         // eviction in the same chunk (compaction may have moved it).
-        for (uint32_t k = gw; k < N; k += GW) {
+        for (uint32_t k = tg; k < N; k += NT) {
+            if (tm.wr != 0) {  // helper warp: join the leader's eviction scans
+                for (;;) {
+                    tm.sync();
+                    const uint32_t cmd = tm.ctl[0];
+                    if (cmd == 1) evict_team(a, k, tm, lane);
+                    tm.sync();
+                    if (cmd != 1) break;
+                }
+                continue;
+            }
             uint32_t bsz = __ldcg(&a.nst[k * 4 + 0]), top = __ldcg(&a.nst[k * 4 + 1]);
             const uint32_t lb = noff[k], le = noff[k + 1];
             const uint32_t kw = k >> 5, kb = 1u << (k & 31);
@@ -1139,7 +1208,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
                     const bool mine = (run >> lane) & 1u;
                     if (hitrun && pending) {
                         if (bsz > a.C) {
-                            wide_evict(a, k, bsz, top, g, lane, my_hist);
+                            wide_evict(a, k, bsz, top, g, lane, tm);
                             if (res && !((done >> lane) & 1u)) {  // slots may have moved
                                 ws = __ldcg(&whk[x]);
                                 old = uint32_t(__ldcg(&sk[ws]) >> 32);
@@ -1171,12 +1240,15 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
                     done |= run;
                 }
             }
-            if (pending && bsz > a.C) wide_evict(a, k, bsz, top, g, lane, my_hist);
+            if (pending && bsz > a.C) wide_evict(a, k, bsz, top, g, lane, tm);
             if (lane == 0) {
                 a.nst[k * 4 + 0] = bsz;
                 a.nst[k * 4 + 1] = top;
+                tm.ctl[0] = 0;  // release the helpers
             }
             __syncwarp();
+            tm.sync();
+            tm.sync();
         }
         cl.sync();  // (7)
         WPHASE(6)
@@ -1227,6 +1299,7 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.nst = sc.get<uint32_t>(size_t(N) * 4);
     a.evb = sc.get<uint32_t>(size_t(N) * a.EBW);
     a.cand = sc.get<uint32_t>(size_t(N) * SC);
+    a.candid = sc.get<uint32_t>(size_t(N) * SC);
     a.holes = sc.get<uint32_t>(size_t(N) * SC);
     a.movedbm = sc.get<uint32_t>(size_t(N) * a.MBW);
     a.jx = sc.get<uint32_t>(dm.B);
@@ -1245,7 +1318,7 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.mpos = sc.get<uint32_t>(size_t(N) * dm.b);
     a.recv = sc.get<uint32_t>(size_t(N) * dm.b);
     a.ur = sc.get<uint32_t>(dm.B);
-    if (!a.hm || !a.where || !a.slot || !a.cnt || !a.nst || !a.evb || !a.cand || !a.holes || !a.movedbm ||
+    if (!a.hm || !a.where || !a.slot || !a.cnt || !a.nst || !a.evb || !a.cand || !a.candid || !a.holes || !a.movedbm ||
         !a.jx || !a.jnu || !a.jmask || !a.jcls || !a.jS || !a.pre || !a.fx || !a.fnu || !a.mj || !a.mpo || !a.mhc ||
         !a.pairs || !a.massign || !a.mpos || !a.recv || !a.ur)
         return set_error(kInternal, "plan: wide planner scratch allocation failed");

@@ -203,12 +203,19 @@ def test_plan_errors(ls):
 
 @pytest.mark.parametrize("D,E,N,b,frac,seed", [(65536, 3, 32, 512, 0.5 / 32, 1), (40000, 4, 16, 1000, 0.03, 2),
                                                (32768 + 777, 3, 32, 300, 0.02, 3)])
-def test_plan_large_global_batch(ls, D, E, N, b, frac, seed):
-    """global batch > 8192: per-item arrays in L2-resident global scratch
-    (cfg5's 32-rank shape, b=512 -> B=16384)."""
+@pytest.mark.parametrize("kernel", ["0", "1"])
+def test_plan_large_global_batch(ls, D, E, N, b, frac, seed, kernel):
+    """global batch > 8192 (cfg5's 32-rank shape, b=512 -> B=16384) through
+    both step-loop kernels: the single-CTA one with per-item arrays in
+    L2-resident global scratch (LSG_PLAN_WIDE=0) and the cluster one."""
+    import os
     c = O.Cfg(D, E, N, b, seed=seed, buffer_capacity=max(1, int(frac * D)), pso_iters=30,
               drop_last=seed != 3)
-    out, ref = check_plan(ls, c)
+    os.environ["LSG_PLAN_WIDE"] = kernel
+    try:
+        out, ref = check_plan(ls, c)
+    finally:
+        del os.environ["LSG_PLAN_WIDE"]
     sim = ls.simulate_plan(out.plan, c.buffer_capacity)
     h, m = O.simulate(ref.items, ref.node_off, N, D, c.buffer_capacity)
     assert np.array_equal(u32(sim.hits), h) and np.array_equal(u32(sim.misses), m)
