@@ -90,6 +90,8 @@ struct ReplayArgs {
     uint32_t* nz;      // [N][nzw] next-use steps that may hold residents
     uint32_t* pbm;     // [N][T][bw] list positions per next-use step
     uint32_t* infbm;   // [N][infw]
+    uint32_t* infsum;  // [N][sumw] non-empty infbm words
+    uint32_t sumw;
     uint32_t* fstack;  // [N][C] freed slots (null when slots are not wanted)
     uint32_t* hits;    // [T][N]
     uint32_t* misses;  // [T][N]
@@ -128,60 +130,127 @@ struct NodeState {
     uint32_t size, top, inftop, infcnt, fresh, nfree;
 };
 
+// Take the `want` largest ids of a node's never-used bitmap (whole warp).
+// The bitmap (bm, one bit per id) has a summary level (sm1, one bit per
+// non-empty bm word), so the walk visits non-empty words only: new never-used
+// residents land at random ids above the harvested region, and a flat walk
+// would cross the whole id range on every eviction. Up to 32 non-empty words
+// are gathered per round (wbuf, 32 shared words of this warp), lane 0 holding
+// the highest; prefix sums of their popcounts tell each lane how many of its
+// word's top bits go. Freed slots are pushed in eviction order (descending
+// id). Returns the ids taken; `top` stays an upper bound of the highest word.
+__device__ __forceinline__ uint32_t never_take(uint32_t* bm, uint32_t* sm1, uint32_t& top, uint32_t want,
+                                               uint32_t* keyk, uint32_t* slotk, uint32_t* fs, uint32_t& nfree,
+                                               uint32_t* wbuf, uint32_t lane) {
+    const uint32_t lt = lanemask_lt_r();
+    uint32_t taken = 0;
+    int32_t cur = int32_t(top);  // highest bm word still to visit
+    while (taken < want && cur >= 0) {
+        // gather up to 32 non-empty bm words <= cur, descending
+        uint32_t ngot = 0;
+        int32_t sw = cur >> 5;
+        uint32_t firstmask = (cur & 31) == 31 ? 0xFFFFFFFFu : ((2u << (cur & 31)) - 1u);
+        while (ngot < 32 && sw >= 0) {
+            const int32_t myws = sw - int32_t(lane);
+            uint32_t v = myws >= 0 ? __ldcg(&sm1[myws]) : 0u;
+            if (lane == 0) v &= firstmask;
+            const uint32_t c = __popc(v);
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= uint32_t(d)) incl += o;
+            }
+            uint32_t r = ngot + incl - c;
+            while (v && r < 32) {
+                const uint32_t bit = 31 - __clz(v);
+                v &= ~(1u << bit);
+                wbuf[r++] = uint32_t(myws) * 32 + bit;
+            }
+            ngot += __shfl_sync(0xFFFFFFFFu, incl, 31);
+            sw -= 32;
+            firstmask = 0xFFFFFFFFu;
+        }
+        __syncwarp();
+        ngot = min(ngot, 32u);
+        if (ngot == 0) break;
+        const int32_t myw = lane < ngot ? int32_t(wbuf[lane]) : -1;
+        const uint32_t lastw = wbuf[ngot - 1];
+        __syncwarp();
+        const uint32_t v = myw >= 0 ? __ldcg(&bm[myw]) : 0u;
+        const uint32_t cnt = __popc(v);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= uint32_t(d)) incl += o;
+        }
+        const uint32_t before = incl - cnt, left = want - taken;
+        const uint32_t take = before < left ? min(cnt, left - before) : 0u;
+        // pass 1: which of my taken ids hold a slot (a miss of the current
+        // run has none yet)
+        uint32_t rest = v, pushes = 0;
+        for (uint32_t t = 0; t < take; ++t) {
+            const uint32_t bit = 31 - __clz(rest);
+            rest &= ~(1u << bit);
+            if (fs && __ldcg(&slotk[uint32_t(myw) * 32 + bit]) != kNone) ++pushes;
+        }
+        uint32_t pinc = pushes;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, pinc, d);
+            if (lane >= uint32_t(d)) pinc += o;
+        }
+        uint32_t q = nfree + pinc - pushes;
+        rest = v;
+        for (uint32_t t = 0; t < take; ++t) {
+            const uint32_t bit = 31 - __clz(rest);
+            rest &= ~(1u << bit);
+            const uint32_t x = uint32_t(myw) * 32 + bit;
+            keyk[x] = kNone;
+            const uint32_t sl = slotk[x];
+            if (sl != kNone) {
+                if (fs) fs[q++] = sl;
+                slotk[x] = kNone;
+            }
+        }
+        if (take) {
+            bm[myw] = rest;
+            if (rest == 0) atomicAnd(&sm1[myw >> 5], ~(1u << (myw & 31)));
+        }
+        nfree += __shfl_sync(0xFFFFFFFFu, pinc, 31);
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const uint32_t got = min(tot, left);
+        taken += got;
+        if (got < tot || taken >= want) {  // stopped inside this round
+            const uint32_t tb = __ballot_sync(0xFFFFFFFFu, take > 0);
+            cur = tb ? int32_t(__shfl_sync(0xFFFFFFFFu, uint32_t(myw), 31 - __clz(tb))) : cur;
+            break;
+        }
+        cur = int32_t(lastw) - 1;
+    }
+    top = cur < 0 ? 0u : uint32_t(cur);
+    __syncwarp();
+    return taken;
+}
+
 // Evict the `need` largest keys of node k (whole warp).
 __device__ void r_evict(const ReplayArgs& a, NodeState& ns, uint32_t k, uint32_t need, uint32_t lane,
-                        uint32_t lt) {
+                        uint32_t lt, uint32_t* wbuf) {
     uint32_t* keyk = a.key + size_t(k) * a.D;
     uint32_t* slotk = a.slot + size_t(k) * a.D;
     uint32_t* fs = a.fstack ? a.fstack + size_t(k) * a.C : nullptr;
     while (need > 0) {
         if (ns.infcnt > 0) {  // never used again on this node: ids descending
-            uint32_t* bm = a.infbm + size_t(k) * a.infw;
-            int32_t wi = int32_t(ns.inftop);
-            bool found = false;
-            while (wi >= 0 && !found) {
-                const int32_t myw = wi - int32_t(lane);
-                const uint32_t v = myw >= 0 ? __ldcg(&bm[myw]) : 0u;
-                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-                if (bal) {
-                    const uint32_t src = __ffs(bal) - 1;
-                    const int32_t hw = wi - int32_t(src);
-                    const uint32_t word = __shfl_sync(0xFFFFFFFFu, v, src);
-                    const uint32_t take = min(uint32_t(__popc(word)), need);
-                    // lane t takes the t-th highest bit of the word
-                    uint32_t m = word, bit = 0;
-                    for (uint32_t t = 0; t <= lane && t < take; ++t) {
-                        bit = 31 - __clz(m);
-                        m &= ~(1u << bit);
-                    }
-                    uint32_t s = kNone;
-                    if (lane < take) {
-                        const uint32_t x = uint32_t(hw) * 32 + bit;
-                        keyk[x] = kNone;
-                        s = slotk[x];
-                        slotk[x] = kNone;
-                    }
-                    const bool push = lane < take && s != kNone && fs;
-                    const uint32_t sbal = __ballot_sync(0xFFFFFFFFu, push);
-                    if (push) fs[ns.nfree + __popc(sbal & lt)] = s;
-                    uint32_t rest = word;
-                    for (uint32_t t = 0; t < take; ++t) rest &= ~(1u << (31 - __clz(rest)));
-                    if (lane == 0) bm[hw] = rest;
-                    ns.nfree += __popc(sbal);
-                    ns.infcnt -= take;
-                    ns.size -= take;
-                    need -= take;
-                    ns.inftop = uint32_t(hw);
-                    found = true;
-                } else {
-                    wi -= 32;
-                }
-            }
-            __syncwarp();
-            if (!found) {
+            const uint32_t got = never_take(a.infbm + size_t(k) * a.infw, a.infsum + size_t(k) * a.sumw, ns.inftop,
+                                            min(need, ns.infcnt), keyk, slotk, fs, ns.nfree, wbuf, lane);
+            if (got == 0) {
                 if (lane == 0) atomicOr(a.status, 2u);
                 ns.infcnt = 0;
             }
+            ns.infcnt -= min(got, ns.infcnt);
+            ns.size -= got;
+            need -= got;
             continue;
         }
         uint32_t* nzk = a.nz + size_t(k) * a.nzw;
@@ -264,6 +333,7 @@ __device__ void r_evict(const ReplayArgs& a, NodeState& ns, uint32_t k, uint32_t
 
 __global__ void __launch_bounds__(kRWarps * 32) k_replay(ReplayArgs a) {
     extern __shared__ __align__(16) uint32_t rdyn[];
+    __shared__ uint32_t rwbuf[kRWarps][32];
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint32_t k = a.k0 + blockIdx.x * kRWarps + wib;
     if (k >= a.k1) return;
@@ -299,7 +369,7 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay(ReplayArgs a) {
         uint32_t run0 = 0;
         auto flush = [&](uint32_t run1) {
             const uint32_t need = ns.size > a.C ? ns.size - a.C : 0u;
-            if (need) r_evict(a, ns, k, need, lane, lt);
+            if (need) r_evict(a, ns, k, need, lane, lt, rwbuf[wib]);
             __syncwarp();
             if (fs) {  // survivors of the run take slots, in list order
                 for (uint32_t c = run0; c < run1; c += 32) {
@@ -345,6 +415,7 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay(ReplayArgs a) {
                     keyk[x] = nu;
                     if (nev) {
                         atomicOr(&infk[x >> 5], 1u << (x & 31));
+                        atomicOr(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
                     } else {
                         const uint32_t beta = nu / a.L, p = nu - beta * a.L;
                         atomicOr(&a.pbm[(size_t(k) * a.T + beta) * a.bw + (p >> 5)], 1u << (p & 31));
@@ -394,6 +465,8 @@ struct ReplayArgsCta {
     uint32_t* slot;    // [N][D]
     uint32_t* nz;      // [N][nzw]
     uint32_t* infbm;   // [N][infw]
+    uint32_t* infsum;  // [N][sumw] non-empty infbm words
+    uint32_t sumw;
     uint32_t* fstack;  // [N][C] freed slots
     uint32_t* hits;    // [T][N]
     uint32_t* misses;  // [T][N]
@@ -427,6 +500,7 @@ __global__ void __launch_bounds__(kRT) k_replay_nextuse_cta(ReplayArgsCta a) {
 
 struct RSharedCta {
     uint32_t size, top, inftop, infcnt, fresh, nfree;
+    uint32_t wbuf[32];  // never_take gather
     uint32_t nruns;
     uint32_t hitcnt;
     uint32_t wsum[kRT / 32];
@@ -437,6 +511,7 @@ __device__ __forceinline__ void r_set_key_cta(const ReplayArgsCta& a, RSharedCta
     a.key[size_t(k) * a.D + x] = nu;
     if (nu == kNever) {
         atomicOr(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
+        atomicOr(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
         atomicAdd(&sh.infcnt, 1u);
         atomicMax(&sh.inftop, x >> 5);
     } else {
@@ -453,43 +528,24 @@ __device__ void r_evict_cta(const ReplayArgsCta& a, RSharedCta& sh, uint32_t k, 
     uint32_t* slotk = a.slot + size_t(k) * a.D;
     uint32_t* fs = a.fstack + size_t(k) * a.C;
     while (need > 0) {
-        if (sh.infcnt > 0) {
-            uint32_t* bm = a.infbm + size_t(k) * a.infw;
-            int32_t wi = int32_t(sh.inftop);
-            bool found = false;
-            while (wi >= 0 && !found) {
-                const int32_t myw = wi - int32_t(lane);
-                const uint32_t v = myw >= 0 ? __ldcg(&bm[myw]) : 0u;
-                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-                if (bal) {
-                    const uint32_t src = __ffs(bal) - 1;
-                    const int32_t hw = wi - int32_t(src);
-                    uint32_t word = __shfl_sync(0xFFFFFFFFu, v, src);
-                    while (word && need > 0) {
-                        const uint32_t bit = 31 - __clz(word);
-                        word &= ~(1u << bit);
-                        const uint32_t x = uint32_t(hw) * 32 + bit;
-                        if (lane == 0) {
-                            keyk[x] = kNone;
-                            atomicAnd(&bm[hw], ~(1u << bit));
-                            const uint32_t s = slotk[x];
-                            if (s != kNone && a.fstack) { fs[sh.nfree++] = s; slotk[x] = kNone; }
-                            sh.infcnt -= 1;
-                            sh.size -= 1;
-                        }
-                        --need;
-                    }
-                    if (lane == 0) sh.inftop = uint32_t(hw);
-                    found = true;
-                } else {
-                    wi -= 32;
+        if (sh.infcnt > 0) {  // never used again on this node: ids descending
+            uint32_t top = sh.inftop, nf = sh.nfree;
+            __syncwarp();
+            const uint32_t got = never_take(a.infbm + size_t(k) * a.infw, a.infsum + size_t(k) * a.sumw, top,
+                                            min(need, sh.infcnt), keyk, slotk, a.fstack ? fs : nullptr, nf,
+                                            sh.wbuf, lane);
+            if (lane == 0) {
+                sh.inftop = top;
+                sh.nfree = nf;
+                if (got == 0) {
+                    atomicOr(a.status, 2u);
+                    sh.infcnt = 0;
                 }
-                __syncwarp();
+                sh.infcnt -= min(got, sh.infcnt);
+                sh.size -= got;
             }
-            if (!found) {
-                if (lane == 0) { atomicOr(a.status, 2u); sh.infcnt = 0; }
-                __syncwarp();
-            }
+            __syncwarp();
+            need -= got;
             continue;
         }
         uint32_t* nzk = a.nz + size_t(k) * a.nzw;
@@ -749,8 +805,10 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     a.nz = sc.get<uint32_t>(size_t(N) * a.nzw);
     a.pbm = L > 128 ? nullptr : sc.get<uint32_t>(size_t(N) * T * a.bw);
     a.infbm = sc.get<uint32_t>(size_t(N) * a.infw);
+    a.sumw = (a.infw + 31) / 32;
+    a.infsum = sc.get<uint32_t>(size_t(N) * a.sumw);
     a.fstack = d_slot ? sc.get<uint32_t>(size_t(N) * std::min<uint64_t>(C, D)) : nullptr;
-    if (!a.nuk || !a.last || !a.key || !a.slot || !a.nz || (L <= 128 && !a.pbm) || !a.infbm || (d_slot && !a.fstack))
+    if (!a.nuk || !a.last || !a.key || !a.slot || !a.nz || (L <= 128 && !a.pbm) || !a.infbm || !a.infsum || (d_slot && !a.fstack))
         return set_error(kInternal, "simulate: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.last, 0xFF, size_t(N) * D * 4, st));  // kNone = no later access
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(N) * D * 4, st));
@@ -758,6 +816,7 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     LSG_CUDA(cudaMemsetAsync(a.nz, 0, size_t(N) * a.nzw * 4, st));
     if (a.pbm) LSG_CUDA(cudaMemsetAsync(a.pbm, 0, size_t(N) * T * a.bw * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.infbm, 0, size_t(N) * a.infw * 4, st));
+    LSG_CUDA(cudaMemsetAsync(a.infsum, 0, size_t(N) * a.sumw * 4, st));
     a.hits = d_hits;
     a.misses = d_misses;
     a.slot_out = d_slot;
@@ -769,7 +828,7 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         c.nzw = a.nzw; c.infw = a.infw;
         c.items = d_items; c.node_off = d_node_off; c.gb = gb;
         c.nuk = a.nuk; c.last = a.last; c.key = a.key; c.slot = a.slot; c.nz = a.nz;
-        c.infbm = a.infbm; c.fstack = a.fstack; c.hits = d_hits; c.misses = d_misses;
+        c.infbm = a.infbm; c.infsum = a.infsum; c.sumw = a.sumw; c.fstack = a.fstack; c.hits = d_hits; c.misses = d_misses;
         c.slot_out = d_slot; c.status = d_status;
         k_replay_nextuse_cta<<<nk, kRT, 0, st>>>(c);
         LSG_LAUNCH_CHECK("k_replay_nextuse_cta");
