@@ -35,6 +35,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "lru.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -59,15 +60,16 @@ struct WideArgs {
     uint32_t SC;                      // slots per node (C + B)
     uint32_t EBW;                     // eviction-flag words per node
     uint32_t MBW;                     // moved-flag words per node
-    int remap, balance;
+    int remap, balance, lru;
     const uint32_t* trace;            // [E][keep]
     const uint32_t* order;            // [E]
     const uint32_t* nu;               // [E*keep] next-use step, execution order
     uint32_t* hm;                     // [D][W] holder masks
-    uint32_t* where;                  // [N][D] slot of a resident id, kNone otherwise
+    uint32_t* where;                  // [N][D] slot of a resident id (LRU: node time of its last access), kNone otherwise
+    uint32_t* sbase;                  // [T] first item of each step (LRU front walk)
     unsigned long long* slot;         // [N][SC] (key << 32 | id), dense in [0, size)
     uint32_t* cnt;                    // [N][T+1] residents per key bin (bin T = never used)
-    uint32_t* nst;                    // [N][4] size, top finite key
+    uint32_t* nst;                    // [N][8] size, top finite key | LRU: size, -, t, front step/index/time
     uint32_t* evb;                    // [N][EBW] eviction flags (zero between uses)
     uint32_t* cand;                   // [N][SC] threshold-bin slots
     uint32_t* candid;                 // [N][SC] their ids
@@ -702,6 +704,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
         const uint32_t* nurow = a.nu + size_t(i) * a.keep + lo;
         const uint32_t R = ((len + GW * 32 - 1) / (GW * 32)) * 32;
         const uint32_t j0 = min(gw * R, len), j1 = min(j0 + R, len);
+        if (a.lru && c == 0 && tid == 0) a.sbase[g] = uint32_t(gbase);
 
         // ------------------------------------------------ A: load + classify
         for (uint32_t k = lane; k < N; k += 32) {
@@ -1172,7 +1175,32 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
                 }
                 continue;
             }
-            uint32_t bsz = __ldcg(&a.nst[k * 4 + 0]), top = __ldcg(&a.nst[k * 4 + 1]);
+            if (a.lru) {  // LruBuffer (buffer.cpp:61-82) through lru.cuh
+                uint32_t* ns = a.nst + size_t(k) * 8;
+                LruNode st{__ldcg(&ns[0]), __ldcg(&ns[2]), __ldcg(&ns[3]), __ldcg(&ns[4]), __ldcg(&ns[5]), 0};
+                const LruPlanView v{a.items, a.node_off, nullptr, a.sbase, N, k};
+                const uint32_t kw = k >> 5, kb = 1u << (k & 31);
+                lru_step(
+                    v, st, a.where + size_t(k) * a.D, a.items + gbase + noff[k], noff[k + 1] - noff[k], a.C, lane,
+                    a.status, [](uint32_t, uint32_t) {},
+                    [&](uint32_t x, uint32_t y) {
+                        atomicOr(&a.hm[size_t(x) * W + kw], kb);
+                        if (y != kNone) atomicAnd(&a.hm[size_t(y) * W + kw], ~kb);
+                    });
+                if (lane == 0) {
+                    ns[0] = st.size;
+                    ns[2] = st.t;
+                    ns[3] = st.fg;
+                    ns[4] = st.fi;
+                    ns[5] = st.ft;
+                    tm.ctl[0] = 0;  // release the helpers
+                }
+                __syncwarp();
+                tm.sync();
+                tm.sync();
+                continue;
+            }
+            uint32_t bsz = __ldcg(&a.nst[k * 8 + 0]), top = __ldcg(&a.nst[k * 8 + 1]);
             const uint32_t lb = noff[k], le = noff[k + 1];
             const uint32_t kw = k >> 5, kb = 1u << (k & 31);
             uint32_t* cntk = a.cnt + size_t(k) * (a.T + 1);
@@ -1242,8 +1270,8 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
             }
             if (pending && bsz > a.C) wide_evict(a, k, bsz, top, g, lane, tm);
             if (lane == 0) {
-                a.nst[k * 4 + 0] = bsz;
-                a.nst[k * 4 + 1] = top;
+                a.nst[k * 8 + 0] = bsz;
+                a.nst[k * 8 + 1] = top;
                 tm.ctl[0] = 0;  // release the helpers
             }
             __syncwarp();
@@ -1261,7 +1289,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
 
 }  // namespace
 
-int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, const uint32_t* d_trace,
+int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int balance, const uint32_t* d_trace,
                      const uint32_t* d_order, const uint32_t* d_nu, uint32_t* d_items, uint32_t* d_node_off,
                      uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status, cudaStream_t st) {
     if (dm.N > kWMaxN)
@@ -1289,6 +1317,7 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.MBW = (dm.b + 31) / 32;
     a.remap = remap;
     a.balance = balance;
+    a.lru = lru;
     a.trace = d_trace;
     a.order = d_order;
     a.nu = d_nu;
@@ -1296,7 +1325,8 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.where = sc.get<uint32_t>(size_t(N) * dm.D);
     a.slot = sc.get<unsigned long long>(size_t(N) * SC);
     a.cnt = sc.get<uint32_t>(size_t(N) * (dm.T + 1));
-    a.nst = sc.get<uint32_t>(size_t(N) * 4);
+    a.nst = sc.get<uint32_t>(size_t(N) * 8);
+    a.sbase = sc.get<uint32_t>(dm.T + 1);
     a.evb = sc.get<uint32_t>(size_t(N) * a.EBW);
     a.cand = sc.get<uint32_t>(size_t(N) * SC);
     a.candid = sc.get<uint32_t>(size_t(N) * SC);
@@ -1318,14 +1348,14 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int remap, int balance, con
     a.mpos = sc.get<uint32_t>(size_t(N) * dm.b);
     a.recv = sc.get<uint32_t>(size_t(N) * dm.b);
     a.ur = sc.get<uint32_t>(dm.B);
-    if (!a.hm || !a.where || !a.slot || !a.cnt || !a.nst || !a.evb || !a.cand || !a.candid || !a.holes || !a.movedbm ||
+    if (!a.hm || !a.where || !a.slot || !a.cnt || !a.nst || !a.sbase || !a.evb || !a.cand || !a.candid || !a.holes || !a.movedbm ||
         !a.jx || !a.jnu || !a.jmask || !a.jcls || !a.jS || !a.pre || !a.fx || !a.fnu || !a.mj || !a.mpo || !a.mhc ||
         !a.pairs || !a.massign || !a.mpos || !a.recv || !a.ur)
         return set_error(kInternal, "plan: wide planner scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.hm, 0, size_t(dm.D) * W * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.where, 0xFF, size_t(N) * dm.D * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.cnt, 0, size_t(N) * (dm.T + 1) * 4, st));
-    LSG_CUDA(cudaMemsetAsync(a.nst, 0, size_t(N) * 16, st));
+    LSG_CUDA(cudaMemsetAsync(a.nst, 0, size_t(N) * 32, st));
     LSG_CUDA(cudaMemsetAsync(a.evb, 0, size_t(N) * a.EBW * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.movedbm, 0, size_t(N) * a.MBW * 4, st));
     a.items = d_items;

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "lru.cuh"
 
 namespace lsg {
 
@@ -753,10 +754,81 @@ __global__ void __launch_bounds__(kRT) k_replay_cta(ReplayArgsCta a) {
     }
 }
 
+// ---- LRU replay (simulate_plan with Policy::Lru, buffer.cpp:61-82): one
+// warp per node walks the node's accesses through lru_step (lru.cuh). Slots:
+// a miss takes its victim's slot, or a fresh one while the buffer fills; hits
+// report their slot at the access (bit 31), misses the slot they hold at the
+// end of the step (LSG_NEVER if a later miss of the step evicted them again).
+struct LruReplayArgs {
+    uint32_t T, N, D, C, k0, k1;
+    const uint32_t* items;
+    const uint32_t* node_off;
+    const uint64_t* gb;
+    uint32_t* last;      // [N][D]
+    uint32_t* slot;      // [N][D] or null
+    uint32_t* hits;      // [T][N]
+    uint32_t* misses;    // [T][N]
+    uint32_t* slot_out;  // [total items] or null
+    uint32_t* status;
+};
+
+__global__ void __launch_bounds__(kRWarps * 32) k_replay_lru(LruReplayArgs a) {
+    __shared__ uint32_t hbm_all[kRWarps][kRMaxList / 32];  // hit flags of the step
+    uint32_t* hbm = hbm_all[threadIdx.x >> 5];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t k = a.k0 + blockIdx.x * kRWarps + (threadIdx.x >> 5);
+    if (k >= a.k1) return;
+    uint32_t* last = a.last + size_t(k) * a.D;
+    uint32_t* slotk = a.slot ? a.slot + size_t(k) * a.D : nullptr;
+    const LruPlanView v{a.items, a.node_off, a.gb, nullptr, a.N, k};
+    LruNode st{0, 0, 0, 0, 0, 0};
+    for (uint32_t g = 0; g < a.T; ++g) {
+        const uint32_t L = v.len(g);
+        const uint64_t base = a.gb[g] + a.node_off[size_t(g) * (a.N + 1) + k];
+        const uint32_t* lst = a.items + base;
+        uint32_t* so = a.slot_out ? a.slot_out + base : nullptr;
+        if (so) {
+            for (uint32_t wd = lane; wd < (L + 31) / 32; wd += 32) hbm[wd] = 0;
+            __syncwarp();
+        }
+        const uint32_t miss = lru_step(
+            v, st, last, lst, L, a.C, lane, a.status,
+            [&](uint32_t i, uint32_t x) {
+                if (so) {
+                    so[i] = slotk[x] | kHit;
+                    atomicOr(&hbm[i >> 5], 1u << (i & 31));
+                }
+            },
+            [&](uint32_t x, uint32_t y) {
+                if (!slotk) return;
+                if (y != kNone) {
+                    slotk[x] = slotk[y];
+                    slotk[y] = kNone;
+                } else {
+                    slotk[x] = st.fresh++;
+                }
+            });
+        st.fresh = __shfl_sync(0xFFFFFFFFu, st.fresh, 0);
+        if (so) {
+            __syncwarp();
+            for (uint32_t i = lane; i < L; i += 32) {
+                if ((hbm[i >> 5] >> (i & 31)) & 1u) continue;  // a hit, reported at its access
+                const uint32_t x = __ldcg(&lst[i]) & ~kHit;
+                so[i] = __ldcg(&last[x]) != kNone ? slotk[x] : kNever;
+            }
+        }
+        if (lane == 0) {
+            a.hits[size_t(g) * a.N + k] = L - miss;
+            a.misses[size_t(g) * a.N + k] = miss;
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace
 
 int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N,
-                    uint64_t D, uint64_t C, uint32_t k0, uint32_t k1, uint32_t* d_hits,
+                    uint64_t D, uint64_t C, int policy, uint32_t k0, uint32_t k1, uint32_t* d_hits,
                     uint32_t* d_misses, uint32_t* d_slot, uint32_t* d_status, cudaStream_t st) {
     if (k1 <= k0 || T == 0) return kOk;
     Scratch sc(st);
@@ -783,6 +855,31 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     if (L == 0) L = 1;
     if (T * L >= 0xFFFFFFF0ull) return set_error(kCapability, "simulate: plan too large for 32-bit position keys");
     if (L > kRMaxList) return set_error(kCapability, "simulate: node list longer than 16384 samples");
+    if (policy == 1) {  // LRU
+        LruReplayArgs r{};
+        r.T = uint32_t(T);
+        r.N = N;
+        r.D = uint32_t(D);
+        r.C = uint32_t(std::min<uint64_t>(C, 0xFFFFFFF0ull));
+        r.k0 = k0;
+        r.k1 = k1;
+        r.items = d_items;
+        r.node_off = d_node_off;
+        r.gb = gb;
+        r.last = sc.get<uint32_t>(size_t(N) * D);
+        r.slot = d_slot ? sc.get<uint32_t>(size_t(N) * D) : nullptr;
+        if (!r.last || (d_slot && !r.slot)) return set_error(kInternal, "simulate: scratch allocation failed");
+        LSG_CUDA(cudaMemsetAsync(r.last, 0xFF, size_t(N) * D * 4, st));
+        if (r.slot) LSG_CUDA(cudaMemsetAsync(r.slot, 0xFF, size_t(N) * D * 4, st));
+        r.hits = d_hits;
+        r.misses = d_misses;
+        r.slot_out = d_slot;
+        r.status = d_status;
+        const uint32_t nk = k1 - k0;
+        k_replay_lru<<<(nk + kRWarps - 1) / kRWarps, kRWarps * 32, 0, st>>>(r);
+        LSG_LAUNCH_CHECK("k_replay_lru");
+        return kOk;
+    }
     ReplayArgs a{};
     a.T = uint32_t(T);
     a.N = N;

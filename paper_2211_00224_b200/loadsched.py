@@ -20,7 +20,7 @@ from ._lib import HIT_BIT, NEVER, LsgConfig, LsgError, LsgPlanOut, LsgShape, che
 __all__ = [
     "TraceConfig", "PsoParams", "PipelineConfig", "AccessTrace", "ReuseGraph", "EpochOrder",
     "PsoResult", "SchedulePlan", "PlanOutput", "SimResult", "generate_trace", "build_reuse_graph",
-    "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "simulate_plan",
+    "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "baseline_config", "simulate_plan",
     "store_fill", "gather", "batch_fetch", "StepFetcher", "Error", "ConfigError", "ValidationError", "CapabilityError",
     "StorageError", "InternalError", "HIT_BIT", "NEVER",
 ]
@@ -353,6 +353,14 @@ def plan_schedule_host(config: PipelineConfig, pinned: bool = True) -> PlanOutpu
     c = config.to_c()
     _check(lib().lsg_plan_host(ctypes.byref(c), ctypes.byref(out), _stream()))
     return _wrap_plan(config, sh, b)
+
+
+def baseline_config(config: PipelineConfig) -> PipelineConfig:
+    """pipeline.cpp:122-131 — the comparison pass run_pipeline plans beside the
+    optimised one: LRU buffers, identity order, slicing, no balance, no chunks."""
+    import dataclasses
+    return dataclasses.replace(config, policy="lru", optim_order=False, optim_remap=False,
+                               optim_balance=False, optim_chunk=False, chunk_insert_redundant=False)
 
 
 def simulate_plan(plan: SchedulePlan, capacity: int, policy: str = "clairvoyant",
