@@ -6,9 +6,10 @@
 // names, function signatures and exception classes below follow the reference
 // API for the planner path (cited per declaration); results are bit-identical.
 // Everything is computed on the current CUDA device; inputs are uploaded and
-// outputs returned by value as the reference does. Out of this header (and out
-// of scope): text formats, Store files, the cost model,
-// the LRU policy, chunk_insert_redundant.
+// outputs returned by value as the reference does. Both buffer policies
+// (Clairvoyant, Lru) run on device. Out of this header (and out of scope, see
+// DESIGN.md §8): text formats, Store files, the cost model,
+// chunk_insert_redundant.
 #pragma once
 
 #include <cstdint>
@@ -206,5 +207,9 @@ struct PlanOutput {
 };
 
 PlanOutput plan_schedule(const PipelineConfig& config);
+
+// pipeline.cpp:122-131: the comparison pass of run_pipeline (LRU buffers,
+// identity order, slicing, no balance, no chunking).
+PipelineConfig baseline_config(const PipelineConfig& config);
 
 }  // namespace loadsched

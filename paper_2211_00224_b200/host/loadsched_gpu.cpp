@@ -244,6 +244,17 @@ bool same_multiset(const StepAssignment& step, const std::vector<SampleId>& batc
     return got == want;
 }
 
+PipelineConfig baseline_config(const PipelineConfig& config) {
+    PipelineConfig base = config;
+    base.policy = Policy::Lru;
+    base.optim_order = false;
+    base.optim_remap = false;
+    base.optim_balance = false;
+    base.optim_chunk = false;
+    base.chunk_insert_redundant = false;
+    return base;
+}
+
 PlanOutput plan_schedule(const PipelineConfig& config) {
     const lsg_config c = to_c(config);
     lsg_shape sh;

@@ -71,6 +71,11 @@ static int run_checks() {
     SimResult sim = simulate_plan(out.plan, 64, Policy::Clairvoyant);
     EXPECT(sim.total_misses == 4864 && sim.total_hits == 1280);
     EXPECT(sim.rows.size() == 6 * 32 * 4);
+    // the README demo's baseline pass: LRU, identity order, slicing (README.md:87)
+    const PipelineConfig base = baseline_config(c);
+    EXPECT(base.policy == Policy::Lru && !base.optim_order && !base.optim_remap && !base.optim_balance);
+    SimResult bs = simulate_plan(plan_schedule(base).plan, 64, Policy::Lru);
+    EXPECT(bs.total_misses == 6109);
     // a buffer holding the whole dataset only cold-misses (tests/test_pipeline.cpp:164-173)
     PipelineConfig w;
     w.trace = {64, 3, 1, 8, 5, true};
