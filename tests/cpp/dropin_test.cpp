@@ -83,9 +83,9 @@ static int run_checks() {
     SimResult ws = simulate_plan(plan_schedule(w).plan, 64, Policy::Clairvoyant);
     EXPECT(ws.total_misses == 64 && ws.total_hits == 3 * 64 - 64);
     // capability guards are typed, never a silent CPU path
-    PipelineConfig lru = demo();
-    lru.policy = Policy::Lru;
-    EXPECT(throws<CapabilityError>([&] { plan_schedule(lru); }));
+    PipelineConfig red = demo();
+    red.chunk_insert_redundant = true;
+    EXPECT(throws<CapabilityError>([&] { plan_schedule(red); }));
     std::printf("dropin_test: %d passed, %d failed\n", passes, fails);
     return fails ? 1 : 0;
 }
