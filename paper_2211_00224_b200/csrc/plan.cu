@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 uint32_t Mk[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) Mk[k] = 0;
+                unsigned long long dchain = 0;
                 const uint32_t nm = sm.nmulti;
                 const uint32_t kSent = (b << 4) - 1u;
                 auto stage = [&](uint32_t base, uint32_t buf) {
@@ -559,6 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     const uint32_t myj = lane < cnt ? s.pre[base + lane] : 0u;
                     const uint4* rows = reinterpret_cast<const uint4*>(&sm.stg[buf][0][0]);
                     uint32_t myres = kSent;
+                    const unsigned long long tc0 = a.prof ? clock64() : 0ull;
 #pragma unroll
                     for (int u = 0; u < 32; ++u) {
                         const uint4 r0 = rows[2 * u], r1 = rows[2 * u + 1];
@@ -571,6 +573,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                         Mk[4] += cl == K4 ? 16u : 0u; Mk[5] += cl == K5 ? 16u : 0u;
                         Mk[6] += cl == K6 ? 16u : 0u; Mk[7] += cl == K7 ? 16u : 0u;
                         myres = lane == uint32_t(u) ? cl : myres;
+                    }
+                    if (a.prof) {
+                        const uint32_t dep = myres & 1u;  // keep the timer after the chain
+                        const unsigned long long tc1 = clock64() + dep;
+                        if (lane == 0) dchain += tc1 - tc0;
                     }
                     // lane u: item u's decision -> node list position + E's input
                     if (lane < cnt) {
@@ -585,7 +592,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     }
                     __syncwarp();
                 }
-                if (a.prof && lane == 0) atomicAdd(&a.prof[12], (unsigned long long)nm);
+                if (a.prof && lane == 0) {
+                    atomicAdd(&a.prof[12], (unsigned long long)nm);
+                    atomicAdd(&a.prof[13], dchain);
+                }
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     if (lane == uint32_t(k) && uint32_t(k) < N) sm.mtot[k] = Mk[k] >> 4;
@@ -1118,8 +1128,8 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
         unsigned long long tot = 0;
         for (int q = 0; q < 10; ++q) tot += h[q];
 
-        fprintf(stderr, "[lsg profile] D: %llu multi-holder items (%.1f cyc/item incl. barrier)\n", h[12],
-                double(h[2]) / double(h[12] ? h[12] : 1));
+        fprintf(stderr, "[lsg profile] D: %llu multi-holder items (%.1f cyc/item incl. barrier, %.1f in the chain)\n",
+                h[12], double(h[2]) / double(h[12] ? h[12] : 1), double(h[13]) / double(h[12] ? h[12] : 1));
         fprintf(stderr, "[lsg profile] plan loop T=%llu steps, %.1f Mcycles total\n",
                 (unsigned long long)dm.T, tot / 1e6);
         for (int q = 0; q < 10; ++q)
