@@ -164,6 +164,44 @@ int lsg_fetch_step(void* const* d_bufs, void* const* d_outs, const uint32_t* d_i
                    uint32_t node_end, uint64_t rows_hint, uint64_t sample_bytes, uint64_t fill_seed,
                    void* stream);
 
+/* ---- The sample Store (store.hpp:13-81, store.cpp:37-148): SLRD files
+ *      (22-byte header + one continuous splitmix64 payload stream).
+ *      Errors: Storage (6) for I/O, format and budget failures, Validation
+ *      (3) for bad ranges, as the reference throws them. */
+typedef struct lsg_store lsg_store;
+
+/* create_store(path, count, size, fill_seed, max_bytes) (store.cpp:37-82);
+ * the payload is computed on the GPU and written out. Byte-identical to the
+ * reference file. */
+int lsg_store_create(const char* path, uint64_t sample_count, uint64_t sample_size, uint64_t fill_seed,
+                     uint64_t max_bytes, void* stream);
+
+/* Store::Store (store.cpp:84-117): validates magic, version, file length. */
+int lsg_store_open(const char* path, lsg_store** out);
+int lsg_store_info(const lsg_store* h, uint64_t* sample_count, uint64_t* sample_size);
+void lsg_store_close(lsg_store* h);
+
+/* Store::read_chunk (store.cpp:141-148) into host memory; read_one is
+ * count == 1 (store.cpp:134-139). */
+int lsg_store_read(const lsg_store* h, uint64_t start, uint64_t count, void* h_dst);
+
+/* Samples h_ids[0..n) into device rows (pitch = sample size): the ids are
+ * cut into chunk reads of span <= threshold (plan_chunks, chunking.cpp:9-33)
+ * read in parallel into pinned staging, moved to HBM in one async copy and
+ * scattered to their rows. Stream-ordered. */
+int lsg_store_read_rows(lsg_store* h, const uint32_t* h_ids, uint64_t n, uint64_t threshold, void* d_rows,
+                        void* stream);
+
+/* lsg_fetch_step with the misses read from the Store instead of
+ * synthesised: hits gathered from the HBM buffers, misses read from the file
+ * (chunk reads of span <= threshold) into their batch rows and, unless the
+ * replay bypassed them, their new buffer slots. h_bufs / h_outs: HOST arrays
+ * holding the same device pointers as d_bufs / d_outs. */
+int lsg_fetch_step_store(lsg_store* h, void* const* d_bufs, void* const* d_outs, void* const* h_bufs,
+                         void* const* h_outs, const uint32_t* d_items, const uint32_t* d_slots,
+                         const uint32_t* d_node_off, uint32_t node_begin, uint32_t node_end, uint64_t rows_hint,
+                         uint64_t threshold, void* stream);
+
 /* Number of kernel launches issued by this library since load (for the
  * bench's gpu_launches claim). */
 uint64_t lsg_launch_count(void);

@@ -380,6 +380,12 @@ def ref_time(cfg: Cfg, reps: int = 1) -> dict:
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
+def ref_store_file(path: str, count: int, size: int, seed: int) -> None:
+    """The UNMODIFIED reference create_store writes `path` (header + payload)."""
+    subprocess.run([REF_DUMP, "storefile", str(path), str(count), str(size), str(seed)], check=True,
+                   capture_output=True)
+
+
 def ref_store(count: int, size: int, seed: int) -> np.ndarray:
     with tempfile.TemporaryDirectory() as d:
         p = os.path.join(d, "payload")

@@ -10,6 +10,7 @@
 //   ref_dump simulate <indir>  C policy       simulate_plan over a dumped plan
 //   ref_dump time     <samples> key=value...  stage timings (JSON on stdout)
 //   ref_dump store    <out> count size seed   Store payload bytes (no header)
+//   ref_dump storefile <path> count size seed  the reference's store file
 //   ref_dump gather   <dir> count size n thr  Store::read_one batch-fetch timing
 //
 // key=value pairs go through the reference's apply_config_entry
@@ -327,6 +328,13 @@ int cmd_store(int argc, char** argv) {
     return 0;
 }
 
+// the reference's create_store output itself (header + payload) at <path>
+int cmd_storefile(int argc, char** argv) {
+    if (argc < 6) throw ValidationError("storefile <path> count size seed");
+    create_store(argv[2], std::stoull(argv[3]), std::stoull(argv[4]), std::stoull(argv[5]), ~0ULL);
+    return 0;
+}
+
 } // namespace
 
 int main(int argc, char** argv) {
@@ -340,6 +348,7 @@ int main(int argc, char** argv) {
         if (cmd == "simulate") return cmd_simulate(argc, argv);
         if (cmd == "time") return cmd_time(argc, argv);
         if (cmd == "store") return cmd_store(argc, argv);
+        if (cmd == "storefile") return cmd_storefile(argc, argv);
         if (cmd == "gather") return cmd_gather(argc, argv);
         std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
         return 1;

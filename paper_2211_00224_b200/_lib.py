@@ -70,6 +70,8 @@ EXPORTS = [
     "lsg_version", "lsg_last_error", "lsg_shape_of", "lsg_generate_trace",
     "lsg_build_reuse_graph", "lsg_pso_order", "lsg_plan", "lsg_plan_host", "lsg_simulate",
     "lsg_store_fill", "lsg_gather", "lsg_batch_fetch", "lsg_fetch_step", "lsg_launch_count",
+    "lsg_store_create", "lsg_store_open", "lsg_store_info", "lsg_store_close", "lsg_store_read",
+    "lsg_store_read_rows", "lsg_fetch_step_store",
 ]
 
 
@@ -109,6 +111,14 @@ def lib() -> ctypes.CDLL:
         L.lsg_gather.argtypes = [P, P, u64, u64, P, P]
         L.lsg_batch_fetch.argtypes = [P, P, P, u64, u64, u64, P, P]
         L.lsg_fetch_step.argtypes = [P, P, P, P, P, u32, u32, u64, u64, u64, P]
+        L.lsg_store_create.argtypes = [ctypes.c_char_p, u64, u64, u64, u64, P]
+        L.lsg_store_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+        L.lsg_store_info.argtypes = [P, ctypes.POINTER(u64), ctypes.POINTER(u64)]
+        L.lsg_store_close.argtypes = [P]
+        L.lsg_store_close.restype = None
+        L.lsg_store_read.argtypes = [P, u64, u64, P]
+        L.lsg_store_read_rows.argtypes = [P, P, u64, u64, P, P]
+        L.lsg_fetch_step_store.argtypes = [P, P, P, P, P, P, P, P, u32, u32, u64, u64, P]
         _lib = L
     return _lib
 

@@ -228,6 +228,29 @@ int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* 
     return kOk;
 }
 
+// hits only (the Store-backed step fetch reads the misses from the file)
+int gather_step_hits_device(void* const* d_bufs, void* const* d_outs, const uint32_t* d_slots,
+                            const uint32_t* d_node_off, uint32_t k0, uint32_t k1, uint64_t rows_hint,
+                            uint64_t sample_bytes, cudaStream_t st) {
+    if (k1 <= k0) return kOk;
+    if (sample_bytes == 0 || sample_bytes % 16 != 0)
+        return set_error(kValidation, "fetch_step: sample_bytes must be a positive multiple of 16");
+    StepFetch f{};
+    f.slots = d_slots;
+    f.node_off = d_node_off;
+    f.bufs = reinterpret_cast<uint4* const*>(d_bufs);
+    f.outs = reinterpret_cast<uint4* const*>(d_outs);
+    f.k0 = k0;
+    f.k1 = k1;
+    f.vec_per_row = sample_bytes / 16;
+    f.tiles_per_row = (f.vec_per_row + kTileVec - 1) / kTileVec;
+    const uint64_t rows = rows_hint ? rows_hint : 1;
+    const unsigned grid = unsigned(std::min<uint64_t>(rows * f.tiles_per_row, 148ull * 8));
+    k_fetch_step_hits<<<grid, kGatherThreads, 0, st>>>(f);
+    LSG_LAUNCH_CHECK("k_fetch_step_hits");
+    return kOk;
+}
+
 int batch_fetch_device(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots, uint64_t n,
                        uint64_t sample_bytes, uint64_t seed, void* d_out, cudaStream_t st) {
     if (n == 0) return kOk;

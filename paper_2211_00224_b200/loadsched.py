@@ -21,7 +21,8 @@ __all__ = [
     "TraceConfig", "PsoParams", "PipelineConfig", "AccessTrace", "ReuseGraph", "EpochOrder",
     "PsoResult", "SchedulePlan", "PlanOutput", "SimResult", "generate_trace", "build_reuse_graph",
     "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "baseline_config", "simulate_plan",
-    "store_fill", "gather", "batch_fetch", "StepFetcher", "Error", "ConfigError", "ValidationError", "CapabilityError",
+    "store_fill", "gather", "batch_fetch", "StepFetcher", "StoreHeader", "Store", "create_store",
+    "STORE_HEADER_BYTES", "DEFAULT_STORE_BUDGET", "Error", "ConfigError", "ValidationError", "CapabilityError",
     "StorageError", "InternalError", "HIT_BIT", "NEVER",
 ]
 
@@ -414,22 +415,120 @@ def batch_fetch(buf: torch.Tensor, ids: torch.Tensor, slots: torch.Tensor, sampl
     return out
 
 
+# ------------------------------------------------------------------ Store --
+STORE_HEADER_BYTES = 22          # kStoreHeaderBytes (store.hpp:23)
+DEFAULT_STORE_BUDGET = 1 << 30   # kDefaultStoreBudget (store.hpp:24)
+
+
+@dataclass
+class StoreHeader:
+    """store.hpp:16-20"""
+    version: int = 1
+    sample_count: int = 0
+    sample_size: int = 0
+
+
+def create_store(path: str, sample_count: int, sample_size: int, fill_seed: int,
+                 max_bytes: int = DEFAULT_STORE_BUDGET) -> None:
+    """store.cpp:37-82 — SLRD file, byte-identical to the reference's; the
+    splitmix64 payload is computed on the GPU."""
+    _check(lib().lsg_store_create(str(path).encode(), sample_count, sample_size, fill_seed, max_bytes,
+                                  _stream()))
+
+
+class Store:
+    """store.hpp:26-50 — read-only handle over an SLRD file (positional reads,
+    safe for concurrent use). Open validates magic, version and length
+    (StorageError); out-of-range reads raise ValidationError."""
+
+    def __init__(self, path: str):
+        h = ctypes.c_void_p()
+        _check(lib().lsg_store_open(str(path).encode(), ctypes.byref(h)))
+        self._h = h
+        c, z = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib().lsg_store_info(self._h, ctypes.byref(c), ctypes.byref(z)))
+        self._header = StoreHeader(1, c.value, z.value)
+
+    def header(self) -> StoreHeader:
+        return self._header
+
+    @property
+    def sample_count(self) -> int:
+        return self._header.sample_count
+
+    @property
+    def sample_size(self) -> int:
+        return self._header.sample_size
+
+    def read_chunk(self, start: int, count: int) -> bytes:
+        """store.cpp:141-148: one contiguous read of `count` samples."""
+        if count == 0:
+            _check(lib().lsg_store_read(self._h, start, 0, ctypes.c_void_p(1)))
+        buf = ctypes.create_string_buffer(max(1, count * self.sample_size))
+        _check(lib().lsg_store_read(self._h, start, count, buf))
+        return buf.raw[: count * self.sample_size]
+
+    def read_one(self, index: int) -> bytes:
+        """store.cpp:134-139"""
+        return self.read_chunk(index, 1)
+
+    def read_rows(self, ids, threshold: int = 15, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Samples `ids` straight into HBM rows (chunk reads of span <=
+        threshold, parallel preads, one async host-to-device copy)."""
+        import numpy as np
+        h_ids = np.ascontiguousarray(np.asarray(ids.cpu() if isinstance(ids, torch.Tensor) else ids,
+                                                dtype=np.uint32))
+        n = h_ids.size
+        if out is None:
+            out = torch.empty((n, self.sample_size), dtype=torch.uint8, device=_dev())
+        _check(lib().lsg_store_read_rows(self._h, h_ids.ctypes.data_as(ctypes.c_void_p), n, threshold,
+                                         _ptr(out), _stream()))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().lsg_store_close(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class StepFetcher:
     """The per-step loading phase for a contiguous range of ranks (lsg_fetch_step):
     owns the device arrays of buffer / batch pointers so one call fetches every
     local rank's batch of a step."""
 
     def __init__(self, bufs: list, outs: list, node_range: tuple[int, int], sample_bytes: int,
-                 fill_seed: int):
+                 fill_seed: int, store: "Store | None" = None, threshold: int = 15):
         dev = bufs[0].device
         self.k0, self.k1 = node_range
         self.bufs, self.outs = bufs, outs
         self.pb = torch.tensor([t.data_ptr() for t in bufs], dtype=torch.int64, device=dev)
         self.po = torch.tensor([t.data_ptr() for t in outs], dtype=torch.int64, device=dev)
+        self.hb = (ctypes.c_void_p * len(bufs))(*[t.data_ptr() for t in bufs])
+        self.ho = (ctypes.c_void_p * len(outs))(*[t.data_ptr() for t in outs])
         self.sample_bytes, self.fill_seed = sample_bytes, fill_seed
+        self.store, self.threshold = store, threshold
+        if store is not None and store.sample_size != sample_bytes:
+            raise ValidationError(3, "StepFetcher: store sample size differs from sample_bytes")
 
     def __call__(self, items: torch.Tensor, slots: torch.Tensor, node_off_row: torch.Tensor,
                  rows_hint: int = 0) -> None:
+        if self.store is not None:  # misses read from the Store file
+            _check(lib().lsg_fetch_step_store(self.store._h, _ptr(self.pb), _ptr(self.po), self.hb, self.ho,
+                                              _ptr(items), _ptr(slots), _ptr(node_off_row), self.k0, self.k1,
+                                              rows_hint, self.threshold, _stream()))
+            return
         _check(lib().lsg_fetch_step(_ptr(self.pb), _ptr(self.po), _ptr(items), _ptr(slots),
                                     _ptr(node_off_row), self.k0, self.k1, rows_hint,
                                     self.sample_bytes, self.fill_seed, _stream()))
