@@ -7,11 +7,12 @@
 // API for the planner path (cited per declaration); results are bit-identical.
 // Everything is computed on the current CUDA device; inputs are uploaded and
 // outputs returned by value as the reference does. Both buffer policies
-// (Clairvoyant, Lru) run on device. Out of this header (and out of scope, see
-// DESIGN.md §8): text formats, Store files, the cost model,
-// chunk_insert_redundant.
+// (Clairvoyant, Lru) run on device; Store files are read and written in the
+// reference's format. Out of this header (and out of scope, see DESIGN.md
+// §8): text formats, the cost model, chunk_insert_redundant.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <optional>
 #include <stdexcept>
@@ -207,6 +208,45 @@ struct PlanOutput {
 };
 
 PlanOutput plan_schedule(const PipelineConfig& config);
+
+// ---- store.hpp:13-50 --------------------------------------------------------
+// SLRD sample files; create_store computes the splitmix64 payload on the GPU
+// and writes a file byte-identical to the reference's. Store::read_one /
+// read_chunk return host bytes like the reference; read_rows_device() moves
+// a set of samples straight into HBM (chunked parallel reads).
+struct StoreHeader {
+    std::uint16_t version = 1;
+    std::uint64_t sample_count = 0;
+    std::uint64_t sample_size = 0;
+};
+
+inline constexpr std::size_t kStoreHeaderBytes = 4 + 2 + 8 + 8;
+inline constexpr std::uint64_t kDefaultStoreBudget = 1ULL << 30;  // 1 GiB
+
+void create_store(const std::string& path, std::uint64_t sample_count, std::uint64_t sample_size,
+                  std::uint64_t fill_seed, std::uint64_t max_bytes = kDefaultStoreBudget);
+
+class Store {
+  public:
+    explicit Store(const std::string& path);
+    ~Store();
+    Store(const Store&) = delete;
+    Store& operator=(const Store&) = delete;
+
+    const StoreHeader& header() const { return header_; }
+    std::uint64_t sample_count() const { return header_.sample_count; }
+    std::uint64_t sample_size() const { return header_.sample_size; }
+
+    std::vector<std::byte> read_one(std::uint64_t index) const;
+    std::vector<std::byte> read_chunk(std::uint64_t start, std::uint64_t count) const;
+    // B200 extension: samples ids into device rows (pitch = sample size)
+    void read_rows_device(const std::vector<SampleId>& ids, void* d_rows, std::uint64_t threshold = 15,
+                          void* stream = nullptr) const;
+
+  private:
+    void* h_ = nullptr;  // lsg_store*
+    StoreHeader header_;
+};
 
 // pipeline.cpp:122-131: the comparison pass of run_pipeline (LRU buffers,
 // identity order, slicing, no balance, no chunking).

@@ -244,6 +244,39 @@ bool same_multiset(const StepAssignment& step, const std::vector<SampleId>& batc
     return got == want;
 }
 
+void create_store(const std::string& path, std::uint64_t sample_count, std::uint64_t sample_size,
+                  std::uint64_t fill_seed, std::uint64_t max_bytes) {
+    check(lsg_store_create(path.c_str(), sample_count, sample_size, fill_seed, max_bytes, nullptr));
+}
+
+Store::Store(const std::string& path) {
+    lsg_store* h = nullptr;
+    check(lsg_store_open(path.c_str(), &h));
+    h_ = h;
+    check(lsg_store_info(h, &header_.sample_count, &header_.sample_size));
+}
+
+Store::~Store() { lsg_store_close(static_cast<lsg_store*>(h_)); }
+
+std::vector<std::byte> Store::read_chunk(std::uint64_t start, std::uint64_t count) const {
+    std::vector<std::byte> out(std::max<std::uint64_t>(count, 1) * header_.sample_size);
+    check(lsg_store_read(static_cast<lsg_store*>(h_), start, count, out.data()));
+    out.resize(count * header_.sample_size);
+    return out;
+}
+
+std::vector<std::byte> Store::read_one(std::uint64_t index) const { return read_chunk(index, 1); }
+
+void Store::read_rows_device(const std::vector<SampleId>& ids, void* d_rows, std::uint64_t threshold,
+                             void* stream) const {
+    std::vector<std::uint32_t> v(ids.size());
+    for (std::size_t i = 0; i < ids.size(); ++i) {
+        if (ids[i] >= header_.sample_count) throw ValidationError("store: sample index out of range");
+        v[i] = std::uint32_t(ids[i]);
+    }
+    check(lsg_store_read_rows(static_cast<lsg_store*>(h_), v.data(), v.size(), threshold, d_rows, stream));
+}
+
 PipelineConfig baseline_config(const PipelineConfig& config) {
     PipelineConfig base = config;
     base.policy = Policy::Lru;

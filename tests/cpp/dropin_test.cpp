@@ -82,6 +82,30 @@ static int run_checks() {
     w.buffer_capacity = 64;
     SimResult ws = simulate_plan(plan_schedule(w).plan, 64, Policy::Clairvoyant);
     EXPECT(ws.total_misses == 64 && ws.total_hits == 3 * 64 - 64);
+    // the Store (tests/test_store.cpp:63-65 golden; :73-91 chunk == singles)
+    {
+        const std::string sp = "/tmp/lsg_dropin_store.bin";
+        create_store(sp, 8, 16, 1);
+        Store st(sp);
+        EXPECT(st.sample_count() == 8 && st.sample_size() == 16 && st.header().version == 1);
+        auto a = st.read_one(0), b2 = st.read_one(1);
+        static const unsigned char gold[32] = {0xc1, 0x5c, 0x02, 0x89, 0xec, 0x2d, 0x0a, 0x91, 0x67, 0xec, 0x8e,
+                                               0x65, 0xa1, 0x8d, 0xeb, 0xbe, 0x5e, 0x55, 0x32, 0xfb, 0xee, 0xa2,
+                                               0x93, 0xf8, 0x0b, 0xc9, 0x42, 0xee, 0x90, 0x86, 0xc1, 0x71};
+        EXPECT(std::memcmp(a.data(), gold, 16) == 0 && std::memcmp(b2.data(), gold + 16, 16) == 0);
+        auto ch = st.read_chunk(2, 5);
+        bool same = true;
+        for (std::uint64_t i = 0; i < 5; ++i) {
+            auto one = st.read_one(2 + i);
+            same = same && std::memcmp(ch.data() + i * 16, one.data(), 16) == 0;
+        }
+        EXPECT(same);
+        EXPECT(throws<ValidationError>([&] { st.read_one(8); }));
+        EXPECT(throws<ValidationError>([&] { st.read_chunk(0, 0); }));
+        EXPECT(throws<StorageError>([&] { Store bad("/nonexistent/lsg.bin"); }));
+        EXPECT(throws<StorageError>([&] { create_store(sp, 0, 4, 1); }));
+        std::remove(sp.c_str());
+    }
     // capability guards are typed, never a silent CPU path
     PipelineConfig red = demo();
     red.chunk_insert_redundant = true;

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     hdr = open(os.path.join(ROOT, "include", "lsg.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|uint64_t)\s+(lsg_\w+)\(", hdr, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*|uint64_t)\s+(lsg_\w+)\(", hdr, re.M)))
 
 
 def test_header_declares_the_boundary():
