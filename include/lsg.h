@@ -130,6 +130,17 @@ int lsg_simulate(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T
                  uint32_t node_end, uint32_t* d_hits, uint32_t* d_misses, uint32_t* d_slot,
                  void* stream);
 
+/* Same with simulate_plan's insert_redundant (buffer.cpp:224-238): after each
+ * (step, node) list, the ids its chunk reads stream without requesting them
+ * (redundant_ids, chunking.cpp:35-45) are inserted silently with their next
+ * position on the node. d_read_*: the plan's reads at its item offsets
+ * (lsg_plan_out.read_start / read_end / read_count). Clairvoyant policy;
+ * d_slot must be NULL when insert_redundant is set. */
+int lsg_simulate_ex(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N, uint64_t D,
+                    uint64_t capacity, int32_t policy, int32_t insert_redundant, const uint32_t* d_read_start,
+                    const uint32_t* d_read_end, const uint32_t* d_read_count, uint32_t node_begin,
+                    uint32_t node_end, uint32_t* d_hits, uint32_t* d_misses, uint32_t* d_slot, void* stream);
+
 /* ---- K9: Store payload (store.cpp:70-80) of samples ids[0..n) written to
  *      dst rows: row r of `dst` (row pitch sample_bytes) receives the bytes
  *      Store::read_one(ids[r]) would return for fill_seed. */

@@ -185,6 +185,7 @@ def lib() -> ctypes.CDLL:
         L.or_balance_step.argtypes = [P, P, u32, P]
         L.or_plan.argtypes = [ctypes.POINTER(OrConfig), P, P, P, P, P, P, P, P, P, P, P]
         L.or_simulate.argtypes = [P, P, u64, u32, u64, u64, i32, P, P]
+        L.or_simulate_ex.argtypes = [P, P, u64, u32, u64, u64, i32, P, P, P, P, P]
         L.or_simulate_sequence.argtypes = [P, u64, u64, u64, i32, P]
         L.or_plan_reads.argtypes = [P, P, u64, u32, i32, u64, P, P, P, P, P]
         L.or_store_payload.argtypes = [u64, u64, u64, P]
@@ -300,6 +301,22 @@ def simulate(items, node_off, N, D, C, policy="clairvoyant"):
     misses = np.zeros((T, N), dtype=np.uint32)
     _check(lib().or_simulate(_p(items), _p(node_off), T, N, D, C,
                              0 if policy == "clairvoyant" else 1, _p(hits), _p(misses)), "simulate")
+    return hits, misses
+
+
+def simulate_redundant(items, node_off, N, D, C, rstart, rend, rcount, policy="clairvoyant"):
+    """simulate_plan(..., insert_redundant=true) (buffer.cpp:224-238); the
+    reads of list (g, k) sit at its item offsets (plan_reads layout)."""
+    items = np.ascontiguousarray(items, dtype=np.uint32)
+    node_off = np.ascontiguousarray(node_off, dtype=np.uint32).reshape(-1, N + 1)
+    rstart = np.ascontiguousarray(rstart, dtype=np.uint32)
+    rend = np.ascontiguousarray(rend, dtype=np.uint32)
+    rcount = np.ascontiguousarray(rcount, dtype=np.uint32)
+    T = node_off.shape[0]
+    hits = np.zeros((T, N), dtype=np.uint32)
+    misses = np.zeros((T, N), dtype=np.uint32)
+    _check(lib().or_simulate_ex(_p(items), _p(node_off), T, N, D, C, 0 if policy == "clairvoyant" else 1,
+                                _p(rstart), _p(rend), _p(rcount), _p(hits), _p(misses)), "simulate")
     return hits, misses
 
 

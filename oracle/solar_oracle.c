@@ -702,6 +702,22 @@ int or_plan(const or_config* c, uint32_t* trace, uint64_t* graph, uint32_t* orde
  * (buffer.cpp:103-112) on each node's flattened sequence. */
 int or_simulate(const uint32_t* items, const uint32_t* node_off, uint64_t T, uint32_t N,
                 uint64_t D, uint64_t C, int policy, uint32_t* hits, uint32_t* misses) {
+    return or_simulate_ex(items, node_off, T, N, D, C, policy, NULL, NULL, NULL, hits, misses);
+}
+
+/* buffer.cpp:183-247 with insert_redundant (:224-238) when rstart != NULL:
+ * after list (g, k), redundant_ids(reads, fetch_ids) (chunking.cpp:35-45;
+ * a read with start < end is a Chunk, start == end a Single) are inserted
+ * silently with next = the first position of the id on node k at or after
+ * the node's cursor (std::lower_bound over its positions). Reads of list
+ * (g, k) sit at the list's item offsets, rcount[g*N+k] of them. */
+static int cmp_u32r(const void* a, const void* b) {
+    uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+    return x < y ? -1 : x > y;
+}
+int or_simulate_ex(const uint32_t* items, const uint32_t* node_off, uint64_t T, uint32_t N,
+                   uint64_t D, uint64_t C, int policy, const uint32_t* rstart, const uint32_t* rend,
+                   const uint32_t* rcount, uint32_t* hits, uint32_t* misses) {
     if (C == 0) return 3;
     uint64_t* len = (uint64_t*)calloc(N, sizeof(uint64_t));
     uint64_t base = 0;
@@ -731,9 +747,28 @@ int or_simulate(const uint32_t* items, const uint32_t* node_off, uint64_t T, uin
             last[x] = i - 1;
         }
     }
+    /* positions of every id on every node (CSR by id), for the silent inserts */
+    uint64_t** pstart = NULL;
+    uint64_t** plist = NULL;
+    if (rstart) {
+        pstart = (uint64_t**)malloc(N * sizeof(uint64_t*));
+        plist = (uint64_t**)malloc(N * sizeof(uint64_t*));
+        for (uint32_t k = 0; k < N; ++k) {
+            pstart[k] = (uint64_t*)calloc(D + 1, sizeof(uint64_t));
+            plist[k] = (uint64_t*)malloc((len[k] + 1) * sizeof(uint64_t));
+            for (uint64_t i = 0; i < len[k]; ++i) pstart[k][seq[k][i] + 1]++;
+            for (uint64_t x = 0; x < D; ++x) pstart[k][x + 1] += pstart[k][x];
+            uint64_t* f2 = (uint64_t*)calloc(D + 1, sizeof(uint64_t));
+            for (uint64_t i = 0; i < len[k]; ++i) { uint32_t x = seq[k][i]; plist[k][pstart[k][x] + f2[x]++] = i; }
+            free(f2);
+        }
+    }
+    uint32_t* fetch = (uint32_t*)malloc(sizeof(uint32_t));
+    uint64_t fcap = 1;
     int rc = 0;
     obuf* bufs = (obuf*)malloc(N * sizeof(obuf));
     for (uint32_t k = 0; k < N; ++k) { buf_init(&bufs[k], policy, C, D); fillp[k] = 0; }
+    uint64_t gbase = 0;
     for (uint64_t g = 0; g < T && !rc; ++g) {
         const uint32_t* off = node_off + g * (N + 1);
         for (uint32_t k = 0; k < N; ++k) {
@@ -746,9 +781,38 @@ int or_simulate(const uint32_t* items, const uint32_t* node_off, uint64_t T, uin
             }
             hits[g * N + k] = h;
             misses[g * N + k] = m;
+            if (rstart && !rc) {
+                const uint64_t lo = gbase + off[k], L = off[k + 1] - off[k];
+                if (L > fcap) { fcap = L; fetch = (uint32_t*)realloc(fetch, fcap * sizeof(uint32_t)); }
+                uint64_t nf = 0;
+                for (uint64_t i = 0; i < L; ++i)
+                    if (!(items[lo + i] & OR_HIT_BIT)) fetch[nf++] = items[lo + i];
+                qsort(fetch, nf, sizeof(uint32_t), cmp_u32r);
+                for (uint32_t r = 0; r < rcount[g * N + k]; ++r) {
+                    const uint32_t st = rstart[lo + r], en = rend[lo + r];
+                    if (st >= en) continue;
+                    for (uint64_t id = st; id <= en; ++id) {
+                        uint32_t key = (uint32_t)id;
+                        if (bsearch(&key, fetch, nf, sizeof(uint32_t), cmp_u32r)) continue;
+                        /* std::lower_bound(positions, cursor) */
+                        uint64_t nx = OR_NEVER;
+                        const uint64_t* pl = plist[k] + pstart[k][id];
+                        uint64_t a0 = 0, a1 = pstart[k][id + 1] - pstart[k][id];
+                        while (a0 < a1) { uint64_t mid = (a0 + a1) / 2; if (pl[mid] < fillp[k]) a0 = mid + 1; else a1 = mid; }
+                        if (a0 < pstart[k][id + 1] - pstart[k][id]) nx = pl[a0];
+                        if (buf_insert_silent(&bufs[k], key, nx)) { rc = 7; break; }
+                    }
+                    if (rc) break;
+                }
+            }
         }
+        gbase += off[N];
     }
-    for (uint32_t k = 0; k < N; ++k) { buf_free(&bufs[k]); free(seq[k]); free(nxt[k]); }
+    for (uint32_t k = 0; k < N; ++k) {
+        buf_free(&bufs[k]); free(seq[k]); free(nxt[k]);
+        if (pstart) { free(pstart[k]); free(plist[k]); }
+    }
+    free(pstart); free(plist); free(fetch);
     free(bufs); free(seq); free(nxt); free(len); free(fillp); free(last);
     return rc;
 }

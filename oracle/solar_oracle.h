@@ -84,6 +84,9 @@ int or_plan(const or_config* cfg, uint32_t* trace, uint64_t* graph, uint32_t* or
 
 /* buffer.cpp:183-247 (insert_redundant = false). Steps in execution order;
  * hits/misses[T*N]. */
+int or_simulate_ex(const uint32_t* items, const uint32_t* node_off, uint64_t T, uint32_t N,
+                   uint64_t D, uint64_t C, int policy, const uint32_t* rstart, const uint32_t* rend,
+                   const uint32_t* rcount, uint32_t* hits, uint32_t* misses);
 int or_simulate(const uint32_t* items, const uint32_t* node_off, uint64_t T, uint32_t N,
                 uint64_t D, uint64_t C, int policy, uint32_t* hits, uint32_t* misses);
 

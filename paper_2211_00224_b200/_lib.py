@@ -71,7 +71,7 @@ EXPORTS = [
     "lsg_build_reuse_graph", "lsg_pso_order", "lsg_plan", "lsg_plan_host", "lsg_simulate",
     "lsg_store_fill", "lsg_gather", "lsg_batch_fetch", "lsg_fetch_step", "lsg_launch_count",
     "lsg_store_create", "lsg_store_open", "lsg_store_info", "lsg_store_close", "lsg_store_read",
-    "lsg_store_read_rows", "lsg_fetch_step_store",
+    "lsg_store_read_rows", "lsg_fetch_step_store", "lsg_simulate_ex",
 ]
 
 
@@ -107,6 +107,7 @@ def lib() -> ctypes.CDLL:
         L.lsg_plan.argtypes = [ctypes.POINTER(LsgConfig), ctypes.POINTER(LsgPlanOut), P]
         L.lsg_plan_host.argtypes = [ctypes.POINTER(LsgConfig), ctypes.POINTER(LsgPlanOut), P]
         L.lsg_simulate.argtypes = [P, P, u64, u32, u64, u64, i32, u32, u32, P, P, P, P]
+        L.lsg_simulate_ex.argtypes = [P, P, u64, u32, u64, u64, i32, i32, P, P, P, u32, u32, P, P, P, P]
         L.lsg_store_fill.argtypes = [P, u64, u64, u64, P, P]
         L.lsg_gather.argtypes = [P, P, u64, u64, P, P]
         L.lsg_batch_fetch.argtypes = [P, P, P, u64, u64, u64, P, P]

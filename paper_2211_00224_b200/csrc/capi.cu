@@ -21,13 +21,15 @@ int pso_order_device(const uint64_t* d_w, uint32_t E, uint32_t swarm, uint32_t i
                      double pg, double inertia, double kick, uint32_t stagnation, uint32_t restart,
                      uint64_t seed, uint32_t* d_order, uint64_t* d_cost, uint64_t* d_hist,
                      uint32_t* d_iters, uint32_t* d_status, cudaStream_t st);
-int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int balance, const uint32_t* d_trace,
+int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int balance, int insred, uint64_t thr,
+                     const uint32_t* d_trace,
                      const uint32_t* d_order, const uint32_t* d_inv, uint32_t* d_items,
                      uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
                      cudaStream_t st);
 int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N,
                     uint64_t D, uint64_t C, int policy, uint32_t k0, uint32_t k1, uint32_t* d_hits,
-                    uint32_t* d_misses, uint32_t* d_slot, uint32_t* d_status, cudaStream_t st);
+                    uint32_t* d_misses, uint32_t* d_slot, const uint32_t* d_rstart, const uint32_t* d_rend,
+                    const uint32_t* d_rcount, int insred, uint32_t* d_status, cudaStream_t st);
 int plan_reads_device(const uint32_t* d_items, const uint32_t* d_node_off, uint32_t T, uint32_t N,
                       uint32_t S, uint32_t B, uint32_t keep, int chunked, uint64_t thr, uint32_t* rstart,
                       uint32_t* rend, uint32_t* rcount, uint32_t* needed, uint32_t* redundant,
@@ -184,8 +186,6 @@ int lsg_plan(const lsg_config* cfg, const lsg_plan_out* out, void* stream) {
     int rc = validate(cfg, &sh);
     if (rc) return rc;
     if (!out || !out->items || !out->node_off) return set_error(kValidation, "plan: items and node_off are required");
-    if (cfg->insert_redundant && cfg->optim_chunk)
-        return set_error(kCapability, "plan: chunk_insert_redundant is not on the device path yet");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const uint32_t E = cfg->num_epochs, N = cfg->num_nodes;
     const uint64_t D = cfg->dataset_size;
@@ -215,7 +215,8 @@ int lsg_plan(const lsg_config* cfg, const lsg_plan_out* out, void* stream) {
     }
     PlanDims dm{D, sh.global_batch, sh.steps_per_epoch, sh.keep, sh.total_steps, N, E,
                 uint32_t(cfg->local_batch)};
-    if ((rc = plan_loop_device(dm, cfg->buffer_capacity, cfg->policy, cfg->optim_remap, cfg->optim_balance, trace,
+    if ((rc = plan_loop_device(dm, cfg->buffer_capacity, cfg->policy, cfg->optim_remap, cfg->optim_balance,
+                               cfg->insert_redundant && cfg->optim_chunk, cfg->chunk_threshold, trace,
                                order, inv, out->items, out->node_off, out->fetch_before,
                                out->fetch_after, status, st)))
         return rc;
@@ -275,6 +276,14 @@ int lsg_plan_host(const lsg_config* cfg, const lsg_plan_out* h, void* stream) {
 int lsg_simulate(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N, uint64_t D,
                  uint64_t capacity, int32_t policy, uint32_t node_begin, uint32_t node_end,
                  uint32_t* d_hits, uint32_t* d_misses, uint32_t* d_slot, void* stream) {
+    return lsg_simulate_ex(d_items, d_node_off, T, N, D, capacity, policy, 0, nullptr, nullptr, nullptr,
+                           node_begin, node_end, d_hits, d_misses, d_slot, stream);
+}
+
+int lsg_simulate_ex(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N, uint64_t D,
+                    uint64_t capacity, int32_t policy, int32_t insert_redundant, const uint32_t* d_read_start,
+                    const uint32_t* d_read_end, const uint32_t* d_read_count, uint32_t node_begin,
+                    uint32_t node_end, uint32_t* d_hits, uint32_t* d_misses, uint32_t* d_slot, void* stream) {
     if (capacity == 0) return set_error(kValidation, "buffer capacity must be >= 1");
     if (policy != 0 && policy != 1) return set_error(kConfig, "simulate: policy must be clairvoyant (0) or lru (1)");
     if (N == 0) return set_error(kValidation, "simulate: num_nodes must be >= 1");
@@ -286,7 +295,8 @@ int lsg_simulate(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T
     if (!status) return set_error(kInternal, "simulate: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(status, 0, 4, st));
     int rc = simulate_device(d_items, d_node_off, T, N, D, capacity, policy, node_begin, node_end, d_hits,
-                             d_misses, d_slot, status, st);
+                             d_misses, d_slot, d_read_start, d_read_end, d_read_count, insert_redundant != 0,
+                             status, st);
     if (rc) return rc;
     uint32_t h = 0;
     LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));

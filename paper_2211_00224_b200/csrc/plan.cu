@@ -1017,11 +1017,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
 }  // namespace
 
 
-int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int balance, const uint32_t* d_trace,
-                     const uint32_t* d_order, const uint32_t* d_nu, uint32_t* d_items, uint32_t* d_node_off,
-                     uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status, cudaStream_t st);
+int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int balance, int insred, uint64_t thr,
+                     const uint32_t* d_trace, const uint32_t* d_order, const uint32_t* d_inv, const uint32_t* d_nu,
+                     uint32_t* d_items, uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
+                     cudaStream_t st);
 
-int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int balance, const uint32_t* d_trace,
+int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int balance, int insred, uint64_t thr,
+                     const uint32_t* d_trace,
                      const uint32_t* d_order, const uint32_t* d_inv, uint32_t* d_items,
                      uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
                      cudaStream_t st) {
@@ -1030,9 +1032,10 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
     // is faster there (cfg5 N=32: 292 vs 528 us/step); LSG_PLAN_WIDE=1 / 0
     // forces / forbids it (parity tests of both kernels on the same configs)
     const char* fw = std::getenv("LSG_PLAN_WIDE");
-    bool wide = dm.N > kMaxN || dm.B > kMaxSmemB || dm.T * dm.B >= 0xFFFFFFF0ull || policy == 1;
+    bool wide = dm.N > kMaxN || dm.B > kMaxSmemB || dm.T * dm.B >= 0xFFFFFFF0ull || policy == 1 || insred;
     if (fw && fw[0] == '1') wide = true;
-    if (fw && fw[0] == '0' && dm.N <= kMaxN && dm.B <= kMaxB && dm.T * dm.B < 0xFFFFFFF0ull && policy == 0)
+    if (fw && fw[0] == '0' && dm.N <= kMaxN && dm.B <= kMaxB && dm.T * dm.B < 0xFFFFFFF0ull && policy == 0 &&
+        !insred)
         wide = false;
     Scratch sc(st);
     const size_t EK = size_t(dm.E) * dm.keep;
@@ -1042,7 +1045,8 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
         k_nextuse<<<dim3(grid_for(dm.keep, 256, 1024), dm.E), 256, 0, st>>>(
             d_trace, d_order, d_inv, dm.E, uint32_t(dm.keep), uint32_t(dm.D), uint32_t(dm.S), uint32_t(dm.B), nu);
         LSG_LAUNCH_CHECK("k_nextuse");
-        return plan_wide_device(dm, C, policy == 1, remap, balance, d_trace, d_order, nu, d_items, d_node_off, d_fb, d_fa,
+        return plan_wide_device(dm, C, policy == 1, remap, balance, insred, thr, d_trace, d_order, d_inv, nu, d_items,
+                                d_node_off, d_fb, d_fa,
                                 d_status, st);
     }
     uint32_t* sb = sc.get<uint32_t>(EK);

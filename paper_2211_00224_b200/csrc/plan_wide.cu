@@ -61,6 +61,11 @@ struct WideArgs {
     uint32_t EBW;                     // eviction-flag words per node
     uint32_t MBW;                     // moved-flag words per node
     int remap, balance, lru;
+    int insred;                       // chunk_insert_redundant (pipeline.cpp:103-114)
+    uint32_t thr;                     // chunk threshold
+    uint32_t E;
+    const uint32_t* inv;              // [E][D] position of id in epoch e's trace, kNone if not kept
+    uint32_t* redbuf;                 // [N][B] sort scratch for lists longer than shared memory
     const uint32_t* trace;            // [E][keep]
     const uint32_t* order;            // [E]
     const uint32_t* nu;               // [E*keep] next-use step, execution order
@@ -644,6 +649,108 @@ __device__ __forceinline__ void multi_pass(const uint32_t* pairs, uint32_t* mpos
         __syncwarp();
         q0 += ncommit;
     }
+}
+
+// First scheduled step of id y after step g (the reference's occ[y][cursor]
+// once step g's accesses are walked), from the inverse permutations.
+__device__ __forceinline__ uint32_t next_step_after(const WideArgs& a, uint32_t y, uint32_t g) {
+    for (uint32_t j = g / a.S; j < a.E; ++j) {
+        const uint32_t p = __ldcg(&a.inv[size_t(a.order[j]) * a.D + y]);
+        if (p == kNone) continue;
+        const uint32_t st = j * a.S + p / a.B;
+        if (st > g) return st;
+    }
+    return kNever;
+}
+
+// pipeline.cpp:103-114 for node k after its step-g advance: the ids a chunk
+// read of its fetch list streams without being requested (redundant_ids,
+// chunking.cpp:35-45, ascending) are inserted silently (buffer.cpp:48-53:
+// resident ids are left alone) with their next scheduled step as key. Keep-C-
+// smallest is associative, so the inserts form one miss run; the run is
+// flushed early only when the slot array is about to overflow. Leader warp of
+// the team (the team joins the evictions).
+__device__ void redundant_inserts(const WideArgs& a, uint32_t k, uint32_t& bsz, uint32_t& top, uint32_t g,
+                                  uint32_t lane, const Team& tm, const uint32_t* list, uint32_t L,
+                                  uint32_t* sbuf /*[2*kSortCap] shared*/) {
+    const uint32_t lt = lanemask_lt_w();
+    // fetch ids of the list (items without the hit tag)
+    uint32_t nf = 0;
+    for (uint32_t c = 0; c < L; c += 32) {
+        const uint32_t it = c + lane < L ? __ldcg(&list[c + lane]) : kHit;
+        const bool f = !(it & kHit);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
+        nf += __popc(bal);
+    }
+    if (nf < 2) return;
+    uint32_t P2 = 1;
+    while (P2 < nf) P2 <<= 1;
+    uint32_t* v = P2 <= 2 * kSortCap ? sbuf : a.redbuf + size_t(k) * a.B;
+    nf = 0;
+    for (uint32_t c = 0; c < L; c += 32) {
+        const uint32_t it = c + lane < L ? __ldcg(&list[c + lane]) : kHit;
+        const bool f = !(it & kHit);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
+        if (f) v[nf + __popc(bal & lt)] = it;
+        nf += __popc(bal);
+    }
+    for (uint32_t q = nf + lane; q < P2; q += 32) v[q] = 0xFFFFFFFFu;
+    __syncwarp();
+    for (uint32_t sz = 2; sz <= P2; sz <<= 1)
+        for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+            for (uint32_t r = lane; r < P2 / 2; r += 32) {
+                const uint32_t x0 = 2 * st * (r / st) + (r % st), x1 = x0 + st;
+                const bool up = (x0 & sz) == 0;
+                const uint32_t p = v[x0], q = v[x1];
+                if ((p > q) == up) {
+                    v[x0] = q;
+                    v[x1] = p;
+                }
+            }
+            __syncwarp();
+        }
+    // greedy reads of span <= thr over the unique ids (chunking.cpp:17-30);
+    // the gaps inside every chunk read are the redundant ids
+    const uint32_t kw = k >> 5, kb = 1u << (k & 31);
+    uint32_t* cntk = a.cnt + size_t(k) * (a.T + 1);
+    unsigned long long* sk = a.slot + size_t(k) * a.SC;
+    uint32_t i = 0;
+    while (i < nf) {
+        const uint32_t start = v[i];
+        uint32_t j = i + 1, prev = start;
+        // walk the read; between consecutive unique ids the gap ids go in
+        while (j < nf && v[j] - start + 1 <= a.thr) {
+            const uint32_t cur = v[j];
+            if (cur != prev) {
+                for (uint32_t y0 = prev + 1; y0 < cur; y0 += 32) {
+                    // room for a full batch (SC >= C + 64)
+                    if (bsz + 32 > a.SC && bsz > a.C) wide_evict(a, k, bsz, top, g, lane, tm);
+                    const uint32_t y = y0 + lane;
+                    bool ins = false;
+                    uint32_t key = 0;
+                    if (y < cur && __ldcg(&a.where[size_t(k) * a.D + y]) == kNone) {
+                        ins = true;
+                        key = next_step_after(a, y, g);
+                    }
+                    const uint32_t ib = __ballot_sync(0xFFFFFFFFu, ins);
+                    if (ins) {
+                        const uint32_t s2 = bsz + __popc(ib & lt);
+                        a.where[size_t(k) * a.D + y] = s2;
+                        sk[s2] = (static_cast<unsigned long long>(key) << 32) | y;
+                        atomicAdd(&cntk[bin_of(key, a.T)], 1u);
+                        atomicOr(&a.hm[size_t(y) * a.W + kw], kb);
+                    }
+                    top = max(top, __reduce_max_sync(0xFFFFFFFFu, ins && key != kNever ? key : 0u));
+                    bsz += __popc(ib);
+                    __syncwarp();
+                }
+                prev = cur;
+            }
+            ++j;
+        }
+        i = j;
+    }
+    if (bsz > a.C) wide_evict(a, k, bsz, top, g, lane, tm);
 }
 
 __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
@@ -1269,6 +1376,9 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
                 }
             }
             if (pending && bsz > a.C) wide_evict(a, k, bsz, top, g, lane, tm);
+            if (a.insred)
+                redundant_inserts(a, k, bsz, top, g, lane, tm, a.items + gbase + lb, le - lb,
+                                  reinterpret_cast<uint32_t*>(my_sort));
             if (lane == 0) {
                 a.nst[k * 8 + 0] = bsz;
                 a.nst[k * 8 + 1] = top;
@@ -1289,9 +1399,12 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
 
 }  // namespace
 
-int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int balance, const uint32_t* d_trace,
-                     const uint32_t* d_order, const uint32_t* d_nu, uint32_t* d_items, uint32_t* d_node_off,
-                     uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status, cudaStream_t st) {
+int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int balance, int insred, uint64_t thr,
+                     const uint32_t* d_trace, const uint32_t* d_order, const uint32_t* d_inv, const uint32_t* d_nu,
+                     uint32_t* d_items, uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
+                     cudaStream_t st) {
+    if (insred && lru)
+        return set_error(kCapability, "plan: chunk_insert_redundant with the LRU policy is not on the device path");
     if (dm.N > kWMaxN)
         return set_error(kCapability, "plan: device planner supports num_nodes <= 256 in this build");
     if (dm.b >= (1u << 21)) return set_error(kCapability, "plan: local_batch must be < 2^21 on device");
@@ -1299,7 +1412,7 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int bal
         return set_error(kCapability, "plan: global batch / steps too large for the device planner");
     const uint32_t N = dm.N, W = (N + 31) / 32;
     const uint64_t Ceff = std::min<uint64_t>(C, dm.D);
-    const uint64_t SC = Ceff + dm.B;
+    const uint64_t SC = Ceff + std::max<uint64_t>(dm.B, 64);  // a miss run, or a batch of silent inserts
     if (SC >= (1ull << 31)) return set_error(kCapability, "plan: buffer capacity too large for the device planner");
     Scratch sc(st);
     WideArgs a{};
@@ -1318,6 +1431,12 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int bal
     a.remap = remap;
     a.balance = balance;
     a.lru = lru;
+    a.insred = insred;
+    a.thr = uint32_t(std::min<uint64_t>(thr, 0xFFFFFFFFull));
+    a.E = dm.E;
+    a.inv = d_inv;
+    a.redbuf = insred ? sc.get<uint32_t>(size_t(N) * dm.B) : nullptr;
+    if (insred && !a.redbuf) return set_error(kInternal, "plan: wide planner scratch allocation failed");
     a.trace = d_trace;
     a.order = d_order;
     a.nu = d_nu;

@@ -25,6 +25,7 @@
 //     a stale bit in its current step, which is never reached). kNeverUsed
 //     residents sit in an id bitmap scanned from the top (ties by larger id,
 //     buffer.cpp:27-28).
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -473,6 +474,12 @@ struct ReplayArgsCta {
     uint32_t* misses;  // [T][N]
     uint32_t* slot_out;  // [total items] or null
     uint32_t* status;
+    // simulate_plan(..., insert_redundant = true) (buffer.cpp:224-238): the
+    // redundant ids of list (g, k) are red_ids[red_off[g*N+k] .. +1], their
+    // next position on the node red_key (filled by the backward pass)
+    const uint64_t* red_off;  // [T*N+1] or null
+    const uint32_t* red_ids;
+    uint32_t* red_key;
 };
 
 // backward pass: next-use key (g'*B + i') of every access on this node
@@ -489,6 +496,14 @@ __global__ void __launch_bounds__(kRT) k_replay_nextuse_cta(ReplayArgsCta a) {
             a.nuk[base + i] = v == kNone ? kNever : v;
         }
         __syncthreads();
+        if (a.red_off) {  // silent inserts after step g: next position after the step
+            const uint64_t q0 = a.red_off[size_t(g) * a.N + k], q1 = a.red_off[size_t(g) * a.N + k + 1];
+            for (uint64_t q = q0 + threadIdx.x; q < q1; q += kRT) {
+                const uint32_t v = __ldcg(&last[a.red_ids[q]]);
+                a.red_key[q] = v == kNone ? kNever : v;
+            }
+            __syncthreads();
+        }
         const uint32_t here = uint32_t(g) * a.B;
         for (uint32_t i = threadIdx.x; i < L; i += kRT) {
             const uint32_t x = a.items[base + i] & ~kHit;
@@ -740,6 +755,27 @@ __global__ void __launch_bounds__(kRT) k_replay_cta(ReplayArgsCta a) {
                 __syncthreads();
             }
         }
+        // insert_silent of the step's redundant ids (buffer.cpp:48-53): the
+        // non-resident ones form one more miss run (keep-C-smallest is
+        // associative); slots are not tracked on this path
+        if (a.red_off) {
+            const uint64_t q0 = a.red_off[size_t(g) * a.N + k], q1 = a.red_off[size_t(g) * a.N + k + 1];
+            uint32_t ins = 0;
+            for (uint64_t q = q0 + tid; q < q1; q += kRT) {
+                const uint32_t y = a.red_ids[q];
+                if (__ldcg(&keyk[y]) != kNone) continue;
+                r_set_key_cta(a, sh, k, y, a.red_key[q]);
+                ++ins;
+            }
+            for (int d = 16; d > 0; d >>= 1) ins += __shfl_xor_sync(0xFFFFFFFFu, ins, d);
+            if (lane == 0) atomicAdd(&sh.size, ins);
+            __syncthreads();
+            if (w == 0) {
+                const uint32_t need = sh.size > a.C ? sh.size - a.C : 0u;
+                if (need) r_evict_cta(a, sh, k, need, lane);
+            }
+            __syncthreads();
+        }
         // misses report the slot they hold at the END of the step: one that
         // a later run of the same step evicted again is a bypass (its slot may
         // already belong to another miss of this step)
@@ -752,6 +788,124 @@ __global__ void __launch_bounds__(kRT) k_replay_cta(ReplayArgsCta a) {
             }
         __syncthreads();
     }
+}
+
+// ---- redundant_ids (chunking.cpp:35-45) of every (step, node) list of a
+// plan with reads: the ids inside its chunk reads (start < end) that are not
+// among the list's fetch ids, unique and ascending. One warp per list; pass 0
+// counts, pass 1 writes at red_off.
+struct RedArgs {
+    const uint32_t* items;
+    const uint32_t* node_off;
+    const uint64_t* gb;
+    const uint32_t* rstart;
+    const uint32_t* rend;
+    const uint32_t* rcount;
+    uint32_t T, N, P2;
+    uint64_t* red_cnt;        // pass 0: [T*N]
+    const uint64_t* red_off;  // pass 1: [T*N+1]
+    uint32_t* red_ids;        // pass 1
+    uint32_t* status;
+};
+
+__global__ void k_redundant_ids(RedArgs a, int pass) {
+    extern __shared__ uint32_t rbuf[];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    uint32_t* buf = rbuf + size_t(wib) * a.P2;
+    const uint32_t lt = lanemask_lt_r();
+    for (uint64_t list = uint64_t(blockIdx.x) * wpb + wib; list < uint64_t(a.T) * a.N;
+         list += uint64_t(gridDim.x) * wpb) {
+        const uint32_t g = uint32_t(list / a.N), k = uint32_t(list % a.N);
+        const uint32_t* off = a.node_off + size_t(g) * (a.N + 1);
+        const uint64_t lo = a.gb[g] + off[k];
+        const uint32_t L = off[k + 1] - off[k], R = a.rcount[list];
+        uint32_t F = 0;
+        for (uint32_t c = 0; c < L; c += 32) {
+            const uint32_t v = c + lane < L ? a.items[lo + c + lane] : kHit;
+            const bool f = !(v & kHit);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
+            if (f) buf[F + __popc(bal & lt)] = v;
+            F += __popc(bal);
+        }
+        uint32_t P = 1;
+        while (P < F) P <<= 1;
+        for (uint32_t i = F + lane; i < P; i += 32) buf[i] = 0xFFFFFFFFu;
+        __syncwarp();
+        for (uint32_t size = 2; size <= P; size <<= 1)
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t r = lane; r < P / 2; r += 32) {
+                    const uint32_t x0 = 2 * stride * (r / stride) + (r % stride), x1 = x0 + stride;
+                    const bool up = (x0 & size) == 0;
+                    const uint32_t p = buf[x0], q = buf[x1];
+                    if ((p > q) == up) { buf[x0] = q; buf[x1] = p; }
+                }
+                __syncwarp();
+            }
+        // reads in file order may overlap in a foreign plan: ids are emitted
+        // once, from the first read that covers them
+        uint64_t n = 0;
+        const uint64_t wbase = pass ? a.red_off[list] : 0;
+        for (uint32_t r = 0; r < R; ++r) {
+            const uint32_t st = a.rstart[lo + r], en = a.rend[lo + r];
+            if (st >= en) continue;  // a Single read streams nothing extra
+            for (uint64_t y0 = st; y0 <= en; y0 += 32) {
+                const uint64_t y = y0 + lane;
+                bool red = false;
+                if (y <= en) {
+                    uint32_t l0 = 0, l1 = F;  // fetch ids: binary search
+                    while (l0 < l1) {
+                        const uint32_t mid = (l0 + l1) >> 1;
+                        if (buf[mid] < y) l0 = mid + 1; else l1 = mid;
+                    }
+                    red = !(l0 < F && buf[l0] == y);
+                    for (uint32_t r2 = 0; r2 < r && red; ++r2) {
+                        const uint32_t s2 = a.rstart[lo + r2], e2 = a.rend[lo + r2];
+                        if (s2 < e2 && y >= s2 && y <= e2) red = false;
+                    }
+                }
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, red);
+                if (pass && red) a.red_ids[wbase + n + __popc(bal & lt)] = uint32_t(y);
+                n += __popc(bal);
+            }
+        }
+        if (!pass && lane == 0) a.red_cnt[list] = n;
+        __syncwarp();
+    }
+}
+
+__global__ void k_scan_u64(const uint64_t* __restrict__ in, uint64_t n, uint64_t* __restrict__ out) {
+    // single block exclusive scan (n = T*N lists), out[n] = total
+    __shared__ uint64_t part[32];
+    __shared__ uint64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint64_t c = 0; c < n; c += 1024) {
+        const uint64_t i = c + threadIdx.x;
+        const uint64_t v = i < n ? in[i] : 0;
+        uint64_t inc = v;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= uint32_t(d)) inc += o;
+        }
+        if (lane == 31) part[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const uint64_t p = part[lane];
+            uint64_t pi = p;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint64_t o = __shfl_up_sync(0xFFFFFFFFu, pi, d);
+                if (lane >= uint32_t(d)) pi += o;
+            }
+            part[lane] = pi - p;
+        }
+        __syncthreads();
+        if (i < n) out[i] = carry + part[w] + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += part[w] + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[n] = carry;
 }
 
 // ---- LRU replay (simulate_plan with Policy::Lru, buffer.cpp:61-82): one
@@ -829,8 +983,15 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay_lru(LruReplayArgs a) {
 
 int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N,
                     uint64_t D, uint64_t C, int policy, uint32_t k0, uint32_t k1, uint32_t* d_hits,
-                    uint32_t* d_misses, uint32_t* d_slot, uint32_t* d_status, cudaStream_t st) {
+                    uint32_t* d_misses, uint32_t* d_slot, const uint32_t* d_rstart, const uint32_t* d_rend,
+                    const uint32_t* d_rcount, int insred, uint32_t* d_status, cudaStream_t st) {
     if (k1 <= k0 || T == 0) return kOk;
+    if (insred && policy != 0)
+        return set_error(kCapability, "simulate: insert_redundant with the LRU policy is not on the device path");
+    if (insred && d_slot)
+        return set_error(kCapability, "simulate: HBM slots are not tracked with insert_redundant");
+    if (insred && (!d_rstart || !d_rend || !d_rcount))
+        return set_error(kValidation, "simulate: insert_redundant needs the plan's reads");
     Scratch sc(st);
     uint64_t* gb = sc.get<uint64_t>(T + 1);
     if (!gb) return set_error(kInternal, "simulate: scratch allocation failed");
@@ -919,8 +1080,37 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     a.slot_out = d_slot;
     a.status = d_status;
     const uint32_t nk = k1 - k0;
-    if (L > 128) {  // long lists: a CTA per node
+    const char* fc = std::getenv("LSG_REPLAY_CTA");  // tests: force the CTA variant
+    if (L > 128 || insred || (fc && fc[0] == '1')) {  // long lists (and silent inserts): a CTA per node
         ReplayArgsCta c{};
+        if (insred) {  // redundant ids per list (CSR) for the silent inserts
+            uint64_t* cnt = sc.get<uint64_t>(T * N);
+            uint64_t* roff = sc.get<uint64_t>(T * N + 1);
+            if (!cnt || !roff) return set_error(kInternal, "simulate: scratch allocation failed");
+            RedArgs r{d_items, d_node_off, gb, d_rstart, d_rend, d_rcount, uint32_t(T), N, 1, cnt, roff, nullptr,
+                      d_status};
+            while (r.P2 < L) r.P2 <<= 1;
+            const uint32_t wpb = std::max<uint32_t>(1, std::min<uint32_t>(8, (96u * 1024) / (4 * r.P2)));
+            const size_t rs = size_t(wpb) * r.P2 * 4;
+            LSG_CUDA(cudaFuncSetAttribute(k_redundant_ids, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rs)));
+            const unsigned rg = unsigned(std::min<uint64_t>((T * N + wpb - 1) / wpb, 148ull * 8));
+            k_redundant_ids<<<rg, wpb * 32, rs, st>>>(r, 0);
+            LSG_LAUNCH_CHECK("k_redundant_ids");
+            k_scan_u64<<<1, 1024, 0, st>>>(cnt, T * N, roff);
+            LSG_LAUNCH_CHECK("k_scan_u64");
+            uint64_t nred = 0;
+            LSG_CUDA(cudaMemcpyAsync(&nred, roff + T * N, 8, cudaMemcpyDeviceToHost, st));
+            LSG_CUDA(cudaStreamSynchronize(st));
+            uint32_t* ids = sc.get<uint32_t>(nred);
+            uint32_t* keys = sc.get<uint32_t>(nred);
+            if (!ids || !keys) return set_error(kInternal, "simulate: scratch allocation failed");
+            r.red_ids = ids;
+            k_redundant_ids<<<rg, wpb * 32, rs, st>>>(r, 1);
+            LSG_LAUNCH_CHECK("k_redundant_ids");
+            c.red_off = roff;
+            c.red_ids = ids;
+            c.red_key = keys;
+        }
         c.T = a.T; c.N = N; c.D = a.D; c.B = a.L; c.C = a.C; c.k0 = k0;
         c.nzw = a.nzw; c.infw = a.infw;
         c.items = d_items; c.node_off = d_node_off; c.gb = gb;

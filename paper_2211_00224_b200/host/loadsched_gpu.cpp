@@ -362,20 +362,30 @@ PlanOutput plan_schedule(const PipelineConfig& config) {
 }
 
 SimResult simulate_plan(const SchedulePlan& plan, std::uint64_t capacity, Policy policy, bool insert_redundant) {
-    if (insert_redundant) throw CapabilityError("simulate_plan: insert_redundant is not on the device path");
     const std::uint32_t N = plan.num_nodes;
-    std::vector<std::uint32_t> items, off;
+    std::vector<std::uint32_t> items, off, rs, re, rc;
     std::uint64_t T = 0;
     for (const EpochPlan& ep : plan.epochs)
         for (const StepPlan& st : ep.steps) {
             if (st.assignment.nodes.size() != N) throw ValidationError("simulate_plan: node count mismatch");
+            if (insert_redundant && st.reads.size() != N) throw ValidationError("simulate_plan: step without reads");
             std::uint32_t o = 0;
-            for (const auto& list : st.assignment.nodes) {
+            for (std::uint32_t k = 0; k < N; ++k) {
+                const auto& list = st.assignment.nodes[k];
                 off.push_back(o);
                 for (const Assigned& a : list) {
                     if (a.id >= plan.dataset_size) throw ValidationError("simulate_plan: id out of range");
                     items.push_back(std::uint32_t(a.id) | (a.source == Source::BufferHit ? LSG_HIT_BIT : 0u));
                     ++o;
+                }
+                if (insert_redundant) {  // reads at the list's item offsets (lsg_plan_out layout)
+                    const auto& reads = st.reads[k].reads;
+                    if (reads.size() > list.size()) throw ValidationError("simulate_plan: more reads than samples");
+                    for (std::size_t i = 0; i < list.size(); ++i) {
+                        rs.push_back(i < reads.size() ? std::uint32_t(reads[i].start) : 0u);
+                        re.push_back(i < reads.size() ? std::uint32_t(reads[i].end) : 0u);
+                    }
+                    rc.push_back(std::uint32_t(reads.size()));
                 }
             }
             off.push_back(o);
@@ -387,8 +397,17 @@ SimResult simulate_plan(const SchedulePlan& plan, std::uint64_t capacity, Policy
     DevBuf<std::uint32_t> di(items.size()), doff(off.size()), dh(T * N), dm(T * N);
     di.upload(items.data(), items.size());
     doff.upload(off.data(), off.size());
-    check(lsg_simulate(di.p, doff.p, T, N, plan.dataset_size, capacity, policy == Policy::Clairvoyant ? 0 : 1, 0, N,
-                       dh.p, dm.p, nullptr, nullptr));
+    if (insert_redundant) {
+        DevBuf<std::uint32_t> drs(rs.size()), dre(re.size()), drc(rc.size());
+        drs.upload(rs.data(), rs.size());
+        dre.upload(re.data(), re.size());
+        drc.upload(rc.data(), rc.size());
+        check(lsg_simulate_ex(di.p, doff.p, T, N, plan.dataset_size, capacity, policy == Policy::Clairvoyant ? 0 : 1,
+                              1, drs.p, dre.p, drc.p, 0, N, dh.p, dm.p, nullptr, nullptr));
+    } else {
+        check(lsg_simulate(di.p, doff.p, T, N, plan.dataset_size, capacity, policy == Policy::Clairvoyant ? 0 : 1, 0,
+                           N, dh.p, dm.p, nullptr, nullptr));
+    }
     std::vector<std::uint32_t> h(T * N), m(T * N);
     dh.download(h.data(), h.size());
     dm.download(m.data(), m.size());

@@ -365,9 +365,12 @@ def baseline_config(config: PipelineConfig) -> PipelineConfig:
 
 
 def simulate_plan(plan: SchedulePlan, capacity: int, policy: str = "clairvoyant",
-                  node_range: tuple[int, int] | None = None, want_slots: bool = False) -> SimResult:
+                  node_range: tuple[int, int] | None = None, want_slots: bool = False,
+                  insert_redundant: bool = False) -> SimResult:
     """buffer.hpp:117-118 / buffer.cpp:183-247 — K7 per-rank replay. node_range
-    restricts the replay to ranks [k0, k1) (multi-GPU sharding)."""
+    restricts the replay to ranks [k0, k1) (multi-GPU sharding). With
+    insert_redundant the plan's chunk reads' unrequested ids are inserted
+    silently after each list (clairvoyant policy, no slots)."""
     N = plan.num_nodes
     T = plan.node_off.shape[0]
     k0, k1 = node_range if node_range is not None else (0, N)
@@ -375,9 +378,18 @@ def simulate_plan(plan: SchedulePlan, capacity: int, policy: str = "clairvoyant"
     hits = torch.zeros((T, N), dtype=torch.int32, device=dev)
     misses = torch.zeros((T, N), dtype=torch.int32, device=dev)
     slots = torch.empty(max(plan.items.numel(), 1), dtype=torch.int32, device=dev) if want_slots else None
-    _check(lib().lsg_simulate(_ptr(plan.items.contiguous()), _ptr(plan.node_off.contiguous()), T, N,
-                              plan.dataset_size, capacity, 0 if policy == "clairvoyant" else 1,
-                              k0, k1, _ptr(hits), _ptr(misses), _ptr(slots), _stream()))
+    pol = 0 if policy == "clairvoyant" else 1
+    if insert_redundant:
+        if plan.read_start is None:
+            raise ValidationError(3, "simulate_plan: insert_redundant needs the plan's reads")
+        _check(lib().lsg_simulate_ex(_ptr(plan.items.contiguous()), _ptr(plan.node_off.contiguous()), T, N,
+                                     plan.dataset_size, capacity, pol, 1, _ptr(plan.read_start),
+                                     _ptr(plan.read_end), _ptr(plan.read_count), k0, k1, _ptr(hits),
+                                     _ptr(misses), _ptr(slots), _stream()))
+    else:
+        _check(lib().lsg_simulate(_ptr(plan.items.contiguous()), _ptr(plan.node_off.contiguous()), T, N,
+                                  plan.dataset_size, capacity, pol, k0, k1, _ptr(hits), _ptr(misses),
+                                  _ptr(slots), _stream()))
     return SimResult(hits, misses, int(hits.sum().item()), int(misses.sum().item()),
                      slots[: plan.items.numel()] if slots is not None else None)
 

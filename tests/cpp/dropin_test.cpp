@@ -109,7 +109,13 @@ static int run_checks() {
     // capability guards are typed, never a silent CPU path
     PipelineConfig red = demo();
     red.chunk_insert_redundant = true;
+    red.policy = Policy::Lru;
     EXPECT(throws<CapabilityError>([&] { plan_schedule(red); }));
+    // chunk_insert_redundant (pipeline.cpp:103-114) with the clairvoyant policy
+    red.policy = Policy::Clairvoyant;
+    PlanOutput ro = plan_schedule(red);
+    SimResult rsim = simulate_plan(ro.plan, 64, Policy::Clairvoyant, true);
+    EXPECT(rsim.total_hits + rsim.total_misses == 6 * 1024);
     std::printf("dropin_test: %d passed, %d failed\n", passes, fails);
     return fails ? 1 : 0;
 }

@@ -131,3 +131,47 @@ def test_wide_properties_full_cfg5_slice(ls):
         assert np.array_equal(cnt, fa[g])
         assert fa[g].max() - fa[g].min() <= 1
         base += off[g, N]
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_insert_redundant_planner(ls, seed):
+    """chunk_insert_redundant (pipeline.cpp:103-114): after each step, the
+    unrequested ids inside every node's chunk reads are inserted silently
+    (buffer.cpp:48-53) with their next scheduled step — clairvoyant policy."""
+    r = random.Random(8000 + seed)
+    N, b = r.choice([1, 2, 4, 8, 40]), r.choice([2, 4, 8, 16])
+    B = N * b
+    D = B * r.randint(2, 16) + r.randint(0, B - 1)
+    c = O.Cfg(D, r.randint(1, 6), N, b, seed=r.randint(0, 10**6),
+              buffer_capacity=r.randint(1, max(1, D // r.choice([2, 4, 8]))),
+              drop_last=r.random() < 0.7, optim_order=r.random() < 0.6, optim_remap=r.random() < 0.8,
+              optim_balance=r.random() < 0.8, optim_chunk=True, chunk_insert_redundant=True,
+              chunk_threshold=r.choice([2, 5, 15, 40]), pso_iters=10)
+    check_plan(ls, c)
+
+
+def test_insert_redundant_lru_is_a_capability_error(ls):
+    c = O.Cfg(256, 2, 2, 8, seed=1, buffer_capacity=40, policy="lru", chunk_insert_redundant=True)
+    from test_gpu_parity import to_pc
+    with pytest.raises(ls.CapabilityError):
+        ls.plan_schedule(to_pc(ls, c))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_insert_redundant_replay(ls, seed):
+    """simulate_plan(..., insert_redundant=true) (buffer.cpp:224-238) on plans
+    with and without redundant planning, vs the oracle (pinned to the
+    reference in tests/test_oracle.py)."""
+    r = random.Random(8500 + seed)
+    N, b = r.choice([1, 2, 4, 8]), r.choice([2, 4, 8, 64])
+    B = N * b
+    D = B * r.randint(2, 12) + r.randint(0, B - 1)
+    thr = r.choice([2, 5, 15, 40])
+    c = O.Cfg(D, r.randint(1, 5), N, b, seed=r.randint(0, 10**6),
+              buffer_capacity=r.randint(1, max(1, D // r.choice([2, 4, 8]))), optim_chunk=True,
+              chunk_insert_redundant=r.random() < 0.5, chunk_threshold=thr, pso_iters=10)
+    out, ref = check_plan(ls, c)
+    sim = ls.simulate_plan(out.plan, c.buffer_capacity, insert_redundant=True)
+    rs, re_, cnt, _, _ = O.plan_reads(ref.items, ref.node_off, N, True, thr)
+    h, m = O.simulate_redundant(ref.items, ref.node_off, N, D, c.buffer_capacity, rs, re_, cnt)
+    assert np.array_equal(u32(sim.hits), h) and np.array_equal(u32(sim.misses), m)

@@ -164,6 +164,10 @@ def test_oracle_matches_reference(seed):
         h, m = O.simulate(p.items, p.node_off, N, D, cfg.buffer_capacity, cfg.policy)
         assert np.array_equal(p.residency, q.residency)
         assert np.array_equal(h, q.hits) and np.array_equal(m, q.misses)
+    else:  # the reference replays with insert_redundant too (pipeline.cpp:266-275)
+        rs, re_, cnt, _, _ = O.plan_reads(p.items, p.node_off, N, True, cfg.chunk_threshold)
+        h, m = O.simulate_redundant(p.items, p.node_off, N, D, cfg.buffer_capacity, rs, re_, cnt, cfg.policy)
+        assert np.array_equal(h, q.hits) and np.array_equal(m, q.misses)
 
 
 @ref
