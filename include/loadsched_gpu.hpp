@@ -14,6 +14,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <iosfwd>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -208,6 +209,22 @@ struct PlanOutput {
 };
 
 PlanOutput plan_schedule(const PipelineConfig& config);
+
+// ---- text artifacts (trace.hpp:42-47, reuse_graph.hpp:55-60, plan.hpp:55-68)
+// Writers format on the GPU (byte-identical to the reference's); readers
+// accept the reference's grammar with its error classes and messages.
+void write_trace(std::ostream& out, const AccessTrace& trace);
+AccessTrace read_trace(std::istream& in);
+void write_trace_file(const std::string& path, const AccessTrace& trace);
+AccessTrace read_trace_file(const std::string& path);
+void write_graph(std::ostream& out, const ReuseGraph& graph);
+ReuseGraph read_graph(std::istream& in);
+void write_graph_file(const std::string& path, const ReuseGraph& graph);
+ReuseGraph read_graph_file(const std::string& path);
+void write_plan(std::ostream& out, const SchedulePlan& plan);
+SchedulePlan read_plan(std::istream& in);
+void write_plan_file(const std::string& path, const SchedulePlan& plan);
+SchedulePlan read_plan_file(const std::string& path);
 
 // ---- store.hpp:13-50 --------------------------------------------------------
 // SLRD sample files; create_store computes the splitmix64 payload on the GPU

@@ -213,6 +213,62 @@ int lsg_fetch_step_store(lsg_store* h, void* const* d_bufs, void* const* d_outs,
                          const uint32_t* d_node_off, uint32_t node_begin, uint32_t node_end, uint64_t rows_hint,
                          uint64_t threshold, void* stream);
 
+/* ---- Text artifacts (trace.cpp:72-162, reuse_graph.cpp:103-140,
+ *      plan.cpp:44-214). Writers format on the GPU into h_out when
+ *      cap >= *nbytes (call with h_out = NULL for the size); the bytes are
+ *      identical to the reference's ostream output. Readers accept exactly
+ *      what the reference accepts, with its error classes and messages. */
+int lsg_format_trace(const uint32_t* d_trace, uint64_t dataset_size, uint32_t num_epochs, uint32_t num_nodes,
+                     uint64_t local_batch, uint64_t seed, int32_t drop_last, uint64_t keep, char* h_out,
+                     uint64_t cap, uint64_t* nbytes, void* stream);
+/* Plan rows: N balance rows, the assign rows and the read rows of every
+ * step (T = E * S steps, execution order); reads as lsg_plan_out (NULL:
+ * no read rows); a read with start == end is written as "single". */
+int lsg_format_plan(const uint32_t* d_items, const uint32_t* d_node_off, const uint32_t* d_fetch_before,
+                    const uint32_t* d_fetch_after, const uint32_t* d_read_start, const uint32_t* d_read_end,
+                    const uint32_t* d_read_count, const uint32_t* d_order, uint64_t cost, uint32_t E, uint64_t T,
+                    uint32_t N, uint64_t S, uint64_t dataset_size, uint64_t local_batch, uint64_t chunk_threshold,
+                    char* h_out, uint64_t cap, uint64_t* nbytes, void* stream);
+int lsg_format_graph(const uint64_t* d_w, uint32_t E, char* h_out, uint64_t cap, uint64_t* nbytes, void* stream);
+
+typedef struct lsg_trace_text {
+    uint64_t dataset_size;
+    uint32_t num_epochs, num_nodes;
+    uint64_t local_batch, seed;
+    int32_t drop_last;
+    uint64_t keep; /* ids per epoch */
+} lsg_trace_text;
+/* read_trace (trace.cpp:103-147): header into *hdr; ids ([E][keep]) into
+ * h_ids when cap >= E * keep. */
+int lsg_parse_trace(const char* text, uint64_t len, lsg_trace_text* hdr, uint32_t* h_ids, uint64_t cap);
+/* read_graph (reuse_graph.cpp:114-128): *E, weights into h_w when cap >= E*E. */
+int lsg_parse_graph(const char* text, uint64_t len, uint32_t* E, uint64_t* h_w, uint64_t cap);
+
+/* read_plan (plan.cpp:85-214) in the flat layout: steps in the file's epoch
+ * order (epoch_steps[i] steps for its i-th epoch), node lists in file order,
+ * reads as CSR per (step, node). Arrays are owned by the handle. */
+typedef struct lsg_parsed_plan lsg_parsed_plan;
+typedef struct lsg_plan_view {
+    uint64_t dataset_size, local_batch, chunk_threshold, cost;
+    uint32_t num_nodes, num_epochs;
+    uint64_t num_steps, num_items, num_reads;
+    const uint32_t* order;        /* [num_epochs] (the order line) */
+    const uint32_t* epoch_ids;    /* [num_epochs] */
+    const uint64_t* epoch_steps;  /* [num_epochs] */
+    const uint32_t* items;        /* [num_items] id | LSG_HIT_BIT */
+    const uint32_t* node_off;     /* [num_steps][N+1] */
+    const uint64_t* fetch_before; /* [num_steps][N] */
+    const uint64_t* fetch_after;  /* [num_steps][N] */
+    const uint64_t* read_off;     /* [num_steps*N+1] */
+    const uint64_t* read_start;   /* [num_reads] */
+    const uint64_t* read_end;     /* [num_reads] */
+    const uint8_t* read_chunk;    /* [num_reads] 1 = chunk, 0 = single */
+    const uint64_t* needed;       /* [num_steps][N] ChunkPlan.needed */
+    const uint64_t* redundant;    /* [num_steps][N] ChunkPlan.redundant */
+} lsg_plan_view;
+int lsg_parse_plan(const char* text, uint64_t len, lsg_parsed_plan** out, lsg_plan_view* view);
+void lsg_free_plan(lsg_parsed_plan* p);
+
 /* Number of kernel launches issued by this library since load (for the
  * bench's gpu_launches claim). */
 uint64_t lsg_launch_count(void);

@@ -353,6 +353,29 @@ def ref_available() -> bool:
     return os.path.exists(REF_DUMP)
 
 
+def ref_text(cfg: Cfg) -> dict:
+    """The UNMODIFIED reference's write_trace/write_graph/write_plan files of a
+    plan_schedule run: {"trace": bytes, "graph": bytes, "plan": bytes}."""
+    with tempfile.TemporaryDirectory() as d:
+        subprocess.run([REF_DUMP, "text", d, *cfg.kv()], check=True, capture_output=True)
+        return {k: open(os.path.join(d, k + ".txt"), "rb").read() for k in ("trace", "graph", "plan")}
+
+
+def ref_read(kind: str, data: bytes) -> tuple[int, str]:
+    """The reference's read_trace/read_graph/read_plan on `data`: (0, "") or
+    (error class, message)."""
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "in.txt")
+        with open(p, "wb") as f:
+            f.write(data)
+        out = subprocess.run([REF_DUMP, "read", kind, p], check=True, capture_output=True,
+                             text=True).stdout.rstrip("\n")
+    if out.startswith("ok"):
+        return 0, ""
+    _, code, msg = out.split(" ", 2)
+    return int(code), msg
+
+
 def ref_plan(cfg: Cfg) -> PlanArrays:
     """Run the UNMODIFIED reference plan_schedule + simulate_plan."""
     E, N, T = cfg.num_epochs, cfg.num_nodes, cfg.num_epochs * cfg.steps

@@ -11,6 +11,7 @@
 //   ref_dump time     <samples> key=value...  stage timings (JSON on stdout)
 //   ref_dump store    <out> count size seed   Store payload bytes (no header)
 //   ref_dump storefile <path> count size seed  the reference's store file
+//   ref_dump text <outdir> key=value...        trace.txt, graph.txt, plan.txt
 //   ref_dump gather   <dir> count size n thr  Store::read_one batch-fetch timing
 //
 // key=value pairs go through the reference's apply_config_entry
@@ -328,6 +329,40 @@ int cmd_store(int argc, char** argv) {
     return 0;
 }
 
+// run the reference's reader on a file: prints "ok ..." or "error <class> <msg>"
+int cmd_read(int argc, char** argv) {
+    const std::string kind = argv[2], path = argv[3];
+    try {
+        if (kind == "trace") {
+            const AccessTrace t = read_trace_file(path);
+            std::printf("ok %zu\n", t.epochs.size());
+        } else if (kind == "graph") {
+            const ReuseGraph g = read_graph_file(path);
+            std::printf("ok %u\n", g.num_epochs);
+        } else {
+            const SchedulePlan p = read_plan_file(path);
+            std::printf("ok %zu\n", p.epochs.size());
+        }
+    } catch (const Error& e) {
+        std::printf("error %d %s\n", e.exit_code(), e.what());
+    } catch (const std::exception& e) {
+        std::printf("error 7 %s\n", e.what());
+    }
+    return 0;
+}
+
+// the reference's own text artifacts of a plan_schedule run:
+// <dir>/trace.txt, graph.txt, plan.txt (write_*_file)
+int cmd_text(int argc, char** argv) {
+    const std::string dir = argv[2];
+    const PipelineConfig cfg = parse_kv(argc, argv, 3);
+    const PlanOutput out = plan_schedule(cfg);
+    write_trace_file(dir + "/trace.txt", out.trace);
+    write_graph_file(dir + "/graph.txt", out.graph);
+    write_plan_file(dir + "/plan.txt", out.plan);
+    return 0;
+}
+
 // the reference's create_store output itself (header + payload) at <path>
 int cmd_storefile(int argc, char** argv) {
     if (argc < 6) throw ValidationError("storefile <path> count size seed");
@@ -349,6 +384,8 @@ int main(int argc, char** argv) {
         if (cmd == "time") return cmd_time(argc, argv);
         if (cmd == "store") return cmd_store(argc, argv);
         if (cmd == "storefile") return cmd_storefile(argc, argv);
+        if (cmd == "text") return cmd_text(argc, argv);
+        if (cmd == "read") return cmd_read(argc, argv);
         if (cmd == "gather") return cmd_gather(argc, argv);
         std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
         return 1;

@@ -66,12 +66,31 @@ class LsgPlanOut(ctypes.Structure):
         "read_redundant")]
 
 
+class LsgTraceText(ctypes.Structure):
+    """Field-for-field mirror of ``lsg_trace_text`` (include/lsg.h)."""
+    _fields_ = [("dataset_size", ctypes.c_uint64), ("num_epochs", ctypes.c_uint32),
+                ("num_nodes", ctypes.c_uint32), ("local_batch", ctypes.c_uint64), ("seed", ctypes.c_uint64),
+                ("drop_last", ctypes.c_int32), ("keep", ctypes.c_uint64)]
+
+
+class LsgPlanView(ctypes.Structure):
+    """Field-for-field mirror of ``lsg_plan_view`` (include/lsg.h)."""
+    _fields_ = [("dataset_size", ctypes.c_uint64), ("local_batch", ctypes.c_uint64),
+                ("chunk_threshold", ctypes.c_uint64), ("cost", ctypes.c_uint64),
+                ("num_nodes", ctypes.c_uint32), ("num_epochs", ctypes.c_uint32),
+                ("num_steps", ctypes.c_uint64), ("num_items", ctypes.c_uint64), ("num_reads", ctypes.c_uint64)] + [
+        (n, ctypes.c_void_p) for n in ("order", "epoch_ids", "epoch_steps", "items", "node_off", "fetch_before",
+                                       "fetch_after", "read_off", "read_start", "read_end", "read_chunk",
+                                       "needed", "redundant")]
+
+
 EXPORTS = [
     "lsg_version", "lsg_last_error", "lsg_shape_of", "lsg_generate_trace",
     "lsg_build_reuse_graph", "lsg_pso_order", "lsg_plan", "lsg_plan_host", "lsg_simulate",
     "lsg_store_fill", "lsg_gather", "lsg_batch_fetch", "lsg_fetch_step", "lsg_launch_count",
     "lsg_store_create", "lsg_store_open", "lsg_store_info", "lsg_store_close", "lsg_store_read",
-    "lsg_store_read_rows", "lsg_fetch_step_store", "lsg_simulate_ex",
+    "lsg_store_read_rows", "lsg_fetch_step_store", "lsg_simulate_ex", "lsg_format_trace", "lsg_format_plan",
+    "lsg_format_graph", "lsg_parse_trace", "lsg_parse_graph", "lsg_parse_plan", "lsg_free_plan",
 ]
 
 
@@ -108,6 +127,14 @@ def lib() -> ctypes.CDLL:
         L.lsg_plan_host.argtypes = [ctypes.POINTER(LsgConfig), ctypes.POINTER(LsgPlanOut), P]
         L.lsg_simulate.argtypes = [P, P, u64, u32, u64, u64, i32, u32, u32, P, P, P, P]
         L.lsg_simulate_ex.argtypes = [P, P, u64, u32, u64, u64, i32, i32, P, P, P, u32, u32, P, P, P, P]
+        L.lsg_format_trace.argtypes = [P, u64, u32, u32, u64, u64, i32, u64, P, u64, P, P]
+        L.lsg_format_plan.argtypes = [P, P, P, P, P, P, P, P, u64, u32, u64, u32, u64, u64, u64, u64, P, u64, P, P]
+        L.lsg_format_graph.argtypes = [P, u32, P, u64, P, P]
+        L.lsg_parse_trace.argtypes = [ctypes.c_char_p, u64, P, P, u64]
+        L.lsg_parse_graph.argtypes = [ctypes.c_char_p, u64, P, P, u64]
+        L.lsg_parse_plan.argtypes = [ctypes.c_char_p, u64, P, P]
+        L.lsg_free_plan.argtypes = [P]
+        L.lsg_free_plan.restype = None
         L.lsg_store_fill.argtypes = [P, u64, u64, u64, P, P]
         L.lsg_gather.argtypes = [P, P, u64, u64, P, P]
         L.lsg_batch_fetch.argtypes = [P, P, P, u64, u64, u64, P, P]

@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <memory>
 #include <numeric>
 
@@ -242,6 +244,221 @@ bool same_multiset(const StepAssignment& step, const std::vector<SampleId>& batc
     std::sort(got.begin(), got.end());
     std::sort(want.begin(), want.end());
     return got == want;
+}
+
+// ---- text artifacts ----------------------------------------------------
+namespace {
+
+std::string slurp(std::istream& in) {
+    std::ostringstream ss;
+    ss << in.rdbuf();
+    return ss.str();
+}
+
+template <class Fn>
+std::string two_call(Fn fn) {
+    std::uint64_t n = 0;
+    check(fn(nullptr, 0, &n));
+    std::string s(n, '\0');
+    check(fn(s.data(), n, &n));
+    return s;
+}
+
+void write_all(const std::string& path, const std::string& data) {
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw StorageError("cannot open for writing: " + path);
+    out.write(data.data(), std::streamsize(data.size()));
+    if (!out) throw StorageError("write failed: " + path);
+}
+
+std::string read_all(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw StorageError("cannot open for reading: " + path);
+    return slurp(in);
+}
+
+}  // namespace
+
+void write_trace(std::ostream& out, const AccessTrace& trace) {
+    const TraceConfig& c = trace.config;
+    const std::uint64_t keep = trace.epoch_length();
+    std::vector<std::uint32_t> ids;
+    ids.reserve(trace.epochs.size() * keep);
+    for (const auto& ep : trace.epochs) {
+        if (ep.size() != keep) throw CapabilityError("write_trace: ragged epochs are not on the device path");
+        for (SampleId x : ep) {
+            if (x >= (1ull << 31)) throw CapabilityError("write_trace: sample ids must be < 2^31 on device");
+            ids.push_back(std::uint32_t(x));
+        }
+    }
+    DevBuf<std::uint32_t> d(ids.size());
+    d.upload(ids.data(), ids.size());
+    out << two_call([&](char* h, std::uint64_t cap, std::uint64_t* n) {
+        return lsg_format_trace(d.p, c.dataset_size, std::uint32_t(trace.epochs.size()), c.num_nodes, c.local_batch,
+                                c.seed, c.drop_last ? 1 : 0, keep, h, cap, n, nullptr);
+    });
+}
+
+AccessTrace read_trace(std::istream& in) {
+    const std::string s = slurp(in);
+    lsg_trace_text h{};
+    check(lsg_parse_trace(s.data(), s.size(), &h, nullptr, 0));
+    std::vector<std::uint32_t> ids(std::size_t(h.num_epochs) * h.keep);
+    check(lsg_parse_trace(s.data(), s.size(), &h, ids.data(), ids.size()));
+    AccessTrace t;
+    t.config = {h.dataset_size, h.num_epochs, h.num_nodes, h.local_batch, h.seed, h.drop_last != 0};
+    t.epochs.assign(h.num_epochs, std::vector<SampleId>(h.keep));
+    for (std::uint32_t e = 0; e < h.num_epochs; ++e)
+        for (std::uint64_t i = 0; i < h.keep; ++i) t.epochs[e][i] = ids[e * h.keep + i];
+    return t;
+}
+
+void write_trace_file(const std::string& path, const AccessTrace& trace) {
+    std::ostringstream ss;
+    write_trace(ss, trace);
+    write_all(path, ss.str());
+}
+
+AccessTrace read_trace_file(const std::string& path) {
+    std::istringstream in(read_all(path));
+    return read_trace(in);
+}
+
+void write_graph(std::ostream& out, const ReuseGraph& graph) {
+    DevBuf<std::uint64_t> d(graph.weights.size());
+    d.upload(graph.weights.data(), graph.weights.size());
+    out << two_call([&](char* h, std::uint64_t cap, std::uint64_t* n) {
+        return lsg_format_graph(d.p, graph.num_epochs, h, cap, n, nullptr);
+    });
+}
+
+ReuseGraph read_graph(std::istream& in) {
+    const std::string s = slurp(in);
+    std::uint32_t E = 0;
+    check(lsg_parse_graph(s.data(), s.size(), &E, nullptr, 0));
+    ReuseGraph g;
+    g.num_epochs = E;
+    g.weights.assign(std::size_t(E) * E, 0);
+    check(lsg_parse_graph(s.data(), s.size(), &E, g.weights.data(), g.weights.size()));
+    return g;
+}
+
+void write_graph_file(const std::string& path, const ReuseGraph& graph) {
+    std::ostringstream ss;
+    write_graph(ss, graph);
+    write_all(path, ss.str());
+}
+
+ReuseGraph read_graph_file(const std::string& path) {
+    std::istringstream in(read_all(path));
+    return read_graph(in);
+}
+
+void write_plan(std::ostream& out, const SchedulePlan& plan) {
+    const std::uint32_t N = plan.num_nodes, E = std::uint32_t(plan.epochs.size());
+    const std::uint64_t S = E ? plan.epochs.front().steps.size() : 0;
+    std::vector<std::uint32_t> items, off, fb, fa, rs, re, rc, order;
+    for (std::uint32_t i = 0; i < E; ++i) {
+        const EpochPlan& ep = plan.epochs[i];
+        if (ep.steps.size() != S || i >= plan.order.order.size() || plan.order.order[i] != ep.epoch)
+            throw CapabilityError("write_plan: the device writer needs uniform steps in schedule order");
+        order.push_back(ep.epoch);
+        for (const StepPlan& st : ep.steps) {
+            std::uint32_t o = 0;
+            for (std::uint32_t k = 0; k < N; ++k) {
+                off.push_back(o);
+                fb.push_back(std::uint32_t(st.fetches_before.at(k)));
+                fa.push_back(std::uint32_t(st.fetches_after.at(k)));
+                const auto& list = st.assignment.nodes.at(k);
+                const auto& reads = st.reads.size() == N ? st.reads[k].reads : std::vector<Read>{};
+                if (reads.size() > list.size()) throw CapabilityError("write_plan: more reads than samples in a list");
+                for (std::size_t j = 0; j < list.size(); ++j) {
+                    items.push_back(std::uint32_t(list[j].id) | (list[j].source == Source::BufferHit ? LSG_HIT_BIT : 0u));
+                    const bool has = j < reads.size();
+                    if (has && (reads[j].kind == Read::Kind::Single) != (reads[j].start == reads[j].end))
+                        throw CapabilityError("write_plan: read kind differs from its span");
+                    rs.push_back(has ? std::uint32_t(reads[j].start) : 0u);
+                    re.push_back(has ? std::uint32_t(reads[j].end) : 0u);
+                    ++o;
+                }
+                rc.push_back(std::uint32_t(reads.size()));
+            }
+            off.push_back(o);
+        }
+    }
+    const std::uint64_t T = std::uint64_t(E) * S;
+    DevBuf<std::uint32_t> di(items.size()), doff(off.size()), dfb(fb.size()), dfa(fa.size()), drs(rs.size()),
+        dre(re.size()), drc(rc.size()), dord(order.size());
+    di.upload(items.data(), items.size());
+    doff.upload(off.data(), off.size());
+    dfb.upload(fb.data(), fb.size());
+    dfa.upload(fa.data(), fa.size());
+    drs.upload(rs.data(), rs.size());
+    dre.upload(re.data(), re.size());
+    drc.upload(rc.data(), rc.size());
+    dord.upload(order.data(), order.size());
+    out << two_call([&](char* h, std::uint64_t cap, std::uint64_t* n) {
+        return lsg_format_plan(di.p, doff.p, dfb.p, dfa.p, drs.p, dre.p, drc.p, dord.p, plan.order.cost, E, T, N,
+                               S ? S : 1, plan.dataset_size, plan.local_batch, plan.chunk_threshold, h, cap, n,
+                               nullptr);
+    });
+}
+
+SchedulePlan read_plan(std::istream& in) {
+    const std::string s = slurp(in);
+    lsg_parsed_plan* h = nullptr;
+    lsg_plan_view v{};
+    check(lsg_parse_plan(s.data(), s.size(), &h, &v));
+    std::unique_ptr<lsg_parsed_plan, void (*)(lsg_parsed_plan*)> guard(h, lsg_free_plan);
+    SchedulePlan p;
+    p.dataset_size = v.dataset_size;
+    p.num_nodes = v.num_nodes;
+    p.local_batch = v.local_batch;
+    p.chunk_threshold = v.chunk_threshold;
+    p.order.order.assign(v.order, v.order + v.num_epochs);
+    p.order.cost = v.cost;
+    const std::uint32_t N = v.num_nodes;
+    std::uint64_t g = 0, base = 0;
+    for (std::uint32_t e = 0; e < v.num_epochs; ++e) {
+        EpochPlan ep;
+        ep.epoch = v.epoch_ids[e];
+        for (std::uint64_t t = 0; t < v.epoch_steps[e]; ++t, ++g) {
+            StepPlan st;
+            st.assignment.nodes.resize(N);
+            st.reads.resize(N);
+            const std::uint32_t* off = v.node_off + g * (N + 1);
+            for (std::uint32_t k = 0; k < N; ++k) {
+                for (std::uint32_t i = off[k]; i < off[k + 1]; ++i) {
+                    const std::uint32_t it = v.items[base + i];
+                    st.assignment.nodes[k].push_back(
+                        {it & ~LSG_HIT_BIT, (it & LSG_HIT_BIT) ? Source::BufferHit : Source::PfsFetch});
+                }
+                st.fetches_before.push_back(v.fetch_before[g * N + k]);
+                st.fetches_after.push_back(v.fetch_after[g * N + k]);
+                ChunkPlan& cp = st.reads[k];
+                for (std::uint64_t q = v.read_off[g * N + k]; q < v.read_off[g * N + k + 1]; ++q)
+                    cp.reads.push_back({v.read_chunk[q] ? Read::Kind::Chunk : Read::Kind::Single, v.read_start[q],
+                                        v.read_end[q]});
+                cp.needed = v.needed[g * N + k];
+                cp.redundant = v.redundant[g * N + k];
+            }
+            base += off[N];
+            ep.steps.push_back(std::move(st));
+        }
+        p.epochs.push_back(std::move(ep));
+    }
+    return p;
+}
+
+void write_plan_file(const std::string& path, const SchedulePlan& plan) {
+    std::ostringstream ss;
+    write_plan(ss, plan);
+    write_all(path, ss.str());
+}
+
+SchedulePlan read_plan_file(const std::string& path) {
+    std::istringstream in(read_all(path));
+    return read_plan(in);
 }
 
 void create_store(const std::string& path, std::uint64_t sample_count, std::uint64_t sample_size,

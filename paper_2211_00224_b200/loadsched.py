@@ -22,7 +22,9 @@ __all__ = [
     "PsoResult", "SchedulePlan", "PlanOutput", "SimResult", "generate_trace", "build_reuse_graph",
     "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "baseline_config", "simulate_plan",
     "store_fill", "gather", "batch_fetch", "StepFetcher", "StoreHeader", "Store", "create_store",
-    "STORE_HEADER_BYTES", "DEFAULT_STORE_BUDGET", "Error", "ConfigError", "ValidationError", "CapabilityError",
+    "STORE_HEADER_BYTES", "DEFAULT_STORE_BUDGET", "format_trace", "write_trace_file", "read_trace",
+    "read_trace_file", "format_graph", "write_graph_file", "read_graph", "read_graph_file", "format_plan",
+    "write_plan_file", "read_plan", "read_plan_file", "Error", "ConfigError", "ValidationError", "CapabilityError",
     "StorageError", "InternalError", "HIT_BIT", "NEVER",
 ]
 
@@ -204,6 +206,7 @@ class SchedulePlan:
     read_count: torch.Tensor | None = None
     read_needed: torch.Tensor | None = None
     read_redundant: torch.Tensor | None = None
+    chunk_threshold: int = 0    # plan.hpp: the threshold the reads were cut with (0: no chunking)
 
 
 @dataclass
@@ -322,7 +325,8 @@ def _wrap_plan(config: PipelineConfig, sh, b) -> PlanOutput:
                         b["fetch_before"][: T * N].view(T, N), b["fetch_after"][: T * N].view(T, N),
                         b["read_start"][: E * keep], b["read_end"][: E * keep],
                         b["read_count"][: T * N].view(T, N), b["read_needed"][: T * N].view(T, N),
-                        b["read_redundant"][: T * N].view(T, N))
+                        b["read_redundant"][: T * N].view(T, N),
+                        config.chunk_threshold if config.optim_chunk else 0)  # pipeline.cpp:52
     return PlanOutput(trace, graph, pso, plan)
 
 
@@ -425,6 +429,158 @@ def batch_fetch(buf: torch.Tensor, ids: torch.Tensor, slots: torch.Tensor, sampl
     _check(lib().lsg_batch_fetch(_ptr(buf), _ptr(ids), _ptr(slots), n, sample_bytes, fill_seed,
                                  _ptr(out), _stream()))
     return out
+
+
+# -------------------------------------------------------------- artifacts --
+# trace.cpp:72-162, reuse_graph.cpp:103-140, plan.cpp:44-227. Writers format on
+# the GPU (lsg_format_*), readers accept exactly the reference's grammar.
+def _two_call(fn, *args) -> bytes:
+    n = ctypes.c_uint64(0)
+    _check(fn(*args, None, 0, ctypes.byref(n), _stream()))
+    buf = ctypes.create_string_buffer(max(1, n.value))
+    _check(fn(*args, buf, n.value, ctypes.byref(n), _stream()))
+    return buf.raw[: n.value]
+
+
+def _write(path, data: bytes) -> None:
+    try:
+        with open(path, "wb") as f:
+            f.write(data)
+    except OSError as e:
+        raise StorageError(6, f"cannot open for writing: {path}") from e
+
+
+def _read(path) -> bytes:
+    try:
+        with open(path, "rb") as f:
+            return f.read()
+    except OSError as e:
+        raise StorageError(6, f"cannot open for reading: {path}") from e
+
+
+def format_trace(trace: AccessTrace) -> bytes:
+    """write_trace (trace.cpp:72-84)."""
+    c = trace.config
+    ep = trace.epochs.contiguous()
+    return _two_call(lib().lsg_format_trace, _ptr(ep), c.dataset_size, c.num_epochs, c.num_nodes, c.local_batch,
+                     c.seed, int(c.drop_last), ep.shape[1] if ep.dim() == 2 else 0)
+
+
+def write_trace_file(path, trace: AccessTrace) -> None:
+    _write(path, format_trace(trace))
+
+
+def read_trace(text) -> AccessTrace:
+    """read_trace (trace.cpp:103-147): ids land on the device."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = _lib.LsgTraceText()
+    _check(lib().lsg_parse_trace(data, len(data), ctypes.byref(h), None, 0))
+    n = h.num_epochs * h.keep
+    ids = torch.empty(max(n, 1), dtype=torch.int32)
+    _check(lib().lsg_parse_trace(data, len(data), ctypes.byref(h), ctypes.c_void_p(ids.data_ptr()), n))
+    cfg = TraceConfig(h.dataset_size, h.num_epochs, h.num_nodes, h.local_batch, h.seed, bool(h.drop_last))
+    return AccessTrace(cfg, ids[:n].view(h.num_epochs, h.keep).to(_dev()))
+
+
+def read_trace_file(path) -> AccessTrace:
+    return read_trace(_read(path))
+
+
+def format_graph(graph: ReuseGraph) -> bytes:
+    """write_graph (reuse_graph.cpp:103-112)."""
+    return _two_call(lib().lsg_format_graph, _ptr(graph.weights.contiguous()), graph.num_epochs)
+
+
+def write_graph_file(path, graph: ReuseGraph) -> None:
+    _write(path, format_graph(graph))
+
+
+def read_graph(text) -> ReuseGraph:
+    """read_graph (reuse_graph.cpp:114-128)."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    E = ctypes.c_uint32(0)
+    _check(lib().lsg_parse_graph(data, len(data), ctypes.byref(E), None, 0))
+    w = torch.empty(max(E.value * E.value, 1), dtype=torch.int64)
+    _check(lib().lsg_parse_graph(data, len(data), ctypes.byref(E), ctypes.c_void_p(w.data_ptr()),
+                                 E.value * E.value))
+    return ReuseGraph(E.value, 0, "global", w[: E.value * E.value].view(E.value, E.value).to(_dev()))
+
+
+def read_graph_file(path) -> ReuseGraph:
+    return read_graph(_read(path))
+
+
+def format_plan(plan: SchedulePlan) -> bytes:
+    """write_plan (plan.cpp:44-69), assign/balance/read rows formatted on the GPU."""
+    T = plan.node_off.shape[0]
+    E = plan.order.order.numel()
+    S = plan.steps_per_epoch
+    has_reads = plan.read_start is not None
+    return _two_call(lib().lsg_format_plan, _ptr(plan.items.contiguous()), _ptr(plan.node_off.contiguous()),
+                     _ptr(plan.fetches_before.contiguous()), _ptr(plan.fetches_after.contiguous()),
+                     _ptr(plan.read_start) if has_reads else None, _ptr(plan.read_end) if has_reads else None,
+                     _ptr(plan.read_count) if has_reads else None, _ptr(plan.order.order.contiguous()),
+                     plan.order.cost, E, T, plan.num_nodes, S, plan.dataset_size, plan.local_batch,
+                     plan.chunk_threshold)
+
+
+def write_plan_file(path, plan: SchedulePlan) -> None:
+    _write(path, format_plan(plan))
+
+
+def read_plan(text) -> SchedulePlan:
+    """read_plan (plan.cpp:85-214) into the flat device layout. Every epoch of
+    the file must have the same step count and no list more reads than
+    samples (else CapabilityError: the flat layout keeps reads at item
+    offsets)."""
+    import numpy as np
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h = ctypes.c_void_p()
+    v = _lib.LsgPlanView()
+    _check(lib().lsg_parse_plan(data, len(data), ctypes.byref(h), ctypes.byref(v)))
+    try:
+        N, T, E = v.num_nodes, v.num_steps, v.num_epochs
+        arr = lambda p, n, dt: np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(dt)), shape=(n,)).copy() if n and p else np.zeros(0, np.dtype(dt))  # noqa: E731
+        items = arr(v.items, v.num_items, ctypes.c_uint32)
+        node_off = arr(v.node_off, T * (N + 1), ctypes.c_uint32).reshape(T, N + 1)
+        fb = arr(v.fetch_before, T * N, ctypes.c_uint64).reshape(T, N)
+        fa = arr(v.fetch_after, T * N, ctypes.c_uint64).reshape(T, N)
+        roff = arr(v.read_off, T * N + 1, ctypes.c_uint64)
+        rs = arr(v.read_start, v.num_reads, ctypes.c_uint64)
+        re_ = arr(v.read_end, v.num_reads, ctypes.c_uint64)
+        order = arr(v.order, E, ctypes.c_uint32)
+        steps = arr(v.epoch_steps, E, ctypes.c_uint64)
+        need = arr(v.needed, T * N, ctypes.c_uint64).reshape(T, N)
+        red = arr(v.redundant, T * N, ctypes.c_uint64).reshape(T, N)
+        meta = (v.dataset_size, v.local_batch, v.chunk_threshold, v.cost)
+    finally:
+        lib().lsg_free_plan(h)
+    if E and (steps != steps[0]).any():
+        raise CapabilityError(4, "read_plan: epochs with different step counts")
+    # reads at item offsets (lsg_plan_out layout)
+    gb = np.concatenate([[0], np.cumsum(node_off[:, N].astype(np.int64))])
+    rstart = np.zeros(max(len(items), 1), np.uint32)
+    rend = np.zeros(max(len(items), 1), np.uint32)
+    rcount = (roff[1:] - roff[:-1]).reshape(T, N)
+    for g in range(T):
+        for k in range(N):
+            n = int(rcount[g, k])
+            if not n:
+                continue
+            if n > node_off[g, k + 1] - node_off[g, k]:
+                raise CapabilityError(4, "read_plan: a list has more reads than samples")
+            lo, q = int(gb[g] + node_off[g, k]), int(roff[g * N + k])
+            rstart[lo:lo + n] = rs[q:q + n]
+            rend[lo:lo + n] = re_[q:q + n]
+    dev = _dev()
+    t32 = lambda a: torch.from_numpy(np.ascontiguousarray(a).astype(np.uint32).view(np.int32)).to(dev)  # noqa: E731
+    return SchedulePlan(int(meta[0]), N, int(meta[1]), int(steps[0]) if E else 0,
+                        EpochOrder(t32(order), int(meta[3])), t32(items), t32(node_off), t32(fb), t32(fa),
+                        t32(rstart), t32(rend), t32(rcount), t32(need), t32(red), int(meta[2]))
+
+
+def read_plan_file(path) -> SchedulePlan:
+    return read_plan(_read(path))
 
 
 # ------------------------------------------------------------------ Store --

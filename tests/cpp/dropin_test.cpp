@@ -82,6 +82,21 @@ static int run_checks() {
     w.buffer_capacity = 64;
     SimResult ws = simulate_plan(plan_schedule(w).plan, 64, Policy::Clairvoyant);
     EXPECT(ws.total_misses == 64 && ws.total_hits == 3 * 64 - 64);
+    // text artifacts: write -> read round trips (plan.cpp:44-214, trace.cpp:72-147)
+    {
+        const std::string pp = "/tmp/lsg_dropin_plan.txt", tp = "/tmp/lsg_dropin_trace.txt";
+        write_plan_file(pp, out.plan);
+        const SchedulePlan back = read_plan_file(pp);
+        SimResult s2 = simulate_plan(back, 64, Policy::Clairvoyant);
+        EXPECT(s2.total_misses == 4864 && s2.total_hits == 1280);
+        EXPECT(back.order.order == out.plan.order.order && back.epochs.size() == out.plan.epochs.size());
+        write_trace_file(tp, out.trace);
+        const AccessTrace tb = read_trace_file(tp);
+        EXPECT(tb.epochs == out.trace.epochs && tb.config.seed == 7);
+        std::remove(pp.c_str());
+        std::remove(tp.c_str());
+        EXPECT(throws<StorageError>([&] { read_plan_file("/nonexistent/plan.txt"); }));
+    }
     // the Store (tests/test_store.cpp:63-65 golden; :73-91 chunk == singles)
     {
         const std::string sp = "/tmp/lsg_dropin_store.bin";
