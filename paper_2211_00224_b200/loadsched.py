@@ -20,7 +20,7 @@ from ._lib import HIT_BIT, NEVER, LsgConfig, LsgError, LsgPlanOut, LsgShape, che
 __all__ = [
     "TraceConfig", "PsoParams", "PipelineConfig", "AccessTrace", "ReuseGraph", "EpochOrder",
     "PsoResult", "SchedulePlan", "PlanOutput", "SimResult", "generate_trace", "build_reuse_graph",
-    "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "baseline_config", "simulate_plan",
+    "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "plan_host_buffers", "baseline_config", "simulate_plan",
     "store_fill", "gather", "batch_fetch", "StepFetcher", "StoreHeader", "Store", "create_store",
     "STORE_HEADER_BYTES", "DEFAULT_STORE_BUDGET", "format_trace", "write_trace_file", "read_trace",
     "read_trace_file", "format_graph", "write_graph_file", "read_graph", "read_graph_file", "format_plan",
@@ -339,21 +339,29 @@ def plan_schedule(config: PipelineConfig) -> PlanOutput:
     return _wrap_plan(config, sh, b)
 
 
-def plan_schedule_host(config: PipelineConfig, pinned: bool = True) -> PlanOutput:
-    """plan_schedule with host outputs through lsg_plan_host (the e2e path):
-    device work plus the device->host copies of the whole plan."""
-    _dev()
+def plan_host_buffers(config: PipelineConfig, pinned: bool = True) -> dict:
+    """Host (pinned) output arrays for plan_schedule_host, allocated once by a
+    loader and reused across plans."""
     sh = config.shape()
     E, N, T = config.trace.num_epochs, config.trace.num_nodes, int(sh.total_steps)
     mk = lambda n, dt: torch.empty(max(int(n), 1), dtype=dt, pin_memory=pinned)  # noqa: E731
-    b = dict(trace=mk(sh.total_items, torch.int32), graph=mk(E * E, torch.int64),
-             order=mk(E, torch.int32), cost=mk(1, torch.int64),
-             hist=mk(config.pso.max_iters, torch.int64), iters=mk(1, torch.int32),
-             items=mk(sh.total_items, torch.int32), node_off=mk(T * (N + 1), torch.int32),
-             fetch_before=mk(T * N, torch.int32), fetch_after=mk(T * N, torch.int32),
-             read_start=mk(sh.total_items, torch.int32), read_end=mk(sh.total_items, torch.int32),
-             read_count=mk(T * N, torch.int32), read_needed=mk(T * N, torch.int32),
-             read_redundant=mk(T * N, torch.int32))
+    return dict(trace=mk(sh.total_items, torch.int32), graph=mk(E * E, torch.int64),
+                order=mk(E, torch.int32), cost=mk(1, torch.int64),
+                hist=mk(config.pso.max_iters, torch.int64), iters=mk(1, torch.int32),
+                items=mk(sh.total_items, torch.int32), node_off=mk(T * (N + 1), torch.int32),
+                fetch_before=mk(T * N, torch.int32), fetch_after=mk(T * N, torch.int32),
+                read_start=mk(sh.total_items, torch.int32), read_end=mk(sh.total_items, torch.int32),
+                read_count=mk(T * N, torch.int32), read_needed=mk(T * N, torch.int32),
+                read_redundant=mk(T * N, torch.int32))
+
+
+def plan_schedule_host(config: PipelineConfig, pinned: bool = True, buffers: dict | None = None) -> PlanOutput:
+    """plan_schedule with host outputs through lsg_plan_host (the e2e path):
+    device work plus the device->host copies of the whole plan (into
+    `buffers` from plan_host_buffers when given)."""
+    _dev()
+    sh = config.shape()
+    b = buffers if buffers is not None else plan_host_buffers(config, pinned)
     out = LsgPlanOut(**{k: v.data_ptr() for k, v in b.items()})
     c = config.to_c()
     _check(lib().lsg_plan_host(ctypes.byref(c), ctypes.byref(out), _stream()))
