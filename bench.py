@@ -350,10 +350,11 @@ def main():
                        "bytes_per_step": alg_bytes},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "traffic_note": "dram read+write bytes per k_fetch_step_hits launch (one step, all local "
-                                         "ranks) from profiles/r01_ncu_full_summary.txt; "
-                                         f"{traffic_ratio} x the launch's algorithmic bytes" if traffic else None,
-                         "kernel": "fetch phase (k_fetch_step_hits + k_fetch_step_misses, one pair per step)",
+                         "traffic_note": "dram read+write bytes per k_fetch_step_hits_tma launch (one steady-state "
+                                         "step, all local ranks) from profiles/r01_ncu_full_summary.txt; "
+                                         f"{traffic_ratio:.3f} x that launch's algorithmic bytes" if traffic else None,
+                         "kernel": "fetch phase (k_fetch_step_hits_tma TMA bulk-copy gather + k_fetch_step_misses, "
+                                   "one pair per training step)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6650"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
