@@ -49,6 +49,41 @@ LOADSCHED_GPU_ERROR(InternalError, Internal)
 using SampleId = std::uint64_t;  // trace.hpp:11 (device ids are 32-bit)
 using IdSet = std::unordered_set<SampleId>;
 
+// ---- prng.hpp:12-53: the splitmix64 stream every random choice draws from
+// (host side of the counter-based draws the kernels compute in parallel) ----
+inline constexpr std::uint64_t kGoldenGamma = 0x9E3779B97F4A7C15ULL;
+
+class SplitMix64 {
+  public:
+    using result_type = std::uint64_t;
+    explicit constexpr SplitMix64(std::uint64_t seed) : state_(seed) {}
+    constexpr std::uint64_t next() {
+        std::uint64_t z = (state_ += kGoldenGamma);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+    constexpr std::uint64_t operator()() { return next(); }
+    constexpr std::uint64_t next_below(std::uint64_t bound) { return next() % bound; }
+    constexpr double next_double() { return static_cast<double>(next() >> 11) * (1.0 / 9007199254740992.0); }
+    static constexpr std::uint64_t min() { return 0; }
+    static constexpr std::uint64_t max() { return ~0ULL; }
+
+  private:
+    std::uint64_t state_;
+};
+
+// in-place Fisher-Yates, i = n .. 2 swapping a[i-1] with a[next_below(i)]
+template <typename T>
+void fisher_yates_shuffle(std::vector<T>& a, SplitMix64& rng) {
+    for (std::size_t i = a.size(); i > 1; --i) {
+        const std::size_t j = std::size_t(rng.next_below(i));
+        T t = a[i - 1];
+        a[i - 1] = a[j];
+        a[j] = t;
+    }
+}
+
 // ---- trace.hpp:15-57 -------------------------------------------------------
 struct TraceConfig {
     std::uint64_t dataset_size = 0;
@@ -83,9 +118,15 @@ struct ReuseGraph {
     WindowMode mode = WindowMode::Global;
     std::vector<std::uint64_t> weights;  // row-major E x E
     std::uint64_t weight(std::uint32_t u, std::uint32_t v) const { return weights[std::size_t(u) * num_epochs + v]; }
+    std::uint64_t& weight(std::uint32_t u, std::uint32_t v) { return weights[std::size_t(u) * num_epochs + v]; }
 };
 
 ReuseGraph build_reuse_graph(const AccessTrace& trace, std::uint64_t buffer_size, WindowMode mode);
+// the K2 window bitsets of one epoch as id sets (reuse_graph.hpp:38-48)
+std::vector<IdSet> last_buffer_window(const AccessTrace& trace, std::uint32_t epoch, std::uint64_t buffer_size,
+                                      WindowMode mode);
+std::vector<IdSet> first_buffer_window(const AccessTrace& trace, std::uint32_t epoch, std::uint64_t buffer_size,
+                                       WindowMode mode);
 
 // ---- epoch_order.hpp:13-63 -------------------------------------------------
 struct EpochOrder {
@@ -114,6 +155,7 @@ struct PsoResult {
 std::uint64_t path_cost(const ReuseGraph& graph, const std::vector<std::uint32_t>& order);
 PsoResult pso_order(const ReuseGraph& graph, const PsoParams& params);
 EpochOrder identity_order(const ReuseGraph& graph);
+EpochOrder brute_force_order(const ReuseGraph& graph);  // epoch_order.hpp:35-38, E <= 10 on device
 
 // ---- plan.hpp:16-53 --------------------------------------------------------
 enum class Source { BufferHit, PfsFetch };
@@ -135,6 +177,8 @@ struct Read {  // chunking.hpp:13-22
     enum class Kind { Single, Chunk };
     Kind kind = Kind::Single;
     SampleId start = 0, end = 0;
+    std::uint64_t span() const { return end - start + 1; }
+    friend bool operator==(const Read&, const Read&) = default;
 };
 struct ChunkPlan {
     std::vector<Read> reads;
@@ -163,6 +207,13 @@ struct SchedulePlan {
 };
 
 bool same_multiset(const StepAssignment& step, const std::vector<SampleId>& batch);
+
+// ---- chunking.hpp:23-39: plan_chunks runs the device read planner on one
+// list; redundant_ids / chunked_fraction are host-side accessors of a plan
+ChunkPlan plan_chunks(const std::vector<SampleId>& fetch_ids, std::uint64_t threshold);
+std::vector<SampleId> redundant_ids(const ChunkPlan& plan, const std::vector<SampleId>& fetch_ids);
+double chunked_fraction(const ChunkPlan& plan);
+double chunked_fraction(const std::vector<ChunkPlan>& plans);
 
 // ---- buffer.hpp:16-118 (simulation results) --------------------------------
 enum class Policy { Clairvoyant, Lru };

@@ -213,6 +213,20 @@ int lsg_fetch_step_store(lsg_store* h, void* const* d_bufs, void* const* d_outs,
                          const uint32_t* d_node_off, uint32_t node_begin, uint32_t node_end, uint64_t rows_hint,
                          uint64_t threshold, void* stream);
 
+/* ---- Per-call pieces of the reference API around the path ----
+ * first_buffer_window / last_buffer_window (reuse_graph.cpp:43-75): window
+ * bitsets of every epoch, [E][W][ceil(D/32)] words, W = 1 (Global) or N. */
+int lsg_buffer_windows(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64_t D, uint32_t N, uint64_t b,
+                       int32_t drop_last, uint64_t buffer_size, int32_t mode, uint32_t* d_first, uint32_t* d_last,
+                       void* stream);
+/* brute_force_order (epoch_order.cpp:32-52): exact minimum over all E! open
+ * paths, ties to the lexicographically smallest order; E <= 10. */
+int lsg_brute_force_order(const uint64_t* d_w, uint32_t E, uint32_t* d_order, uint64_t* d_cost, void* stream);
+/* plan_chunks (chunking.cpp:9-33) of one host fetch list: reads into h_start /
+ * h_end (capacity n; start == end: Single), h_meta = {reads, needed, redundant}. */
+int lsg_plan_chunks(const uint32_t* h_ids, uint64_t n, uint64_t threshold, uint32_t* h_start, uint32_t* h_end,
+                    uint64_t* h_meta, void* stream);
+
 /* ---- Text artifacts (trace.cpp:72-162, reuse_graph.cpp:103-140,
  *      plan.cpp:44-214). Writers format on the GPU into h_out when
  *      cap >= *nbytes (call with h_out = NULL for the size); the bytes are

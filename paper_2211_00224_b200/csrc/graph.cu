@@ -172,12 +172,42 @@ __global__ void k_rows_distinct(uint32_t len, uint32_t words, const uint32_t* __
 
 }  // namespace
 
+// K2 alone: First/Last window bitsets, [E][nwin][ceil(D/32)] words each
+// (first_buffer_window / last_buffer_window, reuse_graph.cpp:43-75).
+int window_bits_device(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64_t D, uint32_t N, uint64_t b,
+                       bool drop_last, uint64_t buffer_size, int mode, bool rows_distinct_known, uint32_t* Fb,
+                       uint32_t* Lb, cudaStream_t st);
+
 int build_reuse_graph_device(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64_t D,
                              uint32_t N, uint64_t b, bool drop_last, uint64_t buffer_size, int mode,
                              bool rows_distinct_known, uint64_t* d_w, cudaStream_t st) {
     if (buffer_size == 0) return set_error(kValidation, "build_reuse_graph: buffer_size must be >= 1");
     if (E == 0) return kOk;
     LSG_CUDA(cudaMemsetAsync(d_w, 0, size_t(E) * E * sizeof(uint64_t), st));
+    const uint64_t W = uint64_t((D + 31) / 32) * (mode == 0 ? 1 : N);  // words per (epoch) row
+    Scratch sc(st);
+    uint32_t* Fb = sc.get<uint32_t>(size_t(E) * W);
+    uint32_t* Lb = sc.get<uint32_t>(size_t(E) * W);
+    if (!Fb || !Lb) return set_error(kInternal, "build_reuse_graph: scratch allocation failed");
+    if (int rc = window_bits_device(d_trace, E, len, D, N, b, drop_last, buffer_size, mode, rows_distinct_known, Fb,
+                                    Lb, st))
+        return rc;
+    const uint32_t tiles = ((E + kGT - 1) / kGT) * ((E + kGT - 1) / kGT);
+    uint32_t split = std::max<uint32_t>(1, (296 + tiles - 1) / tiles);
+    split = std::min<uint64_t>(split, std::max<uint64_t>(1, W / 256));
+    uint32_t kspan = uint32_t((W + split - 1) / split);
+    kspan = (kspan + kGK - 1) / kGK * kGK;
+    split = uint32_t((W + kspan - 1) / kspan);
+    dim3 grid((E + kGT - 1) / kGT, (E + kGT - 1) / kGT, split);
+    k_reuse_gram<<<grid, 256, 0, st>>>(E, uint32_t(W), kspan, Fb, Lb,
+                                       reinterpret_cast<unsigned long long*>(d_w));
+    LSG_LAUNCH_CHECK("k_reuse_gram");
+    return kOk;
+}
+
+int window_bits_device(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64_t D, uint32_t N, uint64_t b,
+                       bool drop_last, uint64_t buffer_size, int mode, bool rows_distinct_known, uint32_t* Fb,
+                       uint32_t* Lb, cudaStream_t st) {
     WinGeom g;
     g.len = uint32_t(len);
     g.N = N;
@@ -190,9 +220,6 @@ int build_reuse_graph_device(const uint32_t* d_trace, uint32_t E, uint64_t len, 
     g.want = mode == 0 ? buffer_size * N : buffer_size;
     const uint64_t W = uint64_t(g.words) * g.nwin;  // words per (epoch) row
     Scratch sc(st);
-    uint32_t* Fb = sc.get<uint32_t>(size_t(E) * W);
-    uint32_t* Lb = sc.get<uint32_t>(size_t(E) * W);
-    if (!Fb || !Lb) return set_error(kInternal, "build_reuse_graph: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(Fb, 0, size_t(E) * W * 4, st));
     LSG_CUDA(cudaMemsetAsync(Lb, 0, size_t(E) * W * 4, st));
 
@@ -218,16 +245,6 @@ int build_reuse_graph_device(const uint32_t* d_trace, uint32_t E, uint64_t len, 
         k_windows_general<<<grid_for(warps * 32, 256, 1u << 20), 256, 0, st>>>(g, E, d_trace, Fb, Lb);
         LSG_LAUNCH_CHECK("k_windows_general");
     }
-    const uint32_t tiles = ((E + kGT - 1) / kGT) * ((E + kGT - 1) / kGT);
-    uint32_t split = std::max<uint32_t>(1, (296 + tiles - 1) / tiles);
-    split = std::min<uint64_t>(split, std::max<uint64_t>(1, W / 256));
-    uint32_t kspan = uint32_t((W + split - 1) / split);
-    kspan = (kspan + kGK - 1) / kGK * kGK;
-    split = uint32_t((W + kspan - 1) / kspan);
-    dim3 grid((E + kGT - 1) / kGT, (E + kGT - 1) / kGT, split);
-    k_reuse_gram<<<grid, 256, 0, st>>>(E, uint32_t(W), kspan, Fb, Lb,
-                                       reinterpret_cast<unsigned long long*>(d_w));
-    LSG_LAUNCH_CHECK("k_reuse_gram");
     return kOk;
 }
 

@@ -176,6 +176,107 @@ ReuseGraph build_reuse_graph(const AccessTrace& trace, std::uint64_t buffer_size
     return g;
 }
 
+namespace {
+// K2 windows of `epoch` as id sets (reuse_graph.cpp:43-56)
+std::vector<IdSet> buffer_window(const AccessTrace& trace, std::uint32_t epoch, std::uint64_t buffer_size,
+                                 WindowMode mode, bool first) {
+    if (epoch >= trace.epochs.size()) throw ValidationError("buffer window: epoch out of range");
+    if (buffer_size == 0) throw ValidationError("buffer window: buffer_size must be >= 1");
+    const TraceConfig& c = trace.config;
+    const std::uint64_t len = trace.epochs[epoch].size();
+    std::vector<std::uint32_t> flat(std::max<std::uint64_t>(len, 1));
+    for (std::uint64_t i = 0; i < len; ++i) {
+        const SampleId x = trace.epochs[epoch][i];
+        if (x >= (1ull << 31) || x >= c.dataset_size) throw CapabilityError("buffer window: ids must be < dataset_size");
+        flat[i] = std::uint32_t(x);
+    }
+    const std::uint32_t W = mode == WindowMode::Global ? 1u : c.num_nodes;
+    const std::uint64_t words = (c.dataset_size + 31) / 32;
+    DevBuf<std::uint32_t> dt(flat.size()), df(W * words), dl(W * words);
+    dt.upload(flat.data(), flat.size());
+    check(lsg_buffer_windows(dt.p, 1, len, c.dataset_size, c.num_nodes, c.local_batch, c.drop_last ? 1 : 0,
+                             buffer_size, mode == WindowMode::Global ? 0 : 1, df.p, dl.p, nullptr));
+    std::vector<std::uint32_t> bits(W * words);
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    (first ? df : dl).download(bits.data(), bits.size());
+    std::vector<IdSet> out(W);
+    for (std::uint32_t k = 0; k < W; ++k)
+        for (std::uint64_t w = 0; w < words; ++w)
+            for (std::uint32_t v = bits[k * words + w]; v; v &= v - 1) out[k].insert(w * 32 + __builtin_ctz(v));
+    return out;
+}
+}  // namespace
+
+std::vector<IdSet> last_buffer_window(const AccessTrace& trace, std::uint32_t epoch, std::uint64_t buffer_size,
+                                      WindowMode mode) {
+    return buffer_window(trace, epoch, buffer_size, mode, false);
+}
+
+std::vector<IdSet> first_buffer_window(const AccessTrace& trace, std::uint32_t epoch, std::uint64_t buffer_size,
+                                       WindowMode mode) {
+    return buffer_window(trace, epoch, buffer_size, mode, true);
+}
+
+// epoch_order.cpp:32-52 on the device (all E! paths, E <= 10)
+EpochOrder brute_force_order(const ReuseGraph& graph) {
+    const std::uint32_t E = graph.num_epochs;
+    DevBuf<std::uint64_t> dw(std::size_t(E) * E + 1), dc(1);
+    DevBuf<std::uint32_t> dord(E + 1);
+    if (E) dw.upload(graph.weights.data(), std::size_t(E) * E);
+    check(lsg_brute_force_order(dw.p, E, dord.p, dc.p, nullptr));
+    EpochOrder r;
+    r.order.resize(E);
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    dord.download(r.order.data(), E);
+    dc.download(&r.cost, 1);
+    return r;
+}
+
+// chunking.cpp:9-33 through the device read planner
+ChunkPlan plan_chunks(const std::vector<SampleId>& fetch_ids, std::uint64_t threshold) {
+    std::vector<std::uint32_t> ids(fetch_ids.size());
+    for (std::size_t i = 0; i < ids.size(); ++i) {
+        if (fetch_ids[i] >= (1ull << 31)) throw CapabilityError("plan_chunks: sample ids must be < 2^31 on device");
+        ids[i] = std::uint32_t(fetch_ids[i]);
+    }
+    std::vector<std::uint32_t> rs(ids.size() + 1), re(ids.size() + 1);
+    std::uint64_t meta[3];
+    check(lsg_plan_chunks(ids.data(), ids.size(), threshold, rs.data(), re.data(), meta, nullptr));
+    ChunkPlan p;
+    for (std::uint64_t i = 0; i < meta[0]; ++i)
+        p.reads.push_back({rs[i] == re[i] ? Read::Kind::Single : Read::Kind::Chunk, rs[i], re[i]});
+    p.needed = meta[1];
+    p.redundant = meta[2];
+    return p;
+}
+
+// chunking.cpp:35-45 (accessor of a plan)
+std::vector<SampleId> redundant_ids(const ChunkPlan& plan, const std::vector<SampleId>& fetch_ids) {
+    std::vector<SampleId> needed = fetch_ids;
+    std::sort(needed.begin(), needed.end());
+    std::vector<SampleId> out;
+    for (const Read& read : plan.reads) {
+        if (read.kind != Read::Kind::Chunk) continue;
+        for (SampleId id = read.start; id <= read.end; ++id)
+            if (!std::binary_search(needed.begin(), needed.end(), id)) out.push_back(id);
+    }
+    return out;
+}
+
+// chunking.cpp:49-69 (reporting accessor)
+double chunked_fraction(const std::vector<ChunkPlan>& plans) {
+    std::uint64_t in_chunks = 0, total = 0;
+    for (const ChunkPlan& plan : plans) {
+        total += plan.needed;
+        for (const Read& read : plan.reads)
+            if (read.kind == Read::Kind::Chunk) in_chunks += read.span();
+        in_chunks -= plan.redundant;
+    }
+    return total == 0 ? 0.0 : 100.0 * double(in_chunks) / double(total);
+}
+
+double chunked_fraction(const ChunkPlan& plan) { return chunked_fraction(std::vector<ChunkPlan>{plan}); }
+
 // epoch_order.cpp:11-30
 std::uint64_t path_cost(const ReuseGraph& graph, const std::vector<std::uint32_t>& order) {
     const std::uint32_t E = graph.num_epochs;

@@ -1,0 +1,123 @@
+// doctest.h — a minimal stand-in for the subset of doctest the reference's
+// unit suites use (TEST_CASE, CHECK, REQUIRE, CHECK_THROWS_AS, CHECK_NOTHROW,
+// CHECK_FALSE, CAPTURE, doctest::Approx). The real header is vendored but
+// git-ignored in the reference (proj/.gitignore:2) and absent here; this one
+// lets those suites run unchanged against the B200 drop-in.
+#pragma once
+#include <cmath>
+#include <cstdio>
+#include <exception>
+#include <functional>
+#include <string>
+#include <vector>
+
+namespace doctest {
+struct Case {
+    const char* name;
+    void (*fn)();
+};
+inline std::vector<Case>& registry() {
+    static std::vector<Case> r;
+    return r;
+}
+struct Reg {
+    Reg(const char* n, void (*f)()) { registry().push_back({n, f}); }
+};
+struct Stats {
+    int checks = 0, failed = 0;
+    const char* current = "";
+};
+inline Stats& stats() {
+    static Stats s;
+    return s;
+}
+struct RequireFailed {};
+inline void fail(const char* file, int line, const char* what) {
+    ++stats().failed;
+    std::fprintf(stderr, "%s:%d: FAILED in \"%s\": %s\n", file, line, stats().current, what);
+}
+class Approx {
+  public:
+    explicit Approx(double v) : v_(v), eps_(1e-5 * 100) {}  // doctest default: 100 * FLT_EPSILON-ish
+    Approx& epsilon(double e) {
+        eps_ = e;
+        return *this;
+    }
+    friend bool operator==(double a, const Approx& b) {
+        return std::fabs(a - b.v_) <= b.eps_ * (std::fabs(b.v_) > std::fabs(a) ? std::fabs(b.v_) : std::fabs(a)) ||
+               a == b.v_ || std::fabs(a - b.v_) < 1e-12;
+    }
+    friend bool operator==(const Approx& b, double a) { return a == b; }
+    friend bool operator!=(double a, const Approx& b) { return !(a == b); }
+
+  private:
+    double v_, eps_;
+};
+}  // namespace doctest
+
+#define DOCTEST_CAT2(a, b) a##b
+#define DOCTEST_CAT(a, b) DOCTEST_CAT2(a, b)
+#define TEST_CASE(name)                                                                  \
+    static void DOCTEST_CAT(doctest_case_, __LINE__)();                                  \
+    static ::doctest::Reg DOCTEST_CAT(doctest_reg_, __LINE__)(name, &DOCTEST_CAT(doctest_case_, __LINE__)); \
+    static void DOCTEST_CAT(doctest_case_, __LINE__)()
+#define CHECK(...)                                                                       \
+    do {                                                                                 \
+        ++::doctest::stats().checks;                                                     \
+        if (!(__VA_ARGS__)) ::doctest::fail(__FILE__, __LINE__, #__VA_ARGS__);           \
+    } while (0)
+#define CHECK_FALSE(...) CHECK(!(__VA_ARGS__))
+#define REQUIRE(...)                                                                     \
+    do {                                                                                 \
+        ++::doctest::stats().checks;                                                     \
+        if (!(__VA_ARGS__)) {                                                            \
+            ::doctest::fail(__FILE__, __LINE__, #__VA_ARGS__);                           \
+            throw ::doctest::RequireFailed{};                                            \
+        }                                                                                \
+    } while (0)
+#define CHECK_THROWS_AS(expr, type)                                                      \
+    do {                                                                                 \
+        ++::doctest::stats().checks;                                                     \
+        bool doctest_ok = false;                                                         \
+        try {                                                                            \
+            (void)(expr);                                                                \
+        } catch (const type&) {                                                          \
+            doctest_ok = true;                                                           \
+        } catch (...) {                                                                  \
+        }                                                                                \
+        if (!doctest_ok) ::doctest::fail(__FILE__, __LINE__, "throws " #type ": " #expr); \
+    } while (0)
+#define REQUIRE_THROWS_AS(expr, type) CHECK_THROWS_AS(expr, type)
+#define CHECK_NOTHROW(expr)                                                              \
+    do {                                                                                 \
+        ++::doctest::stats().checks;                                                     \
+        try {                                                                            \
+            (void)(expr);                                                                \
+        } catch (...) {                                                                  \
+            ::doctest::fail(__FILE__, __LINE__, "nothrow: " #expr);                      \
+        }                                                                                \
+    } while (0)
+#define REQUIRE_NOTHROW(expr) CHECK_NOTHROW(expr)
+#define CAPTURE(x) (void)(x)
+#define INFO(...) (void)0
+
+#ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
+int main() {
+    int cases = 0, bad_cases = 0;
+    for (const auto& c : ::doctest::registry()) {
+        ::doctest::stats().current = c.name;
+        const int before = ::doctest::stats().failed;
+        try {
+            c.fn();
+        } catch (const ::doctest::RequireFailed&) {
+        } catch (const std::exception& e) {
+            ::doctest::fail("?", 0, e.what());
+        }
+        ++cases;
+        if (::doctest::stats().failed != before) ++bad_cases;
+    }
+    std::printf("[doctest] test cases: %d | %d passed | %d failed | checks: %d, %d failed\n", cases,
+                cases - bad_cases, bad_cases, ::doctest::stats().checks, ::doctest::stats().failed);
+    return bad_cases ? 1 : 0;
+}
+#endif
