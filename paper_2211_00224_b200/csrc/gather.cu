@@ -143,6 +143,8 @@ struct StepFetch {
     uint4* const* outs;        // [k1-k0] batch tensors
     uint32_t k0, k1;
     uint64_t vec_per_row, tiles_per_row, seed;
+    uint32_t* mlist;           // miss rows of the step (filled by the TMA hit kernel) or null
+    uint32_t* mctl;            // [2] miss count, finished misses blocks
 };
 
 __device__ __forceinline__ uint32_t node_of_row(const StepFetch& f, uint32_t r) {
@@ -222,6 +224,9 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
                               : nullptr;
                 dst_row = reinterpret_cast<unsigned char*>(f.outs[kk - f.k0]) +
                           uint64_t(r - __ldg(&f.node_off[kk])) * row_bytes;
+                // a miss row goes on the misses kernel's list, once: by the
+                // CTA whose tile range holds the row's first tile
+                if (!hit && f.mlist && rr * tpr >= tb) f.mlist[atomicAdd(&f.mctl[0], 1u)] = r;
             }
             if (src_row) break;
             tn = (rr + 1) * tpr;  // a miss row: the misses kernel writes it
@@ -259,10 +264,16 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Misses of the step: with the TMA hit kernel's list (mlist) only the miss
+// rows are visited (a small fixed grid; the last block to finish resets the
+// list for the next step), else every row of the step is scanned.
 __global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
     const uint32_t r0 = __ldg(&f.node_off[f.k0]), r1 = __ldg(&f.node_off[f.k1]);
     const uint64_t pairs = f.vec_per_row;  // 16-byte pairs of payload words
-    for (uint32_t r = r0 + blockIdx.y; r < r1; r += gridDim.y) {
+    const uint32_t nlist = f.mlist ? __ldcg(&f.mctl[0]) : 0u;
+    const uint32_t n = f.mlist ? nlist : r1 - r0;
+    for (uint32_t m = blockIdx.y; m < n; m += gridDim.y) {
+        const uint32_t r = f.mlist ? __ldcg(&f.mlist[m]) : r0 + m;
         const uint32_t sl = __ldg(&f.slots[r]);
         if (sl != kNever && (sl & kHit)) continue;
         const uint32_t k = node_of_row(f, r);
@@ -278,11 +289,49 @@ __global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
             if (buf) __stcs(&buf[p], v);
         }
     }
+    if (f.mlist) {  // every block has read the count: the last one resets the list
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const uint32_t ticket = atomicAdd(&f.mctl[1], 1u);
+            if (ticket == gridDim.x * gridDim.y - 1) {
+                f.mctl[0] = 0;
+                f.mctl[1] = 0;
+            }
+        }
+    }
+}
+
+// per-device miss-row list of the step fetch (grown on demand; the counters
+// are zero between steps)
+struct MissList {
+    uint32_t* buf = nullptr;  // [2 + cap]
+    uint64_t cap = 0;
+};
+
+int miss_list(uint64_t rows, cudaStream_t st, uint32_t** list, uint32_t** ctl) {
+    static MissList ml[64];
+    int dev = 0;
+    LSG_CUDA(cudaGetDevice(&dev));
+    MissList& m = ml[dev & 63];
+    if (m.cap < rows) {
+        if (m.buf) {
+            LSG_CUDA(cudaDeviceSynchronize());
+            cudaFree(m.buf);
+        }
+        m.cap = std::max<uint64_t>(rows, 4096);
+        LSG_CUDA(cudaMalloc(&m.buf, (m.cap + 2) * 4));
+        LSG_CUDA(cudaMemsetAsync(m.buf, 0, 8, st));
+    }
+    *ctl = m.buf;
+    *list = m.buf + 2;
+    return kOk;
 }
 
 // TMA gather when rows are whole tiles (LSG_GATHER_LSU=1 keeps the 128-bit
 // load/store kernel, for comparison)
-int launch_hits(const StepFetch& f, uint64_t rows, uint64_t sample_bytes, cudaStream_t st) {
+int launch_hits(const StepFetch& f, uint64_t rows, uint64_t sample_bytes, cudaStream_t st, bool* tma = nullptr) {
+    if (tma) *tma = false;
     static const bool lsu = [] {
         const char* e = std::getenv("LSG_GATHER_LSU");
         return e && e[0] == '1';
@@ -301,6 +350,7 @@ int launch_hits(const StepFetch& f, uint64_t rows, uint64_t sample_bytes, cudaSt
         const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 148ull * 2)));
         k_fetch_step_hits_tma<<<grid, 32, smem, st>>>(f);
         LSG_LAUNCH_CHECK("k_fetch_step_hits_tma");
+        if (tma) *tma = true;
         return kOk;
     }
     const unsigned grid = unsigned(std::min<uint64_t>(rows * f.tiles_per_row, 148ull * 8));
@@ -328,12 +378,19 @@ int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* 
     f.vec_per_row = sample_bytes / 16;
     f.tiles_per_row = (f.vec_per_row + kTileVec - 1) / kTileVec;
     f.seed = seed;
+    f.mlist = nullptr;
+    f.mctl = nullptr;
     const uint64_t rows = rows_hint ? rows_hint : 1;
-    if (int rc = launch_hits(f, rows, sample_bytes, st)) return rc;
+    // with a row count the TMA kernel lists the step's miss rows
+    if (rows_hint && sample_bytes % kTmaTile == 0)
+        if (int rc = miss_list(rows_hint, st, &f.mlist, &f.mctl)) return rc;
+    bool tma = false;
+    if (int rc = launch_hits(f, rows, sample_bytes, st, &tma)) return rc;
+    if (!tma) f.mlist = f.mctl = nullptr;
     // each miss row is spread over up to 256 blocks (a 16 MiB row is 1 Mi
-    // 16-byte pairs); rows are strided over grid.y
+    // 16-byte pairs); listed miss rows over grid.y = 148, else every row
     dim3 g2(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 256)),
-            unsigned(std::min<uint64_t>(std::max<uint64_t>(rows, 1), 1024)));
+            unsigned(f.mlist ? std::min<uint64_t>(rows, 148) : std::min<uint64_t>(std::max<uint64_t>(rows, 1), 1024)));
     k_fetch_step_misses<<<g2, 256, 0, st>>>(f);
     LSG_LAUNCH_CHECK("k_fetch_step_misses");
     return kOk;
@@ -355,6 +412,8 @@ int gather_step_hits_device(void* const* d_bufs, void* const* d_outs, const uint
     f.k1 = k1;
     f.vec_per_row = sample_bytes / 16;
     f.tiles_per_row = (f.vec_per_row + kTileVec - 1) / kTileVec;
+    f.mlist = nullptr;
+    f.mctl = nullptr;
     const uint64_t rows = rows_hint ? rows_hint : 1;
     return launch_hits(f, rows, sample_bytes, st);
 }
