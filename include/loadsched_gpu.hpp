@@ -208,12 +208,42 @@ struct SchedulePlan {
 
 bool same_multiset(const StepAssignment& step, const std::vector<SampleId>& batch);
 
+// ---- locality.hpp:23-39 / balance.hpp:13-32: one step against explicit
+// residency sets, on the device (lsg_remap_step / lsg_balance_step)
+StepAssignment remap_step(const std::vector<const IdSet*>& buffers, const std::vector<SampleId>& batch,
+                          std::uint64_t local_batch);
+std::vector<StepAssignment> remap_epoch(const std::vector<IdSet>& prev_buffers,
+                                        const std::vector<std::vector<SampleId>>& epoch_batches,
+                                        std::uint64_t local_batch);
+StepAssignment slice_step(const std::vector<const IdSet*>& buffers, const std::vector<SampleId>& batch,
+                          std::uint64_t local_batch);
+std::uint64_t balance_step(StepAssignment& step);
+
+struct CostModel {  // cost_model.hpp:13-16
+    double seek_cost = 13.0;
+    double stream_cost = 1.0;
+};
+double barrier_time(const StepAssignment& step, const CostModel& model);
+struct StepSizes {
+    std::uint32_t epoch = 0;
+    std::uint64_t step = 0;
+    std::vector<std::uint64_t> sizes;
+    double stddev = 0.0;
+};
+// host reporting helper over a finished plan (balance.cpp:52-72)
+std::vector<StepSizes> batch_size_stats(const SchedulePlan& plan);
+
 // ---- chunking.hpp:23-39: plan_chunks runs the device read planner on one
 // list; redundant_ids / chunked_fraction are host-side accessors of a plan
 ChunkPlan plan_chunks(const std::vector<SampleId>& fetch_ids, std::uint64_t threshold);
 std::vector<SampleId> redundant_ids(const ChunkPlan& plan, const std::vector<SampleId>& fetch_ids);
 double chunked_fraction(const ChunkPlan& plan);
 double chunked_fraction(const std::vector<ChunkPlan>& plans);
+// cost_model.hpp:24-27, 45-48: host formulas that price a read plan and set
+// the chunk threshold the device read planner uses
+double read_cost(const ChunkPlan& plan, const CostModel& model);
+double read_cost(const std::vector<Read>& reads, const CostModel& model);
+std::uint64_t derive_threshold(const CostModel& model, std::uint64_t max_threshold);
 
 // ---- buffer.hpp:16-118 (simulation results) --------------------------------
 enum class Policy { Clairvoyant, Lru };

@@ -222,6 +222,16 @@ int lsg_buffer_windows(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64
 /* brute_force_order (epoch_order.cpp:32-52): exact minimum over all E! open
  * paths, ties to the lexicographically smallest order; E <= 10. */
 int lsg_brute_force_order(const uint64_t* d_w, uint32_t E, uint32_t* d_order, uint64_t* d_cost, void* stream);
+/* remap_step / slice_step (locality.cpp:7-73, slice != 0) of one batch
+ * against explicit residency sets (node k holds h_res_ids[h_res_off[k] ..
+ * h_res_off[k+1])): node lists into h_items (len, id | LSG_HIT_BIT) at
+ * h_node_off[N+1]. Runs the cluster step loop for one step, no advance. */
+int lsg_remap_step(const uint64_t* h_res_off, const uint32_t* h_res_ids, uint32_t N, const uint32_t* h_batch,
+                   uint64_t len, uint64_t local_batch, int32_t slice, uint32_t* h_items, uint32_t* h_node_off,
+                   void* stream);
+/* balance_step (balance.cpp:10-39) of one step's lists, in place; *h_moves
+ * receives the number of moves. */
+int lsg_balance_step(uint32_t* h_items, uint32_t* h_node_off, uint32_t N, uint64_t* h_moves, void* stream);
 /* plan_chunks (chunking.cpp:9-33) of one host fetch list: reads into h_start /
  * h_end (capacity n; start == end: Single), h_meta = {reads, needed, redundant}. */
 int lsg_plan_chunks(const uint32_t* h_ids, uint64_t n, uint64_t threshold, uint32_t* h_start, uint32_t* h_end,

@@ -91,6 +91,7 @@ EXPORTS = [
     "lsg_store_create", "lsg_store_open", "lsg_store_info", "lsg_store_close", "lsg_store_read",
     "lsg_store_read_rows", "lsg_fetch_step_store", "lsg_simulate_ex", "lsg_format_trace", "lsg_format_plan",
     "lsg_format_graph", "lsg_parse_trace", "lsg_parse_graph", "lsg_parse_plan", "lsg_free_plan",
+    "lsg_buffer_windows", "lsg_brute_force_order", "lsg_remap_step", "lsg_balance_step", "lsg_plan_chunks",
 ]
 
 
@@ -134,6 +135,11 @@ def lib() -> ctypes.CDLL:
         L.lsg_parse_graph.argtypes = [ctypes.c_char_p, u64, P, P, u64]
         L.lsg_parse_plan.argtypes = [ctypes.c_char_p, u64, P, P]
         L.lsg_free_plan.argtypes = [P]
+        L.lsg_buffer_windows.argtypes = [P, u32, u64, u64, u32, u64, i32, u64, i32, P, P, P]
+        L.lsg_brute_force_order.argtypes = [P, u32, P, P, P]
+        L.lsg_remap_step.argtypes = [P, P, u32, P, u64, u64, i32, P, P, P]
+        L.lsg_balance_step.argtypes = [P, P, u32, P, P]
+        L.lsg_plan_chunks.argtypes = [P, u64, u64, P, P, P, P]
         L.lsg_free_plan.restype = None
         L.lsg_store_fill.argtypes = [P, u64, u64, u64, P, P]
         L.lsg_gather.argtypes = [P, P, u64, u64, P, P]

@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
 int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int balance, int insred, uint64_t thr,
                      const uint32_t* d_trace, const uint32_t* d_order, const uint32_t* d_inv, const uint32_t* d_nu,
                      uint32_t* d_items, uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
-                     cudaStream_t st);
+                     cudaStream_t st, const uint32_t* d_hm_init = nullptr, int advance = 1);
 
 int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int balance, int insred, uint64_t thr,
                      const uint32_t* d_trace,

@@ -62,6 +62,7 @@ struct WideArgs {
     uint32_t MBW;                     // moved-flag words per node
     int remap, balance, lru;
     int insred;                       // chunk_insert_redundant (pipeline.cpp:103-114)
+    int advance;                      // 0: assignment only (remap_step / slice_step per call)
     uint32_t thr;                     // chunk threshold
     uint32_t E;
     const uint32_t* inv;              // [E][D] position of id in epoch e's trace, kNone if not kept
@@ -1271,7 +1272,7 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
         // of the (size - C)+ largest). Records are prefetched a chunk ahead;
         // a resident's slot is read once per chunk and re-read only after an
         // eviction in the same chunk (compaction may have moved it).
-        for (uint32_t k = tg; k < N; k += NT) {
+        for (uint32_t k = tg; k < N && a.advance; k += NT) {
             if (tm.wr != 0) {  // helper warp: join the leader's eviction scans
                 for (;;) {
                     tm.sync();
@@ -1397,12 +1398,145 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
         for (int q = 0; q < 7; ++q) a.prof[q] = pacc[q];
 }
 
+// ---- balance_step (balance.cpp:10-39) on one step's lists, one CTA: the
+// closed-form move table of wide_balance_cf, then the donors' q-th largest
+// fetch ids (first occurrence on equal ids, balance.cpp:27-30) move to their
+// recipients' tails; everything else keeps its order.
+struct BalArgs {
+    const uint32_t* items;  // [total] id | hit
+    const uint32_t* off;    // [N+1]
+    uint32_t* out;          // [total]
+    uint32_t* out_off;      // [N+1]
+    uint32_t* moved;        // [total] scratch flags, zero
+    unsigned long long* moves;
+    uint32_t N, Lmax;
+};
+
+__global__ void __launch_bounds__(kWT, 1) k_balance_lists(BalArgs b, WideArgs a) {
+    extern __shared__ __align__(16) unsigned char bsm[];
+    unsigned long long* sortb = reinterpret_cast<unsigned long long*>(bsm);  // [kWW][kSortCap]
+    uint32_t* lv = reinterpret_cast<uint32_t*>(sortb + kWW * kSortCap);     // [4 * kLevCap]
+    uint32_t* fcnt = lv + 4 * kLevCap;
+    uint32_t* outk = fcnt + b.N;
+    uint32_t* ink = outk + b.N;
+    uint32_t* rl = ink + b.N;
+    uint32_t* rl2 = rl + b.N;
+    uint32_t* lenpre = rl2 + b.N;
+    uint32_t* lenfin = lenpre + b.N;
+    uint32_t* noff = lenfin + b.N;  // [N+1]
+    __shared__ uint32_t bsc[8];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5, N = b.N;
+    const uint32_t lt = lanemask_lt_w();
+    for (uint32_t k = w; k < N; k += kWW) {
+        const uint32_t lo = b.off[k], hi = b.off[k + 1];
+        uint32_t f = 0;
+        for (uint32_t p = lo + lane; p < hi; p += 32) f += !(b.items[p] & kHitM);
+        f = __reduce_add_sync(0xFFFFFFFFu, f);
+        if (lane == 0) {
+            fcnt[k] = f;
+            lenpre[k] = hi - lo;
+        }
+    }
+    __syncthreads();
+    wide_balance_cf(a, N, b.Lmax, fcnt, outk, ink, lv, bsc, rl, rl2, true, tid, lane, w);
+    if (w == 0) {
+        for (uint32_t k = lane; k < N; k += 32) lenfin[k] = lenpre[k] - outk[k] + ink[k];
+        __syncwarp();
+        warp_prefix(lenfin, noff, N, lane);
+    }
+    __syncthreads();
+    unsigned long long* my_sort = sortb + w * kSortCap;
+    unsigned long long mv = 0;
+    for (uint32_t k = w; k < N; k += kWW) {
+        const uint32_t lo = b.off[k], lp = lenpre[k], nout = outk[k];
+        mv += nout;
+        auto move_one = [&](uint32_t q, uint32_t p) {
+            b.moved[lo + p] = 1;
+            const uint32_t rec = __ldcg(&a.recv[size_t(k) * b.Lmax + q]);
+            const uint32_t r = rec & 0x3FFu, ii = rec >> 10;
+            b.out[noff[r] + lenpre[r] + ii] = b.items[lo + p];
+        };
+        if (nout) {
+            const bool fits = fcnt[k] <= kSortCap;
+            uint32_t nf = 0;
+            for (uint32_t p0 = 0; p0 < lp; p0 += 32) {
+                const uint32_t p = p0 + lane;
+                const uint32_t it = p < lp ? b.items[lo + p] : kHitM;
+                const bool isf = !(it & kHitM);
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, isf);
+                // (id desc, position asc): the largest id, first occurrence
+                if (isf && fits)
+                    my_sort[nf + __popc(bal & lt)] = (static_cast<unsigned long long>(it) << 32) | (0xFFFFFFFFu - p);
+                nf += __popc(bal);
+            }
+            if (fits) {
+                uint32_t P2 = 1;
+                while (P2 < nf) P2 <<= 1;
+                for (uint32_t q = nf + lane; q < P2; q += 32) my_sort[q] = 0ull;
+                __syncwarp();
+                for (uint32_t sz = 2; sz <= P2; sz <<= 1)
+                    for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+                        for (uint32_t r = lane; r < P2 / 2; r += 32) {
+                            const uint32_t x0 = 2 * st * (r / st) + (r % st), x1 = x0 + st;
+                            const bool desc = (x0 & sz) == 0;
+                            const unsigned long long u = my_sort[x0], v = my_sort[x1];
+                            if ((u < v) == desc) {
+                                my_sort[x0] = v;
+                                my_sort[x1] = u;
+                            }
+                        }
+                        __syncwarp();
+                    }
+                for (uint32_t q = lane; q < nout; q += 32) move_one(q, 0xFFFFFFFFu - uint32_t(my_sort[q]));
+            } else {
+                for (uint32_t q = 0; q < nout; ++q) {
+                    unsigned long long best = 0;
+                    for (uint32_t p = lane; p < lp; p += 32) {
+                        const uint32_t it = b.items[lo + p];
+                        if (!(it & kHitM) && !__ldcg(&b.moved[lo + p]))
+                            best = max(best, (static_cast<unsigned long long>(it + 1ull) << 32) | (0xFFFFFFFFu - p));
+                    }
+#pragma unroll
+                    for (int d = 16; d > 0; d >>= 1) best = max(best, __shfl_xor_sync(0xFFFFFFFFu, best, d));
+                    if (lane == 0) move_one(q, 0xFFFFFFFFu - uint32_t(best));
+                    __syncwarp();
+                }
+            }
+            __syncwarp();
+        }
+        uint32_t kept = 0;
+        for (uint32_t p0 = 0; p0 < lp; p0 += 32) {
+            const uint32_t p = p0 + lane;
+            const bool keep = p < lp && !(nout && __ldcg(&b.moved[lo + p]));
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, keep);
+            if (keep) b.out[noff[k] + kept + __popc(bal & lt)] = b.items[lo + p];
+            kept += __popc(bal);
+        }
+    }
+    if (lane == 0 && mv) atomicAdd(b.moves, mv);
+    for (uint32_t k = tid; k <= N; k += kWT) b.out_off[k] = noff[k];
+}
+
+__global__ void k_set_holders(const unsigned long long* __restrict__ roff, const uint32_t* __restrict__ ids,
+                              uint32_t N, uint32_t W, uint32_t* __restrict__ hm) {
+    const uint64_t total = roff[N];
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint32_t l0 = 0, l1 = N;  // node k of entry i: first k with roff[k+1] > i
+        while (l0 < l1) {
+            const uint32_t mid = (l0 + l1) >> 1;
+            if (roff[mid + 1] > i) l1 = mid; else l0 = mid + 1;
+        }
+        atomicOr(&hm[size_t(ids[i]) * W + (l0 >> 5)], 1u << (l0 & 31));
+    }
+}
+
 }  // namespace
 
 int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int balance, int insred, uint64_t thr,
                      const uint32_t* d_trace, const uint32_t* d_order, const uint32_t* d_inv, const uint32_t* d_nu,
                      uint32_t* d_items, uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
-                     cudaStream_t st) {
+                     cudaStream_t st, const uint32_t* d_hm_init, int advance) {
     if (insred && lru)
         return set_error(kCapability, "plan: chunk_insert_redundant with the LRU policy is not on the device path");
     if (dm.N > kWMaxN)
@@ -1471,7 +1605,9 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int bal
         !a.jx || !a.jnu || !a.jmask || !a.jcls || !a.jS || !a.pre || !a.fx || !a.fnu || !a.mj || !a.mpo || !a.mhc ||
         !a.pairs || !a.massign || !a.mpos || !a.recv || !a.ur)
         return set_error(kInternal, "plan: wide planner scratch allocation failed");
-    LSG_CUDA(cudaMemsetAsync(a.hm, 0, size_t(dm.D) * W * 4, st));
+    if (d_hm_init) LSG_CUDA(cudaMemcpyAsync(a.hm, d_hm_init, size_t(dm.D) * W * 4, cudaMemcpyDeviceToDevice, st));
+    else LSG_CUDA(cudaMemsetAsync(a.hm, 0, size_t(dm.D) * W * 4, st));
+    a.advance = advance;
     LSG_CUDA(cudaMemsetAsync(a.where, 0xFF, size_t(N) * dm.D * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.cnt, 0, size_t(N) * (dm.T + 1) * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.nst, 0, size_t(N) * 32, st));
@@ -1534,3 +1670,122 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int bal
 }
 
 }  // namespace lsg
+
+using namespace lsg;
+
+extern "C" {
+
+// remap_step / slice_step (locality.cpp:7-73) of one batch against explicit
+// residency sets: node k holds h_res_ids[h_res_off[k] .. h_res_off[k+1]).
+// The cluster step loop runs one step without a buffer advance.
+int lsg_remap_step(const uint64_t* h_res_off, const uint32_t* h_res_ids, uint32_t N, const uint32_t* h_batch,
+                   uint64_t len, uint64_t local_batch, int32_t slice, uint32_t* h_items, uint32_t* h_node_off,
+                   void* stream) {
+    const char* who = slice ? "slice_step" : "remap_step";
+    if (N == 0) return set_error(kValidation, std::string(who) + ": no nodes");
+    if (local_batch == 0) return set_error(kValidation, std::string(who) + ": local_batch must be >= 1");
+    if (len > uint64_t(N) * local_batch)
+        return set_error(kValidation, std::string(who) + ": batch larger than N * local_batch");
+    if (N > kWMaxN) return set_error(kCapability, std::string(who) + ": num_nodes <= 256 on the device");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    uint64_t D = 1;
+    for (uint64_t i = 0; i < len; ++i) D = std::max<uint64_t>(D, uint64_t(h_batch[i]) + 1);
+    const uint64_t nres = h_res_off[N];
+    for (uint64_t i = 0; i < nres; ++i) D = std::max<uint64_t>(D, uint64_t(h_res_ids[i]) + 1);
+    if (D >= (1ull << 31)) return set_error(kCapability, std::string(who) + ": sample ids must be < 2^31 on device");
+    for (uint32_t k = 0; k < N; ++k)
+        if (h_res_off[k + 1] < h_res_off[k]) return set_error(kValidation, std::string(who) + ": bad residency offsets");
+    h_node_off[0] = 0;
+    if (len == 0) {
+        for (uint32_t k = 0; k <= N; ++k) h_node_off[k] = 0;
+        return kOk;
+    }
+    const uint32_t W = (N + 31) / 32;
+    Scratch sc(st);
+    uint32_t* hm = sc.get<uint32_t>(size_t(D) * W);
+    unsigned long long* roff = sc.get<unsigned long long>(N + 1);
+    uint32_t* rid = sc.get<uint32_t>(nres + 1);
+    uint32_t* trace = sc.get<uint32_t>(len);
+    uint32_t* order = sc.get<uint32_t>(1);
+    uint32_t* nu = sc.get<uint32_t>(len);
+    uint32_t* items = sc.get<uint32_t>(len);
+    uint32_t* off = sc.get<uint32_t>(N + 1);
+    uint32_t* status = sc.get<uint32_t>(1);
+    if (!hm || !roff || !rid || !trace || !order || !nu || !items || !off || !status)
+        return set_error(kInternal, "remap_step: scratch allocation failed");
+    LSG_CUDA(cudaMemsetAsync(hm, 0, size_t(D) * W * 4, st));
+    LSG_CUDA(cudaMemsetAsync(order, 0, 4, st));
+    LSG_CUDA(cudaMemsetAsync(nu, 0xFF, len * 4, st));
+    LSG_CUDA(cudaMemsetAsync(status, 0, 4, st));
+    LSG_CUDA(cudaMemcpyAsync(roff, h_res_off, (N + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (nres) LSG_CUDA(cudaMemcpyAsync(rid, h_res_ids, nres * 4, cudaMemcpyHostToDevice, st));
+    LSG_CUDA(cudaMemcpyAsync(trace, h_batch, len * 4, cudaMemcpyHostToDevice, st));
+    if (nres) {
+        k_set_holders<<<grid_for(nres, 256, 1184), 256, 0, st>>>(roff, rid, N, W, hm);
+        LSG_LAUNCH_CHECK("k_set_holders");
+    }
+    PlanDims dm{D, uint64_t(N) * local_batch, 1, len, 1, N, 1, uint32_t(local_batch)};
+    if (int rc = plan_wide_device(dm, 1, 0, slice ? 0 : 1, 0, 0, 1, trace, order, nullptr, nu, items, off, nullptr,
+                                  nullptr, status, st, hm, 0))
+        return rc;
+    uint32_t h = 0;
+    LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaMemcpyAsync(h_items, items, len * 4, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaMemcpyAsync(h_node_off, off, (N + 1) * 4, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaStreamSynchronize(st));
+    if (h & 64u) return set_error(kInternal, "remap_step: ran out of capacity");
+    if (h) return set_error(kInternal, std::string(who) + ": device invariant violated");
+    return kOk;
+}
+
+// balance_step (balance.cpp:10-39) on one step's lists (in place).
+int lsg_balance_step(uint32_t* h_items, uint32_t* h_node_off, uint32_t N, uint64_t* h_moves, void* stream) {
+    if (N == 0) return set_error(kValidation, "balance_step: no nodes");
+    if (N > kWMaxN) return set_error(kCapability, "balance_step: num_nodes <= 256 on the device");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t total = h_node_off[N];
+    uint32_t Lmax = 1;
+    for (uint32_t k = 0; k < N; ++k) {
+        if (h_node_off[k + 1] < h_node_off[k]) return set_error(kValidation, "balance_step: bad offsets");
+        Lmax = std::max<uint32_t>(Lmax, h_node_off[k + 1] - h_node_off[k]);
+    }
+    if (total >= (1ull << 31)) return set_error(kCapability, "balance_step: step too large for the device");
+    Scratch sc(st);
+    uint32_t* items = sc.get<uint32_t>(total + 1);
+    uint32_t* out = sc.get<uint32_t>(total + 1);
+    uint32_t* off = sc.get<uint32_t>(N + 1);
+    uint32_t* out_off = sc.get<uint32_t>(N + 1);
+    uint32_t* moved = sc.get<uint32_t>(total + 1);
+    uint32_t* recv = sc.get<uint32_t>(size_t(N) * Lmax);
+    uint32_t* ur = sc.get<uint32_t>(total + 1);
+    uint32_t* status = sc.get<uint32_t>(1);
+    unsigned long long* moves = sc.get<unsigned long long>(1);
+    if (!items || !out || !off || !out_off || !moved || !recv || !ur || !status || !moves)
+        return set_error(kInternal, "balance_step: scratch allocation failed");
+    LSG_CUDA(cudaMemcpyAsync(items, h_items, total * 4, cudaMemcpyHostToDevice, st));
+    LSG_CUDA(cudaMemcpyAsync(off, h_node_off, (N + 1) * 4, cudaMemcpyHostToDevice, st));
+    LSG_CUDA(cudaMemsetAsync(moved, 0, (total + 1) * 4, st));
+    LSG_CUDA(cudaMemsetAsync(status, 0, 4, st));
+    LSG_CUDA(cudaMemsetAsync(moves, 0, 8, st));
+    BalArgs b{items, off, out, out_off, moved, moves, N, Lmax};
+    WideArgs a{};
+    a.recv = recv;
+    a.ur = ur;
+    a.status = status;
+    const size_t smem = size_t(kWW) * kSortCap * 8 + size_t(4) * kLevCap * 4 + (size_t(7) * N + N + 1) * 4;
+    LSG_CUDA(cudaFuncSetAttribute(k_balance_lists, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_balance_lists<<<1, kWT, smem, st>>>(b, a);
+    LSG_LAUNCH_CHECK("k_balance_lists");
+    uint32_t h = 0;
+    unsigned long long mv = 0;
+    LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaMemcpyAsync(&mv, moves, 8, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaMemcpyAsync(h_items, out, total * 4, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaMemcpyAsync(h_node_off, out_off, (N + 1) * 4, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaStreamSynchronize(st));
+    if (h) return set_error(kInternal, "balance_step: device invariant violated");
+    if (h_moves) *h_moves = mv;
+    return kOk;
+}
+
+}  // extern "C"

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <fstream>
 #include <sstream>
@@ -248,6 +249,133 @@ ChunkPlan plan_chunks(const std::vector<SampleId>& fetch_ids, std::uint64_t thre
     p.needed = meta[1];
     p.redundant = meta[2];
     return p;
+}
+
+namespace {
+
+StepAssignment step_from_lists(const std::vector<std::uint32_t>& items, const std::vector<std::uint32_t>& off,
+                               std::size_t N) {
+    StepAssignment step;
+    step.nodes.resize(N);
+    for (std::size_t k = 0; k < N; ++k)
+        for (std::uint32_t p = off[k]; p < off[k + 1]; ++p)
+            step.nodes[k].push_back({items[p] & ~LSG_HIT_BIT, (items[p] & LSG_HIT_BIT) ? Source::BufferHit : Source::PfsFetch});
+    return step;
+}
+
+StepAssignment locality_step(const std::vector<const IdSet*>& buffers, const std::vector<SampleId>& batch,
+                             std::uint64_t local_batch, bool slice) {
+    const char* who = slice ? "slice_step" : "remap_step";
+    const std::size_t N = buffers.size();
+    std::vector<std::uint64_t> roff(N + 1, 0);
+    std::vector<std::uint32_t> rids;
+    for (std::size_t k = 0; k < N; ++k) {
+        for (SampleId id : *buffers[k]) {
+            if (id >= (1ull << 31)) throw CapabilityError(std::string(who) + ": sample ids must be < 2^31 on device");
+            rids.push_back(std::uint32_t(id));
+        }
+        roff[k + 1] = rids.size();
+    }
+    std::vector<std::uint32_t> ids(batch.size());
+    for (std::size_t i = 0; i < batch.size(); ++i) {
+        if (batch[i] >= (1ull << 31)) throw CapabilityError(std::string(who) + ": sample ids must be < 2^31 on device");
+        ids[i] = std::uint32_t(batch[i]);
+    }
+    std::vector<std::uint32_t> items(ids.size() + 1), off(N + 1, 0);
+    check(lsg_remap_step(roff.data(), rids.data(), std::uint32_t(N), ids.data(), ids.size(), local_batch,
+                         slice ? 1 : 0, items.data(), off.data(), nullptr));
+    StepAssignment step = step_from_lists(items, off, N);
+    if (!slice && !same_multiset(step, batch)) throw InternalError("remap_step: assignment multiset mismatch");
+    return step;
+}
+
+}  // namespace
+
+// locality.cpp:7-39
+StepAssignment remap_step(const std::vector<const IdSet*>& buffers, const std::vector<SampleId>& batch,
+                          std::uint64_t local_batch) {
+    return locality_step(buffers, batch, local_batch, false);
+}
+
+// locality.cpp:41-54: every step against one fixed residency snapshot
+std::vector<StepAssignment> remap_epoch(const std::vector<IdSet>& prev_buffers,
+                                        const std::vector<std::vector<SampleId>>& epoch_batches,
+                                        std::uint64_t local_batch) {
+    std::vector<const IdSet*> views;
+    for (const IdSet& s : prev_buffers) views.push_back(&s);
+    std::vector<StepAssignment> out;
+    out.reserve(epoch_batches.size());
+    for (const auto& batch : epoch_batches) out.push_back(remap_step(views, batch, local_batch));
+    return out;
+}
+
+// locality.cpp:56-73
+StepAssignment slice_step(const std::vector<const IdSet*>& buffers, const std::vector<SampleId>& batch,
+                          std::uint64_t local_batch) {
+    return locality_step(buffers, batch, local_batch, true);
+}
+
+// balance.cpp:10-39
+std::uint64_t balance_step(StepAssignment& step) {
+    const std::size_t N = step.nodes.size();
+    if (N == 0) throw ValidationError("balance_step: no nodes");
+    std::vector<std::uint32_t> items, off(N + 1, 0);
+    for (std::size_t k = 0; k < N; ++k) {
+        for (const Assigned& a : step.nodes[k]) {
+            if (a.id >= (1ull << 31)) throw CapabilityError("balance_step: sample ids must be < 2^31 on device");
+            items.push_back(std::uint32_t(a.id) | (a.source == Source::BufferHit ? LSG_HIT_BIT : 0u));
+        }
+        off[k + 1] = std::uint32_t(items.size());
+    }
+    std::uint64_t moves = 0;
+    items.push_back(0);
+    check(lsg_balance_step(items.data(), off.data(), std::uint32_t(N), &moves, nullptr));
+    step = step_from_lists(items, off, N);
+    return moves;
+}
+
+// balance.cpp:41-49
+double barrier_time(const StepAssignment& step, const CostModel& model) {
+    const double per_fetch = model.seek_cost + model.stream_cost;
+    double worst = 0.0;
+    for (std::uint64_t c : step.fetch_counts()) worst = std::max(worst, double(c) * per_fetch);
+    return worst;
+}
+
+// balance.cpp:51-72
+std::vector<StepSizes> batch_size_stats(const SchedulePlan& plan) {
+    std::vector<StepSizes> out;
+    for (const EpochPlan& ep : plan.epochs)
+        for (std::size_t t = 0; t < ep.steps.size(); ++t) {
+            StepSizes row;
+            row.epoch = ep.epoch;
+            row.step = t;
+            for (const auto& list : ep.steps[t].assignment.nodes) row.sizes.push_back(list.size());
+            double mean = 0.0, var = 0.0;
+            for (std::uint64_t v : row.sizes) mean += double(v);
+            mean /= double(row.sizes.size());
+            for (std::uint64_t v : row.sizes) var += (double(v) - mean) * (double(v) - mean);
+            row.stddev = std::sqrt(var / double(row.sizes.size()));
+            out.push_back(std::move(row));
+        }
+    return out;
+}
+
+// cost_model.cpp:9-18
+double read_cost(const std::vector<Read>& reads, const CostModel& model) {
+    double cost = 0.0;
+    for (const Read& r : reads) cost += model.seek_cost + double(r.span()) * model.stream_cost;
+    return cost;
+}
+double read_cost(const ChunkPlan& plan, const CostModel& model) { return read_cost(plan.reads, model); }
+
+// cost_model.cpp:64-71: floor(seek / stream + 2), capped
+std::uint64_t derive_threshold(const CostModel& model, std::uint64_t max_threshold) {
+    if (model.seek_cost < 0.0 || model.stream_cost < 0.0)
+        throw ValidationError("derive_threshold: negative model parameters");
+    if (model.stream_cost == 0.0) return max_threshold;
+    const double bound = model.seek_cost / model.stream_cost + 2.0;
+    return bound >= double(max_threshold) ? max_threshold : std::uint64_t(std::floor(bound));
 }
 
 // chunking.cpp:35-45 (accessor of a plan)

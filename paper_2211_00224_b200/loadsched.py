@@ -12,6 +12,7 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -25,7 +26,8 @@ __all__ = [
     "STORE_HEADER_BYTES", "DEFAULT_STORE_BUDGET", "format_trace", "write_trace_file", "read_trace",
     "read_trace_file", "format_graph", "write_graph_file", "read_graph", "read_graph_file", "format_plan",
     "write_plan_file", "read_plan", "read_plan_file", "Error", "ConfigError", "ValidationError", "CapabilityError",
-    "StorageError", "InternalError", "HIT_BIT", "NEVER",
+    "StorageError", "InternalError", "HIT_BIT", "NEVER", "brute_force_order", "remap_step", "slice_step",
+    "remap_epoch", "balance_step", "Read", "ChunkPlan", "plan_chunks",
 ]
 
 
@@ -293,6 +295,105 @@ def identity_order(graph: ReuseGraph) -> EpochOrder:
     idx = torch.arange(E, device=graph.weights.device)
     cost = int(graph.weights[idx[:-1], idx[1:]].sum().item()) if E > 1 else 0
     return EpochOrder(idx.to(torch.int32), cost)
+
+
+def brute_force_order(graph: ReuseGraph) -> EpochOrder:
+    """epoch_order.hpp:35-38 / epoch_order.cpp:32-52 — one CTA over all E!
+    open paths (E <= 10), ties to the lexicographically smallest order."""
+    E = graph.num_epochs
+    dev = graph.weights.device
+    order = torch.empty(max(E, 1), dtype=torch.int32, device=dev)
+    cost = torch.empty(1, dtype=torch.int64, device=dev)
+    w = graph.weights.contiguous()
+    _check(lib().lsg_brute_force_order(_ptr(w), E, _ptr(order), _ptr(cost), _stream()))
+    return EpochOrder(order[:E], int(cost.item()))
+
+
+def _host_u32(a, what: str) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.int64).reshape(-1))
+    if a.size and (a.min() < 0 or a.max() >= 1 << 31):
+        raise CapabilityError(_lib.CAPABILITY, f"{what}: sample ids must be < 2^31 on device")
+    return a.astype(np.uint32)
+
+
+def _np_ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data) if a.size else None
+
+
+def _locality(buffers, batch, local_batch: int, slice_: bool):
+    N = len(buffers)
+    res = [_host_u32(sorted(s), "remap_step") for s in buffers]
+    roff = np.zeros(N + 1, dtype=np.uint64)
+    if N:
+        roff[1:] = np.cumsum([r.size for r in res])
+    rids = np.concatenate(res) if N and roff[N] else np.zeros(1, dtype=np.uint32)
+    ids = _host_u32(batch, "remap_step")
+    items = np.zeros(ids.size + 1, dtype=np.uint32)
+    off = np.zeros(N + 1, dtype=np.uint32)
+    _check(lib().lsg_remap_step(_np_ptr(roff), _np_ptr(rids), N, _np_ptr(ids), ids.size, local_batch,
+                                int(slice_), _np_ptr(items), _np_ptr(off), None))
+    return items[: off[N]], off
+
+
+def remap_step(buffers, batch, local_batch: int):
+    """locality.hpp:23-25 / locality.cpp:7-39 — one step of the device step
+    loop against explicit residency sets (buffers: one id collection per node).
+    Returns (items uint32 with bit 31 = hit, node_off uint32 [N+1])."""
+    return _locality(buffers, batch, local_batch, False)
+
+
+def slice_step(buffers, batch, local_batch: int):
+    """locality.hpp:36-38 / locality.cpp:56-73"""
+    return _locality(buffers, batch, local_batch, True)
+
+
+def remap_epoch(prev_buffers, epoch_batches, local_batch: int):
+    """locality.hpp:30-32: every step against one fixed residency snapshot."""
+    return [remap_step(prev_buffers, b, local_batch) for b in epoch_batches]
+
+
+def balance_step(items, node_off):
+    """balance.hpp:20 / balance.cpp:10-39 — closed-form move table on the
+    device. Returns (items, node_off, moves)."""
+    it = np.array(items, dtype=np.uint32).reshape(-1)
+    off = np.array(node_off, dtype=np.uint32).reshape(-1)
+    buf = np.zeros(it.size + 1, dtype=np.uint32)
+    buf[: it.size] = it
+    moves = np.zeros(1, dtype=np.uint64)
+    _check(lib().lsg_balance_step(_np_ptr(buf), _np_ptr(off), max(off.size - 1, 0), _np_ptr(moves), None))
+    return buf[: it.size], off, int(moves[0])
+
+
+@dataclass
+class Read:
+    """chunking.hpp:13-22"""
+
+    kind: str  # "single" | "chunk"
+    start: int
+    end: int
+
+    def span(self) -> int:
+        return self.end - self.start + 1
+
+
+@dataclass
+class ChunkPlan:
+    reads: list
+    needed: int
+    redundant: int
+
+
+def plan_chunks(fetch_ids, threshold: int) -> ChunkPlan:
+    """chunking.hpp:23-30 / chunking.cpp:9-33 — the device read planner on one list."""
+    ids = _host_u32(fetch_ids, "plan_chunks")
+    rs = np.zeros(ids.size + 1, dtype=np.uint32)
+    re = np.zeros(ids.size + 1, dtype=np.uint32)
+    meta = np.zeros(3, dtype=np.uint64)
+    _check(lib().lsg_plan_chunks(_np_ptr(ids), ids.size, threshold, _np_ptr(rs), _np_ptr(re), _np_ptr(meta),
+                                 None))
+    n = int(meta[0])
+    reads = [Read("single" if rs[i] == re[i] else "chunk", int(rs[i]), int(re[i])) for i in range(n)]
+    return ChunkPlan(reads, int(meta[1]), int(meta[2]))
 
 
 def _plan_buffers(config: PipelineConfig, dev):

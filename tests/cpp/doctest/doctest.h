@@ -49,6 +49,10 @@ class Approx {
     }
     friend bool operator==(const Approx& b, double a) { return a == b; }
     friend bool operator!=(double a, const Approx& b) { return !(a == b); }
+    friend bool operator<=(double a, const Approx& b) { return a < b.v_ || a == b; }
+    friend bool operator>=(double a, const Approx& b) { return a > b.v_ || a == b; }
+    friend bool operator<(double a, const Approx& b) { return a < b.v_ && a != b; }
+    friend bool operator>(double a, const Approx& b) { return a > b.v_ && a != b; }
 
   private:
     double v_, eps_;
