@@ -19,6 +19,7 @@
 #include <stdexcept>
 #include <string>
 #include <unordered_set>
+#include <memory>
 #include <vector>
 
 namespace loadsched {
@@ -265,6 +266,56 @@ struct SimResult {
 
 SimResult simulate_plan(const SchedulePlan& plan, std::uint64_t capacity, Policy policy,
                         bool insert_redundant = false);
+
+// ---- buffer.hpp:19-96: one node's buffer as device-resident state
+// (lsg_buffer_*); every call applies its accesses on the GPU in order.
+inline constexpr std::uint64_t kNeverUsed = ~std::uint64_t{0};
+
+class Buffer {
+  public:
+    explicit Buffer(std::uint64_t capacity) : Buffer(Policy::Clairvoyant, capacity) {}
+    virtual ~Buffer();
+    Buffer(const Buffer&) = delete;
+    Buffer& operator=(const Buffer&) = delete;
+
+    virtual bool access(SampleId id, std::uint64_t next_use);
+    virtual void insert_silent(SampleId id, std::uint64_t next_use);
+    virtual void clear();
+    // batched Buffer::access over a sequence, one device launch
+    std::vector<bool> access_batch(const std::vector<SampleId>& ids, const std::vector<std::uint64_t>& next_use);
+
+    const IdSet& resident() const;
+    std::uint64_t capacity() const { return capacity_; }
+
+  protected:
+    Buffer(Policy policy, std::uint64_t capacity);
+    std::uint64_t capacity_;
+
+  private:
+    void* handle_ = nullptr;
+    mutable IdSet resident_;
+    mutable bool stale_ = true;
+};
+
+class ClairvoyantBuffer : public Buffer {
+  public:
+    explicit ClairvoyantBuffer(std::uint64_t capacity) : Buffer(Policy::Clairvoyant, capacity) {}
+};
+
+class LruBuffer : public Buffer {
+  public:
+    explicit LruBuffer(std::uint64_t capacity) : Buffer(Policy::Lru, capacity) {}
+};
+
+std::unique_ptr<Buffer> make_buffer(Policy policy, std::uint64_t capacity);
+std::uint64_t simulate_sequence(const std::vector<SampleId>& seq, std::uint64_t capacity, Policy policy);
+
+struct OracleWorkspace {  // kept for signature parity; the device DP needs no host scratch
+    std::vector<std::int8_t> memo;
+    std::vector<std::uint8_t> labels;
+};
+std::uint64_t optimal_miss_oracle(const std::vector<SampleId>& seq, std::uint64_t capacity);
+std::uint64_t optimal_miss_oracle(const std::vector<SampleId>& seq, std::uint64_t capacity, OracleWorkspace& ws);
 
 // ---- config.hpp:17-36 / pipeline.hpp:17-27 ---------------------------------
 struct PipelineConfig {

@@ -232,6 +232,24 @@ int lsg_remap_step(const uint64_t* h_res_off, const uint32_t* h_res_ids, uint32_
 /* balance_step (balance.cpp:10-39) of one step's lists, in place; *h_moves
  * receives the number of moves. */
 int lsg_balance_step(uint32_t* h_items, uint32_t* h_node_off, uint32_t N, uint64_t* h_moves, void* stream);
+/* ---- Buffer (buffer.hpp:21-79): one node's buffer as a device-resident
+ *      slot array; make_buffer == lsg_buffer_create. Accesses are applied in
+ *      order by one CTA (silent != 0: insert_silent). Host arrays. */
+typedef struct lsg_buffer lsg_buffer;
+int lsg_buffer_create(int32_t policy, uint64_t capacity, lsg_buffer** out);
+void lsg_buffer_destroy(lsg_buffer* b);
+int lsg_buffer_access(lsg_buffer* b, const uint64_t* h_ids, const uint64_t* h_next_use, uint64_t n, int32_t silent,
+                      uint8_t* h_hits, void* stream);
+int lsg_buffer_clear(lsg_buffer* b);
+int lsg_buffer_resident(lsg_buffer* b, uint64_t* h_ids, uint64_t cap, uint64_t* h_n);
+/* simulate_sequence (buffer.cpp:116-125): misses of one access sequence
+ * through one buffer, via the K7 replay (one node, one access per step). */
+int lsg_simulate_sequence(const uint32_t* h_seq, uint64_t len, uint64_t capacity, int32_t policy,
+                          uint64_t* h_misses, void* stream);
+/* optimal_miss_oracle (buffer.cpp:132-182): exhaustive optimum, length <= 16,
+ * capacity in [1, 4]; a backward DP over (position, resident mask). */
+int lsg_optimal_miss_oracle(const uint64_t* h_seq, uint64_t len, uint64_t capacity, uint64_t* h_misses,
+                            void* stream);
 /* plan_chunks (chunking.cpp:9-33) of one host fetch list: reads into h_start /
  * h_end (capacity n; start == end: Single), h_meta = {reads, needed, redundant}. */
 int lsg_plan_chunks(const uint32_t* h_ids, uint64_t n, uint64_t threshold, uint32_t* h_start, uint32_t* h_end,

@@ -92,6 +92,8 @@ EXPORTS = [
     "lsg_store_read_rows", "lsg_fetch_step_store", "lsg_simulate_ex", "lsg_format_trace", "lsg_format_plan",
     "lsg_format_graph", "lsg_parse_trace", "lsg_parse_graph", "lsg_parse_plan", "lsg_free_plan",
     "lsg_buffer_windows", "lsg_brute_force_order", "lsg_remap_step", "lsg_balance_step", "lsg_plan_chunks",
+    "lsg_buffer_create", "lsg_buffer_destroy", "lsg_buffer_access", "lsg_buffer_clear", "lsg_buffer_resident",
+    "lsg_simulate_sequence", "lsg_optimal_miss_oracle",
 ]
 
 
@@ -140,6 +142,14 @@ def lib() -> ctypes.CDLL:
         L.lsg_remap_step.argtypes = [P, P, u32, P, u64, u64, i32, P, P, P]
         L.lsg_balance_step.argtypes = [P, P, u32, P, P]
         L.lsg_plan_chunks.argtypes = [P, u64, u64, P, P, P, P]
+        L.lsg_buffer_create.argtypes = [i32, u64, ctypes.POINTER(ctypes.c_void_p)]
+        L.lsg_buffer_destroy.argtypes = [P]
+        L.lsg_buffer_destroy.restype = None
+        L.lsg_buffer_access.argtypes = [P, P, P, u64, i32, P, P]
+        L.lsg_buffer_clear.argtypes = [P]
+        L.lsg_buffer_resident.argtypes = [P, P, u64, ctypes.POINTER(u64)]
+        L.lsg_simulate_sequence.argtypes = [P, u64, u64, i32, ctypes.POINTER(u64), P]
+        L.lsg_optimal_miss_oracle.argtypes = [P, u64, u64, ctypes.POINTER(u64), P]
         L.lsg_free_plan.restype = None
         L.lsg_store_fill.argtypes = [P, u64, u64, u64, P, P]
         L.lsg_gather.argtypes = [P, P, u64, u64, P, P]

@@ -361,6 +361,81 @@ std::vector<StepSizes> batch_size_stats(const SchedulePlan& plan) {
     return out;
 }
 
+// ---- buffer.cpp:10-98 on the device (buffer_api.cu) ------------------------
+Buffer::Buffer(Policy policy, std::uint64_t capacity) : capacity_(capacity) {
+    if (capacity == 0) throw ValidationError("buffer capacity must be >= 1");
+    lsg_buffer* h = nullptr;
+    check(lsg_buffer_create(policy == Policy::Lru ? 1 : 0, capacity, &h));
+    handle_ = h;
+}
+
+Buffer::~Buffer() { lsg_buffer_destroy(static_cast<lsg_buffer*>(handle_)); }
+
+bool Buffer::access(SampleId id, std::uint64_t next_use) {
+    std::uint8_t hit = 0;
+    check(lsg_buffer_access(static_cast<lsg_buffer*>(handle_), &id, &next_use, 1, 0, &hit, nullptr));
+    stale_ = true;
+    return hit != 0;
+}
+
+std::vector<bool> Buffer::access_batch(const std::vector<SampleId>& ids, const std::vector<std::uint64_t>& next_use) {
+    if (ids.size() != next_use.size()) throw ValidationError("access_batch: ids and next_use differ in length");
+    std::vector<std::uint8_t> hit(ids.size());
+    check(lsg_buffer_access(static_cast<lsg_buffer*>(handle_), ids.data(), next_use.data(), ids.size(), 0,
+                            hit.data(), nullptr));
+    stale_ = true;
+    return std::vector<bool>(hit.begin(), hit.end());
+}
+
+void Buffer::insert_silent(SampleId id, std::uint64_t next_use) {
+    check(lsg_buffer_access(static_cast<lsg_buffer*>(handle_), &id, &next_use, 1, 1, nullptr, nullptr));
+    stale_ = true;
+}
+
+void Buffer::clear() {
+    check(lsg_buffer_clear(static_cast<lsg_buffer*>(handle_)));
+    stale_ = true;
+}
+
+const IdSet& Buffer::resident() const {
+    if (stale_) {
+        std::uint64_t n = 0;
+        check(lsg_buffer_resident(static_cast<lsg_buffer*>(handle_), nullptr, 0, &n));
+        std::vector<std::uint64_t> ids(n);
+        check(lsg_buffer_resident(static_cast<lsg_buffer*>(handle_), ids.data(), n, &n));
+        resident_ = IdSet(ids.begin(), ids.end());
+        stale_ = false;
+    }
+    return resident_;
+}
+
+std::unique_ptr<Buffer> make_buffer(Policy policy, std::uint64_t capacity) {
+    if (policy == Policy::Clairvoyant) return std::make_unique<ClairvoyantBuffer>(capacity);
+    return std::make_unique<LruBuffer>(capacity);
+}
+
+// buffer.cpp:116-125 through the K7 replay
+std::uint64_t simulate_sequence(const std::vector<SampleId>& seq, std::uint64_t capacity, Policy policy) {
+    std::vector<std::uint32_t> ids(seq.size());
+    for (std::size_t i = 0; i < seq.size(); ++i) {
+        if (seq[i] >= (1ull << 31)) throw CapabilityError("simulate_sequence: sample ids must be < 2^31 on device");
+        ids[i] = std::uint32_t(seq[i]);
+    }
+    std::uint64_t misses = 0;
+    check(lsg_simulate_sequence(ids.data(), ids.size(), capacity, policy == Policy::Lru ? 1 : 0, &misses, nullptr));
+    return misses;
+}
+
+std::uint64_t optimal_miss_oracle(const std::vector<SampleId>& seq, std::uint64_t capacity) {
+    std::uint64_t misses = 0;
+    check(lsg_optimal_miss_oracle(seq.data(), seq.size(), capacity, &misses, nullptr));
+    return misses;
+}
+
+std::uint64_t optimal_miss_oracle(const std::vector<SampleId>& seq, std::uint64_t capacity, OracleWorkspace&) {
+    return optimal_miss_oracle(seq, capacity);
+}
+
 // cost_model.cpp:9-18
 double read_cost(const std::vector<Read>& reads, const CostModel& model) {
     double cost = 0.0;

@@ -27,7 +27,8 @@ __all__ = [
     "read_trace_file", "format_graph", "write_graph_file", "read_graph", "read_graph_file", "format_plan",
     "write_plan_file", "read_plan", "read_plan_file", "Error", "ConfigError", "ValidationError", "CapabilityError",
     "StorageError", "InternalError", "HIT_BIT", "NEVER", "brute_force_order", "remap_step", "slice_step",
-    "remap_epoch", "balance_step", "Read", "ChunkPlan", "plan_chunks",
+    "remap_epoch", "balance_step", "Read", "ChunkPlan", "plan_chunks", "K_NEVER_USED", "Buffer", "make_buffer",
+    "simulate_sequence", "optimal_miss_oracle",
 ]
 
 
@@ -394,6 +395,84 @@ def plan_chunks(fetch_ids, threshold: int) -> ChunkPlan:
     n = int(meta[0])
     reads = [Read("single" if rs[i] == re[i] else "chunk", int(rs[i]), int(re[i])) for i in range(n)]
     return ChunkPlan(reads, int(meta[1]), int(meta[2]))
+
+
+K_NEVER_USED = (1 << 64) - 1  # buffer.hpp:19
+
+
+class Buffer:
+    """buffer.hpp:21-79 — one node's buffer as device-resident state
+    (lsg_buffer_*). access / insert_silent / clear / resident as in the
+    reference; access_batch applies a whole sequence in one launch."""
+
+    def __init__(self, policy: str, capacity: int):
+        if capacity == 0:
+            raise ValidationError(_lib.VALIDATION, "buffer capacity must be >= 1")
+        self.policy, self._cap = policy, capacity
+        h = ctypes.c_void_p()
+        _check(lib().lsg_buffer_create(0 if policy == "clairvoyant" else 1, capacity, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().lsg_buffer_destroy(h)
+            self._h = None
+
+    def capacity(self) -> int:
+        return self._cap
+
+    def _ops(self, ids, next_use, silent: bool) -> np.ndarray:
+        ids = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64).reshape(-1))
+        nu = np.ascontiguousarray(np.asarray(next_use, dtype=np.uint64).reshape(-1))
+        if nu.size != ids.size:
+            raise ValidationError(_lib.VALIDATION, "access_batch: ids and next_use differ in length")
+        hit = np.zeros(max(ids.size, 1), dtype=np.uint8)
+        _check(lib().lsg_buffer_access(self._h, _np_ptr(ids), _np_ptr(nu), ids.size, int(silent), _np_ptr(hit),
+                                       None))
+        return hit[: ids.size].astype(bool)
+
+    def access(self, sample_id: int, next_use: int = K_NEVER_USED) -> bool:
+        return bool(self._ops([sample_id], [next_use], False)[0])
+
+    def access_batch(self, ids, next_use) -> np.ndarray:
+        return self._ops(ids, next_use, False)
+
+    def insert_silent(self, sample_id: int, next_use: int = K_NEVER_USED) -> None:
+        self._ops([sample_id], [next_use], True)
+
+    def clear(self) -> None:
+        _check(lib().lsg_buffer_clear(self._h))
+
+    def resident(self) -> set:
+        n = ctypes.c_uint64(0)
+        _check(lib().lsg_buffer_resident(self._h, None, 0, ctypes.byref(n)))
+        out = np.zeros(max(n.value, 1), dtype=np.uint64)
+        _check(lib().lsg_buffer_resident(self._h, _np_ptr(out), n.value, ctypes.byref(n)))
+        return set(int(v) for v in out[: n.value])
+
+
+def make_buffer(policy: str, capacity: int) -> Buffer:
+    """buffer.hpp:79"""
+    return Buffer(policy, capacity)
+
+
+def simulate_sequence(seq, capacity: int, policy: str = "clairvoyant") -> int:
+    """buffer.hpp:83-84 / buffer.cpp:116-125 — one node through the K7 replay."""
+    ids = _host_u32(seq, "simulate_sequence")
+    m = ctypes.c_uint64(0)
+    _check(lib().lsg_simulate_sequence(_np_ptr(ids), ids.size, capacity, 0 if policy == "clairvoyant" else 1,
+                                       ctypes.byref(m), None))
+    return m.value
+
+
+def optimal_miss_oracle(seq, capacity: int) -> int:
+    """buffer.hpp:88 / buffer.cpp:132-182 — exhaustive optimum (length <= 16,
+    capacity 1..4) as a device DP."""
+    s = np.ascontiguousarray(np.asarray(seq, dtype=np.uint64).reshape(-1))
+    m = ctypes.c_uint64(0)
+    _check(lib().lsg_optimal_miss_oracle(_np_ptr(s), s.size, capacity, ctypes.byref(m), None))
+    return m.value
 
 
 def _plan_buffers(config: PipelineConfig, dev):

@@ -12,7 +12,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 DIR = os.path.join(ROOT, "oracle", "_ref", "reftests")
 SUITES = ["test_trace", "test_prng", "test_epoch_order", "test_reuse_graph", "test_plan", "test_locality",
-          "test_balance", "test_chunking"]
+          "test_balance", "test_chunking", "test_buffer"]
 
 
 @pytest.mark.gpu

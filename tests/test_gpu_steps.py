@@ -1,7 +1,8 @@
 """GPU parity of the per-call entry points against the oracle: remap_step /
 slice_step (locality.cpp:7-73) against explicit residency sets, balance_step
-(balance.cpp:10-39), plan_chunks (chunking.cpp:9-33) and brute_force_order
-(epoch_order.cpp:32-52). The same device code runs inside the planner's
+(balance.cpp:10-39), plan_chunks (chunking.cpp:9-33), brute_force_order
+(epoch_order.cpp:32-52), the Buffer object, simulate_sequence and
+optimal_miss_oracle (buffer.cpp:10-182). The same device code runs inside the planner's
 step loop; these calls expose it one step at a time, like the reference's
 own test_locality / test_balance suites use it."""
 import random
@@ -154,3 +155,61 @@ def test_brute_force_matches_oracle(ls):
         o = ls.brute_force_order(g)
         ro, rc = O.brute_force_order(w.astype(np.uint64))
         assert o.cost == rc and o.order.cpu().numpy().tolist() == ro.tolist(), E
+
+
+def next_use_chain(seq):
+    nxt, last = [O_NEVER] * len(seq), {}
+    for i in range(len(seq) - 1, -1, -1):
+        nxt[i] = last.get(seq[i], O_NEVER)
+        last[seq[i]] = i
+    return nxt
+
+
+O_NEVER = (1 << 64) - 1
+
+
+@pytest.mark.parametrize("policy", ["clairvoyant", "lru"])
+def test_simulate_sequence_and_buffer_match_oracle(ls, policy):
+    rng = random.Random(11 if policy == "lru" else 12)
+    for _ in range(12):
+        n = rng.choice([1, 17, 300, 3000])
+        ids = rng.choice([3, 50, 1000])
+        C = rng.choice([1, 2, 7, 64, 500])
+        seq = [rng.randrange(ids) for _ in range(n)]
+        want = O.simulate_sequence(seq, C, policy)
+        assert ls.simulate_sequence(seq, C, policy) == want, (n, ids, C)
+        buf = ls.make_buffer(policy, C)
+        hits = buf.access_batch(seq, next_use_chain(seq))
+        assert int((~hits).sum()) == want, (n, ids, C)
+        assert len(buf.resident()) == min(C, len(set(seq))) or policy == "clairvoyant"
+
+
+def test_buffer_worked_examples(ls):
+    buf = ls.make_buffer("lru", 2)
+    buf.insert_silent(5)
+    assert 5 in buf.resident() and buf.access(5) and not buf.access(6) and len(buf.resident()) == 2
+    cv = ls.make_buffer("clairvoyant", 2)
+    for x in (0, 1, 2):
+        cv.access(x)
+    assert cv.resident() == {0, 1}
+    cv2 = ls.make_buffer("clairvoyant", 2)
+    cv2.access(7)
+    cv2.access(3)
+    cv2.access(5, 10)
+    assert cv2.resident() == {3, 5}
+    cv2.clear()
+    assert cv2.resident() == set() and not cv2.access(3)
+    with pytest.raises(ls.ValidationError):
+        ls.make_buffer("lru", 0)
+
+
+def test_optimal_miss_oracle(ls):
+    assert ls.optimal_miss_oracle([0, 1, 2, 0, 1], 2) == 3
+    assert ls.optimal_miss_oracle([], 2) == 0
+    with pytest.raises(ls.CapabilityError):
+        ls.optimal_miss_oracle([0] * 17, 2)
+    rng = random.Random(77)
+    for _ in range(200):
+        n, C, k = rng.randint(1, 16), rng.randint(1, 4), rng.randint(1, 6)
+        seq = [rng.randrange(k) for _ in range(n)]
+        assert ls.optimal_miss_oracle(seq, C) == O.simulate_sequence(seq, C, "clairvoyant"), (seq, C)
