@@ -35,6 +35,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -165,6 +167,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--epochs", type=int, default=None, help="override E (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--prio", type=int, default=1, help="replay+fetch stream at high priority")
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
     args = ap.parse_args()
     if args.impl == "reference":
@@ -201,65 +204,113 @@ def main():
     fetcher = ls.StepFetcher([bufs[k] for k in range(k0, k1)], [outs[k] for k in range(k0, k1)],
                              (k0, k1), SB, c["fill_seed"])
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    stream = torch.cuda.current_stream()
+    # replay + fetch (and NCCL) on a high-priority stream, the plan of the
+    # next job on a low-priority one: the block scheduler hands free SMs to
+    # the fetch first, the planner's persistent CTA needs only one
+    fstream = torch.cuda.Stream(priority=-1 if args.prio else 0)  # lower = higher priority
+    pstream = torch.cuda.Stream(priority=0)
+    torch.cuda.set_stream(fstream)
+    # the loader's pinned staging for the e2e path: two sets, so the plan of
+    # job i+1 lands in one while job i's plan is uploaded from the other
+    host_sets = [ls.plan_host_buffers(pc) for _ in range(2)] if not args.no_e2e else None
 
-    def step(host=False):
-        """one pass of the hot path; returns (events, counters)."""
-        e = [ev() for _ in range(4)]
-        e[0].record(stream)
-        out = ls.plan_schedule_host(pc, buffers=host_bufs) if host else ls.plan_schedule(pc)
-        e[1].record(stream)
-        plan = out.plan
-        if host:  # e2e: the plan lives in host memory; the device copy feeds the replay
-            items = plan.items.to(dev, non_blocking=True)
-            noff = plan.node_off.to(dev, non_blocking=True)
-            plan = ls.SchedulePlan(plan.dataset_size, N, b, plan.steps_per_epoch, plan.order, items,
-                                   noff, plan.fetches_before, plan.fetches_after)
-        sim = ls.simulate_plan(plan, C, node_range=(k0, k1), want_slots=True)
-        combine_rows(sim.hits, sim.misses)
-        e[2].record(stream)
-        off = plan.node_off.cpu().numpy() if not host else out.plan.node_off.numpy()
-        if int((off[:, k0 + 1:k1 + 1] - off[:, k0:k1]).max()) > maxlen:
-            raise SystemExit("a node list exceeds the batch tensor rows")
-        bases = [0] * (T + 1)
-        for g in range(T):
-            bases[g + 1] = bases[g] + int(off[g, N])
-        items, slots, noff_d = plan.items, sim.slots, plan.node_off
-        for g in range(T):
-            base = bases[g]
-            fetcher(items[base:], slots[base:], noff_d[g], int(off[g, k1]) - int(off[g, k0]))
-        e[3].record(stream)
-        rows = None
-        if host:
-            rows = (sim.hits.cpu(), sim.misses.cpu())
-        return e, sim, off, rows
+    def run_jobs(n, host=False, pipeline=True, stats=None, t_start=None):
+        """n passes of the hot path. Job i = plan (K1-K6) -> replay (K7, this
+        GPU's ranks, all-gather of the rows) -> fetch (K8/K9, every step of
+        this GPU's ranks). With `pipeline` the plan of job i+1 runs on its own
+        stream (one persistent CTA) from a helper thread while job i's replay
+        and fetch run on the remaining SMs; every job's work is complete when
+        the call returns. host=True is the e2e path: the plan lands in pinned
+        host memory (lsg_plan_host) and is uploaded for the replay, the
+        hit/miss rows are read back to the host."""
+        import queue
+        q = queue.Queue(maxsize=1)
+        free = threading.Semaphore(2)
+        err = []
 
-    # the loader's pinned staging for the e2e path, allocated once
-    host_bufs = ls.plan_host_buffers(pc) if not args.no_e2e else None
+        def planner():
+            try:
+                torch.cuda.set_device(dev)  # the CUDA current device is per host thread
+                with torch.cuda.stream(pstream):
+                    if t_start is not None:
+                        pstream.wait_event(t_start)
+                    for i in range(n):
+                        free.acquire()
+                        a, z = ev(), ev()
+                        a.record(pstream)
+                        out = (ls.plan_schedule_host(pc, buffers=host_sets[i % 2]) if host
+                               else ls.plan_schedule(pc))
+                        z.record(pstream)
+                        q.put((out, a, z, i % 2))
+                        if not pipeline:
+                            z.synchronize()
+            except BaseException as e:  # surfaced on the main thread
+                err.append(e)
+                q.put(None)
+
+        th = threading.Thread(target=planner, daemon=True)
+        th.start()
+        rows = []
+        for i in range(n):
+            got = q.get()
+            if got is None:
+                raise err[0]
+            out, pa, pz, hs = got
+            fstream.wait_event(pz)
+            plan = out.plan
+            if host:  # the plan lives in host memory; the device copy feeds the replay
+                items = plan.items.to(dev, non_blocking=True)
+                noff = plan.node_off.to(dev, non_blocking=True)
+                off = plan.node_off.numpy().copy()  # the staging set is recycled below
+                plan = ls.SchedulePlan(plan.dataset_size, N, b, plan.steps_per_epoch, plan.order, items,
+                                       noff, plan.fetches_before, plan.fetches_after)
+            else:  # device outputs of the plan stream, used on this stream
+                for t in (plan.items, plan.node_off):
+                    t.record_stream(fstream)
+            f0 = ev()
+            f0.record(fstream)
+            sim = ls.simulate_plan(plan, C, node_range=(k0, k1), want_slots=True)
+            combine_rows(sim.hits, sim.misses)
+            if host:
+                rows.append((sim.hits.cpu(), sim.misses.cpu()))  # d2h of the step results
+            else:
+                off = plan.node_off.cpu().numpy()
+            free.release()  # the host staging set of this job has been consumed
+            f1 = ev()
+            f1.record(fstream)
+            if int((off[:, k0 + 1:k1 + 1] - off[:, k0:k1]).max()) > maxlen:
+                raise SystemExit("a node list exceeds the batch tensor rows")
+            fetcher.fetch_steps(plan, sim.slots, off)
+            f2 = ev()
+            f2.record(fstream)
+            if stats is not None:
+                stats.append((pa, pz, f0, f1, f2, sim, off))
+            if not pipeline:
+                f2.synchronize()
+        th.join()
+        return rows
 
     # warm-up (also the first pass that fills the HBM buffers)
-    for _ in range(max(args.warmup, 3 if args.steps else 0)):
-        step()
+    nwarm = max(args.warmup, 3 if args.steps else 0)
+    if nwarm:
+        run_jobs(nwarm)
     torch.cuda.synchronize()
 
     # hit/miss totals of the local ranks (for algorithmic bytes)
-    _, sim0, off0, _ = step()
+    st0 = []
+    run_jobs(1, stats=st0)
     torch.cuda.synchronize()
+    sim0, off0 = st0[0][5], st0[0][6]
     local_hits = int(sim0.hits[:, k0:k1].sum())
     local_misses = int(sim0.misses[:, k0:k1].sum())
     slots_np = sim0.slots.cpu().numpy().view("uint32")
-    kept = int(((slots_np != 0xFFFFFFFE) & ((slots_np >> 31) == 0)).sum())  # all ranks' rows
-    # restrict kept misses to the local ranks
-    bases = [0]
-    for g in range(T):
-        bases.append(bases[-1] + int(off0[g, N]))
+    # kept misses (written to their slot too) of the local ranks
+    bases = np.concatenate([[0], np.cumsum(off0[:, N].astype(np.int64))])
     kept_local = 0
     for g in range(T):
-        for k in range(k0, k1):
-            lo, hi = bases[g] + int(off0[g, k]), bases[g] + int(off0[g, k + 1])
-            s = slots_np[lo:hi]
-            kept_local += int(((s != 0xFFFFFFFE) & ((s >> 31) == 0)).sum())
-    del kept
+        s = slots_np[bases[g] + int(off0[g, k0]): bases[g] + int(off0[g, k1])]
+        kept_local += int(((s != 0xFFFFFFFE) & ((s >> 31) == 0)).sum())
+    del st0, sim0
 
     if world > 1:
         dist.barrier()
@@ -267,24 +318,35 @@ def main():
     launches0 = ls.lib().lsg_launch_count()
     gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
         if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    evs = []
     with ClockSampler(gpu_index) as clk:
         t_start, t_end = ev(), ev()
-        t_start.record(stream)
-        evs = []
-        for _ in range(args.steps):
-            e, _, _, _ = step()
-            evs.append(e)
-        t_end.record(stream)
+        t_start.record(fstream)
+        run_jobs(args.steps, stats=evs, t_start=t_start)
+        t_end.record(fstream)
         torch.cuda.synchronize()
     launches = ls.lib().lsg_launch_count() - launches0
     total_ms = t_start.elapsed_time(t_end)
     plan_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-    replay_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
-    fetch_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    replay_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
+    fetch_ms = statistics.mean(e[3].elapsed_time(e[4]) for e in evs)
+    del evs
+    # one job alone (no overlap): the latency of a single plan+replay+fetch pass
+    serial = []
+    if args.steps:
+        a0, a1 = ev(), ev()
+        if world > 1:
+            dist.barrier()
+        a0.record(fstream)
+        run_jobs(1, pipeline=False, t_start=a0)
+        a1.record(fstream)
+        torch.cuda.synchronize()
+        serial.append(a0.elapsed_time(a1))
+    job_ms = serial[0] if serial else 0.0
     if world > 1:
-        tt = torch.tensor([total_ms, plan_ms, replay_ms, fetch_ms], device=dev, dtype=torch.float64)
+        tt = torch.tensor([total_ms, plan_ms, replay_ms, fetch_ms, job_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms, plan_ms, replay_ms, fetch_ms = [float(x) for x in tt]
+        total_ms, plan_ms, replay_ms, fetch_ms, job_ms = [float(x) for x in tt]
     ms_per_step = total_ms / max(args.steps, 1)
 
     # fetch-phase algorithmic bytes: hits read a slot and write the batch row;
@@ -305,21 +367,22 @@ def main():
     except Exception:
         pass
 
-    # e2e through the C-ABI host path (lsg_plan_host: the plan lands in host
-    # memory; hit/miss rows read back)
+    # e2e through the public API with host buffers (lsg_plan_host: the plan
+    # lands in pinned host memory, is uploaded for the replay, hit/miss rows
+    # are read back), the same pipelined job stream, K jobs
     e2e = None
     if not args.no_e2e and args.steps:
-        step(host=True)  # untimed warm-up of the host path
+        run_jobs(2, host=True)  # untimed warm-up of the host path
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         a0, a1 = ev(), ev()
-        a0.record(stream)
-        step(host=True)
-        a1.record(stream)
+        a0.record(fstream)
+        run_jobs(args.steps, host=True, t_start=a0)
+        a1.record(fstream)
         torch.cuda.synchronize()
-        e2e_ms = a0.elapsed_time(a1)
+        e2e_ms = a0.elapsed_time(a1) / args.steps
         if world > 1:
             tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -328,8 +391,9 @@ def main():
             + pc.pso.max_iters * 8 + T * N * 4 * 2 + T * (N + 1) * 4
         e2e = {"value": A / (e2e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": T * (N + 1) * 4 + A * 4,
                "d2h_bytes_per_step": d2h,
-               "note": "lsg_plan_host (trace, graph, order, plan lists, fetch counts to host), plan "
-                       "re-uploaded for the replay, hit/miss rows read back, batch fetch on device"}
+               "note": "per job: lsg_plan_host (trace, graph, order, plan lists, fetch counts to pinned host), "
+                       "plan re-uploaded for the replay, hit/miss rows read back, batch fetch on device; "
+                       "jobs pipelined as in value"}
 
     cpu = cpu_baseline() if (rank == 0 and world == 1) else None
 
@@ -344,7 +408,10 @@ def main():
                        "global_batch": N * b, "ranks_per_gpu": k1 - k0,
                        "parallelism": f"plan replicated; replay+fetch sharded {k1 - k0} ranks/GPU",
                        "l2": "inputs > L2 (12.8 GiB HBM sample buffer per rank)"},
+            "pipeline": "job i+1's plan (1 persistent CTA, own stream) overlaps job i's replay+fetch; "
+                        "every job's full work is inside the timed region",
             "plan_ms": plan_ms, "replay_ms": replay_ms, "fetch_ms": fetch_ms,
+            "single_job_ms": job_ms, "single_job_samples_per_s": A / (job_ms * 1e-3) if job_ms else None,
             "plan_samples_per_s": A / (plan_ms * 1e-3),
             "gather": {"value": achieved, "unit": "GB/s", "hits": local_hits, "misses": local_misses,
                        "bytes_per_step": alg_bytes},

@@ -102,6 +102,15 @@ int lsg_build_reuse_graph(const uint32_t* d_trace, uint32_t E, uint64_t len, uin
                           uint32_t N, uint64_t b, int32_t drop_last, uint64_t buffer_size,
                           int32_t mode, uint64_t* d_w, void* stream);
 
+/* Rows [row_begin, row_end) of the same matrix into d_w_rows
+ * ([row_end - row_begin][E], row-major): the multi-GPU row sharding of K3
+ * (each GPU builds all window bitsets and its row block; an all-gather of the
+ * blocks yields build_reuse_graph's weights on every GPU). */
+int lsg_build_reuse_graph_rows(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64_t D,
+                               uint32_t N, uint64_t b, int32_t drop_last, uint64_t buffer_size,
+                               int32_t mode, uint32_t row_begin, uint32_t row_end, uint64_t* d_w_rows,
+                               void* stream);
+
 /* ---- K4: pso_order(graph, PsoParams) -> PsoResult
  *      (epoch_order.hpp:60, epoch_order.cpp:121-221). Bit-exact. */
 int lsg_pso_order(const uint64_t* d_w, uint32_t E, uint32_t swarm, uint32_t iters,
@@ -174,6 +183,17 @@ int lsg_fetch_step(void* const* d_bufs, void* const* d_outs, const uint32_t* d_i
                    const uint32_t* d_slots, const uint32_t* d_node_off, uint32_t node_begin,
                    uint32_t node_end, uint64_t rows_hint, uint64_t sample_bytes, uint64_t fill_seed,
                    void* stream);
+
+/* The loading phase of steps [step_begin, step_end) of a plan, in step order
+ * (one lsg_fetch_step per step, launched from C without host round trips):
+ * d_items/d_slots/d_node_off are the WHOLE plan's arrays (lsg_plan_out
+ * layout, [T][N+1] offsets), h_node_off a host copy of the offsets (step
+ * bases and grid sizes). Every step writes the same batch tensors, as a
+ * trainer consuming batch t before t+1 would see them. */
+int lsg_fetch_steps(void* const* d_bufs, void* const* d_outs, const uint32_t* d_items, const uint32_t* d_slots,
+                    const uint32_t* d_node_off, const uint32_t* h_node_off, uint64_t step_begin,
+                    uint64_t step_end, uint32_t N, uint32_t node_begin, uint32_t node_end,
+                    uint64_t sample_bytes, uint64_t fill_seed, void* stream);
 
 /* ---- The sample Store (store.hpp:13-81, store.cpp:37-148): SLRD files
  *      (22-byte header + one continuous splitmix64 payload stream).

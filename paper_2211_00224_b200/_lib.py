@@ -93,7 +93,8 @@ EXPORTS = [
     "lsg_format_graph", "lsg_parse_trace", "lsg_parse_graph", "lsg_parse_plan", "lsg_free_plan",
     "lsg_buffer_windows", "lsg_brute_force_order", "lsg_remap_step", "lsg_balance_step", "lsg_plan_chunks",
     "lsg_buffer_create", "lsg_buffer_destroy", "lsg_buffer_access", "lsg_buffer_clear", "lsg_buffer_resident",
-    "lsg_simulate_sequence", "lsg_optimal_miss_oracle",
+    "lsg_simulate_sequence", "lsg_optimal_miss_oracle", "lsg_build_reuse_graph_rows",
+    "lsg_fetch_steps",
 ]
 
 
@@ -125,6 +126,8 @@ def lib() -> ctypes.CDLL:
         L.lsg_shape_of.argtypes = [ctypes.POINTER(LsgConfig), ctypes.POINTER(LsgShape)]
         L.lsg_generate_trace.argtypes = [ctypes.POINTER(LsgConfig), P, P]
         L.lsg_build_reuse_graph.argtypes = [P, u32, u64, u64, u32, u64, i32, u64, i32, P, P]
+        L.lsg_build_reuse_graph_rows.argtypes = [P, u32, u64, u64, u32, u64, i32, u64, i32, u32, u32, P, P]
+        L.lsg_fetch_steps.argtypes = [P, P, P, P, P, P, u64, u64, u32, u32, u32, u64, u64, P]
         L.lsg_pso_order.argtypes = [P, u32, u32, u32, dbl, dbl, dbl, dbl, u32, u32, u64, P, P, P, P, P]
         L.lsg_plan.argtypes = [ctypes.POINTER(LsgConfig), ctypes.POINTER(LsgPlanOut), P]
         L.lsg_plan_host.argtypes = [ctypes.POINTER(LsgConfig), ctypes.POINTER(LsgPlanOut), P]

@@ -16,7 +16,8 @@ int generate_trace_device(uint64_t D, uint32_t E, uint64_t keep, uint64_t seed, 
                           uint32_t* d_inv, cudaStream_t st);
 int build_reuse_graph_device(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64_t D,
                              uint32_t N, uint64_t b, bool drop_last, uint64_t buffer_size, int mode,
-                             bool rows_distinct_known, uint64_t* d_w, cudaStream_t st);
+                             bool rows_distinct_known, uint64_t* d_w, cudaStream_t st, uint32_t r0 = 0,
+                             uint32_t r1 = kNone);
 int pso_order_device(const uint64_t* d_w, uint32_t E, uint32_t swarm, uint32_t iters, double pp,
                      double pg, double inertia, double kick, uint32_t stagnation, uint32_t restart,
                      uint64_t seed, uint32_t* d_order, uint64_t* d_cost, uint64_t* d_hist,
@@ -160,6 +161,16 @@ int lsg_build_reuse_graph(const uint32_t* d_trace, uint32_t E, uint64_t len, uin
     if (D >= (1ull << 31) || len >= (1ull << 31)) return set_error(kCapability, "trace too large for device ids");
     return build_reuse_graph_device(d_trace, E, len, D, N, b, drop_last != 0, buffer_size, mode, false,
                                     d_w, static_cast<cudaStream_t>(stream));
+}
+
+int lsg_build_reuse_graph_rows(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64_t D, uint32_t N,
+                               uint64_t b, int32_t drop_last, uint64_t buffer_size, int32_t mode,
+                               uint32_t row_begin, uint32_t row_end, uint64_t* d_w_rows, void* stream) {
+    if (N == 0 || b == 0) return set_error(kConfig, "num_nodes and local_batch must be >= 1");
+    if (D >= (1ull << 31) || len >= (1ull << 31)) return set_error(kCapability, "trace too large for device ids");
+    if (row_begin > row_end || row_end > E) return set_error(kValidation, "build_reuse_graph_rows: bad row range");
+    return build_reuse_graph_device(d_trace, E, len, D, N, b, drop_last != 0, buffer_size, mode, false,
+                                    d_w_rows, static_cast<cudaStream_t>(stream), row_begin, row_end);
 }
 
 int lsg_pso_order(const uint64_t* d_w, uint32_t E, uint32_t swarm, uint32_t iters, double p_personal,
@@ -327,6 +338,26 @@ int lsg_fetch_step(void* const* d_bufs, void* const* d_outs, const uint32_t* d_i
                    void* stream) {
     return fetch_step_device(d_bufs, d_outs, d_items, d_slots, d_node_off, node_begin, node_end,
                              rows_hint, sample_bytes, fill_seed, static_cast<cudaStream_t>(stream));
+}
+
+int lsg_fetch_steps(void* const* d_bufs, void* const* d_outs, const uint32_t* d_items, const uint32_t* d_slots,
+                    const uint32_t* d_node_off, const uint32_t* h_node_off, uint64_t step_begin,
+                    uint64_t step_end, uint32_t N, uint32_t node_begin, uint32_t node_end,
+                    uint64_t sample_bytes, uint64_t fill_seed, void* stream) {
+    if (node_begin > node_end || node_end > N) return set_error(kValidation, "fetch_steps: bad node range");
+    if (step_begin > step_end) return set_error(kValidation, "fetch_steps: bad step range");
+    if (!h_node_off) return set_error(kValidation, "fetch_steps: host node offsets required");
+    uint64_t base = 0;
+    for (uint64_t g = 0; g < step_begin; ++g) base += h_node_off[g * (N + 1) + N];
+    for (uint64_t g = step_begin; g < step_end; ++g) {
+        const uint32_t* o = h_node_off + g * (N + 1);
+        if (int rc = fetch_step_device(d_bufs, d_outs, d_items + base, d_slots + base, d_node_off + g * (N + 1),
+                                       node_begin, node_end, uint64_t(o[node_end] - o[node_begin]), sample_bytes,
+                                       fill_seed, static_cast<cudaStream_t>(stream)))
+            return rc;
+        base += o[N];
+    }
+    return kOk;
 }
 
 }  // extern "C"

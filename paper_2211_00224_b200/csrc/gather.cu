@@ -144,7 +144,7 @@ struct StepFetch {
     uint32_t k0, k1;
     uint64_t vec_per_row, tiles_per_row, seed;
     uint32_t* mlist;           // miss rows of the step (filled by the TMA hit kernel) or null
-    uint32_t* mctl;            // [2] miss count, finished misses blocks
+    uint32_t* mctl;            // [3] miss count, finished misses blocks, hit-tile chunks claimed
 };
 
 __device__ __forceinline__ uint32_t node_of_row(const StepFetch& f, uint32_t r) {
@@ -185,10 +185,13 @@ __global__ void __launch_bounds__(kGatherThreads) k_fetch_step_hits(StepFetch f)
 // complete_tx) -> global (cp.async.bulk bulk_group), kStages tiles per CTA;
 // a slot is refilled once the store of its tile has read it, checked kLag
 // stores later, so up to kLag+1 stores and kStages-kLag-1 loads are in
-// flight. Each CTA takes a contiguous range of tiles (row descriptors change
-// once per row); miss rows are skipped whole. Measured at 6.56
-// TB/s on the cfg2 shape vs 5.75 for the LSU gather (tools/ubench_gather.cu).
-constexpr int kTmaTile = 8192, kTmaStages = 12, kTmaLag = 3;
+// flight. CTAs claim chunks of kTmaChunk consecutive tiles from a per-step
+// counter (mctl[2], reset by the misses kernel), so a CTA that starts late
+// (an SM shared with the planner's persistent CTA) takes fewer chunks instead
+// of stretching the step; row descriptors change once per row and miss rows
+// are skipped whole. Measured at 6.56 TB/s on the cfg2 shape vs 5.75 for the
+// LSU gather (tools/ubench_gather.cu).
+constexpr int kTmaTile = 8192, kTmaStages = 12, kTmaLag = 3, kTmaChunk = 16;
 
 __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
     extern __shared__ __align__(128) unsigned char tsm[];
@@ -203,15 +206,29 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
     const uint64_t row_bytes = f.vec_per_row * 16, tpr = row_bytes / kTmaTile;
     const uint32_t r0 = __ldg(&f.node_off[f.k0]);
     const uint64_t nt = uint64_t(__ldg(&f.node_off[f.k1]) - r0) * tpr;
-    const uint64_t per = (nt + gridDim.x - 1) / gridDim.x;
-    const uint64_t tb = uint64_t(blockIdx.x) * per, te = min(nt, tb + per);
+    // static split without a counter (mctl == null), else dynamic chunks
+    uint64_t tb, te;
+    if (f.mctl) {
+        tb = uint64_t(atomicAdd(&f.mctl[2], 1u)) * kTmaChunk;
+        te = min(nt, tb + kTmaChunk);
+    } else {
+        const uint64_t per = (nt + gridDim.x - 1) / gridDim.x;
+        tb = uint64_t(blockIdx.x) * per;
+        te = min(nt, tb + per);
+    }
     uint64_t cur = ~0ull;  // row of the cached descriptor
     const unsigned char* src_row = nullptr;
     unsigned char* dst_row = nullptr;
     uint64_t tn = tb;  // next tile to issue; miss rows are skipped whole
     auto issue = [&](uint64_t k) -> bool {
         for (;;) {
-            if (tn >= te) return false;
+            if (tn >= te) {
+                if (!f.mctl || tb >= nt) return false;
+                tb = uint64_t(atomicAdd(&f.mctl[2], 1u)) * kTmaChunk;
+                if (tb >= nt) return false;
+                te = min(nt, tb + kTmaChunk);
+                tn = tb;
+            }
             const uint64_t rr = tn / tpr;
             if (rr != cur) {
                 cur = rr;
@@ -225,7 +242,7 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
                 dst_row = reinterpret_cast<unsigned char*>(f.outs[kk - f.k0]) +
                           uint64_t(r - __ldg(&f.node_off[kk])) * row_bytes;
                 // a miss row goes on the misses kernel's list, once: by the
-                // CTA whose tile range holds the row's first tile
+                // CTA whose tile range (chunk) holds the row's first tile
                 if (!hit && f.mlist && rr * tpr >= tb) f.mlist[atomicAdd(&f.mctl[0], 1u)] = r;
             }
             if (src_row) break;
@@ -297,6 +314,7 @@ __global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
             if (ticket == gridDim.x * gridDim.y - 1) {
                 f.mctl[0] = 0;
                 f.mctl[1] = 0;
+                f.mctl[2] = 0;  // the hit kernel's chunk counter
             }
         }
     }
@@ -305,7 +323,7 @@ __global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
 // per-device miss-row list of the step fetch (grown on demand; the counters
 // are zero between steps)
 struct MissList {
-    uint32_t* buf = nullptr;  // [2 + cap]
+    uint32_t* buf = nullptr;  // [4 control words + cap]
     uint64_t cap = 0;
 };
 
@@ -320,11 +338,11 @@ int miss_list(uint64_t rows, cudaStream_t st, uint32_t** list, uint32_t** ctl) {
             cudaFree(m.buf);
         }
         m.cap = std::max<uint64_t>(rows, 4096);
-        LSG_CUDA(cudaMalloc(&m.buf, (m.cap + 2) * 4));
-        LSG_CUDA(cudaMemsetAsync(m.buf, 0, 8, st));
+        LSG_CUDA(cudaMalloc(&m.buf, (m.cap + 4) * 4));
+        LSG_CUDA(cudaMemsetAsync(m.buf, 0, 16, st));
     }
     *ctl = m.buf;
-    *list = m.buf + 2;
+    *list = m.buf + 4;
     return kOk;
 }
 

@@ -113,14 +113,15 @@ constexpr int kGT = 64;   // tile edge (pairs)
 constexpr int kGK = 32;   // words per smem stage
 
 // and-not popcount Gram matrix: w[u][v] += sum popc(F[v] & ~L[u]) over this
-// block's word range; 16x16 threads, 4x4 pairs each.
-__global__ void __launch_bounds__(256) k_reuse_gram(uint32_t E, uint32_t W, uint32_t kspan,
+// block's word range; 16x16 threads, 4x4 pairs each. Rows u in [r0, r1) are
+// written to w[u - r0][v] (a row block, for the multi-GPU row sharding).
+__global__ void __launch_bounds__(256) k_reuse_gram(uint32_t E, uint32_t r0, uint32_t r1, uint32_t W, uint32_t kspan,
                                                     const uint32_t* __restrict__ F,
                                                     const uint32_t* __restrict__ L,
                                                     unsigned long long* __restrict__ w) {
     __shared__ uint32_t Ls[kGK][kGT + 1];
     __shared__ uint32_t Fs[kGK][kGT + 1];
-    const uint32_t u0 = blockIdx.y * kGT, v0 = blockIdx.x * kGT;
+    const uint32_t u0 = r0 + blockIdx.y * kGT, v0 = blockIdx.x * kGT;
     const uint32_t k0 = blockIdx.z * kspan, k1 = std::min<uint32_t>(W, k0 + kspan);
     const uint32_t t = threadIdx.x, tu = t >> 4, tv = t & 15;
     uint32_t acc[4][4] = {};
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(256) k_reuse_gram(uint32_t E, uint32_t W, uint
             const uint32_t wd = kb + kk;
             const bool okw = wd < k1;
             const uint32_t u = u0 + r, v = v0 + r;
-            Ls[kk][r] = (okw && u < E) ? L[size_t(u) * W + wd] : 0xFFFFFFFFu;  // ~L = 0
+            Ls[kk][r] = (okw && u < r1) ? L[size_t(u) * W + wd] : 0xFFFFFFFFu;  // ~L = 0
             Fs[kk][r] = (okw && v < E) ? F[size_t(v) * W + wd] : 0u;
         }
         __syncthreads();
@@ -154,7 +155,8 @@ __global__ void __launch_bounds__(256) k_reuse_gram(uint32_t E, uint32_t W, uint
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const uint32_t u = u0 + tu + 16 * a, v = v0 + tv + 16 * c;
-            if (u < E && v < E && u != v && acc[a][c]) atomicAdd(&w[size_t(u) * E + v], (unsigned long long)acc[a][c]);
+            if (u < r1 && v < E && u != v && acc[a][c])
+                atomicAdd(&w[size_t(u - r0) * E + v], (unsigned long long)acc[a][c]);
         }
 }
 
@@ -178,12 +180,16 @@ int window_bits_device(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64
                        bool drop_last, uint64_t buffer_size, int mode, bool rows_distinct_known, uint32_t* Fb,
                        uint32_t* Lb, cudaStream_t st);
 
+// Rows [r0, r1) of w into d_w ([r1 - r0][E]); the full graph is r0 = 0, r1 = E.
 int build_reuse_graph_device(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64_t D,
                              uint32_t N, uint64_t b, bool drop_last, uint64_t buffer_size, int mode,
-                             bool rows_distinct_known, uint64_t* d_w, cudaStream_t st) {
+                             bool rows_distinct_known, uint64_t* d_w, cudaStream_t st, uint32_t r0,
+                             uint32_t r1) {
     if (buffer_size == 0) return set_error(kValidation, "build_reuse_graph: buffer_size must be >= 1");
-    if (E == 0) return kOk;
-    LSG_CUDA(cudaMemsetAsync(d_w, 0, size_t(E) * E * sizeof(uint64_t), st));
+    if (r1 == kNone) r1 = E;
+    if (r0 > r1 || r1 > E) return set_error(kValidation, "build_reuse_graph: bad row range");
+    if (E == 0 || r0 == r1) return kOk;
+    LSG_CUDA(cudaMemsetAsync(d_w, 0, size_t(r1 - r0) * E * sizeof(uint64_t), st));
     const uint64_t W = uint64_t((D + 31) / 32) * (mode == 0 ? 1 : N);  // words per (epoch) row
     Scratch sc(st);
     uint32_t* Fb = sc.get<uint32_t>(size_t(E) * W);
@@ -192,14 +198,15 @@ int build_reuse_graph_device(const uint32_t* d_trace, uint32_t E, uint64_t len, 
     if (int rc = window_bits_device(d_trace, E, len, D, N, b, drop_last, buffer_size, mode, rows_distinct_known, Fb,
                                     Lb, st))
         return rc;
-    const uint32_t tiles = ((E + kGT - 1) / kGT) * ((E + kGT - 1) / kGT);
+    const uint32_t rows = r1 - r0;
+    const uint32_t tiles = ((rows + kGT - 1) / kGT) * ((E + kGT - 1) / kGT);
     uint32_t split = std::max<uint32_t>(1, (296 + tiles - 1) / tiles);
     split = std::min<uint64_t>(split, std::max<uint64_t>(1, W / 256));
     uint32_t kspan = uint32_t((W + split - 1) / split);
     kspan = (kspan + kGK - 1) / kGK * kGK;
     split = uint32_t((W + kspan - 1) / kspan);
-    dim3 grid((E + kGT - 1) / kGT, (E + kGT - 1) / kGT, split);
-    k_reuse_gram<<<grid, 256, 0, st>>>(E, uint32_t(W), kspan, Fb, Lb,
+    dim3 grid((E + kGT - 1) / kGT, (rows + kGT - 1) / kGT, split);
+    k_reuse_gram<<<grid, 256, 0, st>>>(E, r0, r1, uint32_t(W), kspan, Fb, Lb,
                                        reinterpret_cast<unsigned long long*>(d_w));
     LSG_LAUNCH_CHECK("k_reuse_gram");
     return kOk;

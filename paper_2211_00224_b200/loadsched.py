@@ -21,7 +21,7 @@ from ._lib import HIT_BIT, NEVER, LsgConfig, LsgError, LsgPlanOut, LsgShape, che
 __all__ = [
     "TraceConfig", "PsoParams", "PipelineConfig", "AccessTrace", "ReuseGraph", "EpochOrder",
     "PsoResult", "SchedulePlan", "PlanOutput", "SimResult", "generate_trace", "build_reuse_graph",
-    "pso_order", "identity_order", "plan_schedule", "plan_schedule_host", "plan_host_buffers", "baseline_config", "simulate_plan",
+    "pso_order", "build_reuse_graph_rows", "identity_order", "plan_schedule", "plan_schedule_host", "plan_host_buffers", "baseline_config", "simulate_plan",
     "store_fill", "gather", "batch_fetch", "StepFetcher", "StoreHeader", "Store", "create_store",
     "STORE_HEADER_BYTES", "DEFAULT_STORE_BUDGET", "format_trace", "write_trace_file", "read_trace",
     "read_trace_file", "format_graph", "write_graph_file", "read_graph", "read_graph_file", "format_plan",
@@ -269,6 +269,22 @@ def build_reuse_graph(trace: AccessTrace, buffer_size: int, mode: str = "global"
                                        cfg.local_batch, int(cfg.drop_last), buffer_size,
                                        0 if mode == "global" else 1, _ptr(w), _stream()))
     return ReuseGraph(E, buffer_size, mode, w[:E, :E])
+
+
+def build_reuse_graph_rows(trace: AccessTrace, buffer_size: int, mode: str, row_begin: int,
+                           row_end: int) -> torch.Tensor:
+    """Rows [row_begin, row_end) of build_reuse_graph's weights (int64
+    [row_end - row_begin, E] on device): the row block one GPU computes in the
+    multi-GPU row sharding of K3 (parallel.sharded_reuse_graph)."""
+    ep = trace.epochs.contiguous()
+    E, L = ep.shape
+    rows = torch.empty((max(row_end - row_begin, 0), E), dtype=torch.int64, device=ep.device)
+    cfg = trace.config
+    _check(lib().lsg_build_reuse_graph_rows(_ptr(ep), E, L, cfg.dataset_size, cfg.num_nodes, cfg.local_batch,
+                                            int(cfg.drop_last), buffer_size, 0 if mode == "global" else 1,
+                                            row_begin, row_end, _ptr(rows) if rows.numel() else None,
+                                            _stream()))
+    return rows
 
 
 def pso_order(graph: ReuseGraph, params: PsoParams) -> PsoResult:
@@ -888,3 +904,18 @@ class StepFetcher:
         _check(lib().lsg_fetch_step(_ptr(self.pb), _ptr(self.po), _ptr(items), _ptr(slots),
                                     _ptr(node_off_row), self.k0, self.k1, rows_hint,
                                     self.sample_bytes, self.fill_seed, _stream()))
+
+    def fetch_steps(self, plan: "SchedulePlan", slots: torch.Tensor, host_node_off: np.ndarray,
+                    step_begin: int = 0, step_end: int | None = None) -> None:
+        """The loading phase of steps [step_begin, step_end) of `plan` for this
+        fetcher's ranks, in step order (lsg_fetch_steps: one C call, no host
+        round trips). host_node_off: the plan's [T, N+1] offsets on the host."""
+        if self.store is not None:
+            raise CapabilityError(4, "fetch_steps: Store-backed misses go through per-step calls")
+        off = np.ascontiguousarray(host_node_off, dtype=np.uint32)
+        T = off.shape[0]
+        step_end = T if step_end is None else step_end
+        _check(lib().lsg_fetch_steps(_ptr(self.pb), _ptr(self.po), _ptr(plan.items), _ptr(slots),
+                                     _ptr(plan.node_off), ctypes.c_void_p(off.ctypes.data), step_begin, step_end,
+                                     off.shape[1] - 1, self.k0, self.k1, self.sample_bytes, self.fill_seed,
+                                     _stream()))

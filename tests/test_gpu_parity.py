@@ -115,6 +115,26 @@ def test_graph_large_pernode(ls):
         assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("E,world", [(1, 1), (5, 2), (70, 3), (500, 8), (100, 7)])
+def test_graph_row_blocks(ls, E, world):
+    """lsg_build_reuse_graph_rows (the multi-GPU row sharding of K3): the row
+    blocks of every rank_range split concatenate to build_reuse_graph."""
+    import torch
+    from paper_2211_00224_b200.parallel import rank_range
+    D, N, b = 4096 if E <= 100 else 16384, 4, 8
+    t = ls.generate_trace(ls.TraceConfig(D, E, N, b, E, True))
+    for mode, C in (("global", D // 10), ("pernode", D // 12)):
+        full = u64(ls.build_reuse_graph(t, C, mode).weights)
+        parts = []
+        for r in range(world):
+            u0, u1 = rank_range(E, world, r)
+            rows = ls.build_reuse_graph_rows(t, C, mode, u0, u1)
+            parts.append(u64(rows))
+        assert np.array_equal(np.concatenate(parts, axis=0), full), mode
+    with pytest.raises(ls.ValidationError):
+        ls.build_reuse_graph_rows(t, 10, "global", 0, E + 1)
+
+
 # ------------------------------------------------------------------ K4 ---
 @pytest.mark.parametrize("seed,E", [(s, E) for s, E in zip(range(14), [1, 2, 3, 5, 8, 10, 16, 31, 32, 33, 40, 64, 100, 200])])
 def test_pso_matches_oracle(ls, seed, E):

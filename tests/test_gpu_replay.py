@@ -169,3 +169,43 @@ def test_fetch_step_end_to_end(ls, seed, rng):
             want = ls.store_fill(_dev(items[lo:hi]), SB, fill)
             assert torch.equal(outs[k - k0][: hi - lo], want), (g, k)
         base += off[g, N]
+
+
+@pytest.mark.parametrize("SB", [48, 8192 * 2])
+def test_fetch_steps_matches_per_step(ls, SB):
+    """lsg_fetch_steps (one C call over a step range) leaves the batch tensors
+    and HBM buffers exactly as the per-step lsg_fetch_step loop does, and the
+    last step's batch rows equal Store::read_one of its lists."""
+    import torch
+    N, b, D, C, fill = 4, 8, 4 * 8 * 7, 60, 9
+    c = O.Cfg(D, 4, N, b, seed=3, buffer_capacity=C, pso_iters=20)
+    out = ls.plan_schedule(to_pc(ls, c))
+    k0, k1 = 1, 4
+    sim = ls.simulate_plan(out.plan, C, node_range=(k0, k1), want_slots=True)
+    off = u32(out.plan.node_off)
+    T = off.shape[0]
+    res = []
+    for mode in ("step", "range"):
+        bufs = [torch.zeros((C, SB), dtype=torch.uint8, device="cuda") for _ in range(k0, k1)]
+        outs = [torch.zeros((N * b, SB), dtype=torch.uint8, device="cuda") for _ in range(k0, k1)]
+        f = ls.StepFetcher(bufs, outs, (k0, k1), SB, fill)
+        if mode == "step":
+            base = 0
+            for g in range(T):
+                f(out.plan.items[base:], sim.slots[base:], out.plan.node_off[g], int(off[g, k1] - off[g, k0]))
+                base += off[g, N]
+        else:
+            f.fetch_steps(out.plan, sim.slots, off, 0, T // 2)
+            f.fetch_steps(out.plan, sim.slots, off, T // 2, T)
+        torch.cuda.synchronize()
+        res.append((bufs, outs))
+    for a, z in zip(res[0][0] + res[0][1], res[1][0] + res[1][1]):
+        assert torch.equal(a, z)
+    items = u32(out.plan.items) & 0x7FFFFFFF
+    base = int(off[:-1, N].sum())
+    for k in range(k0, k1):
+        lo, hi = base + off[T - 1, k], base + off[T - 1, k + 1]
+        want = ls.store_fill(_dev(items[lo:hi]), SB, fill)
+        assert torch.equal(res[1][1][k - k0][: hi - lo], want)
+    with pytest.raises(ls.ValidationError):
+        f.fetch_steps(out.plan, sim.slots, off, 3, 2)

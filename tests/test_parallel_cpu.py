@@ -1,6 +1,7 @@
 """World-size-2 gloo tests of the multi-GPU host logic on CPU: rank ranges
-partition the training ranks, and the SUM all-reduce of per-GPU replay rows
-reproduces the reference replay rows (oracle) for every split."""
+partition the training ranks, the all-gather of per-GPU replay columns
+reproduces the reference replay rows (oracle), and the all-gather of reuse
+matrix row blocks reproduces the whole matrix (oracle)."""
 import os
 import socket
 
@@ -11,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle as O
-from paper_2211_00224_b200.parallel import combine_rows, rank_range
+from paper_2211_00224_b200.parallel import allgather_blocks, combine_rows, rank_range
 
 
 def test_rank_range_partitions():
@@ -47,12 +48,19 @@ def _worker(rank, world, port, q):
         hl[:, k0:k1] = torch.from_numpy(h[:, k0:k1].astype(np.int64))
         ml[:, k0:k1] = torch.from_numpy(m[:, k0:k1].astype(np.int64))
         combine_rows(hl, ml)
-        q.put((rank, bool(np.array_equal(hl.numpy(), h)) and bool(np.array_equal(ml.numpy(), m))))
+        ok = bool(np.array_equal(hl.numpy(), h)) and bool(np.array_equal(ml.numpy(), m))
+        # reuse-matrix row blocks (uneven split: E=7 over the world)
+        tr = O.generate_trace(900, 7, 3, 10, 5, True)
+        w = O.build_reuse_graph(tr, 900, 3, 10, 100, "pernode", True).astype(np.int64)
+        u0, u1 = rank_range(7, world, rank)
+        full = allgather_blocks(torch.from_numpy(w[u0:u1].copy()), 7)
+        ok = ok and bool(np.array_equal(full.numpy(), w))
+        q.put((rank, ok))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_sharded_replay_rows_combine_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
