@@ -6,16 +6,21 @@ One bench *step* is one full pass of the hot path over the cfg2 job
 100 epochs, 8 ranks, local batch 512, per-rank HBM buffer 20% of the dataset):
 
   plan     K1 shuffle -> K2/K3 reuse matrix -> K4 PSO order -> K5/K6 step loop
-           (locality remap, balance, clairvoyant eviction)   [replicated per GPU]
-  replay   K7 per-rank Belady replay of this GPU's ranks + NCCL all-reduce of the
-           per-(step, rank) hit/miss rows                    [sharded by rank]
+           (locality remap, balance, clairvoyant eviction)   [one GPU per job:
+           job i on GPU i mod N, node lists broadcast over NVLink (NCCL)]
+  replay   K7 per-rank Belady replay of this GPU's ranks + NCCL all-gather of
+           the per-(step, rank) hit/miss rows                [sharded by rank]
   fetch    K8/K9 every training step's batch of this GPU's ranks: hits gathered
            from the rank's 12.8 GiB HBM sample buffer, misses written from
            storage (synthetic Store payload) into the batch and their slot
 
-value = planned-and-fetched samples of the whole job / step time (max over
-ranks): the loading path's throughput. `plan_samples_per_s` isolates the plan
-(north star: < 1 s for this job). The roofline object is the fetch phase
+Jobs are pipelined: plans run on their own stream (the step loop is ONE
+persistent CTA) from a helper thread, overlapping earlier jobs' replay and
+fetch on the other SMs. `single_job_ms` is one job alone, unpipelined.
+
+value = planned-and-fetched samples of the K timed jobs / timed region (max
+over ranks): the loading path's throughput. `plan_samples_per_s` isolates one
+plan (north star: < 1 s for this job). The roofline object is the fetch phase
 (HBM-bound gather). GPUs own contiguous rank ranges (8 ranks / N GPUs); the
 job is fixed, so scaling is strong.
 
@@ -167,6 +172,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--epochs", type=int, default=None, help="override E (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--plan-shard", default="auto", choices=["auto", "rr", "replicate"],
+                    help="N>1: plan each job on one GPU (rr) or on all (replicate); auto = rr above 2 GPUs")
     ap.add_argument("--prio", type=int, default=1, help="replay+fetch stream at high priority")
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
     args = ap.parse_args()
@@ -208,25 +215,41 @@ def main():
     # next job on a low-priority one: the block scheduler hands free SMs to
     # the fetch first, the planner's persistent CTA needs only one
     fstream = torch.cuda.Stream(priority=-1 if args.prio else 0)  # lower = higher priority
+    rstream = torch.cuda.Stream(priority=-1 if args.prio else 0)  # replay + NCCL
     pstream = torch.cuda.Stream(priority=0)
     torch.cuda.set_stream(fstream)
     # the loader's pinned staging for the e2e path: two sets, so the plan of
     # job i+1 lands in one while job i's plan is uploaded from the other
     host_sets = [ls.plan_host_buffers(pc) for _ in range(2)] if not args.no_e2e else None
 
+    sh_items = int(sh.total_items)
+    # multi-GPU plan placement: "rr" plans job i on GPU i mod N only and
+    # broadcasts its node lists; "replicate" plans every job on every GPU
+    plan_shard = args.plan_shard == "rr" or (args.plan_shard == "auto" and world > 2)
+
     def run_jobs(n, host=False, pipeline=True, stats=None, t_start=None):
         """n passes of the hot path. Job i = plan (K1-K6) -> replay (K7, this
         GPU's ranks, all-gather of the rows) -> fetch (K8/K9, every step of
-        this GPU's ranks). With `pipeline` the plan of job i+1 runs on its own
-        stream (one persistent CTA) from a helper thread while job i's replay
-        and fetch run on the remaining SMs; every job's work is complete when
-        the call returns. host=True is the e2e path: the plan lands in pinned
-        host memory (lsg_plan_host) and is uploaded for the replay, the
+        this GPU's ranks), as three pipelined stages on three streams:
+          planner thread   plans (the step loop is ONE persistent CTA);
+          replayer thread  node-list broadcast (N>1, rr placement), replay
+                           and the row all-gather (all NCCL calls);
+          this thread      the batch fetch of every step.
+        With `pipeline` job i+1's plan and replay overlap job i's fetch on the
+        remaining SMs; every job's work is complete when the call returns.
+        With the rr placement job i is planned once, on GPU i mod N, and its
+        node lists are broadcast over NVLink: jobs are independent units, so
+        the plan stream shards across GPUs although one plan's step
+        recurrence does not. host=True is the e2e path: the plan lands in
+        pinned host memory (lsg_plan_host) and is uploaded by its GPU, the
         hit/miss rows are read back to the host."""
         import queue
-        q = queue.Queue(maxsize=1)
+        qp, qr = queue.Queue(maxsize=1), queue.Queue(maxsize=1)
         free = threading.Semaphore(2)
+        fetched = threading.Semaphore(2 if pipeline else 1)  # replayed jobs ahead of the fetch
         err = []
+        shard = world > 1 and plan_shard
+        mine = [i for i in range(n) if not shard or i % world == rank]
 
         def planner():
             try:
@@ -234,60 +257,94 @@ def main():
                 with torch.cuda.stream(pstream):
                     if t_start is not None:
                         pstream.wait_event(t_start)
-                    for i in range(n):
+                    for j, i in enumerate(mine):
                         free.acquire()
                         a, z = ev(), ev()
                         a.record(pstream)
-                        out = (ls.plan_schedule_host(pc, buffers=host_sets[i % 2]) if host
+                        out = (ls.plan_schedule_host(pc, buffers=host_sets[j % 2]) if host
                                else ls.plan_schedule(pc))
                         z.record(pstream)
-                        q.put((out, a, z, i % 2))
+                        qp.put((out, a, z))
                         if not pipeline:
                             z.synchronize()
             except BaseException as e:  # surfaced on the main thread
                 err.append(e)
-                q.put(None)
+                qp.put(None)
 
-        th = threading.Thread(target=planner, daemon=True)
-        th.start()
         rows = []
+
+        def replayer():
+            try:
+                torch.cuda.set_device(dev)
+                with torch.cuda.stream(rstream):
+                    if t_start is not None:
+                        rstream.wait_event(t_start)
+                    for i in range(n):
+                        owner = i % world if shard else rank
+                        pa = pz = None
+                        if owner == rank:
+                            got = qp.get()
+                            if got is None:
+                                raise err[0]
+                            out, pa, pz = got
+                            rstream.wait_event(pz)
+                            plan = out.plan
+                            if host:  # the plan lives in host memory: upload for the replay
+                                items = plan.items.to(dev, non_blocking=True)
+                                noff = plan.node_off.to(dev, non_blocking=True)
+                            else:  # device outputs of the plan stream
+                                items, noff = plan.items, plan.node_off
+                                for t in (items, noff):
+                                    t.record_stream(rstream)
+                        else:
+                            items = torch.empty(sh_items, dtype=torch.int32, device=dev)
+                            noff = torch.empty((T, N + 1), dtype=torch.int32, device=dev)
+                        fetched.acquire()
+                        f0 = ev()
+                        f0.record(rstream)
+                        if shard:  # the owner's node lists to every GPU
+                            dist.broadcast(items, src=owner)
+                            dist.broadcast(noff, src=owner)
+                        plan = ls.SchedulePlan(D, N, b, int(sh.steps_per_epoch), None, items, noff, None, None)
+                        sim = ls.simulate_plan(plan, C, node_range=(k0, k1), want_slots=True)
+                        combine_rows(sim.hits, sim.misses)
+                        if host:
+                            rows.append((sim.hits.cpu(), sim.misses.cpu()))  # d2h of the step results
+                        off = noff.cpu().numpy()
+                        if owner == rank:
+                            free.release()  # this job's host staging set has been uploaded
+                        f1 = ev()
+                        f1.record(rstream)
+                        for t in (items, noff, sim.slots):
+                            t.record_stream(fstream)
+                        qr.put((plan, sim, off, pa, pz, f0, f1))
+            except BaseException as e:
+                err.append(e)
+                qr.put(None)
+
+        ths = [threading.Thread(target=planner, daemon=True), threading.Thread(target=replayer, daemon=True)]
+        for th in ths:
+            th.start()
         for i in range(n):
-            got = q.get()
+            got = qr.get()
             if got is None:
                 raise err[0]
-            out, pa, pz, hs = got
-            fstream.wait_event(pz)
-            plan = out.plan
-            if host:  # the plan lives in host memory; the device copy feeds the replay
-                items = plan.items.to(dev, non_blocking=True)
-                noff = plan.node_off.to(dev, non_blocking=True)
-                off = plan.node_off.numpy().copy()  # the staging set is recycled below
-                plan = ls.SchedulePlan(plan.dataset_size, N, b, plan.steps_per_epoch, plan.order, items,
-                                       noff, plan.fetches_before, plan.fetches_after)
-            else:  # device outputs of the plan stream, used on this stream
-                for t in (plan.items, plan.node_off):
-                    t.record_stream(fstream)
-            f0 = ev()
-            f0.record(fstream)
-            sim = ls.simulate_plan(plan, C, node_range=(k0, k1), want_slots=True)
-            combine_rows(sim.hits, sim.misses)
-            if host:
-                rows.append((sim.hits.cpu(), sim.misses.cpu()))  # d2h of the step results
-            else:
-                off = plan.node_off.cpu().numpy()
-            free.release()  # the host staging set of this job has been consumed
-            f1 = ev()
-            f1.record(fstream)
+            plan, sim, off, pa, pz, f0, f1 = got
             if int((off[:, k0 + 1:k1 + 1] - off[:, k0:k1]).max()) > maxlen:
                 raise SystemExit("a node list exceeds the batch tensor rows")
+            fstream.wait_event(f1)
+            f1b = ev()
+            f1b.record(fstream)
             fetcher.fetch_steps(plan, sim.slots, off)
             f2 = ev()
             f2.record(fstream)
             if stats is not None:
-                stats.append((pa, pz, f0, f1, f2, sim, off))
+                stats.append((pa, pz, f0, f1, f2, sim, off, f1b))
             if not pipeline:
                 f2.synchronize()
-        th.join()
+            fetched.release()
+        for th in ths:
+            th.join()
         return rows
 
     # warm-up (also the first pass that fills the HBM buffers)
@@ -327,9 +384,10 @@ def main():
         torch.cuda.synchronize()
     launches = ls.lib().lsg_launch_count() - launches0
     total_ms = t_start.elapsed_time(t_end)
-    plan_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    own = [e[0].elapsed_time(e[1]) for e in evs if e[0] is not None]
+    plan_ms = statistics.mean(own) if own else 0.0
     replay_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
-    fetch_ms = statistics.mean(e[3].elapsed_time(e[4]) for e in evs)
+    fetch_ms = statistics.mean(e[7].elapsed_time(e[4]) for e in evs)
     del evs
     # one job alone (no overlap): the latency of a single plan+replay+fetch pass
     serial = []
@@ -406,9 +464,13 @@ def main():
             "config": {"workload": f"cfg2: D={D} E={E} N={N} b={b} C={C} (20%/rank), 256 KiB samples, "
                                    f"plan+replay+fetch of the whole job",
                        "global_batch": N * b, "ranks_per_gpu": k1 - k0,
-                       "parallelism": f"plan replicated; replay+fetch sharded {k1 - k0} ranks/GPU",
+                       "parallelism": (f"jobs' plans round-robin over {world} GPUs (node lists broadcast, NCCL); "
+                                       if world > 1 and plan_shard else
+                                       "plan replicated per GPU; " if world > 1 else "")
+                                      + f"replay+fetch sharded {k1 - k0} ranks/GPU",
                        "l2": "inputs > L2 (12.8 GiB HBM sample buffer per rank)"},
-            "pipeline": "job i+1's plan (1 persistent CTA, own stream) overlaps job i's replay+fetch; "
+            "pipeline": "plan / replay / fetch on three streams: later jobs' plans (1 persistent CTA) and replays "
+                        "overlap job i's fetch; "
                         "every job's full work is inside the timed region",
             "plan_ms": plan_ms, "replay_ms": replay_ms, "fetch_ms": fetch_ms,
             "single_job_ms": job_ms, "single_job_samples_per_s": A / (job_ms * 1e-3) if job_ms else None,

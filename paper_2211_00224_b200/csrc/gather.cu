@@ -145,6 +145,7 @@ struct StepFetch {
     uint64_t vec_per_row, tiles_per_row, seed;
     uint32_t* mlist;           // miss rows of the step (filled by the TMA hit kernel) or null
     uint32_t* mctl;            // [3] miss count, finished misses blocks, hit-tile chunks claimed
+    int l2hint;                // TMA copies tagged L2::evict_first (streaming)
 };
 
 __device__ __forceinline__ uint32_t node_of_row(const StepFetch& f, uint32_t r) {
@@ -216,6 +217,10 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
         tb = uint64_t(blockIdx.x) * per;
         te = min(nt, tb + per);
     }
+    // the gathered bytes stream through L2 once: evict-first, so a planner
+    // running beside the fetch keeps its working set in L2
+    uint64_t pol = 0;
+    if (f.l2hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     uint64_t cur = ~0ull;  // row of the cached descriptor
     const unsigned char* src_row = nullptr;
     unsigned char* dst_row = nullptr;
@@ -254,8 +259,13 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
         const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
         const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(tsm + q * kTmaTile));
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kTmaTile));
-        asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(d), "l"(src_row + c), "r"(kTmaTile), "r"(b) : "memory");
+        if (f.l2hint)
+            asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                         " [%0], [%1], %2, [%3], %4;"
+                         ::"r"(d), "l"(src_row + c), "r"(kTmaTile), "r"(b), "l"(pol) : "memory");
+        else
+            asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(d), "l"(src_row + c), "r"(kTmaTile), "r"(b) : "memory");
         sdst[q] = dst_row + c;
         return true;
     };
@@ -270,8 +280,12 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
             asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
                          : "=r"(done) : "r"(b), "r"(par));
         const unsigned sp = static_cast<unsigned>(__cvta_generic_to_shared(tsm + q * kTmaTile));
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst[q]), "r"(sp),
-                     "r"(kTmaTile) : "memory");
+        if (f.l2hint)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                         ::"l"(sdst[q]), "r"(sp), "r"(kTmaTile), "l"(pol) : "memory");
+        else
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst[q]), "r"(sp),
+                         "r"(kTmaTile) : "memory");
         asm volatile("cp.async.bulk.commit_group;");
         // stage k+S-L goes into the slot of stage k-L: fresh while k < L,
         // else free once that stage's store has read it
@@ -348,7 +362,12 @@ int miss_list(uint64_t rows, cudaStream_t st, uint32_t** list, uint32_t** ctl) {
 
 // TMA gather when rows are whole tiles (LSG_GATHER_LSU=1 keeps the 128-bit
 // load/store kernel, for comparison)
-int launch_hits(const StepFetch& f, uint64_t rows, uint64_t sample_bytes, cudaStream_t st, bool* tma = nullptr) {
+int launch_hits(StepFetch f, uint64_t rows, uint64_t sample_bytes, cudaStream_t st, bool* tma = nullptr) {
+    static const int l2hint = [] {
+        const char* e = std::getenv("LSG_FETCH_L2HINT");
+        return e && e[0] == '1' ? 1 : 0;  // measured: no gain beside the planner (default off)
+    }();
+    f.l2hint = l2hint;
     if (tma) *tma = false;
     static const bool lsu = [] {
         const char* e = std::getenv("LSG_GATHER_LSU");
@@ -385,7 +404,7 @@ int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* 
     if (k1 <= k0) return kOk;
     if (sample_bytes == 0 || sample_bytes % 16 != 0)
         return set_error(kValidation, "fetch_step: sample_bytes must be a positive multiple of 16");
-    StepFetch f;
+    StepFetch f{};
     f.items = d_items;
     f.slots = d_slots;
     f.node_off = d_node_off;
