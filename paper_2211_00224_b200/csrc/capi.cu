@@ -92,6 +92,50 @@ void keep_pool() {
     done_mask.fetch_or(bit);
 }
 
+bool l2_pin(cudaStream_t st, const void* p, size_t bytes) {
+    static int on = -1;
+    if (on < 0) {
+        // measured (tools/replay_probe.py): pinning the replay's state made
+        // both the replay and a planner beside a streaming fetch slower
+        // (replay 232 -> 450 ms), so the window is opt-in
+        const char* e = std::getenv("LSG_L2PIN");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (!on || !p || bytes == 0) return false;
+    int dev = 0, maxp = 0, maxw = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (maxp <= 0 || maxw <= 0) return false;
+    static std::atomic<uint64_t> limit_set{0};  // per device: set-aside configured once
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(limit_set.load() & bit)) {
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, size_t(maxp)) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        limit_set.fetch_or(bit);
+    }
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(p);
+    v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, size_t(maxw));
+    v.accessPolicyWindow.hitRatio = float(std::min<double>(1.0, double(maxp) / double(v.accessPolicyWindow.num_bytes)));
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    if (cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+
+void l2_unpin(cudaStream_t st) {
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaGetLastError();
+}
+
 bool profiling() {
     static int on = -1;
     if (on < 0) {

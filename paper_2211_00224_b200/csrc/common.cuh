@@ -75,6 +75,14 @@ struct Scratch {
     }
 };
 
+// L2 set-aside for a latency-bound kernel's random-access state (LSG_L2PIN=1,
+// default off: measured slower): kernels launched on `st` until l2_unpin see [p, p + bytes) as
+// a persisting access-policy window, so a fetch streaming through L2 beside
+// them does not evict their lines. Returns false (and does nothing) when the
+// device has no persisting L2 or the feature is off.
+bool l2_pin(cudaStream_t st, const void* p, size_t bytes);
+void l2_unpin(cudaStream_t st);
+
 struct PlanDims {
     uint64_t D, B, S, keep, T;
     uint32_t N, E, b;

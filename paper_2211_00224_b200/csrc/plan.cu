@@ -52,6 +52,7 @@ constexpr uint32_t kFetch = 0xFFFFFFFFu;
 constexpr uint32_t kDmv = 32;       // G: moves per donor kept in shared memory
 constexpr uint32_t kNotMoved = 0xFFFFFFFFu;
 constexpr uint32_t kWinWords = 40;  // I1 bucket-bit window (covers 2S <= 1216 steps)
+constexpr uint32_t kPk16B = 2048;   // D8 with 16-bit packed keys below this local batch
 
 // ----------------------------------------------------------------- K5 ----
 // nu for the access of x at execution epoch i, position pos: the first
@@ -486,9 +487,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
 #pragma unroll
                         for (uint32_t k = 0; k < 8; ++k)
                             t[k] = ((k < N && ((m >> k) & 1u)) ? min(b, t[k] + sm.wcnt[w][k]) : b) << 4 | k;
-                        uint4* dst = reinterpret_cast<uint4*>(a.sx + size_t(mi) * 8);
-                        dst[0] = make_uint4(t[0], t[1], t[2], t[3]);
-                        dst[1] = make_uint4(t[4], t[5], t[6], t[7]);
+                        if (b < kPk16B) {  // 16-bit keys, two nodes per word
+                            reinterpret_cast<uint4*>(a.sx)[mi] = make_uint4(
+                                t[0] | t[1] << 16, t[2] | t[3] << 16, t[4] | t[5] << 16, t[6] | t[7] << 16);
+                        } else {
+                            uint4* dst = reinterpret_cast<uint4*>(a.sx + size_t(mi) * 8);
+                            dst[0] = make_uint4(t[0], t[1], t[2], t[3]);
+                            dst[1] = make_uint4(t[4], t[5], t[6], t[7]);
+                        }
                     } else {
                         for (uint32_t k = 0; k < N; ++k)
                             a.sx[size_t(mi) * N + k] =
@@ -516,6 +522,87 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 if (lane < N) sm.mtot[lane] = 0;
             }
             for (int drep = 0; drep < ((a.dbg_skip & 2) ? 2 : 1); ++drep)  // timing: D is idempotent
+            if (kD8 && w == 0 && !(a.dbg_skip & 1) && b < kPk16B) {
+                // N <= 8 and b < 2048: the register decision below with the
+                // 8 keys packed two per word (16 bits: (S + M) << 4 | k stays
+                // below 2^16), so a key row is ONE broadcast 16-byte load, the
+                // minimum is two VIMNMX3.U16x2 plus one 32-bit min, and the
+                // winner's count moves by a per-pair increment: ~23
+                // instructions per item instead of ~38 on the serial chain.
+                uint32_t M01 = 0, M23 = 0, M45 = 0, M67 = 0;  // (M_k << 4) per 16-bit half
+                unsigned long long dchain = 0;
+                const uint32_t nm = sm.nmulti;
+                const uint32_t kSent = (b << 4) - 1u;
+                const uint32_t kSent2 = kSent | kSent << 16;
+                auto stage = [&](uint32_t base, uint32_t buf) {
+                    const uint32_t cnt = min(32u, nm - base);
+                    const uint4* src = reinterpret_cast<const uint4*>(a.sx) + base;
+                    uint4* dst4 = reinterpret_cast<uint4*>(&sm.stg[buf][0][0]);
+                    if (lane < cnt) {
+                        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst4 + lane));
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + lane));
+                    } else {  // padding rows: no candidate
+                        const uint32_t p = b << 4;
+                        dst4[lane] = make_uint4(p | (p | 1) << 16, (p | 2) | (p | 3) << 16, (p | 4) | (p | 5) << 16,
+                                                (p | 6) | (p | 7) << 16);
+                    }
+                    asm volatile("cp.async.commit_group;\n" ::);
+                };
+                if (nm) stage(0, 0);
+                for (uint32_t base = 0, buf = 0; base < nm; base += 32, buf ^= 1) {
+                    if (base + 32 < nm) {
+                        stage(base + 32, buf ^ 1);
+                        asm volatile("cp.async.wait_group 1;\n" ::);
+                    } else {
+                        asm volatile("cp.async.wait_group 0;\n" ::);
+                    }
+                    __syncwarp();
+                    const uint32_t cnt = min(32u, nm - base);
+                    const uint32_t myj = lane < cnt ? s.pre[base + lane] : 0u;
+                    const uint4* rows = reinterpret_cast<const uint4*>(&sm.stg[buf][0][0]);
+                    uint32_t myres = kSent;
+                    const unsigned long long tc0 = a.prof ? clock64() : 0ull;
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        const uint4 r = rows[u];
+                        const uint32_t m2 = __vimin3_u16x2(__vimin3_u16x2(r.x + M01, r.y + M23, r.z + M45),
+                                                           r.w + M67, kSent2);
+                        const uint32_t cl = min(m2 & 0xFFFFu, m2 >> 16);
+                        const uint32_t inc = (cl & 1u) ? 0x100000u : 0x10u;  // odd nodes: high half
+                        const uint32_t pr = (cl >> 1) & 7u;                  // pair; 7 = none (kSent)
+                        M01 += pr == 0 ? inc : 0u;
+                        M23 += pr == 1 ? inc : 0u;
+                        M45 += pr == 2 ? inc : 0u;
+                        M67 += pr == 3 ? inc : 0u;
+                        myres = lane == uint32_t(u) ? cl : myres;
+                    }
+                    if (a.prof) {
+                        const uint32_t dep = myres & 1u;  // keep the timer after the chain
+                        const unsigned long long tc1 = clock64() + dep;
+                        if (lane == 0) dchain += tc1 - tc0;
+                    }
+                    if (lane < cnt) {
+                        if (myres != kSent) {
+                            const uint32_t kk = myres & 15u, c = myres >> 4;
+                            const uint32_t Sk =
+                                reinterpret_cast<const uint16_t*>(&sm.stg[buf][0][0])[lane * 8 + kk] >> 4;
+                            s.fin[kk * b + (c - Sk)] = myj;
+                            s.sinfo[myj] = (c << 5) | kk;  // consumed by E
+                        } else {
+                            s.sinfo[myj] = 0xFFFFFFFFu;
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (a.prof && lane == 0) {
+                    atomicAdd(&a.prof[12], (unsigned long long)nm);
+                    atomicAdd(&a.prof[13], dchain);
+                }
+                const uint32_t Mp[4] = {M01, M23, M45, M67};
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (lane == uint32_t(k) && uint32_t(k) < N) sm.mtot[k] = ((Mp[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) >> 4;
+            } else
             if (kD8 && w == 0 && !(a.dbg_skip & 1)) {
                 // N <= 8: no warp reduction at all. Every lane runs the same
                 // serial decision on registers: node k's running count is
@@ -801,7 +888,58 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
             uint32_t c = lane < N ? sm.fcnt[lane] : 0u;
             if (a.fb && lane < N) a.fb[size_t(g) * N + lane] = c;
             uint32_t outc = 0, inn = 0, nmv = 0;
-            while (a.balance) {
+            const bool in = lane < N;
+            bool rounds = a.balance;
+            if (a.balance) {
+                // closed form (as wide_balance_cf, plan_wide.cu): with L = F / N
+                // the loop consumes donor units (k gives one at count l) in
+                // (l desc, k asc) order and recipient units in (l asc, k asc)
+                // order and pairs the t-th of each; mandatory units are the
+                // donor levels >= L+2 and recipient levels <= L-1, the shorter
+                // side padded at level L+1 (donors) / L (recipients) in node
+                // order. Recipient units are tabled in the (free) D staging.
+                const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, in ? c : 0u);
+                const uint32_t mn = __reduce_min_sync(0xFFFFFFFFu, in ? c : 0xFFFFFFFFu);
+                const uint32_t F = __reduce_add_sync(0xFFFFFFFFu, in ? c : 0u);
+                const uint32_t L = F / N;
+                const uint32_t dm = __reduce_add_sync(0xFFFFFFFFu, in && c > L + 1 ? c - L - 1 : 0u);
+                const uint32_t rm = __reduce_add_sync(0xFFFFFFFFu, in && c < L ? L - c : 0u);
+                const uint32_t mv = max(dm, rm), od = mv - dm, orr = mv - rm;
+                uint32_t* urq = &sm.stg[0][0][0];
+                if (mx - mn <= 1) {
+                    rounds = false;
+                } else if (mv <= 2u * 32u * kMaxN) {
+                    rounds = false;
+                    uint32_t t = 0;
+                    for (uint32_t l = mn; l <= L; ++l) {
+                        const uint32_t br = __ballot_sync(0xFFFFFFFFu, in && c <= l);
+                        const uint32_t lim = l < L ? 32u : orr;
+                        const uint32_t rk = __popc(br & lt);
+                        if (in && c <= l && rk < lim) {
+                            urq[t + rk] = lane | ((l - c) << 8);
+                            ++inn;
+                        }
+                        t += min(uint32_t(__popc(br)), lim);
+                    }
+                    __syncwarp();
+                    t = 0;
+                    for (uint32_t l = mx; l >= L + 1; --l) {
+                        const uint32_t bd = __ballot_sync(0xFFFFFFFFu, in && c >= l);
+                        const uint32_t lim = l > L + 1 ? 32u : od;
+                        const uint32_t rk = __popc(bd & lt);
+                        if (in && c >= l && rk < lim) {
+                            const uint32_t rq = urq[t + rk];
+                            if (outc < kDmv) sm.dmv[lane][outc] = rq;
+                            else a.dmoves[size_t(lane) * a.B + outc] = rq;
+                            ++outc;
+                        }
+                        t += min(uint32_t(__popc(bd)), lim);
+                    }
+                    nmv = mv;
+                    c = c - outc + inn;
+                }
+            }
+            while (rounds) {  // very wide count spread: the round simulation
                 const uint32_t M = __reduce_max_sync(0xFFFFFFFFu, lane < N ? c : 0u);
                 const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, lane < N ? c : 0xFFFFFFFFu);
                 if (M - m <= 1) break;

@@ -1058,13 +1058,18 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     // per-node state is indexed by absolute node id; allocate N rows
     a.nuk = sc.get<uint32_t>(total);
     a.last = sc.get<uint32_t>(size_t(N) * D);
-    a.key = sc.get<uint32_t>(size_t(N) * D);
-    a.slot = sc.get<uint32_t>(size_t(N) * D);
-    a.nz = sc.get<uint32_t>(size_t(N) * a.nzw);
+    // the forward replay's random-access state in ONE block (key, slot, the
+    // never-used bitmaps, the step bitmap), so an L2 access-policy window can
+    // pin it while a fetch streams through L2 beside the replay
+    a.sumw = (uint32_t((D + 31) / 32) + 31) / 32;
+    const size_t hot_words = size_t(N) * D * 2 + size_t(N) * a.infw + size_t(N) * a.sumw + size_t(N) * a.nzw;
+    uint32_t* hot = sc.get<uint32_t>(hot_words);
+    a.key = hot;
+    a.slot = hot ? hot + size_t(N) * D : nullptr;
+    a.infbm = hot ? a.slot + size_t(N) * D : nullptr;
+    a.infsum = hot ? a.infbm + size_t(N) * a.infw : nullptr;
+    a.nz = hot ? a.infsum + size_t(N) * a.sumw : nullptr;
     a.pbm = L > 128 ? nullptr : sc.get<uint32_t>(size_t(N) * T * a.bw);
-    a.infbm = sc.get<uint32_t>(size_t(N) * a.infw);
-    a.sumw = (a.infw + 31) / 32;
-    a.infsum = sc.get<uint32_t>(size_t(N) * a.sumw);
     a.fstack = d_slot ? sc.get<uint32_t>(size_t(N) * std::min<uint64_t>(C, D)) : nullptr;
     if (!a.nuk || !a.last || !a.key || !a.slot || !a.nz || (L <= 128 && !a.pbm) || !a.infbm || !a.infsum || (d_slot && !a.fstack))
         return set_error(kInternal, "simulate: scratch allocation failed");
@@ -1121,8 +1126,10 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         LSG_LAUNCH_CHECK("k_replay_nextuse_cta");
         const size_t smem = size_t(L) * 4 + (L + 2) * 2 + 16;
         LSG_CUDA(cudaFuncSetAttribute(k_replay_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const bool pinned = l2_pin(st, hot, hot_words * 4);
         k_replay_cta<<<nk, kRT, smem, st>>>(c);
         LSG_LAUNCH_CHECK("k_replay_cta");
+        if (pinned) l2_unpin(st);
         return kOk;
     }
     const unsigned grid = (nk + kRWarps - 1) / kRWarps;
