@@ -91,6 +91,10 @@ struct ReplayArgs {
     uint32_t* slot;    // [N][D]
     uint32_t* nz;      // [N][nzw] next-use steps that may hold residents
     uint32_t* pbm;     // [N][T][bw] list positions per next-use step
+    uint32_t* psum;    // [N][psw] non-empty pbm words
+    uint32_t psw;
+    uint32_t* psum2;   // [N][ps2w] non-empty psum words
+    uint32_t ps2w;
     uint32_t* infbm;   // [N][infw]
     uint32_t* infsum;  // [N][sumw] non-empty infbm words
     uint32_t sumw;
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay_nextuse(ReplayArgs a) {
 
 // Warp-uniform node state (every lane holds the same values).
 struct NodeState {
-    uint32_t size, top, inftop, infcnt, fresh, nfree;
+    uint32_t size, top, inftop, infcnt, fresh, nfree, ptop;
 };
 
 // Take the `want` largest ids of a node's never-used bitmap (whole warp).
@@ -141,9 +145,14 @@ struct NodeState {
 // the highest; prefix sums of their popcounts tell each lane how many of its
 // word's top bits go. Freed slots are pushed in eviction order (descending
 // id). Returns the ids taken; `top` stays an upper bound of the highest word.
-__device__ __forceinline__ uint32_t never_take(uint32_t* bm, uint32_t* sm1, uint32_t& top, uint32_t want,
-                                               uint32_t* keyk, uint32_t* slotk, uint32_t* fs, uint32_t& nfree,
-                                               uint32_t* wbuf, uint32_t lane) {
+// bm_take generalises it to any summarised bitmap whose bit (word w, bit) names
+// a resident through `idof`: the never-used id bitmap (identity) and the
+// per-node key-space bitmap of finite keys (pbm, key = (step, list position),
+// see key_take below).
+template <class IdOf>
+__device__ __forceinline__ uint32_t bm_take(uint32_t* bm, uint32_t* sm1, uint32_t* sm2, uint32_t& top, uint32_t want,
+                                            IdOf idof, uint32_t* keyk, uint32_t* slotk, uint32_t* fs, uint32_t& nfree,
+                                            uint32_t* wbuf, uint32_t lane) {
     const uint32_t lt = lanemask_lt_r();
     uint32_t taken = 0;
     int32_t cur = int32_t(top);  // highest bm word still to visit
@@ -152,7 +161,33 @@ __device__ __forceinline__ uint32_t never_take(uint32_t* bm, uint32_t* sm1, uint
         uint32_t ngot = 0;
         int32_t sw = cur >> 5;
         uint32_t firstmask = (cur & 31) == 31 ? 0xFFFFFFFFu : ((2u << (cur & 31)) - 1u);
+        bool skip = sm2 != nullptr;  // entering a possibly empty stretch
         while (ngot < 32 && sw >= 0) {
+            if (skip) {
+                // second summary level (one bit per non-empty sm1 word): jump to
+                // the highest non-empty sm1 word <= sw, 1,024 sm1 words per round
+                int32_t s2 = sw >> 5, found = -1;
+                uint32_t m2 = (sw & 31) == 31 ? 0xFFFFFFFFu : ((2u << (sw & 31)) - 1u);
+                while (s2 >= 0) {
+                    const int32_t my2 = s2 - int32_t(lane);
+                    uint32_t v2 = my2 >= 0 ? __ldcg(&sm2[my2]) : 0u;
+                    if (lane == 0) v2 &= m2;
+                    const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, v2 != 0);
+                    if (b2) {
+                        const uint32_t src = __ffs(b2) - 1;
+                        const uint32_t word = __shfl_sync(0xFFFFFFFFu, v2, src);
+                        found = (s2 - int32_t(src)) * 32 + int32_t(31 - __clz(word));
+                        break;
+                    }
+                    s2 -= 32;
+                    m2 = 0xFFFFFFFFu;
+                }
+                if (found < 0) break;
+                if (found < sw) {
+                    sw = found;
+                    firstmask = 0xFFFFFFFFu;
+                }
+            }
             const int32_t myws = sw - int32_t(lane);
             uint32_t v = myws >= 0 ? __ldcg(&sm1[myws]) : 0u;
             if (lane == 0) v &= firstmask;
@@ -169,7 +204,9 @@ __device__ __forceinline__ uint32_t never_take(uint32_t* bm, uint32_t* sm1, uint
                 v &= ~(1u << bit);
                 wbuf[r++] = uint32_t(myws) * 32 + bit;
             }
-            ngot += __shfl_sync(0xFFFFFFFFu, incl, 31);
+            const uint32_t found1 = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            ngot += found1;
+            skip = sm2 != nullptr && found1 == 0;
             sw -= 32;
             firstmask = 0xFFFFFFFFu;
         }
@@ -190,12 +227,22 @@ __device__ __forceinline__ uint32_t never_take(uint32_t* bm, uint32_t* sm1, uint
         const uint32_t before = incl - cnt, left = want - taken;
         const uint32_t take = before < left ? min(cnt, left - before) : 0u;
         // pass 1: which of my taken ids hold a slot (a miss of the current
-        // run has none yet)
+        // run has none yet). Ids of the word's top `take` bits, 4 at a time so
+        // their loads overlap (the key-space bitmap maps a bit to a list item)
+        const uint64_t wb = myw >= 0 ? uint64_t(idof.base(uint32_t(myw))) : 0ull;
         uint32_t rest = v, pushes = 0;
-        for (uint32_t t = 0; t < take; ++t) {
-            const uint32_t bit = 31 - __clz(rest);
-            rest &= ~(1u << bit);
-            if (fs && __ldcg(&slotk[uint32_t(myw) * 32 + bit]) != kNone) ++pushes;
+        for (uint32_t t = 0; t < take; t += 4) {
+            uint32_t xs[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool on = t + u < take;
+                const uint32_t bit = on ? 31 - __clz(rest) : 0u;
+                if (on) rest &= ~(1u << bit);
+                xs[u] = on ? idof.id(wb, bit) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (t + u < take && fs && __ldcg(&slotk[xs[u]]) != kNone) ++pushes;
         }
         uint32_t pinc = pushes;
 #pragma unroll
@@ -205,20 +252,33 @@ __device__ __forceinline__ uint32_t never_take(uint32_t* bm, uint32_t* sm1, uint
         }
         uint32_t q = nfree + pinc - pushes;
         rest = v;
-        for (uint32_t t = 0; t < take; ++t) {
-            const uint32_t bit = 31 - __clz(rest);
-            rest &= ~(1u << bit);
-            const uint32_t x = uint32_t(myw) * 32 + bit;
-            keyk[x] = kNone;
-            const uint32_t sl = slotk[x];
-            if (sl != kNone) {
-                if (fs) fs[q++] = sl;
-                slotk[x] = kNone;
+        for (uint32_t t = 0; t < take; t += 4) {
+            uint32_t xs[4], sls[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool on = t + u < take;
+                const uint32_t bit = on ? 31 - __clz(rest) : 0u;
+                if (on) rest &= ~(1u << bit);
+                xs[u] = on ? idof.id(wb, bit) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) sls[u] = t + u < take ? slotk[xs[u]] : kNone;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (t + u >= take) break;
+                keyk[xs[u]] = kNone;
+                if (sls[u] != kNone) {
+                    if (fs) fs[q++] = sls[u];
+                    slotk[xs[u]] = kNone;
+                }
             }
         }
         if (take) {
             bm[myw] = rest;
-            if (rest == 0) atomicAnd(&sm1[myw >> 5], ~(1u << (myw & 31)));
+            if (rest == 0) {
+                const uint32_t old1 = atomicAnd(&sm1[myw >> 5], ~(1u << (myw & 31)));
+                if (sm2 && (old1 & ~(1u << (myw & 31))) == 0) atomicAnd(&sm2[myw >> 10], ~(1u << ((myw >> 5) & 31)));
+            }
         }
         nfree += __shfl_sync(0xFFFFFFFFu, pinc, 31);
         const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
@@ -234,6 +294,45 @@ __device__ __forceinline__ uint32_t never_take(uint32_t* bm, uint32_t* sm1, uint
     top = cur < 0 ? 0u : uint32_t(cur);
     __syncwarp();
     return taken;
+}
+
+struct IdIdentity {
+    __device__ __forceinline__ uint32_t base(uint32_t w) const { return w * 32; }
+    __device__ __forceinline__ uint32_t id(uint64_t b, uint32_t bit) const { return uint32_t(b) + bit; }
+};
+
+__device__ __forceinline__ uint32_t never_take(uint32_t* bm, uint32_t* sm1, uint32_t& top, uint32_t want,
+                                               uint32_t* keyk, uint32_t* slotk, uint32_t* fs, uint32_t& nfree,
+                                               uint32_t* wbuf, uint32_t lane) {
+    return bm_take(bm, sm1, nullptr, top, want, IdIdentity{}, keyk, slotk, fs, nfree, wbuf, lane);
+}
+
+// Finite keys: node k's (step, list position) bitmap is bw words per step, so
+// word w = beta * bw + p / 32 and the resident is the item at position p of
+// the node's list at step beta. The summary (one bit per non-empty pbm word)
+// lets an eviction take the largest keys 32 words per round, whatever the
+// spread of next-use steps (a walk bucket by bucket pays a round trip per
+// step holding residents: cfg5, 1,000 epochs).
+struct IdOfKey {
+    const uint32_t* items;
+    const uint32_t* node_off;
+    const uint64_t* gb;
+    uint32_t N, k, bw;
+    // item index of the word's bit 0 (64-bit plans: the item array offset)
+    __device__ __forceinline__ uint64_t base(uint32_t w) const {
+        const uint32_t beta = w / bw;
+        return __ldg(&gb[beta]) + __ldg(&node_off[size_t(beta) * (N + 1) + k]) + (w - beta * bw) * 32;
+    }
+    __device__ __forceinline__ uint32_t id(uint64_t b, uint32_t bit) const { return __ldg(&items[b + bit]) & ~kHit; }
+};
+
+__device__ __forceinline__ void key_mark(uint32_t* pbmk, uint32_t* psumk, uint32_t* psum2k, uint32_t bw, uint32_t L,
+                                         uint32_t nu) {
+    const uint32_t beta = nu / L, p = nu - beta * L;
+    const uint32_t w = beta * bw + (p >> 5);
+    atomicOr(&pbmk[w], 1u << (p & 31));
+    if (!(atomicOr(&psumk[w >> 5], 1u << (w & 31)) & (1u << (w & 31))))
+        atomicOr(&psum2k[w >> 10], 1u << ((w >> 5) & 31));
 }
 
 // Evict the `need` largest keys of node k (whole warp).
@@ -255,81 +354,16 @@ __device__ void r_evict(const ReplayArgs& a, NodeState& ns, uint32_t k, uint32_t
             need -= got;
             continue;
         }
-        uint32_t* nzk = a.nz + size_t(k) * a.nzw;
-        int32_t wi = int32_t(ns.top >> 5);
-        int32_t beta = -1;
-        while (wi >= 0) {
-            const int32_t myw = wi - int32_t(lane);
-            const uint32_t v = myw >= 0 ? __ldcg(&nzk[myw]) : 0u;
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, v != 0);
-            if (bal) {
-                const uint32_t src = __ffs(bal) - 1;
-                const uint32_t word = __shfl_sync(0xFFFFFFFFu, v, src);
-                beta = (wi - int32_t(src)) * 32 + (31 - __clz(word));
-                break;
-            }
-            wi -= 32;
-        }
-        if (beta < 0) {
+        const IdOfKey idof{a.items, a.node_off, a.gb, a.N, k, a.bw};
+        const uint32_t got = bm_take(a.pbm + size_t(k) * a.T * a.bw, a.psum + size_t(k) * a.psw,
+                                     a.psum2 + size_t(k) * a.ps2w, ns.ptop, need, idof,
+                                     keyk, slotk, fs, ns.nfree, wbuf, lane);
+        if (got == 0) {
             if (lane == 0) atomicOr(a.status, 4u);
             return;
         }
-        const uint64_t lbase = a.gb[beta] + a.node_off[size_t(beta) * (a.N + 1) + k];
-        uint32_t* pw = a.pbm + (size_t(k) * a.T + uint32_t(beta)) * a.bw;
-        bool left = false;
-        int32_t w1 = int32_t(a.bw) - 1;
-        // positions descending: lane t of a group holds word (w1 - t)
-        for (; w1 >= 0 && need > 0; w1 -= 32) {
-            const int32_t myw = w1 - int32_t(lane);
-            const uint32_t word = myw >= 0 ? __ldcg(&pw[myw]) : 0u;
-            const uint32_t cnt = __popc(word);
-            uint32_t inc = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-                if (lane >= uint32_t(d)) inc += o;
-            }
-            const uint32_t before = inc - cnt, total = __shfl_sync(0xFFFFFFFFu, inc, 31);
-            const uint32_t take = before < need ? min(cnt, need - before) : 0u;
-            // freed slots, in eviction order (deterministic)
-            uint32_t rest = word, pushes = 0;
-            for (uint32_t t = 0; t < take; ++t) {
-                const uint32_t bit = 31 - __clz(rest);
-                rest &= ~(1u << bit);
-                const uint32_t x = a.items[lbase + uint32_t(myw) * 32 + bit] & ~kHit;
-                keyk[x] = kNone;
-                pushes += (fs && slotk[x] != kNone) ? 1u : 0u;
-            }
-            uint32_t pinc = pushes;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, pinc, d);
-                if (lane >= uint32_t(d)) pinc += o;
-            }
-            if (pushes) {
-                uint32_t r2 = word, q = ns.nfree + pinc - pushes;
-                for (uint32_t t = 0; t < take; ++t) {
-                    const uint32_t bit = 31 - __clz(r2);
-                    r2 &= ~(1u << bit);
-                    const uint32_t x = a.items[lbase + uint32_t(myw) * 32 + bit] & ~kHit;
-                    const uint32_t s = slotk[x];
-                    if (s != kNone) {
-                        fs[q++] = s;
-                        slotk[x] = kNone;
-                    }
-                }
-            }
-            ns.nfree += __shfl_sync(0xFFFFFFFFu, pinc, 31);
-            if (myw >= 0 && rest != word) pw[myw] = rest;
-            left = left || (__ballot_sync(0xFFFFFFFFu, rest != 0) != 0);
-            const uint32_t took = min(total, need);
-            need -= took;
-            ns.size -= took;
-        }
-        __syncwarp();
-        if (w1 < 0 && !left && lane == 0) atomicAnd(&nzk[beta >> 5], ~(1u << (beta & 31)));
-        ns.top = uint32_t(beta);
-        __syncwarp();
+        ns.size -= got;
+        need -= got;
     }
 }
 
@@ -344,9 +378,8 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay(ReplayArgs a) {
     uint32_t* keyk = a.key + size_t(k) * a.D;
     uint32_t* slotk = a.slot + size_t(k) * a.D;
     uint32_t* fs = a.fstack ? a.fstack + size_t(k) * a.C : nullptr;
-    uint32_t* nzk = a.nz + size_t(k) * a.nzw;
     uint32_t* infk = a.infbm + size_t(k) * a.infw;
-    NodeState ns{0, 0, 0, 0, 0, 0};
+    NodeState ns{0, 0, 0, 0, 0, 0, 0};
     for (uint32_t g = 0; g < a.T; ++g) {
         const uint32_t* off = a.node_off + size_t(g) * (a.N + 1);
         const uint32_t o = off[k], len = off[k + 1] - o;
@@ -419,15 +452,15 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay(ReplayArgs a) {
                         atomicOr(&infk[x >> 5], 1u << (x & 31));
                         atomicOr(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
                     } else {
-                        const uint32_t beta = nu / a.L, p = nu - beta * a.L;
-                        atomicOr(&a.pbm[(size_t(k) * a.T + beta) * a.bw + (p >> 5)], 1u << (p & 31));
-                        atomicOr(&nzk[beta >> 5], 1u << (beta & 31));
+                        key_mark(a.pbm + size_t(k) * a.T * a.bw, a.psum + size_t(k) * a.psw,
+                                 a.psum2 + size_t(k) * a.ps2w, a.bw, a.L, nu);
                     }
                 }
                 const uint32_t nevb = __ballot_sync(0xFFFFFFFFu, nev);
                 ns.infcnt += __popc(nevb);
                 ns.inftop = max(ns.inftop, __reduce_max_sync(0xFFFFFFFFu, nev ? (x >> 5) : 0u));
-                ns.top = max(ns.top, __reduce_max_sync(0xFFFFFFFFu, (mine && !nev) ? nu / a.L : 0u));
+                ns.ptop = max(ns.ptop, __reduce_max_sync(0xFFFFFFFFu, (mine && !nev) ? (nu / a.L) * a.bw +
+                                                                               ((nu - (nu / a.L) * a.L) >> 5) : 0u));
                 if (!hitrun) {
                     ns.size += __popc(run);
                     if (!pending) run0 = c + first;
@@ -466,6 +499,12 @@ struct ReplayArgsCta {
     uint32_t* key;     // [N][D]
     uint32_t* slot;    // [N][D]
     uint32_t* nz;      // [N][nzw]
+    uint32_t* pbm;     // [N][T][bw] list positions per next-use step, or null (list scan)
+    uint32_t bw;
+    uint32_t* psum;    // [N][psw] non-empty pbm words
+    uint32_t psw;
+    uint32_t* psum2;   // [N][ps2w] non-empty psum words
+    uint32_t ps2w;
     uint32_t* infbm;   // [N][infw]
     uint32_t* infsum;  // [N][sumw] non-empty infbm words
     uint32_t sumw;
@@ -515,7 +554,7 @@ __global__ void __launch_bounds__(kRT) k_replay_nextuse_cta(ReplayArgsCta a) {
 }
 
 struct RSharedCta {
-    uint32_t size, top, inftop, infcnt, fresh, nfree;
+    uint32_t size, top, inftop, infcnt, fresh, nfree, ptop;
     uint32_t wbuf[32];  // never_take gather
     uint32_t nruns;
     uint32_t hitcnt;
@@ -534,6 +573,11 @@ __device__ __forceinline__ void r_set_key_cta(const ReplayArgsCta& a, RSharedCta
         const uint32_t beta = nu / a.B;
         atomicOr(&a.nz[size_t(k) * a.nzw + (beta >> 5)], 1u << (beta & 31));
         atomicMax(&sh.top, beta);
+        if (a.pbm) {
+            key_mark(a.pbm + size_t(k) * a.T * a.bw, a.psum + size_t(k) * a.psw, a.psum2 + size_t(k) * a.ps2w, a.bw,
+                     a.B, nu);
+            atomicMax(&sh.ptop, beta * a.bw + ((nu - beta * a.B) >> 5));
+        }
     }
 }
 
@@ -564,6 +608,24 @@ __device__ void r_evict_cta(const ReplayArgsCta& a, RSharedCta& sh, uint32_t k, 
             need -= got;
             continue;
         }
+        if (a.pbm) {  // largest finite keys, 32 key-space words per round
+            uint32_t top = sh.ptop, nf = sh.nfree;
+            __syncwarp();
+            const IdOfKey idof{a.items, a.node_off, a.gb, a.N, k, a.bw};
+            const uint32_t got = bm_take(a.pbm + size_t(k) * a.T * a.bw, a.psum + size_t(k) * a.psw,
+                                         a.psum2 + size_t(k) * a.ps2w, top, need, idof,
+                                         keyk, slotk, a.fstack ? fs : nullptr, nf, sh.wbuf, lane);
+            if (lane == 0) {
+                sh.ptop = top;
+                sh.nfree = nf;
+                sh.size -= got;
+                if (got == 0) atomicOr(a.status, 4u);
+            }
+            __syncwarp();
+            if (got == 0) return;
+            need -= got;
+            continue;
+        }
         uint32_t* nzk = a.nz + size_t(k) * a.nzw;
         int32_t wi = int32_t(sh.top >> 5);
         int32_t beta = -1;
@@ -586,6 +648,7 @@ __device__ void r_evict_cta(const ReplayArgsCta& a, RSharedCta& sh, uint32_t k, 
         const uint32_t* off = a.node_off + size_t(beta) * (a.N + 1);
         const uint32_t o = off[k], L = off[k + 1] - o;
         const uint64_t base = a.gb[beta] + o;
+
         const uint32_t kb = uint32_t(beta) * a.B;
         uint32_t c = 0;
         for (; c < L && need > 0; c += 128) {
@@ -646,6 +709,7 @@ __global__ void __launch_bounds__(kRT) k_replay_cta(ReplayArgsCta a) {
     if (tid == 0) {
         sh.size = 0;
         sh.top = 0;
+        sh.ptop = 0;
         sh.inftop = 0;
         sh.infcnt = 0;
         sh.fresh = 0;
@@ -1069,15 +1133,25 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     a.infbm = hot ? a.slot + size_t(N) * D : nullptr;
     a.infsum = hot ? a.infbm + size_t(N) * a.infw : nullptr;
     a.nz = hot ? a.infsum + size_t(N) * a.sumw : nullptr;
-    a.pbm = L > 128 ? nullptr : sc.get<uint32_t>(size_t(N) * T * a.bw);
+    // (next-use step, position) bitmaps: always for short lists (warp path);
+    // for the CTA path when they fit the budget (else its list-scan eviction)
+    const size_t pbm_words = size_t(N) * T * a.bw;
+    const bool want_pbm = L <= 128 || (pbm_words * 4 <= (size_t(4) << 30) && !std::getenv("LSG_REPLAY_SCAN"));
+    a.pbm = want_pbm ? sc.get<uint32_t>(pbm_words) : nullptr;
+    a.psw = uint32_t((uint64_t(T) * a.bw + 31) / 32);
+    a.psum = want_pbm ? sc.get<uint32_t>(size_t(N) * a.psw) : nullptr;
+    a.ps2w = (a.psw + 31) / 32;
+    a.psum2 = want_pbm ? sc.get<uint32_t>(size_t(N) * a.ps2w) : nullptr;
     a.fstack = d_slot ? sc.get<uint32_t>(size_t(N) * std::min<uint64_t>(C, D)) : nullptr;
-    if (!a.nuk || !a.last || !a.key || !a.slot || !a.nz || (L <= 128 && !a.pbm) || !a.infbm || !a.infsum || (d_slot && !a.fstack))
+    if (!a.nuk || !a.last || !a.key || !a.slot || !a.nz || (want_pbm && (!a.pbm || !a.psum || !a.psum2)) || !a.infbm || !a.infsum || (d_slot && !a.fstack))
         return set_error(kInternal, "simulate: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.last, 0xFF, size_t(N) * D * 4, st));  // kNone = no later access
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(N) * D * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.slot, 0xFF, size_t(N) * D * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.nz, 0, size_t(N) * a.nzw * 4, st));
     if (a.pbm) LSG_CUDA(cudaMemsetAsync(a.pbm, 0, size_t(N) * T * a.bw * 4, st));
+    if (a.psum) LSG_CUDA(cudaMemsetAsync(a.psum, 0, size_t(N) * a.psw * 4, st));
+    if (a.psum2) LSG_CUDA(cudaMemsetAsync(a.psum2, 0, size_t(N) * a.ps2w * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.infbm, 0, size_t(N) * a.infw * 4, st));
     LSG_CUDA(cudaMemsetAsync(a.infsum, 0, size_t(N) * a.sumw * 4, st));
     a.hits = d_hits;
@@ -1120,6 +1194,7 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         c.nzw = a.nzw; c.infw = a.infw;
         c.items = d_items; c.node_off = d_node_off; c.gb = gb;
         c.nuk = a.nuk; c.last = a.last; c.key = a.key; c.slot = a.slot; c.nz = a.nz;
+        c.pbm = a.pbm; c.bw = a.bw; c.psum = a.psum; c.psw = a.psw; c.psum2 = a.psum2; c.ps2w = a.ps2w;
         c.infbm = a.infbm; c.infsum = a.infsum; c.sumw = a.sumw; c.fstack = a.fstack; c.hits = d_hits; c.misses = d_misses;
         c.slot_out = d_slot; c.status = d_status;
         k_replay_nextuse_cta<<<nk, kRT, 0, st>>>(c);

@@ -17,6 +17,11 @@ CFGS = {
     "cfg5_N64_E10": (1 << 20, 10, 64, 512, (1 << 20) // 128),
     "cfg5_N128_E10": (1 << 20, 10, 128, 512, (1 << 20) // 256),
     "cfg5_N256_E10": (1 << 20, 10, 256, 512, (1 << 20) // 512),
+    # full cfg5 (BASELINE configs[4]: 1,000 epochs)
+    "cfg5_N32_E1000": (1 << 20, 1000, 32, 512, (1 << 20) // 64),
+    "cfg5_N64_E1000": (1 << 20, 1000, 64, 512, (1 << 20) // 128),
+    "cfg5_N128_E1000": (1 << 20, 1000, 128, 512, (1 << 20) // 256),
+    "cfg5_N256_E1000": (1 << 20, 1000, 256, 512, (1 << 20) // 512),
 }
 if __name__ != "__main__":
     names = []
