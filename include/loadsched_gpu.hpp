@@ -342,6 +342,15 @@ struct PlanOutput {
 
 PlanOutput plan_schedule(const PipelineConfig& config);
 
+// ---- run reporting over a finished plan (config.cpp:157-159,
+// pipeline.hpp:43-44, 62-63): host formulas/formatters over the device
+// planner's and replay's outputs, byte-identical to the reference's
+const char* policy_name(Policy policy);
+double total_barrier_cost(const SchedulePlan& plan, const CostModel& model);
+double total_io_cost(const SchedulePlan& plan, const CostModel& model);
+// metrics.csv: one row per (epoch, step, node) in execution order
+void write_metrics(std::ostream& out, const SchedulePlan& plan, const SimResult& sim, const CostModel& model);
+
 // ---- text artifacts (trace.hpp:42-47, reuse_graph.hpp:55-60, plan.hpp:55-68)
 // Writers format on the GPU (byte-identical to the reference's); readers
 // accept the reference's grammar with its error classes and messages.

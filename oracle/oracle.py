@@ -355,10 +355,14 @@ def ref_available() -> bool:
 
 def ref_text(cfg: Cfg) -> dict:
     """The UNMODIFIED reference's write_trace/write_graph/write_plan files of a
-    plan_schedule run: {"trace": bytes, "graph": bytes, "plan": bytes}."""
+    plan_schedule run, its write_metrics (metrics.csv of the configured pass)
+    and total_barrier_cost / total_io_cost ("%.6f %.6f"): {"trace", "graph",
+    "plan", "metrics", "costs"} -> bytes."""
     with tempfile.TemporaryDirectory() as d:
         subprocess.run([REF_DUMP, "text", d, *cfg.kv()], check=True, capture_output=True)
-        return {k: open(os.path.join(d, k + ".txt"), "rb").read() for k in ("trace", "graph", "plan")}
+        out = {k: open(os.path.join(d, k + ".txt"), "rb").read() for k in ("trace", "graph", "plan", "costs")}
+        out["metrics"] = open(os.path.join(d, "metrics.csv"), "rb").read()
+        return out
 
 
 def ref_read(kind: str, data: bytes) -> tuple[int, str]:

@@ -360,6 +360,14 @@ int cmd_text(int argc, char** argv) {
     write_trace_file(dir + "/trace.txt", out.trace);
     write_graph_file(dir + "/graph.txt", out.graph);
     write_plan_file(dir + "/plan.txt", out.plan);
+    // metrics.csv as run_pipeline writes it (pipeline.cpp:153-179, 193-196)
+    const SimResult sim = simulate_plan(out.plan, cfg.buffer_capacity, cfg.policy,
+                                        cfg.chunk_insert_redundant && cfg.optim_chunk);
+    std::ofstream m(dir + "/metrics.csv");
+    write_metrics(m, out.plan, sim, CostModel{});
+    std::FILE* f = std::fopen((dir + "/costs.txt").c_str(), "w");
+    std::fprintf(f, "%.6f %.6f\n", total_barrier_cost(out.plan, CostModel{}), total_io_cost(out.plan, CostModel{}));
+    std::fclose(f);
     return 0;
 }
 

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <sstream>
@@ -941,6 +942,81 @@ SimResult simulate_plan(const SchedulePlan& plan, std::uint64_t capacity, Policy
                 r.total_misses += m[g * N + k];
             }
     return r;
+}
+
+// ---- run reporting (config.cpp:157-159, pipeline.cpp:133-179) -------------
+const char* policy_name(Policy policy) { return policy == Policy::Clairvoyant ? "clairvoyant" : "lru"; }
+
+double total_barrier_cost(const SchedulePlan& plan, const CostModel& model) {
+    double total = 0.0;
+    for (const EpochPlan& epoch : plan.epochs)
+        for (const StepPlan& step : epoch.steps) total += barrier_time(step.assignment, model);
+    return total;
+}
+
+double total_io_cost(const SchedulePlan& plan, const CostModel& model) {
+    double total = 0.0;
+    for (const EpochPlan& epoch : plan.epochs)
+        for (const StepPlan& step : epoch.steps) {
+            double worst = 0.0;
+            for (const ChunkPlan& reads : step.reads) worst = std::max(worst, read_cost(reads, model));
+            total += worst;
+        }
+    return total;
+}
+
+namespace {
+std::string fixed6(double v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.6f", v);
+    return buf;
+}
+}  // namespace
+
+void write_metrics(std::ostream& out, const SchedulePlan& plan, const SimResult& sim, const CostModel& model) {
+    out << "epoch,step,node,hits,misses,policy,fetches_before,fetches_after,barrier_before,barrier_after\n";
+    const double per_fetch = model.seek_cost + model.stream_cost;
+    std::size_t row = 0;
+    std::string buf;
+    for (const EpochPlan& epoch : plan.epochs) {
+        for (std::size_t t = 0; t < epoch.steps.size(); ++t) {
+            const StepPlan& step = epoch.steps[t];
+            std::uint64_t max_before = 0, max_after = 0;
+            for (std::uint32_t k = 0; k < plan.num_nodes; ++k) {
+                max_before = std::max(max_before, step.fetches_before[k]);
+                max_after = std::max(max_after, step.fetches_after[k]);
+            }
+            const std::string bb = fixed6(double(max_before) * per_fetch), ba = fixed6(double(max_after) * per_fetch);
+            for (std::uint32_t k = 0; k < plan.num_nodes; ++k, ++row) {
+                if (row >= sim.rows.size()) throw InternalError("write_metrics: simulation rows out of order");
+                const StepNodeStats& st = sim.rows[row];
+                if (st.epoch != epoch.epoch || st.step != t || st.node != k)
+                    throw InternalError("write_metrics: simulation rows out of order");
+                buf.clear();
+                buf += std::to_string(epoch.epoch);
+                buf += ',';
+                buf += std::to_string(t);
+                buf += ',';
+                buf += std::to_string(k);
+                buf += ',';
+                buf += std::to_string(st.hits);
+                buf += ',';
+                buf += std::to_string(st.misses);
+                buf += ',';
+                buf += policy_name(sim.policy);
+                buf += ',';
+                buf += std::to_string(step.fetches_before[k]);
+                buf += ',';
+                buf += std::to_string(step.fetches_after[k]);
+                buf += ',';
+                buf += bb;
+                buf += ',';
+                buf += ba;
+                buf += '\n';
+                out << buf;
+            }
+        }
+    }
 }
 
 }  // namespace loadsched

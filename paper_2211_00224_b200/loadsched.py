@@ -28,7 +28,8 @@ __all__ = [
     "write_plan_file", "read_plan", "read_plan_file", "Error", "ConfigError", "ValidationError", "CapabilityError",
     "StorageError", "InternalError", "HIT_BIT", "NEVER", "brute_force_order", "remap_step", "slice_step",
     "remap_epoch", "balance_step", "Read", "ChunkPlan", "plan_chunks", "K_NEVER_USED", "Buffer", "make_buffer",
-    "simulate_sequence", "optimal_miss_oracle",
+    "simulate_sequence", "optimal_miss_oracle", "CostModel", "policy_name", "total_barrier_cost",
+    "total_io_cost", "format_metrics", "write_metrics_file",
 ]
 
 
@@ -730,6 +731,88 @@ def format_plan(plan: SchedulePlan) -> bytes:
 
 def write_plan_file(path, plan: SchedulePlan) -> None:
     _write(path, format_plan(plan))
+
+
+# ---------------------------------------------------------- run reports --
+# config.cpp:157-159, cost_model.hpp:13-16, pipeline.cpp:133-179: host
+# formulas and the metrics.csv formatter over the device planner's and
+# replay's outputs (T*N rows), byte-identical to the reference's.
+@dataclass
+class CostModel:
+    """cost_model.hpp:13-16"""
+
+    seek_cost: float = 13.0
+    stream_cost: float = 1.0
+
+
+def policy_name(policy: str) -> str:
+    """config.cpp:157-159"""
+    return "clairvoyant" if policy == "clairvoyant" else "lru"
+
+
+def total_barrier_cost(plan: SchedulePlan, model: CostModel = CostModel()) -> float:
+    """pipeline.cpp:133-138 with barrier_time (balance.cpp:41-47): the sum over
+    steps of max per-node fetch count x (seek + stream)."""
+    per_fetch = model.seek_cost + model.stream_cost
+    total = 0.0
+    for m in plan.fetches_after.max(dim=1).values.cpu().tolist():
+        total += max(0.0, float(m) * per_fetch)
+    return total
+
+
+def total_io_cost(plan: SchedulePlan, model: CostModel = CostModel()) -> float:
+    """pipeline.cpp:140-151 with read_cost (cost_model.cpp:9-18): the sum over
+    steps of the max per-node read-plan cost, each read seek + span x stream,
+    accumulated in read order like the reference."""
+    if plan.read_start is None:
+        raise ValidationError(3, "total_io_cost: the plan has no read plans")
+    off = plan.node_off.cpu().numpy().astype(np.int64)
+    cnt = plan.read_count.cpu().numpy().astype(np.int64)
+    rs = plan.read_start.cpu().numpy().view(np.uint32).astype(np.int64)
+    re_ = plan.read_end.cpu().numpy().view(np.uint32).astype(np.int64)
+    T, N = cnt.shape
+    bases = np.concatenate([[0], np.cumsum(off[:, N])])
+    total = 0.0
+    for g in range(T):
+        worst = 0.0
+        for k in range(N):
+            lo = int(bases[g] + off[g, k])
+            c = 0.0
+            for sp in (re_[lo:lo + cnt[g, k]] - rs[lo:lo + cnt[g, k]] + 1).tolist():
+                c += model.seek_cost + float(sp) * model.stream_cost
+            worst = max(worst, c)
+        total += worst
+    return total
+
+
+def format_metrics(plan: SchedulePlan, sim: "SimResult", policy: str = "clairvoyant",
+                   model: CostModel = CostModel()) -> bytes:
+    """write_metrics (pipeline.cpp:153-179): one row per (epoch, step, node) in
+    execution order with the replay's hits/misses, the per-node fetch counts
+    before/after balancing and the step's barrier before/after."""
+    per_fetch = model.seek_cost + model.stream_cost
+    T, N = plan.fetches_before.shape
+    S = plan.steps_per_epoch
+    order = plan.order.order.cpu().numpy().view(np.uint32).tolist()
+    fb = plan.fetches_before.cpu().numpy().view(np.uint32)
+    fa = plan.fetches_after.cpu().numpy().view(np.uint32)
+    h = sim.hits.cpu().numpy().view(np.uint32)
+    m = sim.misses.cpu().numpy().view(np.uint32)
+    bb = ["%.6f" % (float(v) * per_fetch) for v in fb.max(axis=1).tolist()] if N else []
+    ba = ["%.6f" % (float(v) * per_fetch) for v in fa.max(axis=1).tolist()] if N else []
+    pol = policy_name(policy)
+    fbl, fal, hl, ml = fb.tolist(), fa.tolist(), h.tolist(), m.tolist()
+    out = ["epoch,step,node,hits,misses,policy,fetches_before,fetches_after,barrier_before,barrier_after\n"]
+    for g in range(T):
+        head = f"{order[g // S]},{g % S},"
+        tail = f",{bb[g]},{ba[g]}\n"
+        out.extend(f"{head}{k},{hl[g][k]},{ml[g][k]},{pol},{fbl[g][k]},{fal[g][k]}{tail}" for k in range(N))
+    return "".join(out).encode()
+
+
+def write_metrics_file(path, plan: SchedulePlan, sim: "SimResult", policy: str = "clairvoyant",
+                       model: CostModel = CostModel()) -> None:
+    _write(path, format_metrics(plan, sim, policy, model))
 
 
 def read_plan(text) -> SchedulePlan:

@@ -170,6 +170,11 @@ static int dump(int argc, char** argv) {
         rows.write(reinterpret_cast<const char*>(hm), 8);
     }
     ord.write(reinterpret_cast<const char*>(out.plan.order.order.data()), 4 * out.plan.order.order.size());
+    std::ofstream met(dir + "/metrics.csv");
+    write_metrics(met, out.plan, sim, CostModel{});
+    std::FILE* f = std::fopen((dir + "/costs.txt").c_str(), "w");
+    std::fprintf(f, "%.6f %.6f\n", total_barrier_cost(out.plan, CostModel{}), total_io_cost(out.plan, CostModel{}));
+    std::fclose(f);
     return 0;
 }
 

@@ -173,6 +173,32 @@ def test_writers_match_reference_files(ls, seed):
     assert ls.format_trace(out.trace) == txt["trace"]
     assert ls.format_graph(out.graph) == txt["graph"]
     assert ls.format_plan(out.plan) == txt["plan"]
+    # run reports: metrics.csv of the configured pass and the cost totals
+    pol = c.policy
+    sim = ls.simulate_plan(out.plan, c.buffer_capacity, pol,
+                           insert_redundant=bool(c.chunk_insert_redundant and c.optim_chunk))
+    assert ls.format_metrics(out.plan, sim, pol) == txt["metrics"]
+    costs = b"%.6f %.6f\n" % (ls.total_barrier_cost(out.plan), ls.total_io_cost(out.plan))
+    assert costs == txt["costs"]
+
+
+@ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,policy,red", [(1, "lru", False), (2, "clairvoyant", True), (3, "lru", False),
+                                             (4, "clairvoyant", True)])
+def test_metrics_match_reference(ls, seed, policy, red):
+    """write_metrics (pipeline.cpp:153-179) and total_barrier_cost /
+    total_io_cost of LRU and redundant-insert passes, byte for byte."""
+    import dataclasses
+    from test_gpu_parity import to_pc
+    c = dataclasses.replace(rand_cfg(seed), policy=policy, chunk_insert_redundant=red, optim_chunk=True)
+    out = ls.plan_schedule(to_pc(ls, c))
+    txt = O.ref_text(c)
+    sim = ls.simulate_plan(out.plan, c.buffer_capacity, policy, insert_redundant=red)
+    assert ls.format_metrics(out.plan, sim, policy) == txt["metrics"]
+    assert b"%.6f %.6f\n" % (ls.total_barrier_cost(out.plan), ls.total_io_cost(out.plan)) == txt["costs"]
+    assert ls.format_metrics(out.plan, sim, policy, ls.CostModel(2.5, 0.125)).count(b"\n") == \
+        1 + out.plan.node_off.shape[0] * out.plan.num_nodes
 
 
 @pytest.mark.gpu

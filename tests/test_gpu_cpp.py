@@ -51,3 +51,7 @@ def test_cpp_dropin_matches_oracle(ls, binary, seed):
         h, m = O.simulate(ref.items, ref.node_off, N, D, c.buffer_capacity)
         rows = rd("rows.u32").reshape(-1, 2)
         assert np.array_equal(rows[:, 0], h.ravel()) and np.array_equal(rows[:, 1], m.ravel())
+        if O.ref_available():  # write_metrics / cost totals byte-identical to the reference's
+            ref = O.ref_text(c)
+            assert open(os.path.join(d, "metrics.csv"), "rb").read() == ref["metrics"]
+            assert open(os.path.join(d, "costs.txt"), "rb").read() == ref["costs"]
