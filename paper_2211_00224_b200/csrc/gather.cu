@@ -204,6 +204,11 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
+    // programmatic dependent launch: the next kernel of the stream may be
+    // scheduled now (it waits below for this grid); this grid waits for the
+    // previous step's kernels (slots it filled, batch rows, the counters)
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint64_t row_bytes = f.vec_per_row * 16, tpr = row_bytes / kTmaTile;
     const uint32_t r0 = __ldg(&f.node_off[f.k0]);
     const uint64_t nt = uint64_t(__ldg(&f.node_off[f.k1]) - r0) * tpr;
@@ -299,6 +304,8 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
 // rows are visited (a small fixed grid; the last block to finish resets the
 // list for the next step), else every row of the step is scanned.
 __global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the hit kernel's miss list
     const uint32_t r0 = __ldg(&f.node_off[f.k0]), r1 = __ldg(&f.node_off[f.k1]);
     const uint64_t pairs = f.vec_per_row;  // 16-byte pairs of payload words
     const uint32_t nlist = f.mlist ? __ldcg(&f.mctl[0]) : 0u;
@@ -332,6 +339,28 @@ __global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
             }
         }
     }
+}
+
+// launch with programmatic stream serialization (PDL): back-to-back step
+// kernels overlap launch and ramp-up with the previous kernel's tail; the
+// kernels order their memory through griddepcontrol.wait (LSG_PDL=0: off)
+template <class K>
+cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const StepFetch& f) {
+    static const bool on = [] {
+        const char* e = std::getenv("LSG_PDL");
+        return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = on ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, f);
 }
 
 // per-device miss-row list of the step fetch (grown on demand; the counters
@@ -385,7 +414,7 @@ int launch_hits(StepFetch f, uint64_t rows, uint64_t sample_bytes, cudaStream_t 
         }
         const uint64_t tiles = rows * (sample_bytes / kTmaTile);
         const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 148ull * 2)));
-        k_fetch_step_hits_tma<<<grid, 32, smem, st>>>(f);
+        LSG_CUDA(launch_pdl(k_fetch_step_hits_tma, dim3(grid), dim3(32), size_t(smem), st, f));
         LSG_LAUNCH_CHECK("k_fetch_step_hits_tma");
         if (tma) *tma = true;
         return kOk;
@@ -428,7 +457,7 @@ int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* 
     // 16-byte pairs); listed miss rows over grid.y = 148, else every row
     dim3 g2(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 256)),
             unsigned(f.mlist ? std::min<uint64_t>(rows, 148) : std::min<uint64_t>(std::max<uint64_t>(rows, 1), 1024)));
-    k_fetch_step_misses<<<g2, 256, 0, st>>>(f);
+    LSG_CUDA(launch_pdl(k_fetch_step_misses, g2, dim3(256), 0, st, f));
     LSG_LAUNCH_CHECK("k_fetch_step_misses");
     return kOk;
 }
