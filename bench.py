@@ -42,6 +42,11 @@ import time
 
 import numpy as np
 
+# more hardware work queues than the default 8, so the plan / replay / fetch
+# streams never share one (a shared queue serialises a replay behind the
+# planner's persistent kernel); must be set before CUDA initialises
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -174,7 +179,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--plan-shard", default="auto", choices=["auto", "rr", "replicate"],
                     help="N>1: plan each job on one GPU (rr) or on all (replicate); auto = rr above 2 GPUs")
-    ap.add_argument("--prio", type=int, default=1, help="replay+fetch stream at high priority")
+    ap.add_argument("--prio", type=int, default=1, help="plan and replay streams at high priority")
     ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
     args = ap.parse_args()
     if args.impl == "reference":
@@ -211,12 +216,15 @@ def main():
     fetcher = ls.StepFetcher([bufs[k] for k in range(k0, k1)], [outs[k] for k in range(k0, k1)],
                              (k0, k1), SB, c["fill_seed"])
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    # replay + fetch (and NCCL) on a high-priority stream, the plan of the
-    # next job on a low-priority one: the block scheduler hands free SMs to
-    # the fetch first, the planner's persistent CTA needs only one
-    fstream = torch.cuda.Stream(priority=-1 if args.prio else 0)  # lower = higher priority
-    rstream = torch.cuda.Stream(priority=-1 if args.prio else 0)  # replay + NCCL
-    pstream = torch.cuda.Stream(priority=0)
+    # the latency-bound stages (the planner's persistent CTA, the per-rank
+    # replay CTAs, NCCL) on high-priority streams, the fetch on a low-priority
+    # one: the fetch keeps every SM's CTA slots filled (back-to-back step
+    # kernels, programmatic dependent launch), so without priority the block
+    # scheduler starves the few planner/replay CTAs (measured: plan 0.38 ->
+    # 2.0 s beside the fetch); with it they take a slot as soon as one frees
+    fstream = torch.cuda.Stream(priority=0)                        # batch fetch
+    rstream = torch.cuda.Stream(priority=-1 if args.prio else 0)  # replay + NCCL (lower = higher priority)
+    pstream = torch.cuda.Stream(priority=-1 if args.prio else 0)  # plans
     torch.cuda.set_stream(fstream)
     # the loader's pinned staging for the e2e path: two sets, so the plan of
     # job i+1 lands in one while job i's plan is uploaded from the other
@@ -306,11 +314,16 @@ def main():
                             dist.broadcast(items, src=owner)
                             dist.broadcast(noff, src=owner)
                         plan = ls.SchedulePlan(D, N, b, int(sh.steps_per_epoch), None, items, noff, None, None)
+                        h0 = time.perf_counter()
                         sim = ls.simulate_plan(plan, C, node_range=(k0, k1), want_slots=True)
+                        h1 = time.perf_counter()
                         combine_rows(sim.hits, sim.misses)
-                        if host:
-                            rows.append((sim.hits.cpu(), sim.misses.cpu()))  # d2h of the step results
-                        off = noff.cpu().numpy()
+                        if host:  # d2h of the step results
+                            rows.append((ls.to_host(sim.hits), ls.to_host(sim.misses)))
+                        off = ls.to_host(noff).numpy()
+                        if os.environ.get("LSG_BENCH_TIMELINE"):
+                            print(f"[replayer] job {i}: simulate_plan {1e3 * (h1 - h0):.1f} ms host, "
+                                  f"rows+off {1e3 * (time.perf_counter() - h1):.1f} ms", file=sys.stderr, flush=True)
                         if owner == rank:
                             free.release()  # this job's host staging set has been uploaded
                         f1 = ev()
@@ -384,6 +397,10 @@ def main():
         torch.cuda.synchronize()
     launches = ls.lib().lsg_launch_count() - launches0
     total_ms = t_start.elapsed_time(t_end)
+    timeline = None
+    if os.environ.get("LSG_BENCH_TIMELINE"):  # per-job stage windows (ms from t_start)
+        timeline = [[round(t_start.elapsed_time(x), 1) if x is not None else None for x in (e[0], e[1], e[2], e[3], e[7], e[4])]
+                    for e in evs]
     own = [e[0].elapsed_time(e[1]) for e in evs if e[0] is not None]
     plan_ms = statistics.mean(own) if own else 0.0
     replay_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
@@ -486,6 +503,7 @@ def main():
                                    "one pair per training step)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6650"},
             "gpu_launches": int(launches),
+            **({"timeline_plan0_plan1_rep0_rep1_fetch0_fetch1": timeline} if timeline else {}),
             "clocks": clk.summary(),
         }
         if e2e:

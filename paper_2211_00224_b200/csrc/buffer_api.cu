@@ -307,8 +307,8 @@ int lsg_simulate_sequence(const uint32_t* h_seq, uint64_t len, uint64_t capacity
     LSG_LAUNCH_CHECK("k_sum_u32");
     uint32_t h = 0;
     unsigned long long m = 0;
-    LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
-    LSG_CUDA(cudaMemcpyAsync(&m, tot, 8, cudaMemcpyDeviceToHost, st));
+    if (int _rc = d2h_small(&h, status, 4, st)) return _rc;
+    if (int _rc = d2h_small(&m, tot, 8, st)) return _rc;
     LSG_CUDA(cudaStreamSynchronize(st));
     if (h) return set_error(kInternal, "simulate_sequence: device invariant violated");
     *h_misses = m;
@@ -334,7 +334,7 @@ int lsg_optimal_miss_oracle(const uint64_t* h_seq, uint64_t len, uint64_t capaci
     k_opt_oracle<<<1, 1024, smem, st>>>(seq, uint32_t(len), uint32_t(capacity), out);
     LSG_LAUNCH_CHECK("k_opt_oracle");
     uint32_t m = 0;
-    LSG_CUDA(cudaMemcpyAsync(&m, out, 4, cudaMemcpyDeviceToHost, st));
+    if (int _rc = d2h_small(&m, out, 4, st)) return _rc;
     LSG_CUDA(cudaStreamSynchronize(st));
     *h_misses = m;
     return kOk;

@@ -88,6 +88,14 @@ void keep_pool() {
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        // no cross-stream reuse that would insert a wait: the planner frees
+        // its step-loop scratch right after launching the persistent kernel,
+        // and a replay on another stream reusing that block would wait for
+        // the whole plan (measured: the replay ended exactly with the
+        // concurrent plan). Opportunistic reuse (already-completed frees)
+        // stays on.
+        int no = 0;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
     }
     done_mask.fetch_or(bit);
 }
@@ -134,6 +142,26 @@ void l2_unpin(cudaStream_t st) {
     v.accessPolicyWindow.num_bytes = 0;
     cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
     cudaGetLastError();
+}
+
+int d2h_small(void* h, const void* d, size_t bytes, cudaStream_t st) {
+    static thread_local void* stage = nullptr;
+    if (bytes > 64) return set_error(kInternal, "d2h_small: readback larger than 64 bytes");
+    if (!stage) LSG_CUDA(cudaMallocHost(&stage, 64));
+    LSG_CUDA(cudaMemcpyAsync(stage, d, bytes, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaStreamSynchronize(st));
+    std::memcpy(h, stage, bytes);
+    return kOk;
+}
+
+size_t exclusive_smem(size_t need) {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = std::getenv("LSG_EXCLUSIVE_SM");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    constexpr size_t kWhole = 200 * 1024;  // > half an SM's 228 KB: no second CTA of this size or a fetch CTA fits
+    return on ? std::max(need, kWhole) : need;
 }
 
 bool profiling() {
@@ -230,7 +258,7 @@ int lsg_pso_order(const uint64_t* d_w, uint32_t E, uint32_t swarm, uint32_t iter
                               restart, seed, d_order, d_cost, d_hist, d_iters, status, st);
     if (rc) return rc;
     uint32_t h = 0;
-    LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
+    if (int _rc = d2h_small(&h, status, 4, st)) return _rc;
     LSG_CUDA(cudaStreamSynchronize(st));
     if (h) return set_error(kInternal, "pso_order: velocity capacity exceeded");
     return kOk;
@@ -282,7 +310,7 @@ int lsg_plan(const lsg_config* cfg, const lsg_plan_out* out, void* stream) {
                                 out->read_count, out->read_needed, out->read_redundant, st)))
         return rc;
     uint32_t h = 0;
-    LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
+    if (int _rc = d2h_small(&h, status, 4, st)) return _rc;
     LSG_CUDA(cudaStreamSynchronize(st));
     if (h) return set_error(kInternal, "plan: device invariant violated (status " + std::to_string(h) + ")");
     return kOk;
@@ -354,7 +382,7 @@ int lsg_simulate_ex(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
                              status, st);
     if (rc) return rc;
     uint32_t h = 0;
-    LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
+    if (int _rc = d2h_small(&h, status, 4, st)) return _rc;
     LSG_CUDA(cudaStreamSynchronize(st));
     if (h) return set_error(kInternal, "simulate: device invariant violated (status " + std::to_string(h) + ")");
     return kOk;

@@ -126,7 +126,7 @@ int plan_reads_device(const uint32_t* d_items, const uint32_t* d_node_off, uint3
         LSG_CUDA(cudaMemsetAsync(d_m, 0, 4, st));
         k_max_list<<<grid_for(uint64_t(T) * N, 256, 592), 256, 0, st>>>(d_node_off, T, N, d_m);
         LSG_LAUNCH_CHECK("k_max_list");
-        LSG_CUDA(cudaMemcpyAsync(&lmax, d_m, 4, cudaMemcpyDeviceToHost, st));
+        if (int _rc = d2h_small(&lmax, d_m, 4, st)) return _rc;
         LSG_CUDA(cudaStreamSynchronize(st));
     }
     while (a.P2 < lmax) a.P2 <<= 1;

@@ -83,6 +83,20 @@ struct Scratch {
 bool l2_pin(cudaStream_t st, const void* p, size_t bytes);
 void l2_unpin(cudaStream_t st);
 
+// Dynamic shared memory for the latency-bound single-CTA-per-unit kernels
+// (the planner's persistent step loop, the per-rank replay): rounded up so the
+// CTA holds its SM alone (LSG_EXCLUSIVE_SM=0: the bare need). Beside the
+// fetch's TMA CTAs or each other they otherwise share an SM's issue slots and
+// load/store pipes, and one shared SM stretches the whole stage.
+size_t exclusive_smem(size_t need);
+
+// Small device->host readback (status words, counts; <= 64 bytes) through a
+// per-thread PINNED staging buffer, then a sync of `st` only. A copy into
+// pageable host memory is staged by the driver and waited for beside other
+// streams' kernels: a replay's status read sat behind a concurrent planner's
+// persistent kernel (the whole plan) on another stream.
+int d2h_small(void* h, const void* d, size_t bytes, cudaStream_t st);
+
 struct PlanDims {
     uint64_t D, B, S, keep, T;
     uint32_t N, E, b;

@@ -239,7 +239,7 @@ int window_bits_device(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64
         k_rows_distinct<<<dim3(grid_for(len, 256, 1024), E), 256, 0, st>>>(g.len, g.words, d_trace, seen, dup);
         LSG_LAUNCH_CHECK("k_rows_distinct");
         uint32_t h = 1;
-        LSG_CUDA(cudaMemcpyAsync(&h, dup, 4, cudaMemcpyDeviceToHost, st));
+        if (int _rc = d2h_small(&h, dup, 4, st)) return _rc;
         LSG_CUDA(cudaStreamSynchronize(st));
         distinct = h == 0;
     }

@@ -1251,13 +1251,15 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
     a.dbg_skip = std::getenv("LSG_DEBUG_SKIP") ? std::atoi(std::getenv("LSG_DEBUG_SKIP")) : 0;
     if (a.prof) LSG_CUDA(cudaMemsetAsync(a.prof, 0, (16 + 256) * 8, st));
     if (smem_items) {
-        const size_t smem = size_t(6) * dm.B * 4;
+        const size_t smem = exclusive_smem(size_t(6) * dm.B * 4);
         auto kern = dm.N <= 8 ? k_plan_loop<true, true> : k_plan_loop<true, false>;
         LSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         kern<<<1, kThreads, smem, st>>>(a);
     } else {
+        const size_t smem = exclusive_smem(0);
         auto kern = dm.N <= 8 ? k_plan_loop<false, true> : k_plan_loop<false, false>;
-        kern<<<1, kThreads, 0, st>>>(a);
+        LSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        kern<<<1, kThreads, smem, st>>>(a);
     }
     LSG_LAUNCH_CHECK("k_plan_loop");
     if (a.prof) {

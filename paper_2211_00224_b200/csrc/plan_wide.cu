@@ -1729,7 +1729,7 @@ int lsg_remap_step(const uint64_t* h_res_off, const uint32_t* h_res_ids, uint32_
                                   nullptr, status, st, hm, 0))
         return rc;
     uint32_t h = 0;
-    LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
+    if (int _rc = d2h_small(&h, status, 4, st)) return _rc;
     LSG_CUDA(cudaMemcpyAsync(h_items, items, len * 4, cudaMemcpyDeviceToHost, st));
     LSG_CUDA(cudaMemcpyAsync(h_node_off, off, (N + 1) * 4, cudaMemcpyDeviceToHost, st));
     LSG_CUDA(cudaStreamSynchronize(st));
@@ -1778,8 +1778,8 @@ int lsg_balance_step(uint32_t* h_items, uint32_t* h_node_off, uint32_t N, uint64
     LSG_LAUNCH_CHECK("k_balance_lists");
     uint32_t h = 0;
     unsigned long long mv = 0;
-    LSG_CUDA(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
-    LSG_CUDA(cudaMemcpyAsync(&mv, moves, 8, cudaMemcpyDeviceToHost, st));
+    if (int _rc = d2h_small(&h, status, 4, st)) return _rc;
+    if (int _rc = d2h_small(&mv, moves, 8, st)) return _rc;
     LSG_CUDA(cudaMemcpyAsync(h_items, out, total * 4, cudaMemcpyDeviceToHost, st));
     LSG_CUDA(cudaMemcpyAsync(h_node_off, out_off, (N + 1) * 4, cudaMemcpyDeviceToHost, st));
     LSG_CUDA(cudaStreamSynchronize(st));

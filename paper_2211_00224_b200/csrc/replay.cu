@@ -1062,7 +1062,7 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     k_step_bases<<<1, 1024, 0, st>>>(d_node_off, uint32_t(T), N, gb);
     LSG_LAUNCH_CHECK("k_step_bases");
     uint64_t total = 0, L = 0;
-    LSG_CUDA(cudaMemcpyAsync(&total, gb + T, 8, cudaMemcpyDeviceToHost, st));
+    if (int _rc = d2h_small(&total, gb + T, 8, st)) return _rc;
     {
         // key stride = the longest node list of any step (keys are g*L + i)
         std::vector<uint32_t> hv(size_t(T) * (N + 1));
@@ -1178,7 +1178,7 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
             k_scan_u64<<<1, 1024, 0, st>>>(cnt, T * N, roff);
             LSG_LAUNCH_CHECK("k_scan_u64");
             uint64_t nred = 0;
-            LSG_CUDA(cudaMemcpyAsync(&nred, roff + T * N, 8, cudaMemcpyDeviceToHost, st));
+            if (int _rc = d2h_small(&nred, roff + T * N, 8, st)) return _rc;
             LSG_CUDA(cudaStreamSynchronize(st));
             uint32_t* ids = sc.get<uint32_t>(nred);
             uint32_t* keys = sc.get<uint32_t>(nred);
@@ -1199,7 +1199,7 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         c.slot_out = d_slot; c.status = d_status;
         k_replay_nextuse_cta<<<nk, kRT, 0, st>>>(c);
         LSG_LAUNCH_CHECK("k_replay_nextuse_cta");
-        const size_t smem = size_t(L) * 4 + (L + 2) * 2 + 16;
+        const size_t smem = exclusive_smem(size_t(L) * 4 + (L + 2) * 2 + 16);
         LSG_CUDA(cudaFuncSetAttribute(k_replay_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         const bool pinned = l2_pin(st, hot, hot_words * 4);
         k_replay_cta<<<nk, kRT, smem, st>>>(c);

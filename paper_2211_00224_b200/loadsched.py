@@ -29,7 +29,7 @@ __all__ = [
     "StorageError", "InternalError", "HIT_BIT", "NEVER", "brute_force_order", "remap_step", "slice_step",
     "remap_epoch", "balance_step", "Read", "ChunkPlan", "plan_chunks", "K_NEVER_USED", "Buffer", "make_buffer",
     "simulate_sequence", "optimal_miss_oracle", "CostModel", "policy_name", "total_barrier_cost",
-    "total_io_cost", "format_metrics", "write_metrics_file",
+    "total_io_cost", "format_metrics", "write_metrics_file", "to_host",
 ]
 
 
@@ -236,6 +236,17 @@ class SimResult:
 
 def _stream() -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def to_host(t: torch.Tensor) -> torch.Tensor:
+    """Device -> host copy through PINNED memory on the current stream, then a
+    sync of that stream only. (A copy into pageable memory is staged by the
+    driver and can wait for kernels of OTHER streams: a replay's readback sat
+    behind a concurrent planner's persistent kernel.)"""
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return h
 
 
 def _ptr(t: torch.Tensor | None):
@@ -599,8 +610,8 @@ def simulate_plan(plan: SchedulePlan, capacity: int, policy: str = "clairvoyant"
         _check(lib().lsg_simulate(_ptr(plan.items.contiguous()), _ptr(plan.node_off.contiguous()), T, N,
                                   plan.dataset_size, capacity, pol, k0, k1, _ptr(hits), _ptr(misses),
                                   _ptr(slots), _stream()))
-    return SimResult(hits, misses, int(hits.sum().item()), int(misses.sum().item()),
-                     slots[: plan.items.numel()] if slots is not None else None)
+    tot = to_host(torch.stack([hits.sum(dtype=torch.int64), misses.sum(dtype=torch.int64)]))
+    return SimResult(hits, misses, int(tot[0]), int(tot[1]), slots[: plan.items.numel()] if slots is not None else None)
 
 
 def store_fill(ids: torch.Tensor, sample_bytes: int, fill_seed: int,

@@ -29,6 +29,19 @@ def plan1():
     return a.elapsed_time(z)
 
 res = {"alone_replay": [replay() for _ in range(3)], "alone_plan": [plan1() for _ in range(2)]}
+P = torch.cuda.Stream()
+out = []
+for _ in range(2):
+    def planner():
+        torch.cuda.set_device(0)
+        with torch.cuda.stream(P):
+            ls.plan_schedule(pc)
+    th = threading.Thread(target=planner)
+    th.start()
+    import time; time.sleep(0.03)
+    out.append(replay())
+    th.join(); torch.cuda.synchronize()
+res["beside_plan_replay"] = out
 for what, fn in (("replay", replay), ("plan", plan1)):
     out = []
     for _ in range(2):
