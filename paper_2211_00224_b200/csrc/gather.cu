@@ -144,7 +144,7 @@ struct StepFetch {
     uint32_t k0, k1;
     uint64_t vec_per_row, tiles_per_row, seed;
     uint32_t* mlist;           // miss rows of the step (filled by the TMA hit kernel) or null
-    uint32_t* mctl;            // [3] miss count, finished misses blocks, hit-tile chunks claimed
+    uint32_t* mctl;            // [3] miss count, finished misses blocks, hit tiles claimed
     int l2hint;                // TMA copies tagged L2::evict_first (streaming)
 };
 
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_fetch_step_hits(StepFetch f)
 // of stretching the step; row descriptors change once per row and miss rows
 // are skipped whole. Measured at 6.56 TB/s on the cfg2 shape vs 5.75 for the
 // LSU gather (tools/ubench_gather.cu).
-constexpr int kTmaTile = 8192, kTmaStages = 12, kTmaLag = 3, kTmaChunk = 16;
+constexpr int kTmaTile = 8192, kTmaStages = 12, kTmaLag = 3, kTmaChunk = 16, kTmaTail = 4;
 
 __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
     extern __shared__ __align__(128) unsigned char tsm[];
@@ -214,9 +214,13 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
     const uint64_t nt = uint64_t(__ldg(&f.node_off[f.k1]) - r0) * tpr;
     // static split without a counter (mctl == null), else dynamic chunks
     uint64_t tb, te;
+    // guided claims: kTmaChunk tiles while plenty remain, then kTmaTail, so
+    // the step's last CTAs finish together (shorter tail before the next step)
+    const uint64_t guide = uint64_t(gridDim.x) * 2 * kTmaChunk;
     if (f.mctl) {
-        tb = uint64_t(atomicAdd(&f.mctl[2], 1u)) * kTmaChunk;
-        te = min(nt, tb + kTmaChunk);
+        const uint32_t sz = nt > guide ? kTmaChunk : kTmaTail;
+        tb = atomicAdd(&f.mctl[2], sz);
+        te = min(nt, tb + sz);
     } else {
         const uint64_t per = (nt + gridDim.x - 1) / gridDim.x;
         tb = uint64_t(blockIdx.x) * per;
@@ -234,9 +238,10 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
         for (;;) {
             if (tn >= te) {
                 if (!f.mctl || tb >= nt) return false;
-                tb = uint64_t(atomicAdd(&f.mctl[2], 1u)) * kTmaChunk;
+                const uint32_t sz = nt - te > guide ? kTmaChunk : kTmaTail;
+                tb = atomicAdd(&f.mctl[2], sz);
                 if (tb >= nt) return false;
-                te = min(nt, tb + kTmaChunk);
+                te = min(nt, tb + sz);
                 tn = tb;
             }
             const uint64_t rr = tn / tpr;
@@ -457,6 +462,11 @@ int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* 
     // 16-byte pairs); listed miss rows over grid.y = 148, else every row
     dim3 g2(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 256)),
             unsigned(f.mlist ? std::min<uint64_t>(rows, 148) : std::min<uint64_t>(std::max<uint64_t>(rows, 1), 1024)));
+    static const bool nomiss = std::getenv("LSG_DEBUG_NOMISS") != nullptr;  // timing experiments only
+    if (nomiss && f.mctl) {
+        LSG_CUDA(cudaMemsetAsync(f.mctl, 0, 16, st));
+        return kOk;
+    }
     LSG_CUDA(launch_pdl(k_fetch_step_misses, g2, dim3(256), 0, st, f));
     LSG_LAUNCH_CHECK("k_fetch_step_misses");
     return kOk;
