@@ -562,20 +562,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     const uint4* rows = reinterpret_cast<const uint4*>(&sm.stg[buf][0][0]);
                     uint32_t myres = kSent;
                     const unsigned long long tc0 = a.prof ? clock64() : 0ull;
+                    // v (per 16-bit half) = 0 for the previous item's winner,
+                    // else 1; its count moves by 16 - 16 v. The next keys are
+                    // (r + M + 16) - 16 v: the sum is off the chain, so the
+                    // chain is IMAD -> 2 VIMNMX3 -> half swap + VIMNMX -> IADD
+                    // (K - min, >= 0 per half) -> VIMNMX (v)
+                    uint32_t v01 = 0x10001u, v23 = 0x10001u, v45 = 0x10001u, v67 = 0x10001u;
 #pragma unroll
                     for (int u = 0; u < 32; ++u) {
                         const uint4 r = rows[u];
-                        const uint32_t m2 = __vimin3_u16x2(__vimin3_u16x2(r.x + M01, r.y + M23, r.z + M45),
-                                                           r.w + M67, kSent2);
-                        const uint32_t cl = min(m2 & 0xFFFFu, m2 >> 16);
-                        const uint32_t inc = (cl & 1u) ? 0x100000u : 0x10u;  // odd nodes: high half
-                        const uint32_t pr = (cl >> 1) & 7u;                  // pair; 7 = none (kSent)
-                        M01 += pr == 0 ? inc : 0u;
-                        M23 += pr == 1 ? inc : 0u;
-                        M45 += pr == 2 ? inc : 0u;
-                        M67 += pr == 3 ? inc : 0u;
-                        myres = lane == uint32_t(u) ? cl : myres;
+                        const uint32_t K01 = (r.x + M01 + 0x100010u) - (v01 << 4);
+                        const uint32_t K23 = (r.y + M23 + 0x100010u) - (v23 << 4);
+                        const uint32_t K45 = (r.z + M45 + 0x100010u) - (v45 << 4);
+                        const uint32_t K67 = (r.w + M67 + 0x100010u) - (v67 << 4);
+                        M01 += 0x100010u - (v01 << 4);
+                        M23 += 0x100010u - (v23 << 4);
+                        M45 += 0x100010u - (v45 << 4);
+                        M67 += 0x100010u - (v67 << 4);
+                        const uint32_t m2 = __vimin3_u16x2(__vimin3_u16x2(K01, K23, K45), K67, kSent2);
+                        const uint32_t mm = __vminu2(m2, __byte_perm(m2, 0, 0x1032));  // min in both halves
+                        v01 = __vminu2(K01 - mm, 0x10001u);
+                        v23 = __vminu2(K23 - mm, 0x10001u);
+                        v45 = __vminu2(K45 - mm, 0x10001u);
+                        v67 = __vminu2(K67 - mm, 0x10001u);
+                        myres = lane == uint32_t(u) ? (mm & 0xFFFFu) : myres;
                     }
+                    M01 += 0x100010u - (v01 << 4);  // the chunk's last decision
+                    M23 += 0x100010u - (v23 << 4);
+                    M45 += 0x100010u - (v45 << 4);
+                    M67 += 0x100010u - (v67 << 4);
                     if (a.prof) {
                         const uint32_t dep = myres & 1u;  // keep the timer after the chain
                         const unsigned long long tc1 = clock64() + dep;
