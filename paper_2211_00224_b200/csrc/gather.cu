@@ -350,11 +350,16 @@ __global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
 // kernels overlap launch and ramp-up with the previous kernel's tail; the
 // kernels order their memory through griddepcontrol.wait (LSG_PDL=0: off)
 template <class K>
-cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const StepFetch& f) {
-    static const bool on = [] {
+cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const StepFetch& f, int which) {
+    // LSG_PDL bit 0: hit kernels, bit 1: miss kernels. Default 1: a miss
+    // kernel launched early beside a miss-heavy hit kernel measured slower
+    // (E=4 cfg2 fetch 88.5 -> 96.9 ms), the hit kernels gain (1 rank 52.7 ->
+    // 50.6 us per step)
+    static const int mode = [] {
         const char* e = std::getenv("LSG_PDL");
-        return !(e && e[0] == '0');
+        return e ? std::atoi(e) : 1;
     }();
+    const bool on = (mode >> which) & 1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -419,7 +424,7 @@ int launch_hits(StepFetch f, uint64_t rows, uint64_t sample_bytes, cudaStream_t 
         }
         const uint64_t tiles = rows * (sample_bytes / kTmaTile);
         const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 148ull * 2)));
-        LSG_CUDA(launch_pdl(k_fetch_step_hits_tma, dim3(grid), dim3(32), size_t(smem), st, f));
+        LSG_CUDA(launch_pdl(k_fetch_step_hits_tma, dim3(grid), dim3(32), size_t(smem), st, f, 0));
         LSG_LAUNCH_CHECK("k_fetch_step_hits_tma");
         if (tma) *tma = true;
         return kOk;
@@ -467,7 +472,7 @@ int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* 
         LSG_CUDA(cudaMemsetAsync(f.mctl, 0, 16, st));
         return kOk;
     }
-    LSG_CUDA(launch_pdl(k_fetch_step_misses, g2, dim3(256), 0, st, f));
+    LSG_CUDA(launch_pdl(k_fetch_step_misses, g2, dim3(256), 0, st, f, 1));
     LSG_LAUNCH_CHECK("k_fetch_step_misses");
     return kOk;
 }
