@@ -497,7 +497,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_note": "dram read+write bytes per k_fetch_step_hits_tma launch (one steady-state "
-                                         "step, all local ranks) from profiles/r01c_summary.txt; "
+                                         "step, all local ranks) from profiles/r01f_summary.txt; "
                                          f"{traffic_ratio:.3f} x that launch's algorithmic bytes" if traffic else None,
                          "kernel": "fetch phase (k_fetch_step_hits_tma TMA bulk-copy gather + k_fetch_step_misses, "
                                    "one pair per training step)",
