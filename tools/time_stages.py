@@ -18,7 +18,7 @@ for r in range(reps):
     ev[0].record()
     tr = ls.generate_trace(tc)
     ev[1].record()
-    g = ls.build_reuse_graph(tr, C * N)
+    g = ls.build_reuse_graph(tr, C)
     ev[2].record()
     p = ls.pso_order(g, pc.pso)
     ev[3].record()
