@@ -38,7 +38,13 @@ def main():
     sim, _ = sharded_simulate(ls, plan, 1638, world, rank)
     ok["replay"] = bool(torch.equal(sim.hits, full.hits)) and bool(torch.equal(sim.misses, full.misses)) \
         and sim.total_hits == int(full.hits.sum()) and sim.total_misses == int(full.misses.sum())
-    print(json.dumps({"rank": rank, "world": world, "ok": ok}), flush=True)
+    line = json.dumps({"rank": rank, "world": world, "ok": ok})
+    out_dir = os.environ.get("LSG_MP_OUT")
+    if out_dir:  # one file per rank (stdout lines of the ranks can interleave)
+        with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+            f.write(line)
+    else:
+        print(line, flush=True)
     dist.barrier()
     dist.destroy_process_group()
     return 0 if all(ok.values()) else 1

@@ -6,6 +6,7 @@ import os
 import socket
 import subprocess
 import sys
+import tempfile
 
 import pytest
 
@@ -27,10 +28,11 @@ def test_sharded_graph_and_replay_nccl(ls):
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     n = min(n, 4)
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-                        "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-                        os.path.join(ROOT, "tests", "mp", "nccl_worker.py")],
-                       capture_output=True, text=True, timeout=600)
-    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    with tempfile.TemporaryDirectory() as d:
+        r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+                            os.path.join(ROOT, "tests", "mp", "nccl_worker.py")],
+                           capture_output=True, text=True, timeout=600, env=dict(os.environ, LSG_MP_OUT=d))
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+        lines = [json.load(open(os.path.join(d, f))) for f in sorted(os.listdir(d))]
     assert len(lines) == n and all(all(x["ok"].values()) for x in lines), lines
