@@ -66,6 +66,27 @@ __global__ void k_windows_distinct(WinGeom g, const uint32_t* __restrict__ trace
     }
 }
 
+// Same, one CTA per (epoch, window, direction): the window's D-bit bitset is
+// built in shared memory (atomicOr on banks instead of L2) and written out
+// once, coalesced. Used while a bitset fits in shared memory.
+__global__ void __launch_bounds__(1024) k_windows_smem(WinGeom g, const uint32_t* __restrict__ trace,
+                                                       uint32_t* __restrict__ Fb, uint32_t* __restrict__ Lb) {
+    extern __shared__ uint32_t bits[];
+    const uint32_t e = blockIdx.x / g.nwin, k = blockIdx.x % g.nwin, dir = blockIdx.y;
+    for (uint32_t i = threadIdx.x; i < g.words; i += blockDim.x) bits[i] = 0;
+    __syncthreads();
+    const uint32_t n = node_len(g, k);
+    const uint32_t w = uint32_t(std::min<uint64_t>(g.want, n));
+    const uint32_t* seq = trace + size_t(e) * g.len;
+    for (uint32_t q = threadIdx.x; q < w; q += blockDim.x) {
+        const uint32_t a = __ldg(&seq[node_pos(g, k, dir ? n - 1 - q : q)]);
+        atomicOr(&bits[a >> 5], 1u << (a & 31));
+    }
+    __syncthreads();
+    uint32_t* out = (dir ? Lb : Fb) + (size_t(e) * g.nwin + k) * g.words;
+    for (uint32_t i = threadIdx.x; i < g.words; i += blockDim.x) out[i] = bits[i];
+}
+
 // General path (rows may repeat ids, as read_trace admits): one warp per
 // (epoch, window, direction) walks the sequence 32 positions at a time and
 // stops exactly at the want-th distinct id. Inside a chunk only the first lane
@@ -227,8 +248,12 @@ int window_bits_device(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64
     g.want = mode == 0 ? buffer_size * N : buffer_size;
     const uint64_t W = uint64_t(g.words) * g.nwin;  // words per (epoch) row
     Scratch sc(st);
-    LSG_CUDA(cudaMemsetAsync(Fb, 0, size_t(E) * W * 4, st));
-    LSG_CUDA(cudaMemsetAsync(Lb, 0, size_t(E) * W * 4, st));
+    const size_t smem_bits = size_t(g.words) * 4;
+    const bool smem_fits = smem_bits <= 200 * 1024;
+    if (!(rows_distinct_known && smem_fits)) {  // (the shared-memory path writes every word)
+        LSG_CUDA(cudaMemsetAsync(Fb, 0, size_t(E) * W * 4, st));
+        LSG_CUDA(cudaMemsetAsync(Lb, 0, size_t(E) * W * 4, st));
+    }
 
     bool distinct = rows_distinct_known;
     if (!distinct) {
@@ -243,7 +268,11 @@ int window_bits_device(const uint32_t* d_trace, uint32_t E, uint64_t len, uint64
         LSG_CUDA(cudaStreamSynchronize(st));
         distinct = h == 0;
     }
-    if (distinct) {
+    if (distinct && smem_fits) {
+        LSG_CUDA(cudaFuncSetAttribute(k_windows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bits)));
+        k_windows_smem<<<dim3(E * g.nwin, 2), 1024, smem_bits, st>>>(g, d_trace, Fb, Lb);
+        LSG_LAUNCH_CHECK("k_windows_smem");
+    } else if (distinct) {
         const uint64_t per = std::min<uint64_t>(g.want, len);
         k_windows_distinct<<<dim3(grid_for(per, 256, 1024), E * g.nwin), 256, 0, st>>>(g, d_trace, Fb, Lb);
         LSG_LAUNCH_CHECK("k_windows_distinct");
