@@ -34,13 +34,25 @@ struct LruPlanView {
     const uint64_t* gb64;      // step bases (replay) or null
     const uint32_t* gb32;      // step bases (planner) or null
     uint32_t N, k;
+    // silent inserts (insert_redundant): step g's entries of this node are its
+    // list, then red_ids[red_off[g*N+k] .. red_off[g*N+k+1]) (node time runs
+    // through both); null when there are none
+    const uint64_t* red_off = nullptr;
+    const uint32_t* red_ids = nullptr;
     __device__ __forceinline__ uint64_t base(uint32_t g) const { return gb64 ? gb64[g] : uint64_t(__ldcg(&gb32[g])); }
-    __device__ __forceinline__ uint32_t len(uint32_t g) const {
+    __device__ __forceinline__ uint32_t llen(uint32_t g) const {  // the list
         const uint32_t* o = node_off + size_t(g) * (N + 1);
         return __ldcg(&o[k + 1]) - __ldcg(&o[k]);
     }
+    __device__ __forceinline__ uint32_t len(uint32_t g) const {  // list + silent entries
+        const uint32_t l = llen(g);
+        return red_off ? l + uint32_t(red_off[size_t(g) * N + k + 1] - red_off[size_t(g) * N + k]) : l;
+    }
     __device__ __forceinline__ const uint32_t* list(uint32_t g) const {
         return items + base(g) + __ldcg(&node_off[size_t(g) * (N + 1) + k]);
+    }
+    __device__ __forceinline__ uint32_t at(uint32_t g, uint32_t i, uint32_t l) const {  // entry i, l = llen(g)
+        return i < l ? (__ldcg(&list(g)[i]) & ~kHit) : red_ids[red_off[size_t(g) * N + k] + (i - l)];
     }
 };
 
@@ -48,18 +60,17 @@ struct LruPlanView {
 __device__ __forceinline__ uint32_t lru_evict_front(const LruPlanView& v, LruNode& st, uint32_t* last,
                                                     uint32_t tnow, uint32_t lane, uint32_t* status) {
     for (;;) {
-        const uint32_t L = v.len(st.fg);
+        const uint32_t L = v.len(st.fg), Ll = v.red_off ? v.llen(st.fg) : L;
         if (st.fi >= L) {
             st.fg += 1;
             st.fi = 0;
             continue;
         }
-        const uint32_t* lst = v.list(st.fg);
         const uint32_t j = st.fi + lane;
         uint32_t y = 0;
         bool live = false;
         if (j < L) {
-            y = __ldcg(&lst[j]) & ~kHit;
+            y = v.at(st.fg, j, Ll);
             live = __ldcg(&last[y]) == st.ft + lane;
         }
         const uint32_t vb = __ballot_sync(0xFFFFFFFFu, live);

@@ -988,6 +988,8 @@ struct LruReplayArgs {
     uint32_t* misses;    // [T][N]
     uint32_t* slot_out;  // [total items] or null
     uint32_t* status;
+    const uint64_t* red_off;  // [T*N+1] silent inserts after each list (insert_redundant) or null
+    const uint32_t* red_ids;
 };
 
 __global__ void __launch_bounds__(kRWarps * 32) k_replay_lru(LruReplayArgs a) {
@@ -998,10 +1000,10 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay_lru(LruReplayArgs a) {
     if (k >= a.k1) return;
     uint32_t* last = a.last + size_t(k) * a.D;
     uint32_t* slotk = a.slot ? a.slot + size_t(k) * a.D : nullptr;
-    const LruPlanView v{a.items, a.node_off, a.gb, nullptr, a.N, k};
+    const LruPlanView v{a.items, a.node_off, a.gb, nullptr, a.N, k, a.red_off, a.red_ids};
     LruNode st{0, 0, 0, 0, 0, 0};
     for (uint32_t g = 0; g < a.T; ++g) {
-        const uint32_t L = v.len(g);
+        const uint32_t L = v.llen(g);
         const uint64_t base = a.gb[g] + a.node_off[size_t(g) * (a.N + 1) + k];
         const uint32_t* lst = a.items + base;
         uint32_t* so = a.slot_out ? a.slot_out + base : nullptr;
@@ -1040,18 +1042,54 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay_lru(LruReplayArgs a) {
             a.misses[size_t(g) * a.N + k] = miss;
         }
         __syncwarp();
+        if (a.red_off) {  // the list's redundant ids, touched silently (they follow the list in node time)
+            const uint64_t q0 = a.red_off[size_t(g) * a.N + k], q1 = a.red_off[size_t(g) * a.N + k + 1];
+            lru_step(v, st, last, a.red_ids + q0, uint32_t(q1 - q0), a.C, lane, a.status,
+                     [](uint32_t, uint32_t) {}, [](uint32_t, uint32_t) {});
+            __syncwarp();
+        }
     }
 }
 
 }  // namespace
+
+// redundant_ids of every (step, node) list of a plan with reads, as CSR:
+// roff [T*N+1] (u64 offsets), ids [nred] (ascending per list)
+int red_csr(Scratch& sc, const uint32_t* d_items, const uint32_t* d_node_off, const uint64_t* gb,
+            const uint32_t* d_rstart, const uint32_t* d_rend, const uint32_t* d_rcount, uint64_t T, uint32_t N,
+            uint64_t L, uint32_t* d_status, cudaStream_t st, uint64_t** roff_out, uint32_t** ids_out,
+            uint64_t* nred_out) {
+    uint64_t* cnt = sc.get<uint64_t>(T * N);
+    uint64_t* roff = sc.get<uint64_t>(T * N + 1);
+    if (!cnt || !roff) return set_error(kInternal, "simulate: scratch allocation failed");
+    RedArgs r{d_items, d_node_off, gb, d_rstart, d_rend, d_rcount, uint32_t(T), N, 1, cnt, roff, nullptr, d_status};
+    while (r.P2 < L) r.P2 <<= 1;
+    const uint32_t wpb = std::max<uint32_t>(1, std::min<uint32_t>(8, (96u * 1024) / (4 * r.P2)));
+    const size_t rs = size_t(wpb) * r.P2 * 4;
+    LSG_CUDA(cudaFuncSetAttribute(k_redundant_ids, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rs)));
+    const unsigned rg = unsigned(std::min<uint64_t>((T * N + wpb - 1) / wpb, 148ull * 8));
+    k_redundant_ids<<<rg, wpb * 32, rs, st>>>(r, 0);
+    LSG_LAUNCH_CHECK("k_redundant_ids");
+    k_scan_u64<<<1, 1024, 0, st>>>(cnt, T * N, roff);
+    LSG_LAUNCH_CHECK("k_scan_u64");
+    uint64_t nred = 0;
+    if (int rc = d2h_small(&nred, roff + T * N, 8, st)) return rc;
+    uint32_t* ids = sc.get<uint32_t>(nred);
+    if (!ids) return set_error(kInternal, "simulate: scratch allocation failed");
+    r.red_ids = ids;
+    k_redundant_ids<<<rg, wpb * 32, rs, st>>>(r, 1);
+    LSG_LAUNCH_CHECK("k_redundant_ids");
+    *roff_out = roff;
+    *ids_out = ids;
+    *nred_out = nred;
+    return kOk;
+}
 
 int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_t T, uint32_t N,
                     uint64_t D, uint64_t C, int policy, uint32_t k0, uint32_t k1, uint32_t* d_hits,
                     uint32_t* d_misses, uint32_t* d_slot, const uint32_t* d_rstart, const uint32_t* d_rend,
                     const uint32_t* d_rcount, int insred, uint32_t* d_status, cudaStream_t st) {
     if (k1 <= k0 || T == 0) return kOk;
-    if (insred && policy != 0)
-        return set_error(kCapability, "simulate: insert_redundant with the LRU policy is not on the device path");
     if (insred && d_slot)
         return set_error(kCapability, "simulate: HBM slots are not tracked with insert_redundant");
     if (insred && (!d_rstart || !d_rend || !d_rcount))
@@ -1100,6 +1138,16 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         r.misses = d_misses;
         r.slot_out = d_slot;
         r.status = d_status;
+        if (insred) {  // LruBuffer::insert_silent = touch_or_insert (buffer.cpp:88-91)
+            uint64_t* roff = nullptr;
+            uint32_t* ids = nullptr;
+            uint64_t nred = 0;
+            if (int rc = red_csr(sc, d_items, d_node_off, gb, d_rstart, d_rend, d_rcount, T, N, L, d_status, st,
+                                 &roff, &ids, &nred))
+                return rc;
+            r.red_off = roff;
+            r.red_ids = ids;
+        }
         const uint32_t nk = k1 - k0;
         k_replay_lru<<<(nk + kRWarps - 1) / kRWarps, kRWarps * 32, 0, st>>>(r);
         LSG_LAUNCH_CHECK("k_replay_lru");
@@ -1163,29 +1211,14 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     if (L > 128 || insred || (fc && fc[0] == '1')) {  // long lists (and silent inserts): a CTA per node
         ReplayArgsCta c{};
         if (insred) {  // redundant ids per list (CSR) for the silent inserts
-            uint64_t* cnt = sc.get<uint64_t>(T * N);
-            uint64_t* roff = sc.get<uint64_t>(T * N + 1);
-            if (!cnt || !roff) return set_error(kInternal, "simulate: scratch allocation failed");
-            RedArgs r{d_items, d_node_off, gb, d_rstart, d_rend, d_rcount, uint32_t(T), N, 1, cnt, roff, nullptr,
-                      d_status};
-            while (r.P2 < L) r.P2 <<= 1;
-            const uint32_t wpb = std::max<uint32_t>(1, std::min<uint32_t>(8, (96u * 1024) / (4 * r.P2)));
-            const size_t rs = size_t(wpb) * r.P2 * 4;
-            LSG_CUDA(cudaFuncSetAttribute(k_redundant_ids, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rs)));
-            const unsigned rg = unsigned(std::min<uint64_t>((T * N + wpb - 1) / wpb, 148ull * 8));
-            k_redundant_ids<<<rg, wpb * 32, rs, st>>>(r, 0);
-            LSG_LAUNCH_CHECK("k_redundant_ids");
-            k_scan_u64<<<1, 1024, 0, st>>>(cnt, T * N, roff);
-            LSG_LAUNCH_CHECK("k_scan_u64");
+            uint64_t* roff = nullptr;
+            uint32_t* ids = nullptr;
             uint64_t nred = 0;
-            if (int _rc = d2h_small(&nred, roff + T * N, 8, st)) return _rc;
-            LSG_CUDA(cudaStreamSynchronize(st));
-            uint32_t* ids = sc.get<uint32_t>(nred);
+            if (int rc = red_csr(sc, d_items, d_node_off, gb, d_rstart, d_rend, d_rcount, T, N, L, d_status, st,
+                                 &roff, &ids, &nred))
+                return rc;
             uint32_t* keys = sc.get<uint32_t>(nred);
-            if (!ids || !keys) return set_error(kInternal, "simulate: scratch allocation failed");
-            r.red_ids = ids;
-            k_redundant_ids<<<rg, wpb * 32, rs, st>>>(r, 1);
-            LSG_LAUNCH_CHECK("k_redundant_ids");
+            if (!keys) return set_error(kInternal, "simulate: scratch allocation failed");
             c.red_off = roff;
             c.red_ids = ids;
             c.red_key = keys;

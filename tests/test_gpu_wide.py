@@ -175,3 +175,32 @@ def test_insert_redundant_replay(ls, seed):
     rs, re_, cnt, _, _ = O.plan_reads(ref.items, ref.node_off, N, True, thr)
     h, m = O.simulate_redundant(ref.items, ref.node_off, N, D, c.buffer_capacity, rs, re_, cnt)
     assert np.array_equal(u32(sim.hits), h) and np.array_equal(u32(sim.misses), m)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_insert_redundant_replay_lru_vs_reference(ls, seed):
+    """simulate_plan(plan, C, Lru, insert_redundant=true): the silent inserts
+    are LruBuffer::touch_or_insert (buffer.cpp:88-91) after each list. The
+    plan is the REFERENCE's own LRU + chunk_insert_redundant plan (read from
+    its plan file), and the rows must equal its metrics.csv hits/misses."""
+    if not O.ref_available():
+        pytest.skip("compiled reference not built")
+    r = random.Random(9100 + seed)
+    N, b = r.choice([1, 2, 4]), r.choice([2, 4, 8, 16])
+    B = N * b
+    D = B * r.randint(2, 10) + r.randint(0, B - 1)
+    c = O.Cfg(D, r.randint(1, 4), N, b, seed=r.randint(0, 10**6), buffer_capacity=r.randint(1, max(1, D // 3)),
+              policy="lru", optim_chunk=True, chunk_insert_redundant=True, chunk_threshold=r.choice([2, 5, 15]),
+              pso_iters=10, drop_last=r.random() < 0.7)
+    txt = O.ref_text(c)
+    plan = ls.read_plan(txt["plan"])
+    sim = ls.simulate_plan(plan, c.buffer_capacity, "lru", insert_redundant=True)
+    rows = [ln.split(",") for ln in txt["metrics"].decode().splitlines()[1:]]
+    T, N2 = plan.node_off.shape[0], plan.num_nodes
+    want_h = np.array([int(x[3]) for x in rows], dtype=np.uint32).reshape(T, N2)
+    want_m = np.array([int(x[4]) for x in rows], dtype=np.uint32).reshape(T, N2)
+    assert np.array_equal(u32(sim.hits), want_h) and np.array_equal(u32(sim.misses), want_m)
+    # and the oracle restatement agrees on the same plan
+    rs, re_, cnt = u32(plan.read_start), u32(plan.read_end), u32(plan.read_count)
+    h, m = O.simulate_redundant(u32(plan.items), u32(plan.node_off), N2, D, c.buffer_capacity, rs, re_, cnt, "lru")
+    assert np.array_equal(h, want_h) and np.array_equal(m, want_m)
