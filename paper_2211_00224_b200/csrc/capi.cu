@@ -312,6 +312,8 @@ int lsg_plan(const lsg_config* cfg, const lsg_plan_out* out, void* stream) {
     uint32_t h = 0;
     if (int _rc = d2h_small(&h, status, 4, st)) return _rc;
     LSG_CUDA(cudaStreamSynchronize(st));
+    if (h & (1u << 20))
+        return set_error(kCapability, "plan: the LRU planner's redundant ids exceed its device store (2 GiB)");
     if (h) return set_error(kInternal, "plan: device invariant violated (status " + std::to_string(h) + ")");
     return kOk;
 }

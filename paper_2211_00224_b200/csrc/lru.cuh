@@ -35,10 +35,12 @@ struct LruPlanView {
     const uint32_t* gb32;      // step bases (planner) or null
     uint32_t N, k;
     // silent inserts (insert_redundant): step g's entries of this node are its
-    // list, then red_ids[red_off[g*N+k] .. red_off[g*N+k+1]) (node time runs
-    // through both); null when there are none
+    // list, then red_ids[red_off[g*rs] .. red_off[g*rs+1]) with red_off already
+    // at this node (replay: the (step, node) CSR, rs = N; planner: the node's
+    // own row, rs = 1); node time runs through both. Null when there are none.
     const uint64_t* red_off = nullptr;
     const uint32_t* red_ids = nullptr;
+    uint32_t rs = 0;
     __device__ __forceinline__ uint64_t base(uint32_t g) const { return gb64 ? gb64[g] : uint64_t(__ldcg(&gb32[g])); }
     __device__ __forceinline__ uint32_t llen(uint32_t g) const {  // the list
         const uint32_t* o = node_off + size_t(g) * (N + 1);
@@ -46,13 +48,13 @@ struct LruPlanView {
     }
     __device__ __forceinline__ uint32_t len(uint32_t g) const {  // list + silent entries
         const uint32_t l = llen(g);
-        return red_off ? l + uint32_t(red_off[size_t(g) * N + k + 1] - red_off[size_t(g) * N + k]) : l;
+        return red_off ? l + uint32_t(__ldcg(&red_off[size_t(g) * rs + 1]) - __ldcg(&red_off[size_t(g) * rs])) : l;
     }
     __device__ __forceinline__ const uint32_t* list(uint32_t g) const {
         return items + base(g) + __ldcg(&node_off[size_t(g) * (N + 1) + k]);
     }
     __device__ __forceinline__ uint32_t at(uint32_t g, uint32_t i, uint32_t l) const {  // entry i, l = llen(g)
-        return i < l ? (__ldcg(&list(g)[i]) & ~kHit) : red_ids[red_off[size_t(g) * N + k] + (i - l)];
+        return i < l ? (__ldcg(&list(g)[i]) & ~kHit) : __ldcg(&red_ids[__ldcg(&red_off[size_t(g) * rs]) + (i - l)]);
     }
 };
 

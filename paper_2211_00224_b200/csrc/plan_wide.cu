@@ -67,6 +67,9 @@ struct WideArgs {
     uint32_t E;
     const uint32_t* inv;              // [E][D] position of id in epoch e's trace, kNone if not kept
     uint32_t* redbuf;                 // [N][B] sort scratch for lists longer than shared memory
+    uint32_t* lred;                   // LRU + insred: [N][lcap] each node's silent-touch ids, step by step
+    uint64_t* lroff;                  // LRU + insred: [N][T+1] offsets into the node's lred row
+    uint64_t lcap;
     const uint32_t* trace;            // [E][keep]
     const uint32_t* order;            // [E]
     const uint32_t* nu;               // [E*keep] next-use step, execution order
@@ -754,6 +757,85 @@ __device__ void redundant_inserts(const WideArgs& a, uint32_t k, uint32_t& bsz, 
     if (bsz > a.C) wide_evict(a, k, bsz, top, g, lane, tm);
 }
 
+// LRU + chunk_insert_redundant (pipeline.cpp:103-114 with LruBuffer::
+// insert_silent = touch_or_insert, buffer.cpp:88-91): the redundant ids of
+// node k's step-g list (the gaps inside its chunk reads, ascending, as in
+// redundant_inserts) are appended to the node's silent-touch row, where the
+// LRU front walk finds them after the list in node time. Returns the row
+// range [*r0, *r1). Leader warp of the node's team.
+__device__ void lru_redundant_ids(const WideArgs& a, uint32_t k, uint32_t g, uint32_t lane, const uint32_t* list,
+                                  uint32_t L, uint32_t* sbuf /*[2*kSortCap] shared*/, uint64_t* r0, uint64_t* r1) {
+    const uint32_t lt = lanemask_lt_w();
+    uint64_t* ro = a.lroff + size_t(k) * (a.T + 1);
+    uint32_t* row = a.lred + size_t(k) * a.lcap;
+    const uint64_t c0 = __ldcg(&ro[g]);
+    uint64_t cur_out = c0;
+    uint32_t nf = 0;
+    for (uint32_t c = 0; c < L; c += 32) {
+        const uint32_t it = c + lane < L ? __ldcg(&list[c + lane]) : kHit;
+        nf += __popc(__ballot_sync(0xFFFFFFFFu, !(it & kHit)));
+    }
+    if (nf >= 2) {
+        uint32_t P2 = 1;
+        while (P2 < nf) P2 <<= 1;
+        uint32_t* v = P2 <= 2 * kSortCap ? sbuf : a.redbuf + size_t(k) * a.B;
+        nf = 0;
+        for (uint32_t c = 0; c < L; c += 32) {
+            const uint32_t it = c + lane < L ? __ldcg(&list[c + lane]) : kHit;
+            const bool f = !(it & kHit);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
+            if (f) v[nf + __popc(bal & lt)] = it;
+            nf += __popc(bal);
+        }
+        for (uint32_t q = nf + lane; q < P2; q += 32) v[q] = 0xFFFFFFFFu;
+        __syncwarp();
+        for (uint32_t sz = 2; sz <= P2; sz <<= 1)
+            for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+                for (uint32_t r = lane; r < P2 / 2; r += 32) {
+                    const uint32_t x0 = 2 * st * (r / st) + (r % st), x1 = x0 + st;
+                    const bool up = (x0 & sz) == 0;
+                    const uint32_t p = v[x0], q = v[x1];
+                    if ((p > q) == up) {
+                        v[x0] = q;
+                        v[x1] = p;
+                    }
+                }
+                __syncwarp();
+            }
+        // greedy reads of span <= thr over the unique ids (chunking.cpp:17-30)
+        uint32_t i = 0;
+        while (i < nf) {
+            const uint32_t start = v[i];
+            uint32_t j = i + 1, prev = start;
+            while (j < nf && v[j] - start + 1 <= a.thr) {
+                const uint32_t cur = v[j];
+                if (cur != prev) {
+                    for (uint32_t y0 = prev + 1; y0 < cur; y0 += 32) {
+                        const uint32_t y = y0 + lane;
+                        const bool in = y < cur;
+                        const uint32_t ib = __ballot_sync(0xFFFFFFFFu, in);
+                        const uint64_t at = cur_out + __popc(ib & lt);
+                        if (in && at < a.lcap) row[at] = y;
+                        cur_out += __popc(ib);
+                    }
+                    prev = cur;
+                }
+                ++j;
+            }
+            i = j;
+        }
+        __syncwarp();
+    }
+    if (cur_out > a.lcap) {  // budget exceeded: the plan fails with a CapabilityError
+        if (lane == 0) atomicOr(a.status, 1u << 20);
+        cur_out = a.lcap;
+    }
+    if (lane == 0) ro[g + 1] = cur_out;
+    __syncwarp();
+    *r0 = c0;
+    *r1 = cur_out;
+}
+
 __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
     cg::cluster_group cl = cg::this_cluster();
     const uint32_t P = cl.num_blocks(), c = cl.block_rank();
@@ -1286,15 +1368,28 @@ __global__ void __launch_bounds__(kWT, 1) k_plan_wide(WideArgs a) {
             if (a.lru) {  // LruBuffer (buffer.cpp:61-82) through lru.cuh
                 uint32_t* ns = a.nst + size_t(k) * 8;
                 LruNode st{__ldcg(&ns[0]), __ldcg(&ns[2]), __ldcg(&ns[3]), __ldcg(&ns[4]), __ldcg(&ns[5]), 0};
-                const LruPlanView v{a.items, a.node_off, nullptr, a.sbase, N, k};
+                const LruPlanView v{a.items, a.node_off, nullptr, a.sbase, N, k,
+                                    a.lroff ? a.lroff + size_t(k) * (a.T + 1) : nullptr,
+                                    a.lred ? a.lred + size_t(k) * a.lcap : nullptr, 1};
                 const uint32_t kw = k >> 5, kb = 1u << (k & 31);
-                lru_step(
-                    v, st, a.where + size_t(k) * a.D, a.items + gbase + noff[k], noff[k + 1] - noff[k], a.C, lane,
-                    a.status, [](uint32_t, uint32_t) {},
-                    [&](uint32_t x, uint32_t y) {
-                        atomicOr(&a.hm[size_t(x) * W + kw], kb);
-                        if (y != kNone) atomicAnd(&a.hm[size_t(y) * W + kw], ~kb);
-                    });
+                if (a.insred && lane == 0) {  // no silent entries of step g until they are appended
+                    uint64_t* ro = a.lroff + size_t(k) * (a.T + 1);
+                    ro[g + 1] = __ldcg(&ro[g]);
+                }
+                __syncwarp();
+                auto on_miss = [&](uint32_t x, uint32_t y) {
+                    atomicOr(&a.hm[size_t(x) * W + kw], kb);
+                    if (y != kNone) atomicAnd(&a.hm[size_t(y) * W + kw], ~kb);
+                };
+                lru_step(v, st, a.where + size_t(k) * a.D, a.items + gbase + noff[k], noff[k + 1] - noff[k], a.C, lane,
+                         a.status, [](uint32_t, uint32_t) {}, on_miss);
+                if (a.insred) {  // silent touches after the list (pipeline.cpp:103-114)
+                    uint64_t r0 = 0, r1 = 0;
+                    lru_redundant_ids(a, k, g, lane, a.items + gbase + noff[k], noff[k + 1] - noff[k],
+                                      reinterpret_cast<uint32_t*>(my_sort), &r0, &r1);
+                    lru_step(v, st, a.where + size_t(k) * a.D, a.lred + size_t(k) * a.lcap + r0, uint32_t(r1 - r0),
+                             a.C, lane, a.status, [](uint32_t, uint32_t) {}, on_miss);
+                }
                 if (lane == 0) {
                     ns[0] = st.size;
                     ns[2] = st.t;
@@ -1537,8 +1632,6 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int bal
                      const uint32_t* d_trace, const uint32_t* d_order, const uint32_t* d_inv, const uint32_t* d_nu,
                      uint32_t* d_items, uint32_t* d_node_off, uint32_t* d_fb, uint32_t* d_fa, uint32_t* d_status,
                      cudaStream_t st, const uint32_t* d_hm_init, int advance) {
-    if (insred && lru)
-        return set_error(kCapability, "plan: chunk_insert_redundant with the LRU policy is not on the device path");
     if (dm.N > kWMaxN)
         return set_error(kCapability, "plan: device planner supports num_nodes <= 256 in this build");
     if (dm.b >= (1u << 21)) return set_error(kCapability, "plan: local_batch must be < 2^21 on device");
@@ -1570,6 +1663,17 @@ int plan_wide_device(const PlanDims& dm, uint64_t C, int lru, int remap, int bal
     a.E = dm.E;
     a.inv = d_inv;
     a.redbuf = insred ? sc.get<uint32_t>(size_t(N) * dm.B) : nullptr;
+    if (insred && lru) {
+        // each node's redundant ids (<= thr - 1 per fetch id), kept for the
+        // LRU front walk; beyond the budget the plan reports a CapabilityError
+        const uint64_t per_node = (dm.E * dm.keep + N - 1) / N * 2 + dm.B;
+        const uint64_t want = per_node * std::max<uint64_t>(1, std::min<uint64_t>(thr, 64) - 1);
+        a.lcap = std::min<uint64_t>(want, (uint64_t(2) << 30) / 4 / N);
+        a.lred = sc.get<uint32_t>(size_t(N) * a.lcap);
+        a.lroff = sc.get<uint64_t>(size_t(N) * (dm.T + 1));
+        if (!a.lred || !a.lroff) return set_error(kInternal, "plan: wide planner scratch allocation failed");
+        LSG_CUDA(cudaMemsetAsync(a.lroff, 0, size_t(N) * (dm.T + 1) * 8, st));
+    }
     if (insred && !a.redbuf) return set_error(kInternal, "plan: wide planner scratch allocation failed");
     a.trace = d_trace;
     a.order = d_order;

@@ -1000,7 +1000,8 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay_lru(LruReplayArgs a) {
     if (k >= a.k1) return;
     uint32_t* last = a.last + size_t(k) * a.D;
     uint32_t* slotk = a.slot ? a.slot + size_t(k) * a.D : nullptr;
-    const LruPlanView v{a.items, a.node_off, a.gb, nullptr, a.N, k, a.red_off, a.red_ids};
+    const LruPlanView v{a.items, a.node_off, a.gb, nullptr, a.N, k, a.red_off ? a.red_off + k : nullptr, a.red_ids,
+                        a.N};
     LruNode st{0, 0, 0, 0, 0, 0};
     for (uint32_t g = 0; g < a.T; ++g) {
         const uint32_t L = v.llen(g);

@@ -121,11 +121,13 @@ static int run_checks() {
         EXPECT(throws<StorageError>([&] { create_store(sp, 0, 4, 1); }));
         std::remove(sp.c_str());
     }
-    // capability guards are typed, never a silent CPU path
+    // chunk_insert_redundant with the LRU policy (silent touch_or_insert, buffer.cpp:88-91)
     PipelineConfig red = demo();
     red.chunk_insert_redundant = true;
     red.policy = Policy::Lru;
-    EXPECT(throws<CapabilityError>([&] { plan_schedule(red); }));
+    PlanOutput lro = plan_schedule(red);
+    SimResult lsim = simulate_plan(lro.plan, 64, Policy::Lru, true);
+    EXPECT(lsim.total_hits + lsim.total_misses == 6 * 1024);
     // chunk_insert_redundant (pipeline.cpp:103-114) with the clairvoyant policy
     red.policy = Policy::Clairvoyant;
     PlanOutput ro = plan_schedule(red);

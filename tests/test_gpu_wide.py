@@ -150,11 +150,28 @@ def test_insert_redundant_planner(ls, seed):
     check_plan(ls, c)
 
 
-def test_insert_redundant_lru_is_a_capability_error(ls):
-    c = O.Cfg(256, 2, 2, 8, seed=1, buffer_capacity=40, policy="lru", chunk_insert_redundant=True)
+@pytest.mark.parametrize("seed", range(10))
+def test_insert_redundant_lru_planner_vs_reference(ls, seed):
+    """plan_schedule with the LRU policy and chunk_insert_redundant
+    (pipeline.cpp:103-114, LruBuffer::insert_silent = touch_or_insert): the
+    plan file, metrics.csv and cost totals are byte-identical to the
+    compiled reference's."""
+    if not O.ref_available():
+        pytest.skip("compiled reference not built")
     from test_gpu_parity import to_pc
-    with pytest.raises(ls.CapabilityError):
-        ls.plan_schedule(to_pc(ls, c))
+    r = random.Random(9300 + seed)
+    N, b = r.choice([1, 2, 3, 4, 8]), r.choice([2, 4, 8, 16])
+    B = N * b
+    D = B * r.randint(2, 10) + r.randint(0, B - 1)
+    c = O.Cfg(D, r.randint(1, 4), N, b, seed=r.randint(0, 10**6), buffer_capacity=r.randint(1, max(1, D // 3)),
+              policy="lru", optim_chunk=True, chunk_insert_redundant=True, chunk_threshold=r.choice([2, 5, 15, 40]),
+              optim_remap=r.random() < 0.8, optim_balance=r.random() < 0.8, pso_iters=10,
+              drop_last=r.random() < 0.7)
+    out = ls.plan_schedule(to_pc(ls, c))
+    txt = O.ref_text(c)
+    assert ls.format_plan(out.plan) == txt["plan"]
+    sim = ls.simulate_plan(out.plan, c.buffer_capacity, "lru", insert_redundant=True)
+    assert ls.format_metrics(out.plan, sim, "lru") == txt["metrics"]
 
 
 @pytest.mark.parametrize("seed", range(12))
