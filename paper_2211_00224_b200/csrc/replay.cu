@@ -1233,7 +1233,10 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         c.slot_out = d_slot; c.status = d_status;
         k_replay_nextuse_cta<<<nk, kRT, 0, st>>>(c);
         LSG_LAUNCH_CHECK("k_replay_nextuse_cta");
-        const size_t smem = exclusive_smem(size_t(L) * 4 + (L + 2) * 2 + 16);
+        // a whole SM per rank only while the ranks fit in one wave with room
+        // to spare (256 simulated ranks would otherwise run in two waves)
+        const size_t need = size_t(L) * 4 + (L + 2) * 2 + 16;
+        const size_t smem = nk <= 32 ? exclusive_smem(need) : need;
         LSG_CUDA(cudaFuncSetAttribute(k_replay_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         const bool pinned = l2_pin(st, hot, hot_words * 4);
         k_replay_cta<<<nk, kRT, smem, st>>>(c);
