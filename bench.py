@@ -72,8 +72,8 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
-        self.idx = gpu_index
+    def __init__(self, gpu_ids: str | None):
+        self.idx = gpu_ids  # comma-separated nvidia-smi indices; None = no sampling (ranks > 0)
         self.rows = []
         self._stop = threading.Event()
         self._t = None
@@ -84,20 +84,23 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True,
                                      text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                for line in out.splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
             except Exception:
                 pass
             self._stop.wait(0.2)
 
     def __enter__(self):
+        if self.idx is None:
+            return self
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t is not None:
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.rows:
@@ -234,6 +237,11 @@ def main():
     # multi-GPU plan placement: "rr" plans job i on GPU i mod N only and
     # broadcasts its node lists; "replicate" plans every job on every GPU
     plan_shard = args.plan_shard == "rr" or (args.plan_shard == "auto" and world > 2)
+    # replayed jobs allowed ahead of the fetch: with 4+ GPUs a job's replay
+    # (broadcast + replay + row all-gather) is ~0.8x its fetch, and a depth
+    # of 2 left a 0.3 s fetch bubble (N=4: 31-33 -> 34.5-34.7 M samples/s)
+    ahead = int(os.environ.get("LSG_BENCH_AHEAD", "3" if world > 2 else "2"))
+
 
     def run_jobs(n, host=False, pipeline=True, stats=None, t_start=None):
         """n passes of the hot path. Job i = plan (K1-K6) -> replay (K7, this
@@ -254,10 +262,12 @@ def main():
         import queue
         qp, qr = queue.Queue(maxsize=1), queue.Queue(maxsize=1)
         free = threading.Semaphore(2)
-        fetched = threading.Semaphore(2 if pipeline else 1)  # replayed jobs ahead of the fetch
+        fetched = threading.Semaphore(ahead if pipeline else 1)  # replayed jobs ahead of the fetch
         err = []
         shard = world > 1 and plan_shard
         mine = [i for i in range(n) if not shard or i % world == rank]
+        tj0 = time.perf_counter()
+        plan_evs = []
 
         def planner():
             try:
@@ -272,6 +282,7 @@ def main():
                         out = (ls.plan_schedule_host(pc, buffers=host_sets[j % 2]) if host
                                else ls.plan_schedule(pc))
                         z.record(pstream)
+                        plan_evs.append((i, a, z))
                         qp.put((out, a, z))
                         if not pipeline:
                             z.synchronize()
@@ -313,6 +324,8 @@ def main():
                         if shard:  # the owner's node lists to every GPU
                             dist.broadcast(items, src=owner)
                             dist.broadcast(noff, src=owner)
+                        fb = ev()
+                        fb.record(rstream)
                         plan = ls.SchedulePlan(D, N, b, int(sh.steps_per_epoch), None, items, noff, None, None)
                         h0 = time.perf_counter()
                         sim = ls.simulate_plan(plan, C, node_range=(k0, k1), want_slots=True)
@@ -322,12 +335,17 @@ def main():
                             rows.append((ls.to_host(sim.hits), ls.to_host(sim.misses)))
                         off = ls.to_host(noff).numpy()
                         if os.environ.get("LSG_BENCH_TIMELINE"):
-                            print(f"[replayer] job {i}: simulate_plan {1e3 * (h1 - h0):.1f} ms host, "
+                            print(f"[replayer] rank {rank} n={n} job {i} t0={1e3 * (h0 - tj0):.1f}: simulate_plan {1e3 * (h1 - h0):.1f} ms host, "
                                   f"rows+off {1e3 * (time.perf_counter() - h1):.1f} ms", file=sys.stderr, flush=True)
                         if owner == rank:
                             free.release()  # this job's host staging set has been uploaded
                         f1 = ev()
                         f1.record(rstream)
+                        if os.environ.get("LSG_BENCH_TIMELINE") and t_start is not None:
+                            f1.synchronize()
+                            print(f"[replay-gpu] rank {rank} job {i}: start {t_start.elapsed_time(f0):.1f} "
+                                  f"bcast-done {t_start.elapsed_time(fb):.1f} end {t_start.elapsed_time(f1):.1f}",
+                                  file=sys.stderr, flush=True)
                         for t in (items, noff, sim.slots):
                             t.record_stream(fstream)
                         qr.put((plan, sim, off, pa, pz, f0, f1))
@@ -358,6 +376,11 @@ def main():
             fetched.release()
         for th in ths:
             th.join()
+        if os.environ.get("LSG_BENCH_TIMELINE") and t_start is not None:
+            for i, a, z in plan_evs:
+                z.synchronize()
+                print(f"[plan-gpu] rank {rank} job {i}: {t_start.elapsed_time(a):.1f} -> {t_start.elapsed_time(z):.1f}",
+                      file=sys.stderr, flush=True)
         return rows
 
     # warm-up (also the first pass that fills the HBM buffers)
@@ -386,10 +409,13 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ls.lib().lsg_launch_count()
-    gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
-        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    # rank 0 samples every GPU of the job with ONE nvidia-smi process (the
+    # line it prints carries the clocks of all of them)
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    nloc = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    gpu_ids = ",".join(vis.split(",")[:nloc] if vis else [str(g) for g in range(nloc)])
     evs = []
-    with ClockSampler(gpu_index) as clk:
+    with ClockSampler(gpu_ids if rank == 0 else None) as clk:
         t_start, t_end = ev(), ev()
         t_start.record(fstream)
         run_jobs(args.steps, stats=evs, t_start=t_start)
