@@ -241,6 +241,7 @@ def main():
     # (broadcast + replay + row all-gather) is ~0.8x its fetch, and a depth
     # of 2 left a 0.3 s fetch bubble (N=4: 31-33 -> 34.5-34.7 M samples/s)
     ahead = int(os.environ.get("LSG_BENCH_AHEAD", "3" if world > 2 else "2"))
+    rr_shift = int(os.environ.get("LSG_BENCH_RR_SHIFT", "0"))  # debug: job i planned on GPU (i + shift) mod N
 
 
     def run_jobs(n, host=False, pipeline=True, stats=None, t_start=None):
@@ -265,7 +266,7 @@ def main():
         fetched = threading.Semaphore(ahead if pipeline else 1)  # replayed jobs ahead of the fetch
         err = []
         shard = world > 1 and plan_shard
-        mine = [i for i in range(n) if not shard or i % world == rank]
+        mine = [i for i in range(n) if not shard or (i + rr_shift) % world == rank]
         tj0 = time.perf_counter()
         plan_evs = []
 
@@ -299,7 +300,7 @@ def main():
                     if t_start is not None:
                         rstream.wait_event(t_start)
                     for i in range(n):
-                        owner = i % world if shard else rank
+                        owner = (i + rr_shift) % world if shard else rank
                         pa = pz = None
                         if owner == rank:
                             got = qp.get()
