@@ -386,6 +386,12 @@ def main():
 
     # warm-up (also the first pass that fills the HBM buffers)
     nwarm = max(args.warmup, 3 if args.steps else 0)
+    if nwarm and world > 1 and plan_shard:
+        # every GPU plans at least one warm-up job: a GPU's FIRST plan
+        # allocates its output tensors (cudaMalloc), which waited for the
+        # NCCL broadcast kernel spinning on that GPU, doubling the plan of
+        # job world-1 inside the timed region (4 GPUs: 380 -> 680-800 ms)
+        nwarm = max(nwarm, world)
     if nwarm:
         run_jobs(nwarm)
     torch.cuda.synchronize()
