@@ -430,8 +430,8 @@ def main():
         torch.cuda.synchronize()
     launches = ls.lib().lsg_launch_count() - launches0
     total_ms = t_start.elapsed_time(t_end)
-    timeline = None
-    if os.environ.get("LSG_BENCH_TIMELINE"):  # per-job stage windows (ms from t_start)
+    # per-job stage windows on rank 0 (ms from t_start), read after the timed region
+    if True:
         timeline = [[round(t_start.elapsed_time(x), 1) if x is not None else None for x in (e[0], e[1], e[2], e[3], e[7], e[4])]
                     for e in evs]
     own = [e[0].elapsed_time(e[1]) for e in evs if e[0] is not None]
