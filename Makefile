@@ -23,7 +23,7 @@ tests/cpp/dropin_test: tests/cpp/dropin_test.cpp include/loadsched_gpu.hpp $(HOS
 	g++ -std=c++20 -O2 -Wall -Iinclude tests/cpp/dropin_test.cpp -L$(PKG) -lloadsched_gpu -lsolar_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -o $@
 
-build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh include/lsg.h
+build/%.o: $(CSRC)/%.cu $(wildcard $(CSRC)/*.cuh) include/lsg.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

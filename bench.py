@@ -51,12 +51,45 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "plan samples/s (shuffle+order+evict+assign); HBM-buffer gather GB/s; 1-8 GPU"
-CFG2 = dict(D=262144, E=100, N=8, b=512, C=52428, sample_bytes=256 * 256 * 4, seed=42, fill_seed=1)
-# cfg3 (CosmoFlow 128^3 x 4 fp16 = 16 MiB samples): b, E and C are unspecified
-# in BASELINE.json; SURVEY.md §8d chose b=8, E=10, C=8192 (128 GiB per rank)
-CFG3 = dict(D=65536, E=10, N=8, b=8, C=8192, sample_bytes=4 * 128 ** 3 * 2, seed=42, fill_seed=1)
+# BASELINE.json configs; b, E and C where BASELINE leaves them open are
+# SURVEY.md §8d's choices. kind "job" = plan + replay + batch fetch of the
+# whole job; "plan" = plan + replay (cfg4: reuse matrix + ordering stress,
+# cfg5: replay + assignment sweep over logical ranks).
+CONFIGS = {
+    "cfg1": dict(D=16384, E=10, N=4, b=64, C=1638, sample_bytes=256 * 256 * 4, kind="job",
+                 label="PtychoNN-shaped, 10%/rank"),
+    "cfg2": dict(D=262144, E=100, N=8, b=512, C=52428, sample_bytes=256 * 256 * 4, kind="job",
+                 label="PtychoNN-shaped, 20%/rank"),
+    "cfg3": dict(D=65536, E=10, N=8, b=8, C=8192, sample_bytes=4 * 128 ** 3 * 2, kind="job",
+                 label="CosmoFlow-shaped 16 MiB samples, 128 GiB/rank"),
+    "cfg4": dict(D=131072, E=500, N=8, b=64, C=6553, sample_bytes=64 ** 3 * 4, kind="plan",
+                 label="AutoPhaseNN-shaped, 5%/rank (40% pooled): 500x500 reuse matrix + ordering"),
+    "cfg5": dict(D=1048576, E=1000, N=32, b=512, C=16384, sample_bytes=0, kind="plan",
+                 label="1M-id space, logical ranks, 50% pooled buffer"),
+}
+CFG2 = CONFIGS["cfg2"]
+for _c in CONFIGS.values():
+    _c.setdefault("seed", 42)
+    _c.setdefault("fill_seed", 1)
 HBM_BUDGET = 150 * 2 ** 30  # bytes of sample buffers one GPU may hold
-E_SAMPLE = 3  # reference arm: epochs of the bounded CPU sample
+
+
+def config_for(args) -> dict:
+    c = dict(CONFIGS[args.config])
+    if args.ranks:  # cfg5 sweep: N logical ranks, C = D / (2N) (50% pooled)
+        c["N"] = args.ranks
+        if args.config == "cfg5":
+            c["C"] = c["D"] // (2 * args.ranks)
+    if args.epochs:
+        c["E"] = args.epochs
+    return c
+
+
+def workload(name: str, c: dict) -> str:
+    sb = c["sample_bytes"]
+    size = f", {sb >> 20} MiB samples" if sb >= 1 << 20 else f", {sb >> 10} KiB samples" if sb else ""
+    what = "plan+replay+fetch of the whole job" if c["kind"] == "job" else "plan+replay of the whole job"
+    return (f"{name}: D={c['D']} E={c['E']} N={c['N']} b={c['b']} C={c['C']} ({c['label']}){size}, {what}")
 
 
 def env_rank():
@@ -114,7 +147,50 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- reference --
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def ref_gather(O, c: dict, warmup: int, steps: int) -> dict:
+    """The reference's batch fetch: Store::read_one (store.cpp:134-139) from a
+    page-cached store file, on every host core; each step reads one training
+    step's global batch (N*b random samples). One store, W + K rounds."""
+    SB = c["sample_bytes"]
+    B = c["N"] * c["b"]
+    count = max(B, min(c["D"], (4 << 30) // SB))  # a store of >= 4 GiB (or the dataset)
+    nreads = max(B, (1 << 30) // SB)  # >= 1 GiB per round, so thread start-up is noise
+    tmp = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+    thr = host_cores()
+    out = subprocess.run([O.REF_DUMP, "gather", tmp, str(count), str(SB), str(nreads), str(thr),
+                          str(warmup + steps)], check=True, capture_output=True, text=True)
+    g = json.loads(out.stdout.strip().splitlines()[-1])
+    timed = g["reps"][warmup:]
+    g["step_s"] = timed
+    g["per_sample_s"] = statistics.median(timed) / nreads
+    g["store_samples"] = count
+    return g
+
+
+def ref_planner(O, c: dict, env_extra=None) -> dict:
+    """One plan_schedule + simulate_plan pass (pipeline.cpp:32-120,
+    buffer.cpp:183-247) of the reference on one host core."""
+    cfg = O.Cfg(c["D"], c["E"], c["N"], c["b"], seed=c["seed"], buffer_capacity=c["C"])
+    env = dict(os.environ, REF_DUMP_STAGES="0", **(env_extra or {}))
+    out = subprocess.run([O.REF_DUMP, "time", "1", *cfg.kv()], check=True, capture_output=True, text=True,
+                         env=env).stdout.strip().splitlines()[-1]
+    return json.loads(out)
+
+
 def run_reference(args):
+    """The reference's own CPU implementation of the path (oracle/_ref, the
+    UNMODIFIED library compiled from /root/reference/proj/src) on this host:
+    the planner (single-threaded by construction) on the FULL job once, and the
+    Store::read_one batch fetch on every host core, W warm-up + K timed
+    steps of one global batch each. value = accesses / (planner seconds +
+    accesses x fetch seconds per sample)."""
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
@@ -125,47 +201,50 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_dump not built "
                           "(needs /root/reference at build time)"}))
         return 0
-    c = CFG2
-    cfg = O.Cfg(c["D"], E_SAMPLE, c["N"], c["b"], seed=c["seed"], buffer_capacity=c["C"])
-    ncpu = os.cpu_count() or 1
-    nreads = 4096
-
-    def one_step():
-        t = O.ref_time(cfg, 1)
-        with_tmp = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
-        g = json.loads(subprocess.run([O.REF_DUMP, "gather", with_tmp, "4096", str(c["sample_bytes"]),
-                                       str(nreads), str(ncpu)], check=True, capture_output=True,
-                                      text=True).stdout.strip().splitlines()[-1])
+    c = config_for(args)
+    cores = host_cores()
+    keep = (c["D"] // (c["N"] * c["b"])) * c["N"] * c["b"]
+    A = c["E"] * keep
+    # planner: the whole job when it fits the driver's step budget, else
+    # (cfg5: hours on one core) E = 1 and 3 and a linear fit in E
+    full = args.config != "cfg5"
+    if full:
+        t = ref_planner(O, c)
         plan_s = t["plan_schedule_s"] + t["simulate_s"]
-        per_sample = plan_s / t["accesses"] + g["seconds"] / g["samples"]
-        return per_sample, t, g
-
-    for _ in range(args.warmup):
-        one_step()
-    per, ts = [], []
-    for _ in range(args.steps):
-        p, t, g = one_step()
-        per.append(p)
-        ts.append((t, g))
-    per_sample = statistics.median(per)
-    value = 1.0 / per_sample
-    t, g = ts[len(ts) // 2]
-    A = c["E"] * c["D"]
+        psample = f"full job, {t['accesses']} accesses: plan_schedule {t['plan_schedule_s']:.1f} s + " \
+                  f"simulate_plan {t['simulate_s']:.1f} s (measured, not extrapolated)"
+        same = True
+    else:
+        pts = []
+        for e in (1, 3):
+            ce = dict(c, E=e)
+            t = ref_planner(O, ce)
+            pts.append((e, t["plan_schedule_s"] + t["simulate_s"]))
+        slope = (pts[1][1] - pts[0][1]) / 2
+        plan_s = pts[0][1] + slope * (c["E"] - 1)
+        psample = f"E=1: {pts[0][1]:.1f} s, E=3: {pts[1][1]:.1f} s, linear in E to E={c['E']} " \
+                  "(extrapolated: BASELINE.md §3)"
+        same = False
+    g = ref_gather(O, c, args.warmup, max(args.steps, 1)) if c["sample_bytes"] else None
+    gps = g["per_sample_s"] if g else 0.0
+    total_s = plan_s + A * gps
+    value = A / total_s
+    gsample = (f"; fetch: {args.steps} steps of {g['samples']} x Store::read_one of "
+               f"{c['sample_bytes']} B from a {g['store_samples']}-sample page-cached store on {g['threads']} "
+               f"threads, median {gps * 1e6:.2f} us/sample x {A} accesses") if g else ""
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_sample * A * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": total_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": "cfg2: D=262144 E=100 N=8 b=512 C=52428 (20%/rank), 256 KiB samples",
-                   "global_batch": c["N"] * c["b"], "parallelism": "reference CPU"},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": f"1 (planner, single-threaded by "
-                         f"construction) + {g['threads']} (Store::read_one fetch)", "kind": "reference",
-                         "sample": f"plan_schedule+simulate_plan on the cfg2 shape with E={E_SAMPLE} epochs "
-                                   f"({t['accesses']} accesses, {t['plan_schedule_s'] + t['simulate_s']:.2f} s) + "
-                                   f"{g['samples']} Store::read_one of 256 KiB ({g['seconds']:.3f} s); "
-                                   f"per-sample cost extrapolated to the {A}-access job"},
+        "config": {"workload": workload(args.config, c), "global_batch": c["N"] * c["b"],
+                   "parallelism": "reference CPU (planner single-threaded by construction)"},
+        "cpu_baseline": {"value": value, "unit": "samples/s",
+                         "cores": f"1 (planner) + {cores} (Store::read_one) of {os.cpu_count()} host cores",
+                         "kind": "reference", "sample": "planner: " + psample + gsample,
+                         "same_config": same},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "reference_stages_s": {k: t[k] for k in ("trace_s", "graph_s", "pso_s", "plan_schedule_s", "simulate_s")},
+        "reference_stages_s": {"planner_s": plan_s, "fetch_s_per_sample": gps, "fetch_s_job": A * gps},
     }
     print(json.dumps(line))
     return 0
@@ -183,7 +262,8 @@ def main():
     ap.add_argument("--plan-shard", default="auto", choices=["auto", "rr", "replicate"],
                     help="N>1: plan each job on one GPU (rr) or on all (replicate); auto = rr above 2 GPUs")
     ap.add_argument("--prio", type=int, default=1, help="plan and replay streams at high priority")
-    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--ranks", type=int, default=None, help="cfg5: logical ranks (32-256; C = D/(2N))")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -557,8 +637,11 @@ def main():
     return 0
 
 
-def cpu_baseline():
-    """The reference CPU planner (oracle/_ref) on a bounded sample, rank 0 only."""
+def cpu_baseline(c: dict, name: str):
+    """The reference CPU planner (oracle/_ref) on a bounded sample of the
+    job (~10-20 s of one core: the first E_s epochs) plus Store::read_one on
+    all host cores; rank 0 at N=1 only. The bench's reference arm times the
+    full job."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     try:
         import oracle as O
@@ -567,19 +650,18 @@ def cpu_baseline():
     if not O.ref_available():
         return {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
-    c = CFG2
-    cfg = O.Cfg(c["D"], E_SAMPLE, c["N"], c["b"], seed=c["seed"], buffer_capacity=c["C"])
-    t = O.ref_time(cfg, 1)
-    tmp = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
-    ncpu = os.cpu_count() or 1
-    g = json.loads(subprocess.run([O.REF_DUMP, "gather", tmp, "4096", str(c["sample_bytes"]), "4096",
-                                   str(ncpu)], check=True, capture_output=True, text=True).stdout.strip().splitlines()[-1])
-    per = (t["plan_schedule_s"] + t["simulate_s"]) / t["accesses"] + g["seconds"] / g["samples"]
+    es = min(c["E"], 10 if name in ("cfg2", "cfg4") else 3 if name == "cfg5" else c["E"])
+    ce = dict(c, E=es)
+    t = ref_planner(O, ce)
+    g = ref_gather(O, c, 1, 3) if c["sample_bytes"] else None
+    per = (t["plan_schedule_s"] + t["simulate_s"]) / t["accesses"] + (g["per_sample_s"] if g else 0.0)
     return {"value": 1.0 / per, "unit": "samples/s",
-            "cores": f"1 (planner) + {g['threads']} (Store::read_one)", "kind": "reference",
-            "sample": f"cfg2 shape, E={E_SAMPLE} epochs ({t['accesses']} accesses): plan_schedule "
-                      f"{t['plan_schedule_s']:.2f} s + simulate_plan {t['simulate_s']:.2f} s; "
-                      f"{g['samples']} Store::read_one 256 KiB in {g['seconds']:.3f} s",
+            "cores": f"1 (planner) + {host_cores()} (Store::read_one) of {os.cpu_count()} host cores",
+            "kind": "reference",
+            "sample": f"{name} shape, first E={es} of {c['E']} epochs ({t['accesses']} accesses): plan_schedule "
+                      f"{t['plan_schedule_s']:.2f} s + simulate_plan {t['simulate_s']:.2f} s"
+                      + (f"; Store::read_one of {c['sample_bytes']} B: {g['per_sample_s'] * 1e6:.2f} us/sample "
+                         f"on {g['threads']} threads (median of 3 global batches)" if g else ""),
             "plan_samples_per_s": t["accesses"] / t["plan_schedule_s"]}
 
 

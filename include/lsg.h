@@ -195,6 +195,51 @@ int lsg_fetch_steps(void* const* d_bufs, void* const* d_outs, const uint32_t* d_
                     uint64_t step_end, uint32_t N, uint32_t node_begin, uint32_t node_end,
                     uint64_t sample_bytes, uint64_t fill_seed, void* stream);
 
+/* ---- The loading phase of a whole job with a real miss source ----
+ * The HOST TIER: the Store payload rows of the whole dataset (store.cpp:70-80;
+ * row i at byte i * sample_bytes, i.e. the Store file without its 22-byte
+ * header) in a file on a tmpfs, mapped and pinned (cudaHostRegister, mapped),
+ * so all processes of a box share one copy and the GPU reads it over PCIe.
+ * create != 0 writes the file (host threads); else it is opened and must be
+ * count x sample_bytes long. Errors: Storage (6). */
+typedef struct lsg_host_rows lsg_host_rows;
+int lsg_host_rows_open(const char* path, uint64_t count, uint64_t sample_bytes, uint64_t fill_seed, int32_t create,
+                       lsg_host_rows** out);
+int lsg_host_rows_info(const lsg_host_rows* h, uint64_t* count, uint64_t* sample_bytes, void** host_base);
+void lsg_host_rows_close(lsg_host_rows* h);
+
+/* A job's fetch (replaces Store::read_one/read_chunk, store.hpp:42-44, for the
+ * batches of steps [step_begin, step_end) of ranks [node_begin, node_end)):
+ * hits are gathered from the HBM sample buffers (TMA bulk copies), misses come
+ * from `host` (NULL: the Store payload synthesised on device) into their batch
+ * row and, unless the replay bypassed them, their new buffer slot.
+ * lsg_fetch_job_create builds the job's miss list on `stream` and, with a
+ * host tier, starts the miss prefetcher there (a persistent kernel reading
+ * the host rows over PCIe into a device ring of about ring_bytes, 0 = 2 GiB)
+ * and returns once it is resident; `stream` then stays busy until the job's
+ * misses are consumed, so give each job in flight its own. lsg_fetch_job_run
+ * enqueues the steps on the fetch stream (it waits for the miss list only).
+ * lsg_fetch_job_stats (synchronous) reads {misses, kept misses, host bytes,
+ * hits}; lsg_fetch_job_destroy frees stream-ordered after the job. */
+typedef struct lsg_fetch_job lsg_fetch_job;
+typedef struct {
+    void* const* d_bufs;        /* device array of (node_end - node_begin) HBM buffer pointers */
+    void* const* d_outs;        /* device array of batch tensor pointers */
+    const uint32_t* d_items;    /* the whole plan's items (lsg_plan_out layout) */
+    const uint32_t* d_slots;    /* lsg_simulate d_slot of the same plan */
+    const uint32_t* d_node_off; /* [T][N+1] */
+    const uint32_t* h_node_off; /* host copy of the offsets */
+    uint64_t step_begin, step_end;
+    uint32_t N, node_begin, node_end;
+    uint64_t sample_bytes, fill_seed;
+    const lsg_host_rows* host;  /* NULL: synthesised misses */
+    uint64_t ring_bytes;
+} lsg_fetch_job_desc;
+int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, void* stream);
+int lsg_fetch_job_run(lsg_fetch_job* job, void* stream);
+int lsg_fetch_job_stats(lsg_fetch_job* job, uint64_t* h_stats4, void* stream);
+void lsg_fetch_job_destroy(lsg_fetch_job* job, void* stream);
+
 /* ---- The sample Store (store.hpp:13-81, store.cpp:37-148): SLRD files
  *      (22-byte header + one continuous splitmix64 payload stream).
  *      Errors: Storage (6) for I/O, format and budget failures, Validation

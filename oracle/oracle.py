@@ -348,6 +348,18 @@ def store_payload(fill_seed: int, offset: int, n: int) -> np.ndarray:
     return out[:n]
 
 
+def compact_reads(rstart, rend, rcount, node_off, N):
+    """The valid (start, end) pairs of every (step, node) list in plan order
+    (list (g, k)'s reads sit at its item offsets): the layout-independent form
+    the full-size goldens hash (tools/make_goldens.py)."""
+    node_off = np.asarray(node_off).reshape(-1, N + 1).astype(np.int64)
+    base = np.concatenate([[0], np.cumsum(node_off[:, N])[:-1]])
+    lo = (base[:, None] + node_off[:, :N]).ravel()
+    cnt = np.asarray(rcount).reshape(-1).astype(np.int64)
+    idx = np.repeat(lo, cnt) + (np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt))
+    return np.stack([np.asarray(rstart)[idx], np.asarray(rend)[idx]], axis=1).astype(np.uint32)
+
+
 # ------------------------------------------------------- compiled reference --
 def ref_available() -> bool:
     return os.path.exists(REF_DUMP)

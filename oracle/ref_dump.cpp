@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iostream>
@@ -196,7 +197,9 @@ int cmd_plan(int argc, char** argv) {
     dump_plan(dir, out.plan);
     const bool redundant = cfg.chunk_insert_redundant && cfg.optim_chunk;
     dump_sim(dir, simulate_plan(out.plan, cfg.buffer_capacity, cfg.policy, redundant));
-    if (!redundant) dump_residency(dir, cfg, out);
+    // REF_DUMP_NO_RESIDENCY=1 skips the shadow replay (full-size golden runs)
+    const char* nores = std::getenv("REF_DUMP_NO_RESIDENCY");
+    if (!redundant && !(nores && nores[0] == '1')) dump_residency(dir, cfg, out);
     return 0;
 }
 
@@ -245,19 +248,25 @@ int cmd_time(int argc, char** argv) {
     const PipelineConfig cfg = parse_kv(argc, argv, 3);
     double t_trace = 0, t_graph = 0, t_pso = 0, t_plan = 0, t_sim = 0;
     std::uint64_t accesses = 0, misses = 0;
+    // REF_DUMP_STAGES=0: time plan_schedule + simulate_plan only (the stage
+    // split re-runs trace, graph and PSO outside plan_schedule)
+    const char* stg = std::getenv("REF_DUMP_STAGES");
+    const bool stages = !(stg && stg[0] == '0');
     for (int r = 0; r < reps; ++r) {
         auto t0 = std::chrono::steady_clock::now();
-        const AccessTrace trace = generate_trace(cfg.trace);
-        t_trace += secs(t0);
-        t0 = std::chrono::steady_clock::now();
-        const ReuseGraph graph = build_reuse_graph(trace, cfg.buffer_capacity, cfg.graph_mode);
-        t_graph += secs(t0);
-        if (cfg.optim_order) {
-            PsoParams p = cfg.pso;
-            p.seed = cfg.trace.seed;
+        if (stages) {
+            const AccessTrace trace = generate_trace(cfg.trace);
+            t_trace += secs(t0);
             t0 = std::chrono::steady_clock::now();
-            (void)pso_order(graph, p);
-            t_pso += secs(t0);
+            const ReuseGraph graph = build_reuse_graph(trace, cfg.buffer_capacity, cfg.graph_mode);
+            t_graph += secs(t0);
+            if (cfg.optim_order) {
+                PsoParams p = cfg.pso;
+                p.seed = cfg.trace.seed;
+                t0 = std::chrono::steady_clock::now();
+                (void)pso_order(graph, p);
+                t_pso += secs(t0);
+            }
         }
         t0 = std::chrono::steady_clock::now();
         const PlanOutput out = plan_schedule(cfg); // repeats trace/graph/pso internally
@@ -278,39 +287,45 @@ int cmd_time(int argc, char** argv) {
 }
 
 // Batch fetch through the reference's own Store::read_one (store.cpp:134-139)
-// from a page-cached store file: `nreads` random samples split over
-// `threads` host threads (Store is documented safe for concurrent reads,
-// store.hpp:29-30). Prints JSON.
+// from a page-cached store file: `reps` rounds of `nreads` random samples
+// split over `threads` host threads (Store is documented safe for concurrent
+// reads, store.hpp:29-30). Prints JSON with every round's seconds.
 int cmd_gather(int argc, char** argv) {
-    if (argc < 7) throw ValidationError("gather <dir> count size nreads threads");
+    if (argc < 7) throw ValidationError("gather <dir> count size nreads threads [reps]");
     const std::string path = std::string(argv[2]) + "/ref_gather_store.bin";
     const std::uint64_t count = std::stoull(argv[3]), size = std::stoull(argv[4]);
     const std::uint64_t nreads = std::stoull(argv[5]);
     const unsigned threads = unsigned(std::stoul(argv[6]));
+    const int reps = argc > 7 ? std::stoi(argv[7]) : 1;
     create_store(path, count, size, 1, ~0ULL);
     Store store(path);
     for (std::uint64_t i = 0; i < count; ++i) (void)store.read_one(i);  // page-cache warm
-    std::vector<std::uint64_t> ids(nreads);
     SplitMix64 rng(7);
-    for (auto& v : ids) v = rng.next_below(count);
-    std::vector<std::thread> pool;
-    std::vector<std::uint64_t> sink(threads, 0);
-    const auto t0 = std::chrono::steady_clock::now();
-    for (unsigned t = 0; t < threads; ++t)
-        pool.emplace_back([&, t] {
-            for (std::uint64_t i = t; i < nreads; i += threads) {
-                const auto bytes = store.read_one(ids[i]);
-                sink[t] += std::to_integer<unsigned>(bytes[i % bytes.size()]);
-            }
-        });
-    for (auto& th : pool) th.join();
-    const double sec = secs(t0);
-    std::remove(path.c_str());
+    std::vector<double> secs_per_rep;
     std::uint64_t chk = 0;
-    for (auto v : sink) chk += v;
-    std::printf("{\"seconds\": %.6f, \"samples\": %llu, \"bytes\": %llu, \"threads\": %u, \"chk\": %llu}\n",
-                sec, (unsigned long long)nreads, (unsigned long long)(nreads * size), threads,
+    for (int r = 0; r < reps; ++r) {
+        std::vector<std::uint64_t> ids(nreads);
+        for (auto& v : ids) v = rng.next_below(count);
+        std::vector<std::thread> pool;
+        std::vector<std::uint64_t> sink(threads, 0);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (unsigned t = 0; t < threads; ++t)
+            pool.emplace_back([&, t] {
+                for (std::uint64_t i = t; i < nreads; i += threads) {
+                    const auto bytes = store.read_one(ids[i]);
+                    sink[t] += std::to_integer<unsigned>(bytes[i % bytes.size()]);
+                }
+            });
+        for (auto& th : pool) th.join();
+        secs_per_rep.push_back(secs(t0));
+        for (auto v : sink) chk += v;
+    }
+    std::remove(path.c_str());
+    std::printf("{\"seconds\": %.6f, \"samples\": %llu, \"bytes\": %llu, \"threads\": %u, \"chk\": %llu, \"reps\": [",
+                secs_per_rep.back(), (unsigned long long)nreads, (unsigned long long)(nreads * size), threads,
                 (unsigned long long)chk);
+    for (std::size_t i = 0; i < secs_per_rep.size(); ++i) std::printf("%s%.6f", i ? ", " : "", secs_per_rep[i]);
+    std::printf("]}\n");
     return 0;
 }
 

@@ -94,8 +94,18 @@ EXPORTS = [
     "lsg_buffer_windows", "lsg_brute_force_order", "lsg_remap_step", "lsg_balance_step", "lsg_plan_chunks",
     "lsg_buffer_create", "lsg_buffer_destroy", "lsg_buffer_access", "lsg_buffer_clear", "lsg_buffer_resident",
     "lsg_simulate_sequence", "lsg_optimal_miss_oracle", "lsg_build_reuse_graph_rows",
-    "lsg_fetch_steps",
+    "lsg_fetch_steps", "lsg_host_rows_open", "lsg_host_rows_info", "lsg_host_rows_close",
+    "lsg_fetch_job_create", "lsg_fetch_job_run", "lsg_fetch_job_stats", "lsg_fetch_job_destroy",
 ]
+
+
+class LsgFetchJobDesc(ctypes.Structure):
+    """Field-for-field mirror of ``lsg_fetch_job_desc`` (include/lsg.h)."""
+    _fields_ = [(n, ctypes.c_void_p) for n in ("d_bufs", "d_outs", "d_items", "d_slots", "d_node_off",
+                                               "h_node_off")] + [
+        ("step_begin", ctypes.c_uint64), ("step_end", ctypes.c_uint64), ("N", ctypes.c_uint32),
+        ("node_begin", ctypes.c_uint32), ("node_end", ctypes.c_uint32), ("sample_bytes", ctypes.c_uint64),
+        ("fill_seed", ctypes.c_uint64), ("host", ctypes.c_void_p), ("ring_bytes", ctypes.c_uint64)]
 
 
 class LsgError(RuntimeError):
@@ -166,6 +176,15 @@ def lib() -> ctypes.CDLL:
         L.lsg_store_read.argtypes = [P, u64, u64, P]
         L.lsg_store_read_rows.argtypes = [P, P, u64, u64, P, P]
         L.lsg_fetch_step_store.argtypes = [P, P, P, P, P, P, P, P, u32, u32, u64, u64, P]
+        L.lsg_host_rows_open.argtypes = [ctypes.c_char_p, u64, u64, u64, i32, ctypes.POINTER(ctypes.c_void_p)]
+        L.lsg_host_rows_info.argtypes = [P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_void_p)]
+        L.lsg_host_rows_close.argtypes = [P]
+        L.lsg_host_rows_close.restype = None
+        L.lsg_fetch_job_create.argtypes = [ctypes.POINTER(LsgFetchJobDesc), ctypes.POINTER(ctypes.c_void_p), P]
+        L.lsg_fetch_job_run.argtypes = [P, P]
+        L.lsg_fetch_job_stats.argtypes = [P, ctypes.POINTER(u64), P]
+        L.lsg_fetch_job_destroy.argtypes = [P, P]
+        L.lsg_fetch_job_destroy.restype = None
         _lib = L
     return _lib
 

@@ -418,20 +418,14 @@ int lsg_fetch_steps(void* const* d_bufs, void* const* d_outs, const uint32_t* d_
                     const uint32_t* d_node_off, const uint32_t* h_node_off, uint64_t step_begin,
                     uint64_t step_end, uint32_t N, uint32_t node_begin, uint32_t node_end,
                     uint64_t sample_bytes, uint64_t fill_seed, void* stream) {
-    if (node_begin > node_end || node_end > N) return set_error(kValidation, "fetch_steps: bad node range");
-    if (step_begin > step_end) return set_error(kValidation, "fetch_steps: bad step range");
-    if (!h_node_off) return set_error(kValidation, "fetch_steps: host node offsets required");
-    uint64_t base = 0;
-    for (uint64_t g = 0; g < step_begin; ++g) base += h_node_off[g * (N + 1) + N];
-    for (uint64_t g = step_begin; g < step_end; ++g) {
-        const uint32_t* o = h_node_off + g * (N + 1);
-        if (int rc = fetch_step_device(d_bufs, d_outs, d_items + base, d_slots + base, d_node_off + g * (N + 1),
-                                       node_begin, node_end, uint64_t(o[node_end] - o[node_begin]), sample_bytes,
-                                       fill_seed, static_cast<cudaStream_t>(stream)))
-            return rc;
-        base += o[N];
-    }
-    return kOk;
+    // a job without a host tier: misses synthesised on device (lsg_fetch_job)
+    lsg_fetch_job_desc d{d_bufs, d_outs, d_items, d_slots, d_node_off, h_node_off, step_begin, step_end,
+                         N, node_begin, node_end, sample_bytes, fill_seed, nullptr, 0};
+    lsg_fetch_job* j = nullptr;
+    if (int rc = lsg_fetch_job_create(&d, &j, stream)) return rc;
+    const int rc = lsg_fetch_job_run(j, stream);
+    lsg_fetch_job_destroy(j, stream);
+    return rc;
 }
 
 }  // extern "C"

@@ -1,0 +1,621 @@
+// fetch_job.cu — the loading phase of a whole job (a step range of a plan)
+// with a real miss source.
+//
+// The reference reads every sample of a batch from its Store (store.cpp:123-148,
+// pread at 22 + i*size). Here hits come from the rank's HBM sample buffer
+// (K8, TMA bulk copies, gather.cu) and misses from the HOST TIER: the Store
+// payload rows of the whole dataset in host memory (a tmpfs file, mapped and
+// pinned, so every process of a box shares one copy), read over PCIe.
+//
+//   lsg_host_rows      the host tier: payload byte j of the file = byte j%8 of
+//                      mix(fill_seed + (j/8+1)*gamma) (store.cpp:70-80), row i
+//                      at i*sample_bytes — the Store file without its 22-byte
+//                      header, so rows stay 16-byte aligned for TMA.
+//   miss list          per job: the rows of every step whose replay slot is
+//                      not a hit, in step order (k_miss_list count pass,
+//                      scan, list pass), built on the device.
+//   K10 prefetcher     a persistent kernel (32 single-thread CTAs) walks the
+//                      miss list ahead of the fetch: TMA bulk copies from the
+//                      MAPPED host rows (cp.async.bulk global->shared reads
+//                      host memory over PCIe: 51 GB/s measured,
+//                      tools/ubench_h2d.cu) into a device ring, publishing
+//                      each row with a release flag. It waits for ring space
+//                      on a consumed counter. It is launched when the job is
+//                      created, so it runs ahead while earlier work (the
+//                      previous job's fetch) still holds the fetch stream.
+//   misses kernel      after step g's hit kernel: every miss row of g copied
+//                      ring -> batch row and, unless the replay bypassed the
+//                      sample, -> its new HBM slot; the last block of the step
+//                      releases the step's ring rows. Without a host tier the
+//                      payload is synthesised on device instead (K9).
+//
+// Slot order: a miss may refill a slot whose previous sample was hit earlier
+// in the same step, so misses run after the step's hit kernel (as the
+// single-step path does); the next step's hit kernel runs after them.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fetch.cuh"
+
+struct lsg_host_rows {
+    std::string path;
+    int fd = -1;
+    unsigned char* base = nullptr;
+    unsigned char* dev = nullptr;  // device alias of base (mapped, pinned)
+    uint64_t count = 0, sample_bytes = 0, bytes = 0;
+    bool registered = false;
+};
+
+namespace lsg {
+
+namespace {
+
+constexpr int kPfTile = 8192, kPfStages = 3, kPfCtas = 32;
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// per-step row counts of the node range and the job's step item bases
+struct ListArgs {
+    const uint32_t* items;
+    const uint32_t* slots;
+    const uint32_t* node_off;  // job's first step's [N+1] offsets
+    const uint32_t* base;      // [nsteps] item offset of each step (job-relative)
+    uint32_t N, k0, k1, nsteps;
+    uint32_t* cnt;             // [nsteps] misses per step
+    uint32_t* moff;            // [nsteps+1] exclusive scan of cnt
+    uint32_t* mrow;            // [M] step-relative row of each miss
+    uint32_t* mid;             // [M] its sample id
+    unsigned long long* stats; // [4] misses, kept, host bytes, hits
+    uint64_t host_row_bytes;   // 0 without a host tier
+};
+
+// one block per step: count (pass 0) or list (pass 1) the step's miss rows
+// in row order
+__global__ void __launch_bounds__(256) k_miss_list(ListArgs a, int pass) {
+    __shared__ uint32_t wsum[8];
+    __shared__ uint32_t carry;
+    const uint32_t g = blockIdx.x;
+    const uint32_t* off = a.node_off + size_t(g) * (a.N + 1);
+    const uint32_t r0 = off[a.k0], r1 = off[a.k1];
+    const uint64_t b = a.base[g];  // job-relative item offset of the step
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = pass ? a.moff[g] : 0u;
+    __syncthreads();
+    uint32_t kept = 0;
+    for (uint32_t c = r0; c < r1; c += 256) {
+        const uint32_t r = c + threadIdx.x;
+        bool miss = false;
+        uint32_t sl = kNever;
+        if (r < r1) {
+            sl = __ldg(&a.slots[b + r]);
+            miss = sl == kNever || !(sl & kHit);
+        }
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, miss);
+        if (lane == 0) wsum[w] = __popc(bal);
+        __syncthreads();
+        uint32_t before = 0, total = 0;
+        for (int q = 0; q < 8; ++q) {
+            before += q < int(w) ? wsum[q] : 0u;
+            total += wsum[q];
+        }
+        if (miss) {
+            kept += sl != kNever;
+            if (pass) {
+                const uint32_t at = carry + before + __popc(bal & ((1u << lane) - 1));
+                a.mrow[at] = r;
+                a.mid[at] = __ldg(&a.items[b + r]) & ~kHit;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+    if (pass == 0) {
+        kept = __reduce_add_sync(0xFFFFFFFFu, kept);
+        if (lane == 0 && kept) atomicAdd(&a.stats[1], (unsigned long long)kept);
+        if (threadIdx.x == 0) {
+            a.cnt[g] = carry;
+            atomicAdd(&a.stats[0], (unsigned long long)carry);
+            atomicAdd(&a.stats[2], (unsigned long long)carry * a.host_row_bytes);
+            atomicAdd(&a.stats[3], (unsigned long long)(r1 - r0 - carry));
+        }
+    }
+}
+
+// single-block exclusive scan of u32 values in[i * stride] (n up to a few
+// 1e5) -> out[n+1]
+__global__ void __launch_bounds__(1024) k_scan_u32(const uint32_t* __restrict__ in, uint32_t n, uint32_t stride,
+                                                   uint32_t* __restrict__ out) {
+    __shared__ uint32_t part[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint32_t c = 0; c < n; c += 1024) {
+        const uint32_t i = c + threadIdx.x;
+        const uint32_t v = i < n ? in[size_t(i) * stride] : 0u;
+        uint32_t inc = v;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= uint32_t(d)) inc += o;
+        }
+        if (lane == 31) part[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            const uint32_t p = part[lane];
+            uint32_t pi = p;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, pi, d);
+                if (lane >= uint32_t(d)) pi += o;
+            }
+            part[lane] = pi - p;
+        }
+        __syncthreads();
+        if (i < n) out[i] = carry + part[w] + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += part[w] + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[n] = carry;
+}
+
+struct PrefetchArgs {
+    const unsigned char* host;  // device alias of the mapped host rows
+    const uint32_t* mid;        // sample id of each miss, job order
+    const uint32_t* total;      // &moff[nsteps]
+    uint64_t row_bytes;
+    unsigned char* ring;
+    uint32_t R;                 // ring rows
+    uint32_t* ready;            // [R] row m is in ring slot m % R once ready[m % R] == m + 1
+    const uint32_t* consumed;   // misses released by the consumers (a prefix of the list)
+    unsigned int* resident;     // host-mapped: CTAs that started
+};
+
+// K10: TMA bulk copies host -> shared -> ring, kPfStages tiles in flight per
+// CTA, rows round-robin over the CTAs
+__global__ void __launch_bounds__(32) k_miss_prefetch_tma(PrefetchArgs a) {
+    extern __shared__ __align__(128) unsigned char psm[];
+    __shared__ __align__(8) unsigned long long bar[kPfStages];
+    if (threadIdx.x != 0) return;
+    atomicAdd_system(a.resident, 1u);
+    for (int q = 0; q < kPfStages; ++q) {
+        const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bq));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    const uint32_t M = *a.total;
+    const uint64_t tpr = a.row_bytes / kPfTile;
+    uint32_t phase[kPfStages] = {};
+    for (uint32_t m = blockIdx.x; m < M; m += gridDim.x) {
+        if (m >= a.R)
+            while (ld_acquire(a.consumed) < m - a.R + 1) __nanosleep(256);
+        const unsigned char* src = a.host + uint64_t(__ldg(&a.mid[m])) * a.row_bytes;
+        unsigned char* dst = a.ring + uint64_t(m % a.R) * a.row_bytes;
+        auto load = [&](uint64_t t) {
+            const int q = int(t % kPfStages);
+            const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(psm + q * kPfTile));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bq), "r"(kPfTile));
+            asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(d), "l"(src + t * kPfTile), "r"(kPfTile), "r"(bq) : "memory");
+        };
+        for (uint64_t t = 0; t < tpr && t < uint64_t(kPfStages); ++t) load(t);
+        for (uint64_t t = 0; t < tpr; ++t) {
+            const int q = int(t % kPfStages);
+            const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
+            uint32_t done = 0;
+            while (!done)
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                             : "=r"(done) : "r"(bq), "r"(phase[q]) : "memory");
+            phase[q] ^= 1u;
+            const unsigned sp = static_cast<unsigned>(__cvta_generic_to_shared(psm + q * kPfTile));
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + t * kPfTile),
+                         "r"(sp), "r"(kPfTile) : "memory");
+            asm volatile("cp.async.bulk.commit_group;");
+            if (t + kPfStages < tpr) {  // stage q is reloaded once its store has read it
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                load(t + kPfStages);
+            }
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the row is in the ring
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        st_release(&a.ready[m % a.R], m + 1);
+    }
+}
+
+// K10 for rows that are not whole TMA tiles: 128-bit loads of mapped host memory
+__global__ void __launch_bounds__(256) k_miss_prefetch_lsu(PrefetchArgs a) {
+    if (threadIdx.x == 0) atomicAdd_system(a.resident, 1u);
+    const uint32_t M = *a.total;
+    const uint64_t vpr = a.row_bytes / 16;
+    for (uint32_t m = blockIdx.x; m < M; m += gridDim.x) {
+        if (threadIdx.x == 0 && m >= a.R)
+            while (ld_acquire(a.consumed) < m - a.R + 1) __nanosleep(256);
+        __syncthreads();
+        const uint4* src = reinterpret_cast<const uint4*>(a.host + uint64_t(__ldg(&a.mid[m])) * a.row_bytes);
+        uint4* dst = reinterpret_cast<uint4*>(a.ring + uint64_t(m % a.R) * a.row_bytes);
+        for (uint64_t p = threadIdx.x; p < vpr; p += blockDim.x) __stcg(&dst[p], src[p]);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release(&a.ready[m % a.R], m + 1);
+        }
+    }
+}
+
+struct MissArgs {
+    StepFetch f;               // step g (items/slots/node_off at the step)
+    const uint32_t* moff;      // [nsteps+1]
+    uint32_t gi;               // step index in the job
+    const uint32_t* mrow;
+    const unsigned char* ring; // null: synthesise the Store payload
+    uint32_t R;
+    const uint32_t* ready;
+    uint32_t* consumed;
+    uint32_t* done;            // [nsteps] finished blocks per step
+};
+
+// the misses of one step: batch row and (kept) new slot from the ring or the
+// synthesised payload; the step's last block releases its ring rows
+__global__ void __launch_bounds__(256) k_job_misses(MissArgs a) {
+    const StepFetch& f = a.f;
+    const uint32_t m0 = __ldg(&a.moff[a.gi]), m1 = __ldg(&a.moff[a.gi + 1]);
+    const uint64_t vpr = f.vec_per_row;
+    const uint64_t row_bytes = vpr * 16;
+    for (uint32_t m = m0 + blockIdx.y; m < m1; m += gridDim.y) {
+        const uint32_t r = __ldg(&a.mrow[m]);
+        const uint32_t sl = __ldg(&f.slots[r]);
+        const uint32_t k = node_of_row(f, r);
+        uint4* out = f.outs[k - f.k0] + uint64_t(r - __ldg(&f.node_off[k])) * vpr;
+        uint4* buf = sl != kNever ? f.bufs[k - f.k0] + uint64_t(sl) * vpr : nullptr;
+        if (a.ring) {
+            if (threadIdx.x == 0)
+                while (ld_acquire(&a.ready[m % a.R]) != m + 1) __nanosleep(128);
+            __syncthreads();
+            const uint4* src = reinterpret_cast<const uint4*>(a.ring + uint64_t(m % a.R) * row_bytes);
+            for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < vpr;
+                 p += uint64_t(gridDim.x) * blockDim.x) {
+                const uint4 v = __ldcg(&src[p]);
+                __stcs(&out[p], v);
+                if (buf) __stcs(&buf[p], v);
+            }
+        } else {
+            const uint64_t word0 = uint64_t(__ldg(&f.items[r]) & ~kHit) * (2 * vpr);
+            ulonglong2* o2 = reinterpret_cast<ulonglong2*>(out);
+            ulonglong2* b2 = reinterpret_cast<ulonglong2*>(buf);
+            for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < vpr;
+                 p += uint64_t(gridDim.x) * blockDim.x) {
+                ulonglong2 v;
+                v.x = mix64(f.seed + (word0 + 2 * p + 1) * kGamma);
+                v.y = mix64(f.seed + (word0 + 2 * p + 2) * kGamma);
+                __stcs(&o2[p], v);
+                if (b2) __stcs(&b2[p], v);
+            }
+        }
+    }
+    if (a.ring) {  // every block has read its ring rows: the last one releases the step's
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const uint32_t t = atomicAdd(&a.done[a.gi], 1u);
+            if (t == gridDim.x * gridDim.y - 1) atomicMax(a.consumed, m1);
+        }
+    }
+}
+
+}  // namespace
+
+}  // namespace lsg
+
+struct lsg_fetch_job {
+    lsg_fetch_job_desc d;
+    std::vector<uint64_t> base;  // [nsteps+1] item offset of each step (absolute)
+    std::vector<uint32_t> rows;  // [nsteps] rows of the node range per step
+    uint64_t nsteps = 0;
+    // device state (stream-ordered pool)
+    uint32_t* d_base = nullptr;  // [nsteps+1] job-relative step bases
+    uint32_t* d_ctl = nullptr;   // claims [nsteps] | done [nsteps] | cnt [nsteps] | moff [nsteps+1] | consumed
+    uint32_t* mrow = nullptr;
+    uint32_t* mid = nullptr;
+    unsigned char* ring = nullptr;
+    uint32_t* ready = nullptr;
+    unsigned long long* stats = nullptr;
+    uint32_t R = 0;
+    unsigned int* resident = nullptr;  // pinned host counter
+    cudaEvent_t listed = nullptr;      // the miss list is built (run waits for it)
+    cudaEvent_t prefetched = nullptr;  // the prefetcher finished (destroy waits for it)
+    bool prefetching = false;
+    cudaStream_t prep = nullptr;       // the stream the prefetcher holds
+};
+
+namespace lsg {
+
+namespace {
+
+void fill_payload(unsigned char* base, uint64_t bytes, uint64_t seed) {
+    const uint64_t words = bytes / 8;
+    const unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([=] {
+            const uint64_t w0 = words * t / nt, w1 = words * (t + 1) / nt;
+            uint64_t* p = reinterpret_cast<uint64_t*>(base);
+            for (uint64_t w = w0; w < w1; ++w) p[w] = mix64(seed + (w + 1) * kGamma);  // little-endian bytes
+        });
+    for (auto& x : th) x.join();
+    for (uint64_t j = words * 8; j < bytes; ++j)  // tail bytes
+        base[j] = uint8_t(mix64(seed + (j / 8 + 1) * kGamma) >> (8 * (j % 8)));
+}
+
+}  // namespace
+
+}  // namespace lsg
+
+using namespace lsg;
+
+extern "C" {
+
+int lsg_host_rows_open(const char* path, uint64_t count, uint64_t sample_bytes, uint64_t fill_seed, int32_t create,
+                       lsg_host_rows** out) {
+    if (!path || !out) return set_error(kValidation, "host_rows: path and out are required");
+    if (count == 0 || sample_bytes == 0 || sample_bytes % 16)
+        return set_error(kValidation, "host_rows: count >= 1 and sample_bytes a positive multiple of 16 required");
+    auto* h = new lsg_host_rows();
+    h->path = path;
+    h->count = count;
+    h->sample_bytes = sample_bytes;
+    h->bytes = count * sample_bytes;
+    h->fd = ::open(path, create ? (O_RDWR | O_CREAT | O_TRUNC) : O_RDWR, 0644);
+    auto fail = [&](const std::string& msg) {
+        if (h->base) munmap(h->base, h->bytes);
+        if (h->fd >= 0) ::close(h->fd);
+        delete h;
+        return set_error(kStorage, msg);
+    };
+    if (h->fd < 0) return fail("host_rows: cannot open " + h->path);
+    if (create) {
+        if (ftruncate(h->fd, off_t(h->bytes)) != 0) return fail("host_rows: cannot size " + h->path);
+    } else {
+        struct stat st{};
+        if (fstat(h->fd, &st) != 0 || uint64_t(st.st_size) != h->bytes)
+            return fail("host_rows: " + h->path + " is not count x sample_bytes long");
+    }
+    void* p = mmap(nullptr, h->bytes, PROT_READ | PROT_WRITE, MAP_SHARED, h->fd, 0);
+    if (p == MAP_FAILED) return fail("host_rows: mmap failed for " + h->path);
+    h->base = static_cast<unsigned char*>(p);
+    if (create) fill_payload(h->base, h->bytes, fill_seed);
+    if (cudaHostRegister(h->base, h->bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return fail("host_rows: cudaHostRegister failed for " + h->path);
+    }
+    h->registered = true;
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, h->base, 0) != cudaSuccess) {
+        cudaGetLastError();
+        cudaHostUnregister(h->base);
+        return fail("host_rows: no device alias for " + h->path);
+    }
+    h->dev = static_cast<unsigned char*>(dp);
+    *out = h;
+    return kOk;
+}
+
+int lsg_host_rows_info(const lsg_host_rows* h, uint64_t* count, uint64_t* sample_bytes, void** host_base) {
+    if (!h) return set_error(kValidation, "host_rows: null handle");
+    if (count) *count = h->count;
+    if (sample_bytes) *sample_bytes = h->sample_bytes;
+    if (host_base) *host_base = h->base;
+    return kOk;
+}
+
+void lsg_host_rows_close(lsg_host_rows* h) {
+    if (!h) return;
+    if (h->registered) cudaHostUnregister(h->base);
+    if (h->base) munmap(h->base, h->bytes);
+    if (h->fd >= 0) ::close(h->fd);
+    delete h;
+}
+
+int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, void* stream) {
+    if (!desc || !out) return set_error(kValidation, "fetch_job: desc and out are required");
+    const lsg_fetch_job_desc& d = *desc;
+    if (d.node_begin > d.node_end || d.node_end > d.N) return set_error(kValidation, "fetch_job: bad node range");
+    if (d.step_begin > d.step_end) return set_error(kValidation, "fetch_job: bad step range");
+    if (!d.h_node_off) return set_error(kValidation, "fetch_job: host node offsets required");
+    if (d.sample_bytes == 0 || d.sample_bytes % 16)
+        return set_error(kValidation, "fetch_job: sample_bytes must be a positive multiple of 16");
+    if (d.host && d.host->sample_bytes != d.sample_bytes)
+        return set_error(kValidation, "fetch_job: host rows differ in sample size");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    keep_pool();
+    auto* j = new lsg_fetch_job();
+    j->d = d;
+    const uint32_t N = d.N;
+    j->nsteps = d.step_end - d.step_begin;
+    uint64_t b = 0;
+    for (uint64_t g = 0; g < d.step_begin; ++g) b += d.h_node_off[g * (N + 1) + N];
+    uint64_t total_rows = 0, max_rows = 0;
+    for (uint64_t g = d.step_begin; g < d.step_end; ++g) {
+        const uint32_t* o = d.h_node_off + g * (N + 1);
+        if (o[d.node_end] < o[d.node_begin]) {
+            delete j;
+            return set_error(kValidation, "fetch_job: node offsets not ascending");
+        }
+        j->base.push_back(b);
+        j->rows.push_back(o[d.node_end] - o[d.node_begin]);
+        total_rows += j->rows.back();
+        max_rows = std::max<uint64_t>(max_rows, j->rows.back());
+        b += o[N];
+    }
+    j->base.push_back(b);
+    if (total_rows >= 0xFFFFFFF0ull || b - j->base[0] >= 0xFFFFFFF0ull) {
+        delete j;
+        return set_error(kCapability, "fetch_job: more than 2^32 items in one job");
+    }
+    auto fail = [&](int rc) {
+        lsg_fetch_job_destroy(j, stream);
+        return rc;
+    };
+    const uint64_t ns = j->nsteps;
+    auto alloc = [&](void** p, size_t bytes) { return cudaMallocAsync(p, std::max<size_t>(bytes, 16), st) == cudaSuccess; };
+    if (!alloc(reinterpret_cast<void**>(&j->d_base), (ns + 1) * 4) ||
+        !alloc(reinterpret_cast<void**>(&j->d_ctl), (4 * ns + 2) * 4) ||
+        !alloc(reinterpret_cast<void**>(&j->stats), 32) ||
+        !alloc(reinterpret_cast<void**>(&j->mrow), total_rows * 4) ||
+        !alloc(reinterpret_cast<void**>(&j->mid), total_rows * 4))
+        return fail(set_error(kInternal, "fetch_job: device allocation failed"));
+    if (cudaMemsetAsync(j->d_ctl, 0, (4 * ns + 2) * 4, st) != cudaSuccess ||
+        cudaMemsetAsync(j->stats, 0, 32, st) != cudaSuccess)
+        return fail(cuda_error(cudaGetLastError(), "fetch_job setup"));
+    uint32_t* cnt = j->d_ctl + 2 * ns;
+    uint32_t* moff = j->d_ctl + 3 * ns;
+    if (ns) {
+        const uint32_t* noff = d.d_node_off + d.step_begin * (N + 1);
+        k_scan_u32<<<1, 1024, 0, st>>>(noff + N, uint32_t(ns), N + 1, j->d_base);  // step bases
+        count_launch();
+        ListArgs la{d.d_items + j->base[0], d.d_slots + j->base[0], noff, j->d_base, N, d.node_begin, d.node_end,
+                    uint32_t(ns), cnt, moff, j->mrow, j->mid, j->stats, d.host ? d.sample_bytes : 0};
+        k_miss_list<<<unsigned(ns), 256, 0, st>>>(la, 0);
+        count_launch();
+        k_scan_u32<<<1, 1024, 0, st>>>(cnt, uint32_t(ns), 1, moff);
+        count_launch();
+        k_miss_list<<<unsigned(ns), 256, 0, st>>>(la, 1);
+        count_launch();
+    }
+    if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return fail(cuda_error(e, "fetch_job: miss list"));
+    cudaEventCreateWithFlags(&j->listed, cudaEventDisableTiming);
+    cudaEventRecord(j->listed, st);
+    if (d.host && ns && total_rows) {
+        // ring: at least the largest step (a step's misses are consumed
+        // together), at most ring_bytes beyond that
+        const uint64_t want = d.ring_bytes ? d.ring_bytes : (uint64_t(2) << 30);
+        const uint64_t R = std::min<uint64_t>(total_rows, std::max<uint64_t>(max_rows, want / d.sample_bytes));
+        j->R = uint32_t(R);
+        if (!alloc(reinterpret_cast<void**>(&j->ring), R * d.sample_bytes) ||
+            !alloc(reinterpret_cast<void**>(&j->ready), R * 4))
+            return fail(set_error(kInternal, "fetch_job: ring allocation failed"));
+        if (cudaMemsetAsync(j->ready, 0, R * 4, st) != cudaSuccess)
+            return fail(cuda_error(cudaGetLastError(), "fetch_job ring"));
+        if (cudaHostAlloc(&j->resident, 4, cudaHostAllocMapped) != cudaSuccess)
+            return fail(set_error(kInternal, "fetch_job: pinned counter"));
+        *j->resident = 0;
+        unsigned int* dres = nullptr;
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&dres), j->resident, 0);
+        PrefetchArgs pa{d.host->dev, j->mid, moff + ns, d.sample_bytes, j->ring, j->R, j->ready,
+                        j->d_ctl + 4 * ns + 1, dres};
+        const bool tma = d.sample_bytes % kPfTile == 0;
+        if (tma) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_miss_prefetch_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kPfTile * kPfStages);
+                attr = true;
+            }
+            k_miss_prefetch_tma<<<kPfCtas, 32, kPfTile * kPfStages, st>>>(pa);
+        } else {
+            k_miss_prefetch_lsu<<<kPfCtas, 256, 0, st>>>(pa);
+        }
+        count_launch();
+        if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return fail(cuda_error(e, "k_miss_prefetch"));
+        cudaEventCreateWithFlags(&j->prefetched, cudaEventDisableTiming);
+        cudaEventRecord(j->prefetched, st);
+        j->prefetching = true;
+        j->prep = st;
+        // the consumers spin on ring rows: return only once every prefetch
+        // CTA is resident (it then runs to completion beside anything)
+        const auto t0 = std::chrono::steady_clock::now();
+        while (__atomic_load_n(j->resident, __ATOMIC_ACQUIRE) < unsigned(kPfCtas)) {
+            if (cudaStreamQuery(st) == cudaSuccess) break;  // finished already (tiny job)
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+                return fail(set_error(kInternal, "fetch_job: the miss prefetcher never became resident"));
+            std::this_thread::yield();
+        }
+    }
+    *out = j;
+    return kOk;
+}
+
+int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
+    if (!j) return set_error(kValidation, "fetch_job: null job");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (j->prefetching && st == j->prep)
+        return set_error(kValidation, "fetch_job: run on the stream the miss prefetcher holds (it would wait for itself)");
+    const lsg_fetch_job_desc& d = j->d;
+    const uint32_t N = d.N, ns = uint32_t(j->nsteps);
+    if (j->listed) LSG_CUDA(cudaStreamWaitEvent(st, j->listed, 0));  // NOT the prefetcher: it needs these kernels
+    uint32_t* claims = j->d_ctl;
+    uint32_t* done = j->d_ctl + ns;
+    uint32_t* moff = j->d_ctl + 3 * ns;
+    uint32_t* consumed = j->d_ctl + 4 * ns + 1;
+    for (uint32_t gi = 0; gi < ns; ++gi) {
+        const uint64_t g = d.step_begin + gi;
+        const uint64_t b = j->base[gi];
+        StepFetch f{};
+        f.items = d.d_items + b;
+        f.slots = d.d_slots + b;
+        f.node_off = d.d_node_off + g * (N + 1);
+        f.bufs = reinterpret_cast<uint4* const*>(d.d_bufs);
+        f.outs = reinterpret_cast<uint4* const*>(d.d_outs);
+        f.k0 = d.node_begin;
+        f.k1 = d.node_end;
+        f.vec_per_row = d.sample_bytes / 16;
+        f.tiles_per_row = (f.vec_per_row + 1023) / 1024;
+        f.seed = d.fill_seed;
+        f.claim = claims + gi;
+        const uint64_t rows = j->rows[gi];
+        if (rows == 0 || d.node_begin == d.node_end) continue;
+        if (int rc = launch_fetch_hits(f, rows, d.sample_bytes, st, nullptr)) return rc;
+        MissArgs ma{f, moff, gi, j->mrow, j->ring, j->R, j->ready, consumed, done};
+        const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 64)),
+                        unsigned(std::min<uint64_t>(rows, 148)));
+        k_job_misses<<<grid, 256, 0, st>>>(ma);
+        LSG_LAUNCH_CHECK("k_job_misses");
+    }
+    return kOk;
+}
+
+int lsg_fetch_job_stats(lsg_fetch_job* j, uint64_t* h_stats, void* stream) {
+    if (!j || !h_stats) return set_error(kValidation, "fetch_job: null argument");
+    unsigned long long s[4] = {};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    LSG_CUDA(cudaMemcpyAsync(s, j->stats, 32, cudaMemcpyDeviceToHost, st));
+    LSG_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i < 4; ++i) h_stats[i] = s[i];
+    return kOk;
+}
+
+void lsg_fetch_job_destroy(lsg_fetch_job* j, void* stream) {
+    if (!j) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (j->prefetching) cudaStreamWaitEvent(st, j->prefetched, 0);
+    for (void* p : {static_cast<void*>(j->d_base), static_cast<void*>(j->d_ctl), static_cast<void*>(j->mrow),
+                    static_cast<void*>(j->mid), static_cast<void*>(j->ring), static_cast<void*>(j->ready),
+                    static_cast<void*>(j->stats)})
+        if (p) cudaFreeAsync(p, st);
+    if (j->prefetched) cudaEventDestroy(j->prefetched);
+    if (j->listed) cudaEventDestroy(j->listed);
+    if (j->resident) {
+        cudaStreamSynchronize(st);  // nothing still writes the mapped counter
+        cudaFreeHost(j->resident);
+    }
+    delete j;
+}
+
+}  // extern "C"

@@ -15,7 +15,7 @@
 #include <atomic>
 #include <cstdlib>
 
-#include "common.cuh"
+#include "fetch.cuh"
 
 namespace lsg {
 
@@ -131,29 +131,6 @@ __global__ void __launch_bounds__(256) k_fill_misses(const uint32_t* __restrict_
     }
 }
 
-// Step-level fetch for a contiguous range of nodes [k0, k1): their lists are
-// contiguous in the step's item array (rows node_off[k0] .. node_off[k1]), so
-// one launch covers every local rank of the step. Row r of node k goes to
-// outs[k - k0] row r - node_off[k] and, for hits, comes from bufs[k - k0].
-struct StepFetch {
-    const uint32_t* items;     // step's items (ids | hit tag)
-    const uint32_t* slots;     // step's replay slots (bit 31 = resident at step start)
-    const uint32_t* node_off;  // [N+1] of the step
-    uint4* const* bufs;        // [k1-k0] HBM sample buffers
-    uint4* const* outs;        // [k1-k0] batch tensors
-    uint32_t k0, k1;
-    uint64_t vec_per_row, tiles_per_row, seed;
-    uint32_t* mlist;           // miss rows of the step (filled by the TMA hit kernel) or null
-    uint32_t* mctl;            // [3] miss count, finished misses blocks, hit tiles claimed
-    int l2hint;                // TMA copies tagged L2::evict_first (streaming)
-};
-
-__device__ __forceinline__ uint32_t node_of_row(const StepFetch& f, uint32_t r) {
-    uint32_t k = f.k0;
-    while (k + 1 < f.k1 && __ldg(&f.node_off[k + 1]) <= r) ++k;
-    return k;
-}
-
 __global__ void __launch_bounds__(kGatherThreads) k_fetch_step_hits(StepFetch f) {
     const uint32_t r0 = __ldg(&f.node_off[f.k0]);
     const uint64_t nrows = __ldg(&f.node_off[f.k1]) - r0;
@@ -187,7 +164,7 @@ __global__ void __launch_bounds__(kGatherThreads) k_fetch_step_hits(StepFetch f)
 // a slot is refilled once the store of its tile has read it, checked kLag
 // stores later, so up to kLag+1 stores and kStages-kLag-1 loads are in
 // flight. CTAs claim chunks of kTmaChunk consecutive tiles from a per-step
-// counter (mctl[2], reset by the misses kernel), so a CTA that starts late
+// counter (f.claim, zeroed per call), so a CTA that starts late
 // (an SM shared with the planner's persistent CTA) takes fewer chunks instead
 // of stretching the step; row descriptors change once per row and miss rows
 // are skipped whole. Measured at 6.56 TB/s on the cfg2 shape vs 5.75 for the
@@ -212,14 +189,14 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
     const uint64_t row_bytes = f.vec_per_row * 16, tpr = row_bytes / kTmaTile;
     const uint32_t r0 = __ldg(&f.node_off[f.k0]);
     const uint64_t nt = uint64_t(__ldg(&f.node_off[f.k1]) - r0) * tpr;
-    // static split without a counter (mctl == null), else dynamic chunks
+    // static split without a counter (claim == null), else dynamic chunks
     uint64_t tb, te;
     // guided claims: kTmaChunk tiles while plenty remain, then kTmaTail, so
     // the step's last CTAs finish together (shorter tail before the next step)
     const uint64_t guide = uint64_t(gridDim.x) * 2 * kTmaChunk;
-    if (f.mctl) {
+    if (f.claim) {
         const uint32_t sz = nt > guide ? kTmaChunk : kTmaTail;
-        tb = atomicAdd(&f.mctl[2], sz);
+        tb = atomicAdd(f.claim, sz);
         te = min(nt, tb + sz);
     } else {
         const uint64_t per = (nt + gridDim.x - 1) / gridDim.x;
@@ -237,9 +214,9 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
     auto issue = [&](uint64_t k) -> bool {
         for (;;) {
             if (tn >= te) {
-                if (!f.mctl || tb >= nt) return false;
+                if (!f.claim || tb >= nt) return false;
                 const uint32_t sz = nt - te > guide ? kTmaChunk : kTmaTail;
-                tb = atomicAdd(&f.mctl[2], sz);
+                tb = atomicAdd(f.claim, sz);
                 if (tb >= nt) return false;
                 te = min(nt, tb + sz);
                 tn = tb;
@@ -258,7 +235,10 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
                           uint64_t(r - __ldg(&f.node_off[kk])) * row_bytes;
                 // a miss row goes on the misses kernel's list, once: by the
                 // CTA whose tile range (chunk) holds the row's first tile
-                if (!hit && f.mlist && rr * tpr >= tb) f.mlist[atomicAdd(&f.mctl[0], 1u)] = r;
+                if (!hit && f.mlist && rr * tpr >= tb) {
+                    const uint32_t at = atomicAdd(f.mctl, 1u);
+                    if (at < f.mcap) f.mlist[at] = r;  // past mcap the misses kernel scans every row
+                }
             }
             if (src_row) break;
             tn = (rr + 1) * tpr;  // a miss row: the misses kernel writes it
@@ -306,17 +286,18 @@ __global__ void __launch_bounds__(32) k_fetch_step_hits_tma(StepFetch f) {
 }
 
 // Misses of the step: with the TMA hit kernel's list (mlist) only the miss
-// rows are visited (a small fixed grid; the last block to finish resets the
-// list for the next step), else every row of the step is scanned.
+// rows are visited, else (no list, or more misses than it holds) every row of
+// the step is scanned.
 __global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
     asm volatile("griddepcontrol.launch_dependents;");
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the hit kernel's miss list
     const uint32_t r0 = __ldg(&f.node_off[f.k0]), r1 = __ldg(&f.node_off[f.k1]);
     const uint64_t pairs = f.vec_per_row;  // 16-byte pairs of payload words
-    const uint32_t nlist = f.mlist ? __ldcg(&f.mctl[0]) : 0u;
-    const uint32_t n = f.mlist ? nlist : r1 - r0;
+    const uint32_t nlist = f.mlist ? __ldcg(f.mctl) : 0u;
+    const bool listed = f.mlist && nlist <= f.mcap;
+    const uint32_t n = listed ? nlist : r1 - r0;
     for (uint32_t m = blockIdx.y; m < n; m += gridDim.y) {
-        const uint32_t r = f.mlist ? __ldcg(&f.mlist[m]) : r0 + m;
+        const uint32_t r = listed ? __ldcg(&f.mlist[m]) : r0 + m;
         const uint32_t sl = __ldg(&f.slots[r]);
         if (sl != kNever && (sl & kHit)) continue;
         const uint32_t k = node_of_row(f, r);
@@ -332,25 +313,11 @@ __global__ void __launch_bounds__(256) k_fetch_step_misses(StepFetch f) {
             if (buf) __stcs(&buf[p], v);
         }
     }
-    if (f.mlist) {  // every block has read the count: the last one resets the list
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            const uint32_t ticket = atomicAdd(&f.mctl[1], 1u);
-            if (ticket == gridDim.x * gridDim.y - 1) {
-                f.mctl[0] = 0;
-                f.mctl[1] = 0;
-                f.mctl[2] = 0;  // the hit kernel's chunk counter
-            }
-        }
-    }
 }
 
-// launch with programmatic stream serialization (PDL): back-to-back step
-// kernels overlap launch and ramp-up with the previous kernel's tail; the
-// kernels order their memory through griddepcontrol.wait (LSG_PDL=0: off)
-template <class K>
-cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const StepFetch& f, int which) {
+}  // namespace
+
+bool pdl_on(int which) {
     // LSG_PDL bit 0: hit kernels, bit 1: miss kernels. Default 1: a miss
     // kernel launched early beside a miss-heavy hit kernel measured slower
     // (E=4 cfg2 fetch 88.5 -> 96.9 ms), the hit kernels gain (1 rank 52.7 ->
@@ -359,7 +326,16 @@ cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t 
         const char* e = std::getenv("LSG_PDL");
         return e ? std::atoi(e) : 1;
     }();
-    const bool on = (mode >> which) & 1;
+    return (mode >> which) & 1;
+}
+
+namespace {
+
+// launch with programmatic stream serialization (PDL): back-to-back step
+// kernels overlap launch and ramp-up with the previous kernel's tail; the
+// kernels order their memory through griddepcontrol.wait (LSG_PDL=0: off)
+template <class K>
+cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, const StepFetch& f, int which) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -369,39 +345,15 @@ cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = on ? 1 : 0;
+    cfg.numAttrs = pdl_on(which) ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, f);
-}
-
-// per-device miss-row list of the step fetch (grown on demand; the counters
-// are zero between steps)
-struct MissList {
-    uint32_t* buf = nullptr;  // [4 control words + cap]
-    uint64_t cap = 0;
-};
-
-int miss_list(uint64_t rows, cudaStream_t st, uint32_t** list, uint32_t** ctl) {
-    static MissList ml[64];
-    int dev = 0;
-    LSG_CUDA(cudaGetDevice(&dev));
-    MissList& m = ml[dev & 63];
-    if (m.cap < rows) {
-        if (m.buf) {
-            LSG_CUDA(cudaDeviceSynchronize());
-            cudaFree(m.buf);
-        }
-        m.cap = std::max<uint64_t>(rows, 4096);
-        LSG_CUDA(cudaMalloc(&m.buf, (m.cap + 4) * 4));
-        LSG_CUDA(cudaMemsetAsync(m.buf, 0, 16, st));
-    }
-    *ctl = m.buf;
-    *list = m.buf + 4;
-    return kOk;
 }
 
 // TMA gather when rows are whole tiles (LSG_GATHER_LSU=1 keeps the 128-bit
 // load/store kernel, for comparison)
-int launch_hits(StepFetch f, uint64_t rows, uint64_t sample_bytes, cudaStream_t st, bool* tma = nullptr) {
+}  // namespace
+
+int launch_fetch_hits(StepFetch f, uint64_t rows, uint64_t sample_bytes, cudaStream_t st, bool* tma) {
     static const int l2hint = [] {
         const char* e = std::getenv("LSG_FETCH_L2HINT");
         return e && e[0] == '1' ? 1 : 0;  // measured: no gain beside the planner (default off)
@@ -435,8 +387,6 @@ int launch_hits(StepFetch f, uint64_t rows, uint64_t sample_bytes, cudaStream_t 
     return kOk;
 }
 
-}  // namespace
-
 int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* d_items,
                       const uint32_t* d_slots, const uint32_t* d_node_off, uint32_t k0, uint32_t k1,
                       uint64_t rows_hint, uint64_t sample_bytes, uint64_t seed, cudaStream_t st) {
@@ -454,24 +404,30 @@ int fetch_step_device(void* const* d_bufs, void* const* d_outs, const uint32_t* 
     f.vec_per_row = sample_bytes / 16;
     f.tiles_per_row = (f.vec_per_row + kTileVec - 1) / kTileVec;
     f.seed = seed;
-    f.mlist = nullptr;
-    f.mctl = nullptr;
     const uint64_t rows = rows_hint ? rows_hint : 1;
-    // with a row count the TMA kernel lists the step's miss rows
-    if (rows_hint && sample_bytes % kTmaTile == 0)
-        if (int rc = miss_list(rows_hint, st, &f.mlist, &f.mctl)) return rc;
+    // this call's own control words (stream-ordered pool): the claim counter
+    // and, with a row count, the TMA kernel's miss-row list; a list shorter
+    // than the step (a low rows_hint) only makes the misses kernel scan
+    Scratch sc(st);
+    const bool tma_rows = sample_bytes % kTmaTile == 0;
+    uint32_t* ctl = sc.get<uint32_t>(2 + (rows_hint && tma_rows ? rows_hint : 0));
+    if (!ctl) return set_error(kInternal, "fetch_step: scratch allocation failed");
+    LSG_CUDA(cudaMemsetAsync(ctl, 0, 8, st));
+    f.claim = ctl;
+    if (rows_hint && tma_rows) {
+        f.mctl = ctl + 1;
+        f.mlist = ctl + 2;
+        f.mcap = uint32_t(std::min<uint64_t>(rows_hint, 0xFFFFFFFFull));
+    }
     bool tma = false;
-    if (int rc = launch_hits(f, rows, sample_bytes, st, &tma)) return rc;
+    if (int rc = launch_fetch_hits(f, rows, sample_bytes, st, &tma)) return rc;
     if (!tma) f.mlist = f.mctl = nullptr;
     // each miss row is spread over up to 256 blocks (a 16 MiB row is 1 Mi
     // 16-byte pairs); listed miss rows over grid.y = 148, else every row
     dim3 g2(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 256)),
             unsigned(f.mlist ? std::min<uint64_t>(rows, 148) : std::min<uint64_t>(std::max<uint64_t>(rows, 1), 1024)));
     static const bool nomiss = std::getenv("LSG_DEBUG_NOMISS") != nullptr;  // timing experiments only
-    if (nomiss && f.mctl) {
-        LSG_CUDA(cudaMemsetAsync(f.mctl, 0, 16, st));
-        return kOk;
-    }
+    if (nomiss) return kOk;
     LSG_CUDA(launch_pdl(k_fetch_step_misses, g2, dim3(256), 0, st, f, 1));
     LSG_LAUNCH_CHECK("k_fetch_step_misses");
     return kOk;
@@ -493,10 +449,12 @@ int gather_step_hits_device(void* const* d_bufs, void* const* d_outs, const uint
     f.k1 = k1;
     f.vec_per_row = sample_bytes / 16;
     f.tiles_per_row = (f.vec_per_row + kTileVec - 1) / kTileVec;
-    f.mlist = nullptr;
-    f.mctl = nullptr;
     const uint64_t rows = rows_hint ? rows_hint : 1;
-    return launch_hits(f, rows, sample_bytes, st);
+    Scratch sc(st);
+    f.claim = sc.get<uint32_t>(1);
+    if (!f.claim) return set_error(kInternal, "fetch_step: scratch allocation failed");
+    LSG_CUDA(cudaMemsetAsync(f.claim, 0, 4, st));
+    return launch_fetch_hits(f, rows, sample_bytes, st, nullptr);
 }
 
 int batch_fetch_device(void* d_buf, const uint32_t* d_ids, const uint32_t* d_slots, uint64_t n,

@@ -26,6 +26,7 @@
 //     residents sit in an id bitmap scanned from the top (ties by larger id,
 //     buffer.cpp:27-28).
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -77,6 +78,17 @@ __global__ void __launch_bounds__(1024) k_step_bases(const uint32_t* __restrict_
         __syncthreads();
     }
     if (threadIdx.x == 0) gb[T] = carry;
+}
+
+// largest sample id of a plan's lists (hit bit stripped): the replay indexes
+// per-node tables by id, so ids >= dataset_size are rejected up front
+__global__ void __launch_bounds__(256) k_max_id(const uint32_t* __restrict__ items, uint64_t n,
+                                                uint32_t* __restrict__ out) {
+    uint32_t m = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        m = max(m, __ldg(&items[i]) & ~kHit);
+    m = __reduce_max_sync(0xFFFFFFFFu, m);
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
 struct ReplayArgs {
@@ -1118,6 +1130,22 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     }
     if (L == 0) L = 1;
     if (T * L >= 0xFFFFFFF0ull) return set_error(kCapability, "simulate: plan too large for 32-bit position keys");
+    if (total) {  // every id must index the per-node [D] tables
+        uint32_t* mx = sc.get<uint32_t>(1);
+        if (!mx) return set_error(kInternal, "simulate: scratch allocation failed");
+        LSG_CUDA(cudaMemsetAsync(mx, 0, 4, st));
+        k_max_id<<<grid_for(total, 256, 148u * 8), 256, 0, st>>>(d_items, total, mx);
+        LSG_LAUNCH_CHECK("k_max_id");
+        uint32_t hmax = 0;
+        if (int rc = d2h_small(&hmax, mx, 4, st)) return rc;
+        // the reference's buffers are hash sets, so simulate_plan accepts a
+        // plan (read_plan, plan.cpp:85-214) whose ids exceed its dataset_size:
+        // widen the id space to cover them, within the device tables' budget
+        if (uint64_t(hmax) >= D) D = uint64_t(hmax) + 1;
+        if (uint64_t(N) * D > (uint64_t(1) << 33))
+            return set_error(kCapability, "simulate: nodes x id space (" + std::to_string(N) + " x " +
+                                              std::to_string(D) + ") exceeds the replay's device tables");
+    }
     if (L > kRMaxList) return set_error(kCapability, "simulate: node list longer than 16384 samples");
     if (policy == 1) {  // LRU
         LruReplayArgs r{};

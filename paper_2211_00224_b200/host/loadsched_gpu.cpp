@@ -896,7 +896,7 @@ SimResult simulate_plan(const SchedulePlan& plan, std::uint64_t capacity, Policy
                 const auto& list = st.assignment.nodes[k];
                 off.push_back(o);
                 for (const Assigned& a : list) {
-                    if (a.id >= plan.dataset_size) throw ValidationError("simulate_plan: id out of range");
+                    if (a.id >= (1ull << 31)) throw CapabilityError("simulate_plan: sample ids must be < 2^31 on device");
                     items.push_back(std::uint32_t(a.id) | (a.source == Source::BufferHit ? LSG_HIT_BIT : 0u));
                     ++o;
                 }

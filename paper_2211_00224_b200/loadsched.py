@@ -29,7 +29,7 @@ __all__ = [
     "StorageError", "InternalError", "HIT_BIT", "NEVER", "brute_force_order", "remap_step", "slice_step",
     "remap_epoch", "balance_step", "Read", "ChunkPlan", "plan_chunks", "K_NEVER_USED", "Buffer", "make_buffer",
     "simulate_sequence", "optimal_miss_oracle", "CostModel", "policy_name", "total_barrier_cost",
-    "total_io_cost", "format_metrics", "write_metrics_file", "to_host",
+    "total_io_cost", "format_metrics", "write_metrics_file", "to_host", "HostRows", "FetchJob",
 ]
 
 
@@ -67,6 +67,24 @@ _BY_CODE = {_lib.CONFIG: ConfigError, _lib.VALIDATION: ValidationError,
 def _check(rc: int) -> None:
     if rc != 0:
         raise _BY_CODE.get(rc, Error)(rc, lib().lsg_last_error().decode())
+
+
+def _policy_code(policy: str) -> int:
+    """config.cpp:71-74: anything but the two names is a ConfigError."""
+    if policy == "clairvoyant":
+        return 0
+    if policy == "lru":
+        return 1
+    raise ConfigError(2, "policy must be clairvoyant or lru")
+
+
+def _mode_code(mode: str) -> int:
+    """config.cpp:75-78"""
+    if mode == "global":
+        return 0
+    if mode == "pernode":
+        return 1
+    raise ConfigError(2, "graph_mode must be global or pernode")
 
 
 # --------------------------------------------------------------- config --
@@ -130,9 +148,9 @@ class PipelineConfig:
         t = self.trace
         c.dataset_size, c.num_epochs, c.num_nodes = t.dataset_size, t.num_epochs, t.num_nodes
         c.local_batch, c.seed, c.drop_last = t.local_batch, t.seed, int(t.drop_last)
-        c.policy = 0 if self.policy == "clairvoyant" else 1
+        c.policy = _policy_code(self.policy)
         c.buffer_capacity = self.buffer_capacity
-        c.graph_mode = 0 if self.graph_mode == "global" else 1
+        c.graph_mode = _mode_code(self.graph_mode)
         c.insert_redundant = int(self.chunk_insert_redundant)
         c.chunk_threshold = self.chunk_threshold
         c.optim_order, c.optim_remap = int(self.optim_order), int(self.optim_remap)
@@ -232,6 +250,7 @@ class SimResult:
     total_hits: int
     total_misses: int
     slots: torch.Tensor | None = None
+    policy: str = "clairvoyant"  # the replay's policy (metrics.csv labels its rows with it)
 
 
 def _stream() -> ctypes.c_void_p:
@@ -279,7 +298,7 @@ def build_reuse_graph(trace: AccessTrace, buffer_size: int, mode: str = "global"
     cfg = trace.config
     _check(lib().lsg_build_reuse_graph(_ptr(ep), E, L, cfg.dataset_size, cfg.num_nodes,
                                        cfg.local_batch, int(cfg.drop_last), buffer_size,
-                                       0 if mode == "global" else 1, _ptr(w), _stream()))
+                                       _mode_code(mode), _ptr(w), _stream()))
     return ReuseGraph(E, buffer_size, mode, w[:E, :E])
 
 
@@ -293,7 +312,7 @@ def build_reuse_graph_rows(trace: AccessTrace, buffer_size: int, mode: str, row_
     rows = torch.empty((max(row_end - row_begin, 0), E), dtype=torch.int64, device=ep.device)
     cfg = trace.config
     _check(lib().lsg_build_reuse_graph_rows(_ptr(ep), E, L, cfg.dataset_size, cfg.num_nodes, cfg.local_batch,
-                                            int(cfg.drop_last), buffer_size, 0 if mode == "global" else 1,
+                                            int(cfg.drop_last), buffer_size, _mode_code(mode),
                                             row_begin, row_end, _ptr(rows) if rows.numel() else None,
                                             _stream()))
     return rows
@@ -438,7 +457,7 @@ class Buffer:
             raise ValidationError(_lib.VALIDATION, "buffer capacity must be >= 1")
         self.policy, self._cap = policy, capacity
         h = ctypes.c_void_p()
-        _check(lib().lsg_buffer_create(0 if policy == "clairvoyant" else 1, capacity, ctypes.byref(h)))
+        _check(lib().lsg_buffer_create(_policy_code(policy), capacity, ctypes.byref(h)))
         self._h = h
 
     def __del__(self):
@@ -489,7 +508,7 @@ def simulate_sequence(seq, capacity: int, policy: str = "clairvoyant") -> int:
     """buffer.hpp:83-84 / buffer.cpp:116-125 — one node through the K7 replay."""
     ids = _host_u32(seq, "simulate_sequence")
     m = ctypes.c_uint64(0)
-    _check(lib().lsg_simulate_sequence(_np_ptr(ids), ids.size, capacity, 0 if policy == "clairvoyant" else 1,
+    _check(lib().lsg_simulate_sequence(_np_ptr(ids), ids.size, capacity, _policy_code(policy),
                                        ctypes.byref(m), None))
     return m.value
 
@@ -598,7 +617,7 @@ def simulate_plan(plan: SchedulePlan, capacity: int, policy: str = "clairvoyant"
     hits = torch.zeros((T, N), dtype=torch.int32, device=dev)
     misses = torch.zeros((T, N), dtype=torch.int32, device=dev)
     slots = torch.empty(max(plan.items.numel(), 1), dtype=torch.int32, device=dev) if want_slots else None
-    pol = 0 if policy == "clairvoyant" else 1
+    pol = _policy_code(policy)
     if insert_redundant:
         if plan.read_start is None:
             raise ValidationError(3, "simulate_plan: insert_redundant needs the plan's reads")
@@ -611,7 +630,8 @@ def simulate_plan(plan: SchedulePlan, capacity: int, policy: str = "clairvoyant"
                                   plan.dataset_size, capacity, pol, k0, k1, _ptr(hits), _ptr(misses),
                                   _ptr(slots), _stream()))
     tot = to_host(torch.stack([hits.sum(dtype=torch.int64), misses.sum(dtype=torch.int64)]))
-    return SimResult(hits, misses, int(tot[0]), int(tot[1]), slots[: plan.items.numel()] if slots is not None else None)
+    return SimResult(hits, misses, int(tot[0]), int(tot[1]), slots[: plan.items.numel()] if slots is not None else None,
+                     policy_name(policy))
 
 
 def store_fill(ids: torch.Tensor, sample_bytes: int, fill_seed: int,
@@ -758,7 +778,7 @@ class CostModel:
 
 def policy_name(policy: str) -> str:
     """config.cpp:157-159"""
-    return "clairvoyant" if policy == "clairvoyant" else "lru"
+    return ("clairvoyant", "lru")[_policy_code(policy)]
 
 
 def total_barrier_cost(plan: SchedulePlan, model: CostModel = CostModel()) -> float:
@@ -796,7 +816,7 @@ def total_io_cost(plan: SchedulePlan, model: CostModel = CostModel()) -> float:
     return total
 
 
-def format_metrics(plan: SchedulePlan, sim: "SimResult", policy: str = "clairvoyant",
+def format_metrics(plan: SchedulePlan, sim: "SimResult", policy: str | None = None,
                    model: CostModel = CostModel()) -> bytes:
     """write_metrics (pipeline.cpp:153-179): one row per (epoch, step, node) in
     execution order with the replay's hits/misses, the per-node fetch counts
@@ -811,7 +831,7 @@ def format_metrics(plan: SchedulePlan, sim: "SimResult", policy: str = "clairvoy
     m = sim.misses.cpu().numpy().view(np.uint32)
     bb = ["%.6f" % (float(v) * per_fetch) for v in fb.max(axis=1).tolist()] if N else []
     ba = ["%.6f" % (float(v) * per_fetch) for v in fa.max(axis=1).tolist()] if N else []
-    pol = policy_name(policy)
+    pol = policy_name(policy if policy is not None else sim.policy)
     fbl, fal, hl, ml = fb.tolist(), fa.tolist(), h.tolist(), m.tolist()
     out = ["epoch,step,node,hits,misses,policy,fetches_before,fetches_after,barrier_before,barrier_after\n"]
     for g in range(T):
@@ -821,7 +841,7 @@ def format_metrics(plan: SchedulePlan, sim: "SimResult", policy: str = "clairvoy
     return "".join(out).encode()
 
 
-def write_metrics_file(path, plan: SchedulePlan, sim: "SimResult", policy: str = "clairvoyant",
+def write_metrics_file(path, plan: SchedulePlan, sim: "SimResult", policy: str | None = None,
                        model: CostModel = CostModel()) -> None:
     _write(path, format_metrics(plan, sim, policy, model))
 
@@ -1013,3 +1033,95 @@ class StepFetcher:
                                      _ptr(plan.node_off), ctypes.c_void_p(off.ctypes.data), step_begin, step_end,
                                      off.shape[1] - 1, self.k0, self.k1, self.sample_bytes, self.fill_seed,
                                      _stream()))
+
+
+class HostRows:
+    """The host tier of the miss path (lsg_host_rows): the Store payload rows
+    of a dataset (store.cpp:70-80, row i at i * sample_bytes) in a tmpfs file,
+    mapped and pinned so the GPU reads them over PCIe; every process of a box
+    maps the same file. create=True writes it."""
+
+    def __init__(self, path: str, count: int, sample_bytes: int, fill_seed: int = 1, create: bool = True):
+        h = ctypes.c_void_p()
+        _check(lib().lsg_host_rows_open(str(path).encode(), count, sample_bytes, fill_seed, int(create),
+                                        ctypes.byref(h)))
+        self._h, self.path, self.count, self.sample_bytes = h, str(path), count, sample_bytes
+
+    def view(self) -> np.ndarray:
+        """The rows as a [count, sample_bytes] uint8 host array (no copy)."""
+        base = ctypes.c_void_p()
+        _check(lib().lsg_host_rows_info(self._h, None, None, ctypes.byref(base)))
+        buf = (ctypes.c_uint8 * (self.count * self.sample_bytes)).from_address(base.value)
+        return np.frombuffer(buf, dtype=np.uint8).reshape(self.count, self.sample_bytes)
+
+    def close(self) -> None:
+        if self._h:
+            lib().lsg_host_rows_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter teardown
+            pass
+
+
+class FetchJob:
+    """The loading phase of a whole job (lsg_fetch_job): every step's batch
+    for ranks node_range, hits from the HBM buffers, misses from `host` (a
+    HostRows; None = the Store payload synthesised on device) into their
+    batch row and new slot. The constructor builds the miss list and starts
+    the miss prefetcher on `prep_stream` (which then stays busy until the
+    job's misses are consumed); run() enqueues the steps on the current
+    stream; stats() = {misses, kept, host_bytes, hits} (synchronous)."""
+
+    def __init__(self, bufs: list, outs: list, node_range: tuple[int, int], plan: "SchedulePlan",
+                 slots: torch.Tensor, host_node_off: np.ndarray, sample_bytes: int, fill_seed: int = 1,
+                 host: HostRows | None = None, step_range: tuple[int, int] | None = None,
+                 prep_stream: torch.cuda.Stream | None = None, ring_bytes: int = 0):
+        dev = bufs[0].device
+        k0, k1 = node_range
+        self._keep = [bufs, outs, plan, slots]
+        self.pb = torch.tensor([t.data_ptr() for t in bufs], dtype=torch.int64, device=dev)
+        self.po = torch.tensor([t.data_ptr() for t in outs], dtype=torch.int64, device=dev)
+        self.off = np.ascontiguousarray(host_node_off, dtype=np.uint32)
+        T = self.off.shape[0]
+        g0, g1 = step_range if step_range is not None else (0, T)
+        d = _lib.LsgFetchJobDesc()
+        d.d_bufs, d.d_outs = self.pb.data_ptr(), self.po.data_ptr()
+        d.d_items, d.d_slots, d.d_node_off = plan.items.data_ptr(), slots.data_ptr(), plan.node_off.data_ptr()
+        d.h_node_off = self.off.ctypes.data
+        d.step_begin, d.step_end, d.N = g0, g1, self.off.shape[1] - 1
+        d.node_begin, d.node_end = k0, k1
+        d.sample_bytes, d.fill_seed = sample_bytes, fill_seed
+        d.host = host._h if host is not None else None
+        d.ring_bytes = ring_bytes
+        self.host = host
+        if prep_stream is None:  # with a host tier the prefetcher holds its stream: never the fetch's
+            prep_stream = torch.cuda.Stream(device=dev) if host is not None else torch.cuda.current_stream()
+        st = prep_stream
+        if host is not None:
+            st.wait_stream(torch.cuda.current_stream())  # the plan and the replay's slots
+        self._prep = st
+        h = ctypes.c_void_p()
+        _check(lib().lsg_fetch_job_create(ctypes.byref(d), ctypes.byref(h), ctypes.c_void_p(st.cuda_stream)))
+        self._h = h
+
+    def run(self) -> None:
+        _check(lib().lsg_fetch_job_run(self._h, _stream()))
+
+    def stats(self) -> dict:
+        a = (ctypes.c_uint64 * 4)()
+        _check(lib().lsg_fetch_job_stats(self._h, a, _stream()))
+        return {"misses": a[0], "kept": a[1], "host_bytes": a[2], "hits": a[3]}
+
+    def close(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Free the job's device state, stream-ordered after its work on
+        `stream` (default: the current stream, where run() enqueued it)."""
+        if self._h:
+            st = stream if stream is not None else torch.cuda.current_stream()
+            lib().lsg_fetch_job_destroy(self._h, ctypes.c_void_p(st.cuda_stream))
+            for t in (self.pb, self.po):
+                t.record_stream(st)
+            self._h = None
+

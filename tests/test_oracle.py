@@ -241,3 +241,18 @@ def test_oracle_matches_reference_many_nodes(seed):
     h, m = O.simulate(p.items, p.node_off, N, D, cfg.buffer_capacity)
     assert np.array_equal(p.residency, q.residency)
     assert np.array_equal(h, q.hits) and np.array_equal(m, q.misses)
+
+
+def test_full_shape_goldens_hold_survey_anchors():
+    """tests/golden/full_shapes.json (the reference's outputs at the full
+    BASELINE shapes, tools/make_goldens.py) holds the figures SURVEY.md §6
+    recorded from the compiled reference during the survey."""
+    import json
+    import os
+    GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "full_shapes.json")))
+    assert (GOLD["cfg2_global"]["total_hits"], GOLD["cfg2_global"]["total_misses"]) == (25870743, 343657)
+    assert GOLD["cfg2_pernode"]["iterations"] == 444 and GOLD["cfg2_pernode"]["cost"] == 22682160
+    assert GOLD["cfg4"]["cost"] == 15637500 and GOLD["cfg4"]["iterations"] == 500
+    assert GOLD["cfg4"]["graph_sum"] == pytest.approx(7.85e9, rel=5e-3)
+    assert GOLD["cfg1"]["iterations"] == 121 and GOLD["cfg1"]["cost"] == 34977
+    assert (GOLD["cfg1"]["total_misses"], GOLD["cfg1"]["total_hits"]) == (104872, 58968)
