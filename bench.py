@@ -251,6 +251,27 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ ours --
+def host_tier_path(c: dict) -> str:
+    d = "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp"
+    return os.path.join(d, f"lsg_rows_D{c['D']}_SB{c['sample_bytes']}_s{c['fill_seed']}")
+
+
+def host_tier_fits(c: dict) -> tuple[bool, str]:
+    """The host tier holds the whole dataset's payload rows: it must fit the
+    tmpfs and leave most of the host RAM free."""
+    need = c["D"] * c["sample_bytes"]
+    try:
+        avail = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
+    except Exception:  # pragma: no cover
+        avail = 0
+    shm = os.statvfs(os.path.dirname(host_tier_path(c)))
+    free = shm.f_bavail * shm.f_frsize
+    if need > 0.6 * avail or need > 0.9 * free:
+        return False, (f"dataset {need / 2**30:.0f} GiB exceeds the host tier budget "
+                       f"({avail / 2**30:.0f} GiB RAM available, {free / 2**30:.0f} GiB tmpfs)")
+    return True, ""
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -259,6 +280,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--epochs", type=int, default=None, help="override E (debug only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-verify", action="store_true", help="skip the one-shot byte check of the fetch")
     ap.add_argument("--plan-shard", default="auto", choices=["auto", "rr", "replicate"],
                     help="N>1: plan each job on one GPU (rr) or on all (replicate); auto = rr above 2 GPUs")
     ap.add_argument("--prio", type=int, default=1, help="plan and replay streams at high priority")
@@ -267,6 +289,9 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if os.environ.get("LSG_BENCH_WATCHDOG"):  # debugging: every thread's stack, then exit
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["LSG_BENCH_WATCHDOG"]), exit=True)
 
     import torch
     import torch.distributed as dist
@@ -278,26 +303,25 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    c = dict(CFG2 if args.config == "cfg2" else CFG3)
-    if args.epochs:
-        c["E"] = args.epochs
+    c = config_for(args)
+    if c["kind"] == "plan":
+        return run_plan_kind(args, c, ls, torch, dist, rank, world, dev)
     D, E, N, b, C, SB = c["D"], c["E"], c["N"], c["b"], c["C"], c["sample_bytes"]
     from paper_2211_00224_b200.parallel import combine_rows, rank_range
 
     k0, k1 = rank_range(N, world, rank)
-    # ranks whose HBM buffers fit on this GPU (cfg3: one 128 GiB buffer per GPU)
-    k1 = min(k1, k0 + max(1, HBM_BUDGET // (C * SB)))
+    # ranks whose HBM buffers fit on this GPU at once; more ranks per GPU run
+    # one group after another through the same buffers (cfg3: 128 GiB/rank)
+    per = max(1, min(k1 - k0, HBM_BUDGET // (C * SB)))
+    groups = [(g, min(g + per, k1)) for g in range(k0, k1, per)]
     pc = ls.PipelineConfig(trace=ls.TraceConfig(D, E, N, b, c["seed"], True), buffer_capacity=C)
     sh = pc.shape()
-    T, A = int(sh.total_steps), E * D
+    T, A = int(sh.total_steps), int(sh.total_items)
 
-    # per-rank HBM sample buffers (C slots x 256 KiB) and batch tensors
-    bufs = {k: torch.empty((C, SB), dtype=torch.uint8, device=dev) for k in range(k0, k1)}
-    maxlen = min(c["N"] * b, 1024)  # node lists stay near b (checked below)
-    outs = {k: torch.empty((maxlen, SB), dtype=torch.uint8, device=dev) for k in range(k0, k1)}
-
-    fetcher = ls.StepFetcher([bufs[k] for k in range(k0, k1)], [outs[k] for k in range(k0, k1)],
-                             (k0, k1), SB, c["fill_seed"])
+    # per-rank HBM sample buffers (C slots x sample_bytes) and batch tensors
+    bufs = [torch.empty((C, SB), dtype=torch.uint8, device=dev) for _ in range(per)]
+    maxlen = min(N * b, max(1024, 2 * b))  # node lists stay near b (checked below)
+    outs = [torch.empty((maxlen, SB), dtype=torch.uint8, device=dev) for _ in range(per)]
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     # the latency-bound stages (the planner's persistent CTA, the per-rank
     # replay CTAs, NCCL) on high-priority streams, the fetch on a low-priority
@@ -322,15 +346,48 @@ def main():
     # of 2 left a 0.3 s fetch bubble (N=4: 31-33 -> 34.5-34.7 M samples/s)
     ahead = int(os.environ.get("LSG_BENCH_AHEAD", "3" if world > 2 else "2"))
     rr_shift = int(os.environ.get("LSG_BENCH_RR_SHIFT", "0"))  # debug: job i planned on GPU (i + shift) mod N
+    # one miss-list / prefetch stream per job in flight: a job's prefetcher
+    # holds its stream until the job's misses are consumed
+    prep = [torch.cuda.Stream(priority=-1 if args.prio else 0) for _ in range(ahead + 2)]
+    ring_bytes = int(float(os.environ.get("LSG_BENCH_RING_GB", "12")) * 2 ** 30)
 
+    # the host tier (e2e miss source): the dataset's Store payload rows in a
+    # tmpfs file, pinned; local rank 0 writes it, every process maps it
+    hostrows, host_note = None, ""
+    if not args.no_e2e and args.steps:
+        ok, host_note = host_tier_fits(c)
+        if ok:
+            path = host_tier_path(c)
+            lr = int(os.environ.get("LOCAL_RANK", 0))
+            t0 = time.perf_counter()
+            if lr == 0:
+                hostrows = ls.HostRows(path, D, SB, c["fill_seed"], create=True)
+            if world > 1:
+                dist.barrier()
+            if lr != 0:
+                hostrows = ls.HostRows(path, D, SB, c["fill_seed"], create=False)
+            host_note = (f"host tier: {D} x {SB} B Store payload rows ({D * SB / 2**30:.0f} GiB) in {path}, "
+                         f"pinned + mapped; set up in {time.perf_counter() - t0:.1f} s (outside timing)")
 
-    def run_jobs(n, host=False, pipeline=True, stats=None, t_start=None):
+    def make_jobs(plan, slots, off, host, i):
+        """The fetch of job i for every rank group of this GPU (FetchJob:
+        miss list, and with the host tier the miss prefetcher, started on a
+        prep stream that waits only for this job's replay)."""
+        st = prep[i % len(prep)]
+        st.wait_stream(torch.cuda.current_stream())
+        return [ls.FetchJob(bufs[: g1 - g0], outs[: g1 - g0], (g0, g1), plan, slots, off, SB, c["fill_seed"],
+                            host=hostrows if host else None, prep_stream=st, ring_bytes=ring_bytes)
+                for g0, g1 in groups]
+
+    def run_jobs(n, host=False, pipeline=True, stats=None, t_start=None, keep_jobs=False):
         """n passes of the hot path. Job i = plan (K1-K6) -> replay (K7, this
-        GPU's ranks, all-gather of the rows) -> fetch (K8/K9, every step of
-        this GPU's ranks), as three pipelined stages on three streams:
+        GPU's ranks, all-gather of the rows) -> fetch (K8 hits from HBM, misses
+        from storage, every step of this GPU's ranks), as three pipelined stages on
+        three streams:
           planner thread   plans (the step loop is ONE persistent CTA);
-          replayer thread  node-list broadcast (N>1, rr placement), replay
-                           and the row all-gather (all NCCL calls);
+          replayer thread  node-list broadcast (N>1, rr placement), replay,
+                           the row all-gather (all NCCL calls) and the
+                           fetch job's miss list / miss prefetcher;
           this thread      the batch fetch of every step.
         With `pipeline` job i+1's plan and replay overlap job i's fetch on the
         remaining SMs; every job's work is complete when the call returns.
@@ -339,7 +396,8 @@ def main():
         the plan stream shards across GPUs although one plan's step
         recurrence does not. host=True is the e2e path: the plan lands in
         pinned host memory (lsg_plan_host) and is uploaded by its GPU, the
-        hit/miss rows are read back to the host."""
+        hit/miss rows are read back to the host, and misses are read from the
+        host tier over PCIe."""
         import queue
         qp, qr = queue.Queue(maxsize=1), queue.Queue(maxsize=1)
         free = threading.Semaphore(2)
@@ -415,6 +473,8 @@ def main():
                         if host:  # d2h of the step results
                             rows.append((ls.to_host(sim.hits), ls.to_host(sim.misses)))
                         off = ls.to_host(noff).numpy()
+                        if int((off[:, k0 + 1:k1 + 1] - off[:, k0:k1]).max()) > maxlen:
+                            raise SystemExit("a node list exceeds the batch tensor rows")
                         if os.environ.get("LSG_BENCH_TIMELINE"):
                             print(f"[replayer] rank {rank} n={n} job {i} t0={1e3 * (h0 - tj0):.1f}: simulate_plan {1e3 * (h1 - h0):.1f} ms host, "
                                   f"rows+off {1e3 * (time.perf_counter() - h1):.1f} ms", file=sys.stderr, flush=True)
@@ -422,6 +482,7 @@ def main():
                             free.release()  # this job's host staging set has been uploaded
                         f1 = ev()
                         f1.record(rstream)
+                        jobs = make_jobs(plan, sim.slots, off, host, i)
                         if os.environ.get("LSG_BENCH_TIMELINE") and t_start is not None:
                             f1.synchronize()
                             print(f"[replay-gpu] rank {rank} job {i}: start {t_start.elapsed_time(f0):.1f} "
@@ -429,7 +490,7 @@ def main():
                                   file=sys.stderr, flush=True)
                         for t in (items, noff, sim.slots):
                             t.record_stream(fstream)
-                        qr.put((plan, sim, off, pa, pz, f0, f1))
+                        qr.put((plan, sim, off, pa, pz, f0, f1, jobs))
             except BaseException as e:
                 err.append(e)
                 qr.put(None)
@@ -441,17 +502,19 @@ def main():
             got = qr.get()
             if got is None:
                 raise err[0]
-            plan, sim, off, pa, pz, f0, f1 = got
-            if int((off[:, k0 + 1:k1 + 1] - off[:, k0:k1]).max()) > maxlen:
-                raise SystemExit("a node list exceeds the batch tensor rows")
+            plan, sim, off, pa, pz, f0, f1, jobs = got
             fstream.wait_event(f1)
             f1b = ev()
             f1b.record(fstream)
-            fetcher.fetch_steps(plan, sim.slots, off)
+            for job in jobs:  # rank groups one after another (shared buffers)
+                job.run()
             f2 = ev()
             f2.record(fstream)
             if stats is not None:
-                stats.append((pa, pz, f0, f1, f2, sim, off, f1b))
+                stats.append((pa, pz, f0, f1, f2, sim, off, f1b, jobs if keep_jobs else None, plan))
+            if not keep_jobs:
+                for job in jobs:  # stream-ordered free after the job's kernels (rings, lists)
+                    job.close(fstream)
             if not pipeline:
                 f2.synchronize()
             fetched.release()
@@ -476,21 +539,20 @@ def main():
         run_jobs(nwarm)
     torch.cuda.synchronize()
 
-    # hit/miss totals of the local ranks (for algorithmic bytes)
+    # hit/miss totals of the local ranks (for algorithmic bytes), from the
+    # fetch jobs' own counts
     st0 = []
-    run_jobs(1, stats=st0)
+    run_jobs(1, stats=st0, keep_jobs=True)
     torch.cuda.synchronize()
-    sim0, off0 = st0[0][5], st0[0][6]
-    local_hits = int(sim0.hits[:, k0:k1].sum())
-    local_misses = int(sim0.misses[:, k0:k1].sum())
-    slots_np = sim0.slots.cpu().numpy().view("uint32")
-    # kept misses (written to their slot too) of the local ranks
-    bases = np.concatenate([[0], np.cumsum(off0[:, N].astype(np.int64))])
-    kept_local = 0
-    for g in range(T):
-        s = slots_np[bases[g] + int(off0[g, k0]): bases[g] + int(off0[g, k1])]
-        kept_local += int(((s != 0xFFFFFFFE) & ((s >> 31) == 0)).sum())
-    del st0, sim0
+    fst = [j.stats() for j in st0[0][8]]
+    for j in st0[0][8]:
+        j.close(fstream)
+    local_hits = sum(s["hits"] for s in fst)
+    local_misses = sum(s["misses"] for s in fst)
+    kept_local = sum(s["kept"] for s in fst)
+    assert local_hits == int(st0[0][5].hits[:, k0:k1].sum()) and local_misses == int(st0[0][5].misses[:, k0:k1].sum())
+    keep_plan = st0[0]  # plan, replay and offsets of one job, for the byte check below
+    del st0
 
     if world > 1:
         dist.barrier()
@@ -511,9 +573,8 @@ def main():
     launches = ls.lib().lsg_launch_count() - launches0
     total_ms = t_start.elapsed_time(t_end)
     # per-job stage windows on rank 0 (ms from t_start), read after the timed region
-    if True:
-        timeline = [[round(t_start.elapsed_time(x), 1) if x is not None else None for x in (e[0], e[1], e[2], e[3], e[7], e[4])]
-                    for e in evs]
+    timeline = [[round(t_start.elapsed_time(x), 1) if x is not None else None for x in (e[0], e[1], e[2], e[3], e[7], e[4])]
+                for e in evs]
     own = [e[0].elapsed_time(e[1]) for e in evs if e[0] is not None]
     plan_ms = statistics.mean(own) if own else 0.0
     replay_ms = statistics.mean(e[2].elapsed_time(e[3]) for e in evs)
@@ -541,10 +602,11 @@ def main():
         total_ms, plan_ms, replay_ms, fetch_ms, job_ms, plan_alone_ms = [float(x) for x in tt]
     ms_per_step = total_ms / max(args.steps, 1)
 
-    # fetch-phase algorithmic bytes: hits read a slot and write the batch row;
-    # misses write the batch row (+ the slot when kept)
-    alg_bytes = 2 * SB * local_hits + SB * local_misses + SB * kept_local
-    achieved = alg_bytes / (fetch_ms * 1e-3) / 1e9
+    # HBM-gather algorithmic bytes: hits read a slot and write the batch row
+    # (SURVEY §8d); misses come from storage and are reported apart
+    hit_bytes = 2 * SB * local_hits
+    miss_bytes = SB * local_misses + SB * kept_local  # batch row + kept slot writes
+    achieved = hit_bytes / (fetch_ms * 1e-3) / 1e9
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -559,9 +621,10 @@ def main():
     except Exception:
         pass
 
-    # e2e through the public API with host buffers (lsg_plan_host: the plan
-    # lands in pinned host memory, is uploaded for the replay, hit/miss rows
-    # are read back), the same pipelined job stream, K jobs
+    # e2e through the public API with host buffers: the plan lands in pinned
+    # host memory (lsg_plan_host) and is uploaded for the replay, hit/miss rows
+    # are read back, and every miss is read from the host tier over PCIe (the
+    # TMA miss prefetcher); the same pipelined job stream, K jobs
     e2e = None
     if not args.no_e2e and args.steps:
         run_jobs(2, host=True)  # untimed warm-up of the host path
@@ -570,24 +633,45 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         a0, a1 = ev(), ev()
+        est = []
         a0.record(fstream)
-        run_jobs(args.steps, host=True, t_start=a0)
+        run_jobs(args.steps, host=True, t_start=a0, stats=est)
         a1.record(fstream)
         torch.cuda.synchronize()
         e2e_ms = a0.elapsed_time(a1) / args.steps
+        e2e_fetch_ms = statistics.mean(e[7].elapsed_time(e[4]) for e in est)
+        host_bytes = local_misses * SB if hostrows is not None else 0  # every miss read once from the host tier
+        del est
         if world > 1:
-            tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            tt = torch.tensor([e2e_ms, e2e_fetch_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_ms = float(tt[0])
+            e2e_ms, e2e_fetch_ms = float(tt[0]), float(tt[1])
+            hb = torch.tensor([host_bytes], device=dev, dtype=torch.int64)
+            dist.all_reduce(hb)
+            host_bytes = int(hb[0])
         d2h = A * 4 * 2 + T * (N + 1) * 4 + 2 * T * N * 4 * 2 + E * E * 8 + E * 4 + 8 + 4 \
             + pc.pso.max_iters * 8 + T * N * 4 * 2 + T * (N + 1) * 4
-        e2e = {"value": A / (e2e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": T * (N + 1) * 4 + A * 4,
+        e2e = {"value": A / (e2e_ms * 1e-3), "unit": "samples/s",
+               "h2d_bytes_per_step": T * (N + 1) * 4 + A * 4 + host_bytes,
                "d2h_bytes_per_step": d2h,
+               "miss_source": ("host tier over PCIe (TMA prefetcher)" if hostrows is not None else
+                               "Store payload synthesised on device: " + host_note),
+               "pcie": ({"miss_bytes_per_job": host_bytes,
+                         "achieved_gbs": host_bytes / (e2e_fetch_ms * 1e-3) / 1e9 / max(world, 1),
+                         "fetch_ms": e2e_fetch_ms,
+                         "note": "per GPU: host-tier bytes / fetch-phase time (the PCIe reads overlap the HBM "
+                                 "gather; epoch 0 is all misses)"} if hostrows is not None else None),
                "note": "per job: lsg_plan_host (trace, graph, order, plan lists, fetch counts to pinned host), "
-                       "plan re-uploaded for the replay, hit/miss rows read back, batch fetch on device; "
-                       "jobs pipelined as in value"}
+                       "plan re-uploaded for the replay, hit/miss rows read back, batch fetch with every miss "
+                       "read from storage; jobs pipelined as in value" + ("; " + host_note if host_note else "")}
 
-    cpu = cpu_baseline() if (rank == 0 and world == 1) else None
+    # one-shot byte check of the benched fetch (off the timed region): the
+    # job's batches at evenly spaced steps equal Store::read_one of their ids
+    verify = None
+    if not args.no_verify and args.steps:
+        verify = verify_fetch(ls, torch, keep_plan, groups, bufs, outs, SB, c["fill_seed"], hostrows, T)
+    del keep_plan
+    cpu = cpu_baseline(c, args.config) if (rank == 0 and world == 1) else None
 
     if rank == 0:
         line = {
@@ -595,17 +679,16 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (splitmix64 traces and Store payload, seed 42 / fill_seed 1)",
-            "config": {"workload": f"cfg2: D={D} E={E} N={N} b={b} C={C} (20%/rank), 256 KiB samples, "
-                                   f"plan+replay+fetch of the whole job",
-                       "global_batch": N * b, "ranks_per_gpu": k1 - k0,
+            "config": {"workload": workload(args.config, c),
+                       "global_batch": N * b, "ranks_per_gpu": k1 - k0, "rank_groups": len(groups),
                        "parallelism": (f"jobs' plans round-robin over {world} GPUs (node lists broadcast, NCCL); "
                                        if world > 1 and plan_shard else
                                        "plan replicated per GPU; " if world > 1 else "")
                                       + f"replay+fetch sharded {k1 - k0} ranks/GPU",
-                       "l2": "inputs > L2 (12.8 GiB HBM sample buffer per rank)"},
+                       "l2": f"inputs > L2 ({C * SB / 2**30:.1f} GiB HBM sample buffer per rank)"},
             "pipeline": "plan / replay / fetch on three streams: later jobs' plans (1 persistent CTA) and replays "
-                        "overlap job i's fetch; "
-                        "every job's full work is inside the timed region",
+                        "overlap job i's fetch; every job's full work is inside the timed region; "
+                        "value: misses written from the Store payload synthesised on device",
             "plan_ms": plan_ms, "replay_ms": replay_ms, "fetch_ms": fetch_ms,
             "single_job_ms": job_ms, "single_job_samples_per_s": A / (job_ms * 1e-3) if job_ms else None,
             "plan_alone_ms": plan_alone_ms,
@@ -613,13 +696,16 @@ def main():
             "plan_samples_per_s_note": "one plan (shuffle+order+evict+assign of the whole job) alone; plan_ms is "
                                        "the mean plan time inside the pipeline, beside other jobs' fetch",
             "gather": {"value": achieved, "unit": "GB/s", "hits": local_hits, "misses": local_misses,
-                       "bytes_per_step": alg_bytes},
+                       "kept_misses": kept_local, "hit_bytes_per_job": hit_bytes,
+                       "miss_bytes_per_job": miss_bytes,
+                       "note": "HBM gather = 2 x sample_bytes per hit over the fetch phase (the misses' time "
+                               "included, their bytes not: SURVEY §8d)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_note": "dram read+write bytes per k_fetch_step_hits_tma launch (one steady-state "
-                                         "step, all local ranks) from profiles/r01f_summary.txt; "
+                                         "step, all local ranks) from profiles/; "
                                          f"{traffic_ratio:.3f} x that launch's algorithmic bytes" if traffic else None,
-                         "kernel": "fetch phase (k_fetch_step_hits_tma TMA bulk-copy gather + k_fetch_step_misses, "
+                         "kernel": "fetch phase (k_fetch_step_hits_tma TMA bulk-copy gather + k_job_misses, "
                                    "one pair per training step)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6650"},
             "gpu_launches": int(launches),
@@ -628,6 +714,147 @@ def main():
         }
         if e2e:
             line["e2e"] = e2e
+        if verify:
+            line["verify"] = verify
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+    if hostrows is not None:
+        hostrows.close()
+        if world > 1:
+            dist.barrier()
+        if int(os.environ.get("LOCAL_RANK", 0)) == 0:
+            try:
+                os.remove(host_tier_path(c))
+            except OSError:
+                pass
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def verify_fetch(ls, torch, kept, groups, bufs, outs, SB, fill_seed, hostrows, T, npts=24):
+    """Byte check of the fetch at the bench shape: one planned+replayed job
+    fetched in segments (the same FetchJob path as the timed region), and
+    after each segment every batch row of its last step compared with the
+    Store payload of its id (store.cpp:134-139, via K9 store_fill). Runs the
+    device-synthesised miss path and, with a host tier, the PCIe miss path."""
+    sim, off, plan = kept[5], kept[6], kept[9]
+    pts = sorted({max(0, int(T * (i + 1) / npts) - 1) for i in range(npts)})
+    items = plan.items
+    N = off.shape[1] - 1
+    bases = np.concatenate([[0], np.cumsum(off[:, N].astype(np.int64))])
+    out = {"steps_checked": 0, "rows_checked": 0, "mismatched_rows": 0, "paths": []}
+    for path, host in (("misses synthesised on device", None), ("misses from the host tier", hostrows)):
+        if path.endswith("tier") and host is None:
+            continue
+        out["paths"].append(path)
+        for g0, g1 in groups:
+            prev = 0
+            for g in pts:
+                j = ls.FetchJob(bufs[: g1 - g0], outs[: g1 - g0], (g0, g1), plan, sim.slots, off, SB, fill_seed,
+                                host=host, step_range=(prev, g + 1))
+                j.run()
+                j.close()
+                prev = g + 1
+                ids = items[bases[g]: bases[g + 1]] & 0x7FFFFFFF
+                for k in range(g0, g1):
+                    lo, hi = int(off[g, k]), int(off[g, k + 1])
+                    if hi == lo:
+                        continue
+                    want = ls.store_fill(ids[lo:hi], SB, fill_seed)
+                    bad = int((outs[k - g0][: hi - lo] != want).any(dim=1).sum())
+                    out["rows_checked"] += hi - lo
+                    out["mismatched_rows"] += bad
+                out["steps_checked"] += 1
+    torch.cuda.synchronize()
+    if out["mismatched_rows"]:
+        raise SystemExit(f"fetch byte check FAILED: {out}")
+    return out
+
+
+def run_plan_kind(args, c, ls, torch, dist, rank, world, dev):
+    """cfg4 / cfg5: the plan (K1-K6) + replay (K7) of the whole job, K jobs
+    per GPU (independent jobs, weak scaling). value = planned-and-replayed
+    samples of all GPUs / timed region (max over ranks)."""
+    D, E, N, b, C = c["D"], c["E"], c["N"], c["b"], c["C"]
+    pc = ls.PipelineConfig(trace=ls.TraceConfig(D, E, N, b, c["seed"], True), buffer_capacity=C)
+    sh = pc.shape()
+    A = int(sh.total_items)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    st = torch.cuda.current_stream()
+
+    def one():
+        a, m, z = ev(), ev(), ev()
+        a.record(st)
+        out = ls.plan_schedule(pc)
+        m.record(st)
+        sim = ls.simulate_plan(out.plan, C)
+        z.record(st)
+        return a, m, z, out, sim
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = ls.lib().lsg_launch_count()
+    res = []
+    with ClockSampler(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0] if rank == 0 else None) as clk:
+        t0, t1 = ev(), ev()
+        t0.record(st)
+        for _ in range(args.steps):
+            a, m, z, out, sim = one()
+            res.append((a, m, z))
+            del out
+        t1.record(st)
+        torch.cuda.synchronize()
+    launches = ls.lib().lsg_launch_count() - launches0
+    total_ms = t0.elapsed_time(t1)
+    plan_ms = statistics.mean(a.elapsed_time(m) for a, m, z in res)
+    replay_ms = statistics.mean(m.elapsed_time(z) for a, m, z in res)
+    # the HBM-bound stage that is callable alone: K1 (trace + inverse
+    # permutations): 4 B per emitted index
+    tr = []
+    for _ in range(3):
+        a, z = ev(), ev()
+        a.record(st)
+        ls.generate_trace(pc.trace)
+        z.record(st)
+        torch.cuda.synchronize()
+        tr.append(a.elapsed_time(z))
+    k1_ms = min(tr)
+    if world > 1:
+        tt = torch.tensor([total_ms, plan_ms, replay_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, plan_ms, replay_ms = [float(x) for x in tt]
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    k1_gbs = 4 * A / (k1_ms * 1e-3) / 1e9
+    cpu = cpu_baseline(c, args.config) if (rank == 0 and world == 1) else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": world * args.steps * A / (total_ms * 1e-3), "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (splitmix64 traces, seed 42)",
+            "config": {"workload": workload(args.config, c), "global_batch": N * b,
+                       "parallelism": f"independent jobs, {args.steps} per GPU" if world > 1 else "one GPU",
+                       "l2": "trace and next-use arrays > L2"},
+            "plan_ms": plan_ms, "replay_ms": replay_ms,
+            "plan_samples_per_s": A / (plan_ms * 1e-3),
+            "roofline": {"bound": "hbm", "achieved": k1_gbs, "peak": peak, "unit": "GB/s", "frac": k1_gbs / peak,
+                         "traffic": None, "kernel": "K1 shuffle (generate_trace: 4 B per emitted index; the plan "
+                                                    "and replay are latency-bound step recurrences)"},
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+            "e2e": None,
+        }
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -338,7 +339,8 @@ struct lsg_fetch_job {
     uint32_t* ready = nullptr;
     unsigned long long* stats = nullptr;
     uint32_t R = 0;
-    unsigned int* resident = nullptr;  // pinned host counter
+    unsigned int* resident = nullptr;  // mapped pinned counter (recycled, never freed)
+    int resident_idx = -1;
     cudaEvent_t listed = nullptr;      // the miss list is built (run waits for it)
     cudaEvent_t prefetched = nullptr;  // the prefetcher finished (destroy waits for it)
     bool prefetching = false;
@@ -348,6 +350,38 @@ struct lsg_fetch_job {
 namespace lsg {
 
 namespace {
+
+// Residency counters of the miss prefetchers: mapped pinned words from one
+// page allocated once per process. cudaFreeHost may synchronise the whole
+// device, which would wait for a LATER job's prefetcher that in turn waits for
+// kernels the calling thread has not enqueued yet, so counters are recycled
+// instead of freed.
+std::mutex g_res_mu;
+unsigned int* g_res = nullptr;
+std::vector<int> g_res_free;
+constexpr int kResSlots = 1024;
+
+unsigned int* resident_acquire(int* idx) {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    if (!g_res) {
+        if (cudaHostAlloc(&g_res, kResSlots * sizeof(unsigned int), cudaHostAllocMapped | cudaHostAllocPortable) !=
+            cudaSuccess) {
+            g_res = nullptr;
+            return nullptr;
+        }
+        for (int i = kResSlots - 1; i >= 0; --i) g_res_free.push_back(i);
+    }
+    if (g_res_free.empty()) return nullptr;
+    *idx = g_res_free.back();
+    g_res_free.pop_back();
+    g_res[*idx] = 0;
+    return g_res + *idx;
+}
+
+void resident_release(int idx) {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    g_res_free.push_back(idx);
+}
 
 void fill_payload(unsigned char* base, uint64_t bytes, uint64_t seed) {
     const uint64_t words = bytes / 8;
@@ -513,9 +547,8 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
             return fail(set_error(kInternal, "fetch_job: ring allocation failed"));
         if (cudaMemsetAsync(j->ready, 0, R * 4, st) != cudaSuccess)
             return fail(cuda_error(cudaGetLastError(), "fetch_job ring"));
-        if (cudaHostAlloc(&j->resident, 4, cudaHostAllocMapped) != cudaSuccess)
-            return fail(set_error(kInternal, "fetch_job: pinned counter"));
-        *j->resident = 0;
+        j->resident = resident_acquire(&j->resident_idx);
+        if (!j->resident) return fail(set_error(kInternal, "fetch_job: no residency counter"));
         unsigned int* dres = nullptr;
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&dres), j->resident, 0);
         PrefetchArgs pa{d.host->dev, j->mid, moff + ns, d.sample_bytes, j->ring, j->R, j->ready,
@@ -611,10 +644,9 @@ void lsg_fetch_job_destroy(lsg_fetch_job* j, void* stream) {
         if (p) cudaFreeAsync(p, st);
     if (j->prefetched) cudaEventDestroy(j->prefetched);
     if (j->listed) cudaEventDestroy(j->listed);
-    if (j->resident) {
-        cudaStreamSynchronize(st);  // nothing still writes the mapped counter
-        cudaFreeHost(j->resident);
-    }
+    // the counter is written only when the prefetcher starts, which create
+    // waited for: it can be recycled now
+    if (j->resident_idx >= 0) resident_release(j->resident_idx);
     delete j;
 }
 
