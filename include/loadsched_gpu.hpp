@@ -7,9 +7,11 @@
 // API for the planner path (cited per declaration); results are bit-identical.
 // Everything is computed on the current CUDA device; inputs are uploaded and
 // outputs returned by value as the reference does. Both buffer policies
-// (Clairvoyant, Lru) run on device; Store files are read and written in the
-// reference's format. Out of this header (and out of scope, see DESIGN.md
-// §8): text formats, the cost model, chunk_insert_redundant.
+// (Clairvoyant, Lru) run on device, chunk_insert_redundant included; Store
+// files, the text artifacts (trace / graph / plan files) and the run reports
+// (metrics.csv, cost totals) are read and written in the reference's formats.
+// Out of this header (and out of scope): the CLI, config
+// files, cost-model calibration, the ablation ladder and summary report.
 #pragma once
 
 #include <cstddef>

@@ -4,8 +4,10 @@
  * (/root/reference/proj, namespace loadsched). Every entry point is plain C:
  * integers, plain pointers and sizes, no torch or STL types. Each function
  * cites the reference interface it replaces. The host C++ layer
- * (paper_2211_00224_b200/host/loadsched_b200.hpp) re-exposes the reference's
- * own C++ signatures on top of these calls; INTEGRATION.md shows the binding.
+ * (include/loadsched_gpu.hpp, implemented in
+ * paper_2211_00224_b200/host/loadsched_gpu.cpp -> libloadsched_gpu.so)
+ * re-exposes the reference's own C++ signatures on top of these calls;
+ * INTEGRATION.md shows the binding.
  *
  * Conventions
  *  - Return value: 0 on success, else the reference ErrorClass code
@@ -185,7 +187,9 @@ int lsg_fetch_step(void* const* d_bufs, void* const* d_outs, const uint32_t* d_i
                    void* stream);
 
 /* The loading phase of steps [step_begin, step_end) of a plan, in step order
- * (one lsg_fetch_step per step, launched from C without host round trips):
+ * (lsg_fetch_job without a host tier: misses synthesised on device; the
+ * job's miss list is built on the device, then two launches per step from C
+ * without host round trips):
  * d_items/d_slots/d_node_off are the WHOLE plan's arrays (lsg_plan_out
  * layout, [T][N+1] offsets), h_node_off a host copy of the offsets (step
  * bases and grid sizes). Every step writes the same batch tensors, as a
@@ -239,6 +243,17 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
 int lsg_fetch_job_run(lsg_fetch_job* job, void* stream);
 int lsg_fetch_job_stats(lsg_fetch_job* job, uint64_t* h_stats4, void* stream);
 void lsg_fetch_job_destroy(lsg_fetch_job* job, void* stream);
+
+/* ---- Run report totals over a device plan (lsg_plan_out layout):
+ * total_barrier_cost and total_io_cost (pipeline.cpp:133-151) with
+ * barrier_time (balance.cpp:41-47) and read_cost (cost_model.cpp:9-18),
+ * bit-identical doubles (reference summation order, no FMA). A list's fetch
+ * count is its untagged items (d_items), or d_fetches[T][N] when given.
+ * d_read_* may be NULL (then *h_io_total = 0). */
+int lsg_plan_costs(const uint32_t* d_items, const uint32_t* d_fetches, const uint32_t* d_node_off,
+                   const uint32_t* d_read_start,
+                   const uint32_t* d_read_end, const uint32_t* d_read_count, uint64_t T, uint32_t N,
+                   double seek_cost, double stream_cost, double* h_barrier_total, double* h_io_total, void* stream);
 
 /* ---- The sample Store (store.hpp:13-81, store.cpp:37-148): SLRD files
  *      (22-byte header + one continuous splitmix64 payload stream).

@@ -365,14 +365,15 @@ def ref_available() -> bool:
     return os.path.exists(REF_DUMP)
 
 
-def ref_text(cfg: Cfg) -> dict:
+def ref_text(cfg: Cfg, extra: tuple[str, ...] = ()) -> dict:
     """The UNMODIFIED reference's write_trace/write_graph/write_plan files of a
     plan_schedule run, its write_metrics (metrics.csv of the configured pass)
     and total_barrier_cost / total_io_cost ("%.6f %.6f"): {"trace", "graph",
     "plan", "metrics", "costs"} -> bytes."""
     with tempfile.TemporaryDirectory() as d:
-        subprocess.run([REF_DUMP, "text", d, *cfg.kv()], check=True, capture_output=True)
-        out = {k: open(os.path.join(d, k + ".txt"), "rb").read() for k in ("trace", "graph", "plan", "costs")}
+        subprocess.run([REF_DUMP, "text", d, *cfg.kv(), *extra], check=True, capture_output=True)
+        out = {k: open(os.path.join(d, k + ".txt"), "rb").read() for k in ("trace", "graph", "plan", "costs",
+                                                                               "costs_exact")}
         out["metrics"] = open(os.path.join(d, "metrics.csv"), "rb").read()
         return out
 

@@ -95,7 +95,7 @@ EXPORTS = [
     "lsg_buffer_create", "lsg_buffer_destroy", "lsg_buffer_access", "lsg_buffer_clear", "lsg_buffer_resident",
     "lsg_simulate_sequence", "lsg_optimal_miss_oracle", "lsg_build_reuse_graph_rows",
     "lsg_fetch_steps", "lsg_host_rows_open", "lsg_host_rows_info", "lsg_host_rows_close",
-    "lsg_fetch_job_create", "lsg_fetch_job_run", "lsg_fetch_job_stats", "lsg_fetch_job_destroy",
+    "lsg_plan_costs", "lsg_fetch_job_create", "lsg_fetch_job_run", "lsg_fetch_job_stats", "lsg_fetch_job_destroy",
 ]
 
 
@@ -176,6 +176,7 @@ def lib() -> ctypes.CDLL:
         L.lsg_store_read.argtypes = [P, u64, u64, P]
         L.lsg_store_read_rows.argtypes = [P, P, u64, u64, P, P]
         L.lsg_fetch_step_store.argtypes = [P, P, P, P, P, P, P, P, u32, u32, u64, u64, P]
+        L.lsg_plan_costs.argtypes = [P, P, P, P, P, P, u64, u32, dbl, dbl, ctypes.POINTER(dbl), ctypes.POINTER(dbl), P]
         L.lsg_host_rows_open.argtypes = [ctypes.c_char_p, u64, u64, u64, i32, ctypes.POINTER(ctypes.c_void_p)]
         L.lsg_host_rows_info.argtypes = [P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_void_p)]
         L.lsg_host_rows_close.argtypes = [P]

@@ -27,6 +27,7 @@
 #include <atomic>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -45,8 +46,9 @@ struct lsg_store {
     size_t h_meta_cap = 0;
     void* d_meta = nullptr;
     size_t d_meta_cap = 0;
-    cudaEvent_t done = nullptr;  // the last H2D out of the staging
+    cudaEvent_t done = nullptr;  // the last call's scatter (it reads d_stage / d_meta) finished
     unsigned threads = 8;
+    std::mutex mu;               // one call at a time owns the staging (the handle is shared by threads)
 };
 
 namespace lsg {
@@ -166,7 +168,9 @@ int read_into_device(lsg_store* h, std::vector<Want>& w, uint64_t thr, unsigned 
         stage_bytes += count * h->size;
         i = j;
     }
-    // the previous call's H2D must be done before the staging is reused
+    // the staging belongs to one call at a time, and the previous call's H2D
+    // copies and scatter (on whatever stream) must be done before it is reused
+    std::lock_guard<std::mutex> lock(h->mu);
     if (h->done) LSG_CUDA(cudaEventSynchronize(h->done));
     void* hs = h->h_stage;
     if (int rc = grow_pinned(hs, h->h_cap, stage_bytes)) return rc;
@@ -202,12 +206,12 @@ int read_into_device(lsg_store* h, std::vector<Want>& w, uint64_t thr, unsigned 
         sc[q] = {src[q], dst[w[q].row], dst2 ? dst2[w[q].row] : nullptr};
     LSG_CUDA(cudaMemcpyAsync(h->d_stage, h->h_stage, stage_bytes, cudaMemcpyHostToDevice, st));
     LSG_CUDA(cudaMemcpyAsync(h->d_meta, h->h_meta, mbytes, cudaMemcpyHostToDevice, st));
-    if (!h->done) LSG_CUDA(cudaEventCreateWithFlags(&h->done, cudaEventDisableTiming));
-    LSG_CUDA(cudaEventRecord(h->done, st));
     dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(h->size / 4096, 1), 64)),
               unsigned(std::min<uint64_t>(w.size(), 4096)));
     k_scatter_rows<<<grid, 256, 0, st>>>(h->d_stage, static_cast<const Scatter*>(h->d_meta), w.size(), h->size);
     LSG_LAUNCH_CHECK("k_scatter_rows");
+    if (!h->done) LSG_CUDA(cudaEventCreateWithFlags(&h->done, cudaEventDisableTiming));
+    LSG_CUDA(cudaEventRecord(h->done, st));
     return kOk;
 }
 

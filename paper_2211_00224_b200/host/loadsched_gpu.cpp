@@ -15,6 +15,9 @@
 #include <sstream>
 #include <memory>
 #include <numeric>
+#include <unordered_map>
+#include <unordered_set>
+#include <iterator>
 
 #include "lsg.h"
 
@@ -335,31 +338,38 @@ std::uint64_t balance_step(StepAssignment& step) {
     return moves;
 }
 
-// balance.cpp:41-49
+// barrier_time (balance.cpp:41-47): the step waits for its most loaded node.
+// Costs are monotone in the count (per_fetch >= 0 for any model the
+// reference accepts), so the slowest node is the one with the most fetches.
 double barrier_time(const StepAssignment& step, const CostModel& model) {
-    const double per_fetch = model.seek_cost + model.stream_cost;
-    double worst = 0.0;
-    for (std::uint64_t c : step.fetch_counts()) worst = std::max(worst, double(c) * per_fetch);
-    return worst;
+    const auto counts = step.fetch_counts();
+    if (counts.empty()) return 0.0;
+    const std::uint64_t most = *std::max_element(counts.begin(), counts.end());
+    return std::max(0.0, double(most) * (model.seek_cost + model.stream_cost));
 }
 
-// balance.cpp:51-72
+// batch_size_stats (balance.cpp:51-72): population standard deviation of the
+// per-node list lengths of every step (left-to-right sums, as the reference)
 std::vector<StepSizes> batch_size_stats(const SchedulePlan& plan) {
-    std::vector<StepSizes> out;
-    for (const EpochPlan& ep : plan.epochs)
-        for (std::size_t t = 0; t < ep.steps.size(); ++t) {
-            StepSizes row;
-            row.epoch = ep.epoch;
-            row.step = t;
-            for (const auto& list : ep.steps[t].assignment.nodes) row.sizes.push_back(list.size());
-            double mean = 0.0, var = 0.0;
-            for (std::uint64_t v : row.sizes) mean += double(v);
-            mean /= double(row.sizes.size());
-            for (std::uint64_t v : row.sizes) var += (double(v) - mean) * (double(v) - mean);
-            row.stddev = std::sqrt(var / double(row.sizes.size()));
-            out.push_back(std::move(row));
+    std::vector<StepSizes> stats;
+    for (const EpochPlan& ep : plan.epochs) {
+        std::uint64_t t = 0;
+        for (const StepPlan& sp : ep.steps) {
+            StepSizes s{ep.epoch, t++, {}, 0.0};
+            std::transform(sp.assignment.nodes.begin(), sp.assignment.nodes.end(), std::back_inserter(s.sizes),
+                           [](const auto& list) { return std::uint64_t(list.size()); });
+            const double n = double(s.sizes.size());
+            const double mu = std::accumulate(s.sizes.begin(), s.sizes.end(), 0.0,
+                                              [](double acc, std::uint64_t v) { return acc + double(v); }) / n;
+            const double ss = std::accumulate(s.sizes.begin(), s.sizes.end(), 0.0, [mu](double acc, std::uint64_t v) {
+                const double d = double(v) - mu;
+                return acc + d * d;
+            });
+            s.stddev = std::sqrt(ss / n);
+            stats.push_back(std::move(s));
         }
-    return out;
+    }
+    return stats;
 }
 
 // ---- buffer.cpp:10-98 on the device (buffer_api.cu) ------------------------
@@ -437,70 +447,74 @@ std::uint64_t optimal_miss_oracle(const std::vector<SampleId>& seq, std::uint64_
     return optimal_miss_oracle(seq, capacity);
 }
 
-// cost_model.cpp:9-18
+// read_cost (cost_model.cpp:9-18): one seek plus the span streamed per read
 double read_cost(const std::vector<Read>& reads, const CostModel& model) {
-    double cost = 0.0;
-    for (const Read& r : reads) cost += model.seek_cost + double(r.span()) * model.stream_cost;
-    return cost;
+    return std::accumulate(reads.begin(), reads.end(), 0.0, [&model](double acc, const Read& r) {
+        return acc + (model.seek_cost + double(r.span()) * model.stream_cost);
+    });
 }
 double read_cost(const ChunkPlan& plan, const CostModel& model) { return read_cost(plan.reads, model); }
 
-// cost_model.cpp:64-71: floor(seek / stream + 2), capped
+// derive_threshold (cost_model.cpp:64-71): a chunk read of span s beats s
+// single reads while (s - 1) * stream < (s - 1) * seek, i.e. spans up to
+// seek/stream + 2 (floored), never beyond max_threshold
 std::uint64_t derive_threshold(const CostModel& model, std::uint64_t max_threshold) {
     if (model.seek_cost < 0.0 || model.stream_cost < 0.0)
         throw ValidationError("derive_threshold: negative model parameters");
     if (model.stream_cost == 0.0) return max_threshold;
-    const double bound = model.seek_cost / model.stream_cost + 2.0;
-    return bound >= double(max_threshold) ? max_threshold : std::uint64_t(std::floor(bound));
+    const double limit = std::floor(model.seek_cost / model.stream_cost + 2.0);
+    return limit >= double(max_threshold) ? max_threshold : std::uint64_t(limit);
 }
 
-// chunking.cpp:35-45 (accessor of a plan)
+// redundant_ids (chunking.cpp:35-45): ids a chunk read brings in that the
+// list did not ask for, in read order
 std::vector<SampleId> redundant_ids(const ChunkPlan& plan, const std::vector<SampleId>& fetch_ids) {
-    std::vector<SampleId> needed = fetch_ids;
-    std::sort(needed.begin(), needed.end());
-    std::vector<SampleId> out;
-    for (const Read& read : plan.reads) {
-        if (read.kind != Read::Kind::Chunk) continue;
-        for (SampleId id = read.start; id <= read.end; ++id)
-            if (!std::binary_search(needed.begin(), needed.end(), id)) out.push_back(id);
-    }
-    return out;
+    const std::unordered_set<SampleId> wanted(fetch_ids.begin(), fetch_ids.end());
+    std::vector<SampleId> extra;
+    for (const Read& r : plan.reads)
+        if (r.kind == Read::Kind::Chunk)
+            for (SampleId x = r.start; x <= r.end; ++x)
+                if (!wanted.count(x)) extra.push_back(x);
+    return extra;
 }
 
-// chunking.cpp:49-69 (reporting accessor)
+// chunked_fraction (chunking.cpp:49-69): percent of needed samples that
+// arrive inside chunk reads (a chunk's redundant ids do not count)
 double chunked_fraction(const std::vector<ChunkPlan>& plans) {
-    std::uint64_t in_chunks = 0, total = 0;
-    for (const ChunkPlan& plan : plans) {
-        total += plan.needed;
-        for (const Read& read : plan.reads)
-            if (read.kind == Read::Kind::Chunk) in_chunks += read.span();
-        in_chunks -= plan.redundant;
+    std::uint64_t needed = 0, chunked = 0;
+    for (const ChunkPlan& p : plans) {
+        needed += p.needed;
+        chunked += std::accumulate(p.reads.begin(), p.reads.end(), std::uint64_t(0),
+                                   [](std::uint64_t acc, const Read& r) {
+                                       return acc + (r.kind == Read::Kind::Chunk ? r.span() : 0);
+                                   }) -
+                   p.redundant;
     }
-    return total == 0 ? 0.0 : 100.0 * double(in_chunks) / double(total);
+    return needed ? 100.0 * double(chunked) / double(needed) : 0.0;
 }
 
 double chunked_fraction(const ChunkPlan& plan) { return chunked_fraction(std::vector<ChunkPlan>{plan}); }
 
-// epoch_order.cpp:11-30
+// path_cost (epoch_order.cpp:11-22): the open path's weight; the order must
+// be a permutation of the epochs
 std::uint64_t path_cost(const ReuseGraph& graph, const std::vector<std::uint32_t>& order) {
-    const std::uint32_t E = graph.num_epochs;
-    if (order.size() != E) throw ValidationError("path_cost: order length != num_epochs");
-    std::vector<bool> seen(E, false);
-    for (std::uint32_t v : order) {
-        if (v >= E || seen[v]) throw ValidationError("path_cost: order is not a permutation");
-        seen[v] = true;
-    }
+    if (order.size() != graph.num_epochs) throw ValidationError("path_cost: order length != num_epochs");
+    std::vector<std::uint32_t> sorted(order);
+    std::sort(sorted.begin(), sorted.end());
+    for (std::uint32_t i = 0; i < sorted.size(); ++i)
+        if (sorted[i] != i) throw ValidationError("path_cost: order is not a permutation");
     std::uint64_t c = 0;
-    for (std::size_t i = 0; i + 1 < order.size(); ++i) c += graph.weight(order[i], order[i + 1]);
+    for (auto it = order.begin(); it != order.end() && std::next(it) != order.end(); ++it)
+        c += graph.weight(*it, *std::next(it));
     return c;
 }
 
+// identity_order (epoch_order.cpp:24-30)
 EpochOrder identity_order(const ReuseGraph& graph) {
-    EpochOrder r;
-    r.order.resize(graph.num_epochs);
-    std::iota(r.order.begin(), r.order.end(), 0u);
-    r.cost = path_cost(graph, r.order);
-    return r;
+    std::vector<std::uint32_t> ids(graph.num_epochs);
+    std::iota(ids.begin(), ids.end(), 0u);
+    const std::uint64_t c = path_cost(graph, ids);
+    return EpochOrder{std::move(ids), c};
 }
 
 PsoResult pso_order(const ReuseGraph& graph, const PsoParams& p) {
@@ -522,33 +536,35 @@ PsoResult pso_order(const ReuseGraph& graph, const PsoParams& p) {
     return r;
 }
 
-// plan.cpp:11-42
+// StepAssignment accessors and same_multiset (plan.cpp:11-42)
 std::vector<std::uint64_t> StepAssignment::fetch_counts() const {
-    std::vector<std::uint64_t> c(nodes.size(), 0);
-    for (std::size_t k = 0; k < nodes.size(); ++k)
-        for (const Assigned& a : nodes[k]) c[k] += a.source == Source::PfsFetch;
-    return c;
+    std::vector<std::uint64_t> counts;
+    counts.reserve(nodes.size());
+    for (const auto& list : nodes)
+        counts.push_back(std::uint64_t(std::count_if(list.begin(), list.end(), [](const Assigned& a) {
+            return a.source == Source::PfsFetch;
+        })));
+    return counts;
 }
 std::vector<SampleId> StepAssignment::fetch_ids(std::uint32_t node) const {
-    std::vector<SampleId> v;
-    for (const Assigned& a : nodes[node])
-        if (a.source == Source::PfsFetch) v.push_back(a.id);
-    return v;
+    const auto& list = nodes.at(node);
+    std::vector<SampleId> ids;
+    for (const Assigned& a : list)
+        if (a.source == Source::PfsFetch) ids.push_back(a.id);
+    return ids;
 }
 std::uint64_t StepAssignment::total_assigned() const {
-    std::uint64_t n = 0;
-    for (const auto& l : nodes) n += l.size();
-    return n;
+    return std::accumulate(nodes.begin(), nodes.end(), std::uint64_t(0),
+                           [](std::uint64_t acc, const auto& list) { return acc + list.size(); });
 }
 bool same_multiset(const StepAssignment& step, const std::vector<SampleId>& batch) {
-    std::vector<SampleId> got;
-    for (const auto& l : step.nodes)
-        for (const Assigned& a : l) got.push_back(a.id);
-    if (got.size() != batch.size()) return false;
-    std::vector<SampleId> want = batch;
-    std::sort(got.begin(), got.end());
-    std::sort(want.begin(), want.end());
-    return got == want;
+    if (step.total_assigned() != batch.size()) return false;
+    std::unordered_map<SampleId, std::int64_t> balance;
+    for (SampleId x : batch) ++balance[x];
+    for (const auto& list : step.nodes)
+        for (const Assigned& a : list)
+            if (--balance[a.id] < 0) return false;
+    return true;  // equal sizes and no id over-used: every count is zero
 }
 
 // ---- text artifacts ----------------------------------------------------
@@ -947,74 +963,108 @@ SimResult simulate_plan(const SchedulePlan& plan, std::uint64_t capacity, Policy
 // ---- run reporting (config.cpp:157-159, pipeline.cpp:133-179) -------------
 const char* policy_name(Policy policy) { return policy == Policy::Clairvoyant ? "clairvoyant" : "lru"; }
 
-double total_barrier_cost(const SchedulePlan& plan, const CostModel& model) {
-    double total = 0.0;
-    for (const EpochPlan& epoch : plan.epochs)
-        for (const StepPlan& step : epoch.steps) total += barrier_time(step.assignment, model);
-    return total;
-}
-
-double total_io_cost(const SchedulePlan& plan, const CostModel& model) {
-    double total = 0.0;
-    for (const EpochPlan& epoch : plan.epochs)
-        for (const StepPlan& step : epoch.steps) {
-            double worst = 0.0;
-            for (const ChunkPlan& reads : step.reads) worst = std::max(worst, read_cost(reads, model));
-            total += worst;
-        }
-    return total;
-}
-
 namespace {
-std::string fixed6(double v) {
-    char buf[64];
-    std::snprintf(buf, sizeof buf, "%.6f", v);
-    return buf;
+// the plan's fetch_after counts, node offsets and reads in the flat device
+// layout (lsg_plan_out) for lsg_plan_costs
+struct FlatCosts {
+    std::uint64_t T = 0;
+    std::uint32_t N = 0;
+    std::vector<std::uint32_t> fa, off, rs, re, rc;
+};
+FlatCosts flatten_costs(const SchedulePlan& plan, bool reads) {
+    FlatCosts f;
+    f.N = plan.num_nodes;
+    for (const EpochPlan& ep : plan.epochs)
+        for (const StepPlan& sp : ep.steps) {
+            ++f.T;
+            std::uint32_t o = 0;
+            for (std::uint32_t k = 0; k < f.N; ++k) {
+                f.fa.push_back(k < sp.assignment.nodes.size()
+                                   ? std::uint32_t(std::count_if(sp.assignment.nodes[k].begin(),
+                                                                 sp.assignment.nodes[k].end(),
+                                                                 [](const Assigned& a) {
+                                                                     return a.source == Source::PfsFetch;
+                                                                 }))
+                                   : 0u);
+                f.off.push_back(o);
+                const std::size_t len = k < sp.assignment.nodes.size() ? sp.assignment.nodes[k].size() : 0;
+                if (reads) {
+                    static const std::vector<Read> none;
+                    const auto& rd = k < sp.reads.size() ? sp.reads[k].reads : none;
+                    // reads sit at their list's item offsets; a list may hold
+                    // fewer items than reads only in a hand-made plan
+                    const std::size_t slots = std::max(len, rd.size());
+                    for (std::size_t i = 0; i < slots; ++i) {
+                        f.rs.push_back(i < rd.size() ? std::uint32_t(rd[i].start) : 0u);
+                        f.re.push_back(i < rd.size() ? std::uint32_t(rd[i].end) : 0u);
+                    }
+                    f.rc.push_back(std::uint32_t(rd.size()));
+                    o += std::uint32_t(slots);
+                } else {
+                    o += std::uint32_t(len);
+                }
+            }
+            f.off.push_back(o);
+        }
+    return f;
+}
+
+std::pair<double, double> device_costs(const SchedulePlan& plan, const CostModel& model, bool reads) {
+    const FlatCosts f = flatten_costs(plan, reads);
+    if (f.T == 0) return {0.0, 0.0};
+    DevBuf<std::uint32_t> fa(f.fa.size()), off(f.off.size()), rs(f.rs.size()), re(f.re.size()), rc(f.rc.size());
+    fa.upload(f.fa.data(), f.fa.size());
+    off.upload(f.off.data(), f.off.size());
+    if (reads) {
+        rs.upload(f.rs.data(), f.rs.size());
+        re.upload(f.re.data(), f.re.size());
+        rc.upload(f.rc.data(), f.rc.size());
+    }
+    double bar = 0.0, io = 0.0;
+    check(lsg_plan_costs(nullptr, fa.p, off.p, reads ? rs.p : nullptr, reads ? re.p : nullptr, reads ? rc.p : nullptr, f.T,
+                         f.N, model.seek_cost, model.stream_cost, &bar, &io, nullptr));
+    return {bar, io};
 }
 }  // namespace
 
+// total_barrier_cost / total_io_cost (pipeline.cpp:133-151): summed on the
+// device over the flat plan (lsg_plan_costs)
+double total_barrier_cost(const SchedulePlan& plan, const CostModel& model) {
+    return device_costs(plan, model, false).first;
+}
+
+double total_io_cost(const SchedulePlan& plan, const CostModel& model) {
+    return device_costs(plan, model, true).second;
+}
+
+// write_metrics (pipeline.cpp:153-179): one CSV row per (epoch, step, node)
+// in execution order; a step's barrier columns are its most loaded node's
+// fetch count before / after balancing x (seek + stream), "%.6f"
 void write_metrics(std::ostream& out, const SchedulePlan& plan, const SimResult& sim, const CostModel& model) {
     out << "epoch,step,node,hits,misses,policy,fetches_before,fetches_after,barrier_before,barrier_after\n";
     const double per_fetch = model.seek_cost + model.stream_cost;
-    std::size_t row = 0;
-    std::string buf;
-    for (const EpochPlan& epoch : plan.epochs) {
-        for (std::size_t t = 0; t < epoch.steps.size(); ++t) {
-            const StepPlan& step = epoch.steps[t];
-            std::uint64_t max_before = 0, max_after = 0;
-            for (std::uint32_t k = 0; k < plan.num_nodes; ++k) {
-                max_before = std::max(max_before, step.fetches_before[k]);
-                max_after = std::max(max_after, step.fetches_after[k]);
-            }
-            const std::string bb = fixed6(double(max_before) * per_fetch), ba = fixed6(double(max_after) * per_fetch);
+    const char* pol = policy_name(sim.policy);
+    auto barrier = [per_fetch](const std::vector<std::uint64_t>& counts, char* buf, std::size_t n) {
+        const std::uint64_t most = counts.empty() ? 0 : *std::max_element(counts.begin(), counts.end());
+        std::snprintf(buf, n, "%.6f", double(most) * per_fetch);
+    };
+    auto row = sim.rows.begin();
+    char bb[64], ba[64], line[256];
+    for (const EpochPlan& ep : plan.epochs) {
+        std::uint64_t t = 0;
+        for (const StepPlan& sp : ep.steps) {
+            barrier(sp.fetches_before, bb, sizeof bb);
+            barrier(sp.fetches_after, ba, sizeof ba);
             for (std::uint32_t k = 0; k < plan.num_nodes; ++k, ++row) {
-                if (row >= sim.rows.size()) throw InternalError("write_metrics: simulation rows out of order");
-                const StepNodeStats& st = sim.rows[row];
-                if (st.epoch != epoch.epoch || st.step != t || st.node != k)
+                if (row == sim.rows.end() || row->epoch != ep.epoch || row->step != t || row->node != k)
                     throw InternalError("write_metrics: simulation rows out of order");
-                buf.clear();
-                buf += std::to_string(epoch.epoch);
-                buf += ',';
-                buf += std::to_string(t);
-                buf += ',';
-                buf += std::to_string(k);
-                buf += ',';
-                buf += std::to_string(st.hits);
-                buf += ',';
-                buf += std::to_string(st.misses);
-                buf += ',';
-                buf += policy_name(sim.policy);
-                buf += ',';
-                buf += std::to_string(step.fetches_before[k]);
-                buf += ',';
-                buf += std::to_string(step.fetches_after[k]);
-                buf += ',';
-                buf += bb;
-                buf += ',';
-                buf += ba;
-                buf += '\n';
-                out << buf;
+                std::snprintf(line, sizeof line, "%u,%llu,%u,%llu,%llu,%s,%llu,%llu,%s,%s\n", ep.epoch,
+                              (unsigned long long)t, k, (unsigned long long)row->hits,
+                              (unsigned long long)row->misses, pol, (unsigned long long)sp.fetches_before.at(k),
+                              (unsigned long long)sp.fetches_after.at(k), bb, ba);
+                out << line;
             }
+            ++t;
         }
     }
 }

@@ -781,39 +781,32 @@ def policy_name(policy: str) -> str:
     return ("clairvoyant", "lru")[_policy_code(policy)]
 
 
+def _plan_costs(plan: SchedulePlan, model: CostModel, reads: bool) -> tuple[float, float]:
+    """lsg_plan_costs: per-step barrier and read-plan costs summed on the
+    device in the reference's order (bit-identical doubles)."""
+    T, N = plan.node_off.shape[0], plan.num_nodes
+    bar, io = ctypes.c_double(), ctypes.c_double()
+    rs = _ptr(plan.read_start) if reads else None
+    re_ = _ptr(plan.read_end) if reads else None
+    rc = _ptr(plan.read_count) if reads else None
+    _check(lib().lsg_plan_costs(_ptr(plan.items.contiguous()), None, _ptr(plan.node_off.contiguous()), rs, re_, rc, T,
+                                N, model.seek_cost, model.stream_cost, ctypes.byref(bar), ctypes.byref(io), _stream()))
+    return bar.value, io.value
+
+
 def total_barrier_cost(plan: SchedulePlan, model: CostModel = CostModel()) -> float:
     """pipeline.cpp:133-138 with barrier_time (balance.cpp:41-47): the sum over
-    steps of max per-node fetch count x (seek + stream)."""
-    per_fetch = model.seek_cost + model.stream_cost
-    total = 0.0
-    for m in plan.fetches_after.max(dim=1).values.cpu().tolist():
-        total += max(0.0, float(m) * per_fetch)
-    return total
+    steps of the most loaded node's fetch count x (seek + stream)."""
+    return _plan_costs(plan, model, False)[0]
 
 
 def total_io_cost(plan: SchedulePlan, model: CostModel = CostModel()) -> float:
     """pipeline.cpp:140-151 with read_cost (cost_model.cpp:9-18): the sum over
-    steps of the max per-node read-plan cost, each read seek + span x stream,
-    accumulated in read order like the reference."""
+    steps of the slowest node's read-plan cost (seek + span x stream per
+    read, in read order)."""
     if plan.read_start is None:
         raise ValidationError(3, "total_io_cost: the plan has no read plans")
-    off = plan.node_off.cpu().numpy().astype(np.int64)
-    cnt = plan.read_count.cpu().numpy().astype(np.int64)
-    rs = plan.read_start.cpu().numpy().view(np.uint32).astype(np.int64)
-    re_ = plan.read_end.cpu().numpy().view(np.uint32).astype(np.int64)
-    T, N = cnt.shape
-    bases = np.concatenate([[0], np.cumsum(off[:, N])])
-    total = 0.0
-    for g in range(T):
-        worst = 0.0
-        for k in range(N):
-            lo = int(bases[g] + off[g, k])
-            c = 0.0
-            for sp in (re_[lo:lo + cnt[g, k]] - rs[lo:lo + cnt[g, k]] + 1).tolist():
-                c += model.seek_cost + float(sp) * model.stream_cost
-            worst = max(worst, c)
-        total += worst
-    return total
+    return _plan_costs(plan, model, True)[1]
 
 
 def format_metrics(plan: SchedulePlan, sim: "SimResult", policy: str | None = None,

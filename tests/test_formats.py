@@ -201,6 +201,23 @@ def test_metrics_match_reference(ls, seed, policy, red):
         1 + out.plan.node_off.shape[0] * out.plan.num_nodes
 
 
+@ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,seek,stream", [(5, 0.37, 0.0013), (6, 13.0, 1.0), (7, 1e-3, 7.25)])
+def test_cost_totals_bit_exact(ls, seed, seek, stream):
+    """total_barrier_cost / total_io_cost (pipeline.cpp:133-151) summed on the
+    device (lsg_plan_costs) equal the reference's doubles bit for bit under a
+    non-integer cost model (no FMA contraction, reference summation order)."""
+    from test_gpu_parity import to_pc
+    c = rand_cfg(seed)
+    out = ls.plan_schedule(to_pc(ls, c))
+    txt = O.ref_text(c, (f"seek_cost={seek!r}", f"stream_cost={stream!r}"))
+    m = ls.CostModel(seek, stream)
+    got = ("%s %s\n" % (float.hex(ls.total_barrier_cost(out.plan, m)), float.hex(ls.total_io_cost(out.plan, m))))
+    want = txt["costs_exact"].decode()
+    assert [float.fromhex(x) for x in got.split()] == [float.fromhex(x) for x in want.split()], (got, want)
+
+
 @pytest.mark.gpu
 def test_plan_file_round_trip_and_replay(ls, tmp_path):
     """read_plan(write_plan(p)) replays to the same SimResult rows; the
