@@ -565,6 +565,57 @@ __global__ void __launch_bounds__(kRT) k_replay_nextuse_cta(ReplayArgsCta a) {
     }
 }
 
+// Next-use keys by SEGMENTS of steps, each fully parallel. A plan that
+// plan_schedule emits holds every id at most once per epoch (over all
+// nodes), so within an epoch-aligned segment an access's next use on its node
+// lies in a LATER segment: walking the segments backward, every access of a
+// segment reads its node's last-seen key of the id and replaces it with its
+// own, all at once (atomicExch; no (node, id) is touched twice). One block per
+// step of the segment. An id seen twice on a node inside the segment (a
+// foreign plan) shows as a previous key inside the segment: flagged, and the
+// caller redoes the pass serially per node. Streaming traffic is the item read
+// and the key write (8 B per access); the [N][D] last-seen table is the
+// random part (L2-resident at cfg2: 8 MB).
+constexpr uint32_t kNuRows = 1024, kNuThreads = 256;  // rows per block, 4 per thread in flight
+
+__global__ void __launch_bounds__(kNuThreads) k_nextuse_seg(const uint32_t* __restrict__ items,
+                                                           const uint32_t* __restrict__ node_off,
+                                                           const uint64_t* __restrict__ gb, uint32_t N, uint64_t D,
+                                                           uint32_t L, uint32_t g0, uint32_t g1, uint32_t chunks,
+                                                           uint32_t* __restrict__ last, uint32_t* __restrict__ nuk,
+                                                           uint32_t* __restrict__ conflict) {
+    extern __shared__ uint32_t soff[];  // [N+1] offsets of this block's step
+    const uint32_t g = g0 + blockIdx.x / chunks, r0 = (blockIdx.x % chunks) * kNuRows;
+    for (uint32_t k = threadIdx.x; k <= N; k += blockDim.x) soff[k] = __ldg(&node_off[size_t(g) * (N + 1) + k]);
+    __syncthreads();
+    const uint64_t base = __ldg(&gb[g]);
+    const uint32_t len = soff[N];
+    const uint64_t seg_lo = uint64_t(g0) * L, seg_hi = uint64_t(g1) * L;
+    bool bad = false;
+    uint32_t old[kNuRows / kNuThreads], rr[kNuRows / kNuThreads];
+#pragma unroll
+    for (uint32_t u = 0; u < kNuRows / kNuThreads; ++u) {  // independent atomics, all in flight
+        const uint32_t r = r0 + u * kNuThreads + threadIdx.x;
+        rr[u] = r;
+        old[u] = kNone;
+        if (r >= len) continue;
+        uint32_t lo = 0, hi = N;  // node of row r: soff[lo] <= r < soff[lo + 1]
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (soff[mid] <= r) lo = mid; else hi = mid;
+        }
+        const uint32_t x = __ldcs(&items[base + r]) & ~kHit;
+        old[u] = atomicExch(&last[size_t(lo) * D + x], g * L + (r - soff[lo]));
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kNuRows / kNuThreads; ++u) {
+        if (rr[u] >= len) continue;
+        __stcs(&nuk[base + rr[u]], old[u] == kNone ? kNever : old[u]);
+        bad |= old[u] != kNone && uint64_t(old[u]) >= seg_lo && uint64_t(old[u]) < seg_hi;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(conflict, 1u);
+}
+
 struct RSharedCta {
     uint32_t size, top, inftop, infcnt, fresh, nfree, ptop;
     uint32_t wbuf[32];  // never_take gather
@@ -1114,9 +1165,9 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
     LSG_LAUNCH_CHECK("k_step_bases");
     uint64_t total = 0, L = 0;
     if (int _rc = d2h_small(&total, gb + T, 8, st)) return _rc;
+    std::vector<uint32_t> hv(size_t(T) * (N + 1));
     {
         // key stride = the longest node list of any step (keys are g*L + i)
-        std::vector<uint32_t> hv(size_t(T) * (N + 1));
         uint32_t* hoff = hv.data();
         const size_t nb = size_t(T) * (N + 1) * 4;
         LSG_CUDA(cudaMemcpyAsync(hoff, d_node_off, nb, cudaMemcpyDeviceToHost, st));
@@ -1147,6 +1198,33 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
                                               std::to_string(D) + ") exceeds the replay's device tables");
     }
     if (L > kRMaxList) return set_error(kCapability, "simulate: node list longer than 16384 samples");
+    // segments of whole steps holding at most D accesses (over all nodes):
+    // epoch-aligned for plan_schedule's plans
+    auto nextuse_segments = [&](uint32_t* last, uint32_t* nuk, uint32_t* conflict) -> int {
+        std::vector<uint32_t> cut{uint32_t(T)};
+        uint64_t acc = 0;
+        for (int64_t g = int64_t(T) - 1; g >= 0; --g) {
+            const uint64_t len = hv[size_t(g) * (N + 1) + N];
+            if (acc + len > D && acc > 0) {
+                cut.push_back(uint32_t(g + 1));
+                acc = 0;
+            }
+            acc += len;
+        }
+        cut.push_back(0);  // cut: descending step boundaries
+        const size_t smem = size_t(N + 1) * 4;
+        for (size_t c = 0; c + 1 < cut.size(); ++c) {
+            const uint32_t g1 = cut[c], g0 = cut[c + 1];
+            if (g1 <= g0) continue;
+            uint64_t longest = 1;  // rows of the segment's longest step
+            for (uint32_t g = g0; g < g1; ++g) longest = std::max<uint64_t>(longest, hv[size_t(g) * (N + 1) + N]);
+            const uint32_t chunks = uint32_t((longest + kNuRows - 1) / kNuRows);
+            k_nextuse_seg<<<(g1 - g0) * chunks, kNuThreads, smem, st>>>(d_items, d_node_off, gb, N, D, uint32_t(L),
+                                                                        g0, g1, chunks, last, nuk, conflict);
+            LSG_LAUNCH_CHECK("k_nextuse_seg");
+        }
+        return kOk;
+    };
     if (policy == 1) {  // LRU
         LruReplayArgs r{};
         r.T = uint32_t(T);
@@ -1259,8 +1337,23 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         c.pbm = a.pbm; c.bw = a.bw; c.psum = a.psum; c.psw = a.psw; c.psum2 = a.psum2; c.ps2w = a.ps2w;
         c.infbm = a.infbm; c.infsum = a.infsum; c.sumw = a.sumw; c.fstack = a.fstack; c.hits = d_hits; c.misses = d_misses;
         c.slot_out = d_slot; c.status = d_status;
-        k_replay_nextuse_cta<<<nk, kRT, 0, st>>>(c);
-        LSG_LAUNCH_CHECK("k_replay_nextuse_cta");
+        bool serial = insred || std::getenv("LSG_NEXTUSE_SERIAL");
+        if (!serial) {  // all nodes' keys (the replay reads only nodes [k0, k1))
+            uint32_t* conflict = sc.get<uint32_t>(1);
+            if (!conflict) return set_error(kInternal, "simulate: scratch allocation failed");
+            LSG_CUDA(cudaMemsetAsync(conflict, 0, 4, st));
+            if (int rc = nextuse_segments(a.last, a.nuk, conflict)) return rc;
+            uint32_t hc = 0;
+            if (int rc = d2h_small(&hc, conflict, 4, st)) return rc;
+            if (hc) {  // an id twice on a node inside a segment: redo serially
+                serial = true;
+                LSG_CUDA(cudaMemsetAsync(a.last, 0xFF, size_t(N) * D * 4, st));
+            }
+        }
+        if (serial) {
+            k_replay_nextuse_cta<<<nk, kRT, 0, st>>>(c);
+            LSG_LAUNCH_CHECK("k_replay_nextuse_cta");
+        }
         // a whole SM per rank only while the ranks fit in one wave with room
         // to spare (256 simulated ranks would otherwise run in two waves)
         const size_t need = size_t(L) * 4 + (L + 2) * 2 + 16;
@@ -1273,8 +1366,23 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         return kOk;
     }
     const unsigned grid = (nk + kRWarps - 1) / kRWarps;
-    k_replay_nextuse<<<grid, kRWarps * 32, 0, st>>>(a);
-    LSG_LAUNCH_CHECK("k_replay_nextuse");
+    bool serial = std::getenv("LSG_NEXTUSE_SERIAL") != nullptr;
+    if (!serial) {
+        uint32_t* conflict = sc.get<uint32_t>(1);
+        if (!conflict) return set_error(kInternal, "simulate: scratch allocation failed");
+        LSG_CUDA(cudaMemsetAsync(conflict, 0, 4, st));
+        if (int rc = nextuse_segments(a.last, a.nuk, conflict)) return rc;
+        uint32_t hc = 0;
+        if (int rc = d2h_small(&hc, conflict, 4, st)) return rc;
+        if (hc) {
+            serial = true;
+            LSG_CUDA(cudaMemsetAsync(a.last, 0xFF, size_t(N) * D * 4, st));
+        }
+    }
+    if (serial) {
+        k_replay_nextuse<<<grid, kRWarps * 32, 0, st>>>(a);
+        LSG_LAUNCH_CHECK("k_replay_nextuse");
+    }
     const size_t smem = size_t(kRWarps) * L * 4;
     LSG_CUDA(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k_replay<<<grid, kRWarps * 32, smem, st>>>(a);
