@@ -349,7 +349,7 @@ def main():
     # one miss-list / prefetch stream per job in flight: a job's prefetcher
     # holds its stream until the job's misses are consumed
     prep = [torch.cuda.Stream(priority=-1 if args.prio else 0) for _ in range(ahead + 2)]
-    ring_bytes = int(float(os.environ.get("LSG_BENCH_RING_GB", "12")) * 2 ** 30)
+    ring_bytes = int(float(os.environ.get("LSG_BENCH_RING_GB", "2")) * 2 ** 30)
 
     # the host tier (e2e miss source): the dataset's Store payload rows in a
     # tmpfs file, pinned; local rank 0 writes it, every process maps it
@@ -369,6 +369,16 @@ def main():
             host_note = (f"host tier: {D} x {SB} B Store payload rows ({D * SB / 2**30:.0f} GiB) in {path}, "
                          f"pinned + mapped; set up in {time.perf_counter() - t0:.1f} s (outside timing)")
 
+    # the e2e miss ring, shared by consecutive jobs: job i+1's misses (its
+    # all-miss first epoch) stream over PCIe into it while job i still fetches
+    misses = None
+    if hostrows is not None:
+        free = torch.cuda.mem_get_info()[0]
+        want = int(float(os.environ.get("LSG_BENCH_STREAM_GB", "48")) * 2 ** 30)
+        ring = max(min(want, free - 24 * 2 ** 30), 2 * maxlen * per * SB)
+        misses = ls.MissStream(SB, ring // SB * SB)
+        host_note += f"; miss ring shared across jobs: {ring / 2**30:.1f} GiB"
+
     def make_jobs(plan, slots, off, host, i):
         """The fetch of job i for every rank group of this GPU (FetchJob:
         miss list, and with the host tier the miss prefetcher, started on a
@@ -376,7 +386,8 @@ def main():
         st = prep[i % len(prep)]
         st.wait_stream(torch.cuda.current_stream())
         return [ls.FetchJob(bufs[: g1 - g0], outs[: g1 - g0], (g0, g1), plan, slots, off, SB, c["fill_seed"],
-                            host=hostrows if host else None, prep_stream=st, ring_bytes=ring_bytes)
+                            host=hostrows if host else None, prep_stream=st, ring_bytes=ring_bytes,
+                            misses=misses if host else None)
                 for g0, g1 in groups]
 
     def run_jobs(n, host=False, pipeline=True, stats=None, t_start=None, keep_jobs=False):
@@ -640,6 +651,7 @@ def main():
         torch.cuda.synchronize()
         e2e_ms = a0.elapsed_time(a1) / args.steps
         e2e_fetch_ms = statistics.mean(e[7].elapsed_time(e[4]) for e in est)
+        e2e_timeline = [[round(a0.elapsed_time(x), 1) for x in (e[7], e[4])] for e in est]
         host_bytes = local_misses * SB if hostrows is not None else 0  # every miss read once from the host tier
         del est
         if world > 1:
@@ -661,6 +673,7 @@ def main():
                          "fetch_ms": e2e_fetch_ms,
                          "note": "per GPU: host-tier bytes / fetch-phase time (the PCIe reads overlap the HBM "
                                  "gather; epoch 0 is all misses)"} if hostrows is not None else None),
+               "fetch_windows_ms": e2e_timeline,
                "note": "per job: lsg_plan_host (trace, graph, order, plan lists, fetch counts to pinned host), "
                        "plan re-uploaded for the replay, hit/miss rows read back, batch fetch with every miss "
                        "read from storage; jobs pipelined as in value" + ("; " + host_note if host_note else "")}
@@ -721,6 +734,8 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+    if misses is not None:
+        misses.close()
     if hostrows is not None:
         hostrows.close()
         if world > 1:

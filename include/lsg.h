@@ -226,6 +226,15 @@ void lsg_host_rows_close(lsg_host_rows* h);
  * lsg_fetch_job_stats (synchronous) reads {misses, kept misses, host bytes,
  * hits}; lsg_fetch_job_destroy frees stream-ordered after the job. */
 typedef struct lsg_fetch_job lsg_fetch_job;
+/* A miss ring shared by consecutive jobs of one fetch stream (same ranks and
+ * buffers, jobs fetched in creation order): a job's prefetcher runs on into
+ * the ring while the previous job still fetches, so a job's all-miss first
+ * epoch is largely staged in HBM before its fetch starts. The ring must hold
+ * a step's rows; destroy it (a device synchronisation) only when no job that
+ * uses it is in flight. */
+typedef struct lsg_miss_stream lsg_miss_stream;
+int lsg_miss_stream_create(uint64_t sample_bytes, uint64_t ring_bytes, lsg_miss_stream** out);
+void lsg_miss_stream_destroy(lsg_miss_stream* ms);
 typedef struct {
     void* const* d_bufs;        /* device array of (node_end - node_begin) HBM buffer pointers */
     void* const* d_outs;        /* device array of batch tensor pointers */
@@ -237,7 +246,8 @@ typedef struct {
     uint32_t N, node_begin, node_end;
     uint64_t sample_bytes, fill_seed;
     const lsg_host_rows* host;  /* NULL: synthesised misses */
-    uint64_t ring_bytes;
+    uint64_t ring_bytes;        /* the job's own ring (0 = 2 GiB) when misses is NULL */
+    lsg_miss_stream* misses;    /* shared ring, or NULL */
 } lsg_fetch_job_desc;
 int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, void* stream);
 int lsg_fetch_job_run(lsg_fetch_job* job, void* stream);

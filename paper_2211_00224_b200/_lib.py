@@ -95,7 +95,7 @@ EXPORTS = [
     "lsg_buffer_create", "lsg_buffer_destroy", "lsg_buffer_access", "lsg_buffer_clear", "lsg_buffer_resident",
     "lsg_simulate_sequence", "lsg_optimal_miss_oracle", "lsg_build_reuse_graph_rows",
     "lsg_fetch_steps", "lsg_host_rows_open", "lsg_host_rows_info", "lsg_host_rows_close",
-    "lsg_plan_costs", "lsg_fetch_job_create", "lsg_fetch_job_run", "lsg_fetch_job_stats", "lsg_fetch_job_destroy",
+    "lsg_plan_costs", "lsg_miss_stream_create", "lsg_miss_stream_destroy", "lsg_fetch_job_create", "lsg_fetch_job_run", "lsg_fetch_job_stats", "lsg_fetch_job_destroy",
 ]
 
 
@@ -105,7 +105,8 @@ class LsgFetchJobDesc(ctypes.Structure):
                                                "h_node_off")] + [
         ("step_begin", ctypes.c_uint64), ("step_end", ctypes.c_uint64), ("N", ctypes.c_uint32),
         ("node_begin", ctypes.c_uint32), ("node_end", ctypes.c_uint32), ("sample_bytes", ctypes.c_uint64),
-        ("fill_seed", ctypes.c_uint64), ("host", ctypes.c_void_p), ("ring_bytes", ctypes.c_uint64)]
+        ("fill_seed", ctypes.c_uint64), ("host", ctypes.c_void_p), ("ring_bytes", ctypes.c_uint64),
+        ("misses", ctypes.c_void_p)]
 
 
 class LsgError(RuntimeError):
@@ -181,6 +182,9 @@ def lib() -> ctypes.CDLL:
         L.lsg_host_rows_info.argtypes = [P, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_void_p)]
         L.lsg_host_rows_close.argtypes = [P]
         L.lsg_host_rows_close.restype = None
+        L.lsg_miss_stream_create.argtypes = [u64, u64, ctypes.POINTER(ctypes.c_void_p)]
+        L.lsg_miss_stream_destroy.argtypes = [P]
+        L.lsg_miss_stream_destroy.restype = None
         L.lsg_fetch_job_create.argtypes = [ctypes.POINTER(LsgFetchJobDesc), ctypes.POINTER(ctypes.c_void_p), P]
         L.lsg_fetch_job_run.argtypes = [P, P]
         L.lsg_fetch_job_stats.argtypes = [P, ctypes.POINTER(u64), P]

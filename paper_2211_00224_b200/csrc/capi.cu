@@ -420,7 +420,7 @@ int lsg_fetch_steps(void* const* d_bufs, void* const* d_outs, const uint32_t* d_
                     uint64_t sample_bytes, uint64_t fill_seed, void* stream) {
     // a job without a host tier: misses synthesised on device (lsg_fetch_job)
     lsg_fetch_job_desc d{d_bufs, d_outs, d_items, d_slots, d_node_off, h_node_off, step_begin, step_end,
-                         N, node_begin, node_end, sample_bytes, fill_seed, nullptr, 0};
+                         N, node_begin, node_end, sample_bytes, fill_seed, nullptr, 0, nullptr};
     lsg_fetch_job* j = nullptr;
     if (int rc = lsg_fetch_job_create(&d, &j, stream)) return rc;
     const int rc = lsg_fetch_job_run(j, stream);

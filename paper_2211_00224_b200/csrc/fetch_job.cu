@@ -39,6 +39,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -184,9 +185,24 @@ struct PrefetchArgs {
     unsigned char* ring;
     uint32_t R;                 // ring rows
     uint32_t* ready;            // [R] row m is in ring slot m % R once ready[m % R] == m + 1
-    const uint32_t* consumed;   // misses released by the consumers (a prefix of the list)
+    const uint32_t* consumed;   // sequence numbers released by the consumers (a prefix)
     unsigned int* resident;     // host-mapped: CTAs that started
+    const uint32_t* seq0;       // sequence number of the job's first miss (0 with a private ring)
+    uint32_t* pf_done;          // sequence numbers fully prefetched (jobs prefetch one after another)
+    uint32_t* ctas_done;        // this job's finished prefetch CTAs
 };
+
+// Jobs sharing a ring prefetch strictly in sequence order: a prefetcher
+// starts once the previous job's prefetcher has published every row, so it
+// never takes PCIe bandwidth from an earlier job whose fetch waits on it; the
+// last CTA to finish passes the baton.
+__device__ __forceinline__ void pf_wait_turn(const PrefetchArgs& a, uint32_t s0) {
+    while (ld_acquire(a.pf_done) < s0) __nanosleep(512);
+}
+__device__ __forceinline__ void pf_pass_turn(const PrefetchArgs& a, uint32_t s0, uint32_t M) {
+    __threadfence();
+    if (atomicAdd(a.ctas_done, 1u) == gridDim.x - 1) atomicMax(a.pf_done, s0 + M);
+}
 
 // K10: TMA bulk copies host -> shared -> ring, kPfStages tiles in flight per
 // CTA, rows round-robin over the CTAs
@@ -200,14 +216,16 @@ __global__ void __launch_bounds__(32) k_miss_prefetch_tma(PrefetchArgs a) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bq));
     }
     asm volatile("fence.mbarrier_init.release.cluster;");
-    const uint32_t M = *a.total;
+    const uint32_t M = *a.total, s0 = *a.seq0;
     const uint64_t tpr = a.row_bytes / kPfTile;
     uint32_t phase[kPfStages] = {};
+    pf_wait_turn(a, s0);
     for (uint32_t m = blockIdx.x; m < M; m += gridDim.x) {
-        if (m >= a.R)
-            while (ld_acquire(a.consumed) < m - a.R + 1) __nanosleep(256);
+        const uint32_t q = s0 + m;  // sequence number: ring slot q % R
+        if (q >= a.R)
+            while (ld_acquire(a.consumed) < q - a.R + 1) __nanosleep(256);
         const unsigned char* src = a.host + uint64_t(__ldg(&a.mid[m])) * a.row_bytes;
-        unsigned char* dst = a.ring + uint64_t(m % a.R) * a.row_bytes;
+        unsigned char* dst = a.ring + uint64_t(q % a.R) * a.row_bytes;
         auto load = [&](uint64_t t) {
             const int q = int(t % kPfStages);
             const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
@@ -237,28 +255,41 @@ __global__ void __launch_bounds__(32) k_miss_prefetch_tma(PrefetchArgs a) {
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the row is in the ring
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __threadfence();
-        st_release(&a.ready[m % a.R], m + 1);
+        st_release(&a.ready[q % a.R], q + 1);
     }
+    pf_pass_turn(a, s0, M);
 }
 
 // K10 for rows that are not whole TMA tiles: 128-bit loads of mapped host memory
 __global__ void __launch_bounds__(256) k_miss_prefetch_lsu(PrefetchArgs a) {
     if (threadIdx.x == 0) atomicAdd_system(a.resident, 1u);
-    const uint32_t M = *a.total;
+    const uint32_t M = *a.total, s0 = *a.seq0;
     const uint64_t vpr = a.row_bytes / 16;
+    if (threadIdx.x == 0) pf_wait_turn(a, s0);
+    __syncthreads();
     for (uint32_t m = blockIdx.x; m < M; m += gridDim.x) {
-        if (threadIdx.x == 0 && m >= a.R)
-            while (ld_acquire(a.consumed) < m - a.R + 1) __nanosleep(256);
+        const uint32_t q = s0 + m;
+        if (threadIdx.x == 0 && q >= a.R)
+            while (ld_acquire(a.consumed) < q - a.R + 1) __nanosleep(256);
         __syncthreads();
         const uint4* src = reinterpret_cast<const uint4*>(a.host + uint64_t(__ldg(&a.mid[m])) * a.row_bytes);
-        uint4* dst = reinterpret_cast<uint4*>(a.ring + uint64_t(m % a.R) * a.row_bytes);
-        for (uint64_t p = threadIdx.x; p < vpr; p += blockDim.x) __stcg(&dst[p], src[p]);
+        uint4* dst = reinterpret_cast<uint4*>(a.ring + uint64_t(q % a.R) * a.row_bytes);
+        uint64_t p = threadIdx.x;
+        for (; p + 3 * blockDim.x < vpr; p += 4 * blockDim.x) {  // 4 loads in flight per thread
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = src[p + u * blockDim.x];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) __stcg(&dst[p + u * blockDim.x], v[u]);
+        }
+        for (; p < vpr; p += blockDim.x) __stcg(&dst[p], src[p]);
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
-            st_release(&a.ready[m % a.R], m + 1);
+            st_release(&a.ready[q % a.R], q + 1);
         }
     }
+    if (threadIdx.x == 0) pf_pass_turn(a, s0, M);
 }
 
 struct MissArgs {
@@ -271,6 +302,7 @@ struct MissArgs {
     const uint32_t* ready;
     uint32_t* consumed;
     uint32_t* done;            // [nsteps] finished blocks per step
+    const uint32_t* seq0;      // sequence number of the job's first miss
 };
 
 // the misses of one step: batch row and (kept) new slot from the ring or the
@@ -278,6 +310,7 @@ struct MissArgs {
 __global__ void __launch_bounds__(256) k_job_misses(MissArgs a) {
     const StepFetch& f = a.f;
     const uint32_t m0 = __ldg(&a.moff[a.gi]), m1 = __ldg(&a.moff[a.gi + 1]);
+    const uint32_t s0 = a.ring ? __ldg(a.seq0) : 0u;
     const uint64_t vpr = f.vec_per_row;
     const uint64_t row_bytes = vpr * 16;
     for (uint32_t m = m0 + blockIdx.y; m < m1; m += gridDim.y) {
@@ -287,10 +320,11 @@ __global__ void __launch_bounds__(256) k_job_misses(MissArgs a) {
         uint4* out = f.outs[k - f.k0] + uint64_t(r - __ldg(&f.node_off[k])) * vpr;
         uint4* buf = sl != kNever ? f.bufs[k - f.k0] + uint64_t(sl) * vpr : nullptr;
         if (a.ring) {
+            const uint32_t q = s0 + m;
             if (threadIdx.x == 0)
-                while (ld_acquire(&a.ready[m % a.R]) != m + 1) __nanosleep(128);
+                while (ld_acquire(&a.ready[q % a.R]) != q + 1) __nanosleep(128);
             __syncthreads();
-            const uint4* src = reinterpret_cast<const uint4*>(a.ring + uint64_t(m % a.R) * row_bytes);
+            const uint4* src = reinterpret_cast<const uint4*>(a.ring + uint64_t(q % a.R) * row_bytes);
             for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < vpr;
                  p += uint64_t(gridDim.x) * blockDim.x) {
                 const uint4 v = __ldcg(&src[p]);
@@ -316,14 +350,36 @@ __global__ void __launch_bounds__(256) k_job_misses(MissArgs a) {
         if (threadIdx.x == 0) {
             __threadfence();
             const uint32_t t = atomicAdd(&a.done[a.gi], 1u);
-            if (t == gridDim.x * gridDim.y - 1) atomicMax(a.consumed, m1);
+            if (t == gridDim.x * gridDim.y - 1) atomicMax(a.consumed, s0 + m1);
         }
     }
+}
+
+// a job's place in a shared miss stream: its misses take the next M sequence
+// numbers (jobs reserve in the order their fetches run)
+__global__ void k_reserve(const uint32_t* __restrict__ total, uint32_t* __restrict__ next_seq,
+                          uint32_t* __restrict__ seq0) {
+    const uint32_t s = *next_seq;
+    *seq0 = s;
+    *next_seq = s + *total;
 }
 
 }  // namespace
 
 }  // namespace lsg
+
+// A ring shared by consecutive jobs of one fetch stream (same ranks, same
+// buffers): job j+1's miss prefetcher fills the ring while job j is still
+// fetching, so the all-miss first epoch of job j+1 is largely in HBM when its
+// fetch starts. Sequence numbers run on across jobs.
+struct lsg_miss_stream {
+    unsigned char* ring = nullptr;
+    uint32_t* words = nullptr;  // ready [R] | next_seq | consumed | pf_done
+    uint32_t R = 0;
+    uint64_t sample_bytes = 0;
+    cudaEvent_t reserved = nullptr;  // the last job's reservation
+    bool any = false;
+};
 
 struct lsg_fetch_job {
     lsg_fetch_job_desc d;
@@ -332,11 +388,15 @@ struct lsg_fetch_job {
     uint64_t nsteps = 0;
     // device state (stream-ordered pool)
     uint32_t* d_base = nullptr;  // [nsteps+1] job-relative step bases
-    uint32_t* d_ctl = nullptr;   // claims [nsteps] | done [nsteps] | cnt [nsteps] | moff [nsteps+1] | consumed
+    uint32_t* d_ctl = nullptr;   // claims [ns] | done [ns] | cnt [ns] | moff [ns+1] | consumed | seq0 | pf_done | ctas
     uint32_t* mrow = nullptr;
     uint32_t* mid = nullptr;
-    unsigned char* ring = nullptr;
+    unsigned char* ring = nullptr;  // the job's own ring, or the shared stream's
     uint32_t* ready = nullptr;
+    uint32_t* consumed = nullptr;
+    uint32_t* seq0 = nullptr;
+    uint32_t* pf_done = nullptr;
+    bool own_ring = false;
     unsigned long long* stats = nullptr;
     uint32_t R = 0;
     unsigned int* resident = nullptr;  // mapped pinned counter (recycled, never freed)
@@ -510,12 +570,12 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
     const uint64_t ns = j->nsteps;
     auto alloc = [&](void** p, size_t bytes) { return cudaMallocAsync(p, std::max<size_t>(bytes, 16), st) == cudaSuccess; };
     if (!alloc(reinterpret_cast<void**>(&j->d_base), (ns + 1) * 4) ||
-        !alloc(reinterpret_cast<void**>(&j->d_ctl), (4 * ns + 2) * 4) ||
+        !alloc(reinterpret_cast<void**>(&j->d_ctl), (4 * ns + 5) * 4) ||
         !alloc(reinterpret_cast<void**>(&j->stats), 32) ||
         !alloc(reinterpret_cast<void**>(&j->mrow), total_rows * 4) ||
         !alloc(reinterpret_cast<void**>(&j->mid), total_rows * 4))
         return fail(set_error(kInternal, "fetch_job: device allocation failed"));
-    if (cudaMemsetAsync(j->d_ctl, 0, (4 * ns + 2) * 4, st) != cudaSuccess ||
+    if (cudaMemsetAsync(j->d_ctl, 0, (4 * ns + 5) * 4, st) != cudaSuccess ||
         cudaMemsetAsync(j->stats, 0, 32, st) != cudaSuccess)
         return fail(cuda_error(cudaGetLastError(), "fetch_job setup"));
     uint32_t* cnt = j->d_ctl + 2 * ns;
@@ -537,23 +597,49 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
     cudaEventCreateWithFlags(&j->listed, cudaEventDisableTiming);
     cudaEventRecord(j->listed, st);
     if (d.host && ns && total_rows) {
-        // ring: at least the largest step (a step's misses are consumed
-        // together), at most ring_bytes beyond that
-        const uint64_t want = d.ring_bytes ? d.ring_bytes : (uint64_t(2) << 30);
-        const uint64_t R = std::min<uint64_t>(total_rows, std::max<uint64_t>(max_rows, want / d.sample_bytes));
-        j->R = uint32_t(R);
-        if (!alloc(reinterpret_cast<void**>(&j->ring), R * d.sample_bytes) ||
-            !alloc(reinterpret_cast<void**>(&j->ready), R * 4))
-            return fail(set_error(kInternal, "fetch_job: ring allocation failed"));
-        if (cudaMemsetAsync(j->ready, 0, R * 4, st) != cudaSuccess)
-            return fail(cuda_error(cudaGetLastError(), "fetch_job ring"));
+        j->seq0 = j->d_ctl + 4 * ns + 2;
+        if (lsg_miss_stream* ms = d.misses) {  // the shared ring: reserve the job's sequence numbers
+            if (ms->sample_bytes != d.sample_bytes)
+                return fail(set_error(kValidation, "fetch_job: miss stream differs in sample size"));
+            if (max_rows > ms->R)
+                return fail(set_error(kCapability, "fetch_job: a step has more rows than the miss stream's ring"));
+            j->R = ms->R;
+            j->ring = ms->ring;
+            j->ready = ms->words;
+            j->consumed = ms->words + ms->R + 1;
+            j->pf_done = ms->words + ms->R + 2;
+            if (ms->any) LSG_CUDA(cudaStreamWaitEvent(st, ms->reserved, 0));  // jobs reserve in creation order
+            k_reserve<<<1, 1, 0, st>>>(moff + ns, ms->words + ms->R, j->seq0);
+            count_launch();
+            if (!ms->reserved) cudaEventCreateWithFlags(&ms->reserved, cudaEventDisableTiming);
+            cudaEventRecord(ms->reserved, st);
+            ms->any = true;
+        } else {
+            // own ring: at least the largest step (a step's misses are
+            // consumed together), at most ring_bytes beyond that
+            const uint64_t want = d.ring_bytes ? d.ring_bytes : (uint64_t(2) << 30);
+            const uint64_t R = std::min<uint64_t>(total_rows, std::max<uint64_t>(max_rows, want / d.sample_bytes));
+            j->R = uint32_t(R);
+            j->own_ring = true;
+            if (!alloc(reinterpret_cast<void**>(&j->ring), R * d.sample_bytes) ||
+                !alloc(reinterpret_cast<void**>(&j->ready), R * 4))
+                return fail(set_error(kInternal, "fetch_job: ring allocation failed"));
+            if (cudaMemsetAsync(j->ready, 0, R * 4, st) != cudaSuccess)
+                return fail(cuda_error(cudaGetLastError(), "fetch_job ring"));
+            j->consumed = j->d_ctl + 4 * ns + 1;
+            j->pf_done = j->d_ctl + 4 * ns + 3;
+        }
         j->resident = resident_acquire(&j->resident_idx);
         if (!j->resident) return fail(set_error(kInternal, "fetch_job: no residency counter"));
         unsigned int* dres = nullptr;
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&dres), j->resident, 0);
         PrefetchArgs pa{d.host->dev, j->mid, moff + ns, d.sample_bytes, j->ring, j->R, j->ready,
-                        j->d_ctl + 4 * ns + 1, dres};
-        const bool tma = d.sample_bytes % kPfTile == 0;
+                        j->consumed, dres, j->seq0, j->pf_done, j->d_ctl + 4 * ns + 4};
+        static const bool lsu = [] {  // LSG_PF_LSU=1: 128-bit loads instead of TMA
+            const char* e = std::getenv("LSG_PF_LSU");
+            return e && e[0] == '1';
+        }();
+        const bool tma = d.sample_bytes % kPfTile == 0 && !lsu;
         if (tma) {
             static bool attr = false;
             if (!attr) {
@@ -596,7 +682,6 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
     uint32_t* claims = j->d_ctl;
     uint32_t* done = j->d_ctl + ns;
     uint32_t* moff = j->d_ctl + 3 * ns;
-    uint32_t* consumed = j->d_ctl + 4 * ns + 1;
     for (uint32_t gi = 0; gi < ns; ++gi) {
         const uint64_t g = d.step_begin + gi;
         const uint64_t b = j->base[gi];
@@ -615,7 +700,7 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
         const uint64_t rows = j->rows[gi];
         if (rows == 0 || d.node_begin == d.node_end) continue;
         if (int rc = launch_fetch_hits(f, rows, d.sample_bytes, st, nullptr)) return rc;
-        MissArgs ma{f, moff, gi, j->mrow, j->ring, j->R, j->ready, consumed, done};
+        MissArgs ma{f, moff, gi, j->mrow, j->ring, j->R, j->ready, j->consumed, done, j->seq0};
         const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 64)),
                         unsigned(std::min<uint64_t>(rows, 148)));
         k_job_misses<<<grid, 256, 0, st>>>(ma);
@@ -639,15 +724,44 @@ void lsg_fetch_job_destroy(lsg_fetch_job* j, void* stream) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (j->prefetching) cudaStreamWaitEvent(st, j->prefetched, 0);
     for (void* p : {static_cast<void*>(j->d_base), static_cast<void*>(j->d_ctl), static_cast<void*>(j->mrow),
-                    static_cast<void*>(j->mid), static_cast<void*>(j->ring), static_cast<void*>(j->ready),
-                    static_cast<void*>(j->stats)})
+                    static_cast<void*>(j->mid), static_cast<void*>(j->stats)})
         if (p) cudaFreeAsync(p, st);
+    if (j->own_ring) {
+        if (j->ring) cudaFreeAsync(j->ring, st);
+        if (j->ready) cudaFreeAsync(j->ready, st);
+    }
     if (j->prefetched) cudaEventDestroy(j->prefetched);
     if (j->listed) cudaEventDestroy(j->listed);
     // the counter is written only when the prefetcher starts, which create
     // waited for: it can be recycled now
     if (j->resident_idx >= 0) resident_release(j->resident_idx);
     delete j;
+}
+
+int lsg_miss_stream_create(uint64_t sample_bytes, uint64_t ring_bytes, lsg_miss_stream** out) {
+    if (!out || sample_bytes == 0 || sample_bytes % 16)
+        return set_error(kValidation, "miss_stream: sample_bytes must be a positive multiple of 16");
+    const uint64_t R = ring_bytes / sample_bytes;
+    if (R == 0 || R >= 0x7FFFFFFFull) return set_error(kValidation, "miss_stream: ring_bytes out of range");
+    auto* ms = new lsg_miss_stream();
+    ms->R = uint32_t(R);
+    ms->sample_bytes = sample_bytes;
+    if (cudaMalloc(&ms->ring, R * sample_bytes) != cudaSuccess ||
+        cudaMalloc(&ms->words, (R + 3) * 4) != cudaSuccess || cudaMemset(ms->words, 0, (R + 3) * 4) != cudaSuccess) {
+        cudaGetLastError();
+        lsg_miss_stream_destroy(ms);
+        return set_error(kInternal, "miss_stream: ring allocation failed");
+    }
+    *out = ms;
+    return kOk;
+}
+
+void lsg_miss_stream_destroy(lsg_miss_stream* ms) {
+    if (!ms) return;
+    if (ms->ring) cudaFree(ms->ring);
+    if (ms->words) cudaFree(ms->words);
+    if (ms->reserved) cudaEventDestroy(ms->reserved);
+    delete ms;
 }
 
 }  // extern "C"

@@ -29,7 +29,7 @@ __all__ = [
     "StorageError", "InternalError", "HIT_BIT", "NEVER", "brute_force_order", "remap_step", "slice_step",
     "remap_epoch", "balance_step", "Read", "ChunkPlan", "plan_chunks", "K_NEVER_USED", "Buffer", "make_buffer",
     "simulate_sequence", "optimal_miss_oracle", "CostModel", "policy_name", "total_barrier_cost",
-    "total_io_cost", "format_metrics", "write_metrics_file", "to_host", "HostRows", "FetchJob",
+    "total_io_cost", "format_metrics", "write_metrics_file", "to_host", "HostRows", "FetchJob", "MissStream",
 ]
 
 
@@ -1059,6 +1059,23 @@ class HostRows:
             pass
 
 
+class MissStream:
+    """A miss ring shared by consecutive FetchJobs of one fetch stream
+    (lsg_miss_stream): each job's prefetcher runs on into the ring while the
+    previous job still fetches. close() synchronises the device."""
+
+    def __init__(self, sample_bytes: int, ring_bytes: int):
+        h = ctypes.c_void_p()
+        _check(lib().lsg_miss_stream_create(sample_bytes, ring_bytes, ctypes.byref(h)))
+        self._h, self.sample_bytes, self.ring_bytes = h, sample_bytes, ring_bytes
+
+    def close(self) -> None:
+        if self._h:
+            torch.cuda.synchronize()
+            lib().lsg_miss_stream_destroy(self._h)
+            self._h = None
+
+
 class FetchJob:
     """The loading phase of a whole job (lsg_fetch_job): every step's batch
     for ranks node_range, hits from the HBM buffers, misses from `host` (a
@@ -1071,7 +1088,8 @@ class FetchJob:
     def __init__(self, bufs: list, outs: list, node_range: tuple[int, int], plan: "SchedulePlan",
                  slots: torch.Tensor, host_node_off: np.ndarray, sample_bytes: int, fill_seed: int = 1,
                  host: HostRows | None = None, step_range: tuple[int, int] | None = None,
-                 prep_stream: torch.cuda.Stream | None = None, ring_bytes: int = 0):
+                 prep_stream: torch.cuda.Stream | None = None, ring_bytes: int = 0,
+                 misses: MissStream | None = None):
         dev = bufs[0].device
         k0, k1 = node_range
         self._keep = [bufs, outs, plan, slots]
@@ -1089,7 +1107,8 @@ class FetchJob:
         d.sample_bytes, d.fill_seed = sample_bytes, fill_seed
         d.host = host._h if host is not None else None
         d.ring_bytes = ring_bytes
-        self.host = host
+        d.misses = misses._h if misses is not None else None
+        self.host, self.misses = host, misses
         if prep_stream is None:  # with a host tier the prefetcher holds its stream: never the fetch's
             prep_stream = torch.cuda.Stream(device=dev) if host is not None else torch.cuda.current_stream()
         st = prep_stream

@@ -180,3 +180,32 @@ def test_host_tier_wrong_sample_size(ls, host_rows):
     bufs, outs = tensors(N, pc.buffer_capacity, 2 * b, 8192)
     with pytest.raises(ls.ValidationError):
         ls.FetchJob(bufs, outs, (0, N), plan, sim.slots, u32(plan.node_off), 8192, 1, host=h)
+
+
+@pytest.mark.parametrize("SB,ring_rows", [(8192, 96), (1024, 70)])
+def test_shared_miss_stream_across_jobs(ls, host_rows, SB, ring_rows):
+    """Consecutive jobs through one MissStream (ring far smaller than a job,
+    sequence numbers running on across jobs, every job created before the
+    previous one has fetched): each job's last batch and final buffer
+    contents are the Store payload."""
+    D, E, N, b = 2048, 4, 2, 32
+    h = host_rows(D, SB)
+    ms = ls.MissStream(SB, ring_rows * SB)
+    fstream = torch.cuda.current_stream()
+    jobs = []
+    for seed in (1, 2, 3):
+        pc, plan, sim = setup(ls, D, E, N, b, 0.2, seed=seed)
+        off = u32(plan.node_off)
+        bufs, outs = tensors(N, pc.buffer_capacity, 2 * b, SB)
+        prep = torch.cuda.Stream()
+        j = ls.FetchJob(bufs, outs, (0, N), plan, sim.slots, off, SB, 1, host=h, prep_stream=prep, misses=ms)
+        jobs.append((j, plan, sim, off, bufs, outs))
+    for j, *_ in jobs:
+        j.run()
+    torch.cuda.synchronize()
+    for j, plan, sim, off, bufs, outs in jobs:
+        assert j.stats()["misses"] == int(u32(sim.misses).sum())
+        j.close()
+        check_step(ls, plan, off, off.shape[0] - 1, outs, 0, N, SB)
+        check_final_slots(ls, plan, sim, off, bufs, 0, N, SB)
+    ms.close()
