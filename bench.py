@@ -286,6 +286,9 @@ def main():
     ap.add_argument("--prio", type=int, default=1, help="plan and replay streams at high priority")
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--ranks", type=int, default=None, help="cfg5: logical ranks (32-256; C = D/(2N))")
+    ap.add_argument("--ranks-per-gpu", type=int, default=None,
+                    help="diagnostic: fetch only this many of the GPU's ranks (e.g. 1 = the 8-GPU per-GPU shape "
+                         "on one GPU); value then counts the fetched ranks' samples")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -310,6 +313,8 @@ def main():
     from paper_2211_00224_b200.parallel import combine_rows, rank_range
 
     k0, k1 = rank_range(N, world, rank)
+    if args.ranks_per_gpu:
+        k1 = min(k1, k0 + args.ranks_per_gpu)
     # ranks whose HBM buffers fit on this GPU at once; more ranks per GPU run
     # one group after another through the same buffers (cfg3: 128 GiB/rank)
     per = max(1, min(k1 - k0, HBM_BUDGET // (C * SB)))
@@ -612,6 +617,9 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms, plan_ms, replay_ms, fetch_ms, job_ms, plan_alone_ms = [float(x) for x in tt]
     ms_per_step = total_ms / max(args.steps, 1)
+    # samples of one job: the whole job, or (diagnostic --ranks-per-gpu) the
+    # fetched ranks' rows on every GPU
+    A_job = A if not args.ranks_per_gpu else (local_hits + local_misses) * world
 
     # HBM-gather algorithmic bytes: hits read a slot and write the batch row
     # (SURVEY §8d); misses come from storage and are reported apart
@@ -688,7 +696,7 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": A / (ms_per_step * 1e-3), "unit": "samples/s", "n_gpus": world,
+            "metric": METRIC, "value": A_job / (ms_per_step * 1e-3), "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (splitmix64 traces and Store payload, seed 42 / fill_seed 1)",

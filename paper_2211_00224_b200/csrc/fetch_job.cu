@@ -38,6 +38,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -355,6 +356,319 @@ __global__ void __launch_bounds__(256) k_job_misses(MissArgs a) {
     }
 }
 
+// ---- the fused step kernel (rows of whole 8 KiB tiles) ----------------------
+// Per row of a step a flag word (k_row_flags), miss index in the upper bits:
+//   kRowEarly    a hit whose slot content was NOT written in the previous
+//                step: its loads may start before the previous step's kernel
+//                has finished (programmatic dependent launch);
+//   kRowInplace  a kept miss whose slot was not read by a hit of the same
+//                step: its slot is written by this kernel, beside the batch
+//                row; other kept misses are written to their slot from the
+//                batch row by k_deferred_slots once the step's kernel is done.
+constexpr uint32_t kRowEarly = 1u, kRowInplace = 2u;
+
+struct FlagArgs {
+    const uint32_t* slots;
+    const uint32_t* node_off;  // job's first step
+    const uint32_t* base;      // [ns] job-relative step bases
+    const uint32_t* moff;      // [ns+1] job miss offsets
+    uint32_t N, k0, k1, P2;
+    uint32_t* flags;           // [job items] per row: (miss index << 2) | bits
+    uint32_t* ndefer;          // [ns] deferred slot writes per step
+};
+
+__device__ __forceinline__ bool sl_hit(uint32_t sl) { return sl != kNever && (sl & kHit); }
+
+// one block per step, nodes [k0, k1) in turn: sort the node's hit slots of
+// this step and its kept-miss slots of the previous step, then flag every row
+__global__ void __launch_bounds__(256) k_row_flags(FlagArgs a) {
+    extern __shared__ uint32_t fsm[];
+    uint32_t* hs = fsm;          // [P2] hit slots of (g, k), sorted
+    uint32_t* ps = fsm + a.P2;   // [P2] kept-miss slots of (g-1, k), sorted
+    __shared__ uint32_t cnt[2], carry, ndef;
+    __shared__ uint32_t wc[8];
+    const uint32_t gi = blockIdx.x;
+    const uint32_t* off = a.node_off + size_t(gi) * (a.N + 1);
+    const uint64_t b = a.base[gi];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        carry = a.moff[gi];  // miss index of the step's next miss
+        ndef = 0;
+    }
+    auto has = [](const uint32_t* v, uint32_t n, uint32_t x) {
+        uint32_t l0 = 0, l1 = n;
+        while (l0 < l1) {
+            const uint32_t mid = (l0 + l1) >> 1;
+            if (v[mid] < x) l0 = mid + 1; else l1 = mid;
+        }
+        return l0 < n && v[l0] == x;
+    };
+    for (uint32_t k = a.k0; k < a.k1; ++k) {
+        const uint32_t lo = off[k], hi = off[k + 1];
+        if (threadIdx.x == 0) cnt[0] = cnt[1] = 0;
+        for (uint32_t i = threadIdx.x; i < a.P2; i += blockDim.x) hs[i] = ps[i] = 0xFFFFFFFFu;
+        __syncthreads();
+        for (uint32_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
+            const uint32_t sl = a.slots[b + r];
+            if (sl_hit(sl)) hs[atomicAdd(&cnt[0], 1u)] = sl & ~kHit;
+        }
+        if (gi > 0) {  // the first step of a job never loads early
+            const uint32_t* off0 = off - (a.N + 1);
+            const uint64_t b0 = a.base[gi - 1];
+            for (uint32_t r = off0[k] + threadIdx.x; r < off0[k + 1]; r += blockDim.x) {
+                const uint32_t sl = a.slots[b0 + r];
+                if (!sl_hit(sl) && sl != kNever) ps[atomicAdd(&cnt[1], 1u)] = sl;
+            }
+        }
+        __syncthreads();
+        for (uint32_t size = 2; size <= a.P2; size <<= 1)  // both arrays at once, bitonic
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t t = threadIdx.x; t < a.P2; t += blockDim.x) {
+                    const uint32_t q = t & (a.P2 / 2 - 1);
+                    uint32_t* v = t >= a.P2 / 2 ? ps : hs;
+                    const uint32_t x0 = 2 * stride * (q / stride) + (q % stride), x1 = x0 + stride;
+                    const bool up = (x0 & size) == 0;
+                    const uint32_t p = v[x0], r2 = v[x1];
+                    if ((p > r2) == up) { v[x0] = r2; v[x1] = p; }
+                }
+                __syncthreads();
+            }
+        // rows in order: a miss's index is the step's misses before it
+        for (uint32_t c = lo; c < hi; c += blockDim.x) {
+            const uint32_t r = c + threadIdx.x;
+            const uint32_t sl = r < hi ? a.slots[b + r] : kHit;
+            const bool miss = r < hi && !sl_hit(sl);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, miss);
+            if (lane == 0) wc[w] = __popc(bal);
+            __syncthreads();
+            uint32_t pre = carry;
+            for (uint32_t q = 0; q < w; ++q) pre += wc[q];
+            if (r < hi) {
+                uint32_t f;
+                if (!miss) {
+                    f = (gi > 0 && !has(ps, cnt[1], sl & ~kHit)) ? kRowEarly : 0u;
+                } else {
+                    const uint32_t m = pre + __popc(bal & ((1u << lane) - 1));
+                    const bool inplace = sl == kNever || !has(hs, cnt[0], sl);
+                    if (!inplace) atomicAdd(&ndef, 1u);
+                    f = (m << 2) | (inplace ? kRowInplace : 0u);
+                }
+                a.flags[b + r] = f;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (uint32_t q = 0; q < blockDim.x / 32; ++q) carry += wc[q];
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) a.ndefer[gi] = ndef;
+}
+
+constexpr int kFTile = 8192, kFStages = 12, kFLag = 3, kFChunk = 16, kFTail = 4;
+
+struct FusedStep {
+    const uint32_t* items;     // step's items
+    const uint32_t* slots;     // step's replay slots
+    const uint32_t* flags;     // step's row flags
+    const uint32_t* node_off;  // step's [N+1]
+    unsigned char* const* bufs;
+    unsigned char* const* outs;
+    uint32_t k0, k1;
+    uint64_t row_bytes, seed;
+    uint32_t* claim;
+    const unsigned char* ring;  // host-tier misses (null: synthesised payload)
+    uint32_t R;
+    const uint32_t* ready;
+    const uint32_t* seq0;
+    const uint32_t* moff;       // [ns+1] job miss offsets
+    uint32_t gi;                // step index in the job
+    uint32_t* done;             // [ns] CTAs finished per step
+    uint32_t* consumed;         // ring sequence numbers released
+};
+
+__device__ __forceinline__ uint32_t fnode_of_row(const FusedStep& f, uint32_t r) {
+    uint32_t k = f.k0;
+    while (k + 1 < f.k1 && __ldg(&f.node_off[k + 1]) <= r) ++k;
+    return k;
+}
+
+// One training step of ranks [k0, k1): every row's 8 KiB tiles through a
+// kFStages-deep TMA pipeline per CTA (one warp; lane 0 issues the bulk
+// copies). Hit tiles: HBM slot -> shared -> batch row. Miss tiles: the ring
+// (host tier, after the row's ready flag) or the Store payload computed by
+// the warp -> shared -> batch row and, for in-place misses, the new slot.
+// Before griddepcontrol.wait the CTA already claims its first chunk and
+// issues loads for early hit rows, so the previous step's tail overlaps this
+// step's first loads; every store waits.
+__global__ void __launch_bounds__(32) k_fetch_fused(FusedStep f) {
+    extern __shared__ __align__(128) unsigned char fsm2[];
+    __shared__ __align__(8) unsigned long long bar[kFStages];
+    __shared__ unsigned char* sdst[kFStages];
+    __shared__ unsigned char* sdst2[kFStages];
+    const uint32_t lane = threadIdx.x;
+    if (lane == 0) {
+        for (int q = 0; q < kFStages; ++q) {
+            const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bq));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncwarp();
+    const uint64_t tpr = f.row_bytes / kFTile;
+    const uint32_t r0 = __ldg(&f.node_off[f.k0]);
+    const uint64_t nt = uint64_t(__ldg(&f.node_off[f.k1]) - r0) * tpr;
+    const uint64_t guide = uint64_t(gridDim.x) * 2 * kFChunk;
+    const uint32_t s0 = f.ring ? __ldg(f.seq0) : 0u;
+    auto claim = [&](uint64_t left_hint) -> uint64_t {
+        uint32_t v = 0;
+        const uint32_t sz = left_hint > guide ? kFChunk : kFTail;
+        if (lane == 0) v = atomicAdd(f.claim, sz);
+        return (uint64_t(__shfl_sync(0xFFFFFFFFu, v, 0)) << 8) | sz;
+    };
+    uint64_t tb, te;
+    {
+        const uint64_t c = claim(nt);
+        tb = c >> 8;
+        te = min(nt, tb + (c & 0xFF));
+    }
+    uint64_t cur = ~0ull, tn = tb;
+    const unsigned char* src_row = nullptr;
+    unsigned char* dst_row = nullptr;
+    unsigned char* dst2_row = nullptr;
+    uint32_t row_flags = 0, row_id = 0;
+    bool row_hit = false, row_ready = false;
+    // next tile into stage k % kFStages; false = nothing (more) to issue now
+    auto issue = [&](uint64_t k, bool early) -> bool {
+        if (tn >= te) {
+            if (tb >= nt) return false;
+            const uint64_t c = claim(nt - te);
+            tb = c >> 8;
+            if (tb >= nt) return false;
+            te = min(nt, tb + (c & 0xFF));
+            tn = tb;
+        }
+        const uint64_t rr = tn / tpr;
+        if (rr != cur) {
+            const uint32_t r = r0 + uint32_t(rr);
+            const uint32_t sl = __ldg(&f.slots[r]);
+            const uint32_t fl = __ldg(&f.flags[r]);
+            const bool hit = sl_hit(sl);
+            if (early && !(hit && (fl & kRowEarly))) return false;  // wait for the previous step first
+            cur = rr;
+            const uint32_t kk = fnode_of_row(f, r);
+            row_hit = hit;
+            row_flags = fl;
+            row_id = __ldg(&f.items[r]) & ~kHit;
+            row_ready = false;
+            src_row = hit ? f.bufs[kk - f.k0] + uint64_t(sl & ~kHit) * f.row_bytes : nullptr;
+            dst_row = f.outs[kk - f.k0] + uint64_t(r - __ldg(&f.node_off[kk])) * f.row_bytes;
+            dst2_row = (!hit && sl != kNever && (fl & kRowInplace)) ? f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes
+                                                                    : nullptr;
+        }
+        const uint64_t c = (tn - cur * tpr) * kFTile;
+        ++tn;
+        const int q = int(k % kFStages);
+        const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
+        unsigned char* st = fsm2 + q * kFTile;
+        if (row_hit || f.ring) {
+            const unsigned char* src = src_row;
+            if (!row_hit) {  // host-tier miss: its ring row, once the prefetcher published it
+                const uint32_t sq = s0 + (row_flags >> 2);
+                if (!row_ready) {
+                    if (lane == 0)
+                        while (ld_acquire(&f.ready[sq % f.R]) != sq + 1) __nanosleep(64);
+                    __syncwarp();
+                    row_ready = true;
+                }
+                src = f.ring + uint64_t(sq % f.R) * f.row_bytes;
+            }
+            if (lane == 0) {
+                const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(st));
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bq), "r"(kFTile));
+                asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(d), "l"(src + c), "r"(kFTile), "r"(bq) : "memory");
+            }
+        } else {  // synthesised Store payload (store.cpp:70-80): words of this tile
+            const uint64_t w0 = (uint64_t(row_id) * f.row_bytes + c) / 8;
+            unsigned long long* sw = reinterpret_cast<unsigned long long*>(st);
+#pragma unroll 4
+            for (uint32_t i = lane; i < kFTile / 8; i += 32) sw[i] = mix64(f.seed + (w0 + i + 1) * kGamma);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bq) : "memory");
+        }
+        if (lane == 0) {
+            sdst[q] = dst_row + c;
+            sdst2[q] = dst2_row ? dst2_row + c : nullptr;
+        }
+        return true;
+    };
+    // every stage is free before the first store: fill them all
+    uint64_t issued = 0;
+    while (issued < uint64_t(kFStages) && issue(issued, true)) ++issued;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous step's kernels are done
+    asm volatile("griddepcontrol.launch_dependents;");  // (only now: the next step may load early)
+    while (issued < uint64_t(kFStages) && issue(issued, false)) ++issued;
+    for (uint64_t k = 0; k < issued; ++k) {
+        const int q = int(k % kFStages);
+        const uint32_t par = uint32_t((k / kFStages) & 1);
+        const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                         : "=r"(done) : "r"(bq), "r"(par) : "memory");
+        if (lane == 0) {
+            const unsigned sp = static_cast<unsigned>(__cvta_generic_to_shared(fsm2 + q * kFTile));
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst[q]), "r"(sp),
+                         "r"(kFTile) : "memory");
+            if (sdst2[q])
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst2[q]), "r"(sp),
+                             "r"(kFTile) : "memory");
+            asm volatile("cp.async.bulk.commit_group;");
+            // stage k+S-L reuses the stage of k-L: free once that store read it
+            if (k >= uint64_t(kFLag)) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kFLag) : "memory");
+        }
+        __syncwarp();
+        if (issued == k + uint64_t(kFStages - kFLag) && issue(issued, false)) ++issued;
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (f.ring && lane == 0) {  // every ring tile this CTA loaded has landed: the last CTA releases the step's rows
+        __threadfence();
+        if (atomicAdd(&f.done[f.gi], 1u) == gridDim.x - 1) atomicMax(f.consumed, s0 + __ldg(&f.moff[f.gi + 1]));
+    }
+}
+
+// kept misses whose slot a hit of the same step read: batch row -> slot,
+// after the step's kernel
+struct DeferArgs {
+    const uint32_t* slots;
+    const uint32_t* flags;
+    const uint32_t* node_off;
+    const uint32_t* mrow;
+    const uint32_t* moff;
+    uint32_t gi, k0, k1;
+    unsigned char* const* bufs;
+    unsigned char* const* outs;
+    uint64_t vpr;
+};
+
+__global__ void __launch_bounds__(256) k_deferred_slots(DeferArgs a) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the step's fused kernel is done
+    asm volatile("griddepcontrol.launch_dependents;");
+    const uint32_t m0 = a.moff[a.gi], m1 = a.moff[a.gi + 1];
+    for (uint32_t m = m0 + blockIdx.y; m < m1; m += gridDim.y) {
+        const uint32_t r = a.mrow[m];
+        const uint32_t sl = a.slots[r];
+        if (sl == kNever || (a.flags[r] & kRowInplace)) continue;
+        uint32_t k = a.k0;
+        while (k + 1 < a.k1 && a.node_off[k + 1] <= r) ++k;
+        const uint4* src = reinterpret_cast<const uint4*>(a.outs[k - a.k0]) + uint64_t(r - a.node_off[k]) * a.vpr;
+        uint4* dst = reinterpret_cast<uint4*>(a.bufs[k - a.k0]) + uint64_t(sl) * a.vpr;
+        for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < a.vpr; p += uint64_t(gridDim.x) * blockDim.x)
+            __stcs(&dst[p], __ldcg(&src[p]));
+    }
+}
+
 // a job's place in a shared miss stream: its misses take the next M sequence
 // numbers (jobs reserve in the order their fetches run)
 __global__ void k_reserve(const uint32_t* __restrict__ total, uint32_t* __restrict__ next_seq,
@@ -397,6 +711,11 @@ struct lsg_fetch_job {
     uint32_t* seq0 = nullptr;
     uint32_t* pf_done = nullptr;
     bool own_ring = false;
+    // fused step kernel (rows of whole 8 KiB tiles)
+    bool fused = false;
+    uint32_t* flags = nullptr;       // [job items] row flags
+    uint32_t* ndefer_d = nullptr;    // [ns]
+    std::vector<uint32_t> ndefer;    // deferred slot writes per step (host)
     unsigned long long* stats = nullptr;
     uint32_t R = 0;
     unsigned int* resident = nullptr;  // mapped pinned counter (recycled, never freed)
@@ -441,6 +760,20 @@ unsigned int* resident_acquire(int* idx) {
 void resident_release(int idx) {
     std::lock_guard<std::mutex> lk(g_res_mu);
     g_res_free.push_back(idx);
+}
+
+// a per-thread pinned bounce buffer for small device->host reads, grown by
+// replacing (never freed: cudaFreeHost may synchronise the device)
+void* pinned_bounce(size_t bytes) {
+    static thread_local void* buf = nullptr;
+    static thread_local size_t cap = 0;
+    if (cap < bytes) {
+        void* p = nullptr;
+        if (cudaMallocHost(&p, std::max<size_t>(bytes, size_t(4) << 20)) != cudaSuccess) return nullptr;
+        buf = p;
+        cap = std::max<size_t>(bytes, size_t(4) << 20);
+    }
+    return buf;
 }
 
 void fill_payload(unsigned char* base, uint64_t bytes, uint64_t seed) {
@@ -545,9 +878,11 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
     j->nsteps = d.step_end - d.step_begin;
     uint64_t b = 0;
     for (uint64_t g = 0; g < d.step_begin; ++g) b += d.h_node_off[g * (N + 1) + N];
-    uint64_t total_rows = 0, max_rows = 0;
+    uint64_t total_rows = 0, max_rows = 0, max_list = 1;
     for (uint64_t g = d.step_begin; g < d.step_end; ++g) {
         const uint32_t* o = d.h_node_off + g * (N + 1);
+        for (uint32_t k = d.node_begin; k < d.node_end; ++k)
+            max_list = std::max<uint64_t>(max_list, o[k + 1] > o[k] ? o[k + 1] - o[k] : 0);
         if (o[d.node_end] < o[d.node_begin]) {
             delete j;
             return set_error(kValidation, "fetch_job: node offsets not ascending");
@@ -594,6 +929,39 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
         count_launch();
     }
     if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return fail(cuda_error(e, "fetch_job: miss list"));
+    static const bool two_kernels = [] {  // LSG_FETCH_FUSED=0: the hit + misses kernel pair per step
+        const char* e = std::getenv("LSG_FETCH_FUSED");
+        return e && e[0] == '0';
+    }();
+    uint32_t P2 = 2;
+    while (P2 < max_list) P2 <<= 1;
+    j->fused = ns && d.sample_bytes % kFTile == 0 && !two_kernels && P2 <= 16384;
+    if (j->fused) {
+        if (!alloc(reinterpret_cast<void**>(&j->flags), (j->base[ns] - j->base[0]) * 4) ||
+            !alloc(reinterpret_cast<void**>(&j->ndefer_d), ns * 4))
+            return fail(set_error(kInternal, "fetch_job: device allocation failed"));
+        const size_t smem = size_t(2) * P2 * 4;
+        static std::atomic<uint64_t> attr_done{0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!(attr_done.load() & (1ull << (dev & 63)))) {
+            cudaFuncSetAttribute(k_row_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16384 * 4);
+            cudaFuncSetAttribute(k_fetch_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kFTile * kFStages);
+            attr_done.fetch_or(1ull << (dev & 63));
+        }
+        FlagArgs fa{d.d_slots + j->base[0], d.d_node_off + d.step_begin * (N + 1), j->d_base, moff, N,
+                    d.node_begin, d.node_end, P2, j->flags, j->ndefer_d};
+        k_row_flags<<<unsigned(ns), 256, smem, st>>>(fa);
+        count_launch();
+        if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return fail(cuda_error(e, "k_row_flags"));
+        // the host needs the steps with deferred slot writes (one read per job)
+        void* hb = pinned_bounce(ns * 4);
+        if (!hb) return fail(set_error(kInternal, "fetch_job: pinned bounce buffer"));
+        if (cudaMemcpyAsync(hb, j->ndefer_d, ns * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return fail(cuda_error(cudaGetLastError(), "fetch_job: deferred counts"));
+        j->ndefer.assign(static_cast<uint32_t*>(hb), static_cast<uint32_t*>(hb) + ns);
+    }
     cudaEventCreateWithFlags(&j->listed, cudaEventDisableTiming);
     cudaEventRecord(j->listed, st);
     if (d.host && ns && total_rows) {
@@ -699,6 +1067,41 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
         f.claim = claims + gi;
         const uint64_t rows = j->rows[gi];
         if (rows == 0 || d.node_begin == d.node_end) continue;
+        if (j->fused) {
+            FusedStep fs{f.items, f.slots, j->flags + (b - j->base[0]), f.node_off,
+                         reinterpret_cast<unsigned char* const*>(d.d_bufs),
+                         reinterpret_cast<unsigned char* const*>(d.d_outs), d.node_begin, d.node_end,
+                         d.sample_bytes, d.fill_seed, f.claim, j->ring, j->R, j->ready, j->seq0, moff, gi, done,
+                         j->consumed};
+            const uint64_t tiles = rows * (d.sample_bytes / kFTile);
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 148ull * 2))));
+            cfg.blockDim = dim3(32);
+            cfg.dynamicSmemBytes = size_t(kFTile) * kFStages;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = pdl_on(0) ? 1 : 0;
+            LSG_CUDA(cudaLaunchKernelEx(&cfg, k_fetch_fused, fs));
+            LSG_LAUNCH_CHECK("k_fetch_fused");
+            if (j->ndefer[gi]) {
+                DeferArgs da{f.slots, fs.flags, f.node_off, j->mrow, moff, gi, d.node_begin, d.node_end, fs.bufs,
+                             fs.outs, d.sample_bytes / 16};
+                const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(da.vpr / 4096, 1), 64)),
+                                unsigned(std::min<uint64_t>(j->ndefer[gi], 148)));
+                cudaLaunchConfig_t dc{};
+                dc.gridDim = grid;
+                dc.blockDim = dim3(256);
+                dc.stream = st;
+                dc.attrs = attr;
+                dc.numAttrs = cfg.numAttrs;
+                LSG_CUDA(cudaLaunchKernelEx(&dc, k_deferred_slots, da));
+                LSG_LAUNCH_CHECK("k_deferred_slots");
+            }
+            continue;
+        }
         if (int rc = launch_fetch_hits(f, rows, d.sample_bytes, st, nullptr)) return rc;
         MissArgs ma{f, moff, gi, j->mrow, j->ring, j->R, j->ready, j->consumed, done, j->seq0};
         const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 64)),
@@ -726,6 +1129,8 @@ void lsg_fetch_job_destroy(lsg_fetch_job* j, void* stream) {
     for (void* p : {static_cast<void*>(j->d_base), static_cast<void*>(j->d_ctl), static_cast<void*>(j->mrow),
                     static_cast<void*>(j->mid), static_cast<void*>(j->stats)})
         if (p) cudaFreeAsync(p, st);
+    if (j->flags) cudaFreeAsync(j->flags, st);
+    if (j->ndefer_d) cudaFreeAsync(j->ndefer_d, st);
     if (j->own_ring) {
         if (j->ring) cudaFreeAsync(j->ring, st);
         if (j->ready) cudaFreeAsync(j->ready, st);
