@@ -719,6 +719,7 @@ def main():
             "gather": {"value": achieved, "unit": "GB/s", "hits": local_hits, "misses": local_misses,
                        "kept_misses": kept_local, "hit_bytes_per_job": hit_bytes,
                        "miss_bytes_per_job": miss_bytes,
+                       "all_bytes_gbs": (hit_bytes + miss_bytes) / (fetch_ms * 1e-3) / 1e9,
                        "note": "HBM gather = 2 x sample_bytes per hit over the fetch phase (the misses' time "
                                "included, their bytes not: SURVEY §8d)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -726,8 +727,8 @@ def main():
                          "traffic_note": "dram read+write bytes per k_fetch_step_hits_tma launch (one steady-state "
                                          "step, all local ranks) from profiles/; "
                                          f"{traffic_ratio:.3f} x that launch's algorithmic bytes" if traffic else None,
-                         "kernel": "fetch phase (k_fetch_step_hits_tma TMA bulk-copy gather + k_job_misses, "
-                                   "one pair per training step)",
+                         "kernel": "fetch phase (k_fetch_fused: one TMA bulk-copy pipeline per training step for "
+                                   "hits and misses, + k_deferred_slots / k_job_misses where needed)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6650"},
             "gpu_launches": int(launches),
             **({"timeline_plan0_plan1_rep0_rep1_fetch0_fetch1": timeline} if timeline else {}),

@@ -309,6 +309,7 @@ struct MissArgs {
 // the misses of one step: batch row and (kept) new slot from the ring or the
 // synthesised payload; the step's last block releases its ring rows
 __global__ void __launch_bounds__(256) k_job_misses(MissArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;");  // the next step's early loads avoid this step's slots
     const StepFetch& f = a.f;
     const uint32_t m0 = __ldg(&a.moff[a.gi]), m1 = __ldg(&a.moff[a.gi + 1]);
     const uint32_t s0 = a.ring ? __ldg(a.seq0) : 0u;
@@ -484,6 +485,7 @@ struct FusedStep {
     uint32_t gi;                // step index in the job
     uint32_t* done;             // [ns] CTAs finished per step
     uint32_t* consumed;         // ring sequence numbers released
+    int skip_misses;            // misses left to k_job_misses (large synthesised rows)
 };
 
 __device__ __forceinline__ uint32_t fnode_of_row(const FusedStep& f, uint32_t r) {
@@ -539,6 +541,7 @@ __global__ void __launch_bounds__(32) k_fetch_fused(FusedStep f) {
     bool row_hit = false, row_ready = false;
     // next tile into stage k % kFStages; false = nothing (more) to issue now
     auto issue = [&](uint64_t k, bool early) -> bool {
+        for (;;) {
         if (tn >= te) {
             if (tb >= nt) return false;
             const uint64_t c = claim(nt - te);
@@ -553,6 +556,10 @@ __global__ void __launch_bounds__(32) k_fetch_fused(FusedStep f) {
             const uint32_t sl = __ldg(&f.slots[r]);
             const uint32_t fl = __ldg(&f.flags[r]);
             const bool hit = sl_hit(sl);
+            if (!hit && f.skip_misses) {  // k_job_misses writes this row: skip its tiles
+                tn = (rr + 1) * tpr;
+                continue;
+            }
             if (early && !(hit && (fl & kRowEarly))) return false;  // wait for the previous step first
             cur = rr;
             const uint32_t kk = fnode_of_row(f, r);
@@ -564,6 +571,8 @@ __global__ void __launch_bounds__(32) k_fetch_fused(FusedStep f) {
             dst_row = f.outs[kk - f.k0] + uint64_t(r - __ldg(&f.node_off[kk])) * f.row_bytes;
             dst2_row = (!hit && sl != kNever && (fl & kRowInplace)) ? f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes
                                                                     : nullptr;
+        }
+        break;
         }
         const uint64_t c = (tn - cur * tpr) * kFTile;
         ++tn;
@@ -716,6 +725,7 @@ struct lsg_fetch_job {
     uint32_t* flags = nullptr;       // [job items] row flags
     uint32_t* ndefer_d = nullptr;    // [ns]
     std::vector<uint32_t> ndefer;    // deferred slot writes per step (host)
+    bool skip_misses = false;        // fused kernel does hits only; k_job_misses after it
     unsigned long long* stats = nullptr;
     uint32_t R = 0;
     unsigned int* resident = nullptr;  // mapped pinned counter (recycled, never freed)
@@ -936,6 +946,9 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
     uint32_t P2 = 2;
     while (P2 < max_list) P2 <<= 1;
     j->fused = ns && d.sample_bytes % kFTile == 0 && !two_kernels && P2 <= 16384;
+    // synthesised payload of large rows (cfg3: 16 MiB) is compute: one warp per
+    // CTA would stall the copy pipeline, so those misses go to a wide kernel
+    j->skip_misses = j->fused && !d.host && d.sample_bytes > (uint64_t(1) << 20);
     if (j->fused) {
         if (!alloc(reinterpret_cast<void**>(&j->flags), (j->base[ns] - j->base[0]) * 4) ||
             !alloc(reinterpret_cast<void**>(&j->ndefer_d), ns * 4))
@@ -1072,7 +1085,7 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
                          reinterpret_cast<unsigned char* const*>(d.d_bufs),
                          reinterpret_cast<unsigned char* const*>(d.d_outs), d.node_begin, d.node_end,
                          d.sample_bytes, d.fill_seed, f.claim, j->ring, j->R, j->ready, j->seq0, moff, gi, done,
-                         j->consumed};
+                         j->consumed, j->skip_misses ? 1 : 0};
             const uint64_t tiles = rows * (d.sample_bytes / kFTile);
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 148ull * 2))));
@@ -1086,6 +1099,14 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
             cfg.numAttrs = pdl_on(0) ? 1 : 0;
             LSG_CUDA(cudaLaunchKernelEx(&cfg, k_fetch_fused, fs));
             LSG_LAUNCH_CHECK("k_fetch_fused");
+            if (j->skip_misses) {  // large synthesised rows: a wide kernel writes the misses after the hits
+                MissArgs ma{f, moff, gi, j->mrow, nullptr, 0, nullptr, nullptr, done, nullptr};
+                const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 64)),
+                                unsigned(std::min<uint64_t>(rows, 148)));
+                k_job_misses<<<grid, 256, 0, st>>>(ma);
+                LSG_LAUNCH_CHECK("k_job_misses");
+                continue;
+            }
             if (j->ndefer[gi]) {
                 DeferArgs da{f.slots, fs.flags, f.node_off, j->mrow, moff, gi, d.node_begin, d.node_end, fs.bufs,
                              fs.outs, d.sample_bytes / 16};

@@ -209,3 +209,19 @@ def test_shared_miss_stream_across_jobs(ls, host_rows, SB, ring_rows):
         check_step(ls, plan, off, off.shape[0] - 1, outs, 0, N, SB)
         check_final_slots(ls, plan, sim, off, bufs, 0, N, SB)
     ms.close()
+
+
+def test_large_rows_hits_fused_misses_wide(ls):
+    """Rows above 1 MiB with synthesised misses (the cfg3 shape in small):
+    the fused kernel moves the hits, a wide kernel writes the misses; every
+    step's batch and the final slots are the Store payload."""
+    D, E, N, b, SB = 512, 4, 2, 8, 2 << 20
+    pc, plan, sim = setup(ls, D, E, N, b, 0.2)
+    off = u32(plan.node_off)
+    T = off.shape[0]
+    bufs, outs = tensors(N, pc.buffer_capacity, 2 * b, SB)
+    f = ls.StepFetcher(bufs, outs, (0, N), SB, 1)
+    for g in range(0, T, 5):
+        f.fetch_steps(plan, sim.slots, off, g, min(T, g + 5))
+        check_step(ls, plan, off, min(T, g + 5) - 1, outs, 0, N, SB)
+    check_final_slots(ls, plan, sim, off, bufs, 0, N, SB)
