@@ -327,6 +327,7 @@ struct PipelineConfig {
     WindowMode graph_mode = WindowMode::Global;
     std::uint64_t chunk_threshold = 15;
     bool chunk_insert_redundant = false;
+    CostModel model{};  // config.hpp:25 (the run reports' cost model)
     PsoParams pso{};
     bool optim_order = true;
     bool optim_remap = true;
@@ -411,5 +412,30 @@ class Store {
 // pipeline.cpp:122-131: the comparison pass of run_pipeline (LRU buffers,
 // identity order, slicing, no balance, no chunking).
 PipelineConfig baseline_config(const PipelineConfig& config);
+
+// pipeline.hpp:33-40 (the ablation ladder's row type; the ladder itself is
+// out of scope)
+struct PassTotals {
+    std::string name;
+    std::uint64_t misses = 0;
+    std::uint64_t hits = 0;
+    double hit_rate = 0.0;
+    double barrier_cost = 0.0;
+    double io_cost = 0.0;
+};
+
+// pipeline.hpp:46-57 / pipeline.cpp:266-311: the configured pass plus the LRU
+// baseline pass, all planned and replayed on the device. With an out_dir the
+// run's artifacts are written in the reference's formats (trace.txt,
+// graph.txt, order.txt, plan.txt, metrics.csv, baseline_metrics.csv); the
+// reference's summary.txt is the ablation-ladder report, out of scope here:
+// after writing the others run_pipeline throws CapabilityError for it.
+struct PipelineResult {
+    PlanOutput output;
+    SimResult sim;
+    SchedulePlan baseline_plan;
+    SimResult baseline_sim;
+};
+PipelineResult run_pipeline(const PipelineConfig& config, const std::string& out_dir);
 
 }  // namespace loadsched

@@ -378,6 +378,13 @@ def ref_text(cfg: Cfg, extra: tuple[str, ...] = ()) -> dict:
         return out
 
 
+def ref_run_pipeline(d: str) -> dict:
+    """The reference's run_pipeline artifacts (test_pipeline.cpp's small
+    config) written into d: {file name: bytes}."""
+    subprocess.run([REF_DUMP, "runpipe", d], check=True, capture_output=True)
+    return {n: open(os.path.join(d, n), "rb").read() for n in sorted(os.listdir(d))}
+
+
 def ref_read(kind: str, data: bytes) -> tuple[int, str]:
     """The reference's read_trace/read_graph/read_plan on `data`: (0, "") or
     (error class, message)."""

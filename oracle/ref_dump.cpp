@@ -390,6 +390,17 @@ int cmd_text(int argc, char** argv) {
     return 0;
 }
 
+// run_pipeline (pipeline.cpp:266-311) of test_pipeline.cpp's small config
+// into <dir> (every artifact, summary.txt included)
+int cmd_runpipe(int argc, char** argv) {
+    if (argc < 3) throw ValidationError("runpipe <dir>");
+    PipelineConfig c;
+    c.trace = {48, 4, 2, 4, 11, true};
+    c.buffer_capacity = 8;
+    (void)run_pipeline(c, argv[2]);
+    return 0;
+}
+
 // the reference's create_store output itself (header + payload) at <path>
 int cmd_storefile(int argc, char** argv) {
     if (argc < 6) throw ValidationError("storefile <path> count size seed");
@@ -414,6 +425,7 @@ int main(int argc, char** argv) {
         if (cmd == "text") return cmd_text(argc, argv);
         if (cmd == "read") return cmd_read(argc, argv);
         if (cmd == "gather") return cmd_gather(argc, argv);
+        if (cmd == "runpipe") return cmd_runpipe(argc, argv);
         std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
         return 1;
     } catch (const Error& e) {

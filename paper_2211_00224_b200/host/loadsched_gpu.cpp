@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
 #include <fstream>
 #include <sstream>
 #include <memory>
@@ -106,8 +107,14 @@ void TraceConfig::validate() const {
 }
 
 void PipelineConfig::validate() const {
-    const lsg_config c = to_c(*this);
+    // config.cpp:11-23 order: trace, buffer, chunk threshold, cost model, PSO
+    PipelineConfig head = *this;
+    head.pso = PsoParams{};
+    const lsg_config c0 = to_c(head);
     lsg_shape sh;
+    check(lsg_shape_of(&c0, &sh));
+    if (model.seek_cost < 0.0 || model.stream_cost < 0.0) throw ConfigError("seek_cost and stream_cost must be >= 0");
+    const lsg_config c = to_c(*this);
     check(lsg_shape_of(&c, &sh));
 }
 
@@ -1067,6 +1074,47 @@ void write_metrics(std::ostream& out, const SchedulePlan& plan, const SimResult&
             ++t;
         }
     }
+}
+
+PipelineResult run_pipeline(const PipelineConfig& config, const std::string& out_dir) {
+    config.validate();
+    PipelineResult r;
+    r.output = plan_schedule(config);
+    r.sim = simulate_plan(r.output.plan, config.buffer_capacity, config.policy,
+                          config.chunk_insert_redundant && config.optim_chunk);
+    const PipelineConfig base = baseline_config(config);
+    r.baseline_plan = plan_schedule(base).plan;
+    r.baseline_sim = simulate_plan(r.baseline_plan, base.buffer_capacity, base.policy, false);
+    if (out_dir.empty()) return r;
+    namespace fs = std::filesystem;
+    std::error_code ec;
+    fs::create_directories(out_dir, ec);
+    if (ec) throw StorageError("cannot create output directory: " + out_dir);
+    const fs::path dir(out_dir);
+    auto open = [&dir](const char* name) {
+        std::ofstream f(dir / name, std::ios::binary);
+        if (!f) throw StorageError(std::string("cannot write ") + name);
+        return f;
+    };
+    write_trace_file((dir / "trace.txt").string(), r.output.trace);
+    write_graph_file((dir / "graph.txt").string(), r.output.graph);
+    {
+        std::ofstream f = open("order.txt");
+        f << "order:";
+        for (std::uint32_t e : r.output.plan.order.order) f << ' ' << e;
+        f << "\ncost: " << r.output.plan.order.cost << "\n";
+    }
+    write_plan_file((dir / "plan.txt").string(), r.output.plan);
+    {
+        std::ofstream f = open("metrics.csv");
+        write_metrics(f, r.output.plan, r.sim, config.model);
+    }
+    {
+        std::ofstream f = open("baseline_metrics.csv");
+        write_metrics(f, r.baseline_plan, r.baseline_sim, config.model);
+    }
+    throw CapabilityError("run_pipeline: summary.txt is the ablation-ladder report, out of scope for the B200 "
+                          "drop-in (the other artifacts were written)");
 }
 
 }  // namespace loadsched

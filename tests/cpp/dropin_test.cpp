@@ -180,7 +180,24 @@ static int dump(int argc, char** argv) {
     return 0;
 }
 
+// run_pipeline (pipeline.cpp:266-311) of the test_pipeline small config into
+// argv[2]; the exit code is the error class (4 = CapabilityError for the
+// out-of-scope summary.txt)
+int run_pipeline_mode(char** argv) {
+    PipelineConfig c;
+    c.trace = {48, 4, 2, 4, 11, true};
+    c.buffer_capacity = 8;
+    try {
+        (void)run_pipeline(c, argv[2]);
+    } catch (const Error& e) {
+        std::printf("%s\n", e.what());
+        return int(e.error_class());
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 2 && std::strcmp(argv[1], "run_pipeline") == 0) return run_pipeline_mode(argv);
     try {
         if (argc > 1 && std::strcmp(argv[1], "dump") == 0) return dump(argc, argv);
         return run_checks();
