@@ -1,33 +1,37 @@
 #!/usr/bin/env python
 """bench.py — the SOLAR loading path on B200 (driver contract: one JSON line).
 
-One bench *step* is one full pass of the hot path over the cfg2 job
-(BASELINE.json configs[1]: 262,144 PtychoNN-shaped samples of 256x256 fp32,
-100 epochs, 8 ranks, local batch 512, per-rank HBM buffer 20% of the dataset):
+One bench *step* is one full pass of the hot path over one job. The default
+job is cfg2 (BASELINE.json configs[1]: 262,144 PtychoNN-shaped samples of
+256x256 fp32, 100 epochs, 8 ranks, local batch 512, per-rank HBM buffer 20%
+of the dataset); `--config cfg1|cfg3|cfg4|cfg5` runs the other named shapes
+(cfg4/cfg5: plan + replay only, as BASELINE names them):
 
   plan     K1 shuffle -> K2/K3 reuse matrix -> K4 PSO order -> K5/K6 step loop
            (locality remap, balance, clairvoyant eviction)   [one GPU per job:
            job i on GPU i mod N, node lists broadcast over NVLink (NCCL)]
   replay   K7 per-rank Belady replay of this GPU's ranks + NCCL all-gather of
            the per-(step, rank) hit/miss rows                [sharded by rank]
-  fetch    K8/K9 every training step's batch of this GPU's ranks: hits gathered
-           from the rank's 12.8 GiB HBM sample buffer, misses written from
-           storage (synthetic Store payload) into the batch and their slot
+  fetch    every training step's batch of this GPU's ranks through the fused
+           TMA step kernel: hits from the rank's 12.8 GiB HBM sample buffer,
+           misses written into the batch and their slot — in `value` from the
+           Store payload computed on device, in `e2e` read over PCIe from the
+           host tier (the dataset's payload rows pinned in host memory)
 
 Jobs are pipelined: plans run on their own stream (the step loop is ONE
 persistent CTA) from a helper thread, overlapping earlier jobs' replay and
 fetch on the other SMs. `single_job_ms` is one job alone, unpipelined.
 
 value = planned-and-fetched samples of the K timed jobs / timed region (max
-over ranks): the loading path's throughput. `plan_samples_per_s` isolates one
-plan (north star: < 1 s for this job). The roofline object is the fetch phase
-(HBM-bound gather). GPUs own contiguous rank ranges (8 ranks / N GPUs); the
-job is fixed, so scaling is strong.
+over ranks). `e2e` = the same through the host-buffer API (plan to pinned
+host and back, hit/miss rows read back, every miss over PCIe). The roofline
+object is the fetch phase (HBM-bound gather; hit bytes only);
+`verify` is a one-shot byte check of the benched fetch (off the timed region).
 
 --impl reference times the reference's own CPU implementation (oracle/_ref,
-compiled from /root/reference/proj/src): plan_schedule + simulate_plan on a
-bounded sample of the same job shape (first E_SAMPLE epochs) plus
-Store::read_one batch fetches, on this host's cores.
+compiled from /root/reference/proj/src): plan_schedule + simulate_plan of the
+FULL job on one core (cfg5: E = 1 and 3, linear in E) plus Store::read_one
+batch fetches on every host core.
 """
 from __future__ import annotations
 
@@ -724,8 +728,8 @@ def main():
                                "included, their bytes not: SURVEY §8d)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "traffic_note": "dram read+write bytes per k_fetch_step_hits_tma launch (one steady-state "
-                                         "step, all local ranks) from profiles/; "
+                         "traffic_note": "dram read+write bytes per k_fetch_fused launch (one steady-state step, "
+                                         "8 ranks on one GPU) from profiles/gather_traffic.json (r02_fetch_fused.ncu-rep); "
                                          f"{traffic_ratio:.3f} x that launch's algorithmic bytes" if traffic else None,
                          "kernel": "fetch phase (k_fetch_fused: one TMA bulk-copy pipeline per training step for "
                                    "hits and misses, + k_deferred_slots / k_job_misses where needed)",

@@ -15,8 +15,11 @@ hi = int(sys.argv[3]) if len(sys.argv) > 3 else None
 rows = [r for r in csv.reader(l for l in open(path) if l.startswith('"'))]
 hdr = rows[0]
 iid, iname, ival = hdr.index("ID"), hdr.index("Kernel Name"), hdr.index("Metric Value")
+imet = hdr.index("Metric Name") if "Metric Name" in hdr else None
 tot, cnt = defaultdict(float), defaultdict(int)
 for r in rows[1:]:
+    if imet is not None and r[imet] != "gpu__time_duration.sum":
+        continue
     i = int(r[iid])
     if lo is not None and not (lo <= i <= hi):
         continue
