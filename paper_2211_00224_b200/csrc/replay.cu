@@ -917,6 +917,366 @@ __global__ void __launch_bounds__(kRT) k_replay_cta(ReplayArgsCta a) {
     }
 }
 
+// ---- the CHAIN replay (clairvoyant, no silent inserts): no id-indexed
+// key/slot tables. A resident is keyed by the position of its next access on
+// the node, so "the access at position q is a hit" is exactly "the key-space
+// bitmap holds bit q" (keys are (step, list position); the bit of an access
+// already served is never reached again, see r_evict_cta). Slots travel along
+// the same chain: when a resident is (re)keyed to position q, its slot is
+// written AHEAD into slot_out[q], so a hit finds its slot at its own index
+// and an eviction by key reads it there; residents never used again keep
+// theirs in an id-indexed array touched once at insert and once at eviction.
+// Per access the streaming traffic is the id, the next-use key and the slot
+// word; the random part is the key-space bitmap (a window of a few epochs:
+// L2-resident).
+template <class Take>
+__device__ __forceinline__ uint32_t bm_take_h(uint32_t* bm, uint32_t* sm1, uint32_t* sm2, uint32_t& top, uint32_t want,
+                                              Take take, uint32_t* fs, uint32_t& nfree, uint32_t* wbuf, uint32_t lane) {
+    // bm_take with a per-taken-bit callback: take(word, bit) retires the
+    // resident and returns its slot (kNone: none yet) for the free stack
+    const uint32_t lt = lanemask_lt_r();
+    uint32_t taken = 0;
+    int32_t cur = int32_t(top);
+    while (taken < want && cur >= 0) {
+        uint32_t ngot = 0;
+        int32_t sw = cur >> 5;
+        uint32_t firstmask = (cur & 31) == 31 ? 0xFFFFFFFFu : ((2u << (cur & 31)) - 1u);
+        bool skip = sm2 != nullptr;
+        while (ngot < 32 && sw >= 0) {
+            if (skip) {
+                int32_t s2 = sw >> 5, found = -1;
+                uint32_t m2 = (sw & 31) == 31 ? 0xFFFFFFFFu : ((2u << (sw & 31)) - 1u);
+                while (s2 >= 0) {
+                    const int32_t my2 = s2 - int32_t(lane);
+                    uint32_t v2 = my2 >= 0 ? __ldcg(&sm2[my2]) : 0u;
+                    if (lane == 0) v2 &= m2;
+                    const uint32_t b2 = __ballot_sync(0xFFFFFFFFu, v2 != 0);
+                    if (b2) {
+                        const uint32_t src = __ffs(b2) - 1;
+                        const uint32_t word = __shfl_sync(0xFFFFFFFFu, v2, src);
+                        found = (s2 - int32_t(src)) * 32 + int32_t(31 - __clz(word));
+                        break;
+                    }
+                    s2 -= 32;
+                    m2 = 0xFFFFFFFFu;
+                }
+                if (found < 0) break;
+                if (found < sw) {
+                    sw = found;
+                    firstmask = 0xFFFFFFFFu;
+                }
+            }
+            const int32_t myws = sw - int32_t(lane);
+            uint32_t v = myws >= 0 ? __ldcg(&sm1[myws]) : 0u;
+            if (lane == 0) v &= firstmask;
+            const uint32_t c = __popc(v);
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if (lane >= uint32_t(d)) incl += o;
+            }
+            uint32_t r = ngot + incl - c;
+            while (v && r < 32) {
+                const uint32_t bit = 31 - __clz(v);
+                v &= ~(1u << bit);
+                wbuf[r++] = uint32_t(myws) * 32 + bit;
+            }
+            const uint32_t found1 = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            ngot += found1;
+            skip = sm2 != nullptr && found1 == 0;
+            sw -= 32;
+            firstmask = 0xFFFFFFFFu;
+        }
+        __syncwarp();
+        ngot = min(ngot, 32u);
+        if (ngot == 0) break;
+        const int32_t myw = lane < ngot ? int32_t(wbuf[lane]) : -1;
+        const uint32_t lastw = wbuf[ngot - 1];
+        __syncwarp();
+        const uint32_t v = myw >= 0 ? __ldcg(&bm[myw]) : 0u;
+        const uint32_t cnt = __popc(v);
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= uint32_t(d)) incl += o;
+        }
+        const uint32_t before = incl - cnt, left = want - taken;
+        const uint32_t take_n = before < left ? min(cnt, left - before) : 0u;
+        uint32_t rest = v, mine = 0;
+        uint32_t sl[32];
+        for (uint32_t t = 0; t < take_n; ++t) {
+            const uint32_t bit = 31 - __clz(rest);
+            rest &= ~(1u << bit);
+            const uint32_t s = take(uint32_t(myw), bit);
+            if (fs && s != kNone) sl[mine++] = s;
+        }
+        // freed slots pushed in eviction order (words descending, bits descending)
+        uint32_t pinc = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, pinc, d);
+            if (lane >= uint32_t(d)) pinc += o;
+        }
+        if (fs)
+            for (uint32_t t = 0; t < mine; ++t) fs[nfree + pinc - mine + t] = sl[t];
+        if (take_n) {
+            bm[myw] = rest;
+            if (rest == 0) {
+                const uint32_t old1 = atomicAnd(&sm1[myw >> 5], ~(1u << (myw & 31)));
+                if (sm2 && (old1 & ~(1u << (myw & 31))) == 0) atomicAnd(&sm2[myw >> 10], ~(1u << ((myw >> 5) & 31)));
+            }
+        }
+        nfree += __shfl_sync(0xFFFFFFFFu, pinc, 31);
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const uint32_t got = min(tot, left);
+        taken += got;
+        if (got < tot || taken >= want) {
+            const uint32_t tb = __ballot_sync(0xFFFFFFFFu, take_n > 0);
+            cur = tb ? int32_t(__shfl_sync(0xFFFFFFFFu, uint32_t(myw), 31 - __clz(tb))) : cur;
+            break;
+        }
+        cur = int32_t(lastw) - 1;
+        (void)lt;
+    }
+    top = cur < 0 ? 0u : uint32_t(cur);
+    __syncwarp();
+    return taken;
+}
+
+struct ChainCtx {
+    const ReplayArgsCta* a;
+    uint32_t k;
+    __device__ __forceinline__ uint64_t pos_index(uint32_t key) const {  // key -> item index
+        const uint32_t beta = key / a->B, p = key - beta * a->B;
+        return __ldg(&a->gb[beta]) + __ldg(&a->node_off[size_t(beta) * (a->N + 1) + k]) + p;
+    }
+    __device__ __forceinline__ uint32_t* pbmk() const { return a->pbm + size_t(k) * a->T * a->bw; }
+    __device__ __forceinline__ bool bit_set(uint32_t key) const {
+        const uint32_t beta = key / a->B, p = key - beta * a->B;
+        return (__ldcg(&pbmk()[size_t(beta) * a->bw + (p >> 5)]) >> (p & 31)) & 1u;
+    }
+    __device__ __forceinline__ bool never_set(uint32_t x) const {
+        return (__ldcg(&a->infbm[size_t(k) * a->infw + (x >> 5)]) >> (x & 31)) & 1u;
+    }
+};
+
+// (re)key a resident: finite keys in the key-space bitmap with the slot
+// written ahead at that position, never-used ids in the id bitmap with the
+// slot in the never-used slot array
+__device__ __forceinline__ void chain_set(const ReplayArgsCta& a, RSharedCta& sh, const ChainCtx& cx, uint32_t x,
+                                          uint32_t nu, uint32_t slot) {
+    const uint32_t k = cx.k;
+    if (nu == kNever) {
+        atomicOr(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
+        atomicOr(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
+        atomicAdd(&sh.infcnt, 1u);
+        atomicMax(&sh.inftop, x >> 5);
+        if (a.slot_out) a.slot[size_t(k) * a.D + x] = slot;
+    } else {
+        const uint32_t beta = nu / a.B;
+        key_mark(cx.pbmk(), a.psum + size_t(k) * a.psw, a.psum2 + size_t(k) * a.ps2w, a.bw, a.B, nu);
+        atomicMax(&sh.ptop, beta * a.bw + ((nu - beta * a.B) >> 5));
+        if (a.slot_out) a.slot_out[cx.pos_index(nu)] = slot;
+    }
+}
+
+// evict the `need` largest keys (warp 0)
+__device__ void chain_evict(const ReplayArgsCta& a, RSharedCta& sh, const ChainCtx& cx, uint32_t need, uint32_t lane) {
+    const uint32_t k = cx.k;
+    uint32_t* fs = a.fstack ? a.fstack + size_t(k) * a.C : nullptr;
+    while (need > 0) {
+        if (sh.infcnt > 0) {  // never used again on this node: ids descending
+            uint32_t top = sh.inftop, nf = sh.nfree;
+            __syncwarp();
+            uint32_t* nvs = a.slot + size_t(k) * a.D;
+            const bool sl = a.slot_out != nullptr;
+            auto take = [&](uint32_t w, uint32_t bit) -> uint32_t {
+                const uint32_t x = w * 32 + bit;
+                return sl ? __ldcg(&nvs[x]) : kNone;
+            };
+            const uint32_t got = bm_take_h(a.infbm + size_t(k) * a.infw, a.infsum + size_t(k) * a.sumw, nullptr, top,
+                                           min(need, sh.infcnt), take, fs, nf, sh.wbuf, lane);
+            if (lane == 0) {
+                sh.inftop = top;
+                sh.nfree = nf;
+                if (got == 0) {
+                    atomicOr(a.status, 2u);
+                    sh.infcnt = 0;
+                }
+                sh.infcnt -= min(got, sh.infcnt);
+                sh.size -= got;
+            }
+            __syncwarp();
+            need -= got;
+            continue;
+        }
+        uint32_t top = sh.ptop, nf = sh.nfree;
+        __syncwarp();
+        const bool sl = a.slot_out != nullptr;
+        auto take = [&](uint32_t w, uint32_t bit) -> uint32_t {  // word w = beta * bw + p / 32
+            if (!sl) return kNone;
+            const uint32_t beta = w / a.bw;
+            const uint64_t idx = __ldg(&a.gb[beta]) + __ldg(&a.node_off[size_t(beta) * (a.N + 1) + k]) +
+                                 (w - beta * a.bw) * 32 + bit;
+            return __ldcg(&a.slot_out[idx]);
+        };
+        const uint32_t got = bm_take_h(cx.pbmk(), a.psum + size_t(k) * a.psw, a.psum2 + size_t(k) * a.ps2w, top, need,
+                                       take, fs, nf, sh.wbuf, lane);
+        if (lane == 0) {
+            sh.ptop = top;
+            sh.nfree = nf;
+            sh.size -= got;
+            if (got == 0) atomicOr(a.status, 4u);
+        }
+        __syncwarp();
+        if (got == 0) return;
+        need -= got;
+    }
+}
+
+__global__ void __launch_bounds__(kRT) k_replay_chain(ReplayArgsCta a) {
+    __shared__ RSharedCta sh;
+    extern __shared__ __align__(16) uint32_t rdyn[];
+    uint32_t* sx = rdyn;                                         // [B] ids | resident bit
+    uint16_t* rstart = reinterpret_cast<uint16_t*>(rdyn + a.B);  // [B+1] run starts
+    const uint32_t k = a.k0 + blockIdx.x;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const ChainCtx cx{&a, k};
+    if (tid == 0) {
+        sh.size = 0;
+        sh.top = 0;
+        sh.ptop = 0;
+        sh.inftop = 0;
+        sh.infcnt = 0;
+        sh.fresh = 0;
+        sh.nfree = 0;
+    }
+    __syncthreads();
+    uint32_t* fs = a.fstack ? a.fstack + size_t(k) * a.C : nullptr;
+    for (uint32_t g = 0; g < a.T; ++g) {
+        const uint32_t* off = a.node_off + size_t(g) * (a.N + 1);
+        const uint32_t o = off[k], L = off[k + 1] - o;
+        const uint64_t base = a.gb[g] + o;
+        if (L > kRMaxList) {
+            if (tid == 0) atomicOr(a.status, 64u);
+            return;
+        }
+        // residency at step start = the key-space bit of the access itself
+        uint32_t hitc = 0;
+        const uint32_t* pw = cx.pbmk() + size_t(g) * a.bw;
+        for (uint32_t c = 0; c < L; c += kRT) {
+            const uint32_t i = c + tid;
+            bool chg = false;
+            if (i < L) {
+                const uint32_t x = a.items[base + i] & ~kHit;
+                const bool res = (__ldcg(&pw[i >> 5]) >> (i & 31)) & 1u;
+                sx[i] = x | (res ? kHit : 0u);
+                if (a.slot_out && res) a.slot_out[base + i] |= kHit;  // its slot was written ahead
+                hitc += res;
+            }
+            __syncthreads();
+            if (i < L) chg = i == 0 || ((sx[i] ^ sx[i - 1]) & kHit);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, chg);
+            if (lane == 0) sh.wsum[w] = __popc(bal);
+            __syncthreads();
+            if (tid == 0) {
+                uint32_t s2 = c == 0 ? 0u : sh.nruns;
+                for (int q = 0; q < kRT / 32; ++q) { const uint32_t v = sh.wsum[q]; sh.wsum[q] = s2; s2 += v; }
+                sh.nruns = s2;
+            }
+            __syncthreads();
+            if (i < L) {
+                const uint32_t rid = sh.wsum[w] + __popc(bal & lanemask_lt_r()) + (chg ? 1u : 0u) - 1u;
+                if (chg) rstart[rid] = uint16_t(i);
+            }
+            __syncthreads();
+        }
+        for (int d = 16; d > 0; d >>= 1) hitc += __shfl_xor_sync(0xFFFFFFFFu, hitc, d);
+        if (lane == 0) sh.wsum[w] = hitc;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t h = 0;
+            for (int q = 0; q < kRT / 32; ++q) h += sh.wsum[q];
+            a.hits[size_t(g) * a.N + k] = h;
+            a.misses[size_t(g) * a.N + k] = L - h;
+            rstart[sh.nruns] = uint16_t(L);
+        }
+        __syncthreads();
+        const uint32_t nruns = L ? sh.nruns : 0;
+        for (uint32_t r = 0; r < nruns; ++r) {
+            const uint32_t r0 = rstart[r], r1 = rstart[r + 1];
+            const bool hitrun = sx[r0] & kHit;
+            for (uint32_t i = r0 + tid; i < r1; i += kRT) {
+                const uint32_t x = sx[i] & ~kHit;
+                // a hit carries its slot on; a miss has none until the run's evictions are done
+                const uint32_t s0 = hitrun && a.slot_out ? (a.slot_out[base + i] & ~kHit) : kNone;
+                chain_set(a, sh, cx, x, a.nuk[base + i], s0);
+            }
+            __syncthreads();
+            if (!hitrun) {
+                if (w == 0) {
+                    uint32_t need = 0;
+                    if (lane == 0) {
+                        sh.size += r1 - r0;
+                        need = sh.size > a.C ? sh.size - a.C : 0u;
+                    }
+                    need = __shfl_sync(0xFFFFFFFFu, need, 0);
+                    if (need) chain_evict(a, sh, cx, need, lane);
+                    __syncwarp();
+                    // survivors of the run take slots, in list order
+                    if (a.slot_out) {
+                        for (uint32_t c = r0; c < r1; c += 32) {
+                            const uint32_t i = c + lane;
+                            bool surv = false;
+                            uint32_t x = 0, nu = kNever;
+                            if (i < r1) {
+                                x = sx[i] & ~kHit;
+                                nu = a.nuk[base + i];
+                                surv = nu == kNever ? cx.never_set(x) : cx.bit_set(nu);
+                            }
+                            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, surv);
+                            const uint32_t rank = __popc(bal & lanemask_lt_r());
+                            const uint32_t nf = sh.nfree, fr = sh.fresh;
+                            if (surv) {
+                                const uint32_t s = rank < nf ? fs[nf - 1 - rank] : fr + (rank - nf);
+                                if (nu == kNever) a.slot[size_t(k) * a.D + x] = s;
+                                else a.slot_out[cx.pos_index(nu)] = s;
+                            }
+                            __syncwarp();
+                            if (lane == 0) {
+                                const uint32_t n = __popc(bal);
+                                const uint32_t from_stack = min(n, nf);
+                                sh.nfree = nf - from_stack;
+                                sh.fresh = fr + (n - from_stack);
+                            }
+                            __syncwarp();
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // misses report the slot they hold at the END of the step (evicted
+        // again by a later run of the step: bypass)
+        if (a.slot_out)
+            for (uint32_t i = tid; i < L; i += kRT) {
+                const uint32_t v = sx[i];
+                if (v & kHit) continue;
+                const uint32_t x = v & ~kHit, nu = a.nuk[base + i];
+                uint32_t s = kNever;
+                if (nu == kNever) {
+                    if (cx.never_set(x)) s = a.slot[size_t(k) * a.D + x];
+                } else if (cx.bit_set(nu)) {
+                    s = __ldcg(&a.slot_out[cx.pos_index(nu)]);
+                }
+                a.slot_out[base + i] = s;
+            }
+        __syncthreads();
+    }
+}
+
 // ---- redundant_ids (chunking.cpp:35-45) of every (step, node) list of a
 // plan with reads: the ids inside its chunk reads (start < end) that are not
 // among the list's fetch ids, unique and ascending. One warp per list; pass 0
@@ -1359,6 +1719,16 @@ int simulate_device(const uint32_t* d_items, const uint32_t* d_node_off, uint64_
         const size_t need = size_t(L) * 4 + (L + 2) * 2 + 16;
         const size_t smem = nk <= 32 ? exclusive_smem(need) : need;
         LSG_CUDA(cudaFuncSetAttribute(k_replay_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        // the chain replay (no id-indexed key/slot tables) needs the key-space
+        // bitmaps and no silent inserts; LSG_REPLAY_TABLES=1 keeps round 1's
+        // table replay
+        const bool chain = a.pbm && !insred && !std::getenv("LSG_REPLAY_TABLES");
+        if (chain) {
+            LSG_CUDA(cudaFuncSetAttribute(k_replay_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            k_replay_chain<<<nk, kRT, smem, st>>>(c);
+            LSG_LAUNCH_CHECK("k_replay_chain");
+            return kOk;
+        }
         const bool pinned = l2_pin(st, hot, hot_words * 4);
         k_replay_cta<<<nk, kRT, smem, st>>>(c);
         LSG_LAUNCH_CHECK("k_replay_cta");

@@ -209,3 +209,45 @@ def test_fetch_steps_matches_per_step(ls, SB):
         assert torch.equal(res[1][1][k - k0][: hi - lo], want)
     with pytest.raises(ls.ValidationError):
         f.fetch_steps(out.plan, sim.slots, off, 3, 2)
+
+
+@pytest.mark.parametrize("variant", ["chain", "tables"])
+@pytest.mark.parametrize("seed", range(12))
+def test_cta_replay_variants(ls, monkeypatch, variant, seed):
+    """The per-rank CTA replay in both forms — the chain replay (residency
+    from the key-space bitmap, slots written ahead; the default for long
+    lists) and round 1's id-indexed tables — forced onto short-list plans:
+    hits/misses equal the oracle's and the slots drive a consistent HBM
+    buffer (every hit's slot holds its sample)."""
+    monkeypatch.setenv("LSG_REPLAY_CTA", "1")
+    if variant == "tables":
+        monkeypatch.setenv("LSG_REPLAY_TABLES", "1")
+    r = random.Random(500 + seed)
+    N, b = r.choice([1, 2, 3, 4, 8]), r.choice([1, 2, 4, 8, 16])
+    B = N * b
+    D = B * r.randint(2, 25) + r.randint(0, B - 1)
+    c = O.Cfg(D, r.randint(1, 7), N, b, seed=seed, buffer_capacity=r.randint(1, max(1, D // 3)),
+              drop_last=r.random() < 0.7, optim_order=r.random() < 0.7,
+              optim_remap=r.random() < 0.8, optim_balance=r.random() < 0.8, pso_iters=20)
+    p = O.plan(c)
+    for C in (c.buffer_capacity, max(1, c.buffer_capacity // 3), D):
+        h, m = O.simulate(p.items, p.node_off, N, D, C)
+        sim = ls.simulate_plan(_plan_obj(ls, p.items, p.node_off, N, D, c.steps), C, want_slots=True)
+        assert np.array_equal(u32(sim.hits), h) and np.array_equal(u32(sim.misses), m), C
+        slots = u32(sim.slots)
+        owner = [dict() for _ in range(N)]
+        base = 0
+        for g in range(p.node_off.shape[0]):
+            for k in range(N):
+                lo, hi = base + p.node_off[g, k], base + p.node_off[g, k + 1]
+                ids = p.items[lo:hi] & 0x7FFFFFFF
+                raw = slots[lo:hi]
+                hit = (raw != 0xFFFFFFFE) & ((raw >> 31) == 1)
+                for i in range(len(ids)):
+                    if hit[i]:
+                        assert owner[k].get(int(raw[i] & 0x7FFFFFFF)) == int(ids[i]), (C, g, k, i)
+                for i in range(len(ids)):
+                    if not hit[i] and raw[i] != 0xFFFFFFFE:
+                        assert raw[i] < C
+                        owner[k][int(raw[i])] = int(ids[i])
+            base += p.node_off[g, N]
