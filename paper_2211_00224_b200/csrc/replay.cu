@@ -1004,23 +1004,43 @@ __device__ __forceinline__ uint32_t bm_take_h(uint32_t* bm, uint32_t* sm1, uint3
         }
         const uint32_t before = incl - cnt, left = want - taken;
         const uint32_t take_n = before < left ? min(cnt, left - before) : 0u;
+        // freed slots are pushed in eviction order (words descending, bits
+        // descending): pass 1 counts them, pass 2 writes; 4 slot loads in flight
         uint32_t rest = v, mine = 0;
-        uint32_t sl[32];
-        for (uint32_t t = 0; t < take_n; ++t) {
-            const uint32_t bit = 31 - __clz(rest);
-            rest &= ~(1u << bit);
-            const uint32_t s = take(uint32_t(myw), bit);
-            if (fs && s != kNone) sl[mine++] = s;
-        }
-        // freed slots pushed in eviction order (words descending, bits descending)
+        if (fs)
+            for (uint32_t t = 0; t < take_n; t += 4) {
+                uint32_t sv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool on = t + u < take_n;
+                    const uint32_t bit = on ? 31 - __clz(rest) : 0u;
+                    if (on) rest &= ~(1u << bit);
+                    sv[u] = on ? take(uint32_t(myw), bit) : kNone;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) mine += sv[u] != kNone;
+            }
         uint32_t pinc = mine;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, pinc, d);
             if (lane >= uint32_t(d)) pinc += o;
         }
-        if (fs)
-            for (uint32_t t = 0; t < mine; ++t) fs[nfree + pinc - mine + t] = sl[t];
+        rest = v;
+        uint32_t q = nfree + pinc - mine;
+        for (uint32_t t = 0; t < take_n; t += 4) {
+            uint32_t sv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool on = t + u < take_n;
+                const uint32_t bit = on ? 31 - __clz(rest) : 0u;
+                if (on) rest &= ~(1u << bit);
+                sv[u] = (on && fs) ? take(uint32_t(myw), bit) : kNone;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (sv[u] != kNone) fs[q++] = sv[u];
+        }
         if (take_n) {
             bm[myw] = rest;
             if (rest == 0) {
@@ -1224,38 +1244,44 @@ __global__ void __launch_bounds__(kRT) k_replay_chain(ReplayArgsCta a) {
                     }
                     need = __shfl_sync(0xFFFFFFFFu, need, 0);
                     if (need) chain_evict(a, sh, cx, need, lane);
-                    __syncwarp();
-                    // survivors of the run take slots, in list order
-                    if (a.slot_out) {
-                        for (uint32_t c = r0; c < r1; c += 32) {
-                            const uint32_t i = c + lane;
-                            bool surv = false;
-                            uint32_t x = 0, nu = kNever;
-                            if (i < r1) {
-                                x = sx[i] & ~kHit;
-                                nu = a.nuk[base + i];
-                                surv = nu == kNever ? cx.never_set(x) : cx.bit_set(nu);
-                            }
-                            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, surv);
-                            const uint32_t rank = __popc(bal & lanemask_lt_r());
-                            const uint32_t nf = sh.nfree, fr = sh.fresh;
-                            if (surv) {
-                                const uint32_t s = rank < nf ? fs[nf - 1 - rank] : fr + (rank - nf);
-                                if (nu == kNever) a.slot[size_t(k) * a.D + x] = s;
-                                else a.slot_out[cx.pos_index(nu)] = s;
-                            }
-                            __syncwarp();
-                            if (lane == 0) {
-                                const uint32_t n = __popc(bal);
-                                const uint32_t from_stack = min(n, nf);
-                                sh.nfree = nf - from_stack;
-                                sh.fresh = fr + (n - from_stack);
-                            }
-                            __syncwarp();
-                        }
-                    }
                 }
                 __syncthreads();
+                // survivors of the run take slots in list order: every warp
+                // checks its items, a block scan ranks them
+                if (a.slot_out) {
+                    for (uint32_t c = r0; c < r1; c += kRT) {
+                        const uint32_t i = c + tid;
+                        bool surv = false;
+                        uint32_t x = 0, nu = kNever;
+                        if (i < r1) {
+                            x = sx[i] & ~kHit;
+                            nu = a.nuk[base + i];
+                            surv = nu == kNever ? cx.never_set(x) : cx.bit_set(nu);
+                        }
+                        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, surv);
+                        if (lane == 0) sh.wsum[w] = __popc(bal);
+                        __syncthreads();
+                        uint32_t before = 0, n = 0;
+                        for (int q = 0; q < kRT / 32; ++q) {
+                            before += q < int(w) ? sh.wsum[q] : 0u;
+                            n += sh.wsum[q];
+                        }
+                        const uint32_t rank = before + __popc(bal & lanemask_lt_r());
+                        const uint32_t nf = sh.nfree, fr = sh.fresh;
+                        if (surv) {
+                            const uint32_t s2 = rank < nf ? fs[nf - 1 - rank] : fr + (rank - nf);
+                            if (nu == kNever) a.slot[size_t(k) * a.D + x] = s2;
+                            else a.slot_out[cx.pos_index(nu)] = s2;
+                        }
+                        __syncthreads();
+                        if (tid == 0) {
+                            const uint32_t from_stack = min(n, nf);
+                            sh.nfree = nf - from_stack;
+                            sh.fresh = fr + (n - from_stack);
+                        }
+                        __syncthreads();
+                    }
+                }
             }
         }
         // misses report the slot they hold at the END of the step (evicted
