@@ -37,9 +37,13 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace lsg {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -159,6 +163,7 @@ struct LoopArgs {
     uint32_t* gitems;                // [6][B] per-item arrays when they do not fit smem
     unsigned long long* prof;        // [8] per-phase cycles (LSG_PROFILE) or null
     int dbg_skip;                    // timing experiments only (LSG_DEBUG_SKIP)
+    uint32_t* nb;                    // [D] overlapped loop: the latest batch each id was classified in, or null
 };
 
 struct Shared {
@@ -193,6 +198,7 @@ struct Small {
     uint32_t rq[kMaxN];             // G: recipient of each rank in a round
     uint32_t win_base;              // I1: first bucket word of the window
     uint32_t win[kMaxN][kWinWords]; // I1: bucket bits aggregated per step
+    uint32_t stamp, conflict;       // (overlapped loop only; unused here)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -207,7 +213,8 @@ __device__ __forceinline__ uint32_t key_step(const LoopArgs& a, uint32_t pk) {
     return a.B == 1 ? pk : uint32_t(__umul64hi(pk, a.bdiv));
 }
 
-__device__ __forceinline__ void set_key(const LoopArgs& a, Small& sm, uint32_t k, uint32_t x, uint32_t pk) {
+template <class SM>
+__device__ __forceinline__ void set_key(const LoopArgs& a, SM& sm, uint32_t k, uint32_t x, uint32_t pk) {
     // one word per resident: (next-use step, rank in that step's sorted batch)
     a.key[size_t(k) * a.D + x] = pk;
     const uint32_t nu = pk == kNever ? kNever : key_step(a, pk), rank = pk - nu * a.B;
@@ -223,13 +230,18 @@ __device__ __forceinline__ void set_key(const LoopArgs& a, Small& sm, uint32_t k
     }
 }
 
-__device__ __forceinline__ void drop(const LoopArgs& a, uint32_t k, uint32_t x) {
+// with the overlapped loop (a.nb), a holder mask that changes for an id of
+// the next, already classified batch invalidates that classification
+template <class SM>
+__device__ __forceinline__ void drop(const LoopArgs& a, SM& sm, uint32_t k, uint32_t x) {
     a.key[size_t(k) * a.D + x] = kNone;
     atomicAnd(&a.hm[x], ~(1u << k));
+    if (a.nb && __ldcg(&a.nb[x]) == sm.stamp) sm.conflict = 1;
 }
 
 // Remove the `need` largest (key, id) residents of node k. Whole warp.
-__device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t need, uint32_t lane,
+template <class SM>
+__device__ void evict_walk(const LoopArgs& a, SM& sm, uint32_t k, uint32_t need, uint32_t lane,
                            uint32_t g) {
     const uint32_t lt = lanemask_lt();
     while (need > 0) {
@@ -251,7 +263,7 @@ __device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t ne
                         word &= ~(1u << bit);
                         const uint32_t x = uint32_t(hw) * 32 + bit;
                         if (lane == 0) {
-                            drop(a, k, x);
+                            drop(a, sm, k, x);
                             atomicAnd(&bm[hw], ~(1u << bit));
                         }
                         --need;
@@ -328,7 +340,7 @@ __device__ void evict_walk(const LoopArgs& a, Small& sm, uint32_t k, uint32_t ne
             for (uint32_t t2 = 0; t2 < take; ++t2) {
                 const uint32_t bit = __ffs(rest) - 1;
                 rest &= rest - 1;
-                drop(a, k, cand[wi2 * 32 + bit]);
+                drop(a, sm, k, cand[wi2 * 32 + bit]);
             }
             if (wi2 < nwords && (rest != word || past)) bw[wi2] = rest;
             left = left || (__ballot_sync(0xFFFFFFFFu, rest != 0) != 0);
@@ -1167,6 +1179,787 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
         for (int q = 0; q < 10; ++q) a.prof[q] = pacc[q];
 }
 
+// ---------------------------------------------------------------------------
+// K6o: the step loop with the serial multi-holder pass OVERLAPPED (N <= 8,
+// b < 2048, B <= 4096, remap on; clairvoyant). Warp 0 (team D) runs the
+// packed multi-holder chain D of step g+1 while warps 1-15 (team P) run the
+// buffer-side phases E..I of step g and then classify step g+2 (A..C):
+//
+//   team D:  D(g)   | D(g+1)              | D(g+2) ...
+//   team P:  E..I(g-1), A..C(g+1) | E..I(g), A..C(g+2) | ...
+//
+// Step g+1 is classified before I(g) has advanced the buffers, i.e. against
+// holder masks one step old. Only ids of batch g+1 whose mask I(g) changes
+// can alter that classification: an insert or a drop of such an id (an id in
+// both batches at an epoch boundary, or an eviction reaching next-step keys)
+// is detected through a per-id stamp of the latest classified batch, and then
+// step g+1 is classified and resolved again after I(g) (once per epoch
+// boundary at most, in practice). Per-step arrays are double-buffered by
+// step parity; the teams hand off through shared-memory step counters
+// (release/acquire at CTA scope), team P synchronises on named barrier 1.
+struct OvPar {  // per step parity
+    uint32_t tot[kMaxN];   // singles per node
+    uint32_t mtot[kMaxN];  // multi assigned per node (D)
+    uint32_t nmulti;
+    uint32_t cf;           // I(g-1) found this batch's masks changed
+};
+
+struct SmallOv {
+    uint32_t wcnt[kWarps][kMaxN];
+    uint32_t cm[kWarps][kMaxN];
+    uint32_t wmul[kWarps];
+    uint32_t wfet[kWarps];
+    uint32_t size[kMaxN];
+    uint32_t free_pre[kMaxN + 1];
+    uint32_t lenk[kMaxN];
+    uint32_t fcnt[kMaxN];
+    uint32_t outk[kMaxN], ink[kMaxN];
+    uint32_t noff[kMaxN + 1];
+    uint32_t bsize[kMaxN];
+    uint32_t top[kMaxN];
+    uint32_t inftop[kMaxN];
+    uint32_t infcnt[kMaxN];
+    uint32_t nfetch, nmoves;
+    alignas(16) uint32_t stg[2][32][kMaxN];
+    uint32_t dmv[kMaxN][kDmv];
+    uint32_t rq[kMaxN];
+    uint32_t win[kMaxN][kWinWords];
+    uint32_t stamp, conflict;
+    OvPar par[2];
+    // team hand-off counters (monotone): steps classified, resolved (D
+    // final), buffer-advanced, speculative-D-finished-on-conflict, re-classified
+    volatile uint32_t ac_cnt, d_cnt, i_cnt, spec_cnt, redo_cnt;
+};
+
+// The teams run on the two SMs of a thread-block cluster: team D (warp 0 of
+// CTA 0; no other warp shares its scheduler) and team C (CTA 0's 12 warps
+// on the other three schedulers, classifying each step in CTA 0's shared
+// memory and copying it over), and team P (all 16 warps of CTA 1), whose
+// per-step arrays and hand-off counters live in CTA 1's shared memory.
+// Teams D and C reach team P's state through distributed shared memory.
+constexpr uint32_t kPWarps = kWarps, kPThreads = kPWarps * 32;
+// team C (classification): CTA 0's 12 warps that do not share warp 0's
+// scheduler (warp w issues on SMSP w % 4)
+constexpr uint32_t kCWarps = 12, kCThreads = kCWarps * 32;
+
+__device__ __forceinline__ void bar_p() { asm volatile("bar.sync 1, %0;" ::"n"(kPThreads) : "memory"); }
+__device__ __forceinline__ void bar_c() { asm volatile("bar.sync 2, %0;" ::"n"(kCThreads) : "memory"); }
+__device__ __forceinline__ void wait_ge(volatile uint32_t* c, uint32_t v) {
+    while (*c < v) __nanosleep(20);
+    __threadfence();  // cluster-visible ordering of the partner's writes (DSMEM and global)
+}
+__device__ __forceinline__ void publish(volatile uint32_t* c, uint32_t v) {
+    __threadfence();
+    *c = v;
+}
+
+struct OvBufs {
+    uint32_t *sx, *snu, *smask, *sinfo, *pre, *fin;
+};
+
+// A..C of step g by team C (CTA 0, 12 warps): load + classify + ranks, exact
+// S_k(j) rows of the multi items for D (global, parity buffer)
+__device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, const OvBufs& sr, OvPar& pp,
+                            uint32_t* smul, uint32_t* dsx, uint32_t* dpre, uint32_t g, uint32_t pw, uint32_t lane) {
+    // sm, s: team C's own scratch and step arrays (local shared memory);
+    // sr / pp: team P's arrays (DSMEM), filled by one coalesced copy at the end
+    const uint32_t N = a.N, b = a.b;
+    const uint32_t lt = lanemask_lt();
+    const uint32_t i = g / a.S, t = g % a.S;
+    const uint32_t lo = t * a.B, len = min(a.B, a.keep - lo);
+    const uint32_t* row = a.trace + size_t(a.order[i]) * a.keep + lo;
+    const uint32_t* pkrow = a.nr + size_t(i) * a.keep + lo;
+    const uint32_t R = ((len + kCThreads - 1) / kCThreads) * 32;
+    const uint32_t j0 = pw * R, j1 = min(j0 + R, len);
+    if (lane < kMaxN) sm.wcnt[pw][lane] = 0;
+    uint32_t wm = 0;
+#pragma unroll 4
+    for (uint32_t j = j0 + lane; j < j1; j += 32) {
+        const uint32_t x = row[j];
+        s.sx[j] = x;
+        s.snu[j] = pkrow[j];
+        a.nb[x] = g;  // this batch's classification is checked by I(g-1)
+    }
+    __syncwarp();
+#pragma unroll 4
+    for (uint32_t j = j0 + lane; j < j1; j += 32) s.smask[j] = __ldcg(&a.hm[s.sx[j]]);
+    __syncwarp();
+    for (uint32_t c = j0; c < j0 + R; c += 32) {
+        const uint32_t j = c + lane;
+        const bool valid = j < j1;
+        const uint32_t m = valid ? s.smask[j] : 0u;
+        const uint32_t hc = __popc(m);
+        const bool single = valid && hc == 1, multi = valid && hc >= 2;
+        const uint32_t h = single ? __ffs(m) - 1 : 0;
+        if (lane < kMaxN) sm.cm[pw][lane] = 0;
+        __syncwarp();
+        const uint32_t grp = __match_any_sync(0xFFFFFFFFu, single ? h : 0x100u + lane);
+        if (single && lane == uint32_t(__ffs(grp) - 1)) sm.cm[pw][h] = grp;
+        __syncwarp();
+        if (single) s.sinfo[j] = sm.wcnt[pw][h] + __popc(grp & lt);
+        const uint32_t mb = __ballot_sync(0xFFFFFFFFu, multi);
+        if (multi) {
+            s.sinfo[j] = wm + __popc(mb & lt);
+            uint32_t mm = m;
+            while (mm) {
+                const uint32_t k = __ffs(mm) - 1;
+                mm &= mm - 1;
+                smul[size_t(j) * N + k] = sm.wcnt[pw][k] + __popc(sm.cm[pw][k] & lt);
+            }
+        }
+        __syncwarp();
+        if (single && lane == uint32_t(__ffs(grp) - 1)) sm.wcnt[pw][h] += __popc(grp);
+        wm += __popc(mb);
+        __syncwarp();
+    }
+    if (lane == 0) sm.wmul[pw] = wm;
+    bar_c();
+    // B: scans over the P warps (warp k: node k; the last warp: multi)
+    for (uint32_t k = pw; k < N; k += kCWarps) {
+        const uint32_t v = lane < kCWarps ? sm.wcnt[lane][k] : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= uint32_t(d)) inc += o;
+        }
+        if (lane < kCWarps) sm.wcnt[lane][k] = inc - v;
+        if (lane == 31) pp.tot[k] = inc;
+    }
+    if (pw == kCWarps - 1) {
+        const uint32_t v = lane < kCWarps ? sm.wmul[lane] : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+            if (lane >= uint32_t(d)) inc += o;
+        }
+        if (lane < kCWarps) sm.wmul[lane] = inc - v;
+        if (lane == 31) pp.nmulti = inc;
+    }
+    bar_c();
+    // C: global ranks; exact S_k(j) rows of the multi items (16-bit packed)
+    for (uint32_t j = j0 + lane; j < j1; j += 32) {
+        const uint32_t m = s.smask[j];
+        const uint32_t hc = __popc(m);
+        if (hc == 1) {
+            s.sinfo[j] += sm.wcnt[pw][__ffs(m) - 1];
+        } else if (hc >= 2) {
+            const uint32_t mi = sm.wmul[pw] + s.sinfo[j];
+            s.sinfo[j] = mi;
+            s.pre[mi] = j;
+        }
+    }
+    __syncwarp();
+    {
+        const uint32_t mb0 = sm.wmul[pw];
+        const uint32_t mcnt = (pw + 1 < kCWarps ? sm.wmul[pw + 1] : pp.nmulti) - mb0;
+        for (uint32_t q = lane; q < mcnt; q += 32) {
+            const uint32_t mi = mb0 + q, j = s.pre[mi], m = s.smask[j];
+            const uint32_t* sm_row = smul + size_t(j) * N;
+            uint32_t tk[8];
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k) tk[k] = (k < N && ((m >> k) & 1u)) ? __ldcg(&sm_row[k]) : 0u;
+#pragma unroll
+            for (uint32_t k = 0; k < 8; ++k)
+                tk[k] = ((k < N && ((m >> k) & 1u)) ? min(b, tk[k] + sm.wcnt[pw][k]) : b) << 4 | k;
+            reinterpret_cast<uint4*>(dsx)[mi] =
+                make_uint4(tk[0] | tk[1] << 16, tk[2] | tk[3] << 16, tk[4] | tk[5] << 16, tk[6] | tk[7] << 16);
+            dpre[mi] = j;  // the multi list for team D, in global memory (no DSMEM on its chain)
+        }
+    }
+    bar_c();
+    // the classified step to team P's shared memory (16-byte DSMEM stores)
+    const uint32_t ctid = pw * 32 + lane, nm = pp.nmulti;
+    const uint32_t len4 = (len + 3) / 4, nm4 = (nm + 3) / 4;
+    for (uint32_t q = ctid; q < 4 * len4 + nm4; q += kCThreads) {
+        const uint32_t arr = q < 4 * len4 ? q / len4 : 4, e = (q < 4 * len4 ? q - arr * len4 : q - 4 * len4) * 4;
+        const uint32_t* src = arr == 0 ? s.sx : arr == 1 ? s.snu : arr == 2 ? s.smask : arr == 3 ? s.sinfo : s.pre;
+        uint32_t* dst = arr == 0 ? sr.sx : arr == 1 ? sr.snu : arr == 2 ? sr.smask : arr == 3 ? sr.sinfo : sr.pre;
+        *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(src + e);
+    }
+    __threadfence_block();
+    bar_c();
+}
+
+// D of one step by warp 0: the packed register chain of k_plan_loop. Inputs
+// from global memory (the multi list and the packed rows), outputs into team
+// D's own shared memory (res[mi] = the chain's minimum key, or kSent; mtot);
+// team P applies them to its lists (ov_apply).
+__device__ void ov_resolve(const LoopArgs& a, SmallOv& sm, const uint32_t* dsx, const uint32_t* dpre, uint32_t nm,
+                           uint32_t* res, uint32_t* mtot, uint32_t lane) {
+    const uint32_t N = a.N, b = a.b;
+    uint32_t M01 = 0, M23 = 0, M45 = 0, M67 = 0;
+    const uint32_t kSent = (b << 4) - 1u;
+    const uint32_t kSent2 = kSent | kSent << 16;
+    (void)dpre;
+    auto stage = [&](uint32_t base, uint32_t buf) {
+        const uint32_t cnt = min(32u, nm - base);
+        const uint4* src = reinterpret_cast<const uint4*>(dsx) + base;
+        uint4* dst4 = reinterpret_cast<uint4*>(&sm.stg[buf][0][0]);
+        if (lane < cnt) {
+            const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst4 + lane));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + lane));
+        } else {
+            const uint32_t p = b << 4;
+            dst4[lane] = make_uint4(p | (p | 1) << 16, (p | 2) | (p | 3) << 16, (p | 4) | (p | 5) << 16,
+                                    (p | 6) | (p | 7) << 16);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    if (nm) stage(0, 0);
+    for (uint32_t base = 0, buf = 0; base < nm; base += 32, buf ^= 1) {
+        if (base + 32 < nm) {
+            stage(base + 32, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        __syncwarp();
+        const uint32_t cnt = min(32u, nm - base);
+        const uint4* rows = reinterpret_cast<const uint4*>(&sm.stg[buf][0][0]);
+        uint32_t myres = kSent;
+        uint32_t v01 = 0x10001u, v23 = 0x10001u, v45 = 0x10001u, v67 = 0x10001u;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const uint4 r = rows[u];
+            const uint32_t K01 = (r.x + M01 + 0x100010u) - (v01 << 4);
+            const uint32_t K23 = (r.y + M23 + 0x100010u) - (v23 << 4);
+            const uint32_t K45 = (r.z + M45 + 0x100010u) - (v45 << 4);
+            const uint32_t K67 = (r.w + M67 + 0x100010u) - (v67 << 4);
+            M01 += 0x100010u - (v01 << 4);
+            M23 += 0x100010u - (v23 << 4);
+            M45 += 0x100010u - (v45 << 4);
+            M67 += 0x100010u - (v67 << 4);
+            const uint32_t m2 = __vimin3_u16x2(__vimin3_u16x2(K01, K23, K45), K67, kSent2);
+            const uint32_t mm = __vminu2(m2, __byte_perm(m2, 0, 0x1032));
+            v01 = __vminu2(K01 - mm, 0x10001u);
+            v23 = __vminu2(K23 - mm, 0x10001u);
+            v45 = __vminu2(K45 - mm, 0x10001u);
+            v67 = __vminu2(K67 - mm, 0x10001u);
+            myres = lane == uint32_t(u) ? (mm & 0xFFFFu) : myres;
+        }
+        M01 += 0x100010u - (v01 << 4);
+        M23 += 0x100010u - (v23 << 4);
+        M45 += 0x100010u - (v45 << 4);
+        M67 += 0x100010u - (v67 << 4);
+        if (lane < cnt) res[base + lane] = myres;
+        __syncwarp();
+    }
+    const uint32_t Mp[4] = {M01, M23, M45, M67};
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (lane == uint32_t(k) && uint32_t(k) < N) mtot[k] = ((Mp[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) >> 4;
+    __syncwarp();
+}
+
+// team P: team D's decisions for the multi items of step g into the lists
+// (node positions in fin, E's input in sinfo) — what k_plan_loop's D writes
+__device__ void ov_apply(const LoopArgs& a, const OvBufs& s, OvPar& pp, const uint32_t* dsx, const uint32_t* res_d,
+                         const uint32_t* mtot_d, uint32_t ptid) {
+    const uint32_t b = a.b, nm = pp.nmulti;
+    const uint32_t kSent = (b << 4) - 1u;
+    for (uint32_t mi = ptid; mi < nm; mi += kPThreads) {
+        const uint32_t r = res_d[mi], j = s.pre[mi];
+        if (r != kSent) {
+            const uint32_t kk = r & 15u, c = r >> 4;
+            const uint32_t Sk = reinterpret_cast<const uint16_t*>(dsx + size_t(mi) * 4)[kk] >> 4;
+            s.fin[kk * b + (c - Sk)] = j;
+            s.sinfo[j] = (c << 5) | kk;
+        } else {
+            s.sinfo[j] = 0xFFFFFFFFu;
+        }
+    }
+    if (ptid < a.N) pp.mtot[ptid] = mtot_d[ptid];
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
+    extern __shared__ __align__(16) uint32_t dyn[];
+    __shared__ SmallOv sm_local;
+    cg::cluster_group cl = cg::this_cluster();
+    const uint32_t crank = cl.block_rank();
+    // team P's state (CTA 1), as seen from either CTA
+    SmallOv& sm = *cl.map_shared_rank(&sm_local, 1);
+    uint32_t* pdyn = cl.map_shared_rank(dyn, 1);
+    OvBufs S2[2];
+    for (int p = 0; p < 2; ++p) {
+        uint32_t* b0 = pdyn + size_t(p) * 6 * a.B;
+        S2[p] = OvBufs{b0, b0 + a.B, b0 + 2 * a.B, b0 + 3 * a.B, b0 + 4 * a.B, b0 + 5 * a.B};
+    }
+    const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t N = a.N, b = a.b;
+    const uint32_t lt = lanemask_lt();
+    if (crank == 1) {
+        if (tid < kMaxN) {
+            sm_local.bsize[tid] = 0;
+            sm_local.top[tid] = 0;
+            sm_local.inftop[tid] = 0;
+            sm_local.infcnt[tid] = 0;
+        }
+        if (tid == 0) {
+            sm_local.ac_cnt = sm_local.d_cnt = sm_local.i_cnt = sm_local.spec_cnt = sm_local.redo_cnt = 0;
+            sm_local.par[0].cf = sm_local.par[1].cf = 0;
+            sm_local.conflict = 0;
+        }
+    }
+    cl.sync();
+    // global scratch by parity: smul [B][N], the D rows [B] x 16 B
+    auto smul_of = [&](uint32_t g) { return a.smul + size_t(g & 1) * a.B * N; };
+    auto dsx_of = [&](uint32_t g) { return a.sx + size_t(g & 1) * a.B * 4; };
+    auto dpre_of = [&](uint32_t g) { return a.sx + size_t(2) * a.B * 4 + size_t(g & 1) * a.B; };
+    // team D's results in CTA 0's shared memory: res [2][B], mtot [2][kMaxN]
+    uint32_t* dres = cl.map_shared_rank(dyn, 0);
+    auto res_of = [&](uint32_t g) { return dres + size_t(g & 1) * a.B; };
+    auto mtot_of = [&](uint32_t g) { return dres + size_t(2) * a.B + size_t(g & 1) * kMaxN; };
+    unsigned long long pf[12] = {}, t0 = clock64();
+    auto tick = [&](int q) {
+        if (a.prof) {
+            const unsigned long long t1 = clock64();
+            pf[q] += t1 - t0;
+            t0 = t1;
+        }
+    };
+    if (crank == 0 && w != 0 && (w & 3) != 0) {
+        // -------------------------------------------- team C (CTA 0)
+        const uint32_t cw = (w >> 2) * 3 + (w & 3) - 1;
+        // team C's step arrays: CTA 0's dynamic smem after team D's results (2B + 64 words)
+        uint32_t* c0 = dyn + size_t(2) * a.B + 2 * kMaxN;
+        const OvBufs SC{c0, c0 + a.B, c0 + 2 * a.B, c0 + 3 * a.B, c0 + 4 * a.B, nullptr};
+        ov_classify(a, sm_local, SC, S2[0], sm.par[0], smul_of(0), dsx_of(0), dpre_of(0), 0, cw, lane);
+        if (cw == 0 && lane == 0) publish(&sm.ac_cnt, 1);
+        for (uint32_t h = 1; h <= a.T; ++h) {
+            // classify step h once I(h-2) is done (its parity buffers are free,
+            // the masks one step old); first the verdict of I(h-2) on step h-1
+            if (h >= 2) {
+                if (cw == 0) wait_ge(&sm.i_cnt, h - 1);
+                bar_c();
+                if (sm.par[(h - 1) & 1].cf) {
+                    if (cw == 0) wait_ge(&sm.spec_cnt, h);  // team D is done with the speculative D(h-1)
+                    bar_c();
+                    ov_classify(a, sm_local, SC, S2[(h - 1) & 1], sm.par[(h - 1) & 1], smul_of(h - 1),
+                                dsx_of(h - 1), dpre_of(h - 1), h - 1, cw, lane);
+                    if (cw == 0 && lane == 0) publish(&sm.redo_cnt, h);
+                }
+            }
+            tick(0);
+            if (h < a.T) {
+                ov_classify(a, sm_local, SC, S2[h & 1], sm.par[h & 1], smul_of(h), dsx_of(h), dpre_of(h), h, cw, lane);
+                if (cw == 0 && lane == 0) publish(&sm.ac_cnt, h + 1);
+            }
+            tick(1);
+        }
+        if (a.prof && cw == 0 && lane == 0)
+            for (int q = 0; q < 2; ++q) a.prof[20 + q] = pf[q];
+    }
+    if (crank == 0) {
+        if (w == 0) {
+            // -------------------------------------------- team D (CTA 0)
+            for (uint32_t g = 0; g < a.T; ++g) {
+                wait_ge(&sm.ac_cnt, g + 1);  // every lane: a one-lane spin left the warp diverged through the chain
+                tick(0);
+                ov_resolve(a, sm_local, dsx_of(g), dpre_of(g), sm.par[g & 1].nmulti, dyn + size_t(g & 1) * a.B,
+                           dyn + size_t(2) * a.B + size_t(g & 1) * kMaxN, lane);
+                tick(1);
+                if (g > 0) {  // the verdict of I(g-1) on this step's classification
+                    wait_ge(&sm.i_cnt, g);
+                    tick(2);
+                    if (sm.par[g & 1].cf) {
+                        if (lane == 0) publish(&sm.spec_cnt, g + 1);
+                        wait_ge(&sm.redo_cnt, g + 1);
+                        ov_resolve(a, sm_local, dsx_of(g), dpre_of(g), sm.par[g & 1].nmulti,
+                                   dyn + size_t(g & 1) * a.B, dyn + size_t(2) * a.B + size_t(g & 1) * kMaxN, lane);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) publish(&sm.d_cnt, g + 1);
+                tick(3);
+            }
+            if (a.prof && lane == 0)
+                for (int q = 0; q < 4; ++q) a.prof[q] = pf[q];
+        }
+        cl.sync();  // team P's shared memory stays alive until team D is done with it
+        return;
+    }
+    // ---------------------------------------------------- team P (CTA 1)
+    {
+    SmallOv& sm = sm_local;  // its own shared memory, addressed directly
+    for (int p = 0; p < 2; ++p) {
+        uint32_t* b0 = dyn + size_t(p) * 6 * a.B;
+        S2[p] = OvBufs{b0, b0 + a.B, b0 + 2 * a.B, b0 + 3 * a.B, b0 + 4 * a.B, b0 + 5 * a.B};
+    }
+    const uint32_t pw = w, ptid = tid;
+    size_t gbase = 0;
+    for (uint32_t g = 0; g < a.T; ++g) {
+        const OvBufs& s = S2[g & 1];
+        OvPar& pp = sm.par[g & 1];
+        const uint32_t len = min(a.B, a.keep - (g % a.S) * a.B);
+        const uint32_t R = ((len + kPThreads - 1) / kPThreads) * 32;
+        const uint32_t j0 = pw * R, j1 = min(j0 + R, len);
+        tick(3);
+        if (ptid == 0) wait_ge(&sm.d_cnt, g + 1);  // D(g) resolved (final); one waiter, the barrier orders the rest
+        bar_p();
+        ov_apply(a, s, pp, dsx_of(g), res_of(g), mtot_of(g), ptid);
+        bar_p();
+        tick(0);
+        if (g + 2 < a.T && !(a.dbg_skip & 8)) {  // batch g+2's rows into L2 for its classification after I(g)
+            const uint32_t g2 = g + 2, i2 = g2 / a.S, t2 = g2 % a.S;
+            const uint32_t lo2 = t2 * a.B, len2 = min(a.B, a.keep - lo2);
+            const char* r0 = reinterpret_cast<const char*>(a.trace + size_t(a.order[i2]) * a.keep + lo2);
+            const char* r1 = reinterpret_cast<const char*>(a.nr + size_t(i2) * a.keep + lo2);
+            for (uint32_t off = ptid * 128; off < len2 * 4; off += kPThreads * 128) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(r0 + off));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(r1 + off));
+            }
+        }
+        // ------------ E: hits/positions for singles; fetch ranks
+        uint32_t wf = 0;
+        for (uint32_t c = j0; c < j0 + R; c += 32) {
+            const uint32_t j = c + lane;
+            const bool valid = j < j1;
+            bool fetch = false;
+            if (valid) {
+                const uint32_t m = s.smask[j];
+                const uint32_t hc = __popc(m);
+                if (hc == 1) {
+                    const uint32_t h = __ffs(m) - 1;
+                    const uint32_t S = s.sinfo[j];
+                    const uint32_t* mp = s.fin + h * b;
+                    uint32_t lo2 = 0, hi2 = pp.mtot[h];
+                    while (lo2 < hi2) {
+                        const uint32_t mid = (lo2 + hi2) >> 1;
+                        if (mp[mid] < j) lo2 = mid + 1; else hi2 = mid;
+                    }
+                    const uint32_t pos = S + lo2;
+                    if (pos < b) s.sinfo[j] = (h << 24) | pos;
+                    else fetch = true;
+                } else if (hc >= 2) {
+                    const uint32_t r = s.sinfo[j];
+                    if (r != 0xFFFFFFFFu) s.sinfo[j] = ((r & 31) << 24) | (r >> 5);
+                    else fetch = true;
+                } else {
+                    fetch = true;
+                }
+            }
+            const uint32_t fbal = __ballot_sync(0xFFFFFFFFu, fetch);
+            if (fetch) s.sinfo[j] = kFetch - (wf + __popc(fbal & lt));
+            wf += __popc(fbal);
+        }
+        if (lane == 0) sm.wfet[pw] = wf;
+        if (ptid < N) sm.size[ptid] = min(b, pp.tot[ptid] + pp.mtot[ptid]);
+        bar_p();
+        if (pw == 0) {
+            const uint32_t v = lane < kPWarps ? sm.wfet[lane] : 0u;
+            uint32_t inc = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                if (lane >= uint32_t(d)) inc += o;
+            }
+            if (lane < kPWarps) sm.wfet[lane] = inc - v;
+            const uint32_t F = __shfl_sync(0xFFFFFFFFu, inc, 31);
+            const uint32_t fr = lane < N ? b - sm.size[lane] : 0;
+            uint32_t pinc = fr;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, pinc, d);
+                if (lane >= uint32_t(d)) pinc += o;
+            }
+            const uint32_t pex = pinc - fr;
+            if (lane < N) {
+                sm.free_pre[lane] = pex;
+                const uint32_t got = F > pex ? min(fr, F - pex) : 0u;
+                sm.fcnt[lane] = got;
+                sm.lenk[lane] = sm.size[lane] + got;
+            }
+            if (lane == N - 1) sm.free_pre[N] = pinc;
+            if (lane == 0) sm.nfetch = F;
+            const uint32_t totfree = __shfl_sync(0xFFFFFFFFu, pinc, N - 1);
+            if (lane == 0 && F > totfree) atomicOr(a.status, 8u);
+        }
+        bar_p();
+        tick(4);
+        // ------------ F: pre-balance lists [hits in batch order][fetches]
+        for (uint32_t j = j0 + lane; j < j1; j += 32) {
+            const uint32_t v = s.sinfo[j];
+            if (v >= kFetch - 65536u) {
+                const uint32_t f = sm.wfet[pw] + (kFetch - v);
+                uint32_t k = 0;
+                while (k + 1 < N && sm.free_pre[k + 1] <= f) ++k;
+                const uint32_t pos = sm.size[k] + (f - sm.free_pre[k]);
+                s.pre[k * b + pos] = j;
+            } else {
+                s.pre[(v >> 24) * b + (v & 0xFFFFFF)] = j | kHit;
+            }
+        }
+        bar_p();
+        tick(5);
+        // ------------ G: balance on counts (closed form, as k_plan_loop)
+        if (pw == 0) {
+            uint32_t c = lane < N ? sm.fcnt[lane] : 0u;
+            if (a.fb && lane < N) a.fb[size_t(g) * N + lane] = c;
+            uint32_t outc = 0, inn = 0, nmv = 0;
+            const bool in = lane < N;
+            bool rounds = a.balance;
+            if (a.balance) {
+                const uint32_t mx = __reduce_max_sync(0xFFFFFFFFu, in ? c : 0u);
+                const uint32_t mn = __reduce_min_sync(0xFFFFFFFFu, in ? c : 0xFFFFFFFFu);
+                const uint32_t F = __reduce_add_sync(0xFFFFFFFFu, in ? c : 0u);
+                const uint32_t L = F / N;
+                const uint32_t dm = __reduce_add_sync(0xFFFFFFFFu, in && c > L + 1 ? c - L - 1 : 0u);
+                const uint32_t rm = __reduce_add_sync(0xFFFFFFFFu, in && c < L ? L - c : 0u);
+                const uint32_t mv = max(dm, rm), od = mv - dm, orr = mv - rm;
+                uint32_t* urq = a.dmoves + size_t(N) * a.B;  // recipient units (D's staging is busy here)
+                if (mx - mn <= 1) {
+                    rounds = false;
+                } else if (mv <= 2u * 32u * kMaxN) {
+                    rounds = false;
+                    uint32_t t = 0;
+                    for (uint32_t l = mn; l <= L; ++l) {
+                        const uint32_t br = __ballot_sync(0xFFFFFFFFu, in && c <= l);
+                        const uint32_t lim = l < L ? 32u : orr;
+                        const uint32_t rk = __popc(br & lt);
+                        if (in && c <= l && rk < lim) {
+                            urq[t + rk] = lane | ((l - c) << 8);
+                            ++inn;
+                        }
+                        t += min(uint32_t(__popc(br)), lim);
+                    }
+                    __syncwarp();
+                    t = 0;
+                    for (uint32_t l = mx; l >= L + 1; --l) {
+                        const uint32_t bd = __ballot_sync(0xFFFFFFFFu, in && c >= l);
+                        const uint32_t lim = l > L + 1 ? 32u : od;
+                        const uint32_t rk = __popc(bd & lt);
+                        if (in && c >= l && rk < lim) {
+                            const uint32_t rq = urq[t + rk];
+                            if (outc < kDmv) sm.dmv[lane][outc] = rq;
+                            else a.dmoves[size_t(lane) * a.B + outc] = rq;
+                            ++outc;
+                        }
+                        t += min(uint32_t(__popc(bd)), lim);
+                    }
+                    nmv = mv;
+                    c = c - outc + inn;
+                }
+            }
+            while (rounds) {
+                const uint32_t M = __reduce_max_sync(0xFFFFFFFFu, lane < N ? c : 0u);
+                const uint32_t m = __reduce_min_sync(0xFFFFFFFFu, lane < N ? c : 0xFFFFFFFFu);
+                if (M - m <= 1) break;
+                const uint32_t dmk = __ballot_sync(0xFFFFFFFFu, lane < N && c == M);
+                const uint32_t rmk = __ballot_sync(0xFFFFFFFFu, lane < N && c == m);
+                const uint32_t n = min(__popc(dmk), __popc(rmk));
+                const bool isd = (dmk >> lane) & 1u, isr = (rmk >> lane) & 1u;
+                const uint32_t rk = __popc((isd ? dmk : rmk) & lt);
+                if (isr && rk < n) {
+                    sm.rq[rk] = lane | (inn << 8);
+                    ++c;
+                    ++inn;
+                }
+                __syncwarp();
+                if (isd && rk < n) {
+                    const uint32_t rq = sm.rq[rk];
+                    if (outc < kDmv) sm.dmv[lane][outc] = rq;
+                    else a.dmoves[size_t(lane) * a.B + outc] = rq;
+                    --c;
+                    ++outc;
+                }
+                __syncwarp();
+                nmv += n;
+            }
+            if (lane < N) {
+                sm.outk[lane] = outc;
+                sm.ink[lane] = inn;
+            }
+            if (lane == 0) sm.nmoves = nmv;
+        }
+        bar_p();
+        if (a.balance && sm.nmoves) {
+            for (uint32_t k = pw; k < N; k += kPWarps) {
+                const uint32_t out = sm.outk[k];
+                if (!out) continue;
+                const uint32_t L = sm.lenk[k], f0 = sm.size[k];
+                for (uint32_t c = f0; c < L; c += 32) {
+                    const uint32_t p = c + lane;
+                    const uint32_t e = p < L ? s.pre[k * b + p] : kHit;
+                    const bool isf = !(e & kHit);
+                    const uint32_t x = isf ? s.sx[e & 0xFFFF] : 0u;
+                    uint32_t rank = 0;
+                    for (uint32_t c2 = f0; c2 < L; c2 += 32) {
+                        const uint32_t p2 = c2 + lane;
+                        const uint32_t e2 = p2 < L ? s.pre[k * b + p2] : kHit;
+                        const uint32_t y = !(e2 & kHit) ? s.sx[e2 & 0xFFFF] : 0u;
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) rank += __shfl_sync(0xFFFFFFFFu, y, q) > x ? 1u : 0u;
+                    }
+                    if (isf)
+                        s.sinfo[e & 0xFFFF] = rank >= out ? kNotMoved
+                                              : rank < kDmv ? sm.dmv[k][rank] : a.dmoves[size_t(k) * a.B + rank];
+                }
+            }
+            bar_p();
+        }
+        tick(6);
+        // ------------ H: final lists + outputs
+        if (pw == 0) {
+            const uint32_t L = lane < N ? sm.lenk[lane] - sm.outk[lane] + sm.ink[lane] : 0;
+            uint32_t inc = L;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                if (lane >= uint32_t(d)) inc += o;
+            }
+            if (lane < N) {
+                sm.noff[lane] = inc - L;
+                a.node_off[size_t(g) * (N + 1) + lane] = inc - L;
+                if (a.fa) a.fa[size_t(g) * N + lane] = sm.fcnt[lane] - sm.outk[lane] + sm.ink[lane];
+            }
+            if (lane == N - 1) {
+                sm.noff[N] = inc;
+                a.node_off[size_t(g) * (N + 1) + N] = inc;
+                if (inc != len) atomicOr(a.status, 16u);
+            }
+        }
+        bar_p();
+        for (uint32_t k = pw; k < N; k += kPWarps) {
+            const uint32_t L = sm.lenk[k], out = sm.outk[k];
+            uint32_t shift = 0;
+            for (uint32_t c = 0; c < L; c += 32) {
+                const uint32_t p = c + lane;
+                uint32_t e = 0;
+                bool moved = false;
+                if (p < L) {
+                    e = s.pre[k * b + p];
+                    moved = out && !(e & kHit) && s.sinfo[e & 0xFFFF] != kNotMoved;
+                }
+                const uint32_t mbal = __ballot_sync(0xFFFFFFFFu, moved);
+                if (p < L) {
+                    uint32_t dst;
+                    if (moved) {
+                        const uint32_t mvv = s.sinfo[e & 0xFFFF];
+                        const uint32_t r = mvv & 0xFF, q = mvv >> 8;
+                        dst = sm.noff[r] + (sm.lenk[r]) + q;
+                        s.fin[dst] = (e & 0xFFFF) | (r << 16);
+                    } else {
+                        dst = sm.noff[k] + p - (shift + __popc(mbal & lt));
+                        s.fin[dst] = (e & 0xFFFF) | (k << 16) | (e & kHit);
+                    }
+                    a.items[gbase + dst] = s.sx[e & 0xFFFF] | (e & kHit);
+                }
+                shift += __popc(mbal);
+            }
+        }
+        bar_p();
+        tick(7);
+        // ------------ I: buffer advance; changes to the masks of batch g+1
+        // (already classified) are caught by the stamp check
+        if (ptid == 0) {
+            sm.stamp = g + 1;
+            sm.conflict = 0;
+        }
+        bar_p();
+        {
+            const uint32_t wbase = (g + 1) >> 5;
+            for (uint32_t q = ptid; q < N * kWinWords; q += kPThreads) sm.win[q / kWinWords][q % kWinWords] = 0;
+            bar_p();
+            for (uint32_t p = ptid; p < len; p += kPThreads) {
+                const uint32_t e = s.fin[p];
+                if (!(e & kHit)) continue;
+                const uint32_t j = e & 0xFFFF, k = (e >> 16) & 0xFF;
+                const uint32_t x = s.sx[j], pk = s.snu[j];
+                const uint32_t nu = pk == kNever ? kNever : key_step(a, pk), rank = pk - nu * a.B;
+                const uint32_t wd = nu >> 5;
+                if (nu != kNever && wd >= wbase && wd - wbase < kWinWords) {
+                    a.key[size_t(k) * a.D + x] = pk;
+                    atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
+                    atomicOr(&sm.win[k][wd - wbase], 1u << (nu & 31));
+                } else {
+                    set_key(a, sm, k, x, pk);
+                }
+            }
+            bar_p();
+            for (uint32_t q = ptid; q < N * kWinWords; q += kPThreads) {
+                const uint32_t k = q / kWinWords, wd = q % kWinWords;
+                const uint32_t v = sm.win[k][wd];
+                if (v) {
+                    atomicOr(&a.nz[size_t(k) * a.nzw + wbase + wd], v);
+                    atomicMax(&sm.top[k], (wbase + wd) * 32 + 31 - __clz(v));
+                }
+            }
+            bar_p();
+        }
+        tick(8);
+        for (uint32_t k = pw; k < N; k += kPWarps) {
+            const uint32_t begin = sm.noff[k] + sm.size[k], end = sm.noff[k + 1];
+            bool pending = false;
+            auto flush = [&]() {
+                uint32_t need = 0;
+                if (lane == 0) need = sm.bsize[k] > a.C ? sm.bsize[k] - a.C : 0u;
+                need = __shfl_sync(0xFFFFFFFFu, need, 0);
+                __syncwarp();
+                if (need) evict_walk(a, sm, k, need, lane, g);
+                __syncwarp();
+                pending = false;
+            };
+            for (uint32_t c = begin; c < end; c += 32) {
+                const uint32_t p = c + lane;
+                const bool valid = p < end;
+                uint32_t j = 0;
+                bool res = false;
+                if (valid) {
+                    j = s.fin[p] & 0xFFFF;
+                    res = (s.smask[j] >> k) & 1u;
+                }
+                const uint32_t vbal = __ballot_sync(0xFFFFFFFFu, valid);
+                const uint32_t rbal = __ballot_sync(0xFFFFFFFFu, res);
+                uint32_t done = 0;
+                while (done != vbal) {
+                    const uint32_t first = __ffs(vbal & ~done) - 1;
+                    const bool hitrun = (rbal >> first) & 1u;
+                    const uint32_t same = hitrun ? rbal : (vbal & ~rbal);
+                    const uint32_t after = (~same) & vbal & ~((1u << first) - 1u) & ~(1u << first);
+                    const uint32_t stop = after ? __ffs(after) - 1 : 32u;
+                    const uint32_t run = (stop == 32 ? 0xFFFFFFFFu : ((1u << stop) - 1u)) & ~((1u << first) - 1u) & vbal;
+                    const bool mine = (run >> lane) & 1u;
+                    if (hitrun && pending) flush();
+                    if (mine) {
+                        const uint32_t x = s.sx[j];
+                        set_key(a, sm, k, x, s.snu[j]);
+                        if (!hitrun) {
+                            atomicOr(&a.hm[x], 1u << k);
+                            if (__ldcg(&a.nb[x]) == g + 1) sm.conflict = 1;
+                        }
+                    }
+                    __syncwarp();
+                    if (!hitrun) {
+                        if (lane == 0) sm.bsize[k] += __popc(run);
+                        pending = true;
+                    }
+                    __syncwarp();
+                    done |= run;
+                }
+            }
+            if (pending) flush();
+        }
+        bar_p();
+        tick(1);
+        gbase += len;
+        // the verdict on step g+1's classification (team C re-classifies on a conflict)
+        if (g + 1 < a.T) {
+            const uint32_t cf = sm.conflict;
+            if (ptid == 0) {
+                sm.par[(g + 1) & 1].cf = cf;
+                publish(&sm.i_cnt, g + 1);
+            }
+            tick(2);
+        }
+    }
+    if (a.prof && ptid == 0)
+        for (int q = 0; q < 12; ++q) a.prof[4 + q] = pf[q];
+    }
+    cl.sync();
+}
+
 }  // namespace
 
 
@@ -1224,9 +2017,17 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
     a.hm = sc.get<uint32_t>(dm.D);
     a.nz = sc.get<uint32_t>(size_t(dm.N) * a.nzw);
     a.infbm = sc.get<uint32_t>(size_t(dm.N) * a.infw);
-    a.smul = sc.get<uint32_t>(size_t(dm.B) * dm.N);
-    a.sx = sc.get<uint32_t>(size_t(dm.B) * std::max<uint32_t>(dm.N, 8u));  // D8 rows are 8 words
-    a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B);
+    // the overlapped loop (K6o): team D resolves step g+1 while team P
+    // advances step g and classifies step g+2 (LSG_PLAN_OV=0: the plain loop)
+    const char* ov_env = std::getenv("LSG_PLAN_OV");
+    const bool ov = remap && dm.N <= 8 && dm.b < kPk16B && dm.B <= 4096 && dm.B % 4 == 0 && !profiling() &&
+                    !std::getenv("LSG_DEBUG_SKIP") && !(ov_env && ov_env[0] == '0');
+    a.smul = sc.get<uint32_t>(size_t(dm.B) * dm.N * (ov ? 2 : 1));
+    a.sx = sc.get<uint32_t>(ov ? size_t(dm.B) * 10 : size_t(dm.B) * std::max<uint32_t>(dm.N, 8u));  // D rows (+ ov: 2 parities + lists)
+    a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B + 2 * 32 * kMaxN);
+    a.nb = ov ? sc.get<uint32_t>(dm.D) : nullptr;
+    if (ov && !a.nb) return set_error(kInternal, "plan: scratch allocation failed");
+    if (ov) LSG_CUDA(cudaMemsetAsync(a.nb, 0xFF, dm.D * 4, st));
     if (!nu || !sb || !nr || !a.bm || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.dmoves)
         return set_error(kInternal, "plan: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(dm.N) * dm.D * 4, st));
@@ -1264,8 +2065,32 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
     if (!smem_items && !a.gitems) return set_error(kInternal, "plan: scratch allocation failed");
     a.prof = profiling() ? sc.get<unsigned long long>(16 + 256) : nullptr;
     a.dbg_skip = std::getenv("LSG_DEBUG_SKIP") ? std::atoi(std::getenv("LSG_DEBUG_SKIP")) : 0;
+    if (ov && std::getenv("LSG_OV_NOPF")) a.dbg_skip = 8;  // experiments: no L2 prefetch of batch g+2
     if (a.prof) LSG_CUDA(cudaMemsetAsync(a.prof, 0, (16 + 256) * 8, st));
-    if (smem_items) {
+    const bool ov_prof = ov && std::getenv("LSG_PROFILE_OV");
+    if (ov_prof) {
+        a.prof = sc.get<unsigned long long>(32);
+        if (!a.prof) return set_error(kInternal, "plan: scratch allocation failed");
+        LSG_CUDA(cudaMemsetAsync(a.prof, 0, 32 * 8, st));
+    }
+    if (ov) {
+        // two parity sets of the six per-step arrays (team D's CTA: its results, res [2][B] + mtot [2][32])
+        const size_t smem = std::max<size_t>(size_t(12) * dm.B, size_t(7) * dm.B + 2 * kMaxN + 16) * 4;
+        LSG_CUDA(cudaFuncSetAttribute(k_plan_loop_ov, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        LSG_CUDA(cudaLaunchKernelEx(&cfg, k_plan_loop_ov, a));
+    } else if (smem_items) {
         const size_t smem = exclusive_smem(size_t(6) * dm.B * 4);
         auto kern = dm.N <= 8 ? k_plan_loop<true, true> : k_plan_loop<true, false>;
         LSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -1277,6 +2102,19 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
         kern<<<1, kThreads, smem, st>>>(a);
     }
     LSG_LAUNCH_CHECK("k_plan_loop");
+    if (ov_prof) {
+        unsigned long long h[32];
+        LSG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof h, cudaMemcpyDeviceToHost, st));
+        LSG_CUDA(cudaStreamSynchronize(st));
+        const double T = double(dm.T ? dm.T : 1);
+        fprintf(stderr, "[lsg ov] team D cyc/step: wait-classified %.0f  resolve %.0f  wait-verdict %.0f  publish %.0f\n",
+                h[0] / T, h[1] / T, h[2] / T, h[3] / T);
+        fprintf(stderr, "[lsg ov] team C cyc/step: wait-verdict %.0f  classify %.0f\n", h[20] / T, h[21] / T);
+        fprintf(stderr, "[lsg ov] team P cyc/step: wait-resolved %.0f  I2 %.0f  verdict+classify %.0f  other %.0f  "
+                "E %.0f  F %.0f  G1/G2 %.0f  H %.0f  I1 %.0f\n",
+                h[4] / T, h[5] / T, h[6] / T, h[7] / T, h[8] / T, h[9] / T, h[10] / T, h[11] / T, h[12] / T);
+        a.prof = nullptr;
+    }
     if (a.prof) {
         unsigned long long h[16 + 256];
         LSG_CUDA(cudaMemcpyAsync(h, a.prof, sizeof h, cudaMemcpyDeviceToHost, st));
