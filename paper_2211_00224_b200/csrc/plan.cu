@@ -1244,12 +1244,15 @@ constexpr uint32_t kCWarps = 12, kCThreads = kCWarps * 32;
 
 __device__ __forceinline__ void bar_p() { asm volatile("bar.sync 1, %0;" ::"n"(kPThreads) : "memory"); }
 __device__ __forceinline__ void bar_c() { asm volatile("bar.sync 2, %0;" ::"n"(kCThreads) : "memory"); }
+// hand-offs between the cluster's CTAs: release/acquire at cluster scope
+// (the counters live in shared memory; partner writes are DSMEM and global)
 __device__ __forceinline__ void wait_ge(volatile uint32_t* c, uint32_t v) {
-    while (*c < v) __nanosleep(20);
-    __threadfence();  // cluster-visible ordering of the partner's writes (DSMEM and global)
+    while (*c < v) {
+    }
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
 }
 __device__ __forceinline__ void publish(volatile uint32_t* c, uint32_t v) {
-    __threadfence();
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
     *c = v;
 }
 
