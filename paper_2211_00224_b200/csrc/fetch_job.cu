@@ -64,6 +64,10 @@ namespace {
 
 constexpr int kPfTile = 8192, kPfStages = 3, kPfCtas = 32;
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -465,185 +469,303 @@ __global__ void __launch_bounds__(256) k_row_flags(FlagArgs a) {
     if (threadIdx.x == 0) a.ndefer[gi] = ndef;
 }
 
-constexpr int kFTile = 8192, kFStages = 12, kFLag = 3, kFChunk = 16, kFTail = 4;
+constexpr int kFTile = 8192, kFStages = 6, kFLag = 2, kFChunk = 16, kFTail = 4;
+constexpr unsigned kFCtasPerSm = 4;
 
 struct FusedStep {
-    const uint32_t* items;     // step's items
-    const uint32_t* slots;     // step's replay slots
-    const uint32_t* flags;     // step's row flags
-    const uint32_t* node_off;  // step's [N+1]
+    const uint32_t* items;     // job's items (job-relative: step s at base[s])
+    const uint32_t* slots;     // job's replay slots
+    const uint32_t* flags;     // job's row flags
+    const uint32_t* node_off;  // job's [ns][N+1]
+    const uint32_t* base;      // [ns] job-relative step bases
+    uint32_t N;
     unsigned char* const* bufs;
     unsigned char* const* outs;
     uint32_t k0, k1;
     uint64_t row_bytes, seed;
-    uint32_t* claim;
+    uint32_t* claim;            // [ns] tile claims per step
+    uint32_t* stored;           // [ns] tiles stored per step (a step is done when all are)
     const unsigned char* ring;  // host-tier misses (null: synthesised payload)
     uint32_t R;
     const uint32_t* ready;
     const uint32_t* seq0;
     const uint32_t* moff;       // [ns+1] job miss offsets
-    uint32_t gi;                // step index in the job
-    uint32_t* done;             // [ns] CTAs finished per step
     uint32_t* consumed;         // ring sequence numbers released
+    uint32_t gA, gB;            // the kernel's steps [gA, gB) of the job
     int skip_misses;            // misses left to k_job_misses (large synthesised rows)
 };
 
-__device__ __forceinline__ uint32_t fnode_of_row(const FusedStep& f, uint32_t r) {
-    uint32_t k = f.k0;
-    while (k + 1 < f.k1 && __ldg(&f.node_off[k + 1]) <= r) ++k;
+__device__ __forceinline__ uint32_t fnode_of_row(const uint32_t* off, uint32_t k0, uint32_t k1, uint32_t r) {
+    uint32_t k = k0;
+    while (k + 1 < k1 && __ldg(&off[k + 1]) <= r) ++k;
     return k;
 }
 
-// One training step of ranks [k0, k1): every row's 8 KiB tiles through a
-// kFStages-deep TMA pipeline per CTA (one warp; lane 0 issues the bulk
-// copies). Hit tiles: HBM slot -> shared -> batch row. Miss tiles: the ring
-// (host tier, after the row's ready flag) or the Store payload computed by
-// the warp -> shared -> batch row and, for in-place misses, the new slot.
-// Before griddepcontrol.wait the CTA already claims its first chunk and
-// issues loads for early hit rows, so the previous step's tail overlaps this
-// step's first loads; every store waits.
-__global__ void __launch_bounds__(32) k_fetch_fused(FusedStep f) {
+// Steps [gA, gB) of ranks [k0, k1) in ONE persistent launch: every row's
+// 8 KiB tiles through an S-stage TMA pipeline per CTA, split between two
+// warps so neither's instruction stream bounds the copy rate: warp 0 (the
+// producer) claims tiles and loads them — hit tiles HBM slot -> shared, miss
+// tiles from the ring (host tier, after the row's ready flag) or as the Store
+// payload computed by the warp; warp 1 (the consumer) stores each landed
+// tile to its batch row and, for in-place misses, the new slot. Stages hand
+// over through full (TMA transaction) and empty (store has read the stage)
+// mbarriers.
+//
+// CTAs claim tile chunks step after step, so a CTA that runs out of work in
+// step s starts loading step s+1 while others finish s. Ordering, with rdy =
+// the number of leading steps whose tiles are all stored (per-step counters):
+//   a hit tile of step s loads once rdy >= s, or rdy >= s-1 for an early row
+//     (its slot was not filled in step s-1) and for a miss (reads no slot);
+//   every store of step s waits for rdy >= s (step s-1's slot fills, and
+//     its reads of slots this step overwrites, are done; batch rows reused).
+// Tiles, not CTAs, are counted, so a CTA that never became resident holds
+// nothing anyone waits for; a consumer with nothing to store publishes what
+// it holds before waiting. Before griddepcontrol.wait, rdy = gA - 1: the
+// previous kernel (the previous steps, or their deferred slot writes) runs
+// at most one step behind.
+template <int S, int L>
+__global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
     extern __shared__ __align__(128) unsigned char fsm2[];
-    __shared__ __align__(8) unsigned long long bar[kFStages];
-    __shared__ unsigned char* sdst[kFStages];
-    __shared__ unsigned char* sdst2[kFStages];
-    const uint32_t lane = threadIdx.x;
-    if (lane == 0) {
-        for (int q = 0; q < kFStages; ++q) {
-            const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bq));
+    __shared__ __align__(8) unsigned long long full[S], empty[S];
+    __shared__ unsigned char* sdst[S];
+    __shared__ unsigned char* sdst2[S];
+    __shared__ int sstep[S];
+    __shared__ uint32_t s_total;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < S; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[q])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[q])));
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
+        s_total = 0xFFFFFFFFu;
     }
-    __syncwarp();
-    const uint64_t tpr = f.row_bytes / kFTile;
-    const uint32_t r0 = __ldg(&f.node_off[f.k0]);
-    const uint64_t nt = uint64_t(__ldg(&f.node_off[f.k1]) - r0) * tpr;
-    const uint64_t guide = uint64_t(gridDim.x) * 2 * kFChunk;
+    __syncthreads();
+    const uint32_t tpr = uint32_t(f.row_bytes / kFTile);
     const uint32_t s0 = f.ring ? __ldg(f.seq0) : 0u;
-    auto claim = [&](uint64_t left_hint) -> uint64_t {
-        uint32_t v = 0;
-        const uint32_t sz = left_hint > guide ? kFChunk : kFTail;
-        if (lane == 0) v = atomicAdd(f.claim, sz);
-        return (uint64_t(__shfl_sync(0xFFFFFFFFu, v, 0)) << 8) | sz;
+    const int gA = int(f.gA), gB = int(f.gB);  // (steps before gA may end in deferred slot writes: never polled)
+    auto step_tiles = [&](int s) -> uint32_t {
+        const uint32_t* o = f.node_off + size_t(s) * (f.N + 1);
+        return (__ldg(&o[f.k1]) - __ldg(&o[f.k0])) * tpr;
     };
-    uint64_t tb, te;
-    {
-        const uint64_t c = claim(nt);
-        tb = c >> 8;
-        te = min(nt, tb + (c & 0xFF));
-    }
-    uint64_t cur = ~0ull, tn = tb;
-    const unsigned char* src_row = nullptr;
-    unsigned char* dst_row = nullptr;
-    unsigned char* dst2_row = nullptr;
-    uint32_t row_flags = 0, row_id = 0;
-    bool row_hit = false, row_ready = false;
-    // next tile into stage k % kFStages; false = nothing (more) to issue now
-    auto issue = [&](uint64_t k, bool early) -> bool {
-        for (;;) {
-        if (tn >= te) {
-            if (tb >= nt) return false;
-            const uint64_t c = claim(nt - te);
-            tb = c >> 8;
-            if (tb >= nt) return false;
-            te = min(nt, tb + (c & 0xFF));
-            tn = tb;
-        }
-        const uint64_t rr = tn / tpr;
-        if (rr != cur) {
-            const uint32_t r = r0 + uint32_t(rr);
-            const uint32_t sl = __ldg(&f.slots[r]);
-            const uint32_t fl = __ldg(&f.flags[r]);
-            const bool hit = sl_hit(sl);
-            if (!hit && f.skip_misses) {  // k_job_misses writes this row: skip its tiles
-                tn = (rr + 1) * tpr;
-                continue;
-            }
-            if (early && !(hit && (fl & kRowEarly))) return false;  // wait for the previous step first
-            cur = rr;
-            const uint32_t kk = fnode_of_row(f, r);
-            row_hit = hit;
-            row_flags = fl;
-            row_id = __ldg(&f.items[r]) & ~kHit;
-            row_ready = false;
-            src_row = hit ? f.bufs[kk - f.k0] + uint64_t(sl & ~kHit) * f.row_bytes : nullptr;
-            dst_row = f.outs[kk - f.k0] + uint64_t(r - __ldg(&f.node_off[kk])) * f.row_bytes;
-            dst2_row = (!hit && sl != kNever && (fl & kRowInplace)) ? f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes
-                                                                    : nullptr;
-        }
-        break;
-        }
-        const uint64_t c = (tn - cur * tpr) * kFTile;
-        ++tn;
-        const int q = int(k % kFStages);
-        const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
-        unsigned char* st = fsm2 + q * kFTile;
-        if (row_hit || f.ring) {
-            const unsigned char* src = src_row;
-            if (!row_hit) {  // host-tier miss: its ring row, once the prefetcher published it
-                const uint32_t sq = s0 + (row_flags >> 2);
-                if (!row_ready) {
-                    if (lane == 0)
-                        while (ld_acquire(&f.ready[sq % f.R]) != sq + 1) __nanosleep(64);
-                    __syncwarp();
+    int rdy = gA - 1;
+    auto poll = [&]() -> bool {  // advance rdy over completed steps (all lanes: the warp stays converged)
+        const int r0 = rdy;
+        while (rdy >= gA && rdy < gB && ld_acquire(&f.stored[rdy]) == step_tiles(rdy)) ++rdy;
+        if (rdy != r0) asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads see those stores
+        return rdy != r0;
+    };
+    if (warp == 0) {
+        // ---------------- producer ----------------
+        const uint32_t guide = gridDim.x * 2 * kFChunk;
+        int sc = gA;
+        const uint32_t* off_s = f.node_off + size_t(sc) * (f.N + 1);
+        uint32_t r0 = __ldg(&off_s[f.k0]), bs = __ldg(&f.base[sc]);
+        uint32_t nt = step_tiles(sc), te = 0, tn = 0, cur = 0xFFFFFFFFu;
+        int cur_step = -1;
+        const unsigned char* src_row = nullptr;
+        unsigned char* dst_row = nullptr;
+        unsigned char* dst2_row = nullptr;
+        uint32_t row_flags = 0, row_id = 0;
+        bool row_hit = false, row_ready = false;
+        // the next tile's row state; 1 = ready, 0 = not yet (inputs not final), -1 = no more tiles
+        auto next = [&]() -> int {
+            for (;;) {
+                if (tn >= te) {  // a new chunk: this step's, else the next step's
+                    if (sc >= gB) return -1;
+                    uint32_t v = 0;
+                    const uint32_t sz = (nt > te ? nt - te : 0u) > guide ? kFChunk : kFTail;
+                    if (lane == 0) v = atomicAdd(&f.claim[sc], sz);
+                    const uint32_t tb = __shfl_sync(0xFFFFFFFFu, v, 0);
+                    if (tb >= nt) {
+                        if (++sc >= gB) return -1;
+                        off_s = f.node_off + size_t(sc) * (f.N + 1);
+                        r0 = __ldg(&off_s[f.k0]);
+                        bs = __ldg(&f.base[sc]);
+                        nt = step_tiles(sc);
+                        te = tn = 0;
+                        continue;
+                    }
+                    te = min(nt, tb + sz);
+                    tn = tb;
+                }
+                const uint32_t rr = tn / tpr;
+                if (rr != cur || sc != cur_step) {
+                    const uint32_t r = r0 + rr;
+                    const uint32_t sl = __ldg(&f.slots[bs + r]);
+                    const uint32_t fl = __ldg(&f.flags[bs + r]);
+                    const bool hit = sl_hit(sl);
+                    if (!hit && f.skip_misses) {  // k_job_misses writes this row: skip its tiles
+                        tn = (rr + 1) * tpr;
+                        continue;
+                    }
+                    const int need = (!hit || (fl & kRowEarly)) ? sc - 1 : sc;
+                    if (rdy < need && (!poll() || rdy < need)) return 0;
+                    cur = rr;
+                    cur_step = sc;
+                    const uint32_t kk = fnode_of_row(off_s, f.k0, f.k1, r);
+                    row_hit = hit;
+                    row_flags = fl;
+                    row_id = __ldg(&f.items[bs + r]) & ~kHit;
+                    row_ready = false;
+                    src_row = hit ? f.bufs[kk - f.k0] + uint64_t(sl & ~kHit) * f.row_bytes : nullptr;
+                    dst_row = f.outs[kk - f.k0] + uint64_t(r - __ldg(&off_s[kk])) * f.row_bytes;
+                    dst2_row = (!hit && sl != kNever && (fl & kRowInplace))
+                                   ? f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes
+                                   : nullptr;
+                }
+                if (!row_hit && f.ring && !row_ready) {  // host-tier miss: wait for the prefetcher's row
+                    uint32_t ok = 0;
+                    if (lane == 0) ok = ld_acquire(&f.ready[(s0 + (row_flags >> 2)) % f.R]) == s0 + (row_flags >> 2) + 1;
+                    if (!__shfl_sync(0xFFFFFFFFu, ok, 0)) return 0;
                     row_ready = true;
                 }
-                src = f.ring + uint64_t(sq % f.R) * f.row_bytes;
+                return 1;
             }
+        };
+        uint32_t k = 0;
+        bool waited = false, trig = false;
+        for (;;) {
+            const int n = next();
+            if (n < 0) break;
+            if (n == 0) {  // blocked on earlier steps or a ring row
+                if (!waited) {
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
+                    waited = true;
+                    rdy = max(rdy, gA);
+                } else if (!poll()) {
+                    __nanosleep(100);
+                }
+                continue;
+            }
+            const int q = int(k % S);
+            if (k >= uint32_t(S)) {  // the stage's previous store has read it
+                const unsigned eb = smem_u32(&empty[q]);
+                const uint32_t par = ((k / S) - 1) & 1;
+                uint32_t ok = 0;
+                while (!ok)
+                    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                                 : "=r"(ok) : "r"(eb), "r"(par) : "memory");
+            }
+            const uint64_t c = uint64_t(tn - cur * tpr) * kFTile;
+            const unsigned fb = smem_u32(&full[q]);
+            unsigned char* st = fsm2 + q * kFTile;
             if (lane == 0) {
-                const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(st));
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bq), "r"(kFTile));
-                asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                             ::"r"(d), "l"(src + c), "r"(kFTile), "r"(bq) : "memory");
+                sdst[q] = dst_row + c;
+                sdst2[q] = dst2_row ? dst2_row + c : nullptr;
+                sstep[q] = cur_step;
             }
-        } else {  // synthesised Store payload (store.cpp:70-80): words of this tile
-            const uint64_t w0 = (uint64_t(row_id) * f.row_bytes + c) / 8;
-            unsigned long long* sw = reinterpret_cast<unsigned long long*>(st);
+            if (row_hit || f.ring) {
+                if (lane == 0) {
+                    const unsigned char* src =
+                        row_hit ? src_row : f.ring + uint64_t((s0 + (row_flags >> 2)) % f.R) * f.row_bytes;
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(kFTile)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                                 ::"r"(smem_u32(st)), "l"(src + c), "r"(kFTile), "r"(fb) : "memory");
+                }
+            } else {  // synthesised Store payload (store.cpp:70-80): words of this tile
+                const uint64_t w0 = (uint64_t(row_id) * f.row_bytes + c) / 8;
+                unsigned long long* sw = reinterpret_cast<unsigned long long*>(st);
 #pragma unroll 4
-            for (uint32_t i = lane; i < kFTile / 8; i += 32) sw[i] = mix64(f.seed + (w0 + i + 1) * kGamma);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bq) : "memory");
+                for (uint32_t i = lane; i < kFTile / 8; i += 32) sw[i] = mix64(f.seed + (w0 + i + 1) * kGamma);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
+            }
+            ++tn;
+            ++k;
+            if (!waited && k == uint32_t(S)) {  // every stage was free: the rest waits for the previous kernel
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                waited = true;
+                rdy = max(rdy, gA);
+            }
+            if (!trig && rdy >= gB - 1) {  // the next kernel assumes at most step gB-1 still runs
+                asm volatile("griddepcontrol.launch_dependents;");
+                trig = true;
+            }
+        }
+        if (!waited) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            rdy = max(rdy, gA);
+        }
+        if (!trig) {
+            while (rdy < gB - 1)
+                if (!poll()) __nanosleep(128);
+            asm volatile("griddepcontrol.launch_dependents;");
         }
         if (lane == 0) {
-            sdst[q] = dst_row + c;
-            sdst2[q] = dst2_row ? dst2_row + c : nullptr;
+            asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_total)), "r"(k) : "memory");
         }
-        return true;
-    };
-    // every stage is free before the first store: fill them all
-    uint64_t issued = 0;
-    while (issued < uint64_t(kFStages) && issue(issued, true)) ++issued;
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous step's kernels are done
-    asm volatile("griddepcontrol.launch_dependents;");  // (only now: the next step may load early)
-    while (issued < uint64_t(kFStages) && issue(issued, false)) ++issued;
-    for (uint64_t k = 0; k < issued; ++k) {
-        const int q = int(k % kFStages);
-        const uint32_t par = uint32_t((k / kFStages) & 1);
-        const unsigned bq = static_cast<unsigned>(__cvta_generic_to_shared(&bar[q]));
-        uint32_t done = 0;
-        while (!done)
-            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
-                         : "=r"(done) : "r"(bq), "r"(par) : "memory");
-        if (lane == 0) {
-            const unsigned sp = static_cast<unsigned>(__cvta_generic_to_shared(fsm2 + q * kFTile));
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst[q]), "r"(sp),
-                         "r"(kFTile) : "memory");
-            if (sdst2[q])
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst2[q]), "r"(sp),
+    } else {
+        // ---------------- consumer ----------------
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel on the stream is done
+        rdy = max(rdy, gA);
+        int pend = -1;
+        uint32_t pend_cnt = 0, freed = 0, k = 0;
+        auto release = [&](uint32_t upto) {  // stages [freed, upto) have been read by their stores
+            if (upto <= freed) return;
+            if (lane == 0)
+                for (uint32_t i = freed; i < upto; ++i)
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[i % S])) : "memory");
+            freed = upto;
+        };
+        auto publish = [&]() {  // this warp's stores of step pend have landed: count them
+            if (pend_cnt) {
+                if (lane == 0) {
+                    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    __threadfence();
+                    const uint32_t old = atomicAdd(&f.stored[pend], pend_cnt);
+                    if (f.ring && old + pend_cnt == step_tiles(pend))  // every ring row of the step has landed
+                        atomicMax(f.consumed, s0 + __ldg(&f.moff[pend + 1]));
+                }
+                __syncwarp();
+                release(k);
+            }
+            pend_cnt = 0;
+        };
+        for (;; ++k) {
+            const int q = int(k % S);
+            const unsigned fb = smem_u32(&full[q]);
+            const uint32_t par = (k / S) & 1;
+            uint32_t ok = 0, spins = 0;
+            bool end = false;
+            for (;;) {
+                asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                             : "=r"(ok) : "r"(fb), "r"(par) : "memory");
+                if (ok) break;
+                uint32_t tot;
+                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tot) : "r"(smem_u32(&s_total)) : "memory");
+                if (tot <= k) {
+                    end = true;
+                    break;
+                }
+                if (++spins == 16) publish();  // idle: others may wait for what this CTA holds
+            }
+            if (end) break;
+            const int sk = sstep[q];
+            if (sk != pend) {
+                publish();
+                pend = sk;
+            }
+            while (rdy < sk)
+                if (!poll()) __nanosleep(64);
+            if (lane == 0) {
+                const unsigned sp = smem_u32(fsm2 + q * kFTile);
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst[q]), "r"(sp),
                              "r"(kFTile) : "memory");
-            asm volatile("cp.async.bulk.commit_group;");
-            // stage k+S-L reuses the stage of k-L: free once that store read it
-            if (k >= uint64_t(kFLag)) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kFLag) : "memory");
+                if (sdst2[q])
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sdst2[q]),
+                                 "r"(sp), "r"(kFTile) : "memory");
+                asm volatile("cp.async.bulk.commit_group;");
+                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(L) : "memory");
+            }
+            __syncwarp();
+            ++pend_cnt;
+            if (k + 1 > uint32_t(L)) release(k + 1 - L);
         }
-        __syncwarp();
-        if (issued == k + uint64_t(kFStages - kFLag) && issue(issued, false)) ++issued;
-    }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    if (f.ring && lane == 0) {  // every ring tile this CTA loaded has landed: the last CTA releases the step's rows
-        __threadfence();
-        if (atomicAdd(&f.done[f.gi], 1u) == gridDim.x - 1) atomicMax(f.consumed, s0 + __ldg(&f.moff[f.gi + 1]));
+        publish();
     }
 }
 
@@ -959,7 +1081,8 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
         cudaGetDevice(&dev);
         if (!(attr_done.load() & (1ull << (dev & 63)))) {
             cudaFuncSetAttribute(k_row_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16384 * 4);
-            cudaFuncSetAttribute(k_fetch_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kFTile * kFStages);
+            cudaFuncSetAttribute(k_fetch_fused<kFStages, kFLag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kFTile * kFStages);
             attr_done.fetch_or(1ull << (dev & 63));
         }
         FlagArgs fa{d.d_slots + j->base[0], d.d_node_off + d.step_begin * (N + 1), j->d_base, moff, N,
@@ -974,6 +1097,12 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
             cudaStreamSynchronize(st) != cudaSuccess)
             return fail(cuda_error(cudaGetLastError(), "fetch_job: deferred counts"));
         j->ndefer.assign(static_cast<uint32_t*>(hb), static_cast<uint32_t*>(hb) + ns);
+        if (std::getenv("LSG_FETCH_VERBOSE")) {
+            uint64_t steps = 0, rows = 0;
+            for (uint32_t v : j->ndefer) steps += v != 0, rows += v;
+            fprintf(stderr, "fetch_job: %llu steps, %llu with deferred slot writes (%llu rows)\n",
+                    (unsigned long long)ns, (unsigned long long)steps, (unsigned long long)rows);
+        }
     }
     cudaEventCreateWithFlags(&j->listed, cudaEventDisableTiming);
     cudaEventRecord(j->listed, st);
@@ -1063,6 +1192,103 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
     uint32_t* claims = j->d_ctl;
     uint32_t* done = j->d_ctl + ns;
     uint32_t* moff = j->d_ctl + 3 * ns;
+    if (j->fused) {
+        // one persistent launch per run of steps, cut after every step with
+        // deferred slot writes (k_deferred_slots) and, for large synthesised
+        // rows, after every step (k_job_misses)
+        FusedStep fs{d.d_items + j->base[0], d.d_slots + j->base[0], j->flags,
+                     d.d_node_off + d.step_begin * (N + 1), j->d_base, N,
+                     reinterpret_cast<unsigned char* const*>(d.d_bufs),
+                     reinterpret_cast<unsigned char* const*>(d.d_outs), d.node_begin, d.node_end, d.sample_bytes,
+                     d.fill_seed, claims, done, j->ring, j->R, j->ready, j->seq0, moff, j->consumed, 0, 0,
+                     j->skip_misses ? 1 : 0};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        const int npdl = pdl_on(0) ? 1 : 0;
+        // a launch holds every SM it runs on, so launches are cut every ~1 GiB of tiles
+        // (~0.3 ms): the plan loop and replay kernels on their high-priority streams get
+        // SMs at the next cut (LSG_FETCH_SEG_TILES overrides)
+        static const uint64_t seg_tiles = [] {
+            const char* e = std::getenv("LSG_FETCH_SEG_TILES");
+            return e ? std::max<uint64_t>(1, std::strtoull(e, nullptr, 10)) : (uint64_t(1) << 17);
+        }();
+        // stages per CTA x CTAs per SM (LSG_FETCH_S / LSG_FETCH_CPS: 5x5, 6x4, 12x2). At one rank
+        // per GPU more, shallower pipelines won (43.3 us per step at 6x4 vs 44.9 at 12x2):
+        // a step's stores wait for the whole previous step, so the slowest CTA's queue of
+        // loaded tiles sets the step boundary
+        static const int nst = [] {
+            const char* e = std::getenv("LSG_FETCH_S");
+            const int v = e ? std::atoi(e) : kFStages;
+            return v == 5 || v == 12 ? v : kFStages;
+        }();
+        static const unsigned cps = [] {
+            const char* e = std::getenv("LSG_FETCH_CPS");
+            return e ? unsigned(std::max(1, std::atoi(e))) : kFCtasPerSm;
+        }();
+        auto kern = nst == 5 ? k_fetch_fused<5, 2> : nst == 12 ? k_fetch_fused<12, 3> : k_fetch_fused<kFStages, kFLag>;
+        static std::atomic<uint32_t> vattr{0};
+        if (!(vattr.fetch_or(1u) & 1u)) {
+            cudaFuncSetAttribute(k_fetch_fused<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFTile * 5);
+            cudaFuncSetAttribute(k_fetch_fused<12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFTile * 12);
+        }
+        for (uint32_t ga = 0; ga < ns;) {
+            uint32_t gb = ga + 1;
+            const uint64_t tpr = d.sample_bytes / kFTile;
+            uint64_t tiles = j->rows[ga] * tpr;
+            while (gb < ns && !j->skip_misses && !j->ndefer[gb - 1] && tiles + j->rows[gb] * tpr <= seg_tiles)
+                tiles += j->rows[gb++] * tpr;
+            fs.gA = ga;
+            fs.gB = gb;
+            if (tiles && d.node_begin != d.node_end) {
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = dim3(unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 148ull * cps))));
+                cfg.blockDim = dim3(64);
+                cfg.dynamicSmemBytes = size_t(kFTile) * nst;
+                cfg.stream = st;
+                cfg.attrs = attr;
+                cfg.numAttrs = npdl;
+                LSG_CUDA(cudaLaunchKernelEx(&cfg, kern, fs));
+                LSG_LAUNCH_CHECK("k_fetch_fused");
+            }
+            const uint32_t gl = gb - 1;  // the segment's last step
+            const uint64_t g = d.step_begin + gl;
+            if (j->skip_misses && j->rows[gl]) {  // large synthesised rows: a wide kernel writes the misses
+                StepFetch f{};
+                f.items = d.d_items + j->base[gl];
+                f.slots = d.d_slots + j->base[gl];
+                f.node_off = d.d_node_off + g * (N + 1);
+                f.bufs = reinterpret_cast<uint4* const*>(d.d_bufs);
+                f.outs = reinterpret_cast<uint4* const*>(d.d_outs);
+                f.k0 = d.node_begin;
+                f.k1 = d.node_end;
+                f.vec_per_row = d.sample_bytes / 16;
+                f.tiles_per_row = (f.vec_per_row + 1023) / 1024;
+                f.seed = d.fill_seed;
+                MissArgs ma{f, moff, gl, j->mrow, nullptr, 0, nullptr, nullptr, done, nullptr};
+                const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 64)),
+                                unsigned(std::min<uint64_t>(j->rows[gl], 148)));
+                k_job_misses<<<grid, 256, 0, st>>>(ma);
+                LSG_LAUNCH_CHECK("k_job_misses");
+            } else if (j->ndefer[gl]) {
+                DeferArgs da{d.d_slots + j->base[gl], j->flags + (j->base[gl] - j->base[0]),
+                             d.d_node_off + g * (N + 1), j->mrow, moff, gl, d.node_begin, d.node_end, fs.bufs,
+                             fs.outs, d.sample_bytes / 16};
+                const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(da.vpr / 4096, 1), 64)),
+                                unsigned(std::min<uint64_t>(j->ndefer[gl], 148)));
+                cudaLaunchConfig_t dc{};
+                dc.gridDim = grid;
+                dc.blockDim = dim3(256);
+                dc.stream = st;
+                dc.attrs = attr;
+                dc.numAttrs = npdl;
+                LSG_CUDA(cudaLaunchKernelEx(&dc, k_deferred_slots, da));
+                LSG_LAUNCH_CHECK("k_deferred_slots");
+            }
+            ga = gb;
+        }
+        return kOk;
+    }
     for (uint32_t gi = 0; gi < ns; ++gi) {
         const uint64_t g = d.step_begin + gi;
         const uint64_t b = j->base[gi];
@@ -1080,49 +1306,6 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
         f.claim = claims + gi;
         const uint64_t rows = j->rows[gi];
         if (rows == 0 || d.node_begin == d.node_end) continue;
-        if (j->fused) {
-            FusedStep fs{f.items, f.slots, j->flags + (b - j->base[0]), f.node_off,
-                         reinterpret_cast<unsigned char* const*>(d.d_bufs),
-                         reinterpret_cast<unsigned char* const*>(d.d_outs), d.node_begin, d.node_end,
-                         d.sample_bytes, d.fill_seed, f.claim, j->ring, j->R, j->ready, j->seq0, moff, gi, done,
-                         j->consumed, j->skip_misses ? 1 : 0};
-            const uint64_t tiles = rows * (d.sample_bytes / kFTile);
-            cudaLaunchConfig_t cfg{};
-            cfg.gridDim = dim3(unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 148ull * 2))));
-            cfg.blockDim = dim3(32);
-            cfg.dynamicSmemBytes = size_t(kFTile) * kFStages;
-            cfg.stream = st;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[0].val.programmaticStreamSerializationAllowed = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = pdl_on(0) ? 1 : 0;
-            LSG_CUDA(cudaLaunchKernelEx(&cfg, k_fetch_fused, fs));
-            LSG_LAUNCH_CHECK("k_fetch_fused");
-            if (j->skip_misses) {  // large synthesised rows: a wide kernel writes the misses after the hits
-                MissArgs ma{f, moff, gi, j->mrow, nullptr, 0, nullptr, nullptr, done, nullptr};
-                const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 64)),
-                                unsigned(std::min<uint64_t>(rows, 148)));
-                k_job_misses<<<grid, 256, 0, st>>>(ma);
-                LSG_LAUNCH_CHECK("k_job_misses");
-                continue;
-            }
-            if (j->ndefer[gi]) {
-                DeferArgs da{f.slots, fs.flags, f.node_off, j->mrow, moff, gi, d.node_begin, d.node_end, fs.bufs,
-                             fs.outs, d.sample_bytes / 16};
-                const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(da.vpr / 4096, 1), 64)),
-                                unsigned(std::min<uint64_t>(j->ndefer[gi], 148)));
-                cudaLaunchConfig_t dc{};
-                dc.gridDim = grid;
-                dc.blockDim = dim3(256);
-                dc.stream = st;
-                dc.attrs = attr;
-                dc.numAttrs = cfg.numAttrs;
-                LSG_CUDA(cudaLaunchKernelEx(&dc, k_deferred_slots, da));
-                LSG_LAUNCH_CHECK("k_deferred_slots");
-            }
-            continue;
-        }
         if (int rc = launch_fetch_hits(f, rows, d.sample_bytes, st, nullptr)) return rc;
         MissArgs ma{f, moff, gi, j->mrow, j->ring, j->R, j->ready, j->consumed, done, j->seq0};
         const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(f.vec_per_row / 4096, 1), 64)),

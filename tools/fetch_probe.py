@@ -24,8 +24,16 @@ for r in [int(x) for x in (sys.argv[1:] or ["1", "2", "8"])]:
     a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(); f.fetch_steps(plan, sim.slots, off); z.record(); torch.cuda.synchronize()
     ms = a.elapsed_time(z)
+    # the job's kernels alone (creation -- miss list, row flags -- outside the events)
+    j = ls.FetchJob(bufs, outs, (0, r), plan, sim.slots, off, SB, 1)
+    torch.cuda.synchronize()
+    a.record(); j.run(); z.record(); torch.cuda.synchronize()
+    run_ms = a.elapsed_time(z)
+    j.close()
     alg = 2 * SB * hits + 2 * SB * miss
     res[r] = {"fetch_ms": round(ms, 1), "TBps": round(alg / ms / 1e9, 3), "us_per_step": round(ms * 1e3 / off.shape[0], 1),
+              "run_ms": round(run_ms, 1), "run_TBps": round(alg / run_ms / 1e9, 3),
+              "run_us_per_step": round(run_ms * 1e3 / off.shape[0], 1),
               "data_us_per_step_at_6.55": round(alg / 6.55e12 * 1e6 / off.shape[0], 1)}
     del bufs, outs, f, sim
     torch.cuda.empty_cache()
