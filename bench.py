@@ -729,10 +729,11 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_note": "dram read+write bytes per k_fetch_fused launch (one steady-state step, "
-                                         "8 ranks on one GPU) from profiles/gather_traffic.json (r02_fetch_fused.ncu-rep); "
+                                         "8 ranks on one GPU) from profiles/gather_traffic.json (r02b_fetch_persist.ncu-rep); "
                                          f"{traffic_ratio:.3f} x that launch's algorithmic bytes" if traffic else None,
-                         "kernel": "fetch phase (k_fetch_fused: one TMA bulk-copy pipeline per training step for "
-                                   "hits and misses, + k_deferred_slots / k_job_misses where needed)",
+                         "kernel": "fetch phase (k_fetch_fused: persistent multi-step TMA bulk-copy pipeline, "
+                                   "producer/consumer warps, hits and misses; + k_deferred_slots / k_job_misses "
+                                   "where needed)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6650"},
             "gpu_launches": int(launches),
             **({"timeline_plan0_plan1_rep0_rep1_fetch0_fetch1": timeline} if timeline else {}),
