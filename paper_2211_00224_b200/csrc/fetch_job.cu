@@ -667,8 +667,9 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
             } else {  // synthesised Store payload (store.cpp:70-80): words of this tile
                 const uint64_t w0 = (uint64_t(row_id) * f.row_bytes + c) / 8;
                 unsigned long long* sw = reinterpret_cast<unsigned long long*>(st);
-#pragma unroll 4
-                for (uint32_t i = lane; i < kFTile / 8; i += 32) sw[i] = mix64(f.seed + (w0 + i + 1) * kGamma);
+                uint64_t x = f.seed + (w0 + lane + 1) * kGamma;  // word counter x gamma, stepped by adds
+#pragma unroll 8
+                for (uint32_t i = lane; i < kFTile / 8; i += 32, x += 32 * kGamma) sw[i] = mix64(x);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
@@ -1068,9 +1069,15 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
     uint32_t P2 = 2;
     while (P2 < max_list) P2 <<= 1;
     j->fused = ns && d.sample_bytes % kFTile == 0 && !two_kernels && P2 <= 16384;
-    // synthesised payload of large rows (cfg3: 16 MiB) is compute: one warp per
-    // CTA would stall the copy pipeline, so those misses go to a wide kernel
-    j->skip_misses = j->fused && !d.host && d.sample_bytes > (uint64_t(1) << 20);
+    // LSG_FETCH_SKIP=1: synthesised misses written by the wide k_job_misses after each
+    // step's hits. The one-warp-per-CTA step kernel stalled its copies computing 16 MiB
+    // payload rows (cfg3), so that was the default above 1 MiB; with a producer warp per
+    // CTA the fused kernel is faster for them too (cfg3 3.92-4.01 s vs 4.39 s per job)
+    static const int skip_env = [] {
+        const char* e = std::getenv("LSG_FETCH_SKIP");
+        return e ? std::atoi(e) : 0;
+    }();
+    j->skip_misses = j->fused && !d.host && skip_env == 1;
     if (j->fused) {
         if (!alloc(reinterpret_cast<void**>(&j->flags), (j->base[ns] - j->base[0]) * 4) ||
             !alloc(reinterpret_cast<void**>(&j->ndefer_d), ns * 4))

@@ -211,10 +211,10 @@ def test_shared_miss_stream_across_jobs(ls, host_rows, SB, ring_rows):
     ms.close()
 
 
-def test_large_rows_hits_fused_misses_wide(ls):
+def test_large_rows_synthesised_misses(ls):
     """Rows above 1 MiB with synthesised misses (the cfg3 shape in small):
-    the fused kernel moves the hits, a wide kernel writes the misses; every
-    step's batch and the final slots are the Store payload."""
+    the producer warps compute 2 MiB payload rows tile by tile beside the hit
+    copies; every step's batch and the final slots are the Store payload."""
     D, E, N, b, SB = 512, 4, 2, 8, 2 << 20
     pc, plan, sim = setup(ls, D, E, N, b, 0.2)
     off = u32(plan.node_off)
