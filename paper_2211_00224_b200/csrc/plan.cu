@@ -36,6 +36,8 @@
 //     per-node id bitmap scanned from the top.
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
+#include <vector>
 
 #include <cooperative_groups.h>
 
@@ -163,7 +165,8 @@ struct LoopArgs {
     uint32_t* gitems;                // [6][B] per-item arrays when they do not fit smem
     unsigned long long* prof;        // [8] per-phase cycles (LSG_PROFILE) or null
     int dbg_skip;                    // timing experiments only (LSG_DEBUG_SKIP)
-    uint32_t* nb;                    // [D] overlapped loop: the latest batch each id was classified in, or null
+    uint32_t* nb;                    // [2][D] overlapped loop: per batch parity, the latest batch each id was
+                                     // classified in, or null
 };
 
 struct Shared {
@@ -198,7 +201,7 @@ struct Small {
     uint32_t rq[kMaxN];             // G: recipient of each rank in a round
     uint32_t win_base;              // I1: first bucket word of the window
     uint32_t win[kMaxN][kWinWords]; // I1: bucket bits aggregated per step
-    uint32_t stamp, conflict;       // (overlapped loop only; unused here)
+    uint32_t stamp, conflict, conflict2;  // (overlapped loop only; unused here)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -231,12 +234,22 @@ __device__ __forceinline__ void set_key(const LoopArgs& a, SM& sm, uint32_t k, u
 }
 
 // with the overlapped loop (a.nb), a holder mask that changes for an id of
-// the next, already classified batch invalidates that classification
+// one of the next two, already classified batches (sm.stamp = g+1, g+2)
+// invalidates that classification. The classifier stamps, fences, then reads
+// masks; the advance changes a mask, fences, then reads the stamps: one of
+// the two sees the other.
+template <class SM>
+__device__ __forceinline__ void nb_check(const LoopArgs& a, SM& sm, uint32_t x) {
+    __threadfence();
+    const uint32_t s1 = sm.stamp, s2 = s1 + 1;
+    if (__ldcg(&a.nb[size_t(s1 & 1) * a.D + x]) == s1) sm.conflict = 1;
+    if (__ldcg(&a.nb[size_t(s2 & 1) * a.D + x]) == s2) sm.conflict2 = 1;
+}
 template <class SM>
 __device__ __forceinline__ void drop(const LoopArgs& a, SM& sm, uint32_t k, uint32_t x) {
     a.key[size_t(k) * a.D + x] = kNone;
     atomicAnd(&a.hm[x], ~(1u << k));
-    if (a.nb && __ldcg(&a.nb[x]) == sm.stamp) sm.conflict = 1;
+    if (a.nb) nb_check(a, sm, x);
 }
 
 // Remove the `need` largest (key, id) residents of node k. Whole warp.
@@ -1180,23 +1193,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K6o: the step loop with the serial multi-holder pass OVERLAPPED (N <= 8,
-// b < 2048, B <= 4096, remap on; clairvoyant). Warp 0 (team D) runs the
-// packed multi-holder chain D of step g+1 while warps 1-15 (team P) run the
-// buffer-side phases E..I of step g and then classify step g+2 (A..C):
-//
-//   team D:  D(g)   | D(g+1)              | D(g+2) ...
-//   team P:  E..I(g-1), A..C(g+1) | E..I(g), A..C(g+2) | ...
-//
-// Step g+1 is classified before I(g) has advanced the buffers, i.e. against
-// holder masks one step old. Only ids of batch g+1 whose mask I(g) changes
-// can alter that classification: an insert or a drop of such an id (an id in
-// both batches at an epoch boundary, or an eviction reaching next-step keys)
-// is detected through a per-id stamp of the latest classified batch, and then
-// step g+1 is classified and resolved again after I(g) (once per epoch
-// boundary at most, in practice). Per-step arrays are double-buffered by
-// step parity; the teams hand off through shared-memory step counters
-// (release/acquire at CTA scope), team P synchronises on named barrier 1.
+// K6o: the step loop with its phases PIPELINED over three teams (N <= 8,
+// b < 2048, B <= 4096, remap on; clairvoyant): team C classifies step h
+// (A..C), team D runs the serial multi-holder chain D of step h, team P
+// applies D and runs the buffer-side phases E..I of step h. Step h is
+// classified once I(h-3) has advanced the buffers, i.e. against holder masks
+// two advances old, so C(h), D(h-1) and P(h-2) run at the same time and the
+// loop P(h-3) -> C(h) -> D(h) -> P(h) spans three steps. Only ids of batch h
+// whose mask I(h-2) or I(h-1) changes can alter its classification: an
+// insert or a drop of such an id (an id in consecutive batches at an epoch
+// boundary, or an eviction reaching next-step keys) is detected through
+// per-id stamps (one array per batch parity, so an id in both pending
+// batches keeps both stamps), and then step h is classified and resolved
+// again after I(h-1) (once per epoch boundary at most, in practice). Team
+// P's step arrays are double-buffered by step parity (team C classifies into
+// its own shared memory and copies a step over once P is done with step
+// h-2); team D's inputs and results are triple-buffered. The teams hand off
+// through shared-memory step counters with cluster-scope release/acquire.
 struct OvPar {  // per step parity
     uint32_t tot[kMaxN];   // singles per node
     uint32_t mtot[kMaxN];  // multi assigned per node (D)
@@ -1220,15 +1233,18 @@ struct SmallOv {
     uint32_t inftop[kMaxN];
     uint32_t infcnt[kMaxN];
     uint32_t nfetch, nmoves;
-    alignas(16) uint32_t stg[2][32][kMaxN];
+    alignas(16) uint32_t stg[2][2][32][kMaxN];  // team D: staging per D warp
     uint32_t dmv[kMaxN][kDmv];
     uint32_t rq[kMaxN];
     uint32_t win[kMaxN][kWinWords];
-    uint32_t stamp, conflict;
+    uint32_t stamp, conflict, conflict2;  // I(g): stamps g+1 / g+2, their batches' verdicts
     OvPar par[2];
+    uint32_t cfv[4];   // verdict per batch (mod 4): a mask it was classified with changed
+    uint32_t cnm[3];   // (team C's copy) multi items per step (mod 3), for team D
     // team hand-off counters (monotone): steps classified, resolved (D
-    // final), buffer-advanced, speculative-D-finished-on-conflict, re-classified
-    volatile uint32_t ac_cnt, d_cnt, i_cnt, spec_cnt, redo_cnt;
+    // final), buffer-advanced, speculative-D-finished-on-conflict,
+    // re-classified, copied into team P's arrays, resolved (first pass)
+    volatile uint32_t ac_cnt, d_cnt, i_cnt, spec_cnt, redo_cnt, copy_cnt, ds_cnt[2];
 };
 
 // The teams run on the two SMs of a thread-block cluster: team D (warp 0 of
@@ -1261,11 +1277,11 @@ struct OvBufs {
 };
 
 // A..C of step g by team C (CTA 0, 12 warps): load + classify + ranks, exact
-// S_k(j) rows of the multi items for D (global, parity buffer)
-__device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, const OvBufs& sr, OvPar& pp,
-                            uint32_t* smul, uint32_t* dsx, uint32_t* dpre, uint32_t g, uint32_t pw, uint32_t lane) {
-    // sm, s: team C's own scratch and step arrays (local shared memory);
-    // sr / pp: team P's arrays (DSMEM), filled by one coalesced copy at the end
+// S_k(j) rows of the multi items for D (global, buffer g % 3)
+__device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, OvPar& pp, uint32_t* smul,
+                            uint32_t* dsx, uint32_t* dpre, uint32_t g, uint32_t pw, uint32_t lane, bool stamp) {
+    // sm, s, pp: team C's own scratch, step arrays and totals (local shared
+    // memory; ov_copy moves them to team P)
     const uint32_t N = a.N, b = a.b;
     const uint32_t lt = lanemask_lt();
     const uint32_t i = g / a.S, t = g % a.S;
@@ -1281,8 +1297,9 @@ __device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, con
         const uint32_t x = row[j];
         s.sx[j] = x;
         s.snu[j] = pkrow[j];
-        a.nb[x] = g;  // this batch's classification is checked by I(g-1)
+        if (stamp) a.nb[size_t(g & 1) * a.D + x] = g;  // this batch's classification is checked by I(g-2), I(g-1)
     }
+    __threadfence();  // stamps before the masks are read (nb_check)
     __syncwarp();
 #pragma unroll 4
     for (uint32_t j = j0 + lane; j < j1; j += 32) s.smask[j] = __ldcg(&a.hm[s.sx[j]]);
@@ -1371,9 +1388,17 @@ __device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, con
             dpre[mi] = j;  // the multi list for team D, in global memory (no DSMEM on its chain)
         }
     }
+    if (pw == 0 && lane == 0) sm.cnm[g % 3] = pp.nmulti;
+    __threadfence_block();
     bar_c();
-    // the classified step to team P's shared memory (16-byte DSMEM stores)
-    const uint32_t ctid = pw * 32 + lane, nm = pp.nmulti;
+}
+
+// the classified step g (team C's arrays + totals) into team P's parity
+// buffers (16-byte DSMEM stores), once team P is done with step g-2
+__device__ void ov_copy(const LoopArgs& a, const OvBufs& s, const OvPar& pc, const OvBufs& sr, OvPar& pp, uint32_t g,
+                        uint32_t pw, uint32_t lane) {
+    const uint32_t len = min(a.B, a.keep - (g % a.S) * a.B);
+    const uint32_t ctid = pw * 32 + lane, nm = pc.nmulti;
     const uint32_t len4 = (len + 3) / 4, nm4 = (nm + 3) / 4;
     for (uint32_t q = ctid; q < 4 * len4 + nm4; q += kCThreads) {
         const uint32_t arr = q < 4 * len4 ? q / len4 : 4, e = (q < 4 * len4 ? q - arr * len4 : q - 4 * len4) * 4;
@@ -1381,6 +1406,8 @@ __device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, con
         uint32_t* dst = arr == 0 ? sr.sx : arr == 1 ? sr.snu : arr == 2 ? sr.smask : arr == 3 ? sr.sinfo : sr.pre;
         *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(src + e);
     }
+    if (ctid < a.N) pp.tot[ctid] = pc.tot[ctid];
+    if (ctid == 0) pp.nmulti = nm;
     __threadfence_block();
     bar_c();
 }
@@ -1389,8 +1416,8 @@ __device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, con
 // from global memory (the multi list and the packed rows), outputs into team
 // D's own shared memory (res[mi] = the chain's minimum key, or kSent; mtot);
 // team P applies them to its lists (ov_apply).
-__device__ void ov_resolve(const LoopArgs& a, SmallOv& sm, const uint32_t* dsx, const uint32_t* dpre, uint32_t nm,
-                           uint32_t* res, uint32_t* mtot, uint32_t lane) {
+__device__ void ov_resolve(const LoopArgs& a, uint32_t (*stg)[32][kMaxN], const uint32_t* dsx, const uint32_t* dpre,
+                           uint32_t nm, uint32_t* res, uint32_t* mtot, uint32_t lane) {
     const uint32_t N = a.N, b = a.b;
     uint32_t M01 = 0, M23 = 0, M45 = 0, M67 = 0;
     const uint32_t kSent = (b << 4) - 1u;
@@ -1399,7 +1426,7 @@ __device__ void ov_resolve(const LoopArgs& a, SmallOv& sm, const uint32_t* dsx, 
     auto stage = [&](uint32_t base, uint32_t buf) {
         const uint32_t cnt = min(32u, nm - base);
         const uint4* src = reinterpret_cast<const uint4*>(dsx) + base;
-        uint4* dst4 = reinterpret_cast<uint4*>(&sm.stg[buf][0][0]);
+        uint4* dst4 = reinterpret_cast<uint4*>(&stg[buf][0][0]);
         if (lane < cnt) {
             const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst4 + lane));
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src + lane));
@@ -1420,7 +1447,7 @@ __device__ void ov_resolve(const LoopArgs& a, SmallOv& sm, const uint32_t* dsx, 
         }
         __syncwarp();
         const uint32_t cnt = min(32u, nm - base);
-        const uint4* rows = reinterpret_cast<const uint4*>(&sm.stg[buf][0][0]);
+        const uint4* rows = reinterpret_cast<const uint4*>(&stg[buf][0][0]);
         uint32_t myres = kSent;
         uint32_t v01 = 0x10001u, v23 = 0x10001u, v45 = 0x10001u, v67 = 0x10001u;
 #pragma unroll
@@ -1501,19 +1528,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         }
         if (tid == 0) {
             sm_local.ac_cnt = sm_local.d_cnt = sm_local.i_cnt = sm_local.spec_cnt = sm_local.redo_cnt = 0;
-            sm_local.par[0].cf = sm_local.par[1].cf = 0;
-            sm_local.conflict = 0;
+            sm_local.copy_cnt = sm_local.ds_cnt[0] = sm_local.ds_cnt[1] = 0;
+            for (int q = 0; q < 4; ++q) sm_local.cfv[q] = 0;
+            sm_local.conflict = sm_local.conflict2 = 0;
         }
     }
     cl.sync();
-    // global scratch by parity: smul [B][N], the D rows [B] x 16 B
+    // global scratch: smul [B][N] (team C only), the D rows [3][B] x 16 B and multi lists [3][B]
     auto smul_of = [&](uint32_t g) { return a.smul + size_t(g & 1) * a.B * N; };
-    auto dsx_of = [&](uint32_t g) { return a.sx + size_t(g & 1) * a.B * 4; };
-    auto dpre_of = [&](uint32_t g) { return a.sx + size_t(2) * a.B * 4 + size_t(g & 1) * a.B; };
-    // team D's results in CTA 0's shared memory: res [2][B], mtot [2][kMaxN]
+    auto dsx_of = [&](uint32_t g) { return a.sx + size_t(g % 3) * a.B * 4; };
+    auto dpre_of = [&](uint32_t g) { return a.sx + size_t(3) * a.B * 4 + size_t(g % 3) * a.B; };
+    // team D's results in CTA 0's shared memory: res [3][B], mtot [3][kMaxN]
     uint32_t* dres = cl.map_shared_rank(dyn, 0);
-    auto res_of = [&](uint32_t g) { return dres + size_t(g & 1) * a.B; };
-    auto mtot_of = [&](uint32_t g) { return dres + size_t(2) * a.B + size_t(g & 1) * kMaxN; };
+    auto res_of = [&](uint32_t g) { return dres + size_t(g % 3) * a.B; };
+    auto mtot_of = [&](uint32_t g) { return dres + size_t(3) * a.B + size_t(g % 3) * kMaxN; };
     unsigned long long pf[12] = {}, t0 = clock64();
     auto tick = [&](int q) {
         if (a.prof) {
@@ -1522,62 +1550,106 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
             t0 = t1;
         }
     };
+    // LSG_PROFILE_OV: global-timer stamps of each team's events for steps 2000..2015
+    auto ev = [&](uint32_t g, int e) {
+        const uint32_t g0 = uint32_t(a.dbg_skip) >> 8;
+        if (a.prof && g >= g0 && g < g0 + 16) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.prof[32 + (g - g0) * 8 + e] = t;
+        }
+    };
     if (crank == 0 && w != 0 && (w & 3) != 0) {
         // -------------------------------------------- team C (CTA 0)
         const uint32_t cw = (w >> 2) * 3 + (w & 3) - 1;
-        // team C's step arrays: CTA 0's dynamic smem after team D's results (2B + 64 words)
-        uint32_t* c0 = dyn + size_t(2) * a.B + 2 * kMaxN;
+        // team C's step arrays: CTA 0's dynamic smem after team D's results (3B + 3*kMaxN words)
+        uint32_t* c0 = dyn + size_t(3) * a.B + 3 * kMaxN;
         const OvBufs SC{c0, c0 + a.B, c0 + 2 * a.B, c0 + 3 * a.B, c0 + 4 * a.B, nullptr};
-        ov_classify(a, sm_local, SC, S2[0], sm.par[0], smul_of(0), dsx_of(0), dpre_of(0), 0, cw, lane);
-        if (cw == 0 && lane == 0) publish(&sm.ac_cnt, 1);
-        for (uint32_t h = 1; h <= a.T; ++h) {
-            // classify step h once I(h-2) is done (its parity buffers are free,
-            // the masks one step old); first the verdict of I(h-2) on step h-1
+        OvPar& pc = sm_local.par[0];  // team C's totals of the step it classified last
+        for (uint32_t h = 0; h < a.T + 2; ++h) {
+            // classify step h once I(h-3) is done; first the verdict of I(h-4), I(h-3) on step h-2
             if (h >= 2) {
+                if (cw == 0) wait_ge(&sm.i_cnt, h - 2);
+                bar_c();
+            }
+            if (h >= 3 && h - 2 < a.T && sm.cfv[(h - 2) & 3]) {
+                if (cw == 0) wait_ge(&sm.ds_cnt[h & 1], h - 1);  // team D is done with the speculative D(h-2)
+                bar_c();
+                ov_classify(a, sm_local, SC, pc, smul_of(h - 2), dsx_of(h - 2), dpre_of(h - 2), h - 2, cw, lane, false);
+                // team P has not started step h-2 (it waits for D(h-2)): its buffers take the new classification
+                ov_copy(a, SC, pc, S2[(h - 2) & 1], sm.par[(h - 2) & 1], h - 2, cw, lane);
+                if (cw == 0 && lane == 0) publish(&sm.redo_cnt, h - 1);
+            }
+            if (h >= a.T) continue;  // (the last two verdicts only)
+            tick(0);
+            if (cw == 0 && lane == 0) ev(h, 0);
+            ov_classify(a, sm_local, SC, pc, smul_of(h), dsx_of(h), dpre_of(h), h, cw, lane, true);
+            if (cw == 0 && lane == 0) publish(&sm.ac_cnt, h + 1);
+            if (cw == 0 && lane == 0) ev(h, 1);
+            tick(1);
+            if (h >= 2) {  // team P is done with step h-2: its parity buffers are free
                 if (cw == 0) wait_ge(&sm.i_cnt, h - 1);
                 bar_c();
-                if (sm.par[(h - 1) & 1].cf) {
-                    if (cw == 0) wait_ge(&sm.spec_cnt, h);  // team D is done with the speculative D(h-1)
-                    bar_c();
-                    ov_classify(a, sm_local, SC, S2[(h - 1) & 1], sm.par[(h - 1) & 1], smul_of(h - 1),
-                                dsx_of(h - 1), dpre_of(h - 1), h - 1, cw, lane);
-                    if (cw == 0 && lane == 0) publish(&sm.redo_cnt, h);
-                }
             }
-            tick(0);
-            if (h < a.T) {
-                ov_classify(a, sm_local, SC, S2[h & 1], sm.par[h & 1], smul_of(h), dsx_of(h), dpre_of(h), h, cw, lane);
-                if (cw == 0 && lane == 0) publish(&sm.ac_cnt, h + 1);
-            }
-            tick(1);
+            tick(2);
+            if (cw == 0 && lane == 0) ev(h, 2);
+            ov_copy(a, SC, pc, S2[h & 1], sm.par[h & 1], h, cw, lane);
+            if (cw == 0 && lane == 0) publish(&sm.copy_cnt, h + 1);
+            if (cw == 0 && lane == 0) ev(h, 3);
+            tick(3);
         }
+        if (cw == 0 && lane == 0) publish(&sm.ac_cnt, a.T + 1);  // team D: no more re-classifications
         if (a.prof && cw == 0 && lane == 0)
-            for (int q = 0; q < 2; ++q) a.prof[20 + q] = pf[q];
+            for (int q = 0; q < 4; ++q) a.prof[20 + q] = pf[q];
     }
     if (crank == 0) {
-        if (w == 0) {
+        if (w == 0 || w == 4) {
             // -------------------------------------------- team D (CTA 0)
-            for (uint32_t g = 0; g < a.T; ++g) {
-                wait_ge(&sm.ac_cnt, g + 1);  // every lane: a one-lane spin left the warp diverged through the chain
-                tick(0);
-                ov_resolve(a, sm_local, dsx_of(g), dpre_of(g), sm.par[g & 1].nmulti, dyn + size_t(g & 1) * a.B,
-                           dyn + size_t(2) * a.B + size_t(g & 1) * kMaxN, lane);
-                tick(1);
-                if (g > 0) {  // the verdict of I(g-1) on this step's classification
-                    wait_ge(&sm.i_cnt, g);
-                    tick(2);
-                    if (sm.par[g & 1].cf) {
-                        if (lane == 0) publish(&sm.spec_cnt, g + 1);
-                        wait_ge(&sm.redo_cnt, g + 1);
-                        ov_resolve(a, sm_local, dsx_of(g), dpre_of(g), sm.par[g & 1].nmulti,
-                                   dyn + size_t(g & 1) * a.B, dyn + size_t(2) * a.B + size_t(g & 1) * kMaxN, lane);
-                    }
-                }
+            // Two warps on scheduler 0 (team C holds the other three), one per
+            // step parity: D(g) of one step does not depend on D(g-1), and one
+            // warp's serial chain leaves most issue slots idle. Speculative D(g)
+            // as soon as step g is classified; a re-classified step (team C,
+            // after I(g-2) or I(g-1) changed one of its masks) is resolved again
+            // when it arrives, and team P waits for that only then.
+            const uint32_t dp = w >> 2;  // this warp's step parity
+            uint32_t (*stg)[32][kMaxN] = sm_local.stg[dp];
+            uint32_t redone = 0;  // re-classifications resolved (redo_cnt values)
+            auto pending = [&]() {
+                const uint32_t r = sm.redo_cnt;
+                return r > redone && ((r - 1) & 1) == dp;
+            };
+            auto redo = [&]() {
+                if (!pending()) return;
+                asm volatile("fence.acq_rel.cluster;" ::: "memory");
+                const uint32_t r = sm.redo_cnt, q = r - 1;
+                ov_resolve(a, stg, dsx_of(q), dpre_of(q), sm_local.cnm[q % 3], dyn + size_t(q % 3) * a.B,
+                           dyn + size_t(3) * a.B + size_t(q % 3) * kMaxN, lane);
                 __syncwarp();
-                if (lane == 0) publish(&sm.d_cnt, g + 1);
-                tick(3);
+                if (lane == 0) publish(&sm.d_cnt, r);
+                redone = r;
+            };
+            for (uint32_t g = dp; g < a.T;) {
+                // every lane spins: a one-lane spin left the warp diverged through the chain
+                while (sm.ac_cnt < g + 1 && !pending()) {
+                }
+                asm volatile("fence.acq_rel.cluster;" ::: "memory");
+                tick(0);
+                redo();  // (at most one pending: the next needs P to finish the step this one blocks)
+                if (sm.ac_cnt < g + 1) continue;
+                asm volatile("fence.acq_rel.cluster;" ::: "memory");
+                if (lane == 0) ev(g, 4);
+                ov_resolve(a, stg, dsx_of(g), dpre_of(g), sm_local.cnm[g % 3], dyn + size_t(g % 3) * a.B,
+                           dyn + size_t(3) * a.B + size_t(g % 3) * kMaxN, lane);
+                __syncwarp();
+                if (lane == 0) publish(&sm.ds_cnt[dp], g + 1);  // team P knows the verdict itself (it ran I(g-1))
+                if (lane == 0) ev(g, 5);
+                tick(1);
+                g += 2;
             }
-            if (a.prof && lane == 0)
+            while (sm.ac_cnt <= a.T) redo();  // team C's last re-classifications (it ends with ac_cnt = T+1)
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            redo();
+            if (a.prof && w == 0 && lane == 0)
                 for (int q = 0; q < 4; ++q) a.prof[q] = pf[q];
         }
         cl.sync();  // team P's shared memory stays alive until team D is done with it
@@ -1599,13 +1671,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         const uint32_t R = ((len + kPThreads - 1) / kPThreads) * 32;
         const uint32_t j0 = pw * R, j1 = min(j0 + R, len);
         tick(3);
-        if (ptid == 0) wait_ge(&sm.d_cnt, g + 1);  // D(g) resolved (final); one waiter, the barrier orders the rest
+        if (ptid == 0) {  // D(g) resolved, step g copied in; one waiter, the barrier orders the rest
+            wait_ge(&sm.ds_cnt[g & 1], g + 1);
+            wait_ge(&sm.copy_cnt, g + 1);
+            // I(g-2) or I(g-1) changed a mask of this batch: wait for its second classification
+            if (g > 0 && sm.cfv[g & 3]) {
+                wait_ge(&sm.d_cnt, g + 1);
+                if (a.prof) a.prof[24] += 1;
+            }
+        }
         bar_p();
+        if (ptid == 0) ev(g, 6);
+        if (a.prof && ptid == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.prof[32 + 128 + 2 * g] = t;
+        }
+        tick(9);
         ov_apply(a, s, pp, dsx_of(g), res_of(g), mtot_of(g), ptid);
         bar_p();
         tick(0);
-        if (g + 2 < a.T && !(a.dbg_skip & 8)) {  // batch g+2's rows into L2 for its classification after I(g)
-            const uint32_t g2 = g + 2, i2 = g2 / a.S, t2 = g2 % a.S;
+        if (g + 3 < a.T && !(a.dbg_skip & 8)) {  // batch g+3's rows into L2 for its classification after I(g)
+            const uint32_t g2 = g + 3, i2 = g2 / a.S, t2 = g2 % a.S;
             const uint32_t lo2 = t2 * a.B, len2 = min(a.B, a.keep - lo2);
             const char* r0 = reinterpret_cast<const char*>(a.trace + size_t(a.order[i2]) * a.keep + lo2);
             const char* r1 = reinterpret_cast<const char*>(a.nr + size_t(i2) * a.keep + lo2);
@@ -1854,11 +1941,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         }
         bar_p();
         tick(7);
-        // ------------ I: buffer advance; changes to the masks of batch g+1
-        // (already classified) are caught by the stamp check
+        // ------------ I: buffer advance; changes to the masks of batches g+1
+        // and g+2 (already classified) are caught by the stamp checks
         if (ptid == 0) {
             sm.stamp = g + 1;
-            sm.conflict = 0;
+            sm.conflict = sm.conflict2 = 0;
         }
         bar_p();
         {
@@ -1930,7 +2017,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
                         set_key(a, sm, k, x, s.snu[j]);
                         if (!hitrun) {
                             atomicOr(&a.hm[x], 1u << k);
-                            if (__ldcg(&a.nb[x]) == g + 1) sm.conflict = 1;
+                            nb_check(a, sm, x);
                         }
                     }
                     __syncwarp();
@@ -1947,15 +2034,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         bar_p();
         tick(1);
         gbase += len;
-        // the verdict on step g+1's classification (team C re-classifies on a conflict)
-        if (g + 1 < a.T) {
-            const uint32_t cf = sm.conflict;
-            if (ptid == 0) {
-                sm.par[(g + 1) & 1].cf = cf;
-                publish(&sm.i_cnt, g + 1);
+        // the verdicts on steps g+1 (final) and g+2 (first half); team C re-classifies on a conflict
+        if (ptid == 0) {
+            sm.cfv[(g + 1) & 3] |= sm.conflict;
+            sm.cfv[(g + 2) & 3] = sm.conflict2;
+            publish(&sm.i_cnt, g + 1);
+            ev(g, 7);
+            if (a.prof) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                a.prof[32 + 128 + 2 * g + 1] = t;
             }
-            tick(2);
         }
+        tick(2);
     }
     if (a.prof && ptid == 0)
         for (int q = 0; q < 12; ++q) a.prof[4 + q] = pf[q];
@@ -2026,11 +2117,11 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
     const bool ov = remap && dm.N <= 8 && dm.b < kPk16B && dm.B <= 4096 && dm.B % 4 == 0 && !profiling() &&
                     !std::getenv("LSG_DEBUG_SKIP") && !(ov_env && ov_env[0] == '0');
     a.smul = sc.get<uint32_t>(size_t(dm.B) * dm.N * (ov ? 2 : 1));
-    a.sx = sc.get<uint32_t>(ov ? size_t(dm.B) * 10 : size_t(dm.B) * std::max<uint32_t>(dm.N, 8u));  // D rows (+ ov: 2 parities + lists)
+    a.sx = sc.get<uint32_t>(ov ? size_t(dm.B) * 15 : size_t(dm.B) * std::max<uint32_t>(dm.N, 8u));  // D rows (+ ov: 3 sets + lists)
     a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B + 2 * 32 * kMaxN);
-    a.nb = ov ? sc.get<uint32_t>(dm.D) : nullptr;
+    a.nb = ov ? sc.get<uint32_t>(size_t(2) * dm.D) : nullptr;
     if (ov && !a.nb) return set_error(kInternal, "plan: scratch allocation failed");
-    if (ov) LSG_CUDA(cudaMemsetAsync(a.nb, 0xFF, dm.D * 4, st));
+    if (ov) LSG_CUDA(cudaMemsetAsync(a.nb, 0xFF, size_t(2) * dm.D * 4, st));
     if (!nu || !sb || !nr || !a.bm || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.dmoves)
         return set_error(kInternal, "plan: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(dm.N) * dm.D * 4, st));
@@ -2068,17 +2159,19 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
     if (!smem_items && !a.gitems) return set_error(kInternal, "plan: scratch allocation failed");
     a.prof = profiling() ? sc.get<unsigned long long>(16 + 256) : nullptr;
     a.dbg_skip = std::getenv("LSG_DEBUG_SKIP") ? std::atoi(std::getenv("LSG_DEBUG_SKIP")) : 0;
-    if (ov && std::getenv("LSG_OV_NOPF")) a.dbg_skip = 8;  // experiments: no L2 prefetch of batch g+2
+    if (ov && std::getenv("LSG_OV_NOPF")) a.dbg_skip = 8;  // experiments: no L2 prefetch of batch g+3
+    if (ov && std::getenv("LSG_OV_EVSTEP")) a.dbg_skip |= std::atoi(std::getenv("LSG_OV_EVSTEP")) << 8;
     if (a.prof) LSG_CUDA(cudaMemsetAsync(a.prof, 0, (16 + 256) * 8, st));
     const bool ov_prof = ov && std::getenv("LSG_PROFILE_OV");
     if (ov_prof) {
-        a.prof = sc.get<unsigned long long>(32);
+        a.prof = sc.get<unsigned long long>(32 + 8 * 16 + 2 * dm.T);
         if (!a.prof) return set_error(kInternal, "plan: scratch allocation failed");
-        LSG_CUDA(cudaMemsetAsync(a.prof, 0, 32 * 8, st));
+        LSG_CUDA(cudaMemsetAsync(a.prof, 0, (32 + 8 * 16 + 2 * dm.T) * 8, st));
     }
     if (ov) {
-        // two parity sets of the six per-step arrays (team D's CTA: its results, res [2][B] + mtot [2][32])
-        const size_t smem = std::max<size_t>(size_t(12) * dm.B, size_t(7) * dm.B + 2 * kMaxN + 16) * 4;
+        // team P: two parity sets of the six per-step arrays; CTA 0: team D's results, res [3][B] +
+        // mtot [3][32], and team C's five step arrays
+        const size_t smem = std::max<size_t>(size_t(12) * dm.B, size_t(8) * dm.B + 3 * kMaxN + 16) * 4;
         LSG_CUDA(cudaFuncSetAttribute(k_plan_loop_ov, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2);
@@ -2112,10 +2205,57 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
         const double T = double(dm.T ? dm.T : 1);
         fprintf(stderr, "[lsg ov] team D cyc/step: wait-classified %.0f  resolve %.0f  wait-verdict %.0f  publish %.0f\n",
                 h[0] / T, h[1] / T, h[2] / T, h[3] / T);
-        fprintf(stderr, "[lsg ov] team C cyc/step: wait-verdict %.0f  classify %.0f\n", h[20] / T, h[21] / T);
-        fprintf(stderr, "[lsg ov] team P cyc/step: wait-resolved %.0f  I2 %.0f  verdict+classify %.0f  other %.0f  "
+        fprintf(stderr, "[lsg ov] team C cyc/step: wait-verdict %.0f  classify %.0f  wait-copy %.0f  copy %.0f; "
+                "re-classified steps %llu\n", h[20] / T, h[21] / T, h[22] / T, h[23] / T, h[24]);
+        fprintf(stderr, "[lsg ov] team P cyc/step: wait D/copy %.0f  apply %.0f  I2 %.0f  verdict %.0f  other %.0f  "
                 "E %.0f  F %.0f  G1/G2 %.0f  H %.0f  I1 %.0f\n",
-                h[4] / T, h[5] / T, h[6] / T, h[7] / T, h[8] / T, h[9] / T, h[10] / T, h[11] / T, h[12] / T);
+                h[13] / T, h[4] / T, h[5] / T, h[6] / T, h[7] / T, h[8] / T, h[9] / T, h[10] / T, h[11] / T, h[12] / T);
+        unsigned long long e[8 * 16];
+        LSG_CUDA(cudaMemcpyAsync(e, a.prof + 32, sizeof e, cudaMemcpyDeviceToHost, st));
+        LSG_CUDA(cudaStreamSynchronize(st));
+        const uint32_t g0 = uint32_t(a.dbg_skip) >> 8;
+        if (dm.T >= g0 + 16) {
+            const unsigned long long z = e[0];
+            fprintf(stderr, "[lsg ov] ns from step %u's classify start: step | C classify | C copy | D resolve | P run\n", g0);
+            for (int q = 0; q < 16; ++q)
+                fprintf(stderr, "[lsg ov] %4u | %7lld %7lld | %7lld %7lld | %7lld %7lld | %7lld %7lld\n", g0 + q,
+                        (long long)(e[q * 8 + 0] - z), (long long)(e[q * 8 + 1] - z), (long long)(e[q * 8 + 2] - z),
+                        (long long)(e[q * 8 + 3] - z), (long long)(e[q * 8 + 4] - z), (long long)(e[q * 8 + 5] - z),
+                        (long long)(e[q * 8 + 6] - z), (long long)(e[q * 8 + 7] - z));
+        }
+        std::vector<unsigned long long> pt(2 * dm.T);
+        LSG_CUDA(cudaMemcpyAsync(pt.data(), a.prof + 32 + 128, pt.size() * 8, cudaMemcpyDeviceToHost, st));
+        LSG_CUDA(cudaStreamSynchronize(st));
+        std::vector<std::pair<long long, uint32_t>> waits;
+        long long wsum = 0, rsum = 0;
+        for (uint32_t g = 1; g < dm.T; ++g) {
+            const long long wt = (long long)(pt[2 * g] - pt[2 * g - 1]);
+            waits.push_back({wt, g});
+            wsum += wt;
+            rsum += (long long)(pt[2 * g + 1] - pt[2 * g]);
+        }
+        std::sort(waits.rbegin(), waits.rend());
+        fprintf(stderr, "[lsg ov] team P: run %.2f us/step, wait %.2f us/step; longest waits (us@step):", rsum / 1e3 / dm.T,
+                wsum / 1e3 / dm.T);
+        for (size_t q = 0; q < std::min<size_t>(24, waits.size()); ++q)
+            fprintf(stderr, " %.1f@%u", waits[q].first / 1e3, waits[q].second);
+        fprintf(stderr, "\n");
+        {  // by step in epoch (S steps)
+            std::vector<double> wb(dm.S, 0.0), rb(dm.S, 0.0);
+            for (uint32_t g = 1; g < dm.T; ++g) {
+                wb[g % dm.S] += (double)(long long)(pt[2 * g] - pt[2 * g - 1]);
+                rb[g % dm.S] += (double)(long long)(pt[2 * g + 1] - pt[2 * g]);
+            }
+            fprintf(stderr, "[lsg ov] team P wait/run us summed over epochs, by step in epoch:");
+            for (uint32_t q = 0; q < dm.S; ++q) fprintf(stderr, " %u:%.0f/%.0f", q, wb[q] / 1e3, rb[q] / 1e3);
+            fprintf(stderr, "\n");
+            const uint32_t E = uint32_t(dm.T / dm.S);
+            std::vector<double> we(E + 1, 0.0);
+            for (uint32_t g = 1; g < dm.T; ++g) we[g / dm.S] += (double)(long long)(pt[2 * g] - pt[2 * g - 1]);
+            fprintf(stderr, "[lsg ov] team P wait us by epoch:");
+            for (uint32_t q = 0; q < E; ++q) fprintf(stderr, " %.0f", we[q] / 1e3);
+            fprintf(stderr, "\n");
+        }
         a.prof = nullptr;
     }
     if (a.prof) {
