@@ -1658,14 +1658,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
     // ---------------------------------------------------- team P (CTA 1)
     {
     SmallOv& sm = sm_local;  // its own shared memory, addressed directly
-    for (int p = 0; p < 2; ++p) {
-        uint32_t* b0 = dyn + size_t(p) * 6 * a.B;
-        S2[p] = OvBufs{b0, b0 + a.B, b0 + 2 * a.B, b0 + 3 * a.B, b0 + 4 * a.B, b0 + 5 * a.B};
-    }
     const uint32_t pw = w, ptid = tid;
     size_t gbase = 0;
     for (uint32_t g = 0; g < a.T; ++g) {
-        const OvBufs& s = S2[g & 1];
+        // the step's arrays straight from the shared-memory symbol (not from the
+        // S2 table, which lives on the stack and would make every access generic)
+        uint32_t* b0 = dyn + size_t(g & 1) * 6 * a.B;
+        const OvBufs s{b0, b0 + a.B, b0 + 2 * a.B, b0 + 3 * a.B, b0 + 4 * a.B, b0 + 5 * a.B};
         OvPar& pp = sm.par[g & 1];
         const uint32_t len = min(a.B, a.keep - (g % a.S) * a.B);
         const uint32_t R = ((len + kPThreads - 1) / kPThreads) * 32;
