@@ -212,6 +212,15 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // buffer.cpp:37-41 (re-key) / :42-46 (insert) without the eviction: key
 // update plus the bucket / never-used summaries.
+// fire-and-forget global OR / AND (RED: no return value, so no scoreboard
+// entry; atomicOr with an unused result compiled to a returning ATOMG here)
+__device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_and(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t key_step(const LoopArgs& a, uint32_t pk) {
     return a.B == 1 ? pk : uint32_t(__umul64hi(pk, a.bdiv));
 }
@@ -222,13 +231,13 @@ __device__ __forceinline__ void set_key(const LoopArgs& a, SM& sm, uint32_t k, u
     a.key[size_t(k) * a.D + x] = pk;
     const uint32_t nu = pk == kNever ? kNever : key_step(a, pk), rank = pk - nu * a.B;
     if (nu != kNever)
-        atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
+        red_or(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
     if (nu == kNever) {
-        atomicOr(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
+        red_or(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
         atomicAdd(&sm.infcnt[k], 1u);
         atomicMax(&sm.inftop[k], x >> 5);
     } else {
-        atomicOr(&a.nz[size_t(k) * a.nzw + (nu >> 5)], 1u << (nu & 31));
+        red_or(&a.nz[size_t(k) * a.nzw + (nu >> 5)], 1u << (nu & 31));
         atomicMax(&sm.top[k], nu);
     }
 }
@@ -248,7 +257,7 @@ __device__ __forceinline__ void nb_check(const LoopArgs& a, SM& sm, uint32_t x) 
 template <class SM>
 __device__ __forceinline__ void drop(const LoopArgs& a, SM& sm, uint32_t k, uint32_t x) {
     a.key[size_t(k) * a.D + x] = kNone;
-    atomicAnd(&a.hm[x], ~(1u << k));
+    red_and(&a.hm[x], ~(1u << k));
     if (a.nb) nb_check(a, sm, x);
 }
 
@@ -1112,7 +1121,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 const uint32_t wd = nu >> 5;
                 if (nu != kNever && wd >= wbase && wd - wbase < kWinWords) {
                     a.key[size_t(k) * a.D + x] = pk;
-                    atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
+                    red_or(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
                     atomicOr(&sm.win[k][wd - wbase], 1u << (nu & 31));
                 } else {
                     set_key(a, sm, k, x, pk);
@@ -1123,7 +1132,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                 const uint32_t k = q / kWinWords, wd = q % kWinWords;
                 const uint32_t v = sm.win[k][wd];
                 if (v) {
-                    atomicOr(&a.nz[size_t(k) * a.nzw + wbase + wd], v);
+                    red_or(&a.nz[size_t(k) * a.nzw + wbase + wd], v);
                     atomicMax(&sm.top[k], (wbase + wd) * 32 + 31 - __clz(v));
                 }
             }
@@ -1170,7 +1179,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
                     if (mine) {
                         const uint32_t x = s.sx[j];
                         set_key(a, sm, k, x, s.snu[j]);
-                        if (!hitrun) atomicOr(&a.hm[x], 1u << k);
+                        if (!hitrun) red_or(&a.hm[x], 1u << k);
                     }
                     __syncwarp();
                     if (!hitrun) {
@@ -1960,7 +1969,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
                 const uint32_t wd = nu >> 5;
                 if (nu != kNever && wd >= wbase && wd - wbase < kWinWords) {
                     a.key[size_t(k) * a.D + x] = pk;
-                    atomicOr(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
+                    red_or(&a.bm[(size_t(k) * a.T + nu) * a.BW + (rank >> 5)], 1u << (rank & 31));
                     atomicOr(&sm.win[k][wd - wbase], 1u << (nu & 31));
                 } else {
                     set_key(a, sm, k, x, pk);
@@ -1971,7 +1980,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
                 const uint32_t k = q / kWinWords, wd = q % kWinWords;
                 const uint32_t v = sm.win[k][wd];
                 if (v) {
-                    atomicOr(&a.nz[size_t(k) * a.nzw + wbase + wd], v);
+                    red_or(&a.nz[size_t(k) * a.nzw + wbase + wd], v);
                     atomicMax(&sm.top[k], (wbase + wd) * 32 + 31 - __clz(v));
                 }
             }
@@ -2015,7 +2024,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
                         const uint32_t x = s.sx[j];
                         set_key(a, sm, k, x, s.snu[j]);
                         if (!hitrun) {
-                            atomicOr(&a.hm[x], 1u << k);
+                            red_or(&a.hm[x], 1u << k);
                             nb_check(a, sm, x);
                         }
                     }
