@@ -2122,8 +2122,12 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
     // the overlapped loop (K6o): team D resolves step g+1 while team P
     // advances step g and classifies step g+2 (LSG_PLAN_OV=0: the plain loop)
     const char* ov_env = std::getenv("LSG_PLAN_OV");
+    // (below B = 2048 the team hand-offs cost more than the overlap wins: cfg4, B = 512, 7.8 s
+    // overlapped vs 5.4 s; cfg1, B = 256, 35 vs 22.5 ms)
+    // LSG_PLAN_OV=1 forces it for any B the kernel supports (tests), =0 turns it off
     const bool ov = remap && dm.N <= 8 && dm.b < kPk16B && dm.B <= 4096 && dm.B % 4 == 0 && !profiling() &&
-                    !std::getenv("LSG_DEBUG_SKIP") && !(ov_env && ov_env[0] == '0');
+                    !std::getenv("LSG_DEBUG_SKIP") && !(ov_env && ov_env[0] == '0') &&
+                    (dm.B >= 2048 || (ov_env && ov_env[0] == '1'));
     a.smul = sc.get<uint32_t>(size_t(dm.B) * dm.N * (ov ? 2 : 1));
     a.sx = sc.get<uint32_t>(ov ? size_t(dm.B) * 15 : size_t(dm.B) * std::max<uint32_t>(dm.N, 8u));  // D rows (+ ov: 3 sets + lists)
     a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B + 2 * 32 * kMaxN);

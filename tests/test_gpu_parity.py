@@ -221,6 +221,33 @@ def test_plan_errors(ls):
         ls.plan_schedule(to_pc(ls, O.Cfg(4, 2, 2, 4, buffer_capacity=3)))
 
 
+@pytest.mark.parametrize("seed", range(24))
+def test_plan_overlapped_loop_forced(ls, seed):
+    """The overlapped step loop (K6o: classify / resolve / advance pipelined
+    over three steps, stamps for two pending batches, re-classification on a
+    conflict) runs by default only for B >= 2048; LSG_PLAN_OV=1 forces it on
+    small random shapes: 1-3 step jobs, ragged last batches (drop_last off),
+    every N <= 8 (B % 4 == 0), tight and loose buffers."""
+    import os
+    r = random.Random(7000 + seed)
+    while True:
+        N, b = r.choice([1, 2, 3, 4, 5, 8]), r.choice([4, 8, 12, 16, 32, 64])
+        if (N * b) % 4 == 0:
+            break
+    B = N * b
+    D = B * r.choice([1, 2, 3, 7, 20]) + (r.randint(0, B - 1) if seed % 3 else 0)
+    c = O.Cfg(D, r.randint(1, 7), N, b, seed=r.randint(0, 10**6),
+              buffer_capacity=r.randint(1, max(1, D // r.choice([1, 2, 4, 8]))),
+              drop_last=r.random() < 0.5, graph_mode=r.choice(["global", "pernode"]),
+              optim_order=r.random() < 0.8, optim_remap=True,
+              optim_balance=r.random() < 0.85, optim_chunk=r.random() < 0.5, pso_iters=30)
+    os.environ["LSG_PLAN_OV"] = "1"
+    try:
+        check_plan(ls, c)
+    finally:
+        del os.environ["LSG_PLAN_OV"]
+
+
 @pytest.mark.parametrize("D,E,N,b,frac,seed", [(65536, 3, 32, 512, 0.5 / 32, 1), (40000, 4, 16, 1000, 0.03, 2),
                                                (32768 + 777, 3, 32, 300, 0.02, 3)])
 @pytest.mark.parametrize("kernel", ["0", "1"])
