@@ -732,8 +732,7 @@ def main():
                                          "8 ranks on one GPU) from profiles/gather_traffic.json (r02b_fetch_persist.ncu-rep); "
                                          f"{traffic_ratio:.3f} x that launch's algorithmic bytes" if traffic else None,
                          "kernel": "fetch phase (k_fetch_fused: persistent multi-step TMA bulk-copy pipeline, "
-                                   "producer/consumer warps, hits and misses; + k_deferred_slots / k_job_misses "
-                                   "where needed)",
+                                   "producer/consumer warps: hits, misses and deferred slot fills)",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks else "fallback 6650"},
             "gpu_launches": int(launches),
             **({"timeline_plan0_plan1_rep0_rep1_fetch0_fetch1": timeline} if timeline else {}),

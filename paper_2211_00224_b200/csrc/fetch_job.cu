@@ -73,6 +73,11 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ uint64_t ld_acquire64(const uint32_t* p) {  // (8-byte aligned)
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -368,8 +373,8 @@ __global__ void __launch_bounds__(256) k_job_misses(MissArgs a) {
 //                has finished (programmatic dependent launch);
 //   kRowInplace  a kept miss whose slot was not read by a hit of the same
 //                step: its slot is written by this kernel, beside the batch
-//                row; other kept misses are written to their slot from the
-//                batch row by k_deferred_slots once the step's kernel is done.
+//                row; other kept misses are written to their slot in the
+//                step's deferred-fill phase, after the step's hits.
 constexpr uint32_t kRowEarly = 1u, kRowInplace = 2u;
 
 struct FlagArgs {
@@ -469,6 +474,37 @@ __global__ void __launch_bounds__(256) k_row_flags(FlagArgs a) {
     if (threadIdx.x == 0) a.ndefer[gi] = ndef;
 }
 
+// the deferred slot writes of every step as a list (rows in order, step gi's
+// at doff[gi]): kept misses whose slot a hit of the same step reads
+__global__ void __launch_bounds__(256) k_defer_list(FlagArgs a, const uint32_t* __restrict__ doff,
+                                                    uint32_t* __restrict__ drow) {
+    __shared__ uint32_t wc[8], carry;
+    const uint32_t gi = blockIdx.x;
+    const uint32_t* off = a.node_off + size_t(gi) * (a.N + 1);
+    const uint64_t b = a.base[gi];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = doff[gi];
+    __syncthreads();
+    for (uint32_t c = off[a.k0]; c < off[a.k1]; c += blockDim.x) {
+        const uint32_t r = c + threadIdx.x;
+        bool d = false;
+        if (r < off[a.k1]) {
+            const uint32_t sl = a.slots[b + r];
+            d = !sl_hit(sl) && sl != kNever && !(a.flags[b + r] & kRowInplace);
+        }
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, d);
+        if (lane == 0) wc[w] = __popc(bal);
+        __syncthreads();
+        uint32_t pre = carry;
+        for (uint32_t q = 0; q < w; ++q) pre += wc[q];
+        if (d) drow[pre + __popc(bal & ((1u << lane) - 1))] = r;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (uint32_t q = 0; q < blockDim.x / 32; ++q) carry += wc[q];
+        __syncthreads();
+    }
+}
+
 constexpr int kFTile = 8192, kFStages = 6, kFLag = 2, kFChunk = 16, kFTail = 4;
 constexpr unsigned kFCtasPerSm = 4;
 
@@ -483,15 +519,19 @@ struct FusedStep {
     unsigned char* const* outs;
     uint32_t k0, k1;
     uint64_t row_bytes, seed;
-    uint32_t* claim;            // [ns] tile claims per step
-    uint32_t* stored;           // [ns] tiles stored per step (a step is done when all are)
+    uint32_t* claim;            // [2ns] tile claims per phase
+    uint32_t* stored;           // [2ns] tiles NOT yet stored per phase (done at 0; 8-byte aligned pairs)
+    const uint32_t* ptiles;     // [2ns] tiles per phase
+    const uint32_t* ndefer;     // [ns] deferred slot writes per step
+    const uint32_t* doff;       // [ns+1] their list offsets
+    const uint32_t* drow;       // their rows (step-relative)
     const unsigned char* ring;  // host-tier misses (null: synthesised payload)
     uint32_t R;
     const uint32_t* ready;
     const uint32_t* seq0;
     const uint32_t* moff;       // [ns+1] job miss offsets
     uint32_t* consumed;         // ring sequence numbers released
-    uint32_t gA, gB;            // the kernel's steps [gA, gB) of the job
+    uint32_t gA, gB;            // the kernel's steps [gA, gB) of the job (phases [2gA, 2gB))
     int skip_misses;            // misses left to k_job_misses (large synthesised rows)
 };
 
@@ -511,19 +551,26 @@ __device__ __forceinline__ uint32_t fnode_of_row(const uint32_t* off, uint32_t k
 // over through full (TMA transaction) and empty (store has read the stage)
 // mbarriers.
 //
-// CTAs claim tile chunks step after step, so a CTA that runs out of work in
-// step s starts loading step s+1 while others finish s. Ordering, with rdy =
-// the number of leading steps whose tiles are all stored (per-step counters):
-//   a hit tile of step s loads once rdy >= s, or rdy >= s-1 for an early row
-//     (its slot was not filled in step s-1) and for a miss (reads no slot);
-//   every store of step s waits for rdy >= s (step s-1's slot fills, and
-//     its reads of slots this step overwrites, are done; batch rows reused).
+// Work is a sequence of PHASES: phase 2s is step s (every row of the step);
+// phase 2s+1 writes the step's deferred slots (kept misses whose slot a hit
+// of step s reads: their payload again, into the slot only, once every hit
+// of step s has been loaded). CTAs claim tile chunks phase after phase, so a
+// CTA that runs out of work in one phase starts loading the next while
+// others finish. Ordering, with rdy = the number of leading phases whose
+// tiles are all stored (per-phase counters), for a tile of phase P:
+//   a hit loads once rdy >= P, or rdy >= P-2 for an early row (its slot was
+//     not filled in step s-1); a miss or a deferred fill (reads no slot)
+//     loads once rdy >= P-2;
+//   every store waits for rdy >= P (earlier slot fills, and the reads of
+//     slots this phase overwrites, are done; batch rows reused).
 // Tiles, not CTAs, are counted, so a CTA that never became resident holds
 // nothing anyone waits for; a consumer with nothing to store publishes what
-// it holds before waiting. Before griddepcontrol.wait, rdy = gA - 1: the
-// previous kernel (the previous steps, or their deferred slot writes) runs
-// at most one step behind.
-template <int S, int L>
+// it holds before waiting. Before griddepcontrol.wait, rdy = 2gA - 2: the
+// previous kernel runs at most its last step (both phases) behind.
+// PP = phases per step: 2, or 1 when the job has no deferred slot writes (the
+// odd phases would all be empty; skipping them saves ~1 us per step at one
+// rank per GPU). Per-phase arrays are indexed 2s (+1), whatever PP.
+template <int S, int L, int PP>
 __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
     extern __shared__ __align__(128) unsigned char fsm2[];
     __shared__ __align__(8) unsigned long long full[S], empty[S];
@@ -543,25 +590,54 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
     __syncthreads();
     const uint32_t tpr = uint32_t(f.row_bytes / kFTile);
     const uint32_t s0 = f.ring ? __ldg(f.seq0) : 0u;
-    const int gA = int(f.gA), gB = int(f.gB);  // (steps before gA may end in deferred slot writes: never polled)
-    auto step_tiles = [&](int s) -> uint32_t {
-        const uint32_t* o = f.node_off + size_t(s) * (f.N + 1);
-        return (__ldg(&o[f.k1]) - __ldg(&o[f.k0])) * tpr;
-    };
-    int rdy = gA - 1;
-    auto poll = [&]() -> bool {  // advance rdy over completed steps (all lanes: the warp stays converged)
+    const int PA = PP * int(f.gA), PB = PP * int(f.gB);  // (phases before PA: never polled)
+    auto ix = [](int P) -> int { return PP == 2 ? P : 2 * P; };  // a phase's slot in the per-phase arrays
+    int rdy = PA - PP;
+    // advance rdy over completed phases (all lanes: the warp stays converged); one
+    // acquire load covers a step's two phases, so an empty deferred-fill phase is free
+    auto poll = [&]() -> bool {
         const int r0 = rdy;
-        while (rdy >= gA && rdy < gB && ld_acquire(&f.stored[rdy]) == step_tiles(rdy)) ++rdy;
+        while (rdy >= PA && rdy < PB) {
+            const uint64_t v = ld_acquire64(&f.stored[ix(rdy) & ~1]);
+            if (PP == 1 || !(rdy & 1)) {
+                if (uint32_t(v)) break;
+                if (++rdy >= PB || PP == 1) continue;
+            }
+            if (uint32_t(v >> 32)) break;
+            ++rdy;
+        }
         if (rdy != r0) asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads see those stores
         return rdy != r0;
     };
     if (warp == 0) {
         // ---------------- producer ----------------
         const uint32_t guide = gridDim.x * 2 * kFChunk;
-        int sc = gA;
-        const uint32_t* off_s = f.node_off + size_t(sc) * (f.N + 1);
-        uint32_t r0 = __ldg(&off_s[f.k0]), bs = __ldg(&f.base[sc]);
-        uint32_t nt = step_tiles(sc), te = 0, tn = 0, cur = 0xFFFFFFFFu;
+        int sc = PA;  // the claim cursor's phase
+        const uint32_t* off_s = f.node_off + size_t(sc / PP) * (f.N + 1);
+        uint32_t r0 = __ldg(&off_s[f.k0]), bs = __ldg(&f.base[sc / PP]), db = 0;
+        // a step's two phase sizes in one load (ptiles is 8-byte aligned)
+        uint2 pt = __ldg(reinterpret_cast<const uint2*>(f.ptiles + ix(sc)));
+        uint32_t nt = pt.x, te = 0, tn = 0, cur = 0xFFFFFFFFu;
+        // the next phase with tiles; an odd phase shares its step's offsets, and
+        // an empty one (no deferred fills: the common case) costs one load
+        auto advance = [&]() -> bool {
+            for (;;) {
+                if (++sc >= PB) return false;
+                te = tn = 0;
+                if (PP == 2 && (sc & 1)) {
+                    nt = pt.y;
+                    if (nt == 0) continue;
+                    db = __ldg(&f.doff[sc >> 1]);
+                    return true;
+                }
+                pt = __ldg(reinterpret_cast<const uint2*>(f.ptiles + ix(sc)));
+                off_s = f.node_off + size_t(sc / PP) * (f.N + 1);
+                r0 = __ldg(&off_s[f.k0]);
+                bs = __ldg(&f.base[sc / PP]);
+                nt = pt.x;
+                if (nt) return true;
+            }
+        };
         int cur_step = -1;
         const unsigned char* src_row = nullptr;
         unsigned char* dst_row = nullptr;
@@ -571,19 +647,18 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
         // the next tile's row state; 1 = ready, 0 = not yet (inputs not final), -1 = no more tiles
         auto next = [&]() -> int {
             for (;;) {
-                if (tn >= te) {  // a new chunk: this step's, else the next step's
-                    if (sc >= gB) return -1;
+                if (tn >= te) {  // a new chunk: this phase's, else the next phase's
+                    if (sc >= PB) return -1;
+                    if (nt == 0) {  // an empty phase: no claim
+                        if (!advance()) return -1;
+                        continue;
+                    }
                     uint32_t v = 0;
                     const uint32_t sz = (nt > te ? nt - te : 0u) > guide ? kFChunk : kFTail;
-                    if (lane == 0) v = atomicAdd(&f.claim[sc], sz);
+                    if (lane == 0) v = atomicAdd(&f.claim[ix(sc)], sz);
                     const uint32_t tb = __shfl_sync(0xFFFFFFFFu, v, 0);
                     if (tb >= nt) {
-                        if (++sc >= gB) return -1;
-                        off_s = f.node_off + size_t(sc) * (f.N + 1);
-                        r0 = __ldg(&off_s[f.k0]);
-                        bs = __ldg(&f.base[sc]);
-                        nt = step_tiles(sc);
-                        te = tn = 0;
+                        if (!advance()) return -1;
                         continue;
                     }
                     te = min(nt, tb + sz);
@@ -591,15 +666,16 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
                 }
                 const uint32_t rr = tn / tpr;
                 if (rr != cur || sc != cur_step) {
-                    const uint32_t r = r0 + rr;
+                    const bool fill = PP == 2 && (sc & 1);  // a deferred slot write of step sc/2
+                    const uint32_t r = fill ? __ldg(&f.drow[db + rr]) : r0 + rr;
                     const uint32_t sl = __ldg(&f.slots[bs + r]);
                     const uint32_t fl = __ldg(&f.flags[bs + r]);
-                    const bool hit = sl_hit(sl);
+                    const bool hit = !fill && sl_hit(sl);
                     if (!hit && f.skip_misses) {  // k_job_misses writes this row: skip its tiles
                         tn = (rr + 1) * tpr;
                         continue;
                     }
-                    const int need = (!hit || (fl & kRowEarly)) ? sc - 1 : sc;
+                    const int need = (!hit || (fl & kRowEarly)) ? sc - PP : sc;
                     if (rdy < need && (!poll() || rdy < need)) return 0;
                     cur = rr;
                     cur_step = sc;
@@ -609,10 +685,15 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
                     row_id = __ldg(&f.items[bs + r]) & ~kHit;
                     row_ready = false;
                     src_row = hit ? f.bufs[kk - f.k0] + uint64_t(sl & ~kHit) * f.row_bytes : nullptr;
-                    dst_row = f.outs[kk - f.k0] + uint64_t(r - __ldg(&off_s[kk])) * f.row_bytes;
-                    dst2_row = (!hit && sl != kNever && (fl & kRowInplace))
-                                   ? f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes
-                                   : nullptr;
+                    if (fill) {  // the slot only
+                        dst_row = f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes;
+                        dst2_row = nullptr;
+                    } else {
+                        dst_row = f.outs[kk - f.k0] + uint64_t(r - __ldg(&off_s[kk])) * f.row_bytes;
+                        dst2_row = (!hit && sl != kNever && (fl & kRowInplace))
+                                       ? f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes
+                                       : nullptr;
+                    }
                 }
                 if (!row_hit && f.ring && !row_ready) {  // host-tier miss: wait for the prefetcher's row
                     uint32_t ok = 0;
@@ -628,11 +709,11 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
         for (;;) {
             const int n = next();
             if (n < 0) break;
-            if (n == 0) {  // blocked on earlier steps or a ring row
+            if (n == 0) {  // blocked on earlier phases or a ring row
                 if (!waited) {
                     asm volatile("griddepcontrol.wait;" ::: "memory");
                     waited = true;
-                    rdy = max(rdy, gA);
+                    rdy = max(rdy, PA);
                 } else if (!poll()) {
                     __nanosleep(100);
                 }
@@ -679,19 +760,19 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
             if (!waited && k == uint32_t(S)) {  // every stage was free: the rest waits for the previous kernel
                 asm volatile("griddepcontrol.wait;" ::: "memory");
                 waited = true;
-                rdy = max(rdy, gA);
+                rdy = max(rdy, PA);
             }
-            if (!trig && rdy >= gB - 1) {  // the next kernel assumes at most step gB-1 still runs
+            if (!trig && rdy >= PB - PP) {  // the next kernel assumes at most step gB-1 still runs
                 asm volatile("griddepcontrol.launch_dependents;");
                 trig = true;
             }
         }
         if (!waited) {
             asm volatile("griddepcontrol.wait;" ::: "memory");
-            rdy = max(rdy, gA);
+            rdy = max(rdy, PA);
         }
         if (!trig) {
-            while (rdy < gB - 1)
+            while (rdy < PB - PP)
                 if (!poll()) __nanosleep(128);
             asm volatile("griddepcontrol.launch_dependents;");
         }
@@ -701,7 +782,7 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
     } else {
         // ---------------- consumer ----------------
         asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel on the stream is done
-        rdy = max(rdy, gA);
+        rdy = max(rdy, PA);
         int pend = -1;
         uint32_t pend_cnt = 0, freed = 0, k = 0;
         auto release = [&](uint32_t upto) {  // stages [freed, upto) have been read by their stores
@@ -711,15 +792,16 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
                     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[i % S])) : "memory");
             freed = upto;
         };
-        auto publish = [&]() {  // this warp's stores of step pend have landed: count them
+        auto publish = [&]() {  // this warp's stores of phase pend have landed: count them
             if (pend_cnt) {
                 if (lane == 0) {
                     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                     __threadfence();
-                    const uint32_t old = atomicAdd(&f.stored[pend], pend_cnt);
-                    if (f.ring && old + pend_cnt == step_tiles(pend))  // every ring row of the step has landed
-                        atomicMax(f.consumed, s0 + __ldg(&f.moff[pend + 1]));
+                    const uint32_t left = atomicSub(&f.stored[ix(pend)], pend_cnt) - pend_cnt;
+                    // every ring row of step pend/2 has landed (in its deferred fills too, if any)
+                    if (f.ring && left == 0 && (PP == 1 || (pend & 1) || !__ldg(&f.ptiles[pend + 1])))
+                        atomicMax(f.consumed, s0 + __ldg(&f.moff[pend / PP + 1]));
                 }
                 __syncwarp();
                 release(k);
@@ -770,37 +852,6 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
     }
 }
 
-// kept misses whose slot a hit of the same step read: batch row -> slot,
-// after the step's kernel
-struct DeferArgs {
-    const uint32_t* slots;
-    const uint32_t* flags;
-    const uint32_t* node_off;
-    const uint32_t* mrow;
-    const uint32_t* moff;
-    uint32_t gi, k0, k1;
-    unsigned char* const* bufs;
-    unsigned char* const* outs;
-    uint64_t vpr;
-};
-
-__global__ void __launch_bounds__(256) k_deferred_slots(DeferArgs a) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the step's fused kernel is done
-    asm volatile("griddepcontrol.launch_dependents;");
-    const uint32_t m0 = a.moff[a.gi], m1 = a.moff[a.gi + 1];
-    for (uint32_t m = m0 + blockIdx.y; m < m1; m += gridDim.y) {
-        const uint32_t r = a.mrow[m];
-        const uint32_t sl = a.slots[r];
-        if (sl == kNever || (a.flags[r] & kRowInplace)) continue;
-        uint32_t k = a.k0;
-        while (k + 1 < a.k1 && a.node_off[k + 1] <= r) ++k;
-        const uint4* src = reinterpret_cast<const uint4*>(a.outs[k - a.k0]) + uint64_t(r - a.node_off[k]) * a.vpr;
-        uint4* dst = reinterpret_cast<uint4*>(a.bufs[k - a.k0]) + uint64_t(sl) * a.vpr;
-        for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < a.vpr; p += uint64_t(gridDim.x) * blockDim.x)
-            __stcs(&dst[p], __ldcg(&src[p]));
-    }
-}
-
 // a job's place in a shared miss stream: its misses take the next M sequence
 // numbers (jobs reserve in the order their fetches run)
 __global__ void k_reserve(const uint32_t* __restrict__ total, uint32_t* __restrict__ next_seq,
@@ -834,7 +885,7 @@ struct lsg_fetch_job {
     uint64_t nsteps = 0;
     // device state (stream-ordered pool)
     uint32_t* d_base = nullptr;  // [nsteps+1] job-relative step bases
-    uint32_t* d_ctl = nullptr;   // claims [ns] | done [ns] | cnt [ns] | moff [ns+1] | consumed | seq0 | pf_done | ctas
+    uint32_t* d_ctl = nullptr;   // claims [2ns] | done [2ns] | cnt [ns] | moff [ns+1] | consumed | seq0 | pf_done | ctas
     uint32_t* mrow = nullptr;
     uint32_t* mid = nullptr;
     unsigned char* ring = nullptr;  // the job's own ring, or the shared stream's
@@ -847,6 +898,10 @@ struct lsg_fetch_job {
     bool fused = false;
     uint32_t* flags = nullptr;       // [job items] row flags
     uint32_t* ndefer_d = nullptr;    // [ns]
+    uint32_t* doff = nullptr;        // [ns+1] deferred rows before each step
+    uint32_t* ptiles = nullptr;      // [2ns] tiles per phase (step s: 2s rows, 2s+1 deferred fills)
+    uint64_t ndefer_rows = 0;        // deferred slot writes in the job
+    uint32_t* drow = nullptr;        // the deferred rows, step by step (step-relative)
     std::vector<uint32_t> ndefer;    // deferred slot writes per step (host)
     bool skip_misses = false;        // fused kernel does hits only; k_job_misses after it
     unsigned long long* stats = nullptr;
@@ -1038,16 +1093,16 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
     const uint64_t ns = j->nsteps;
     auto alloc = [&](void** p, size_t bytes) { return cudaMallocAsync(p, std::max<size_t>(bytes, 16), st) == cudaSuccess; };
     if (!alloc(reinterpret_cast<void**>(&j->d_base), (ns + 1) * 4) ||
-        !alloc(reinterpret_cast<void**>(&j->d_ctl), (4 * ns + 5) * 4) ||
+        !alloc(reinterpret_cast<void**>(&j->d_ctl), (6 * ns + 5) * 4) ||
         !alloc(reinterpret_cast<void**>(&j->stats), 32) ||
         !alloc(reinterpret_cast<void**>(&j->mrow), total_rows * 4) ||
         !alloc(reinterpret_cast<void**>(&j->mid), total_rows * 4))
         return fail(set_error(kInternal, "fetch_job: device allocation failed"));
-    if (cudaMemsetAsync(j->d_ctl, 0, (4 * ns + 5) * 4, st) != cudaSuccess ||
+    if (cudaMemsetAsync(j->d_ctl, 0, (6 * ns + 5) * 4, st) != cudaSuccess ||
         cudaMemsetAsync(j->stats, 0, 32, st) != cudaSuccess)
         return fail(cuda_error(cudaGetLastError(), "fetch_job setup"));
-    uint32_t* cnt = j->d_ctl + 2 * ns;
-    uint32_t* moff = j->d_ctl + 3 * ns;
+    uint32_t* cnt = j->d_ctl + 4 * ns;
+    uint32_t* moff = j->d_ctl + 5 * ns;
     if (ns) {
         const uint32_t* noff = d.d_node_off + d.step_begin * (N + 1);
         k_scan_u32<<<1, 1024, 0, st>>>(noff + N, uint32_t(ns), N + 1, j->d_base);  // step bases
@@ -1088,7 +1143,9 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
         cudaGetDevice(&dev);
         if (!(attr_done.load() & (1ull << (dev & 63)))) {
             cudaFuncSetAttribute(k_row_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16384 * 4);
-            cudaFuncSetAttribute(k_fetch_fused<kFStages, kFLag>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaFuncSetAttribute(k_fetch_fused<kFStages, kFLag, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kFTile * kFStages);
+            cudaFuncSetAttribute(k_fetch_fused<kFStages, kFLag, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kFTile * kFStages);
             attr_done.fetch_or(1ull << (dev & 63));
         }
@@ -1104,6 +1161,35 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
             cudaStreamSynchronize(st) != cudaSuccess)
             return fail(cuda_error(cudaGetLastError(), "fetch_job: deferred counts"));
         j->ndefer.assign(static_cast<uint32_t*>(hb), static_cast<uint32_t*>(hb) + ns);
+        {  // their list, for the fused kernel's deferred-fill phases
+            // ptiles [2ns] | doff [ns+1], uploaded together; ptiles also seeds the
+            // per-phase remaining-tile counters (d_ctl's done region)
+            const uint64_t tpr = d.sample_bytes / kFTile;
+            std::vector<uint32_t> up(3 * ns + 1, 0);
+            for (uint64_t g = 0; g < ns; ++g) {
+                up[2 * g] = uint32_t(j->rows[g] * tpr);
+                up[2 * g + 1] = j->skip_misses ? 0u : uint32_t(j->ndefer[g] * tpr);
+                up[2 * ns + g + 1] = up[2 * ns + g] + j->ndefer[g];
+            }
+            if (!alloc(reinterpret_cast<void**>(&j->ptiles), up.size() * 4) ||
+                !alloc(reinterpret_cast<void**>(&j->drow), size_t(up[3 * ns]) * 4))
+                return fail(set_error(kInternal, "fetch_job: device allocation failed"));
+            j->doff = j->ptiles + 2 * ns;
+            void* hd = pinned_bounce(up.size() * 4);  // (a pageable copy can wait for other streams' kernels)
+            if (!hd) return fail(set_error(kInternal, "fetch_job: pinned bounce buffer"));
+            std::memcpy(hd, up.data(), up.size() * 4);
+            if (cudaMemcpyAsync(j->ptiles, hd, up.size() * 4, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+                cudaMemcpyAsync(j->d_ctl + 2 * ns, j->ptiles, 2 * ns * 4, cudaMemcpyDeviceToDevice, st) !=
+                    cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess)
+                return fail(cuda_error(cudaGetLastError(), "fetch_job: deferred offsets"));
+            j->ndefer_rows = up[3 * ns];
+            if (up[3 * ns]) {
+                k_defer_list<<<unsigned(ns), 256, 0, st>>>(fa, j->doff, j->drow);
+                count_launch();
+                if (cudaError_t e = cudaGetLastError(); e != cudaSuccess) return fail(cuda_error(e, "k_defer_list"));
+            }
+        }
         if (std::getenv("LSG_FETCH_VERBOSE")) {
             uint64_t steps = 0, rows = 0;
             for (uint32_t v : j->ndefer) steps += v != 0, rows += v;
@@ -1114,7 +1200,7 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
     cudaEventCreateWithFlags(&j->listed, cudaEventDisableTiming);
     cudaEventRecord(j->listed, st);
     if (d.host && ns && total_rows) {
-        j->seq0 = j->d_ctl + 4 * ns + 2;
+        j->seq0 = j->d_ctl + 6 * ns + 2;
         if (lsg_miss_stream* ms = d.misses) {  // the shared ring: reserve the job's sequence numbers
             if (ms->sample_bytes != d.sample_bytes)
                 return fail(set_error(kValidation, "fetch_job: miss stream differs in sample size"));
@@ -1143,15 +1229,15 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
                 return fail(set_error(kInternal, "fetch_job: ring allocation failed"));
             if (cudaMemsetAsync(j->ready, 0, R * 4, st) != cudaSuccess)
                 return fail(cuda_error(cudaGetLastError(), "fetch_job ring"));
-            j->consumed = j->d_ctl + 4 * ns + 1;
-            j->pf_done = j->d_ctl + 4 * ns + 3;
+            j->consumed = j->d_ctl + 6 * ns + 1;
+            j->pf_done = j->d_ctl + 6 * ns + 3;
         }
         j->resident = resident_acquire(&j->resident_idx);
         if (!j->resident) return fail(set_error(kInternal, "fetch_job: no residency counter"));
         unsigned int* dres = nullptr;
         cudaHostGetDevicePointer(reinterpret_cast<void**>(&dres), j->resident, 0);
         PrefetchArgs pa{d.host->dev, j->mid, moff + ns, d.sample_bytes, j->ring, j->R, j->ready,
-                        j->consumed, dres, j->seq0, j->pf_done, j->d_ctl + 4 * ns + 4};
+                        j->consumed, dres, j->seq0, j->pf_done, j->d_ctl + 6 * ns + 4};
         static const bool lsu = [] {  // LSG_PF_LSU=1: 128-bit loads instead of TMA
             const char* e = std::getenv("LSG_PF_LSU");
             return e && e[0] == '1';
@@ -1196,19 +1282,18 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
     const lsg_fetch_job_desc& d = j->d;
     const uint32_t N = d.N, ns = uint32_t(j->nsteps);
     if (j->listed) LSG_CUDA(cudaStreamWaitEvent(st, j->listed, 0));  // NOT the prefetcher: it needs these kernels
-    uint32_t* claims = j->d_ctl;
-    uint32_t* done = j->d_ctl + ns;
-    uint32_t* moff = j->d_ctl + 3 * ns;
+    uint32_t* claims = j->d_ctl;      // [2ns]: per step, or per phase (fused)
+    uint32_t* done = j->d_ctl + 2 * ns;
+    uint32_t* moff = j->d_ctl + 5 * ns;
     if (j->fused) {
-        // one persistent launch per run of steps, cut after every step with
-        // deferred slot writes (k_deferred_slots) and, for large synthesised
-        // rows, after every step (k_job_misses)
+        // one persistent launch per run of steps (and, with LSG_FETCH_SKIP=1,
+        // one per step followed by k_job_misses)
         FusedStep fs{d.d_items + j->base[0], d.d_slots + j->base[0], j->flags,
                      d.d_node_off + d.step_begin * (N + 1), j->d_base, N,
                      reinterpret_cast<unsigned char* const*>(d.d_bufs),
                      reinterpret_cast<unsigned char* const*>(d.d_outs), d.node_begin, d.node_end, d.sample_bytes,
-                     d.fill_seed, claims, done, j->ring, j->R, j->ready, j->seq0, moff, j->consumed, 0, 0,
-                     j->skip_misses ? 1 : 0};
+                     d.fill_seed, claims, done, j->ptiles, j->ndefer_d, j->doff, j->drow, j->ring, j->R, j->ready,
+                     j->seq0, moff, j->consumed, 0, 0, j->skip_misses ? 1 : 0};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1233,17 +1318,22 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
             const char* e = std::getenv("LSG_FETCH_CPS");
             return e ? unsigned(std::max(1, std::atoi(e))) : kFCtasPerSm;
         }();
-        auto kern = nst == 5 ? k_fetch_fused<5, 2> : nst == 12 ? k_fetch_fused<12, 3> : k_fetch_fused<kFStages, kFLag>;
+        const bool fills = j->ndefer_rows > 0;  // deferred-fill phases needed
+        auto kern = nst == 5    ? (fills ? k_fetch_fused<5, 2, 2> : k_fetch_fused<5, 2, 1>)
+                    : nst == 12 ? (fills ? k_fetch_fused<12, 3, 2> : k_fetch_fused<12, 3, 1>)
+                                : (fills ? k_fetch_fused<kFStages, kFLag, 2> : k_fetch_fused<kFStages, kFLag, 1>);
         static std::atomic<uint32_t> vattr{0};
         if (!(vattr.fetch_or(1u) & 1u)) {
-            cudaFuncSetAttribute(k_fetch_fused<5, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFTile * 5);
-            cudaFuncSetAttribute(k_fetch_fused<12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFTile * 12);
+            for (auto kf : {k_fetch_fused<5, 2, 1>, k_fetch_fused<5, 2, 2>})
+                cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kFTile * 5);
+            for (auto kf : {k_fetch_fused<12, 3, 1>, k_fetch_fused<12, 3, 2>})
+                cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, kFTile * 12);
         }
         for (uint32_t ga = 0; ga < ns;) {
             uint32_t gb = ga + 1;
             const uint64_t tpr = d.sample_bytes / kFTile;
             uint64_t tiles = j->rows[ga] * tpr;
-            while (gb < ns && !j->skip_misses && !j->ndefer[gb - 1] && tiles + j->rows[gb] * tpr <= seg_tiles)
+            while (gb < ns && !j->skip_misses && tiles + j->rows[gb] * tpr <= seg_tiles)
                 tiles += j->rows[gb++] * tpr;
             fs.gA = ga;
             fs.gB = gb;
@@ -1277,20 +1367,6 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
                                 unsigned(std::min<uint64_t>(j->rows[gl], 148)));
                 k_job_misses<<<grid, 256, 0, st>>>(ma);
                 LSG_LAUNCH_CHECK("k_job_misses");
-            } else if (j->ndefer[gl]) {
-                DeferArgs da{d.d_slots + j->base[gl], j->flags + (j->base[gl] - j->base[0]),
-                             d.d_node_off + g * (N + 1), j->mrow, moff, gl, d.node_begin, d.node_end, fs.bufs,
-                             fs.outs, d.sample_bytes / 16};
-                const dim3 grid(unsigned(std::min<uint64_t>(std::max<uint64_t>(da.vpr / 4096, 1), 64)),
-                                unsigned(std::min<uint64_t>(j->ndefer[gl], 148)));
-                cudaLaunchConfig_t dc{};
-                dc.gridDim = grid;
-                dc.blockDim = dim3(256);
-                dc.stream = st;
-                dc.attrs = attr;
-                dc.numAttrs = npdl;
-                LSG_CUDA(cudaLaunchKernelEx(&dc, k_deferred_slots, da));
-                LSG_LAUNCH_CHECK("k_deferred_slots");
             }
             ga = gb;
         }
@@ -1342,6 +1418,8 @@ void lsg_fetch_job_destroy(lsg_fetch_job* j, void* stream) {
         if (p) cudaFreeAsync(p, st);
     if (j->flags) cudaFreeAsync(j->flags, st);
     if (j->ndefer_d) cudaFreeAsync(j->ndefer_d, st);
+    if (j->ptiles) cudaFreeAsync(j->ptiles, st);
+    if (j->drow) cudaFreeAsync(j->drow, st);
     if (j->own_ring) {
         if (j->ring) cudaFreeAsync(j->ring, st);
         if (j->ready) cudaFreeAsync(j->ready, st);

@@ -8,12 +8,14 @@ import torch
 import paper_2211_00224_b200 as ls
 
 D, E, N, b, C, SB = 262144, 100, 8, 512, 52428, 262144
+if os.environ.get("PROBE_CFG") == "cfg3":  # 16 MiB samples, 128 GiB buffer per rank
+    D, E, N, b, C, SB = 65536, 10, 8, 8, 8192, 16 << 20
 pc = ls.PipelineConfig(trace=ls.TraceConfig(D, E, N, b, 42, True), buffer_capacity=C)
 plan = ls.plan_schedule(pc).plan
 res = {}
 for r in [int(x) for x in (sys.argv[1:] or ["1", "2", "8"])]:
     bufs = [torch.empty((C, SB), dtype=torch.uint8, device="cuda") for _ in range(r)]
-    outs = [torch.empty((1024, SB), dtype=torch.uint8, device="cuda") for _ in range(r)]
+    outs = [torch.empty((2 * b, SB), dtype=torch.uint8, device="cuda") for _ in range(r)]
     f = ls.StepFetcher(bufs, outs, (0, r), SB, 1)
     sim = ls.simulate_plan(plan, C, node_range=(0, r), want_slots=True)
     off = plan.node_off.cpu().numpy()
