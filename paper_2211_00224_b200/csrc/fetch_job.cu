@@ -375,7 +375,9 @@ __global__ void __launch_bounds__(256) k_job_misses(MissArgs a) {
 //                step: its slot is written by this kernel, beside the batch
 //                row; other kept misses are written to their slot in the
 //                step's deferred-fill phase, after the step's hits.
-constexpr uint32_t kRowEarly = 1u, kRowInplace = 2u;
+//   kRowSlotOld  an in-place miss whose slot no row of the previous step read
+//                or wrote: its slot write waits only for the step two back.
+constexpr uint32_t kRowEarly = 1u, kRowInplace = 2u, kRowSlotOld = 4u, kRowShift = 3;
 
 struct FlagArgs {
     const uint32_t* slots;
@@ -390,12 +392,14 @@ struct FlagArgs {
 __device__ __forceinline__ bool sl_hit(uint32_t sl) { return sl != kNever && (sl & kHit); }
 
 // one block per step, nodes [k0, k1) in turn: sort the node's hit slots of
-// this step and its kept-miss slots of the previous step, then flag every row
+// this step and its kept-miss and hit slots of the previous step, then flag
+// every row
 __global__ void __launch_bounds__(256) k_row_flags(FlagArgs a) {
     extern __shared__ uint32_t fsm[];
-    uint32_t* hs = fsm;          // [P2] hit slots of (g, k), sorted
-    uint32_t* ps = fsm + a.P2;   // [P2] kept-miss slots of (g-1, k), sorted
-    __shared__ uint32_t cnt[2], carry, ndef;
+    uint32_t* hs = fsm;              // [P2] hit slots of (g, k), sorted
+    uint32_t* ps = fsm + a.P2;       // [P2] kept-miss slots of (g-1, k), sorted
+    uint32_t* hp = fsm + 2 * a.P2;   // [P2] hit slots of (g-1, k), sorted
+    __shared__ uint32_t cnt[3], carry, ndef;
     __shared__ uint32_t wc[8];
     const uint32_t gi = blockIdx.x;
     const uint32_t* off = a.node_off + size_t(gi) * (a.N + 1);
@@ -415,8 +419,8 @@ __global__ void __launch_bounds__(256) k_row_flags(FlagArgs a) {
     };
     for (uint32_t k = a.k0; k < a.k1; ++k) {
         const uint32_t lo = off[k], hi = off[k + 1];
-        if (threadIdx.x == 0) cnt[0] = cnt[1] = 0;
-        for (uint32_t i = threadIdx.x; i < a.P2; i += blockDim.x) hs[i] = ps[i] = 0xFFFFFFFFu;
+        if (threadIdx.x == 0) cnt[0] = cnt[1] = cnt[2] = 0;
+        for (uint32_t i = threadIdx.x; i < a.P2; i += blockDim.x) hs[i] = ps[i] = hp[i] = 0xFFFFFFFFu;
         __syncthreads();
         for (uint32_t r = lo + threadIdx.x; r < hi; r += blockDim.x) {
             const uint32_t sl = a.slots[b + r];
@@ -428,14 +432,15 @@ __global__ void __launch_bounds__(256) k_row_flags(FlagArgs a) {
             for (uint32_t r = off0[k] + threadIdx.x; r < off0[k + 1]; r += blockDim.x) {
                 const uint32_t sl = a.slots[b0 + r];
                 if (!sl_hit(sl) && sl != kNever) ps[atomicAdd(&cnt[1], 1u)] = sl;
+                else if (sl_hit(sl)) hp[atomicAdd(&cnt[2], 1u)] = sl & ~kHit;
             }
         }
         __syncthreads();
-        for (uint32_t size = 2; size <= a.P2; size <<= 1)  // both arrays at once, bitonic
+        for (uint32_t size = 2; size <= a.P2; size <<= 1)  // the three arrays at once, bitonic
             for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                for (uint32_t t = threadIdx.x; t < a.P2; t += blockDim.x) {
+                for (uint32_t t = threadIdx.x; t < 3 * (a.P2 / 2); t += blockDim.x) {
                     const uint32_t q = t & (a.P2 / 2 - 1);
-                    uint32_t* v = t >= a.P2 / 2 ? ps : hs;
+                    uint32_t* v = fsm + (t / (a.P2 / 2)) * a.P2;
                     const uint32_t x0 = 2 * stride * (q / stride) + (q % stride), x1 = x0 + stride;
                     const bool up = (x0 & size) == 0;
                     const uint32_t p = v[x0], r2 = v[x1];
@@ -461,7 +466,8 @@ __global__ void __launch_bounds__(256) k_row_flags(FlagArgs a) {
                     const uint32_t m = pre + __popc(bal & ((1u << lane) - 1));
                     const bool inplace = sl == kNever || !has(hs, cnt[0], sl);
                     if (!inplace) atomicAdd(&ndef, 1u);
-                    f = (m << 2) | (inplace ? kRowInplace : 0u);
+                    const bool old = inplace && sl != kNever && gi > 0 && !has(ps, cnt[1], sl) && !has(hp, cnt[2], sl);
+                    f = (m << kRowShift) | (inplace ? kRowInplace : 0u) | (old ? kRowSlotOld : 0u);
                 }
                 a.flags[b + r] = f;
             }
@@ -532,6 +538,10 @@ struct FusedStep {
     const uint32_t* moff;       // [ns+1] job miss offsets
     uint32_t* consumed;         // ring sequence numbers released
     uint32_t gA, gB;            // the kernel's steps [gA, gB) of the job (phases [2gA, 2gB))
+    uint32_t ns;                // the job's steps: the last one lands in outs, and steps
+    unsigned char* scratch;     //   alternate back from it between outs and scratch
+    uint32_t srows;             //   ([local rank][srows] rows of row_bytes); null scratch:
+                                //   every step in outs, behind a step-wide barrier
     int skip_misses;            // misses left to k_job_misses (large synthesised rows)
 };
 
@@ -547,29 +557,29 @@ __device__ __forceinline__ uint32_t fnode_of_row(const uint32_t* off, uint32_t k
 // producer) claims tiles and loads them — hit tiles HBM slot -> shared, miss
 // tiles from the ring (host tier, after the row's ready flag) or as the Store
 // payload computed by the warp; warp 1 (the consumer) stores each landed
-// tile to its batch row and, for in-place misses, the new slot. Stages hand
-// over through full (TMA transaction) and empty (store has read the stage)
-// mbarriers.
+// tile. Stages hand over through full (TMA transaction) and empty (store has
+// read the stage) mbarriers.
 //
-// Work is a sequence of PHASES: phase 2s is step s (every row of the step);
-// phase 2s+1 writes the step's deferred slots (kept misses whose slot a hit
-// of step s reads: their payload again, into the slot only, once every hit
-// of step s has been loaded). CTAs claim tile chunks phase after phase, so a
-// CTA that runs out of work in one phase starts loading the next while
-// others finish. Ordering, with rdy = the number of leading phases whose
-// tiles are all stored (per-phase counters), for a tile of phase P:
-//   a hit loads once rdy >= P, or rdy >= P-2 for an early row (its slot was
-//     not filled in step s-1); a miss or a deferred fill (reads no slot)
-//     loads once rdy >= P-2;
-//   every store waits for rdy >= P (earlier slot fills, and the reads of
-//     slots this phase overwrites, are done; batch rows reused).
+// Work is a sequence of PHASES: phase 2s is step s's batch rows; phase 2s+1
+// fills the slots of the step's kept misses (their payload again, into the
+// slot only). CTAs claim tile chunks phase after phase, so a CTA that runs
+// out of work in one phase starts loading the next while others finish.
+// Batch rows alternate between the caller's tensors and a scratch set, the
+// job's last step landing in the caller's. Ordering, with rdy = the number of
+// leading phases whose tiles are all stored (per-phase counters), for a tile
+// of phase P:
+//   a hit loads once rdy >= P (the fills of step s-1 are done), or
+//     rdy >= P-2 for an early row (its slot was not filled in step s-1); a
+//     miss or a fill (reads no slot) loads once rdy >= P-2;
+//   a fill stores once rdy >= P (every hit of its step has loaded the slot);
+//   a batch row stores once rdy >= P-2 (step s-2 wrote the same buffer):
+//     no step-wide barrier between consecutive steps' batch rows.
 // Tiles, not CTAs, are counted, so a CTA that never became resident holds
 // nothing anyone waits for; a consumer with nothing to store publishes what
 // it holds before waiting. Before griddepcontrol.wait, rdy = 2gA - 2: the
 // previous kernel runs at most its last step (both phases) behind.
-// PP = phases per step: 2, or 1 when the job has no deferred slot writes (the
-// odd phases would all be empty; skipping them saves ~1 us per step at one
-// rank per GPU). Per-phase arrays are indexed 2s (+1), whatever PP.
+// PP = phases per step: 2, or 1 when the job has no kept misses (no fills;
+// per-phase arrays are indexed 2s (+1) either way).
 template <int S, int L, int PP>
 __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
     extern __shared__ __align__(128) unsigned char fsm2[];
@@ -577,6 +587,7 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
     __shared__ unsigned char* sdst[S];
     __shared__ unsigned char* sdst2[S];
     __shared__ int sstep[S];
+    __shared__ uint8_t sslot_old[S];  // the stage's slot write needs only the step two back
     __shared__ uint32_t s_total;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
@@ -685,19 +696,21 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
                     row_id = __ldg(&f.items[bs + r]) & ~kHit;
                     row_ready = false;
                     src_row = hit ? f.bufs[kk - f.k0] + uint64_t(sl & ~kHit) * f.row_bytes : nullptr;
+                    dst2_row = nullptr;
                     if (fill) {  // the slot only
                         dst_row = f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes;
-                        dst2_row = nullptr;
-                    } else {
-                        dst_row = f.outs[kk - f.k0] + uint64_t(r - __ldg(&off_s[kk])) * f.row_bytes;
-                        dst2_row = (!hit && sl != kNever && (fl & kRowInplace))
-                                       ? f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes
-                                       : nullptr;
+                    } else {  // the batch row, and the slot of an in-place miss
+                        const uint32_t ri = r - __ldg(&off_s[kk]);
+                        dst_row = (f.scratch && ((f.ns - 1 - uint32_t(sc / PP)) & 1))
+                                      ? f.scratch + (uint64_t(kk - f.k0) * f.srows + ri) * f.row_bytes
+                                      : f.outs[kk - f.k0] + uint64_t(ri) * f.row_bytes;
+                        if (!hit && sl != kNever && (fl & kRowInplace))
+                            dst2_row = f.bufs[kk - f.k0] + uint64_t(sl) * f.row_bytes;
                     }
                 }
                 if (!row_hit && f.ring && !row_ready) {  // host-tier miss: wait for the prefetcher's row
                     uint32_t ok = 0;
-                    if (lane == 0) ok = ld_acquire(&f.ready[(s0 + (row_flags >> 2)) % f.R]) == s0 + (row_flags >> 2) + 1;
+                    if (lane == 0) ok = ld_acquire(&f.ready[(s0 + (row_flags >> kRowShift)) % f.R]) == s0 + (row_flags >> kRowShift) + 1;
                     if (!__shfl_sync(0xFFFFFFFFu, ok, 0)) return 0;
                     row_ready = true;
                 }
@@ -735,11 +748,12 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
                 sdst[q] = dst_row + c;
                 sdst2[q] = dst2_row ? dst2_row + c : nullptr;
                 sstep[q] = cur_step;
+                sslot_old[q] = (row_flags & kRowSlotOld) ? 1 : 0;
             }
             if (row_hit || f.ring) {
                 if (lane == 0) {
                     const unsigned char* src =
-                        row_hit ? src_row : f.ring + uint64_t((s0 + (row_flags >> 2)) % f.R) * f.row_bytes;
+                        row_hit ? src_row : f.ring + uint64_t((s0 + (row_flags >> kRowShift)) % f.R) * f.row_bytes;
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(kFTile)
                                  : "memory");
                     asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -747,10 +761,12 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
                 }
             } else {  // synthesised Store payload (store.cpp:70-80): words of this tile
                 const uint64_t w0 = (uint64_t(row_id) * f.row_bytes + c) / 8;
-                unsigned long long* sw = reinterpret_cast<unsigned long long*>(st);
-                uint64_t x = f.seed + (w0 + lane + 1) * kGamma;  // word counter x gamma, stepped by adds
+                ulonglong2* sw = reinterpret_cast<ulonglong2*>(st);
+                // two consecutive words per lane per 16-byte store; word counter x gamma stepped by adds
+                uint64_t x = f.seed + (w0 + 2 * lane + 1) * kGamma;
 #pragma unroll 8
-                for (uint32_t i = lane; i < kFTile / 8; i += 32, x += 32 * kGamma) sw[i] = mix64(x);
+                for (uint32_t i = lane; i < kFTile / 16; i += 32, x += 64 * kGamma)
+                    sw[i] = make_ulonglong2(mix64(x), mix64(x + kGamma));
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
@@ -832,7 +848,11 @@ __global__ void __launch_bounds__(64) k_fetch_fused(FusedStep f) {
                 publish();
                 pend = sk;
             }
-            while (rdy < sk)
+            // a slot write (a fill, an in-place miss) waits for every phase before it; a
+            // batch row alone only for the step two back, which wrote the same buffer
+            // (steps alternate outs / scratch)
+            const int gate = (!f.scratch || (PP == 2 && (sk & 1)) || (sdst2[q] && !sslot_old[q])) ? sk : sk - PP;
+            while (rdy < gate)
                 if (!poll()) __nanosleep(64);
             if (lane == 0) {
                 const unsigned sp = smem_u32(fsm2 + q * kFTile);
@@ -900,7 +920,9 @@ struct lsg_fetch_job {
     uint32_t* ndefer_d = nullptr;    // [ns]
     uint32_t* doff = nullptr;        // [ns+1] deferred rows before each step
     uint32_t* ptiles = nullptr;      // [2ns] tiles per phase (step s: 2s rows, 2s+1 deferred fills)
-    uint64_t ndefer_rows = 0;        // deferred slot writes in the job
+    uint64_t ndefer_rows = 0;        // slot fills (kept misses) in the job
+    unsigned char* scratch = nullptr;  // the alternate batch rows [local rank][srows][sample_bytes]
+    uint32_t srows = 0;
     uint32_t* drow = nullptr;        // the deferred rows, step by step (step-relative)
     std::vector<uint32_t> ndefer;    // deferred slot writes per step (host)
     bool skip_misses = false;        // fused kernel does hits only; k_job_misses after it
@@ -1137,12 +1159,12 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
         if (!alloc(reinterpret_cast<void**>(&j->flags), (j->base[ns] - j->base[0]) * 4) ||
             !alloc(reinterpret_cast<void**>(&j->ndefer_d), ns * 4))
             return fail(set_error(kInternal, "fetch_job: device allocation failed"));
-        const size_t smem = size_t(2) * P2 * 4;
+        const size_t smem = size_t(3) * P2 * 4;
         static std::atomic<uint64_t> attr_done{0};
         int dev = 0;
         cudaGetDevice(&dev);
         if (!(attr_done.load() & (1ull << (dev & 63)))) {
-            cudaFuncSetAttribute(k_row_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 16384 * 4);
+            cudaFuncSetAttribute(k_row_flags, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 16384 * 4);
             cudaFuncSetAttribute(k_fetch_fused<kFStages, kFLag, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kFTile * kFStages);
             cudaFuncSetAttribute(k_fetch_fused<kFStages, kFLag, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1184,6 +1206,19 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
                 cudaStreamSynchronize(st) != cudaSuccess)
                 return fail(cuda_error(cudaGetLastError(), "fetch_job: deferred offsets"));
             j->ndefer_rows = up[3 * ns];
+            // steps alternate between the caller's batch tensors and these (rows up to 1 MiB:
+            // with cfg3's 16 MiB rows the step-wide barrier measured faster, 48.0 vs 49.7 us
+            // per step, and the scratch set would be 16 rows x 16 MiB per rank)
+            static const int pp_env = [] {  // LSG_FETCH_PINGPONG=0/1 forces the choice
+                const char* e = std::getenv("LSG_FETCH_PINGPONG");
+                return e ? std::atoi(e) : -1;
+            }();
+            if (ns >= 2 && (pp_env >= 0 ? pp_env == 1 : d.sample_bytes <= (uint64_t(1) << 20))) {
+                j->srows = uint32_t(max_list);
+                if (!alloc(reinterpret_cast<void**>(&j->scratch),
+                           size_t(d.node_end - d.node_begin) * max_list * d.sample_bytes))
+                    return fail(set_error(kInternal, "fetch_job: device allocation failed (scratch batch rows)"));
+            }
             if (up[3 * ns]) {
                 k_defer_list<<<unsigned(ns), 256, 0, st>>>(fa, j->doff, j->drow);
                 count_launch();
@@ -1293,7 +1328,7 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
                      reinterpret_cast<unsigned char* const*>(d.d_bufs),
                      reinterpret_cast<unsigned char* const*>(d.d_outs), d.node_begin, d.node_end, d.sample_bytes,
                      d.fill_seed, claims, done, j->ptiles, j->ndefer_d, j->doff, j->drow, j->ring, j->R, j->ready,
-                     j->seq0, moff, j->consumed, 0, 0, j->skip_misses ? 1 : 0};
+                     j->seq0, moff, j->consumed, 0, 0, ns, j->scratch, j->srows, j->skip_misses ? 1 : 0};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1419,6 +1454,7 @@ void lsg_fetch_job_destroy(lsg_fetch_job* j, void* stream) {
     if (j->flags) cudaFreeAsync(j->flags, st);
     if (j->ndefer_d) cudaFreeAsync(j->ndefer_d, st);
     if (j->ptiles) cudaFreeAsync(j->ptiles, st);
+    if (j->scratch) cudaFreeAsync(j->scratch, st);
     if (j->drow) cudaFreeAsync(j->drow, st);
     if (j->own_ring) {
         if (j->ring) cudaFreeAsync(j->ring, st);
