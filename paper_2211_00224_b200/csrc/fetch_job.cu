@@ -1206,14 +1206,14 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
                 cudaStreamSynchronize(st) != cudaSuccess)
                 return fail(cuda_error(cudaGetLastError(), "fetch_job: deferred offsets"));
             j->ndefer_rows = up[3 * ns];
-            // steps alternate between the caller's batch tensors and these (rows up to 1 MiB:
-            // with cfg3's 16 MiB rows the step-wide barrier measured faster, 48.0 vs 49.7 us
-            // per step, and the scratch set would be 16 rows x 16 MiB per rank)
-            static const int pp_env = [] {  // LSG_FETCH_PINGPONG=0/1 forces the choice
+            // steps alternate between the caller's batch tensors and these (one more batch
+            // per local rank: 128 MiB at cfg2, 256 MiB at cfg3); fetch alone at one rank,
+            // cfg2 44.6 -> 42.2 us per step, cfg3 47.7 -> 46.4 (LSG_FETCH_PINGPONG=0: off)
+            static const bool pp_off = [] {
                 const char* e = std::getenv("LSG_FETCH_PINGPONG");
-                return e ? std::atoi(e) : -1;
+                return e && e[0] == '0';
             }();
-            if (ns >= 2 && (pp_env >= 0 ? pp_env == 1 : d.sample_bytes <= (uint64_t(1) << 20))) {
+            if (ns >= 2 && !pp_off) {
                 j->srows = uint32_t(max_list);
                 if (!alloc(reinterpret_cast<void**>(&j->scratch),
                            size_t(d.node_end - d.node_begin) * max_list * d.sample_bytes))
