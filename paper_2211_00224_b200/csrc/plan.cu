@@ -52,6 +52,7 @@ namespace {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kMaxN = 32;
+constexpr uint32_t kOvN = 8;  // the overlapped loop's node limit
 constexpr uint32_t kMaxSmemB = 8192;   // per-item arrays in shared memory up to here
 constexpr uint32_t kMaxB = 16384;      // then in L2-resident global scratch
 constexpr uint32_t kFetch = 0xFFFFFFFFu;
@@ -165,7 +166,7 @@ struct LoopArgs {
     uint32_t* gitems;                // [6][B] per-item arrays when they do not fit smem
     unsigned long long* prof;        // [8] per-phase cycles (LSG_PROFILE) or null
     int dbg_skip;                    // timing experiments only (LSG_DEBUG_SKIP)
-    uint32_t* nb;                    // [2][D] overlapped loop: per batch parity, the latest batch each id was
+    uint32_t* nb;                    // [3][D] overlapped loop: per batch mod 3, the latest batch each id was
                                      // classified in, or null
 };
 
@@ -201,7 +202,7 @@ struct Small {
     uint32_t rq[kMaxN];             // G: recipient of each rank in a round
     uint32_t win_base;              // I1: first bucket word of the window
     uint32_t win[kMaxN][kWinWords]; // I1: bucket bits aggregated per step
-    uint32_t stamp, conflict, conflict2;  // (overlapped loop only; unused here)
+    uint32_t stamp, conflict, conflict2, conflict3;  // (overlapped loop only; unused here)
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -243,16 +244,17 @@ __device__ __forceinline__ void set_key(const LoopArgs& a, SM& sm, uint32_t k, u
 }
 
 // with the overlapped loop (a.nb), a holder mask that changes for an id of
-// one of the next two, already classified batches (sm.stamp = g+1, g+2)
+// one of the next three, already classified batches (sm.stamp = g+1, g+2, g+3)
 // invalidates that classification. The classifier stamps, fences, then reads
 // masks; the advance changes a mask, fences, then reads the stamps: one of
 // the two sees the other.
 template <class SM>
 __device__ __forceinline__ void nb_check(const LoopArgs& a, SM& sm, uint32_t x) {
     __threadfence();
-    const uint32_t s1 = sm.stamp, s2 = s1 + 1;
-    if (__ldcg(&a.nb[size_t(s1 & 1) * a.D + x]) == s1) sm.conflict = 1;
-    if (__ldcg(&a.nb[size_t(s2 & 1) * a.D + x]) == s2) sm.conflict2 = 1;
+    const uint32_t s1 = sm.stamp, s2 = s1 + 1, s3 = s1 + 2;
+    if (__ldcg(&a.nb[size_t(s1 % 3) * a.D + x]) == s1) sm.conflict = 1;
+    if (__ldcg(&a.nb[size_t(s2 % 3) * a.D + x]) == s2) sm.conflict2 = 1;
+    if (__ldcg(&a.nb[size_t(s3 % 3) * a.D + x]) == s3) sm.conflict3 = 1;
 }
 template <class SM>
 __device__ __forceinline__ void drop(const LoopArgs& a, SM& sm, uint32_t k, uint32_t x) {
@@ -1242,14 +1244,14 @@ struct SmallOv {
     uint32_t inftop[kMaxN];
     uint32_t infcnt[kMaxN];
     uint32_t nfetch, nmoves;
-    alignas(16) uint32_t stg[2][2][32][kMaxN];  // team D: staging per D warp
+    alignas(16) uint32_t stg[2][2][32][kOvN];  // team D: staging per D warp (32 packed rows of 16 B)
     uint32_t dmv[kMaxN][kDmv];
     uint32_t rq[kMaxN];
     uint32_t win[kMaxN][kWinWords];
-    uint32_t stamp, conflict, conflict2;  // I(g): stamps g+1 / g+2, their batches' verdicts
+    uint32_t stamp, conflict, conflict2, conflict3;  // I(g): stamps g+1..g+3, their batches' verdicts
     OvPar par[2];
-    uint32_t cfv[4];   // verdict per batch (mod 4): a mask it was classified with changed
-    uint32_t cnm[3];   // (team C's copy) multi items per step (mod 3), for team D
+    uint32_t cfv[8];   // verdict per batch (mod 8): a mask it was classified with changed
+    uint32_t cnm[4];   // (team C's copy) multi items per step (mod 4), for team D
     // team hand-off counters (monotone): steps classified, resolved (D
     // final), buffer-advanced, speculative-D-finished-on-conflict,
     // re-classified, copied into team P's arrays, resolved (first pass)
@@ -1263,6 +1265,7 @@ struct SmallOv {
 // per-step arrays and hand-off counters live in CTA 1's shared memory.
 // Teams D and C reach team P's state through distributed shared memory.
 constexpr uint32_t kPWarps = kWarps, kPThreads = kPWarps * 32;
+constexpr uint32_t kOvDepth = 4;  // steps in flight: step h is classified once I(h-4) is done
 // team C (classification): CTA 0's 12 warps that do not share warp 0's
 // scheduler (warp w issues on SMSP w % 4)
 constexpr uint32_t kCWarps = 12, kCThreads = kCWarps * 32;
@@ -1296,7 +1299,6 @@ __device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, OvP
     const uint32_t i = g / a.S, t = g % a.S;
     const uint32_t lo = t * a.B, len = min(a.B, a.keep - lo);
     const uint32_t* row = a.trace + size_t(a.order[i]) * a.keep + lo;
-    const uint32_t* pkrow = a.nr + size_t(i) * a.keep + lo;
     const uint32_t R = ((len + kCThreads - 1) / kCThreads) * 32;
     const uint32_t j0 = pw * R, j1 = min(j0 + R, len);
     if (lane < kMaxN) sm.wcnt[pw][lane] = 0;
@@ -1305,8 +1307,7 @@ __device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, OvP
     for (uint32_t j = j0 + lane; j < j1; j += 32) {
         const uint32_t x = row[j];
         s.sx[j] = x;
-        s.snu[j] = pkrow[j];
-        if (stamp) a.nb[size_t(g & 1) * a.D + x] = g;  // this batch's classification is checked by I(g-2), I(g-1)
+        if (stamp) a.nb[size_t(g % 3) * a.D + x] = g;  // this batch's classification is checked by I(g-3)..I(g-1)
     }
     __threadfence();  // stamps before the masks are read (nb_check)
     __syncwarp();
@@ -1397,23 +1398,34 @@ __device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, OvP
             dpre[mi] = j;  // the multi list for team D, in global memory (no DSMEM on its chain)
         }
     }
-    if (pw == 0 && lane == 0) sm.cnm[g % 3] = pp.nmulti;
+    if (pw == 0 && lane == 0) sm.cnm[g % kOvDepth] = pp.nmulti;
     __threadfence_block();
     bar_c();
 }
 
-// the classified step g (team C's arrays + totals) into team P's parity
-// buffers (16-byte DSMEM stores), once team P is done with step g-2
+// the classified step g (team C's arrays + totals; the packed next-use keys
+// straight from their global row) into team P's parity buffers (16-byte
+// DSMEM stores), once team P is done with step g-2
 __device__ void ov_copy(const LoopArgs& a, const OvBufs& s, const OvPar& pc, const OvBufs& sr, OvPar& pp, uint32_t g,
                         uint32_t pw, uint32_t lane) {
-    const uint32_t len = min(a.B, a.keep - (g % a.S) * a.B);
+    const uint32_t lo = (g % a.S) * a.B, len = min(a.B, a.keep - lo);
+    const uint32_t* pkrow = a.nr + size_t(g / a.S) * a.keep + lo;  // (any alignment: read by words)
     const uint32_t ctid = pw * 32 + lane, nm = pc.nmulti;
     const uint32_t len4 = (len + 3) / 4, nm4 = (nm + 3) / 4;
     for (uint32_t q = ctid; q < 4 * len4 + nm4; q += kCThreads) {
         const uint32_t arr = q < 4 * len4 ? q / len4 : 4, e = (q < 4 * len4 ? q - arr * len4 : q - 4 * len4) * 4;
-        const uint32_t* src = arr == 0 ? s.sx : arr == 1 ? s.snu : arr == 2 ? s.smask : arr == 3 ? s.sinfo : s.pre;
         uint32_t* dst = arr == 0 ? sr.sx : arr == 1 ? sr.snu : arr == 2 ? sr.smask : arr == 3 ? sr.sinfo : sr.pre;
-        *reinterpret_cast<uint4*>(dst + e) = *reinterpret_cast<const uint4*>(src + e);
+        uint4 v;
+        if (arr == 1) {
+            v.x = __ldcg(&pkrow[e]);
+            v.y = e + 1 < len ? __ldcg(&pkrow[e + 1]) : 0u;
+            v.z = e + 2 < len ? __ldcg(&pkrow[e + 2]) : 0u;
+            v.w = e + 3 < len ? __ldcg(&pkrow[e + 3]) : 0u;
+        } else {
+            const uint32_t* src = arr == 0 ? s.sx : arr == 2 ? s.smask : arr == 3 ? s.sinfo : s.pre;
+            v = *reinterpret_cast<const uint4*>(src + e);
+        }
+        *reinterpret_cast<uint4*>(dst + e) = v;
     }
     if (ctid < a.N) pp.tot[ctid] = pc.tot[ctid];
     if (ctid == 0) pp.nmulti = nm;
@@ -1425,7 +1437,7 @@ __device__ void ov_copy(const LoopArgs& a, const OvBufs& s, const OvPar& pc, con
 // from global memory (the multi list and the packed rows), outputs into team
 // D's own shared memory (res[mi] = the chain's minimum key, or kSent; mtot);
 // team P applies them to its lists (ov_apply).
-__device__ void ov_resolve(const LoopArgs& a, uint32_t (*stg)[32][kMaxN], const uint32_t* dsx, const uint32_t* dpre,
+__device__ void ov_resolve(const LoopArgs& a, uint32_t (*stg)[32][kOvN], const uint32_t* dsx, const uint32_t* dpre,
                            uint32_t nm, uint32_t* res, uint32_t* mtot, uint32_t lane) {
     const uint32_t N = a.N, b = a.b;
     uint32_t M01 = 0, M23 = 0, M45 = 0, M67 = 0;
@@ -1538,19 +1550,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         if (tid == 0) {
             sm_local.ac_cnt = sm_local.d_cnt = sm_local.i_cnt = sm_local.spec_cnt = sm_local.redo_cnt = 0;
             sm_local.copy_cnt = sm_local.ds_cnt[0] = sm_local.ds_cnt[1] = 0;
-            for (int q = 0; q < 4; ++q) sm_local.cfv[q] = 0;
-            sm_local.conflict = sm_local.conflict2 = 0;
+            for (int q = 0; q < 8; ++q) sm_local.cfv[q] = 0;
+            sm_local.conflict = sm_local.conflict2 = sm_local.conflict3 = 0;
         }
     }
     cl.sync();
     // global scratch: smul [B][N] (team C only), the D rows [3][B] x 16 B and multi lists [3][B]
+    // global scratch (a.sx): the D rows [4][B] x 16 B, multi lists [4][B], team D's
+    // results res [4][B] and mtot [4][kMaxN], by step mod 4; smul [2][B][N] (team C only)
     auto smul_of = [&](uint32_t g) { return a.smul + size_t(g & 1) * a.B * N; };
-    auto dsx_of = [&](uint32_t g) { return a.sx + size_t(g % 3) * a.B * 4; };
-    auto dpre_of = [&](uint32_t g) { return a.sx + size_t(3) * a.B * 4 + size_t(g % 3) * a.B; };
-    // team D's results in CTA 0's shared memory: res [3][B], mtot [3][kMaxN]
-    uint32_t* dres = cl.map_shared_rank(dyn, 0);
-    auto res_of = [&](uint32_t g) { return dres + size_t(g % 3) * a.B; };
-    auto mtot_of = [&](uint32_t g) { return dres + size_t(3) * a.B + size_t(g % 3) * kMaxN; };
+    auto dsx_of = [&](uint32_t g) { return a.sx + size_t(g % kOvDepth) * a.B * 4; };
+    auto dpre_of = [&](uint32_t g) { return a.sx + size_t(kOvDepth) * a.B * 4 + size_t(g % kOvDepth) * a.B; };
+    auto res_of = [&](uint32_t g) { return a.sx + size_t(kOvDepth) * a.B * 5 + size_t(g % kOvDepth) * a.B; };
+    auto mtot_of = [&](uint32_t g) { return a.sx + size_t(kOvDepth) * a.B * 6 + size_t(g % kOvDepth) * kMaxN; };
     unsigned long long pf[12] = {}, t0 = clock64();
     auto tick = [&](int q) {
         if (a.prof) {
@@ -1571,41 +1583,51 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
     if (crank == 0 && w != 0 && (w & 3) != 0) {
         // -------------------------------------------- team C (CTA 0)
         const uint32_t cw = (w >> 2) * 3 + (w & 3) - 1;
-        // team C's step arrays: CTA 0's dynamic smem after team D's results (3B + 3*kMaxN words)
-        uint32_t* c0 = dyn + size_t(3) * a.B + 3 * kMaxN;
-        const OvBufs SC{c0, c0 + a.B, c0 + 2 * a.B, c0 + 3 * a.B, c0 + 4 * a.B, nullptr};
-        OvPar& pc = sm_local.par[0];  // team C's totals of the step it classified last
-        for (uint32_t h = 0; h < a.T + 2; ++h) {
-            // classify step h once I(h-3) is done; first the verdict of I(h-4), I(h-3) on step h-2
-            if (h >= 2) {
-                if (cw == 0) wait_ge(&sm.i_cnt, h - 2);
+        // team C's step arrays, two sets (it classifies step h before copying
+        // step h-1): sx, smask, sinfo, pre (the next-use keys are copied from
+        // their global row)
+        auto sc_of = [&](uint32_t h) {
+            uint32_t* c0 = dyn + size_t(h & 1) * 4 * a.B;
+            return OvBufs{c0, nullptr, c0 + a.B, c0 + 2 * a.B, c0 + 3 * a.B, nullptr};
+        };
+        auto pc_of = [&](uint32_t h) -> OvPar& { return sm_local.par[h & 1]; };  // its totals, per set
+        for (uint32_t h = 0; h < a.T + kOvDepth - 1; ++h) {
+            // classify step h once I(h-4) is done; first the final verdict (I(h-6)..I(h-4))
+            // on step h-3, whose re-classification uses set h (not yet written this round)
+            if (h >= kOvDepth - 1) {
+                if (cw == 0) wait_ge(&sm.i_cnt, h - (kOvDepth - 1));
                 bar_c();
             }
-            if (h >= 3 && h - 2 < a.T && sm.cfv[(h - 2) & 3]) {
-                if (cw == 0) wait_ge(&sm.ds_cnt[h & 1], h - 1);  // team D is done with the speculative D(h-2)
+            if (h >= kOvDepth && h - (kOvDepth - 1) < a.T && sm.cfv[(h - (kOvDepth - 1)) & 7]) {
+                const uint32_t q = h - (kOvDepth - 1);
+                if (cw == 0) wait_ge(&sm.ds_cnt[q & 1], q + 1);  // team D is done with the speculative D(q)
                 bar_c();
-                ov_classify(a, sm_local, SC, pc, smul_of(h - 2), dsx_of(h - 2), dpre_of(h - 2), h - 2, cw, lane, false);
-                // team P has not started step h-2 (it waits for D(h-2)): its buffers take the new classification
-                ov_copy(a, SC, pc, S2[(h - 2) & 1], sm.par[(h - 2) & 1], h - 2, cw, lane);
-                if (cw == 0 && lane == 0) publish(&sm.redo_cnt, h - 1);
+                ov_classify(a, sm_local, sc_of(h), pc_of(h), smul_of(q), dsx_of(q), dpre_of(q), q, cw, lane, false);
+                // team P has not started step q (it waits for D(q)): its buffers take the new classification
+                ov_copy(a, sc_of(h), pc_of(h), S2[q & 1], sm.par[q & 1], q, cw, lane);
+                if (cw == 0 && lane == 0) publish(&sm.redo_cnt, q + 1);
             }
-            if (h >= a.T) continue;  // (the last two verdicts only)
-            tick(0);
-            if (cw == 0 && lane == 0) ev(h, 0);
-            ov_classify(a, sm_local, SC, pc, smul_of(h), dsx_of(h), dpre_of(h), h, cw, lane, true);
-            if (cw == 0 && lane == 0) publish(&sm.ac_cnt, h + 1);
-            if (cw == 0 && lane == 0) ev(h, 1);
-            tick(1);
-            if (h >= 2) {  // team P is done with step h-2: its parity buffers are free
-                if (cw == 0) wait_ge(&sm.i_cnt, h - 1);
-                bar_c();
+            if (h < a.T) {
+                tick(0);
+                if (cw == 0 && lane == 0) ev(h, 0);
+                ov_classify(a, sm_local, sc_of(h), pc_of(h), smul_of(h), dsx_of(h), dpre_of(h), h, cw, lane, true);
+                if (cw == 0 && lane == 0) publish(&sm.ac_cnt, h + 1);
+                if (cw == 0 && lane == 0) ev(h, 1);
+                tick(1);
             }
-            tick(2);
-            if (cw == 0 && lane == 0) ev(h, 2);
-            ov_copy(a, SC, pc, S2[h & 1], sm.par[h & 1], h, cw, lane);
-            if (cw == 0 && lane == 0) publish(&sm.copy_cnt, h + 1);
-            if (cw == 0 && lane == 0) ev(h, 3);
-            tick(3);
+            if (h >= 1 && h - 1 < a.T) {  // copy step h-1 once team P is done with step h-3
+                const uint32_t q = h - 1;
+                if (q >= 2) {
+                    if (cw == 0) wait_ge(&sm.i_cnt, q - 1);
+                    bar_c();
+                }
+                tick(2);
+                if (cw == 0 && lane == 0) ev(q, 2);
+                ov_copy(a, sc_of(q), pc_of(q), S2[q & 1], sm.par[q & 1], q, cw, lane);
+                if (cw == 0 && lane == 0) publish(&sm.copy_cnt, q + 1);
+                if (cw == 0 && lane == 0) ev(q, 3);
+                tick(3);
+            }
         }
         if (cw == 0 && lane == 0) publish(&sm.ac_cnt, a.T + 1);  // team D: no more re-classifications
         if (a.prof && cw == 0 && lane == 0)
@@ -1621,7 +1643,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
             // after I(g-2) or I(g-1) changed one of its masks) is resolved again
             // when it arrives, and team P waits for that only then.
             const uint32_t dp = w >> 2;  // this warp's step parity
-            uint32_t (*stg)[32][kMaxN] = sm_local.stg[dp];
+            uint32_t (*stg)[32][kOvN] = sm_local.stg[dp];
             uint32_t redone = 0;  // re-classifications resolved (redo_cnt values)
             auto pending = [&]() {
                 const uint32_t r = sm.redo_cnt;
@@ -1631,8 +1653,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
                 if (!pending()) return;
                 asm volatile("fence.acq_rel.cluster;" ::: "memory");
                 const uint32_t r = sm.redo_cnt, q = r - 1;
-                ov_resolve(a, stg, dsx_of(q), dpre_of(q), sm_local.cnm[q % 3], dyn + size_t(q % 3) * a.B,
-                           dyn + size_t(3) * a.B + size_t(q % 3) * kMaxN, lane);
+                ov_resolve(a, stg, dsx_of(q), dpre_of(q), sm_local.cnm[q % kOvDepth], res_of(q), mtot_of(q), lane);
                 __syncwarp();
                 if (lane == 0) publish(&sm.d_cnt, r);
                 redone = r;
@@ -1647,8 +1668,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
                 if (sm.ac_cnt < g + 1) continue;
                 asm volatile("fence.acq_rel.cluster;" ::: "memory");
                 if (lane == 0) ev(g, 4);
-                ov_resolve(a, stg, dsx_of(g), dpre_of(g), sm_local.cnm[g % 3], dyn + size_t(g % 3) * a.B,
-                           dyn + size_t(3) * a.B + size_t(g % 3) * kMaxN, lane);
+                ov_resolve(a, stg, dsx_of(g), dpre_of(g), sm_local.cnm[g % kOvDepth], res_of(g), mtot_of(g), lane);
                 __syncwarp();
                 if (lane == 0) publish(&sm.ds_cnt[dp], g + 1);  // team P knows the verdict itself (it ran I(g-1))
                 if (lane == 0) ev(g, 5);
@@ -1683,7 +1703,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
             wait_ge(&sm.ds_cnt[g & 1], g + 1);
             wait_ge(&sm.copy_cnt, g + 1);
             // I(g-2) or I(g-1) changed a mask of this batch: wait for its second classification
-            if (g > 0 && sm.cfv[g & 3]) {
+            if (g > 0 && sm.cfv[g & 7]) {
                 wait_ge(&sm.d_cnt, g + 1);
                 if (a.prof) a.prof[24] += 1;
             }
@@ -1699,8 +1719,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         ov_apply(a, s, pp, dsx_of(g), res_of(g), mtot_of(g), ptid);
         bar_p();
         tick(0);
-        if (g + 3 < a.T && !(a.dbg_skip & 8)) {  // batch g+3's rows into L2 for its classification after I(g)
-            const uint32_t g2 = g + 3, i2 = g2 / a.S, t2 = g2 % a.S;
+        if (g + kOvDepth < a.T && !(a.dbg_skip & 8)) {  // batch g+4's rows into L2 for its classification after I(g)
+            const uint32_t g2 = g + kOvDepth, i2 = g2 / a.S, t2 = g2 % a.S;
             const uint32_t lo2 = t2 * a.B, len2 = min(a.B, a.keep - lo2);
             const char* r0 = reinterpret_cast<const char*>(a.trace + size_t(a.order[i2]) * a.keep + lo2);
             const char* r1 = reinterpret_cast<const char*>(a.nr + size_t(i2) * a.keep + lo2);
@@ -1953,7 +1973,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         // and g+2 (already classified) are caught by the stamp checks
         if (ptid == 0) {
             sm.stamp = g + 1;
-            sm.conflict = sm.conflict2 = 0;
+            sm.conflict = sm.conflict2 = sm.conflict3 = 0;
         }
         bar_p();
         {
@@ -2044,8 +2064,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         gbase += len;
         // the verdicts on steps g+1 (final) and g+2 (first half); team C re-classifies on a conflict
         if (ptid == 0) {
-            sm.cfv[(g + 1) & 3] |= sm.conflict;
-            sm.cfv[(g + 2) & 3] = sm.conflict2;
+            sm.cfv[(g + 1) & 7] |= sm.conflict;
+            sm.cfv[(g + 2) & 7] |= sm.conflict2;
+            sm.cfv[(g + 3) & 7] = sm.conflict3;
             publish(&sm.i_cnt, g + 1);
             ev(g, 7);
             if (a.prof) {
@@ -2129,11 +2150,12 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
                     !std::getenv("LSG_DEBUG_SKIP") && !(ov_env && ov_env[0] == '0') &&
                     (dm.B >= 2048 || (ov_env && ov_env[0] == '1'));
     a.smul = sc.get<uint32_t>(size_t(dm.B) * dm.N * (ov ? 2 : 1));
-    a.sx = sc.get<uint32_t>(ov ? size_t(dm.B) * 15 : size_t(dm.B) * std::max<uint32_t>(dm.N, 8u));  // D rows (+ ov: 3 sets + lists)
+    a.sx = sc.get<uint32_t>(ov ? size_t(dm.B) * 4 * 7 + 4 * kMaxN
+                               : size_t(dm.B) * std::max<uint32_t>(dm.N, 8u));  // D rows (+ ov: 4 sets, lists, results)
     a.dmoves = sc.get<uint32_t>(size_t(dm.N) * dm.B + 2 * 32 * kMaxN);
-    a.nb = ov ? sc.get<uint32_t>(size_t(2) * dm.D) : nullptr;
+    a.nb = ov ? sc.get<uint32_t>(size_t(3) * dm.D) : nullptr;
     if (ov && !a.nb) return set_error(kInternal, "plan: scratch allocation failed");
-    if (ov) LSG_CUDA(cudaMemsetAsync(a.nb, 0xFF, size_t(2) * dm.D * 4, st));
+    if (ov) LSG_CUDA(cudaMemsetAsync(a.nb, 0xFF, size_t(3) * dm.D * 4, st));
     if (!nu || !sb || !nr || !a.bm || !a.key || !a.hm || !a.nz || !a.infbm || !a.smul || !a.sx || !a.dmoves)
         return set_error(kInternal, "plan: scratch allocation failed");
     LSG_CUDA(cudaMemsetAsync(a.key, 0xFF, size_t(dm.N) * dm.D * 4, st));
@@ -2181,9 +2203,8 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
         LSG_CUDA(cudaMemsetAsync(a.prof, 0, (32 + 8 * 16 + 2 * dm.T) * 8, st));
     }
     if (ov) {
-        // team P: two parity sets of the six per-step arrays; CTA 0: team D's results, res [3][B] +
-        // mtot [3][32], and team C's five step arrays
-        const size_t smem = std::max<size_t>(size_t(12) * dm.B, size_t(8) * dm.B + 3 * kMaxN + 16) * 4;
+        // team P: two parity sets of the six per-step arrays; CTA 0: team C's two sets of four
+        const size_t smem = size_t(12) * dm.B * 4;
         LSG_CUDA(cudaFuncSetAttribute(k_plan_loop_ov, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(2);
