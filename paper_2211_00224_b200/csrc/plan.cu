@@ -53,6 +53,7 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kMaxN = 32;
 constexpr uint32_t kOvN = 8;  // the overlapped loop's node limit
+constexpr uint32_t kDWarps = 4;  // its team D: one warp per scheduler of CTA 2, one per step mod 4
 constexpr uint32_t kMaxSmemB = 8192;   // per-item arrays in shared memory up to here
 constexpr uint32_t kMaxB = 16384;      // then in L2-resident global scratch
 constexpr uint32_t kFetch = 0xFFFFFFFFu;
@@ -1244,7 +1245,7 @@ struct SmallOv {
     uint32_t inftop[kMaxN];
     uint32_t infcnt[kMaxN];
     uint32_t nfetch, nmoves;
-    alignas(16) uint32_t stg[2][2][32][kOvN];  // team D: staging per D warp (32 packed rows of 16 B)
+    alignas(16) uint32_t stg[kDWarps][2][32][kOvN];  // team D: staging per D warp (32 packed rows of 16 B)
     uint32_t dmv[kMaxN][kDmv];
     uint32_t rq[kMaxN];
     uint32_t win[kMaxN][kWinWords];
@@ -1255,7 +1256,7 @@ struct SmallOv {
     // team hand-off counters (monotone): steps classified, resolved (D
     // final), buffer-advanced, speculative-D-finished-on-conflict,
     // re-classified, copied into team P's arrays, resolved (first pass)
-    volatile uint32_t ac_cnt, d_cnt, i_cnt, spec_cnt, redo_cnt, copy_cnt, ds_cnt[2];
+    volatile uint32_t ac_cnt, d_cnt, i_cnt, spec_cnt, redo_cnt, copy_cnt, ds_cnt[kDWarps];
 };
 
 // The teams run on the two SMs of a thread-block cluster: team D (warp 0 of
@@ -1268,7 +1269,7 @@ constexpr uint32_t kPWarps = kWarps, kPThreads = kPWarps * 32;
 constexpr uint32_t kOvDepth = 4;  // steps in flight: step h is classified once I(h-4) is done
 // team C (classification): CTA 0's 12 warps that do not share warp 0's
 // scheduler (warp w issues on SMSP w % 4)
-constexpr uint32_t kCWarps = 12, kCThreads = kCWarps * 32;
+constexpr uint32_t kCWarps = 16, kCThreads = kCWarps * 32;
 
 __device__ __forceinline__ void bar_p() { asm volatile("bar.sync 1, %0;" ::"n"(kPThreads) : "memory"); }
 __device__ __forceinline__ void bar_c() { asm volatile("bar.sync 2, %0;" ::"n"(kCThreads) : "memory"); }
@@ -1549,7 +1550,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         }
         if (tid == 0) {
             sm_local.ac_cnt = sm_local.d_cnt = sm_local.i_cnt = sm_local.spec_cnt = sm_local.redo_cnt = 0;
-            sm_local.copy_cnt = sm_local.ds_cnt[0] = sm_local.ds_cnt[1] = 0;
+            sm_local.copy_cnt = 0;
+            for (uint32_t q = 0; q < kDWarps; ++q) sm_local.ds_cnt[q] = 0;
             for (int q = 0; q < 8; ++q) sm_local.cfv[q] = 0;
             sm_local.conflict = sm_local.conflict2 = sm_local.conflict3 = 0;
         }
@@ -1580,9 +1582,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
             a.prof[32 + (g - g0) * 8 + e] = t;
         }
     };
-    if (crank == 0 && w != 0 && (w & 3) != 0) {
-        // -------------------------------------------- team C (CTA 0)
-        const uint32_t cw = (w >> 2) * 3 + (w & 3) - 1;
+    if (crank == 0) {
+        // -------------------------------------------- team C (CTA 0, all warps)
+        const uint32_t cw = w;
         // team C's step arrays, two sets (it classifies step h before copying
         // step h-1): sx, smask, sinfo, pre (the next-use keys are copied from
         // their global row)
@@ -1600,7 +1602,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
             }
             if (h >= kOvDepth && h - (kOvDepth - 1) < a.T && sm.cfv[(h - (kOvDepth - 1)) & 7]) {
                 const uint32_t q = h - (kOvDepth - 1);
-                if (cw == 0) wait_ge(&sm.ds_cnt[q & 1], q + 1);  // team D is done with the speculative D(q)
+                if (cw == 0) wait_ge(&sm.ds_cnt[q % kDWarps], q + 1);  // team D is done with the speculative D(q)
                 bar_c();
                 ov_classify(a, sm_local, sc_of(h), pc_of(h), smul_of(q), dsx_of(q), dpre_of(q), q, cw, lane, false);
                 // team P has not started step q (it waits for D(q)): its buffers take the new classification
@@ -1632,28 +1634,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         if (cw == 0 && lane == 0) publish(&sm.ac_cnt, a.T + 1);  // team D: no more re-classifications
         if (a.prof && cw == 0 && lane == 0)
             for (int q = 0; q < 4; ++q) a.prof[20 + q] = pf[q];
+        cl.sync();  // team P's shared memory stays alive until every team is done with it
+        return;
     }
-    if (crank == 0) {
-        if (w == 0 || w == 4) {
-            // -------------------------------------------- team D (CTA 0)
-            // Two warps on scheduler 0 (team C holds the other three), one per
-            // step parity: D(g) of one step does not depend on D(g-1), and one
-            // warp's serial chain leaves most issue slots idle. Speculative D(g)
-            // as soon as step g is classified; a re-classified step (team C,
-            // after I(g-2) or I(g-1) changed one of its masks) is resolved again
-            // when it arrives, and team P waits for that only then.
-            const uint32_t dp = w >> 2;  // this warp's step parity
+    if (crank == 2) {
+        if (w < kDWarps) {
+            // -------------------------------------------- team D (CTA 2)
+            // One warp per scheduler, one per step mod 4: D(g) of one step does
+            // not depend on D(g-1), and one warp's serial chain leaves most of
+            // its scheduler idle. Speculative D(g) as soon as step g is
+            // classified; a re-classified step (team C, after I(g-3)..I(g-1)
+            // changed one of its masks) is resolved again when it arrives, and
+            // team P waits for that only then.
+            const uint32_t dp = w;  // this warp's steps: g % 4 == dp
+            const SmallOv& smc = *cl.map_shared_rank(&sm_local, 0);  // team C's (cnm)
             uint32_t (*stg)[32][kOvN] = sm_local.stg[dp];
             uint32_t redone = 0;  // re-classifications resolved (redo_cnt values)
             auto pending = [&]() {
                 const uint32_t r = sm.redo_cnt;
-                return r > redone && ((r - 1) & 1) == dp;
+                return r > redone && ((r - 1) % kDWarps) == dp;
             };
             auto redo = [&]() {
                 if (!pending()) return;
                 asm volatile("fence.acq_rel.cluster;" ::: "memory");
                 const uint32_t r = sm.redo_cnt, q = r - 1;
-                ov_resolve(a, stg, dsx_of(q), dpre_of(q), sm_local.cnm[q % kOvDepth], res_of(q), mtot_of(q), lane);
+                ov_resolve(a, stg, dsx_of(q), dpre_of(q), smc.cnm[q % kOvDepth], res_of(q), mtot_of(q), lane);
                 __syncwarp();
                 if (lane == 0) publish(&sm.d_cnt, r);
                 redone = r;
@@ -1668,12 +1673,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
                 if (sm.ac_cnt < g + 1) continue;
                 asm volatile("fence.acq_rel.cluster;" ::: "memory");
                 if (lane == 0) ev(g, 4);
-                ov_resolve(a, stg, dsx_of(g), dpre_of(g), sm_local.cnm[g % kOvDepth], res_of(g), mtot_of(g), lane);
+                ov_resolve(a, stg, dsx_of(g), dpre_of(g), smc.cnm[g % kOvDepth], res_of(g), mtot_of(g), lane);
                 __syncwarp();
                 if (lane == 0) publish(&sm.ds_cnt[dp], g + 1);  // team P knows the verdict itself (it ran I(g-1))
                 if (lane == 0) ev(g, 5);
                 tick(1);
-                g += 2;
+                g += kDWarps;
             }
             while (sm.ac_cnt <= a.T) redo();  // team C's last re-classifications (it ends with ac_cnt = T+1)
             asm volatile("fence.acq_rel.cluster;" ::: "memory");
@@ -1700,7 +1705,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
         const uint32_t j0 = pw * R, j1 = min(j0 + R, len);
         tick(3);
         if (ptid == 0) {  // D(g) resolved, step g copied in; one waiter, the barrier orders the rest
-            wait_ge(&sm.ds_cnt[g & 1], g + 1);
+            wait_ge(&sm.ds_cnt[g % kDWarps], g + 1);
             wait_ge(&sm.copy_cnt, g + 1);
             // I(g-2) or I(g-1) changed a mask of this batch: wait for its second classification
             if (g > 0 && sm.cfv[g & 7]) {
@@ -2207,13 +2212,13 @@ int plan_loop_device(const PlanDims& dm, uint64_t C, int policy, int remap, int 
         const size_t smem = size_t(12) * dm.B * 4;
         LSG_CUDA(cudaFuncSetAttribute(k_plan_loop_ov, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(2);
+        cfg.gridDim = dim3(3);
         cfg.blockDim = dim3(kThreads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.x = 3;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
