@@ -1209,19 +1209,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop(LoopArgs a) {
 // b < 2048, B <= 4096, remap on; clairvoyant): team C classifies step h
 // (A..C), team D runs the serial multi-holder chain D of step h, team P
 // applies D and runs the buffer-side phases E..I of step h. Step h is
-// classified once I(h-3) has advanced the buffers, i.e. against holder masks
-// two advances old, so C(h), D(h-1) and P(h-2) run at the same time and the
-// loop P(h-3) -> C(h) -> D(h) -> P(h) spans three steps. Only ids of batch h
-// whose mask I(h-2) or I(h-1) changes can alter its classification: an
-// insert or a drop of such an id (an id in consecutive batches at an epoch
-// boundary, or an eviction reaching next-step keys) is detected through
-// per-id stamps (one array per batch parity, so an id in both pending
-// batches keeps both stamps), and then step h is classified and resolved
-// again after I(h-1) (once per epoch boundary at most, in practice). Team
+// classified once I(h-4) has advanced the buffers, i.e. against holder masks
+// three advances old, so the loop P(h-4) -> C(h) -> D(h) -> P(h) spans four
+// steps. Only ids of batch h whose mask I(h-3)..I(h-1) changes can alter its
+// classification: an insert or a drop of such an id (an id in nearby batches
+// at an epoch boundary, or an eviction reaching next-step keys) is detected
+// through per-id stamps (one array per batch mod 3, so an id in several
+// pending batches keeps every stamp), and then step h is classified and
+// resolved again after I(h-1) (around epoch boundaries, in practice). Team
 // P's step arrays are double-buffered by step parity (team C classifies into
-// its own shared memory and copies a step over once P is done with step
-// h-2); team D's inputs and results are triple-buffered. The teams hand off
-// through shared-memory step counters with cluster-scope release/acquire.
+// its own shared memory, two sets, and copies a step over once P is done
+// with the step two back); team D's inputs and results are in global memory
+// by step mod 4. The teams hand off through shared-memory step counters with
+// cluster-scope release/acquire.
 struct OvPar {  // per step parity
     uint32_t tot[kMaxN];   // singles per node
     uint32_t mtot[kMaxN];  // multi assigned per node (D)
@@ -1259,12 +1259,11 @@ struct SmallOv {
     volatile uint32_t ac_cnt, d_cnt, i_cnt, spec_cnt, redo_cnt, copy_cnt, ds_cnt[kDWarps];
 };
 
-// The teams run on the two SMs of a thread-block cluster: team D (warp 0 of
-// CTA 0; no other warp shares its scheduler) and team C (CTA 0's 12 warps
-// on the other three schedulers, classifying each step in CTA 0's shared
-// memory and copying it over), and team P (all 16 warps of CTA 1), whose
-// per-step arrays and hand-off counters live in CTA 1's shared memory.
-// Teams D and C reach team P's state through distributed shared memory.
+// The teams run on the three SMs of a thread-block cluster: team C (all 16
+// warps of CTA 0), team P (all 16 warps of CTA 1), whose per-step arrays and
+// hand-off counters live in CTA 1's shared memory, and team D (four warps of
+// CTA 2, one per scheduler). Teams C and D reach team P's state through
+// distributed shared memory.
 constexpr uint32_t kPWarps = kWarps, kPThreads = kPWarps * 32;
 constexpr uint32_t kOvDepth = 4;  // steps in flight: step h is classified once I(h-4) is done
 // team C (classification): CTA 0's 12 warps that do not share warp 0's
