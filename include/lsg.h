@@ -192,8 +192,10 @@ int lsg_fetch_step(void* const* d_bufs, void* const* d_outs, const uint32_t* d_i
  * without host round trips):
  * d_items/d_slots/d_node_off are the WHOLE plan's arrays (lsg_plan_out
  * layout, [T][N+1] offsets), h_node_off a host copy of the offsets (step
- * bases and grid sizes). Every step writes the same batch tensors, as a
- * trainer consuming batch t before t+1 would see them. */
+ * bases and grid sizes). When the call returns the batch tensors hold the
+ * LAST step's rows (rows past its list are unspecified): the fused kernel
+ * alternates steps between the tensors and an internal scratch set, so one
+ * step's batch-row stores need not wait for the previous step's. */
 int lsg_fetch_steps(void* const* d_bufs, void* const* d_outs, const uint32_t* d_items, const uint32_t* d_slots,
                     const uint32_t* d_node_off, const uint32_t* h_node_off, uint64_t step_begin,
                     uint64_t step_end, uint32_t N, uint32_t node_begin, uint32_t node_end,
@@ -222,7 +224,9 @@ void lsg_host_rows_close(lsg_host_rows* h);
  * the host rows over PCIe into a device ring of about ring_bytes, 0 = 2 GiB)
  * and returns once it is resident; `stream` then stays busy until the job's
  * misses are consumed, so give each job in flight its own. lsg_fetch_job_run
- * enqueues the steps on the fetch stream (it waits for the miss list only).
+ * enqueues the steps on the fetch stream (it waits for the miss list only);
+ * afterwards the batch tensors hold the job's last step (rows past its list
+ * unspecified; earlier steps alternate with an internal scratch set).
  * lsg_fetch_job_stats (synchronous) reads {misses, kept misses, host bytes,
  * hits}; lsg_fetch_job_destroy frees stream-ordered after the job. */
 typedef struct lsg_fetch_job lsg_fetch_job;

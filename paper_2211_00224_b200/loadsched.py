@@ -1016,7 +1016,9 @@ class StepFetcher:
                     step_begin: int = 0, step_end: int | None = None) -> None:
         """The loading phase of steps [step_begin, step_end) of `plan` for this
         fetcher's ranks, in step order (lsg_fetch_steps: one C call, no host
-        round trips). host_node_off: the plan's [T, N+1] offsets on the host."""
+        round trips). host_node_off: the plan's [T, N+1] offsets on the host.
+        Afterwards the batch tensors hold the last step's rows (rows past its
+        list are unspecified)."""
         if self.store is not None:
             raise CapabilityError(4, "fetch_steps: Store-backed misses go through per-step calls")
         off = np.ascontiguousarray(host_node_off, dtype=np.uint32)
