@@ -22,6 +22,15 @@ constexpr uint32_t kHit = LSG_HIT_BIT;
 // splitmix64 finaliser (prng.hpp:18-23). Draw k (1-based) of a stream seeded
 // s is mix(s + k*gamma): the generator is counter-based, which is what lets
 // every kernel below compute its draws independently.
+// fire-and-forget global OR / AND (RED: no return value, so no scoreboard
+// entry; atomicOr with an unused result compiles to a returning ATOMG)
+__device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_and(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;

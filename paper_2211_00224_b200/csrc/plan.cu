@@ -214,15 +214,6 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // buffer.cpp:37-41 (re-key) / :42-46 (insert) without the eviction: key
 // update plus the bucket / never-used summaries.
-// fire-and-forget global OR / AND (RED: no return value, so no scoreboard
-// entry; atomicOr with an unused result compiled to a returning ATOMG here)
-__device__ __forceinline__ void red_or(uint32_t* p, uint32_t v) {
-    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_and(uint32_t* p, uint32_t v) {
-    asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 __device__ __forceinline__ uint32_t key_step(const LoopArgs& a, uint32_t pk) {
     return a.B == 1 ? pk : uint32_t(__umul64hi(pk, a.bdiv));
 }

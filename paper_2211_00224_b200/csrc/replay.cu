@@ -342,9 +342,9 @@ __device__ __forceinline__ void key_mark(uint32_t* pbmk, uint32_t* psumk, uint32
                                          uint32_t nu) {
     const uint32_t beta = nu / L, p = nu - beta * L;
     const uint32_t w = beta * bw + (p >> 5);
-    atomicOr(&pbmk[w], 1u << (p & 31));
-    if (!(atomicOr(&psumk[w >> 5], 1u << (w & 31)) & (1u << (w & 31))))
-        atomicOr(&psum2k[w >> 10], 1u << ((w >> 5) & 31));
+    red_or(&pbmk[w], 1u << (p & 31));  // (idempotent ORs: no need to read the summary back)
+    red_or(&psumk[w >> 5], 1u << (w & 31));
+    red_or(&psum2k[w >> 10], 1u << ((w >> 5) & 31));
 }
 
 // Evict the `need` largest keys of node k (whole warp).
@@ -461,8 +461,8 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay(ReplayArgs a) {
                 if (mine) {  // buffer.cpp:37-46 without the eviction
                     keyk[x] = nu;
                     if (nev) {
-                        atomicOr(&infk[x >> 5], 1u << (x & 31));
-                        atomicOr(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
+                        red_or(&infk[x >> 5], 1u << (x & 31));
+                        red_or(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
                     } else {
                         key_mark(a.pbm + size_t(k) * a.T * a.bw, a.psum + size_t(k) * a.psw,
                                  a.psum2 + size_t(k) * a.ps2w, a.bw, a.L, nu);
@@ -628,13 +628,13 @@ __device__ __forceinline__ void r_set_key_cta(const ReplayArgsCta& a, RSharedCta
                                           uint32_t nu) {
     a.key[size_t(k) * a.D + x] = nu;
     if (nu == kNever) {
-        atomicOr(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
-        atomicOr(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
+        red_or(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
+        red_or(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
         atomicAdd(&sh.infcnt, 1u);
         atomicMax(&sh.inftop, x >> 5);
     } else {
         const uint32_t beta = nu / a.B;
-        atomicOr(&a.nz[size_t(k) * a.nzw + (beta >> 5)], 1u << (beta & 31));
+        red_or(&a.nz[size_t(k) * a.nzw + (beta >> 5)], 1u << (beta & 31));
         atomicMax(&sh.top, beta);
         if (a.pbm) {
             key_mark(a.pbm + size_t(k) * a.T * a.bw, a.psum + size_t(k) * a.psw, a.psum2 + size_t(k) * a.ps2w, a.bw,
@@ -1089,8 +1089,8 @@ __device__ __forceinline__ void chain_set(const ReplayArgsCta& a, RSharedCta& sh
                                           uint32_t nu, uint32_t slot) {
     const uint32_t k = cx.k;
     if (nu == kNever) {
-        atomicOr(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
-        atomicOr(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
+        red_or(&a.infbm[size_t(k) * a.infw + (x >> 5)], 1u << (x & 31));
+        red_or(&a.infsum[size_t(k) * a.sumw + (x >> 10)], 1u << ((x >> 5) & 31));
         atomicAdd(&sh.infcnt, 1u);
         atomicMax(&sh.inftop, x >> 5);
         if (a.slot_out) a.slot[size_t(k) * a.D + x] = slot;
@@ -1466,7 +1466,7 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay_lru(LruReplayArgs a) {
             [&](uint32_t i, uint32_t x) {
                 if (so) {
                     so[i] = slotk[x] | kHit;
-                    atomicOr(&hbm[i >> 5], 1u << (i & 31));
+                    red_or(&hbm[i >> 5], 1u << (i & 31));
                 }
             },
             [&](uint32_t x, uint32_t y) {
