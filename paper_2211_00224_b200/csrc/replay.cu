@@ -1466,7 +1466,7 @@ __global__ void __launch_bounds__(kRWarps * 32) k_replay_lru(LruReplayArgs a) {
             [&](uint32_t i, uint32_t x) {
                 if (so) {
                     so[i] = slotk[x] | kHit;
-                    red_or(&hbm[i >> 5], 1u << (i & 31));
+                    atomicOr(&hbm[i >> 5], 1u << (i & 31));  // (shared memory)
                 }
             },
             [&](uint32_t x, uint32_t y) {
