@@ -53,6 +53,7 @@ constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kMaxN = 32;
 constexpr uint32_t kOvN = 8;  // the overlapped loop's node limit
+constexpr uint32_t kOvW = 4096 / 32;  // words of a step bitmap at the overlapped loop's largest B
 constexpr uint32_t kDWarps = 4;  // its team D: one warp per scheduler of CTA 2, one per step mod 4
 constexpr uint32_t kMaxSmemB = 8192;   // per-item arrays in shared memory up to here
 constexpr uint32_t kMaxB = 16384;      // then in L2-resident global scratch
@@ -1243,6 +1244,8 @@ struct SmallOv {
     uint32_t stamp, conflict, conflict2, conflict3;  // I(g): stamps g+1..g+3, their batches' verdicts
     OvPar par[2];
     uint32_t cfv[8];   // verdict per batch (mod 8): a mask it was classified with changed
+    uint32_t mbm[kOvN][kOvW];   // team P: the multi items team D assigned to node k, by batch position
+    uint32_t mpre[kOvN][kOvW];  //   and their count before each word
     uint32_t cnm[4];   // (team C's copy) multi items per step (mod 4), for team D
     // team hand-off counters (monotone): steps classified, resolved (D
     // final), buffer-advanced, speculative-D-finished-on-conflict,
@@ -1497,22 +1500,24 @@ __device__ void ov_resolve(const LoopArgs& a, uint32_t (*stg)[32][kOvN], const u
 
 // team P: team D's decisions for the multi items of step g into the lists
 // (node positions in fin, E's input in sinfo) — what k_plan_loop's D writes
-__device__ void ov_apply(const LoopArgs& a, const OvBufs& s, OvPar& pp, const uint32_t* dsx, const uint32_t* res_d,
+// (a bit per multi item in its node's batch-position bitmap: E counts the
+// multi items of node h before a single at j with a prefix and a popc, where
+// the single-CTA loop binary-searches a sorted list)
+__device__ void ov_apply(const LoopArgs& a, const OvBufs& s, OvPar& pp, SmallOv& sm, const uint32_t* res_d,
                          const uint32_t* mtot_d, uint32_t ptid) {
     const uint32_t b = a.b, nm = pp.nmulti;
     const uint32_t kSent = (b << 4) - 1u;
     for (uint32_t mi = ptid; mi < nm; mi += kPThreads) {
-        const uint32_t r = res_d[mi], j = s.pre[mi];
+        const uint32_t r = __ldcg(&res_d[mi]), j = s.pre[mi];
         if (r != kSent) {
             const uint32_t kk = r & 15u, c = r >> 4;
-            const uint32_t Sk = reinterpret_cast<const uint16_t*>(dsx + size_t(mi) * 4)[kk] >> 4;
-            s.fin[kk * b + (c - Sk)] = j;
+            atomicOr(&sm.mbm[kk][j >> 5], 1u << (j & 31));
             s.sinfo[j] = (c << 5) | kk;
         } else {
             s.sinfo[j] = 0xFFFFFFFFu;
         }
     }
-    if (ptid < a.N) pp.mtot[ptid] = mtot_d[ptid];
+    if (ptid < a.N) pp.mtot[ptid] = __ldcg(&mtot_d[ptid]);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
@@ -1711,7 +1716,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
             a.prof[32 + 128 + 2 * g] = t;
         }
         tick(9);
-        ov_apply(a, s, pp, dsx_of(g), res_of(g), mtot_of(g), ptid);
+        const uint32_t lenw = (min(a.B, a.keep - (g % a.S) * a.B) + 31) / 32;
+        for (uint32_t q = ptid; q < N * kOvW; q += kPThreads) sm.mbm[q / kOvW][q % kOvW] = 0;
+        bar_p();
+        ov_apply(a, s, pp, sm, res_of(g), mtot_of(g), ptid);
+        bar_p();
+        for (uint32_t k = pw; k < N; k += kPWarps) {  // per node: multi items before each word
+            uint32_t v[4], t = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t wd = lane * 4 + u;
+                v[u] = wd < lenw ? __popc(sm.mbm[k][wd]) : 0u;
+                t += v[u];
+            }
+            uint32_t inc = t;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+                if (lane >= uint32_t(d)) inc += o;
+            }
+            uint32_t run = inc - t;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                sm.mpre[k][lane * 4 + u] = run;
+                run += v[u];
+            }
+        }
         bar_p();
         tick(0);
         if (g + kOvDepth < a.T && !(a.dbg_skip & 8)) {  // batch g+4's rows into L2 for its classification after I(g)
@@ -1736,13 +1766,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_plan_loop_ov(LoopArgs a) {
                 if (hc == 1) {
                     const uint32_t h = __ffs(m) - 1;
                     const uint32_t S = s.sinfo[j];
-                    const uint32_t* mp = s.fin + h * b;
-                    uint32_t lo2 = 0, hi2 = pp.mtot[h];
-                    while (lo2 < hi2) {
-                        const uint32_t mid = (lo2 + hi2) >> 1;
-                        if (mp[mid] < j) lo2 = mid + 1; else hi2 = mid;
-                    }
-                    const uint32_t pos = S + lo2;
+                    // M_h(<j): multi items before j assigned to h
+                    const uint32_t pos = S + sm.mpre[h][j >> 5] + __popc(sm.mbm[h][j >> 5] & lanemask_lt());
                     if (pos < b) s.sinfo[j] = (h << 24) | pos;
                     else fetch = true;
                 } else if (hc >= 2) {
