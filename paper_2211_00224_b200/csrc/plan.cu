@@ -1297,16 +1297,34 @@ __device__ void ov_classify(const LoopArgs& a, SmallOv& sm, const OvBufs& s, OvP
     const uint32_t j0 = pw * R, j1 = min(j0 + R, len);
     if (lane < kMaxN) sm.wcnt[pw][lane] = 0;
     uint32_t wm = 0;
-#pragma unroll 4
-    for (uint32_t j = j0 + lane; j < j1; j += 32) {
-        const uint32_t x = row[j];
-        s.sx[j] = x;
-        if (stamp) a.nb[size_t(g % 3) * a.D + x] = g;  // this batch's classification is checked by I(g-3)..I(g-1)
+    // every lane's (at most 8: B <= 4096 over 16 warps) ids, then their masks,
+    // each as one batch of independent loads
+    constexpr int kCU = 8;
+    uint32_t xs[kCU];
+#pragma unroll
+    for (int u = 0; u < kCU; ++u) {
+        const uint32_t j = j0 + lane + 32u * u;
+        xs[u] = j < j1 ? __ldg(&row[j]) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kCU; ++u) {
+        const uint32_t j = j0 + lane + 32u * u;
+        if (j < j1) {
+            s.sx[j] = xs[u];
+            if (stamp) a.nb[size_t(g % 3) * a.D + xs[u]] = g;  // this batch's classification is checked by I(g-3)..I(g-1)
+        }
     }
     __threadfence();  // stamps before the masks are read (nb_check)
-    __syncwarp();
-#pragma unroll 4
-    for (uint32_t j = j0 + lane; j < j1; j += 32) s.smask[j] = __ldcg(&a.hm[s.sx[j]]);
+#pragma unroll
+    for (int u = 0; u < kCU; ++u) {
+        const uint32_t j = j0 + lane + 32u * u;
+        xs[u] = j < j1 ? __ldcg(&a.hm[xs[u]]) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kCU; ++u) {
+        const uint32_t j = j0 + lane + 32u * u;
+        if (j < j1) s.smask[j] = xs[u];
+    }
     __syncwarp();
     for (uint32_t c = j0; c < j0 + R; c += 32) {
         const uint32_t j = c + lane;
