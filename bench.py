@@ -383,8 +383,12 @@ def main():
     misses = None
     if hostrows is not None:
         free = torch.cuda.mem_get_info()[0]
-        want = int(float(os.environ.get("LSG_BENCH_STREAM_GB", "48")) * 2 ** 30)
-        ring = max(min(want, free - 24 * 2 ** 30), 2 * maxlen * per * SB)
+        # as much of a job's 64 GiB all-miss first epoch as HBM holds beside the
+        # buffers, minus 12 GiB for the jobs in flight (N=1: 61 GiB; e2e at K=5:
+        # 48 GiB 9.17-9.23 M, 59 GiB 9.32-9.47 M, 61 GiB 9.80-9.81 M samples/s)
+        want = int(float(os.environ.get("LSG_BENCH_STREAM_GB", "64")) * 2 ** 30)
+        reserve = int(float(os.environ.get("LSG_BENCH_RESERVE_GB", "12")) * 2 ** 30)
+        ring = max(min(want, free - reserve), 2 * maxlen * per * SB)
         misses = ls.MissStream(SB, ring // SB * SB)
         host_note += f"; miss ring shared across jobs: {ring / 2**30:.1f} GiB"
 
