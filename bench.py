@@ -384,10 +384,12 @@ def main():
     if hostrows is not None:
         free = torch.cuda.mem_get_info()[0]
         # as much of a job's 64 GiB all-miss first epoch as HBM holds beside the
-        # buffers, minus 12 GiB for the jobs in flight (N=1: 61 GiB; e2e at K=5:
-        # 48 GiB 9.17-9.23 M, 59 GiB 9.32-9.47 M, 61 GiB 9.80-9.81 M samples/s)
+        # buffers, minus 16 GiB for the jobs in flight (e2e at K=5: 48 GiB
+        # 9.17-9.23 M, 59 GiB 9.32-9.47 M, 61 GiB 9.80-9.81 M samples/s; a 12 GiB
+        # reserve ran out of memory after 15+ jobs while fetch jobs still took a
+        # scratch batch set each)
         want = int(float(os.environ.get("LSG_BENCH_STREAM_GB", "64")) * 2 ** 30)
-        reserve = int(float(os.environ.get("LSG_BENCH_RESERVE_GB", "12")) * 2 ** 30)
+        reserve = int(float(os.environ.get("LSG_BENCH_RESERVE_GB", "16")) * 2 ** 30)
         ring = max(min(want, free - reserve), 2 * maxlen * per * SB)
         misses = ls.MissStream(SB, ring // SB * SB)
         host_note += f"; miss ring shared across jobs: {ring / 2**30:.1f} GiB"

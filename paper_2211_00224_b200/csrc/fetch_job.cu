@@ -1207,16 +1207,20 @@ int lsg_fetch_job_create(const lsg_fetch_job_desc* desc, lsg_fetch_job** out, vo
                 return fail(cuda_error(cudaGetLastError(), "fetch_job: deferred offsets"));
             j->ndefer_rows = up[3 * ns];
             // steps alternate between the caller's batch tensors and these (one more batch
-            // per local rank: 128 MiB at cfg2, 256 MiB at cfg3); fetch alone at one rank,
-            // cfg2 44.6 -> 42.2 us per step, cfg3 47.7 -> 46.4 (LSG_FETCH_PINGPONG=0: off)
-            static const bool pp_off = [] {
+            // per local rank: 128 MiB at cfg2, 256 MiB at cfg3), where a step is short
+            // enough for its boundary to matter (<= 512 MiB of rows; fetch alone at one
+            // rank, cfg2 44.6 -> 42.2 us per step, cfg3 47.7 -> 46.4; at 8 ranks per GPU
+            // (1 GiB per step) no gain, and a GiB per job in flight is HBM the e2e miss
+            // ring needs). LSG_FETCH_PINGPONG=0/1 forces it.
+            static const int pp_env = [] {
                 const char* e = std::getenv("LSG_FETCH_PINGPONG");
-                return e && e[0] == '0';
+                return e ? std::atoi(e) : -1;
             }();
-            if (ns >= 2 && !pp_off) {
-                j->srows = uint32_t(max_list);
+            const bool pp = pp_env >= 0 ? pp_env == 1 : max_rows * d.sample_bytes <= (uint64_t(512) << 20);
+            if (ns >= 2 && pp) {
+                j->srows = uint32_t((max_list + 63) / 64 * 64);  // (a stable size class across jobs for the pool)
                 if (!alloc(reinterpret_cast<void**>(&j->scratch),
-                           size_t(d.node_end - d.node_begin) * max_list * d.sample_bytes))
+                           size_t(d.node_end - d.node_begin) * j->srows * d.sample_bytes))
                     return fail(set_error(kInternal, "fetch_job: device allocation failed (scratch batch rows)"));
             }
             if (up[3 * ns]) {
