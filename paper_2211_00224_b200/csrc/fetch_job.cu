@@ -1357,6 +1357,15 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
             const char* e = std::getenv("LSG_FETCH_CPS");
             return e ? unsigned(std::max(1, std::atoi(e))) : kFCtasPerSm;
         }();
+        // the grid leaves 8 SMs' worth of CTA slots to the planner and replay streams: their
+        // many short launches (the next-use pass: 100 per job) otherwise wait for the fetch's
+        // launch cuts. At one rank per GPU beside a fetch: replay 195 -> 157 ms, job period
+        // 334 -> 295 ms; the fetch itself unchanged (HBM-bound at 140 SMs). LSG_FETCH_RESERVE_SMS
+        static const unsigned fetch_sms = [] {
+            const char* e = std::getenv("LSG_FETCH_RESERVE_SMS");
+            const int r = e ? std::atoi(e) : 8;
+            return unsigned(std::max(1, 148 - std::max(0, r)));
+        }();
         const bool fills = j->ndefer_rows > 0;  // deferred-fill phases needed
         auto kern = nst == 5    ? (fills ? k_fetch_fused<5, 2, 2> : k_fetch_fused<5, 2, 1>)
                     : nst == 12 ? (fills ? k_fetch_fused<12, 3, 2> : k_fetch_fused<12, 3, 1>)
@@ -1378,7 +1387,7 @@ int lsg_fetch_job_run(lsg_fetch_job* j, void* stream) {
             fs.gB = gb;
             if (tiles && d.node_begin != d.node_end) {
                 cudaLaunchConfig_t cfg{};
-                cfg.gridDim = dim3(unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tiles, 148ull * cps))));
+                cfg.gridDim = dim3(unsigned(std::max<uint64_t>(1, std::min<uint64_t>(tiles, uint64_t(fetch_sms) * cps))));
                 cfg.blockDim = dim3(64);
                 cfg.dynamicSmemBytes = size_t(kFTile) * nst;
                 cfg.stream = st;
