@@ -735,7 +735,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_note": "dram read+write bytes per k_fetch_fused launch (one steady-state step, "
-                                         "8 ranks on one GPU) from profiles/gather_traffic.json (r02d_fetch_persist.ncu-rep); "
+                                         "8 ranks on one GPU) from profiles/gather_traffic.json (r02f_fetch_final.ncu-rep); "
                                          f"{traffic_ratio:.3f} x that launch's algorithmic bytes" if traffic else None,
                          "kernel": "fetch phase (k_fetch_fused: persistent multi-step TMA bulk-copy pipeline, "
                                    "producer/consumer warps: hits, misses and deferred slot fills)",
